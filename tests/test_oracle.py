@@ -1,0 +1,420 @@
+"""Pins for the CPU oracle (SURVEY.md §8(c) P1–P17), run with -m "not gpu".
+
+Each test pins the oracle to something other than itself: a closed form, a
+worked example printed in the paper (tests/golden/), finite differences, an
+invariant, or brute force.  Citations are PAPER.md lines (P:n) and SPEC.md
+lines (S:n).
+"""
+import math
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+C0 = 0.28209479177387814
+
+
+def scene(means, log_scales=None, quats=None, logits=None, sh=None, sh_degree=0):
+    means = np.asarray(means, np.float32).reshape(-1, 3)
+    P = len(means)
+    K = (sh_degree + 1) ** 2
+    return dict(
+        means=means,
+        log_scales=np.asarray(log_scales if log_scales is not None else np.full((P, 3), -3.0), np.float32).reshape(P, 3),
+        quats=np.asarray(quats if quats is not None else np.tile([1, 0, 0, 0], (P, 1)), np.float32).reshape(P, 4),
+        opacity_logits=np.asarray(logits if logits is not None else np.zeros(P), np.float32).reshape(P),
+        sh=np.asarray(sh if sh is not None else np.zeros((P, K, 3)), np.float32).reshape(P, K, 3),
+        sh_degree=sh_degree,
+    )
+
+
+def cam_identity(W=32, H=32, f=40.0, R=np.eye(3), t=(0, 0, 0), cx=None, cy=None):
+    return synth.cams_array([synth.make_camera(R, t, W, H, f, cx=cx, cy=cy)])
+
+
+# --------------------------------------------------------------------- CA exp
+def test_ca_exp_is_an_exp():
+    """§4.3 canonical exp: within 3 ulp of the true exp on its range, 0 below −87."""
+    xs = np.concatenate([np.linspace(-87, 88, 20001), -np.logspace(-8, 1.9, 2000), [0.0]]).astype(np.float32)
+    got = np.array([oracle.ca_exp(x) for x in xs], np.float64)
+    ref = np.exp(xs.astype(np.float64))
+    ulp = np.spacing(ref.astype(np.float32)).astype(np.float64)
+    assert np.all(np.abs(got - ref) <= 3 * ulp) and np.mean(np.abs(got - ref) <= ulp) > 0.9
+    assert oracle.ca_exp(-87.5) == 0.0 and oracle.ca_exp(0.0) == 1.0
+
+
+# ----------------------------------------------------------- P1/P3 projection
+def test_P3_isotropic_on_axis_conic_and_radius():
+    """Isotropic s at depth z on the optical axis, fx=fy=f: Σ' = ((f s/z)² + 0.3) I,
+    conic = I/σ'², radius = ⌈3√(σ'² + √0.1)⌉ (R5, R7)."""
+    s, z, f = 0.05, 2.0, 40.0
+    g = scene([0, 0, z], log_scales=np.full(3, math.log(s)))
+    o = oracle.Oracle(g, cam_identity(f=f))
+    p = o.pairs()
+    s32 = float(np.exp(np.float32(math.log(s))))
+    sig2 = (f * s32 / z) ** 2 + 0.3
+    assert p["vis"][0, 0] == 1 and p["zvis"][0, 0] == 1
+    np.testing.assert_allclose([p["A"][0, 0], p["B"][0, 0], p["C"][0, 0]], [1 / sig2, 0, 1 / sig2], rtol=2e-6, atol=1e-7)
+    assert p["radius"][0, 0] == math.ceil(3 * math.sqrt(sig2 + math.sqrt(0.1)))
+    # P2: on-axis ⇒ μ' = (cx, cy); depth = z
+    assert p["px"][0, 0] == np.float32(15.5) and p["py"][0, 0] == np.float32(15.5)
+    assert p["depth"][0, 0] == np.float32(z)
+
+
+def test_P1_axis_swap_through_projection():
+    """90° rotation about z swaps the x/y scales: Σ = R diag(a²,b²,c²) Rᵀ = diag(b²,a²,c²)
+    (S:115), seen on-axis as conic = diag(1/((f b/z)²+0.3), 1/((f a/z)²+0.3))."""
+    a, b, c, z, f = 0.08, 0.03, 0.05, 3.0, 50.0
+    q = [math.cos(math.pi / 4), 0, 0, math.sin(math.pi / 4)]
+    g = scene([0, 0, z], log_scales=[math.log(a), math.log(b), math.log(c)], quats=q)
+    p = oracle.Oracle(g, cam_identity(f=f)).pairs()
+    ea, eb = [float(np.exp(np.float32(math.log(v)))) for v in (a, b)]
+    sx = (f * eb / z) ** 2 + 0.3
+    sy = (f * ea / z) ** 2 + 0.3
+    np.testing.assert_allclose([p["A"][0, 0], p["C"][0, 0]], [1 / sx, 1 / sy], rtol=1e-5)
+    assert abs(p["B"][0, 0]) < 1e-6 * p["A"][0, 0]
+
+
+def test_P2_b2_cameras_see_origin_at_centre():
+    """Appendix B.2 pair (tests/golden/b2_cameras.txt, reading R23): both cameras see
+    the origin at the image centre at depth 1."""
+    rows = [l.split("|") for l in open(os.path.join(GOLDEN, "b2_cameras.txt")) if l.strip() and not l.startswith("#")]
+    cams = synth.cams_array([synth.make_camera(np.array(r[1].split(), float).reshape(3, 3),
+                                               np.array(r[2].split(), float), 33, 33, 30.0) for r in rows])
+    p = oracle.Oracle(scene([0, 0, 0]), cams).pairs()
+    for v, r in enumerate(rows):
+        assert p["depth"][v, 0] == np.float32(float(r[3]))
+        assert p["px"][v, 0] == np.float32(16.0) and p["py"][v, 0] == np.float32(16.0)
+
+
+# -------------------------------------------------------------- P4/P5 blending
+def test_P4_single_isotropic_footprint_and_alpha():
+    """One isotropic Gaussian on the axis: n_contrib = 1 exactly on lattice pixels with
+    ‖p − μ'‖² ≤ 2σ'² ln(255 o) inside its rect (α ≥ 1/255, R12), colour =
+    rgb·α + (1−α)·bg with α = o·exp(−‖p−μ'‖²/2σ'²), T_final = 1 − α; elsewhere 0, bg, 1."""
+    s, z, f, W = 0.06, 2.0, 40.0, 32
+    logit = 0.3
+    rgb = np.array([0.9, 0.4, 0.2])
+    g = scene([0, 0, z], log_scales=np.full(3, math.log(s)), logits=[logit],
+              sh=((rgb - 0.5) / C0).reshape(1, 1, 3))
+    bg = np.array([0.1, 0.2, 0.3], np.float32)
+    o = oracle.Oracle(g, cam_identity(W=W, H=W, f=f), bg=bg)
+    im = o.forward()
+    p = o.pairs()
+    s64 = math.exp(float(np.float32(math.log(s))))  # fp64 value chain of the float input
+    sig2 = (f * s64 / z) ** 2 + 0.3
+    op = 1 / (1 + math.exp(-float(np.float32(logit))))
+    thr = 2 * sig2 * math.log(255 * op)
+    yy, xx = np.mgrid[0:W, 0:W]
+    d2 = (xx - 15.5) ** 2 + (yy - 15.5) ** 2
+    assert np.min(np.abs(d2 - thr)) > 1e-3 * thr  # parameters keep every pixel off the threshold
+    inrect = ((xx // 16 >= p["rx0"][0, 0]) & (xx // 16 < p["rx1"][0, 0])
+              & (yy // 16 >= p["ry0"][0, 0]) & (yy // 16 < p["ry1"][0, 0]))
+    foot = (d2 <= thr) & inrect
+    assert foot.sum() > 20 and (~foot).sum() > 20
+    np.testing.assert_array_equal(im["n_contrib"][0], foot.astype(np.int32))
+    alpha = np.where(foot, op * np.exp(-d2 / (2 * sig2)), 0.0)
+    rgb32 = C0 * ((rgb - 0.5) / C0).astype(np.float32).astype(np.float64) + 0.5
+    for ch in range(3):
+        np.testing.assert_allclose(im["rgb"][0, ch], rgb32[ch] * alpha + (1 - alpha) * float(bg[ch]), atol=1e-12)
+    np.testing.assert_allclose(im["T_final"][0], 1 - alpha, atol=1e-12)
+
+
+def test_P5_two_cocentred_terms():
+    """Front o₁=0.5 (c₁), back o₂=0.9 (c₂), both centred on a pixel: C = 0.5c₁ + 0.45c₂,
+    T_final = 0.05 (Eq. 1; S:195 with o₂ reachable by a sigmoid, R13)."""
+    c1, c2 = np.array([1.0, 0.0, 0.25]), np.array([0.0, 1.0, 0.5])
+    g = scene([[0, 0, 2.0], [0, 0, 3.0]], log_scales=np.full((2, 3), math.log(0.05)),
+              logits=[0.0, math.log(9.0)], sh=np.stack([(c1 - 0.5) / C0, (c2 - 0.5) / C0]).reshape(2, 1, 3))
+    o = oracle.Oracle(g, cam_identity(W=33, H=33, f=40.0))
+    im = o.forward()
+    np.testing.assert_allclose(im["rgb"][0, :, 16, 16], 0.5 * c1 + 0.45 * c2, atol=1e-6)
+    assert abs(im["T_final"][0, 16, 16] - 0.05) < 1e-6
+    assert im["n_contrib"][0, 16, 16] == 2
+
+
+def test_P8_early_termination_is_sound():
+    """Disabling early termination changes no pixel by more than 2e-3."""
+    g, cams = synth.make_scene("tiny")
+    a = oracle.Oracle(g, cams).forward()
+    b = oracle.Oracle(g, cams, flags=oracle.NO_EARLY_TERMINATION).forward()
+    assert np.max(np.abs(a["rgb"] - b["rgb"])) <= 2e-3
+    assert np.all(b["n_contrib"] >= a["n_contrib"])
+    assert np.any(b["n_contrib"] > a["n_contrib"])  # termination actually happened
+
+
+# --------------------------------------------------------------- P6/P7 lists
+def test_P6_P7_lists_equal_brute_force():
+    """Per-(view,tile) lists = brute-force O(Q·T) rect test sorted by the tuple
+    (depth bits, gid) (R9/R10); rect = [3DGS] getRect re-derived in numpy."""
+    g, cams = synth.make_scene(synth.scaled(synth.CONFIGS["tiny"], P=300))
+    o = oracle.Oracle(g, cams)
+    p = o.pairs()
+    off, gid = o.lists()
+    TX, TY = o.TX, o.TY
+    # independent rect from (px, py, radius) in float32
+    px, py, r = p["px"], p["py"], p["radius"].astype(np.float32)
+    with np.errstate(invalid="ignore"):
+        def lo(v, T):
+            return np.where(~(v > 0), 0, np.where(v >= T, T, np.trunc(v))).astype(np.int64)
+        rx0 = lo((px - r) * np.float32(0.0625), TX)
+        ry0 = lo((py - r) * np.float32(0.0625), TY)
+        rx1 = lo(((px + r) + np.float32(15)) * np.float32(0.0625), TX)
+        ry1 = lo(((py + r) + np.float32(15)) * np.float32(0.0625), TY)
+    vis = p["vis"].astype(bool)
+    np.testing.assert_array_equal(rx0[vis], p["rx0"][vis])
+    np.testing.assert_array_equal(rx1[vis], p["rx1"][vis])
+    np.testing.assert_array_equal(ry0[vis], p["ry0"][vis])
+    np.testing.assert_array_equal(ry1[vis], p["ry1"][vis])
+    for v in range(o.V):
+        for t in range(o.T):
+            tx, ty = t % TX, t // TX
+            members = [i for i in range(o.P) if vis[v, i] and rx0[v, i] <= tx < rx1[v, i] and ry0[v, i] <= ty < ry1[v, i]]
+            members.sort(key=lambda i: (int(p["depth"][v, i].view(np.uint32)), i))
+            b = v * o.T + t
+            assert list(gid[off[b]:off[b + 1]]) == members
+
+
+# -------------------------------------------------------------- gradients
+def _loss(g, cams, dLdC, bg=(0, 0, 0)):
+    o = oracle.Oracle(g, cams, bg=bg)
+    im = o.forward()
+    return float(np.sum(im["rgb"] * dLdC)), im["n_contrib"], (o.lists()[1], o.decision_hash())
+
+
+def _fd_check(g, cams, dLdC, bg=(0.0, 0.0, 0.0), h=1e-3, rtol=1e-4, atol=1e-7, keys=None):
+    """Central differences with one Richardson step (error O(h⁴)) on the float32 inputs;
+    the actual representable step is used as the divisor."""
+    o = oracle.Oracle(g, cams, bg=bg)
+    grads = o.backward(dLdC)
+    _, nc0, l0 = _loss(g, cams, dLdC, bg)
+    gk = {"means": "d_means", "log_scales": "d_log_scales", "quats": "d_quats",
+          "opacity_logits": "d_opacity_logits", "sh": "d_sh"}
+    checked = 0
+
+    def central(key, idx, step):
+        gp = {k: (v.copy() if isinstance(v, np.ndarray) else v) for k, v in g.items()}
+        gm = {k: (v.copy() if isinstance(v, np.ndarray) else v) for k, v in g.items()}
+        base = g[key].reshape(-1)[idx]
+        gp[key].reshape(-1)[idx] = base + np.float32(step)
+        gm[key].reshape(-1)[idx] = base - np.float32(step)
+        delta = float(gp[key].reshape(-1)[idx]) - float(gm[key].reshape(-1)[idx])
+        lp, ncp, lsp = _loss(gp, cams, dLdC, bg)
+        lm, ncm, lsm = _loss(gm, cams, dLdC, bg)
+        smooth = (np.array_equal(ncp, nc0) and np.array_equal(ncm, nc0)
+                  and np.array_equal(lsp[0], l0[0]) and np.array_equal(lsm[0], l0[0])
+                  and lsp[1] == l0[1] and lsm[1] == l0[1])
+        return (lp - lm) / delta, smooth
+
+    for key, gname in gk.items():
+        if keys and key not in keys:
+            continue
+        arr = g[key]
+        ana = grads[gname].reshape(-1)
+        for idx in range(arr.size):
+            if key == "sh" and (idx // 3) % arr.shape[1] >= (g["sh_degree"] + 1) ** 2:
+                continue
+            step = h * max(1.0, abs(float(arr.reshape(-1)[idx])))
+            f1, s1 = central(key, idx, step)
+            f2, s2 = central(key, idx, step / 2)
+            if not (s1 and s2):
+                continue  # a discrete decision flipped: the loss is not smooth here
+            fd = (4 * f2 - f1) / 3
+            tol = atol + rtol * max(abs(fd), abs(ana[idx]))
+            assert abs(fd - ana[idx]) <= tol, (key, idx, fd, ana[idx], f1, f2)
+            checked += 1
+    return checked
+
+
+def _fd_scene(seed, P=6, sh_degree=3, W=24, H=20, V=2):
+    rng = np.random.default_rng(seed)
+    means = rng.uniform(-0.3, 0.3, (P, 3))
+    g = scene(means, log_scales=rng.uniform(-2.6, -1.8, (P, 3)), quats=rng.normal(size=(P, 4)),
+              logits=rng.uniform(-1, 1.5, P), sh=rng.normal(0, 0.4, (P, (sh_degree + 1) ** 2, 3)),
+              sh_degree=sh_degree)
+    cams = synth.cams_array([synth.look_at([2.0 * math.cos(a), 2.0 * math.sin(a), 0.6], [0, 0, 0], W, H, 0.9 * W)
+                             for a in np.linspace(0.3, 2.0, V)])
+    dL = rng.normal(0, 1, (V, 3, H, W)).astype(np.float32)
+    return g, cams, dL
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_P10_all_gradients_match_finite_differences(seed):
+    """Every parameter gradient (means, log-scales, quaternion incl. normalisation,
+    opacity logit, SH deg 3) = central FD of L = Σ ∂L/∂C · C, in fp64,
+    with a non-zero background so the T_final·bg term is exercised (R16)."""
+    g, cams, dL = _fd_scene(seed)
+    n = _fd_check(g, cams, dL, bg=(0.2, 0.5, 0.1))
+    assert n > 200
+
+
+def test_P10_fd_with_jacobian_clamp():
+    """A Gaussian far off-screen where ũx is clamped (R4: exact zero through the clamp,
+    k=1 in ∂J/∂t.z) — FD agrees with the exact clamp gradient."""
+    W = H = 24
+    g = scene([[1.6, 0.0, 2.0], [0.2, 0.1, 2.5]], log_scales=np.full((2, 3), -0.7),
+              logits=[2.0, 1.0], sh=np.full((2, 1, 3), 0.5))
+    cams = synth.cams_array([synth.make_camera(np.eye(3), [0, 0, 0], W, H, 0.9 * W)])
+    o = oracle.Oracle(g, cams)
+    p = o.pairs()
+    assert p["vis"][0, 0] == 1 and 1.6 / 2.0 > 0.65 * W / (0.9 * W)  # ux beyond the clamp limit
+    dL = np.random.default_rng(3).normal(0, 1, (1, 3, H, W)).astype(np.float32)
+    assert _fd_check(g, cams, dL) > 20
+
+
+def test_P9_linearity():
+    """dL ≡ 0 → every gradient and E is 0; dL → 2·dL doubles them exactly."""
+    g, cams, dL = _fd_scene(5)
+    o = oracle.Oracle(g, cams)
+    z = o.backward(np.zeros_like(dL))
+    assert all(np.all(v == 0) for k, v in z.items() if k != "vis")
+    a = o.backward(dL)
+    b = o.backward(2 * dL)
+    for k in a:
+        if k != "vis":
+            np.testing.assert_array_equal(b[k], 2 * a[k])
+
+
+# -------------------------------------------------------------------- ADC
+def test_P11_adc_golden_examples():
+    for line in open(os.path.join(GOLDEN, "adc_examples.txt")):
+        if not line.strip() or line.startswith("#"):
+            continue
+        name, v, gx, gy, exp = [s.strip() for s in line.split("|")]
+        out = oracle.adc_example([int(x) for x in v.split(",")], [float(x) for x in gx.split(",")],
+                                 [float(x) for x in gy.split(",")])
+        np.testing.assert_allclose(out, [float(x) for x in exp.split()], atol=1e-12, err_msg=name)
+
+
+def test_P12_ordering_and_single_view_collapse():
+    """E1 ≥ E2 ≥ E_old for every Gaussian (triangle inequality); one view ⇒
+    E2 = E_old exactly."""
+    g, cams = synth.make_scene("tiny")
+    dL = synth.make_dLdC_scaled(4, 64, 64, 1)
+    gr = oracle.Oracle(g, cams).backward(dL)
+    assert np.all(gr["e1"] >= gr["e2"] * (1 - 1e-12))
+    assert np.all(gr["e2"] >= gr["e_old"] * (1 - 1e-12))
+    assert np.any(gr["e1"] > 1.01 * gr["e2"]) and np.any(gr["e2"] > 1.01 * gr["e_old"])
+    g1 = oracle.Oracle(g, cams[:1]).backward(dL[:1])
+    np.testing.assert_array_equal(g1["e2"], g1["e_old"])
+    assert g1["e2"].max() > 0
+
+
+def test_E1_is_norm_and_add_per_pixel():
+    """E1 = Σ over pixels of ‖∇_{p_i}L‖ ('norm and add'): the per-pair E1 of a
+    full ∂L/∂C equals the sum of the E1's from each single pixel's ∂L/∂C, while the
+    per-pair Σ∇ is additive (linearity)."""
+    W = H = 8
+    g = scene([[0.02, -0.01, 2.0], [0.0, 0.03, 2.4]], log_scales=np.full((2, 3), -2.2),
+              logits=[0.5, 1.0], sh=np.full((2, 1, 3), 0.4))
+    cams = synth.cams_array([synth.make_camera(np.eye(3), [0, 0, 0], W, H, 10.0)])
+    dL = np.random.default_rng(0).normal(0, 1, (1, 3, H, W)).astype(np.float32)
+    o = oracle.Oracle(g, cams)
+    o.backward(dL)
+    full = o.pair_grads()
+    e1 = np.zeros(2)
+    gs = np.zeros((2, 2))
+    for y in range(H):
+        for x in range(W):
+            d = np.zeros_like(dL)
+            d[0, :, y, x] = dL[0, :, y, x]
+            o.backward(d)
+            pg = o.pair_grads()[0]
+            e1 += pg[:, 2]
+            gs += pg[:, :2]
+            np.testing.assert_allclose(pg[:, 2], np.hypot(pg[:, 0], pg[:, 1]), rtol=1e-12, atol=1e-300)
+    np.testing.assert_allclose(full[0, :, 2], e1, rtol=1e-12)
+    np.testing.assert_allclose(full[0, :, :2], gs, rtol=1e-9, atol=1e-12)
+    assert np.all(full[0, :, 2] > np.hypot(full[0, :, 0], full[0, :, 1]) * 1.01)
+
+
+def test_P13_b2_opposite_cameras_cancel():
+    """Appendix B.2: Gaussian at the origin, opposite cameras (golden file),
+    ∂L/∂C of view B = x-mirror of view A's → per-view Σ∇ are opposite in x, E_old ≈ 0 <
+    E2 ≤ E1, while the world gradient is along x and both views add to it.  Also pins
+    the NDC scale (R2): Σ∇_x = (∂L/∂μ_x)_view · z_cam/P0 with P0 = 2f/W."""
+    rows = [l.split("|") for l in open(os.path.join(GOLDEN, "b2_cameras.txt")) if l.strip() and not l.startswith("#")]
+    W = H = 33
+    f = 30.0
+    cams = synth.cams_array([synth.make_camera(np.array(r[1].split(), float).reshape(3, 3),
+                                               np.array(r[2].split(), float), W, H, f) for r in rows])
+    g = scene([0, 0, 0], log_scales=np.full(3, math.log(0.08)), logits=[1.0], sh=np.full((1, 1, 3), 0.7))
+    xs = np.arange(W) - 16.0
+    ramp = np.tile(np.sign(xs)[None, :] * (1 + 0.01 * np.abs(xs)[None, :]), (H, 1))
+    dA = np.tile(ramp[None], (3, 1, 1))
+    dL = np.stack([dA, dA[:, :, ::-1]]).astype(np.float32)
+    o = oracle.Oracle(g, cams)
+    gr = o.backward(dL)
+    pg = o.pair_grads()[:, 0]
+    assert abs(pg[0, 0]) > 0
+    np.testing.assert_allclose(pg[1, 0], -pg[0, 0], rtol=1e-9)
+    assert abs(pg[0, 1]) < 1e-9 * abs(pg[0, 0])
+    assert gr["e_old"][0] < 1e-8 * gr["e2"][0]
+    np.testing.assert_allclose(gr["e2"][0], 2 * abs(pg[0, 0]), rtol=1e-12)
+    assert gr["e1"][0] >= gr["e2"][0]
+    dm = gr["d_means"][0]
+    assert abs(dm[0]) > 0 and abs(dm[1]) < 1e-9 * abs(dm[0]) and abs(dm[2]) < 1e-9 * abs(dm[0])
+    # single view A: world x-gradient ↔ NDC x-gradient (isotropic on-axis ⇒ only μ' moves)
+    oA = oracle.Oracle(g, cams[:1])
+    gA = oA.backward(dL[:1])
+    P0 = 2 * f / W
+    np.testing.assert_allclose(oA.pair_grads()[0, 0, 0], gA["d_means"][0, 0] * 1.0 / P0, rtol=1e-9)
+
+
+def test_P16_gid_permutation_invariance():
+    """With distinct depths, relabelling the Gaussians changes nothing but the labels."""
+    g, cams = synth.make_scene(synth.scaled(synth.CONFIGS["tiny"], P=400))
+    dL = synth.make_dLdC_scaled(4, 64, 64, 7)
+    perm = np.random.default_rng(1).permutation(400)
+    gp = {k: (v[perm] if isinstance(v, np.ndarray) else v) for k, v in g.items()}
+    a = oracle.Oracle(g, cams)
+    b = oracle.Oracle(gp, cams)
+    ga, gb = a.backward(dL), b.backward(dL)
+    ia, ib = a.image(), b.image()
+    np.testing.assert_array_equal(ia["n_contrib"], ib["n_contrib"])
+    np.testing.assert_array_equal(ia["rgb"], ib["rgb"])
+    for k in ga:
+        np.testing.assert_allclose(gb[k], ga[k][perm], rtol=1e-12, atol=1e-15)
+
+
+# ---------------------------------------------------------------------- SH
+def _Y_textbook(k, d):
+    """Real SH in the [3DGS] sign convention, written from the textbook normalisations
+    (1/2)√(1/π), √(3/4π), (1/2)√(15/π), (1/4)√(5/π), (1/4)√(15/π), (1/4)√(35/2π),
+    (1/2)√(105/π), (1/4)√(21/2π), (1/4)√(7/π)."""
+    x, y, z = d
+    pi = math.pi
+    c = [0.5 * math.sqrt(1 / pi), math.sqrt(3 / (4 * pi))]
+    t = {0: c[0], 1: -c[1] * y, 2: c[1] * z, 3: -c[1] * x,
+         4: 0.5 * math.sqrt(15 / pi) * x * y, 5: -0.5 * math.sqrt(15 / pi) * y * z,
+         6: 0.25 * math.sqrt(5 / pi) * (2 * z * z - x * x - y * y), 7: -0.5 * math.sqrt(15 / pi) * x * z,
+         8: 0.25 * math.sqrt(15 / pi) * (x * x - y * y),
+         9: -0.25 * math.sqrt(35 / (2 * pi)) * y * (3 * x * x - y * y), 10: 0.5 * math.sqrt(105 / pi) * x * y * z,
+         11: -0.25 * math.sqrt(21 / (2 * pi)) * y * (4 * z * z - x * x - y * y),
+         12: 0.25 * math.sqrt(7 / pi) * z * (2 * z * z - 3 * x * x - 3 * y * y),
+         13: -0.25 * math.sqrt(21 / (2 * pi)) * x * (4 * z * z - x * x - y * y),
+         14: 0.25 * math.sqrt(105 / pi) * z * (x * x - y * y),
+         15: -0.25 * math.sqrt(35 / (2 * pi)) * x * (x * x - 3 * y * y)}
+    return t[k]
+
+
+def test_P17_sh_basis_along_axes_and_diagonal():
+    """rgb = max(0, Σ_k Y_k(dir) sh_k + 0.5), dir from the camera centre (R17): one unit
+    coefficient at a time, viewed along ±x, ±y, ±z and a diagonal."""
+    dirs = [(1, 0, 0), (-1, 0, 0), (0, 1, 0), (0, -1, 0), (0, 0, 1), (0, 0, -1), (1, 2, 2)]
+    for dvec in dirs:
+        d = np.array(dvec, float) / np.linalg.norm(dvec)
+        cam = synth.look_at(-2.5 * d, [0, 0, 0], 16, 16, 20.0)
+        for k in range(16):
+            sh = np.zeros((1, 16, 3))
+            sh[0, k, :] = [0.3, -0.2, 0.1]
+            g = scene([0, 0, 0], sh=sh, sh_degree=3)
+            o = oracle.Oracle(g, synth.cams_array([cam]))
+            dd = np.array([0, 0, 0]) - (-(np.array(cam["R"], np.float64).reshape(3, 3).T @ np.array(cam["t"], np.float64)))
+            dd /= np.linalg.norm(dd)
+            exp = np.maximum(0, _Y_textbook(k, dd) * np.array([0.3, -0.2, 0.1], np.float32).astype(float) + 0.5)
+            np.testing.assert_allclose(o.pairs()["rgb"][0, 0], exp, atol=1e-7, err_msg=f"k={k} dir={dvec}")
