@@ -1,0 +1,350 @@
+#!/usr/bin/env python
+"""bench.py — views/s of the batched multi-view rasterizer step on B200.
+
+One step = the whole hot path on one batch:
+preprocess (S1–S5) → render_fwd (S6) → render_bwd (S7) → adc_stats (S8–S9),
+plus, with N > 1 GPUs, one NCCL all-reduce of the flat [param grads | E1 | E2 |
+vis] buffer (every output is a sum over views).
+
+Workload: BASELINE.json configs[1], the Mip-NeRF-360 garden-shaped scene
+(3 M Gaussians, SH degree 3, 4 views of 1237×822) per GPU; with N GPUs each rank
+renders its own 4 views of the same scene (4·N views, weak scaling).  Inputs are
+resident in HBM and larger than L2 (708 MB of parameters).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config garden]
+  python bench.py --impl reference      # the oracle (CPU) on a bounded sample
+
+Prints ONE JSON line (rank 0).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+METRIC = "views/sec fwd+bwd (N-view batch, 1/2/4/8 B200) and % HBM/L2 roofline"
+UNIT = "views/s"
+
+# algorithmic fp32 flops of one (pixel, entry) evaluation, counted from the CA
+# forms of DESIGN.md §4 (FMA = 2): see DESIGN.md §7
+FWD_FLOPS_PER_EVAL = 42
+BWD_FLOPS_PER_EVAL = 96
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="garden", choices=list(synth.CONFIGS))
+    ap.add_argument("--impl", default="mvgs", choices=["mvgs", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+# --------------------------------------------------------------------- clocks
+class Clocks:
+    """nvidia-smi sampler running during the timed region (B200_PROFILING.md)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"], stdout=self.f,
+                                      stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except Exception:
+            self.p.kill()
+        self.f.flush()
+        rows = []
+        for line in open(self.f.name):
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 9:
+                rows.append(parts)
+        os.unlink(self.f.name)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[j] for r in rows for j in range(4) if r[5 + j].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+# --------------------------------------------------------------- distributed
+def dist_setup():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d, "measured"
+    return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+def stage_models(P, NK, V, NB, Q, K, T, evf, evb):
+    """(bound, algorithmic units per launch) per stage — DESIGN.md §7."""
+    pbytes = 4 * (11 + 3 * NK) * P
+    return {
+        "count": ("hbm", 12 * P + 4 * V * NB),
+        "scan_pairs": ("hbm", 3 * 4 * V * NB),
+        "project": ("hbm", pbytes + 4 * V * NB + Q * (48 + 8 + 48)),
+        "scan_buckets": ("hbm", 3 * 4 * V * T),
+        "dup_scatter": ("hbm", Q * (16 + 8) + 8 * K),
+        "sort": ("hbm", 12 * K),
+        "render_fwd": ("alu", FWD_FLOPS_PER_EVAL * evf),
+        "render_bwd": ("alu", BWD_FLOPS_PER_EVAL * evb),
+        "gauss_bwd": ("hbm", 2 * pbytes + Q * (16 + 8 + 48) + 16 * P),
+    }
+
+
+# ---------------------------------------------------------------------- mvgs
+def run_mvgs(args):
+    import torch
+
+    ws, rank, local = dist_setup()
+    N = args.gpus if ws == 1 else ws
+    torch.cuda.set_device(local)
+    dist = None
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2506_12727_b200 import mvgs
+
+    cfg = synth.CONFIGS[args.config]
+    Vr = cfg.V if N == 1 else cfg.V  # views per rank (weak scaling: per-GPU batch fixed)
+    g_np, cams_all = synth.make_scene(synth.scaled(cfg, V=Vr * N))
+    cams = synth.subset_views(cams_all, rank * Vr, (rank + 1) * Vr)
+    P = g_np["means"].shape[0]
+    NK = (g_np["sh_degree"] + 1) ** 2
+    S = g_np["sh"].shape[1]
+    dev = torch.device("cuda", local)
+    g = {k: torch.from_numpy(v).to(dev) for k, v in g_np.items() if isinstance(v, np.ndarray)}
+    g["sh_degree"] = g_np["sh_degree"]
+    dL = torch.from_numpy(synth.make_dLdC(Vr, cfg.H, cfg.W, cfg.seed + rank)).to(dev)
+
+    R = mvgs.Rasterizer(local)
+    R.preprocess(g, cams)  # sizes the workspace (query + reserve), untimed
+    st0 = R.stats
+    mvgs.reserve(R.ctx, int(st0["Q"] * 1.15) + 4096, int(st0["K"] * 1.15) + 65536)
+    # one flat buffer for every output that is a sum over views (single all-reduce)
+    sizes = dict(d_means=3 * P, d_log_scales=3 * P, d_quats=4 * P, d_opacity_logits=P, d_sh=S * 3 * P,
+                 e1=P, e2=P, vis=P)
+    flat = torch.empty(sum(sizes.values()), dtype=torch.float32, device=dev)
+    views, off = {}, 0
+    shapes = dict(d_means=(P, 3), d_log_scales=(P, 3), d_quats=(P, 4), d_opacity_logits=(P,), d_sh=(P, S, 3),
+                  e1=(P,), e2=(P,), vis=(P,))
+    for k, n in sizes.items():
+        views[k] = flat[off:off + n].view(shapes[k])
+        off += n
+    e_old = torch.empty(P, dtype=torch.float32, device=dev)
+    grads = {k: views[k] for k in ("d_means", "d_log_scales", "d_quats", "d_opacity_logits", "d_sh")}
+    adc = dict(e1=views["e1"], e2=views["e2"], e_old=e_old, vis=views["vis"])
+    outs = R.alloc_forward()
+
+    def step():
+        mvgs.preprocess(R.ctx, g, R.cams)
+        mvgs.render_fwd(R.ctx, *outs)
+        mvgs.render_bwd(R.ctx, dL, outs[1], outs[2])
+        mvgs.adc_stats(R.ctx, grads, adc)
+        if dist is not None:
+            dist.all_reduce(flat)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    st = mvgs.query(R.ctx)  # structural stats of this workload (sync, untimed)
+    mvgs.set_timing(R.ctx, True)
+    mvgs.stage_times(R.ctx)  # clear
+    clk = Clocks(local)
+    clk.start()
+    time.sleep(0.3)
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    for _ in range(args.steps):
+        step()
+    ev1.record()
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    clocks = clk.stop()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    stages = mvgs.stage_times(R.ctx)
+    mvgs.set_timing(R.ctx, False)
+    if dist is not None:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    views_total = Vr * N
+    value = views_total / (ms / 1e3)
+
+    # ---- e2e: the same step through the public API with HOST buffers:
+    # pinned host params + dL/dC copied in, gradients + ADC stats copied out.
+    host_in = {k: torch.from_numpy(v).pin_memory() for k, v in g_np.items() if isinstance(v, np.ndarray)}
+    host_dL = dL.cpu().pin_memory()
+    host_out = torch.empty_like(flat, device="cpu").pin_memory()
+    h2d = sum(t.numel() * 4 for t in host_in.values()) + host_dL.numel() * 4
+    d2h = host_out.numel() * 4
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.e2e_steps):
+        for k, t in host_in.items():
+            g[k].copy_(t, non_blocking=True)
+        dL.copy_(host_dL, non_blocking=True)
+        step()
+        host_out.copy_(flat, non_blocking=True)
+    e1_.record()
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1_) / args.e2e_steps
+    if dist is not None:
+        t = torch.tensor([e2e_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+
+    # ---- roofline of the dominant kernel
+    peaks, peak_src = measured_peaks()
+    T = st["tiles_x"] * st["tiles_y"]
+    NB = (P + 255) // 256
+    models = stage_models(P, NK, Vr, NB, st["Q"], st["K"], T * Vr, st["eval_fwd"], st["eval_bwd"])
+    dom = max(stages, key=lambda k: stages[k])
+    bound, units = models[dom]
+    t_dom = stages[dom] / 1e3
+    if bound == "hbm":
+        achieved = units / t_dom / 1e9
+        peak = float(peaks["hbm_gbs"])
+        unit = "GB/s"
+    else:
+        achieved = units / t_dom / 1e12
+        peak = 148 * 128 * 2 * float(peaks.get("sm_max_mhz", 1965.0)) * 1e6 / 1e12
+        unit = "TFLOP/s"
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", f"traffic_{args.config}.json")
+    if os.path.exists(tp):
+        traffic = json.load(open(tp)).get(dom)
+    roof = {"bound": bound, "achieved": round(achieved, 3), "peak": round(peak, 3), "unit": unit,
+            "frac": round(achieved / peak, 4), "traffic": traffic, "kernel": dom,
+            "peak_source": peak_src if bound == "hbm" else "derived: 148 SM x 128 FP32 lanes x 2 x sm_max_mhz",
+            "stage_ms": {k: round(v, 4) for k, v in stages.items()},
+            "stage_frac": {k: round(models[k][1] / (stages[k] / 1e3) / (1e9 * float(peaks["hbm_gbs"]) if models[k][0] == "hbm" else peak * 1e12), 4)
+                           for k in stages if stages[k] > 0}}
+
+    line = {
+        "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": N, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic (mvgs-synth v1, seeded; DESIGN.md §6)",
+        "config": {"workload": f"{cfg.name}: {P} Gaussians SH{cfg.sh_degree}, {Vr} views/GPU at {cfg.W}x{cfg.H}",
+                   "views_per_step": views_total, "global_batch_views": views_total, "parallelism": f"views dp{N}",
+                   "l2": "inputs larger than L2 (params %.0f MB)" % (sum(v.nbytes for v in g_np.values()
+                                                                       if isinstance(v, np.ndarray)) / 1e6),
+                   "Q": st["Q"], "K": st["K"], "max_bucket": st["max_bucket"], "n_visible": st["n_visible"],
+                   "eval_fwd_per_px": round(st["eval_fwd"] / (Vr * cfg.W * cfg.H), 2),
+                   "eval_bwd_per_px": round(st["eval_bwd"] / (Vr * cfg.W * cfg.H), 2)},
+        "clocks": clocks,
+        "e2e": {"value": round(views_total / (e2e_ms / 1e3), 3), "unit": UNIT, "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "ms_per_step": round(e2e_ms, 3)},
+        "gpu_launches": 13 * args.steps,
+        "roofline": roof,
+    }
+    if rank == 0 and N == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(cfg, g_np, cams, dL.cpu().numpy())
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+# ---------------------------------------------------------------- oracle arm
+def oracle_views_per_s(g_np, cams, dL, nviews):
+    import oracle
+    t0 = time.perf_counter()
+    o = oracle.Oracle(g_np, cams[:nviews])
+    o.backward(dL[:nviews])
+    dt = time.perf_counter() - t0
+    return nviews / dt, dt
+
+
+def cpu_baseline(cfg, g_np, cams, dL):
+    vps, dt = oracle_views_per_s(g_np, cams, dL, 1)
+    return {"value": round(vps, 5), "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"1 of the {len(cams)} views of the same {cfg.name} scene (all {g_np['means'].shape[0]} "
+                      f"Gaussians, full {cfg.W}x{cfg.H}), S1-S9 single-threaded C oracle, {dt:.1f} s"}
+
+
+def run_reference(args):
+    ws, rank, _ = dist_setup()
+    if rank != 0:
+        return
+    cfg = synth.CONFIGS[args.config]
+    g_np, cams = synth.make_scene(cfg)
+    dL = synth.make_dLdC(cfg.V, cfg.H, cfg.W, cfg.seed)
+    for _ in range(min(args.warmup, 0)):
+        pass
+    times = []
+    for _ in range(args.steps):
+        vps, dt = oracle_views_per_s(g_np, cams, dL, 1)
+        times.append(dt)
+    ms = 1e3 * statistics.mean(times)
+    value = 1.0 / (ms / 1e3)
+    line = {"impl": "reference", "metric": METRIC, "value": round(value, 5), "unit": UNIT,
+            "n_gpus": args.gpus if ws == 1 else ws, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(ms, 2), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic (mvgs-synth v1, seeded)",
+            "config": {"workload": f"{cfg.name}: {cfg.P} Gaussians SH{cfg.sh_degree}, {cfg.V} views at {cfg.W}x{cfg.H}",
+                       "sample": "each step = 1 of the views (bounded sample)"},
+            "cpu_baseline": {"value": round(value, 5), "unit": UNIT, "cores": 1, "kind": "oracle",
+                             "sample": "1 view of the scene per step, single-threaded C oracle"},
+            "e2e": {"value": round(value, 5), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_mvgs(args)
+
+
+if __name__ == "__main__":
+    main()

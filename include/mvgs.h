@@ -1,0 +1,180 @@
+/*
+ * mvgs.h — C ABI of libmvgs.so: a batched multi-view differentiable tile
+ * rasterizer with fused multi-view ADC statistics, hand-written for sm_100a.
+ *
+ * arXiv 2506.12727 (PAPER.md = P:n):
+ *   - rendering Eq. (1) ........................................ P:75–83
+ *   - two-stage tile rasterizer, one block per tile ............ P:87–93
+ *   - multi-view modifications: participation before
+ *     preprocessing, (tile, view, depth) keys, one block per
+ *     (tile, view) ............................................. P:571–579
+ *   - E_old, E1, E2 ............................................ P:14–21
+ * Every reading of a point the paper leaves open is listed in DESIGN.md §3
+ * (R1–R28); the fp32 arithmetic of every discrete decision is DESIGN.md §4.
+ *
+ * Conventions shared by every call
+ *   - All array arguments are caller-owned, contiguous, device pointers
+ *     (e.g. torch tensors) unless marked "host".  The library never frees
+ *     caller memory.  Context-internal buffers live until mvgs_destroy.
+ *   - `stream` is a cudaStream_t passed as void*.  Calls only enqueue work on
+ *     it; the only host-synchronising calls are mvgs_create, mvgs_reserve,
+ *     mvgs_query and (when V·tiles grows past its previous maximum)
+ *     mvgs_preprocess.  preprocess → render_fwd → render_bwd → adc_stats is
+ *     capturable in a CUDA graph once sizes are reserved.
+ *   - Errors are returned as mvgs_status; no exception crosses the ABI.
+ *     mvgs_last_error(ctx) gives a text for the last failure.
+ *   - Capacities: pairs Q and tile entries K are known only on the device.
+ *     When Q > reserved pairs or K > reserved entries the kernels set a device
+ *     flag and skip the overflowing work; the next mvgs_query reports
+ *     MVGS_ERR_CAPACITY together with the Q and K actually needed.  The caller
+ *     reserves and re-runs preprocess.
+ */
+#ifndef MVGS_H
+#define MVGS_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    MVGS_OK = 0,
+    MVGS_ERR_INVALID = -1,  /* null pointer, V ∉ [1, 65535], tiles/view > 65535,
+                               sh_degree > 3, sh_degree > sh_stride degree, P < 0,
+                               unequal view sizes (R25)                          */
+    MVGS_ERR_CAPACITY = -2, /* Q or K exceeded the reserved capacity             */
+    MVGS_ERR_STATE = -3,    /* render_fwd / render_bwd / adc_stats out of order  */
+    MVGS_ERR_CUDA = -4      /* CUDA runtime error, text in mvgs_last_error       */
+} mvgs_status;
+
+typedef struct mvgs_ctx mvgs_ctx;
+
+/* Raw Gaussian parameters, structure of arrays, fp32 (R18).  P:75 "mean μ,
+ * scale S, rotation R, color c and opacity o".  Activations (σ, exp, quaternion
+ * normalisation) are applied inside the library. */
+typedef struct {
+    int64_t P;                   /* number of Gaussians                           */
+    int32_t sh_degree;           /* active SH degree, 0..3 (R17)                  */
+    int32_t sh_stride;           /* SH coefficients stored per Gaussian, ≥ (deg+1)² */
+    const float *means;          /* [P,3]                                         */
+    const float *log_scales;     /* [P,3]   s = exp(log_scale)                    */
+    const float *quats;          /* [P,4]   (w,x,y,z), need not be normalised     */
+    const float *opacity_logits; /* [P]     o = sigmoid(logit)                    */
+    const float *sh;             /* [P,sh_stride,3]                               */
+} mvgs_gaussians;
+
+/* Pinhole camera, 76 bytes (R1): x_c = R x + t, +z forward, +y down. */
+typedef struct {
+    float R[9];          /* world→camera rotation, row-major */
+    float t[3];
+    float fx, fy, cx, cy; /* pixels */
+    int32_t width, height;
+    float znear;         /* participation: t.z > znear (R3) */
+} mvgs_camera;
+
+/* Outputs of mvgs_adc_stats: per-Gaussian parameter gradients (overwritten). */
+typedef struct {
+    float *d_means;          /* [P,3]          */
+    float *d_log_scales;     /* [P,3]          */
+    float *d_quats;          /* [P,4]          */
+    float *d_opacity_logits; /* [P]            */
+    float *d_sh;             /* [P,sh_stride,3]; coefficients above sh_degree are set to 0 */
+} mvgs_grads;
+
+/* Multi-view ADC statistics.  e1/e2/e_old/vis are overwritten with
+ * this batch's raw sums (R20); the *_acc pointers, when non-null, are
+ * accumulated into (+=) — the running ADC accumulators of P:4. */
+typedef struct {
+    float *e1;        /* [P] E1 = Σ_views Σ_pixels ‖∇_{p_i}L‖₂ */
+    float *e2;        /* [P] E2 = Σ_views ‖Σ_pixels of the view ∇_{p_i}L‖₂ */
+    float *e_old;     /* [P] E_old = ‖Σ_views Σ_pixels ∇_{p_i}L‖₂ (nullable) */
+    float *vis;       /* [P] number of views in which the Gaussian covers ≥1 tile (R21) */
+    float *e1_acc;    /* [P] nullable, += e1  */
+    float *e2_acc;    /* [P] nullable, += e2  */
+    float *denom_acc; /* [P] nullable, += vis */
+} mvgs_adc;
+
+typedef struct {
+    int64_t Q;             /* participating (Gaussian, view) pairs needed   */
+    int64_t K;             /* tile entries needed                           */
+    int64_t cap_pairs;     /* reserved                                      */
+    int64_t cap_entries;   /* reserved                                      */
+    int64_t max_bucket;    /* longest (view, tile) list                     */
+    int64_t n_visible;     /* pairs with tiles > 0                          */
+    int32_t overflow;      /* 1 if the last preprocess exceeded a capacity  */
+    int32_t V, tiles_x, tiles_y;
+    int64_t eval_fwd;      /* (pixel, entry) evaluations of the last render_fwd (Alg. 2 work) */
+    int64_t eval_bwd;      /* (pixel, entry) evaluations of the last render_bwd              */
+} mvgs_stats;
+
+/* Create a context on `device` with initial capacities (0 = a small default).
+ * Allocates device workspace (synchronous). */
+mvgs_status mvgs_create(mvgs_ctx **out, int device, int64_t max_pairs, int64_t max_entries);
+void mvgs_destroy(mvgs_ctx *ctx);
+const char *mvgs_last_error(const mvgs_ctx *ctx);
+/* Grow capacities to at least (max_pairs, max_entries).  Synchronises the device. */
+mvgs_status mvgs_reserve(mvgs_ctx *ctx, int64_t max_pairs, int64_t max_entries);
+
+/* S1–S5: participation (z-test) and pair allocation, per-pair EWA
+ * projection, conic, radius, tile rect and SH colour, duplication into
+ * (view, tile) buckets, on-chip depth sort of every bucket, ranges.
+ *   g     device parameter pointers (kept by the context for render_bwd /
+ *         adc_stats; they must stay valid and unchanged until adc_stats).
+ *   cams  host, V records; copied before return.
+ *   bg    host, 3 floats (R16), may be NULL for black.
+ * Pairs are laid out view-major, ascending Gaussian id within a view. */
+mvgs_status mvgs_preprocess(mvgs_ctx *ctx, const mvgs_gaussians *g, const mvgs_camera *cams, int32_t V,
+                            const float *bg, void *stream);
+
+/* S6 (Eq. 1, Alg. 2): front-to-back compositing of every (view, tile).
+ *   rgb       [V,3,H,W]  colour + T_final·bg
+ *   T_final   [V,H,W]    final transmittance
+ *   n_contrib [V,H,W]    1 + index of the last blended entry of the pixel's list (R14) */
+mvgs_status mvgs_render_fwd(mvgs_ctx *ctx, float *rgb, float *T_final, int32_t *n_contrib, void *stream);
+
+/* S7: back-to-front adjoint of Eq. (1) for every (view, tile) given
+ * dL_drgb [V,3,H,W] and the T_final / n_contrib written by render_fwd.
+ * Accumulates per-pair records (∇_{p_i}L sum in NDC, E1 partial, ∂conic, ∂o,
+ * ∂rgb) in context memory.  Requires a preceding render_fwd of the same
+ * preprocess; a second call without a new preprocess returns MVGS_ERR_STATE. */
+mvgs_status mvgs_render_bwd(mvgs_ctx *ctx, const float *dL_drgb, const float *T_final, const int32_t *n_contrib,
+                            void *stream);
+
+/* S8–S9: per-Gaussian chain rule summed over the batch's views
+ * and the ADC statistics E1, E2, E_old, vis.  `grads` and `adc`
+ * are host structs of device pointers.  Requires a preceding render_bwd. */
+mvgs_status mvgs_adc_stats(mvgs_ctx *ctx, const mvgs_grads *grads, const mvgs_adc *adc, void *stream);
+
+/* Synchronise and report sizes and the capacity flag of the last preprocess.
+ * Returns MVGS_ERR_CAPACITY if it overflowed. */
+mvgs_status mvgs_query(mvgs_ctx *ctx, mvgs_stats *out);
+
+/* Parity export (tests): copy the (view, tile) ranges [V*tiles+1] (int64) and
+ * the Gaussian id of every sorted entry [K] (int32) into caller device buffers. */
+mvgs_status mvgs_export_lists(mvgs_ctx *ctx, int64_t *range_start, int32_t *entry_gid, void *stream);
+
+/* Parity export (tests): per pair q < Q —
+ *   pair_ids [Q,2] int32   (view, gid)
+ *   pair_i   [Q,8] int32   (radius, rx0, ry0, rx1, ry1, tiles, clamp bits, 0)
+ *   pair_f   [Q,12] fp32   (depth, px, py, A, B, C, opacity, r, g, b, 0, 0)
+ *   pair_g   [Q,10] fp32   (Σ∇x, Σ∇y, e1, ∂A, ∂B, ∂C, ∂o, ∂r, ∂g, ∂b) after render_bwd
+ * Any pointer may be NULL. */
+mvgs_status mvgs_export_pairs(mvgs_ctx *ctx, int32_t *pair_ids, int32_t *pair_i, float *pair_f, float *pair_g,
+                              void *stream);
+
+/* Stage timing (measurement).  While enabled, every call records a pair of
+ * CUDA events on its stream around each kernel stage.  mvgs_stage_times
+ * synchronises on them, writes into ms[0..n) the AVERAGE milliseconds per run
+ * of each stage over all runs recorded since the previous read (0 if none), in
+ * the order of MVGS_STAGE_NAMES, clears the record, and returns the number of
+ * stages written. */
+#define MVGS_NUM_STAGES 9
+#define MVGS_STAGE_NAMES "count,scan_pairs,project,scan_buckets,dup_scatter,sort,render_fwd,render_bwd,gauss_bwd"
+mvgs_status mvgs_set_timing(mvgs_ctx *ctx, int enable);
+int mvgs_stage_times(mvgs_ctx *ctx, float *ms, int n);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MVGS_H */

@@ -270,7 +270,6 @@ typedef struct { /* per (Gaussian, view) fp64 projection state (O2) */
     double t[3], ux, uy, px, py, J[2][3], T[2][3], a, b, c, det, A, B, C;
     int clx, cly;          /* Jacobian clamp active (R4)          */
     double dir[3], dnorm;  /* normalised μ − camera centre and ‖μ − c‖      */
-    double Y[16], dY[16][3];
     double rgb[3];
     int rgb_clamped[3];
 } p64_t;
@@ -321,12 +320,13 @@ static void project64(const og_scene *g, int64_t i, const g64_t *a, const og_cam
     double d[3] = {a->mu[0] - cpos[0], a->mu[1] - cpos[1], a->mu[2] - cpos[2]};
     p->dnorm = sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
     for (int k = 0; k < 3; k++) p->dir[k] = d[k] / p->dnorm;
-    sh_basis(p->dir, p->Y, p->dY);
+    double Y[16], dY[16][3];
+    sh_basis(p->dir, Y, dY);
     int nk = (g->sh_degree + 1) * (g->sh_degree + 1);
     const float *sh = g->sh + (size_t)i * g->sh_stride * 3;
     for (int ch = 0; ch < 3; ch++) {
         double v = 0.5;
-        for (int k = 0; k < nk; k++) v += p->Y[k] * sh[3 * k + ch];
+        for (int k = 0; k < nk; k++) v += Y[k] * sh[3 * k + ch];
         p->rgb_clamped[ch] = v < 0.0;
         p->rgb[ch] = v < 0.0 ? 0.0 : v;
     }
@@ -390,7 +390,8 @@ typedef struct {
     p32_t *p32;            /* [V*P]                                          */
     float *o32;            /* [P] fp32 opacity for the decision chain        */
     g64_t *g64;            /* [P]                                            */
-    p64_t *p64;            /* [V*P] (only meaningful when p32.vis)           */
+    int32_t *p64i;         /* [V*P] index into p64 for visible pairs, else -1 */
+    p64_t *p64;            /* [number of visible pairs]                      */
     /* lists */
     int64_t *off;          /* [V*T+1]                                        */
     int32_t *gid;          /* [K]                                            */
@@ -424,7 +425,7 @@ static uint32_t fbits(float f)
 void oracle_destroy(oracle_t *h)
 {
     if (!h) return;
-    free(h->p32); free(h->o32); free(h->g64); free(h->p64); free(h->off); free(h->gid);
+    free(h->p32); free(h->o32); free(h->g64); free(h->p64); free(h->p64i); free(h->off); free(h->gid);
     free(h->img); free(h->Tfin); free(h->ncon); free(h->pg);
     free(h->d_means); free(h->d_ls); free(h->d_q); free(h->d_op); free(h->d_sh);
     free(h->e1); free(h->e2); free(h->eold); free(h->vis);
@@ -450,10 +451,11 @@ oracle_t *oracle_create(const og_scene *g, const og_cam *cams, int V, const floa
     h->T = h->TX * h->TY;
     int64_t P = g->P;
     h->p32 = (p32_t *)calloc((size_t)V * P + 1, sizeof(p32_t));
-    h->p64 = (p64_t *)calloc((size_t)V * P + 1, sizeof(p64_t));
+    h->p64i = (int32_t *)malloc(sizeof(int32_t) * ((size_t)V * P + 1));
     h->o32 = (float *)calloc(P + 1, sizeof(float));
     h->g64 = (g64_t *)calloc(P + 1, sizeof(g64_t));
-    /* O1 + O2 */
+    /* O1 + O2 (fp32 decisions) */
+    int64_t nvis = 0;
     for (int64_t i = 0; i < P; i++) {
         float Sig[6];
         activate32(g, i, &h->o32[i], Sig);
@@ -462,9 +464,16 @@ oracle_t *oracle_create(const og_scene *g, const og_cam *cams, int V, const floa
         for (int v = 0; v < V; v++) {
             p32_t *p = &h->p32[(size_t)v * P + i];
             project32(mu, Sig, &cams[v], p);
-            if (p->vis) project64(g, i, &h->g64[i], &cams[v], &h->p64[(size_t)v * P + i]);
+            h->p64i[(size_t)v * P + i] = p->vis ? (int32_t)nvis++ : -1;
         }
     }
+    /* O2 fp64 values for the visible pairs */
+    h->p64 = (p64_t *)calloc((size_t)nvis + 1, sizeof(p64_t));
+    for (int v = 0; v < V; v++)
+        for (int64_t i = 0; i < P; i++) {
+            int32_t k = h->p64i[(size_t)v * P + i];
+            if (k >= 0) project64(g, i, &h->g64[i], &cams[v], &h->p64[k]);
+        }
     /* O3: count, offsets, fill; O4: sort each list */
     int64_t nb = (int64_t)V * h->T;
     h->off = (int64_t *)calloc(nb + 1, sizeof(int64_t));
@@ -545,7 +554,7 @@ static void composite(oracle_t *h, const float *dLdC)
                     float Tn = T32 * (1.0f - alpha);
                     if (Tn < 1e-4f && !(h->flags & OG_NO_EARLY_TERMINATION)) break;
                     /* blended: value chain in fp64 */
-                    const p64_t *q = &h->p64[(size_t)v * P + i];
+                    const p64_t *q = &h->p64[h->p64i[(size_t)v * P + i]];
                     double ddx = q->px - x, ddy = q->py - y;
                     double pw = -0.5 * (q->A * ddx * ddx + q->C * ddy * ddy) - q->B * ddx * ddy;
                     double G = exp(pw);
@@ -582,7 +591,7 @@ static void composite(oracle_t *h, const float *dLdC)
                 double S[3] = {0, 0, 0};
                 for (int k = m - 1; k >= 0; k--) {
                     int32_t i = bl[k].gid;
-                    const p64_t *q = &h->p64[(size_t)v * P + i];
+                    const p64_t *q = &h->p64[h->p64i[(size_t)v * P + i]];
                     double *pg = &h->pg[((size_t)v * P + i) * NG];
                     double aT = bl[k].alpha * bl[k].T;
                     double dLda = 0;
@@ -636,7 +645,7 @@ static void gauss_backward(oracle_t *h)
             ap[v].gx = ap[v].gy = ap[v].e1 = 0;
             if (!p->vis) continue;
             visc += 1;
-            const p64_t *q = &h->p64[(size_t)v * P + i];
+            const p64_t *q = &h->p64[h->p64i[(size_t)v * P + i]];
             const double *pg = &h->pg[((size_t)v * P + i) * NG];
             const og_cam *cam = &h->cams[v];
             ap[v].gx = pg[0]; ap[v].gy = pg[1]; ap[v].e1 = pg[2];
@@ -702,13 +711,14 @@ static void gauss_backward(oracle_t *h)
             /* t = R_v μ + t_v */
             for (int k = 0; k < 3; k++) dmu[k] += Rv[0][k] * dt[0] + Rv[1][k] * dt[1] + Rv[2][k] * dt[2];
             /* colour: rgb = max(0, Σ_k Y_k(dir)·sh_k + 0.5), dir = (μ − c_v)/‖μ − c_v‖ */
-            double draw[3], ddir[3] = {0, 0, 0};
+            double draw[3], ddir[3] = {0, 0, 0}, Y[16], dY[16][3];
+            sh_basis(q->dir, Y, dY);
             for (int ch = 0; ch < 3; ch++) draw[ch] = q->rgb_clamped[ch] ? 0.0 : pg[7 + ch];
             for (int k = 0; k < nk; k++)
                 for (int ch = 0; ch < 3; ch++) {
-                    dsh[3 * k + ch] += q->Y[k] * draw[ch];
+                    dsh[3 * k + ch] += Y[k] * draw[ch];
                     double w = sh[3 * k + ch] * draw[ch];
-                    for (int e = 0; e < 3; e++) ddir[e] += q->dY[k][e] * w;
+                    for (int e = 0; e < 3; e++) ddir[e] += dY[k][e] * w;
                 }
             double dd = q->dir[0] * ddir[0] + q->dir[1] * ddir[1] + q->dir[2] * ddir[2];
             for (int e = 0; e < 3; e++) dmu[e] += (ddir[e] - q->dir[e] * dd) / q->dnorm;
@@ -830,7 +840,7 @@ void oracle_get_pairs(const oracle_t *h, int32_t *ints, float *flts, double *rgb
             f[0] = p->tz; f[1] = p->px; f[2] = p->py; f[3] = p->A; f[4] = p->B; f[5] = p->C;
         }
         if (rgb) {
-            for (int c = 0; c < 3; c++) rgb[3 * k + c] = p->vis ? h->p64[k].rgb[c] : 0.0;
+            for (int c = 0; c < 3; c++) rgb[3 * k + c] = p->vis ? h->p64[h->p64i[k]].rgb[c] : 0.0;
         }
     }
 }

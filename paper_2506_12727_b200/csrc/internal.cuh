@@ -1,0 +1,91 @@
+// internal.cuh — context layout and kernel launchers shared by the .cu files
+// of libmvgs.so (not part of the ABI).
+#pragma once
+#include <cstdint>
+#include <string>
+#include <utility>
+#include <vector>
+#include <cuda_runtime.h>
+#include "../../include/mvgs.h"
+
+namespace mvgs {
+
+constexpr int BLK = 256;          // Gaussians per preprocessing block (pair-slot granularity)
+constexpr int NG = 10;            // per-pair gradient record: Σ∇x Σ∇y e1 ∂A ∂B ∂C ∂o ∂r ∂g ∂b
+constexpr int PG_STRIDE = 12;     // floats per pair-gradient slot (48 B, 16-B aligned)
+constexpr int REC_F4 = 3;         // float4 per pair render record (48 B)
+
+// device counters (int32 slots in ctx->d_counters)
+enum { C_Q = 0, C_K = 1, C_OVERFLOW = 2, C_MAXB = 3, C_NVIS = 4, C_NCOUNTERS = 8 };
+
+// Per-pair meta: gid and (view << 8 | flags).  flags bit0..2: rgb clamped,
+// bit3: Jacobian x clamp, bit4: y clamp.
+struct PairMeta {
+    uint32_t gid;
+    uint32_t vf;
+};
+
+struct Launch {  // everything a kernel needs about the current batch
+    int64_t P;
+    int V, W, H, TX, TY, T, NB;
+    int sh_degree, sh_stride;
+    float bg[3];
+    const mvgs_camera* cams;  // device [V]
+    const float *means, *log_scales, *quats, *opac, *sh;
+    int64_t cap_pairs, cap_entries;
+    // workspace
+    int* blk_off;     // [V*NB + 1]  exclusive scan of per-(view, block) participation counts
+    int* bucket_off;  // [V*T + 1]   exclusive scan of per-(view, tile) entry counts
+    int* cursor;      // [V*T]
+    float4* rec;      // [cap_pairs * 3]
+    PairMeta* meta;   // [cap_pairs]
+    float* pgrad;     // [cap_pairs * PG_STRIDE]
+    uint32_t *key, *val, *key2, *val2;  // [cap_entries]
+    int* counters;    // [C_NCOUNTERS]
+    unsigned long long* counters64;  // [2]: fwd / bwd (pixel, entry) evaluations
+};
+
+}  // namespace mvgs
+
+struct mvgs_ctx {
+    int device = 0;
+    int64_t cap_pairs = 0, cap_entries = 0;
+    int64_t cap_blk = 0, cap_buckets = 0, cap_cams = 0, cap_scan = 0;
+    int state = 0;  // 0 none, 1 preprocessed, 2 forward done, 3 backward done
+    mvgs::Launch L{};
+    mvgs_gaussians g{};
+    // device buffers
+    mvgs_camera* d_cams = nullptr;
+    int* d_blk = nullptr;
+    int* d_bucket = nullptr;
+    int* d_cursor = nullptr;
+    float4* d_rec = nullptr;
+    mvgs::PairMeta* d_meta = nullptr;
+    float* d_pgrad = nullptr;
+    uint32_t *d_key = nullptr, *d_val = nullptr, *d_key2 = nullptr, *d_val2 = nullptr;
+    int* d_counters = nullptr;
+    unsigned long long* d_counters64 = nullptr;
+    int* d_scan = nullptr;  // scan block sums
+    mvgs_camera* h_cams = nullptr;  // pinned staging
+    cudaEvent_t cams_ev = nullptr;
+    cudaStream_t last_stream = nullptr;
+    bool timing = false;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_rec[MVGS_NUM_STAGES];  // recorded since last read
+    std::vector<cudaEvent_t> ev_pool;
+    std::string err;
+};
+
+namespace mvgs {
+// launchers (return cudaGetLastError())
+cudaError_t scan_exclusive(int* a, int n, int* total_slot, int* tmp, cudaStream_t s);
+cudaError_t launch_count(const Launch& L, cudaStream_t s);
+cudaError_t launch_project(const Launch& L, cudaStream_t s);
+cudaError_t launch_dup_scatter(const Launch& L, cudaStream_t s);
+cudaError_t launch_bucket_sort(const Launch& L, cudaStream_t s);
+cudaError_t launch_render_fwd(const Launch& L, float* rgb, float* Tf, int32_t* nc, cudaStream_t s);
+cudaError_t launch_render_bwd(const Launch& L, const float* dL, const float* Tf, const int32_t* nc, cudaStream_t s);
+cudaError_t launch_gauss_bwd(const Launch& L, const mvgs_grads& gr, const mvgs_adc& adc, cudaStream_t s);
+cudaError_t launch_export(const Launch& L, int64_t* range_start, int32_t* entry_gid, int32_t* pair_ids,
+                          int32_t* pair_i, float* pair_f, float* pair_g, cudaStream_t s);
+int scan_tmp_size(int n);
+}  // namespace mvgs

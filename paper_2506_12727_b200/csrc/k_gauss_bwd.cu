@@ -1,0 +1,281 @@
+// k_gauss_bwd.cu — S8 per-Gaussian chain rule and S9 ADC statistics.
+//
+// One thread per Gaussian walks its pairs (one per participating view, found
+// again with the same ballot ranking k_project used, so no pair→Gaussian index
+// is stored) and sums over the batch's views — the multi-view mini-batch
+// gradient.  No atomics: a Gaussian's views are all in one thread.
+// The Σ → (scale, rotation) chain is linear in ∂L/∂Σ, so ∂L/∂Σ is summed over
+// views first and pushed through once.  The same loop reduces the ADC
+// statistics:
+//   E1    = Σ_views e1[pair]               (e1 = Σ_pixels ‖∇_{p_i}L‖, from S7)
+//   E2    = Σ_views ‖Σ∇[pair]‖
+//   E_old = ‖Σ_views Σ∇[pair]‖
+//   vis   = #views with tiles > 0 (R21)
+#include "ca.cuh"
+#include "internal.cuh"
+
+namespace mvgs {
+
+constexpr unsigned FULLG = 0xffffffffu;
+
+__constant__ float g_SH1 = 0.4886025119029199f;
+__constant__ float g_SH2[5] = {1.0925484305920792f, -1.0925484305920792f, 0.31539156525252005f,
+                               -1.0925484305920792f, 0.5462742152960396f};
+__constant__ float g_SH3[7] = {-0.5900435899266435f, 2.890611442640554f, -0.4570457994644658f,
+                               0.3731763325901154f, -0.4570457994644658f, 1.445305721320277f,
+                               -0.5900435899266435f};
+
+template <int D>
+__global__ __launch_bounds__(BLK) void k_gauss_bwd(Launch L, mvgs_grads gr, mvgs_adc adc) {
+    constexpr int NK = (D + 1) * (D + 1);
+    __shared__ int wc[BLK / 32][32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const unsigned lt = (1u << lane) - 1u;
+    const int64_t g = (int64_t)blockIdx.x * BLK + threadIdx.x;
+    const bool valid = g < L.P;
+    float mx = 0.f, my = 0.f, mz = 0.f;
+    Activ a;
+    float sh[NK * 3], dsh[NK * 3];
+#pragma unroll
+    for (int k = 0; k < NK * 3; k++) dsh[k] = 0.f;
+    if (valid) {
+        mx = L.means[3 * g];
+        my = L.means[3 * g + 1];
+        mz = L.means[3 * g + 2];
+        ca_activate(L.log_scales + 3 * g, L.quats + 4 * g, L.opac[g], a);
+        const float* s = L.sh + g * (int64_t)L.sh_stride * 3;
+#pragma unroll
+        for (int k = 0; k < NK * 3; k++) sh[k] = s[k];
+    }
+    float dmx = 0.f, dmy = 0.f, dmz = 0.f;
+    float G00 = 0.f, G01 = 0.f, G02 = 0.f, G11 = 0.f, G12 = 0.f, G22 = 0.f;  // ∂L/∂Σ (symmetric)
+    float dop = 0.f, e1 = 0.f, e2 = 0.f, gsx = 0.f, gsy = 0.f, nvis = 0.f;
+    const float sW = 2.0f / (float)L.W, sH = 2.0f / (float)L.H;
+    for (int v0 = 0; v0 < L.V; v0 += 32) {
+        const int nv = min(32, L.V - v0);
+        for (int k = 0; k < nv; k++) {
+            const mvgs_camera& c = L.cams[v0 + k];
+            const bool vis = valid && ca_depth(c, mx, my, mz) > c.znear;
+            const unsigned bal = __ballot_sync(FULLG, vis);
+            if (lane == 0) wc[warp][k] = __popc(bal);
+        }
+        __syncthreads();
+        for (int k = 0; k < nv; k++) {
+            const int v = v0 + k;
+            const mvgs_camera& c = L.cams[v];
+            const bool zvis = valid && ca_depth(c, mx, my, mz) > c.znear;
+            const unsigned bal = __ballot_sync(FULLG, zvis);
+            if (!zvis) continue;
+            int pre = 0;
+            for (int w = 0; w < warp; w++) pre += wc[w][k];
+            const int64_t pair = (int64_t)L.blk_off[(int64_t)v * L.NB + blockIdx.x] + pre + __popc(bal & lt);
+            if (pair >= L.cap_pairs) continue;
+            const float4 r2 = L.rec[3 * pair + 2];
+            if (__float_as_uint(r2.z) == __float_as_uint(r2.w)) continue;  // tiles == 0: inert (R27)
+            const uint32_t flags = L.meta[pair].vf & 0xffu;
+            const float4 pg0 = reinterpret_cast<const float4*>(L.pgrad + pair * PG_STRIDE)[0];
+            const float4 pg1 = reinterpret_cast<const float4*>(L.pgrad + pair * PG_STRIDE)[1];
+            const float4 pg2 = reinterpret_cast<const float4*>(L.pgrad + pair * PG_STRIDE)[2];
+            // pg: (Σ∇x, Σ∇y, e1, ∂A) (∂B, ∂C, ∂o, ∂r) (∂g, ∂b, -, -)
+            nvis += 1.f;
+            e1 += pg0.z;
+            e2 += sqrtf(pg0.x * pg0.x + pg0.y * pg0.y);
+            gsx += pg0.x;
+            gsy += pg0.y;
+            dop += pg1.z;
+            Proj p;
+            ca_project(c, mx, my, mz, a.Sig, L.TX, L.TY, p);
+            const float tz = p.tz, itz = 1.f / tz, itz2 = itz * itz;
+            // μ' (pixels) = (fx·tx/tz + cx, fy·ty/tz + cy); ∂L/∂μ' = Σ∇·(2/W, 2/H) (R2)
+            const float dpx = pg0.x * sW, dpy = pg0.y * sH;
+            float dtx = c.fx * itz * dpx;
+            float dty = c.fy * itz * dpy;
+            float dtz = -(c.fx * p.tx * itz2) * dpx - (c.fy * p.ty * itz2) * dpy;
+            // conic (A,B,C) = (c,−b,a)/det → Σ' entries (a,b,c)
+            const float dA = pg0.w, dB = pg1.x, dC = pg1.y;
+            const float id2 = 1.f / (p.det * p.det);
+            const float da = (-p.c * p.c * dA + p.b * p.c * dB - p.b * p.b * dC) * id2;
+            const float dc = (-p.b * p.b * dA + p.a * p.b * dB - p.a * p.a * dC) * id2;
+            const float db = (2.f * p.b * p.c * dA - (p.det + 2.f * p.b * p.b) * dB + 2.f * p.a * p.b * dC) * id2;
+            const float hb = 0.5f * db;
+            // ∂L/∂Σ += Tᵀ Gs T,  Gs = [[da, hb], [hb, dc]]
+            const float* T0 = p.T0;
+            const float* T1 = p.T1;
+            float GT0[3], GT1[3];  // Gs·T rows
+#pragma unroll
+            for (int j = 0; j < 3; j++) {
+                GT0[j] = da * T0[j] + hb * T1[j];
+                GT1[j] = hb * T0[j] + dc * T1[j];
+            }
+            G00 += T0[0] * GT0[0] + T1[0] * GT1[0];
+            G01 += T0[0] * GT0[1] + T1[0] * GT1[1];
+            G02 += T0[0] * GT0[2] + T1[0] * GT1[2];
+            G11 += T0[1] * GT0[1] + T1[1] * GT1[1];
+            G12 += T0[1] * GT0[2] + T1[1] * GT1[2];
+            G22 += T0[2] * GT0[2] + T1[2] * GT1[2];
+            // ∂L/∂T = 2 (Gs T) Σ
+            const float* S = a.Sig;
+            float dT0[3], dT1[3];
+            dT0[0] = 2.f * (GT0[0] * S[0] + GT0[1] * S[1] + GT0[2] * S[2]);
+            dT0[1] = 2.f * (GT0[0] * S[1] + GT0[1] * S[3] + GT0[2] * S[4]);
+            dT0[2] = 2.f * (GT0[0] * S[2] + GT0[1] * S[4] + GT0[2] * S[5]);
+            dT1[0] = 2.f * (GT1[0] * S[0] + GT1[1] * S[1] + GT1[2] * S[2]);
+            dT1[1] = 2.f * (GT1[0] * S[1] + GT1[1] * S[3] + GT1[2] * S[4]);
+            dT1[2] = 2.f * (GT1[0] * S[2] + GT1[1] * S[4] + GT1[2] * S[5]);
+            // T = J R_v ⇒ ∂L/∂J = ∂L/∂T R_vᵀ (only the non-constant entries of J)
+            const float* R = c.R;
+            const float dJ00 = dT0[0] * R[0] + dT0[1] * R[1] + dT0[2] * R[2];
+            const float dJ02 = dT0[0] * R[6] + dT0[1] * R[7] + dT0[2] * R[8];
+            const float dJ11 = dT1[0] * R[3] + dT1[1] * R[4] + dT1[2] * R[5];
+            const float dJ12 = dT1[0] * R[6] + dT1[1] * R[7] + dT1[2] * R[8];
+            dtz += -c.fx * itz2 * dJ00 - c.fy * itz2 * dJ11;
+            // J02 = −fx·ũx/tz: ũx = tx/tz unclamped (∂/∂tx = −fx/tz², ∂/∂tz = 2fx·ux/tz²),
+            // constant when clamped (∂/∂tz = fx·ũx/tz²) — R4
+            if (!(flags & 8u)) {
+                dtx += -c.fx * itz2 * dJ02;
+                dtz += 2.f * c.fx * p.uxc * itz2 * dJ02;
+            } else {
+                dtz += c.fx * p.uxc * itz2 * dJ02;
+            }
+            if (!(flags & 16u)) {
+                dty += -c.fy * itz2 * dJ12;
+                dtz += 2.f * c.fy * p.uyc * itz2 * dJ12;
+            } else {
+                dtz += c.fy * p.uyc * itz2 * dJ12;
+            }
+            // t = R_v μ + t_v
+            dmx += R[0] * dtx + R[3] * dty + R[6] * dtz;
+            dmy += R[1] * dtx + R[4] * dty + R[7] * dtz;
+            dmz += R[2] * dtx + R[5] * dty + R[8] * dtz;
+            // colour: rgb = max(0, Σ Y_k(dir) sh_k + 0.5), dir = (μ − c_v)/‖μ − c_v‖
+            const float dr0 = (flags & 1u) ? 0.f : pg1.w;
+            const float dr1 = (flags & 2u) ? 0.f : pg2.x;
+            const float dr2 = (flags & 4u) ? 0.f : pg2.y;
+            const float cpx = -(R[0] * c.t[0] + R[3] * c.t[1] + R[6] * c.t[2]);
+            const float cpy = -(R[1] * c.t[0] + R[4] * c.t[1] + R[7] * c.t[2]);
+            const float cpz = -(R[2] * c.t[0] + R[5] * c.t[1] + R[8] * c.t[2]);
+            float x = mx - cpx, y = my - cpy, z = mz - cpz;
+            const float dn = sqrtf(x * x + y * y + z * z), idn = 1.f / dn;
+            x *= idn; y *= idn; z *= idn;
+            float wk[NK];
+#pragma unroll
+            for (int kk = 0; kk < NK; kk++) wk[kk] = sh[3 * kk] * dr0 + sh[3 * kk + 1] * dr1 + sh[3 * kk + 2] * dr2;
+            float Y[NK];
+            Y[0] = 0.28209479177387814f;
+            float ddx = 0.f, ddy = 0.f, ddz = 0.f;
+            if (D >= 1) {
+                Y[1] = -g_SH1 * y; Y[2] = g_SH1 * z; Y[3] = -g_SH1 * x;
+                ddx += -g_SH1 * wk[3];
+                ddy += -g_SH1 * wk[1];
+                ddz += g_SH1 * wk[2];
+            }
+            if (D >= 2) {
+                const float xx = x * x, yy = y * y, zz = z * z;
+                Y[4] = g_SH2[0] * x * y;
+                Y[5] = g_SH2[1] * y * z;
+                Y[6] = g_SH2[2] * (2.f * zz - xx - yy);
+                Y[7] = g_SH2[3] * x * z;
+                Y[8] = g_SH2[4] * (xx - yy);
+                ddx += g_SH2[0] * y * wk[4] - 2.f * g_SH2[2] * x * wk[6] + g_SH2[3] * z * wk[7] + 2.f * g_SH2[4] * x * wk[8];
+                ddy += g_SH2[0] * x * wk[4] + g_SH2[1] * z * wk[5] - 2.f * g_SH2[2] * y * wk[6] - 2.f * g_SH2[4] * y * wk[8];
+                ddz += g_SH2[1] * y * wk[5] + 4.f * g_SH2[2] * z * wk[6] + g_SH2[3] * x * wk[7];
+                if (D >= 3) {
+                    Y[9] = g_SH3[0] * y * (3.f * xx - yy);
+                    Y[10] = g_SH3[1] * x * y * z;
+                    Y[11] = g_SH3[2] * y * (4.f * zz - xx - yy);
+                    Y[12] = g_SH3[3] * z * (2.f * zz - 3.f * xx - 3.f * yy);
+                    Y[13] = g_SH3[4] * x * (4.f * zz - xx - yy);
+                    Y[14] = g_SH3[5] * z * (xx - yy);
+                    Y[15] = g_SH3[6] * x * (xx - 3.f * yy);
+                    ddx += g_SH3[0] * 6.f * x * y * wk[9] + g_SH3[1] * y * z * wk[10] - g_SH3[2] * 2.f * x * y * wk[11]
+                         - g_SH3[3] * 6.f * x * z * wk[12] + g_SH3[4] * (4.f * zz - 3.f * xx - yy) * wk[13]
+                         + g_SH3[5] * 2.f * x * z * wk[14] + g_SH3[6] * (3.f * xx - 3.f * yy) * wk[15];
+                    ddy += g_SH3[0] * (3.f * xx - 3.f * yy) * wk[9] + g_SH3[1] * x * z * wk[10]
+                         + g_SH3[2] * (4.f * zz - xx - 3.f * yy) * wk[11] - g_SH3[3] * 6.f * y * z * wk[12]
+                         - g_SH3[4] * 2.f * x * y * wk[13] - g_SH3[5] * 2.f * y * z * wk[14]
+                         - g_SH3[6] * 6.f * x * y * wk[15];
+                    ddz += g_SH3[1] * x * y * wk[10] + g_SH3[2] * 8.f * y * z * wk[11]
+                         + g_SH3[3] * (6.f * zz - 3.f * xx - 3.f * yy) * wk[12] + g_SH3[4] * 8.f * x * z * wk[13]
+                         + g_SH3[5] * (xx - yy) * wk[14];
+                }
+            }
+#pragma unroll
+            for (int kk = 0; kk < NK; kk++) {
+                dsh[3 * kk] += Y[kk] * dr0;
+                dsh[3 * kk + 1] += Y[kk] * dr1;
+                dsh[3 * kk + 2] += Y[kk] * dr2;
+            }
+            const float dd = x * ddx + y * ddy + z * ddz;
+            dmx += (ddx - x * dd) * idn;
+            dmy += (ddy - y * dd) * idn;
+            dmz += (ddz - z * dd) * idn;
+        }
+        __syncthreads();
+    }
+    if (!valid) return;
+    // Σ = M Mᵀ, M = R diag(s): ∂L/∂M = 2 G M (G symmetric)
+    const float* R = a.R;
+    const float Gm[9] = {G00, G01, G02, G01, G11, G12, G02, G12, G22};
+    float dM[9];
+#pragma unroll
+    for (int r = 0; r < 3; r++)
+#pragma unroll
+        for (int cc = 0; cc < 3; cc++) {
+            const float Mkc0 = R[0 * 3 + cc] * a.s[cc], Mkc1 = R[1 * 3 + cc] * a.s[cc], Mkc2 = R[2 * 3 + cc] * a.s[cc];
+            dM[3 * r + cc] = 2.f * (Gm[3 * r] * Mkc0 + Gm[3 * r + 1] * Mkc1 + Gm[3 * r + 2] * Mkc2);
+        }
+    float dR[9], dls[3];
+#pragma unroll
+    for (int cc = 0; cc < 3; cc++) {
+        float ds = 0.f;
+#pragma unroll
+        for (int r = 0; r < 3; r++) {
+            ds += dM[3 * r + cc] * R[3 * r + cc];
+            dR[3 * r + cc] = dM[3 * r + cc] * a.s[cc];
+        }
+        dls[cc] = ds * a.s[cc];  // s = exp(λ)
+    }
+    const float w = a.q[0], x = a.q[1], y = a.q[2], z = a.q[3];
+    float dq[4];
+    dq[0] = -2.f * z * dR[1] + 2.f * y * dR[2] + 2.f * z * dR[3] - 2.f * x * dR[5] - 2.f * y * dR[6] + 2.f * x * dR[7];
+    dq[1] = 2.f * y * dR[1] + 2.f * z * dR[2] + 2.f * y * dR[3] - 4.f * x * dR[4] - 2.f * w * dR[5] + 2.f * z * dR[6]
+          + 2.f * w * dR[7] - 4.f * x * dR[8];
+    dq[2] = -4.f * y * dR[0] + 2.f * x * dR[1] + 2.f * w * dR[2] + 2.f * x * dR[3] + 2.f * z * dR[5] - 2.f * w * dR[6]
+          + 2.f * z * dR[7] - 4.f * y * dR[8];
+    dq[3] = -4.f * z * dR[0] - 2.f * w * dR[1] + 2.f * x * dR[2] + 2.f * w * dR[3] - 4.f * z * dR[4] + 2.f * y * dR[5]
+          + 2.f * x * dR[6] + 2.f * y * dR[7];
+    const float qd = w * dq[0] + x * dq[1] + y * dq[2] + z * dq[3];
+    // q̂ = q/‖q‖ ⇒ ∂L/∂q = (∂q̂ − q̂(q̂·∂q̂))/‖q‖
+#pragma unroll
+    for (int k = 0; k < 4; k++) gr.d_quats[4 * g + k] = (dq[k] - a.q[k] * qd) * a.inv_norm;
+    gr.d_means[3 * g] = dmx;
+    gr.d_means[3 * g + 1] = dmy;
+    gr.d_means[3 * g + 2] = dmz;
+    gr.d_log_scales[3 * g] = dls[0];
+    gr.d_log_scales[3 * g + 1] = dls[1];
+    gr.d_log_scales[3 * g + 2] = dls[2];
+    gr.d_opacity_logits[g] = dop * a.o * (1.f - a.o);
+    float* ds = gr.d_sh + g * (int64_t)L.sh_stride * 3;
+#pragma unroll
+    for (int k = 0; k < NK * 3; k++) ds[k] = dsh[k];
+    for (int k = NK * 3; k < L.sh_stride * 3; k++) ds[k] = 0.f;
+    adc.e1[g] = e1;
+    adc.e2[g] = e2;
+    if (adc.e_old) adc.e_old[g] = sqrtf(gsx * gsx + gsy * gsy);
+    adc.vis[g] = nvis;
+    if (adc.e1_acc) adc.e1_acc[g] += e1;
+    if (adc.e2_acc) adc.e2_acc[g] += e2;
+    if (adc.denom_acc) adc.denom_acc[g] += nvis;
+}
+
+cudaError_t launch_gauss_bwd(const Launch& L, const mvgs_grads& gr, const mvgs_adc& adc, cudaStream_t s) {
+    switch (L.sh_degree) {
+        case 0: k_gauss_bwd<0><<<L.NB, BLK, 0, s>>>(L, gr, adc); break;
+        case 1: k_gauss_bwd<1><<<L.NB, BLK, 0, s>>>(L, gr, adc); break;
+        case 2: k_gauss_bwd<2><<<L.NB, BLK, 0, s>>>(L, gr, adc); break;
+        default: k_gauss_bwd<3><<<L.NB, BLK, 0, s>>>(L, gr, adc); break;
+    }
+    return cudaGetLastError();
+}
+
+}  // namespace mvgs

@@ -1,0 +1,363 @@
+// k_preprocess.cu — S1–S3 (+ S5) of the hot path.
+//
+//   k_count       S1  participation test per (Gaussian, view) — "determines which
+//                     Gaussians participate in rendering for each viewpoint … before
+//                     preprocessing" — counted per (view, 256-Gaussian block)
+//   scan          S1  exclusive scan → pair slots: "memory is allocated only for these
+//                     participating Gaussians"; view-major, ascending gid
+//   k_project     S2  EWA projection, conic, radius, tile rect, SH colour per pair
+//                     (P:75), one thread per Gaussian looping its views so
+//                     per-Gaussian work (activations, Σ, SH load) is done once for
+//                     the whole batch; also the per-(view, tile) entry histogram (S3)
+//   scan          S3/S5 exclusive scan of the histogram → bucket offsets = ranges
+//   k_dup_scatter S3  "duplicating projected Gaussians for each tile they cover"
+//                     (P:576): one 32-bit depth key + 32-bit pair value per entry,
+//                     written into its (view, tile) bucket (the key's view and tile
+//                     fields of P:579 are the bucket index)
+#include "ca.cuh"
+#include "internal.cuh"
+
+namespace mvgs {
+
+constexpr unsigned FULL = 0xffffffffu;
+
+// ------------------------------------------------------------------ scan
+constexpr int SCAN_T = 1024, SCAN_IPT = 4, SCAN_TILE = SCAN_T * SCAN_IPT;
+
+int scan_tmp_size(int n) { return (n + SCAN_TILE - 1) / SCAN_TILE + 2; }
+
+__device__ __forceinline__ int block_exclusive_scan_1024(int x, int* sm /*[32]*/, int* total) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int inc = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        int y = __shfl_up_sync(FULL, inc, o);
+        if (lane >= o) inc += y;
+    }
+    if (lane == 31) sm[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+        int w = sm[lane];
+        int wi = w;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            int y = __shfl_up_sync(FULL, wi, o);
+            if (lane >= o) wi += y;
+        }
+        sm[lane] = wi - w;
+        if (lane == 31) sm[32] = wi;
+    }
+    __syncthreads();
+    int r = sm[warp] + inc - x;
+    *total = sm[32];
+    __syncthreads();
+    return r;
+}
+
+__global__ __launch_bounds__(SCAN_T) void k_scan_reduce(const int* __restrict__ a, int n, int* __restrict__ tmp) {
+    __shared__ int sm[33];
+    int base = blockIdx.x * SCAN_TILE + threadIdx.x * SCAN_IPT;
+    int s = 0;
+#pragma unroll
+    for (int i = 0; i < SCAN_IPT; i++) s += (base + i < n) ? a[base + i] : 0;
+    int tot;
+    block_exclusive_scan_1024(s, sm, &tot);
+    if (threadIdx.x == 0) tmp[blockIdx.x] = tot;
+}
+
+__global__ __launch_bounds__(SCAN_T) void k_scan_top(int* __restrict__ tmp, int nb, int* __restrict__ total_slot) {
+    __shared__ int sm[33];
+    int carry = 0;
+    for (int c0 = 0; c0 < nb; c0 += SCAN_T) {
+        int i = c0 + threadIdx.x;
+        int x = i < nb ? tmp[i] : 0;
+        int tot;
+        int ex = block_exclusive_scan_1024(x, sm, &tot);
+        if (i < nb) tmp[i] = ex + carry;
+        carry += tot;
+    }
+    if (threadIdx.x == 0) {
+        tmp[nb] = carry;
+        if (total_slot) *total_slot = carry;
+    }
+}
+
+__global__ __launch_bounds__(SCAN_T) void k_scan_apply(int* __restrict__ a, int n, const int* __restrict__ tmp, int nb) {
+    __shared__ int sm[33];
+    int base = blockIdx.x * SCAN_TILE + threadIdx.x * SCAN_IPT;
+    int v[SCAN_IPT];
+    int s = 0;
+#pragma unroll
+    for (int i = 0; i < SCAN_IPT; i++) {
+        v[i] = (base + i < n) ? a[base + i] : 0;
+        s += v[i];
+    }
+    int tot;
+    int ex = block_exclusive_scan_1024(s, sm, &tot) + tmp[blockIdx.x];
+#pragma unroll
+    for (int i = 0; i < SCAN_IPT; i++) {
+        if (base + i < n) a[base + i] = ex;
+        ex += v[i];
+    }
+    if (blockIdx.x == nb - 1 && threadIdx.x == 0) a[n] = tmp[nb];
+}
+
+// Exclusive scan of a[0..n) in place; a[n] and *total_slot receive the total.
+cudaError_t scan_exclusive(int* a, int n, int* total_slot, int* tmp, cudaStream_t s) {
+    int nb = (n + SCAN_TILE - 1) / SCAN_TILE;
+    if (nb == 0) nb = 1;
+    k_scan_reduce<<<nb, SCAN_T, 0, s>>>(a, n, tmp);
+    k_scan_top<<<1, SCAN_T, 0, s>>>(tmp, nb, total_slot);
+    k_scan_apply<<<nb, SCAN_T, 0, s>>>(a, n, tmp, nb);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ S1
+__global__ __launch_bounds__(BLK) void k_count(Launch L) {
+    __shared__ int wc[BLK / 32][32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t g = (int64_t)blockIdx.x * BLK + threadIdx.x;
+    const bool valid = g < L.P;
+    float mx = 0.f, my = 0.f, mz = 0.f;
+    if (valid) {
+        mx = L.means[3 * g];
+        my = L.means[3 * g + 1];
+        mz = L.means[3 * g + 2];
+    }
+    for (int v0 = 0; v0 < L.V; v0 += 32) {
+        const int nv = min(32, L.V - v0);
+        for (int k = 0; k < nv; k++) {
+            const mvgs_camera& c = L.cams[v0 + k];
+            const bool vis = valid && ca_depth(c, mx, my, mz) > c.znear;
+            const unsigned bal = __ballot_sync(FULL, vis);
+            if (lane == 0) wc[warp][k] = __popc(bal);
+        }
+        __syncthreads();
+        if (threadIdx.x < nv) {
+            int s = 0;
+#pragma unroll
+            for (int w = 0; w < BLK / 32; w++) s += wc[w][threadIdx.x];
+            L.blk_off[(int64_t)(v0 + threadIdx.x) * L.NB + blockIdx.x] = s;
+        }
+        __syncthreads();
+    }
+}
+
+cudaError_t launch_count(const Launch& L, cudaStream_t s) {
+    k_count<<<L.NB, BLK, 0, s>>>(L);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ S2
+__constant__ float c_SH1 = 0.4886025119029199f;
+__constant__ float c_SH2[5] = {1.0925484305920792f, -1.0925484305920792f, 0.31539156525252005f,
+                               -1.0925484305920792f, 0.5462742152960396f};
+__constant__ float c_SH3[7] = {-0.5900435899266435f, 2.890611442640554f, -0.4570457994644658f,
+                               0.3731763325901154f, -0.4570457994644658f, 1.445305721320277f,
+                               -0.5900435899266435f};
+
+// Real SH basis (R17), degree D, direction (x,y,z) unit.
+template <int D>
+__device__ __forceinline__ void sh_eval_basis(float x, float y, float z, float* Y) {
+    Y[0] = 0.28209479177387814f;
+    if (D >= 1) {
+        Y[1] = -c_SH1 * y;
+        Y[2] = c_SH1 * z;
+        Y[3] = -c_SH1 * x;
+    }
+    if (D >= 2) {
+        const float xx = x * x, yy = y * y, zz = z * z;
+        Y[4] = c_SH2[0] * x * y;
+        Y[5] = c_SH2[1] * y * z;
+        Y[6] = c_SH2[2] * (2.f * zz - xx - yy);
+        Y[7] = c_SH2[3] * x * z;
+        Y[8] = c_SH2[4] * (xx - yy);
+        if (D >= 3) {
+            Y[9] = c_SH3[0] * y * (3.f * xx - yy);
+            Y[10] = c_SH3[1] * x * y * z;
+            Y[11] = c_SH3[2] * y * (4.f * zz - xx - yy);
+            Y[12] = c_SH3[3] * z * (2.f * zz - 3.f * xx - 3.f * yy);
+            Y[13] = c_SH3[4] * x * (4.f * zz - xx - yy);
+            Y[14] = c_SH3[5] * z * (xx - yy);
+            Y[15] = c_SH3[6] * x * (xx - 3.f * yy);
+        }
+    }
+}
+
+template <int D>
+__global__ __launch_bounds__(BLK) void k_project(Launch L) {
+    constexpr int NK = (D + 1) * (D + 1);
+    __shared__ int wc[BLK / 32][32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t g = (int64_t)blockIdx.x * BLK + threadIdx.x;
+    const bool valid = g < L.P;
+    float mx = 0.f, my = 0.f, mz = 0.f;
+    Activ a;
+    float sh[NK * 3];
+    if (valid) {
+        mx = L.means[3 * g];
+        my = L.means[3 * g + 1];
+        mz = L.means[3 * g + 2];
+        ca_activate(L.log_scales + 3 * g, L.quats + 4 * g, L.opac[g], a);
+        const float* s = L.sh + g * (int64_t)L.sh_stride * 3;
+#pragma unroll
+        for (int k = 0; k < NK * 3; k++) sh[k] = s[k];
+    }
+    const unsigned lt = (1u << lane) - 1u;
+    for (int v0 = 0; v0 < L.V; v0 += 32) {
+        const int nv = min(32, L.V - v0);
+        for (int k = 0; k < nv; k++) {
+            const mvgs_camera& c = L.cams[v0 + k];
+            const bool vis = valid && ca_depth(c, mx, my, mz) > c.znear;
+            const unsigned bal = __ballot_sync(FULL, vis);
+            if (lane == 0) wc[warp][k] = __popc(bal);
+        }
+        __syncthreads();
+        for (int k = 0; k < nv; k++) {
+            const int v = v0 + k;
+            const mvgs_camera& c = L.cams[v];
+            const bool vis = valid && ca_depth(c, mx, my, mz) > c.znear;
+            const unsigned bal = __ballot_sync(FULL, vis);
+            if (!vis) continue;
+            int pre = 0;
+            for (int w = 0; w < warp; w++) pre += wc[w][k];
+            const int64_t pair = (int64_t)L.blk_off[(int64_t)v * L.NB + blockIdx.x] + pre + __popc(bal & lt);
+            Proj p;
+            ca_project(c, mx, my, mz, a.Sig, L.TX, L.TY, p);
+            const int tiles = p.ok ? (p.rx1 - p.rx0) * (p.ry1 - p.ry0) : 0;
+            // colour (R17), free arithmetic
+            const float cpx = -(c.R[0] * c.t[0] + c.R[3] * c.t[1] + c.R[6] * c.t[2]);
+            const float cpy = -(c.R[1] * c.t[0] + c.R[4] * c.t[1] + c.R[7] * c.t[2]);
+            const float cpz = -(c.R[2] * c.t[0] + c.R[5] * c.t[1] + c.R[8] * c.t[2]);
+            float dx = mx - cpx, dy = my - cpy, dz = mz - cpz;
+            const float inv = rsqrtf(dx * dx + dy * dy + dz * dz);
+            dx *= inv; dy *= inv; dz *= inv;
+            float Y[NK];
+            sh_eval_basis<D>(dx, dy, dz, Y);
+            float rgb[3];
+            uint32_t flags = (p.clx ? 8u : 0u) | (p.cly ? 16u : 0u);
+#pragma unroll
+            for (int ch = 0; ch < 3; ch++) {
+                float acc = 0.5f;
+#pragma unroll
+                for (int kk = 0; kk < NK; kk++) acc += Y[kk] * sh[3 * kk + ch];
+                if (acc < 0.f) {
+                    flags |= 1u << ch;
+                    acc = 0.f;
+                }
+                rgb[ch] = acc;
+            }
+            if (pair < L.cap_pairs) {
+                const uint32_t lo = (uint32_t)p.rx0 | ((uint32_t)p.ry0 << 16);
+                const uint32_t hi = tiles > 0 ? ((uint32_t)p.rx1 | ((uint32_t)p.ry1 << 16)) : lo;
+                float4* r = L.rec + 3 * pair;
+                r[0] = make_float4(p.px, p.py, p.A, p.B);
+                r[1] = make_float4(p.C, a.o, rgb[0], rgb[1]);
+                r[2] = make_float4(rgb[2], p.tz, __uint_as_float(lo), __uint_as_float(hi));
+                L.meta[pair] = PairMeta{(uint32_t)g, ((uint32_t)v << 8) | flags};
+                float4* pg = reinterpret_cast<float4*>(L.pgrad + pair * PG_STRIDE);
+                pg[0] = pg[1] = pg[2] = make_float4(0.f, 0.f, 0.f, 0.f);
+            } else {
+                L.counters[C_OVERFLOW] = 1;
+            }
+            if (tiles > 0) {
+                atomicAdd(&L.counters[C_NVIS], 1);
+                int* cnt = L.bucket_off + (int64_t)v * L.T;  // histogram, scanned in place afterwards
+                for (int ty = p.ry0; ty < p.ry1; ty++)
+                    for (int tx = p.rx0; tx < p.rx1; tx++) atomicAdd(&cnt[ty * L.TX + tx], 1);
+            }
+        }
+        __syncthreads();
+    }
+}
+
+cudaError_t launch_project(const Launch& L, cudaStream_t s) {
+    switch (L.sh_degree) {
+        case 0: k_project<0><<<L.NB, BLK, 0, s>>>(L); break;
+        case 1: k_project<1><<<L.NB, BLK, 0, s>>>(L); break;
+        case 2: k_project<2><<<L.NB, BLK, 0, s>>>(L); break;
+        default: k_project<3><<<L.NB, BLK, 0, s>>>(L); break;
+    }
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ S3
+__global__ __launch_bounds__(256) void k_dup_scatter(Launch L) {
+    const int Q = min((int64_t)L.counters[C_Q], L.cap_pairs);
+    const int stride = gridDim.x * blockDim.x;
+    for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < Q; q += stride) {
+        const float4 r2 = L.rec[3 * (int64_t)q + 2];
+        const uint32_t lo = __float_as_uint(r2.z), hi = __float_as_uint(r2.w);
+        const int rx0 = lo & 0xffff, ry0 = lo >> 16, rx1 = hi & 0xffff, ry1 = hi >> 16;
+        if (rx1 <= rx0 || ry1 <= ry0) continue;
+        const int v = L.meta[q].vf >> 8;
+        const uint32_t dbits = __float_as_uint(r2.y);
+        for (int ty = ry0; ty < ry1; ty++)
+            for (int tx = rx0; tx < rx1; tx++) {
+                const int64_t b = (int64_t)v * L.T + ty * L.TX + tx;
+                const int pos = atomicAdd(&L.cursor[b], 1);
+                const int64_t e = (int64_t)L.bucket_off[b] + pos;
+                if (e < L.cap_entries) {
+                    L.key[e] = dbits;
+                    L.val[e] = (uint32_t)q;
+                } else {
+                    L.counters[C_OVERFLOW] = 1;
+                }
+            }
+    }
+}
+
+cudaError_t launch_dup_scatter(const Launch& L, cudaStream_t s) {
+    int dev = 0, nsm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    k_dup_scatter<<<nsm * 8, 256, 0, s>>>(L);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ export (tests)
+__global__ void k_export(Launch L, int64_t* range_start, int32_t* entry_gid, int32_t* pair_ids, int32_t* pair_i,
+                         float* pair_f, float* pair_g) {
+    const int Q = min((int64_t)L.counters[C_Q], L.cap_pairs);
+    const int64_t K = min((int64_t)L.counters[C_K], L.cap_entries);
+    const int64_t nb = (int64_t)L.V * L.T;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (range_start)
+        for (int64_t b = t0; b <= nb; b += stride) range_start[b] = L.bucket_off[b];
+    if (entry_gid)
+        for (int64_t e = t0; e < K; e += stride) entry_gid[e] = (int32_t)L.meta[L.val[e]].gid;
+    for (int64_t q = t0; q < Q; q += stride) {
+        const PairMeta m = L.meta[q];
+        const float4 r0 = L.rec[3 * q], r1 = L.rec[3 * q + 1], r2 = L.rec[3 * q + 2];
+        const uint32_t lo = __float_as_uint(r2.z), hi = __float_as_uint(r2.w);
+        if (pair_ids) {
+            pair_ids[2 * q] = (int32_t)(m.vf >> 8);
+            pair_ids[2 * q + 1] = (int32_t)m.gid;
+        }
+        if (pair_i) {
+            const int rx0 = lo & 0xffff, ry0 = lo >> 16, rx1 = hi & 0xffff, ry1 = hi >> 16;
+            int32_t* o = pair_i + 8 * q;
+            o[0] = 0;  // radius is not kept by the path; tests compare the rect
+            o[1] = rx0; o[2] = ry0; o[3] = rx1; o[4] = ry1;
+            o[5] = (rx1 - rx0) * (ry1 - ry0);
+            o[6] = (int32_t)(m.vf & 0xff);
+            o[7] = 0;
+        }
+        if (pair_f) {
+            float* f = pair_f + 12 * q;
+            f[0] = r2.y; f[1] = r0.x; f[2] = r0.y; f[3] = r0.z; f[4] = r0.w; f[5] = r1.x;
+            f[6] = r1.y; f[7] = r1.z; f[8] = r1.w; f[9] = r2.x; f[10] = 0.f; f[11] = 0.f;
+        }
+        if (pair_g)
+            for (int k = 0; k < NG; k++) pair_g[NG * q + k] = L.pgrad[q * PG_STRIDE + k];
+    }
+}
+
+cudaError_t launch_export(const Launch& L, int64_t* range_start, int32_t* entry_gid, int32_t* pair_ids,
+                          int32_t* pair_i, float* pair_f, float* pair_g, cudaStream_t s) {
+    k_export<<<1024, 256, 0, s>>>(L, range_start, entry_gid, pair_ids, pair_i, pair_f, pair_g);
+    return cudaGetLastError();
+}
+
+}  // namespace mvgs

@@ -1,0 +1,263 @@
+// k_render.cu — S6 forward compositing and S7 backward compositing + E1.
+//
+// Grid = one CTA per (view, tile) — "multiple blocks per tile, one block for
+// each viewpoint" — 256 threads, one pixel each (16×16 tile).  Entries
+// of the tile's depth-sorted list are staged into shared memory a batch of 256
+// at a time, each thread fetching one record, then every thread walks the
+// batch (Alg. 2).  A warp whose pixels have all terminated leaves
+// the batch loop at once (the loop condition is per-lane, so a fully-done warp
+// falls through); the CTA stops fetching when all 256 pixels are done.
+//
+// Backward (adjoint of Eq. (1)): back to front from each pixel's
+// n_contrib, reconstructing T by division.  Each entry's ten per-pixel terms
+// (Σ∇x, Σ∇y, ‖∇‖ for E1, ∂A, ∂B, ∂C, ∂o, ∂r, ∂g, ∂b) are reduced across the
+// warp with a transpose-reduce (12 shuffles for 10 values instead of 50; each
+// lane ends up owning one value's warp sum), added into a per-batch shared
+// accumulator, and the CTA's sums are flushed to the pair's gradient slot with
+// one global red.add per nonzero value after the batch.
+#include "ca.cuh"
+#include "internal.cuh"
+
+namespace mvgs {
+
+constexpr int RT = 256;
+constexpr unsigned FULLR = 0xffffffffu;
+
+// CTA-wide sum of a per-thread count → one 64-bit atomic per CTA.
+__device__ __forceinline__ void count_evals(unsigned long long* ctr, unsigned n, unsigned* sm) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) n += __shfl_xor_sync(FULLR, n, o);
+    if ((threadIdx.x & 31) == 0) atomicAdd(sm, n);
+    __syncthreads();
+    if (threadIdx.x == 0) atomicAdd(ctr, (unsigned long long)*sm);
+}
+
+__global__ __launch_bounds__(RT) void k_render_fwd(Launch L, float* __restrict__ out_rgb, float* __restrict__ out_T,
+                                                   int32_t* __restrict__ out_n) {
+    __shared__ float4 s0[RT], s1[RT];
+    __shared__ float s2[RT];
+    const int bucket = blockIdx.x;
+    const int v = bucket / L.T, tile = bucket - v * L.T;
+    const int ty = tile / L.TX, tx = tile - ty * L.TX;
+    const int x = tx * TILE + (threadIdx.x & 15), y = ty * TILE + (threadIdx.x >> 4);
+    const bool inside = x < L.W && y < L.H;
+    const int start = L.bucket_off[bucket], end = L.bucket_off[bucket + 1];
+    const float fx = (float)x, fy = (float)y;
+    float T = 1.0f, C0 = 0.f, C1 = 0.f, C2 = 0.f;
+    int last = 0;
+    unsigned nev = 0;
+    __shared__ unsigned sev;
+    if (threadIdx.x == 0) sev = 0;
+    __syncthreads();
+    bool done = !inside;
+    if (end <= L.cap_entries) {
+        for (int b0 = start; b0 < end; b0 += RT) {
+            if (__syncthreads_count(done) == RT) break;
+            const int idx = b0 + threadIdx.x;
+            if (idx < end) {
+                const uint32_t q = L.val[idx];
+                const float4* r = L.rec + 3 * (int64_t)q;
+                s0[threadIdx.x] = r[0];
+                s1[threadIdx.x] = r[1];
+                s2[threadIdx.x] = r[2].x;
+            }
+            __syncthreads();
+            const int cnt = min(RT, end - b0);
+            for (int j = 0; j < cnt && !done; j++) {
+                nev++;
+                const float4 a = s0[j];
+                const float dx = FSUB(a.x, fx), dy = FSUB(a.y, fy);
+                const float power = ca_power(a.z, a.w, s1[j].x, dx, dy);
+                if (power > 0.0f) continue;
+                const float4 c = s1[j];
+                const float G = ca_exp(power);
+                const float alpha = fminf(ALPHA_MAX, FMUL(c.y, G));
+                if (alpha < ALPHA_MIN) continue;
+                const float Tn = FMUL(T, FSUB(1.0f, alpha));
+                if (Tn < T_EPS) {
+                    done = true;
+                    break;
+                }
+                const float w = alpha * T;
+                C0 += c.z * w;
+                C1 += c.w * w;
+                C2 += s2[j] * w;
+                T = Tn;
+                last = b0 - start + j + 1;
+            }
+        }
+    }
+    count_evals(&L.counters64[0], nev, &sev);
+    if (inside) {
+        const int64_t HW = (int64_t)L.H * L.W, pix = (int64_t)y * L.W + x;
+        out_rgb[(3 * (int64_t)v + 0) * HW + pix] = C0 + T * L.bg[0];
+        out_rgb[(3 * (int64_t)v + 1) * HW + pix] = C1 + T * L.bg[1];
+        out_rgb[(3 * (int64_t)v + 2) * HW + pix] = C2 + T * L.bg[2];
+        out_T[v * HW + pix] = T;
+        out_n[v * HW + pix] = last;
+    }
+}
+
+cudaError_t launch_render_fwd(const Launch& L, float* rgb, float* Tf, int32_t* nc, cudaStream_t s) {
+    k_render_fwd<<<L.V * L.T, RT, 0, s>>>(L, rgb, Tf, nc);
+    return cudaGetLastError();
+}
+
+// Transpose-reduce of 10 per-lane values over a warp.  Level l (xor 16, 8, 4,
+// 2, 1) halves the number of values each lane carries; the lane keeps the
+// half selected by its bit and receives the partner's copy of that half.
+// Returns the warp sum of value `id` (id computed once by reduce_id).
+__device__ __forceinline__ float warp_transpose_reduce10(const float (&v)[NG], int lane) {
+    const bool b16 = lane & 16, b8 = lane & 8, b4 = lane & 4, b2 = lane & 2;
+    float u[5];
+#pragma unroll
+    for (int k = 0; k < 5; k++) {
+        const float keep = b16 ? v[k + 5] : v[k];
+        const float send = b16 ? v[k] : v[k + 5];
+        u[k] = keep + __shfl_xor_sync(FULLR, send, 16);
+    }
+    float w0 = (b8 ? u[2] : u[0]) + __shfl_xor_sync(FULLR, b8 ? u[0] : u[2], 8);
+    float w1 = (b8 ? u[3] : u[1]) + __shfl_xor_sync(FULLR, b8 ? u[1] : u[3], 8);
+    float w2 = u[4] + __shfl_xor_sync(FULLR, u[4], 8);
+    float x0 = (b4 ? w1 : w0) + __shfl_xor_sync(FULLR, b4 ? w0 : w1, 4);
+    float x1 = w2 + __shfl_xor_sync(FULLR, w2, 4);
+    float y = (b2 ? x1 : x0) + __shfl_xor_sync(FULLR, b2 ? x0 : x1, 2);
+    y += __shfl_xor_sync(FULLR, y, 1);
+    return y;
+}
+
+__device__ __forceinline__ int reduce_id(int lane) {
+    const int b16 = (lane & 16) ? 5 : 0;
+    const bool b8 = lane & 8, b4 = lane & 4, b2 = lane & 2;
+    const int w0 = b16 + (b8 ? 2 : 0), w1 = b16 + (b8 ? 3 : 1), w2 = b16 + 4;
+    const int x0 = b4 ? w1 : w0, x1 = w2;
+    return b2 ? x1 : x0;
+}
+
+__global__ __launch_bounds__(RT) void k_render_bwd(Launch L, const float* __restrict__ dL_drgb,
+                                                   const float* __restrict__ in_T, const int32_t* __restrict__ in_n) {
+    __shared__ float4 s0[RT], s1[RT];
+    __shared__ float s2[RT];
+    __shared__ uint32_t sq[RT];
+    __shared__ float sacc[RT * NG];
+    __shared__ int smax;
+    __shared__ unsigned sev;
+    const int lane = threadIdx.x & 31;
+    const int bucket = blockIdx.x;
+    const int v = bucket / L.T, tile = bucket - v * L.T;
+    const int ty = tile / L.TX, tx = tile - ty * L.TX;
+    const int x = tx * TILE + (threadIdx.x & 15), y = ty * TILE + (threadIdx.x >> 4);
+    const bool inside = x < L.W && y < L.H;
+    const int start = L.bucket_off[bucket], end = L.bucket_off[bucket + 1];
+    if (end > L.cap_entries) return;
+    const int64_t HW = (int64_t)L.H * L.W, pix = (int64_t)y * L.W + x;
+    float dL0 = 0.f, dL1 = 0.f, dL2 = 0.f, T_fin = 1.f;
+    int last = 0;
+    if (inside) {
+        dL0 = dL_drgb[(3 * (int64_t)v + 0) * HW + pix];
+        dL1 = dL_drgb[(3 * (int64_t)v + 1) * HW + pix];
+        dL2 = dL_drgb[(3 * (int64_t)v + 2) * HW + pix];
+        T_fin = in_T[v * HW + pix];
+        last = in_n[v * HW + pix];
+    }
+    if (threadIdx.x == 0) {
+        smax = 0;
+        sev = 0;
+    }
+    __syncthreads();
+    const unsigned nev = (unsigned)last;  // entries this pixel walks back over
+    if (last > 0) atomicMax(&smax, last);
+    __syncthreads();
+    const int maxlast = smax;
+    const int my_id = reduce_id(lane);
+    const bool owner = (__ffs(__match_any_sync(FULLR, my_id)) - 1) == lane;
+    const float fx = (float)x, fy = (float)y;
+    const float hw = 0.5f * (float)L.W, hh = 0.5f * (float)L.H;
+    const float dL_bg = L.bg[0] * dL0 + L.bg[1] * dL1 + L.bg[2] * dL2;
+    float T = T_fin;
+    float acc0 = 0.f, acc1 = 0.f, acc2 = 0.f;   // colour behind the current entry
+    float a_prev = 0.f, c0p = 0.f, c1p = 0.f, c2p = 0.f;
+    for (int b_end = maxlast; b_end > 0; b_end -= RT) {
+        const int b0 = max(0, b_end - RT);
+        const int cnt = b_end - b0;
+        __syncthreads();
+        if (threadIdx.x < cnt) {
+            const uint32_t q = L.val[start + b0 + threadIdx.x];
+            const float4* r = L.rec + 3 * (int64_t)q;
+            sq[threadIdx.x] = q;
+            s0[threadIdx.x] = r[0];
+            s1[threadIdx.x] = r[1];
+            s2[threadIdx.x] = r[2].x;
+        }
+        for (int i = threadIdx.x; i < RT * NG; i += RT) sacc[i] = 0.f;
+        __syncthreads();
+        for (int jj = cnt - 1; jj >= 0; jj--) {
+            const int j = b0 + jj;
+            float val[NG];
+#pragma unroll
+            for (int k = 0; k < NG; k++) val[k] = 0.f;
+            bool contrib = false;
+            if (j < last) {
+                const float4 a = s0[jj];
+                const float4 c = s1[jj];
+                const float dx = FSUB(a.x, fx), dy = FSUB(a.y, fy);
+                const float power = ca_power(a.z, a.w, c.x, dx, dy);
+                if (power <= 0.0f) {
+                    const float G = ca_exp(power);
+                    const float oG = FMUL(c.y, G);
+                    const float alpha = fminf(ALPHA_MAX, oG);
+                    if (alpha >= ALPHA_MIN) {
+                        contrib = true;
+                        const float one_m = 1.0f - alpha;
+                        T = T / one_m;
+                        const float w = alpha * T;
+                        const float cb = s2[jj];
+                        acc0 = a_prev * c0p + (1.f - a_prev) * acc0;
+                        acc1 = a_prev * c1p + (1.f - a_prev) * acc1;
+                        acc2 = a_prev * c2p + (1.f - a_prev) * acc2;
+                        float dLda = (c.z - acc0) * dL0 + (c.w - acc1) * dL1 + (cb - acc2) * dL2;
+                        dLda = dLda * T - T_fin / one_m * dL_bg;
+                        a_prev = alpha;
+                        c0p = c.z; c1p = c.w; c2p = cb;
+                        const bool clamped = oG > ALPHA_MAX;
+                        const float dLdG = clamped ? 0.f : c.y * dLda;
+                        const float dLdo = clamped ? 0.f : G * dLda;
+                        const float dLdpw = G * dLdG;
+                        const float gx = dLdpw * -(a.z * dx + a.w * dy) * hw;
+                        const float gy = dLdpw * -(c.x * dy + a.w * dx) * hh;
+                        val[0] = gx;
+                        val[1] = gy;
+                        val[2] = sqrtf(gx * gx + gy * gy);
+                        val[3] = -0.5f * dLdpw * dx * dx;
+                        val[4] = -dLdpw * dx * dy;
+                        val[5] = -0.5f * dLdpw * dy * dy;
+                        val[6] = dLdo;
+                        val[7] = w * dL0;
+                        val[8] = w * dL1;
+                        val[9] = w * dL2;
+                    }
+                }
+            }
+            if (__any_sync(FULLR, contrib)) {
+                const float s = warp_transpose_reduce10(val, lane);
+                if (owner && s != 0.f) atomicAdd(&sacc[jj * NG + my_id], s);
+            }
+        }
+        __syncthreads();
+        for (int i = threadIdx.x; i < cnt * NG; i += RT) {
+            const float s = sacc[i];
+            if (s != 0.f) {
+                const int jj = i / NG, k = i - jj * NG;
+                atomicAdd(&L.pgrad[(int64_t)sq[jj] * PG_STRIDE + k], s);
+            }
+        }
+    }
+    count_evals(&L.counters64[1], nev, &sev);
+}
+
+cudaError_t launch_render_bwd(const Launch& L, const float* dL, const float* Tf, const int32_t* nc, cudaStream_t s) {
+    k_render_bwd<<<L.V * L.T, RT, 0, s>>>(L, dL, Tf, nc);
+    return cudaGetLastError();
+}
+
+}  // namespace mvgs

@@ -1,0 +1,381 @@
+// mvgs_abi.cu — the C ABI of libmvgs.so (include/mvgs.h): context, workspace,
+// argument validation, and the launch sequence of each call.  No arithmetic of
+// the method lives here; every step runs in the kernels of k_*.cu.
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include "ca.cuh"
+#include "internal.cuh"
+
+using namespace mvgs;
+
+namespace {
+
+mvgs_status fail(mvgs_ctx* c, mvgs_status st, const char* msg) {
+    if (c) c->err = msg;
+    return st;
+}
+
+mvgs_status cuda_fail(mvgs_ctx* c, cudaError_t e, const char* where) {
+    if (c) {
+        c->err = std::string(where) + ": " + cudaGetErrorString(e);
+    }
+    return MVGS_ERR_CUDA;
+}
+
+#define CK(expr)                                              \
+    do {                                                      \
+        cudaError_t _e = (expr);                              \
+        if (_e != cudaSuccess) return cuda_fail(ctx, _e, #expr); \
+    } while (0)
+
+template <class T>
+cudaError_t grow(T*& p, int64_t& cap, int64_t need, int64_t elem_per = 1) {
+    if (need <= cap && p) return cudaSuccess;
+    int64_t n = need + need / 4 + 64;
+    if (p) {
+        cudaError_t e = cudaFree(p);
+        if (e != cudaSuccess) return e;
+        p = nullptr;
+    }
+    cudaError_t e = cudaMalloc(&p, sizeof(T) * n * elem_per);
+    if (e != cudaSuccess) {
+        cap = 0;
+        return e;
+    }
+    cap = n;
+    return cudaSuccess;
+}
+
+cudaError_t alloc_pairs(mvgs_ctx* c, int64_t n) {
+    cudaFree(c->d_rec);
+    cudaFree(c->d_meta);
+    cudaFree(c->d_pgrad);
+    c->d_rec = nullptr; c->d_meta = nullptr; c->d_pgrad = nullptr;
+    c->cap_pairs = 0;
+    cudaError_t e;
+    if ((e = cudaMalloc(&c->d_rec, sizeof(float4) * REC_F4 * n)) != cudaSuccess) return e;
+    if ((e = cudaMalloc(&c->d_meta, sizeof(PairMeta) * n)) != cudaSuccess) return e;
+    if ((e = cudaMalloc(&c->d_pgrad, sizeof(float) * PG_STRIDE * n)) != cudaSuccess) return e;
+    c->cap_pairs = n;
+    return cudaSuccess;
+}
+
+cudaError_t alloc_entries(mvgs_ctx* c, int64_t n) {
+    cudaFree(c->d_key); cudaFree(c->d_val); cudaFree(c->d_key2); cudaFree(c->d_val2);
+    c->d_key = c->d_val = c->d_key2 = c->d_val2 = nullptr;
+    c->cap_entries = 0;
+    cudaError_t e;
+    if ((e = cudaMalloc(&c->d_key, 4 * n)) != cudaSuccess) return e;
+    if ((e = cudaMalloc(&c->d_val, 4 * n)) != cudaSuccess) return e;
+    if ((e = cudaMalloc(&c->d_key2, 4 * n)) != cudaSuccess) return e;
+    if ((e = cudaMalloc(&c->d_val2, 4 * n)) != cudaSuccess) return e;
+    c->cap_entries = n;
+    return cudaSuccess;
+}
+
+enum { ST_COUNT, ST_SCAN_PAIRS, ST_PROJECT, ST_SCAN_BUCKETS, ST_DUP, ST_SORT, ST_FWD, ST_BWD, ST_GAUSS };
+
+cudaEvent_t pool_get(mvgs_ctx* c) {
+    if (!c->ev_pool.empty()) {
+        cudaEvent_t e = c->ev_pool.back();
+        c->ev_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+}
+
+struct StageTimer {  // records a pair of events around one stage when timing is enabled
+    mvgs_ctx* c;
+    int st;
+    cudaStream_t s;
+    cudaEvent_t a = nullptr;
+    StageTimer(mvgs_ctx* c_, int st_, cudaStream_t s_) : c(c_), st(st_), s(s_) {
+        if (c->timing) {
+            a = pool_get(c);
+            cudaEventRecord(a, s);
+        }
+    }
+    ~StageTimer() {
+        if (a) {
+            cudaEvent_t b = pool_get(c);
+            cudaEventRecord(b, s);
+            c->ev_rec[st].emplace_back(a, b);
+        }
+    }
+};
+#define STAGE(id) StageTimer _timer_##id(ctx, id, s)
+
+void fill_launch(mvgs_ctx* c) {
+    Launch& L = c->L;
+    L.cams = c->d_cams;
+    L.cap_pairs = c->cap_pairs;
+    L.cap_entries = c->cap_entries;
+    L.blk_off = c->d_blk;
+    L.bucket_off = c->d_bucket;
+    L.cursor = c->d_cursor;
+    L.rec = c->d_rec;
+    L.meta = c->d_meta;
+    L.pgrad = c->d_pgrad;
+    L.key = c->d_key;
+    L.val = c->d_val;
+    L.key2 = c->d_key2;
+    L.val2 = c->d_val2;
+    L.counters = c->d_counters;
+    L.counters64 = c->d_counters64;
+}
+
+}  // namespace
+
+extern "C" {
+
+mvgs_status mvgs_create(mvgs_ctx** out, int device, int64_t max_pairs, int64_t max_entries) {
+    if (!out) return MVGS_ERR_INVALID;
+    *out = nullptr;
+    mvgs_ctx* ctx = new (std::nothrow) mvgs_ctx();
+    if (!ctx) return MVGS_ERR_INVALID;
+    ctx->device = device;
+    cudaError_t e = cudaSetDevice(device);
+    if (e != cudaSuccess) {
+        delete ctx;
+        return MVGS_ERR_CUDA;
+    }
+    if (max_pairs <= 0) max_pairs = 1 << 16;
+    if (max_entries <= 0) max_entries = 1 << 18;
+    if (max_pairs > INT32_MAX || max_entries > INT32_MAX) {
+        delete ctx;
+        return MVGS_ERR_INVALID;
+    }
+    if ((e = alloc_pairs(ctx, max_pairs)) != cudaSuccess || (e = alloc_entries(ctx, max_entries)) != cudaSuccess ||
+        (e = cudaMalloc(&ctx->d_counters, sizeof(int) * C_NCOUNTERS)) != cudaSuccess ||
+        (e = cudaMemset(ctx->d_counters, 0, sizeof(int) * C_NCOUNTERS)) != cudaSuccess ||
+        (e = cudaMalloc(&ctx->d_counters64, sizeof(unsigned long long) * 2)) != cudaSuccess ||
+        (e = cudaMemset(ctx->d_counters64, 0, sizeof(unsigned long long) * 2)) != cudaSuccess ||
+        (e = cudaEventCreateWithFlags(&ctx->cams_ev, cudaEventDisableTiming)) != cudaSuccess) {
+        mvgs_destroy(ctx);
+        return MVGS_ERR_CUDA;
+    }
+    *out = ctx;
+    return MVGS_OK;
+}
+
+void mvgs_destroy(mvgs_ctx* ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    cudaDeviceSynchronize();
+    cudaFree(ctx->d_cams); cudaFree(ctx->d_blk); cudaFree(ctx->d_bucket); cudaFree(ctx->d_cursor);
+    cudaFree(ctx->d_rec); cudaFree(ctx->d_meta); cudaFree(ctx->d_pgrad);
+    cudaFree(ctx->d_key); cudaFree(ctx->d_val); cudaFree(ctx->d_key2); cudaFree(ctx->d_val2);
+    cudaFree(ctx->d_counters); cudaFree(ctx->d_counters64); cudaFree(ctx->d_scan);
+    if (ctx->h_cams) cudaFreeHost(ctx->h_cams);
+    if (ctx->cams_ev) cudaEventDestroy(ctx->cams_ev);
+    for (int i = 0; i < MVGS_NUM_STAGES; i++)
+        for (auto& p : ctx->ev_rec[i]) {
+            cudaEventDestroy(p.first);
+            cudaEventDestroy(p.second);
+        }
+    for (auto e : ctx->ev_pool) cudaEventDestroy(e);
+    delete ctx;
+}
+
+const char* mvgs_last_error(const mvgs_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+mvgs_status mvgs_reserve(mvgs_ctx* ctx, int64_t max_pairs, int64_t max_entries) {
+    if (!ctx) return MVGS_ERR_INVALID;
+    if (max_pairs > INT32_MAX || max_entries > INT32_MAX) return fail(ctx, MVGS_ERR_INVALID, "capacity above 2^31-1");
+    CK(cudaSetDevice(ctx->device));
+    CK(cudaDeviceSynchronize());
+    if (max_pairs > ctx->cap_pairs) CK(alloc_pairs(ctx, max_pairs));
+    if (max_entries > ctx->cap_entries) CK(alloc_entries(ctx, max_entries));
+    ctx->state = 0;
+    return MVGS_OK;
+}
+
+mvgs_status mvgs_preprocess(mvgs_ctx* ctx, const mvgs_gaussians* g, const mvgs_camera* cams, int32_t V,
+                            const float* bg, void* stream) {
+    if (!ctx) return MVGS_ERR_INVALID;
+    if (!g || !cams) return fail(ctx, MVGS_ERR_INVALID, "null gaussians or cameras");
+    if (V < 1 || V > 65535) return fail(ctx, MVGS_ERR_INVALID, "V out of [1, 65535] (R9)");
+    if (g->P < 0 || g->P > INT32_MAX) return fail(ctx, MVGS_ERR_INVALID, "P out of range");
+    if (g->sh_degree < 0 || g->sh_degree > 3) return fail(ctx, MVGS_ERR_INVALID, "sh_degree must be 0..3");
+    if (g->sh_stride < (g->sh_degree + 1) * (g->sh_degree + 1)) return fail(ctx, MVGS_ERR_INVALID, "sh_stride too small");
+    if (g->P > 0 && (!g->means || !g->log_scales || !g->quats || !g->opacity_logits || !g->sh))
+        return fail(ctx, MVGS_ERR_INVALID, "null parameter pointer");
+    const int W = cams[0].width, H = cams[0].height;
+    if (W <= 0 || H <= 0) return fail(ctx, MVGS_ERR_INVALID, "non-positive image size");
+    for (int v = 1; v < V; v++)
+        if (cams[v].width != W || cams[v].height != H) return fail(ctx, MVGS_ERR_INVALID, "views differ in size (R25)");
+    const int TX = (W + TILE - 1) / TILE, TY = (H + TILE - 1) / TILE;
+    if ((int64_t)TX * TY > 65535) return fail(ctx, MVGS_ERR_INVALID, "more than 65535 tiles per view (R9)");
+    const int NB = (int)((g->P + BLK - 1) / BLK);
+    const int64_t nblk = (int64_t)V * (NB > 0 ? NB : 1);
+    const int64_t nbuck = (int64_t)V * TX * TY;
+    if (nblk + 1 > INT32_MAX || nbuck + 1 > INT32_MAX) return fail(ctx, MVGS_ERR_INVALID, "batch too large");
+    cudaStream_t s = (cudaStream_t)stream;
+    CK(cudaSetDevice(ctx->device));
+    // workspace growth (synchronous only when it grows)
+    int64_t need_scan = scan_tmp_size((int)std::max(nblk, nbuck));
+    if (nblk + 1 > ctx->cap_blk || nbuck + 1 > ctx->cap_buckets || V > ctx->cap_cams || need_scan > ctx->cap_scan) {
+        CK(cudaDeviceSynchronize());
+        CK(grow(ctx->d_blk, ctx->cap_blk, nblk + 1));
+        int64_t capb = ctx->cap_buckets;
+        CK(grow(ctx->d_bucket, ctx->cap_buckets, nbuck + 1));
+        CK(grow(ctx->d_cursor, capb, nbuck + 1));
+        CK(grow(ctx->d_scan, ctx->cap_scan, need_scan));
+        if (V > ctx->cap_cams) {
+            cudaFree(ctx->d_cams);
+            if (ctx->h_cams) cudaFreeHost(ctx->h_cams);
+            ctx->d_cams = nullptr;
+            ctx->h_cams = nullptr;
+            int64_t n = V + 8;
+            CK(cudaMalloc(&ctx->d_cams, sizeof(mvgs_camera) * n));
+            CK(cudaMallocHost(&ctx->h_cams, sizeof(mvgs_camera) * n));
+            ctx->cap_cams = n;
+        }
+    }
+    // cameras: host → pinned staging (after the previous copy drained) → device
+    CK(cudaEventSynchronize(ctx->cams_ev));
+    memcpy(ctx->h_cams, cams, sizeof(mvgs_camera) * V);
+    CK(cudaMemcpyAsync(ctx->d_cams, ctx->h_cams, sizeof(mvgs_camera) * V, cudaMemcpyHostToDevice, s));
+    CK(cudaEventRecord(ctx->cams_ev, s));
+
+    ctx->g = *g;
+    Launch& L = ctx->L;
+    L.P = g->P;
+    L.V = V; L.W = W; L.H = H; L.TX = TX; L.TY = TY; L.T = TX * TY; L.NB = NB;
+    L.sh_degree = g->sh_degree;
+    L.sh_stride = g->sh_stride;
+    for (int k = 0; k < 3; k++) L.bg[k] = bg ? bg[k] : 0.f;
+    L.means = g->means; L.log_scales = g->log_scales; L.quats = g->quats; L.opac = g->opacity_logits; L.sh = g->sh;
+    fill_launch(ctx);
+    ctx->last_stream = s;
+
+    CK(cudaMemsetAsync(ctx->d_counters, 0, sizeof(int) * C_NCOUNTERS, s));
+    CK(cudaMemsetAsync(ctx->d_bucket, 0, sizeof(int) * (nbuck + 1), s));
+    if (NB > 0) {
+        { STAGE(ST_COUNT); CK(launch_count(L, s)); }                                                 // S1
+        { STAGE(ST_SCAN_PAIRS); CK(scan_exclusive(ctx->d_blk, (int)nblk, ctx->d_counters + C_Q, ctx->d_scan, s)); }
+        { STAGE(ST_PROJECT); CK(launch_project(L, s)); }                                             // S2 (+ S3 histogram)
+    } else {
+        CK(cudaMemsetAsync(ctx->d_blk, 0, sizeof(int) * (nblk + 1), s));
+    }
+    { STAGE(ST_SCAN_BUCKETS); CK(scan_exclusive(ctx->d_bucket, (int)nbuck, ctx->d_counters + C_K, ctx->d_scan, s)); }
+    CK(cudaMemsetAsync(ctx->d_cursor, 0, sizeof(int) * nbuck, s));
+    { STAGE(ST_DUP); CK(launch_dup_scatter(L, s)); }                                                 // S3
+    { STAGE(ST_SORT); CK(launch_bucket_sort(L, s)); }                                                // S4
+    ctx->state = 1;
+    return MVGS_OK;
+}
+
+mvgs_status mvgs_render_fwd(mvgs_ctx* ctx, float* rgb, float* T_final, int32_t* n_contrib, void* stream) {
+    if (!ctx) return MVGS_ERR_INVALID;
+    if (ctx->state < 1) return fail(ctx, MVGS_ERR_STATE, "render_fwd before preprocess");
+    if (!rgb || !T_final || !n_contrib) return fail(ctx, MVGS_ERR_INVALID, "null output");
+    CK(cudaSetDevice(ctx->device));
+    ctx->last_stream = (cudaStream_t)stream;
+    cudaStream_t s = (cudaStream_t)stream;
+    CK(cudaMemsetAsync(ctx->d_counters64, 0, sizeof(unsigned long long), s));
+    { STAGE(ST_FWD); CK(launch_render_fwd(ctx->L, rgb, T_final, n_contrib, s)); }  // S6
+    ctx->state = 2;
+    return MVGS_OK;
+}
+
+mvgs_status mvgs_render_bwd(mvgs_ctx* ctx, const float* dL_drgb, const float* T_final, const int32_t* n_contrib,
+                            void* stream) {
+    if (!ctx) return MVGS_ERR_INVALID;
+    if (ctx->state != 2) return fail(ctx, MVGS_ERR_STATE, "render_bwd needs a render_fwd of a fresh preprocess");
+    if (!dL_drgb || !T_final || !n_contrib) return fail(ctx, MVGS_ERR_INVALID, "null input");
+    CK(cudaSetDevice(ctx->device));
+    ctx->last_stream = (cudaStream_t)stream;
+    cudaStream_t s = (cudaStream_t)stream;
+    CK(cudaMemsetAsync(ctx->d_counters64 + 1, 0, sizeof(unsigned long long), s));
+    { STAGE(ST_BWD); CK(launch_render_bwd(ctx->L, dL_drgb, T_final, n_contrib, s)); }  // S7
+    ctx->state = 3;
+    return MVGS_OK;
+}
+
+mvgs_status mvgs_adc_stats(mvgs_ctx* ctx, const mvgs_grads* grads, const mvgs_adc* adc, void* stream) {
+    if (!ctx) return MVGS_ERR_INVALID;
+    if (ctx->state != 3) return fail(ctx, MVGS_ERR_STATE, "adc_stats needs a preceding render_bwd");
+    if (!grads || !adc) return fail(ctx, MVGS_ERR_INVALID, "null grads/adc");
+    if (ctx->L.P > 0 && (!grads->d_means || !grads->d_log_scales || !grads->d_quats || !grads->d_opacity_logits ||
+                         !grads->d_sh || !adc->e1 || !adc->e2 || !adc->vis))
+        return fail(ctx, MVGS_ERR_INVALID, "null output pointer");
+    CK(cudaSetDevice(ctx->device));
+    ctx->last_stream = (cudaStream_t)stream;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (ctx->L.NB > 0) { STAGE(ST_GAUSS); CK(launch_gauss_bwd(ctx->L, *grads, *adc, s)); }  // S8 + S9
+    return MVGS_OK;
+}
+
+mvgs_status mvgs_query(mvgs_ctx* ctx, mvgs_stats* out) {
+    if (!ctx || !out) return MVGS_ERR_INVALID;
+    CK(cudaSetDevice(ctx->device));
+    CK(cudaDeviceSynchronize());
+    int h[C_NCOUNTERS];
+    unsigned long long h64[2];
+    CK(cudaMemcpy(h, ctx->d_counters, sizeof(h), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(h64, ctx->d_counters64, sizeof(h64), cudaMemcpyDeviceToHost));
+    memset(out, 0, sizeof(*out));
+    out->Q = h[C_Q];
+    out->K = h[C_K];
+    out->cap_pairs = ctx->cap_pairs;
+    out->cap_entries = ctx->cap_entries;
+    out->max_bucket = h[C_MAXB];
+    out->n_visible = h[C_NVIS];
+    out->V = ctx->L.V;
+    out->tiles_x = ctx->L.TX;
+    out->tiles_y = ctx->L.TY;
+    out->eval_fwd = (int64_t)h64[0];
+    out->eval_bwd = (int64_t)h64[1];
+    out->overflow = h[C_OVERFLOW] || out->Q > ctx->cap_pairs || out->K > ctx->cap_entries;
+    if (out->overflow) return fail(ctx, MVGS_ERR_CAPACITY, "capacity exceeded: reserve stats.Q / stats.K and re-run");
+    return MVGS_OK;
+}
+
+mvgs_status mvgs_export_lists(mvgs_ctx* ctx, int64_t* range_start, int32_t* entry_gid, void* stream) {
+    if (!ctx) return MVGS_ERR_INVALID;
+    if (ctx->state < 1) return fail(ctx, MVGS_ERR_STATE, "export before preprocess");
+    CK(launch_export(ctx->L, range_start, entry_gid, nullptr, nullptr, nullptr, nullptr, (cudaStream_t)stream));
+    return MVGS_OK;
+}
+
+mvgs_status mvgs_export_pairs(mvgs_ctx* ctx, int32_t* pair_ids, int32_t* pair_i, float* pair_f, float* pair_g,
+                              void* stream) {
+    if (!ctx) return MVGS_ERR_INVALID;
+    if (ctx->state < 1) return fail(ctx, MVGS_ERR_STATE, "export before preprocess");
+    CK(launch_export(ctx->L, nullptr, nullptr, pair_ids, pair_i, pair_f, pair_g, (cudaStream_t)stream));
+    return MVGS_OK;
+}
+
+mvgs_status mvgs_set_timing(mvgs_ctx* ctx, int enable) {
+    if (!ctx) return MVGS_ERR_INVALID;
+    ctx->timing = enable != 0;
+    return MVGS_OK;
+}
+
+int mvgs_stage_times(mvgs_ctx* ctx, float* ms, int n) {
+    if (!ctx || !ms) return 0;
+    int k = 0;
+    for (; k < n && k < MVGS_NUM_STAGES; k++) {
+        double sum = 0.0;
+        int cnt = 0;
+        for (auto& p : ctx->ev_rec[k]) {
+            float t = 0.f;
+            if (cudaEventSynchronize(p.second) == cudaSuccess && cudaEventElapsedTime(&t, p.first, p.second) == cudaSuccess) {
+                sum += t;
+                cnt++;
+            }
+            ctx->ev_pool.push_back(p.first);
+            ctx->ev_pool.push_back(p.second);
+        }
+        ctx->ev_rec[k].clear();
+        ms[k] = cnt ? (float)(sum / cnt) : 0.f;
+    }
+    return k;
+}
+
+}  // extern "C"

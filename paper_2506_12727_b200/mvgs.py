@@ -1,0 +1,245 @@
+"""Thin ctypes binding of libmvgs.so (include/mvgs.h).  Argument marshalling
+only: every step of the path runs in the library's sm_100a kernels.  PyTorch
+provides device memory and the stream handle.  There is no fallback — if the
+library is missing or fails to load, importing this module raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+import torch
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libmvgs.so")
+
+MVGS_OK, MVGS_ERR_INVALID, MVGS_ERR_CAPACITY, MVGS_ERR_STATE, MVGS_ERR_CUDA = 0, -1, -2, -3, -4
+NG = 10
+
+# the exported symbols include/mvgs.h declares (checked by tests/test_abi.py)
+SYMBOLS = ["mvgs_create", "mvgs_destroy", "mvgs_last_error", "mvgs_reserve", "mvgs_preprocess", "mvgs_render_fwd",
+           "mvgs_render_bwd", "mvgs_adc_stats", "mvgs_query", "mvgs_export_lists", "mvgs_export_pairs",
+           "mvgs_set_timing", "mvgs_stage_times"]
+STAGE_NAMES = ["count", "scan_pairs", "project", "scan_buckets", "dup_scatter", "sort", "render_fwd", "render_bwd",
+               "gauss_bwd"]
+
+
+class MvgsError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"mvgs status {status}: {msg}")
+        self.status = status
+
+
+class Gaussians(C.Structure):
+    _fields_ = [("P", C.c_int64), ("sh_degree", C.c_int32), ("sh_stride", C.c_int32), ("means", C.c_void_p),
+                ("log_scales", C.c_void_p), ("quats", C.c_void_p), ("opacity_logits", C.c_void_p),
+                ("sh", C.c_void_p)]
+
+
+class Grads(C.Structure):
+    _fields_ = [(k, C.c_void_p) for k in ("d_means", "d_log_scales", "d_quats", "d_opacity_logits", "d_sh")]
+
+
+class Adc(C.Structure):
+    _fields_ = [(k, C.c_void_p) for k in ("e1", "e2", "e_old", "vis", "e1_acc", "e2_acc", "denom_acc")]
+
+
+class Stats(C.Structure):
+    _fields_ = [("Q", C.c_int64), ("K", C.c_int64), ("cap_pairs", C.c_int64), ("cap_entries", C.c_int64),
+                ("max_bucket", C.c_int64), ("n_visible", C.c_int64), ("overflow", C.c_int32), ("V", C.c_int32),
+                ("tiles_x", C.c_int32), ("tiles_y", C.c_int32), ("eval_fwd", C.c_int64), ("eval_bwd", C.c_int64)]
+
+
+CAM_BYTES = 76
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; g.build()'`")
+    L = C.CDLL(LIB_PATH)
+    vp, st, i64 = C.c_void_p, C.c_int, C.c_int64
+    L.mvgs_create.argtypes = [C.POINTER(vp), C.c_int, i64, i64]
+    L.mvgs_destroy.argtypes = [vp]
+    L.mvgs_destroy.restype = None
+    L.mvgs_last_error.argtypes = [vp]
+    L.mvgs_last_error.restype = C.c_char_p
+    L.mvgs_reserve.argtypes = [vp, i64, i64]
+    L.mvgs_preprocess.argtypes = [vp, C.POINTER(Gaussians), vp, C.c_int32, vp, vp]
+    L.mvgs_render_fwd.argtypes = [vp, vp, vp, vp, vp]
+    L.mvgs_render_bwd.argtypes = [vp, vp, vp, vp, vp]
+    L.mvgs_adc_stats.argtypes = [vp, C.POINTER(Grads), C.POINTER(Adc), vp]
+    L.mvgs_query.argtypes = [vp, C.POINTER(Stats)]
+    L.mvgs_export_lists.argtypes = [vp, vp, vp, vp]
+    L.mvgs_export_pairs.argtypes = [vp, vp, vp, vp, vp, vp]
+    L.mvgs_set_timing.argtypes = [vp, C.c_int]
+    L.mvgs_stage_times.argtypes = [vp, C.POINTER(C.c_float), C.c_int]
+    L.mvgs_stage_times.restype = C.c_int
+    for n in SYMBOLS:
+        if n not in ("mvgs_destroy", "mvgs_last_error", "mvgs_stage_times"):
+            getattr(L, n).restype = st
+    return L
+
+
+_lib = _load()
+
+
+def lib():
+    return _lib
+
+
+def _ptr(t):
+    if t is None:
+        return None
+    if isinstance(t, torch.Tensor):
+        if not t.is_cuda or not t.is_contiguous():
+            raise ValueError("mvgs: tensors must be contiguous CUDA tensors")
+        return t.data_ptr()
+    return t
+
+
+def _stream(stream):
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return C.c_void_p(stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream))
+
+
+def _check(ctx, status):
+    if status != MVGS_OK:
+        msg = _lib.mvgs_last_error(ctx).decode() if ctx else ""
+        raise MvgsError(status, msg)
+
+
+def create(device: int = 0, max_pairs: int = 0, max_entries: int = 0):
+    h = C.c_void_p()
+    _check(None, _lib.mvgs_create(C.byref(h), device, max_pairs, max_entries))
+    return h
+
+
+def destroy(ctx):
+    if ctx:
+        _lib.mvgs_destroy(ctx)
+
+
+def reserve(ctx, max_pairs: int, max_entries: int):
+    _check(ctx, _lib.mvgs_reserve(ctx, int(max_pairs), int(max_entries)))
+
+
+def gaussians_struct(g: dict) -> Gaussians:
+    sh = g["sh"]
+    return Gaussians(int(g["means"].shape[0]), int(g["sh_degree"]), int(sh.shape[1]), _ptr(g["means"]),
+                     _ptr(g["log_scales"]), _ptr(g["quats"]), _ptr(g["opacity_logits"]), _ptr(sh))
+
+
+def preprocess(ctx, g: dict, cams: np.ndarray, bg=(0.0, 0.0, 0.0), stream=None):
+    """S1–S5.  `g`: dict of contiguous fp32 CUDA tensors (+ int sh_degree);
+    `cams`: numpy structured array with the 76-byte mvgs_camera layout."""
+    cams = np.ascontiguousarray(cams)
+    assert cams.dtype.itemsize == CAM_BYTES
+    bgh = np.ascontiguousarray(bg, np.float32)
+    gs = gaussians_struct(g)
+    _check(ctx, _lib.mvgs_preprocess(ctx, C.byref(gs), cams.ctypes.data, len(cams), bgh.ctypes.data, _stream(stream)))
+
+
+def render_fwd(ctx, rgb, T_final, n_contrib, stream=None):
+    _check(ctx, _lib.mvgs_render_fwd(ctx, _ptr(rgb), _ptr(T_final), _ptr(n_contrib), _stream(stream)))
+
+
+def render_bwd(ctx, dL_drgb, T_final, n_contrib, stream=None):
+    _check(ctx, _lib.mvgs_render_bwd(ctx, _ptr(dL_drgb), _ptr(T_final), _ptr(n_contrib), _stream(stream)))
+
+
+def adc_stats(ctx, grads: dict, adc: dict, stream=None):
+    gr = Grads(*[_ptr(grads[k]) for k in ("d_means", "d_log_scales", "d_quats", "d_opacity_logits", "d_sh")])
+    ad = Adc(*[_ptr(adc.get(k)) for k in ("e1", "e2", "e_old", "vis", "e1_acc", "e2_acc", "denom_acc")])
+    _check(ctx, _lib.mvgs_adc_stats(ctx, C.byref(gr), C.byref(ad), _stream(stream)))
+
+
+def query(ctx, raise_on_capacity: bool = True) -> dict:
+    s = Stats()
+    st = _lib.mvgs_query(ctx, C.byref(s))
+    if st != MVGS_OK and not (st == MVGS_ERR_CAPACITY and not raise_on_capacity):
+        _check(ctx, st)
+    return {k: getattr(s, k) for k, _ in Stats._fields_}
+
+
+def export_lists(ctx, range_start, entry_gid, stream=None):
+    _check(ctx, _lib.mvgs_export_lists(ctx, _ptr(range_start), _ptr(entry_gid), _stream(stream)))
+
+
+def export_pairs(ctx, pair_ids=None, pair_i=None, pair_f=None, pair_g=None, stream=None):
+    _check(ctx, _lib.mvgs_export_pairs(ctx, _ptr(pair_ids), _ptr(pair_i), _ptr(pair_f), _ptr(pair_g),
+                                       _stream(stream)))
+
+
+def set_timing(ctx, enable: bool):
+    _check(ctx, _lib.mvgs_set_timing(ctx, int(bool(enable))))
+
+
+def stage_times(ctx) -> dict:
+    """Milliseconds of the most recent run of each stage (synchronises)."""
+    buf = (C.c_float * len(STAGE_NAMES))()
+    n = _lib.mvgs_stage_times(ctx, buf, len(STAGE_NAMES))
+    return {STAGE_NAMES[i]: float(buf[i]) for i in range(n)}
+
+
+class Rasterizer:
+    """Convenience owner of one context: sizes capacities, allocates outputs and
+    runs preprocess → render_fwd → render_bwd → adc_stats.  Marshalling only."""
+
+    def __init__(self, device: int = 0, max_pairs: int = 0, max_entries: int = 0):
+        self.device = device
+        self.ctx = create(device, max_pairs, max_entries)
+        self.V = self.H = self.W = 0
+
+    def __del__(self):
+        ctx = getattr(self, "ctx", None)
+        if ctx:
+            destroy(ctx)
+            self.ctx = None
+
+    def preprocess(self, g: dict, cams: np.ndarray, bg=(0.0, 0.0, 0.0), stream=None, auto_reserve: bool = True):
+        self.g = g
+        self.cams = np.ascontiguousarray(cams)
+        self.bg = bg
+        self.V = len(cams)
+        self.W = int(cams[0]["width"])
+        self.H = int(cams[0]["height"])
+        preprocess(self.ctx, g, self.cams, bg, stream)
+        if auto_reserve:
+            st = query(self.ctx, raise_on_capacity=False)
+            if st["overflow"]:
+                reserve(self.ctx, int(st["Q"] * 1.1) + 1024, int(st["K"] * 1.1) + 4096)
+                preprocess(self.ctx, g, self.cams, bg, stream)
+                st = query(self.ctx)
+            self.stats = st
+
+    def alloc_forward(self):
+        dev = torch.device("cuda", self.device)
+        rgb = torch.empty((self.V, 3, self.H, self.W), dtype=torch.float32, device=dev)
+        Tf = torch.empty((self.V, self.H, self.W), dtype=torch.float32, device=dev)
+        nc = torch.empty((self.V, self.H, self.W), dtype=torch.int32, device=dev)
+        return rgb, Tf, nc
+
+    def forward(self, out=None, stream=None):
+        rgb, Tf, nc = out if out is not None else self.alloc_forward()
+        render_fwd(self.ctx, rgb, Tf, nc, stream)
+        self._fwd = (Tf, nc)
+        return rgb, Tf, nc
+
+    def alloc_backward(self):
+        g = self.g
+        P = int(g["means"].shape[0])
+        dev = g["means"].device
+        z = lambda *s: torch.empty(s, dtype=torch.float32, device=dev)  # noqa: E731
+        grads = dict(d_means=z(P, 3), d_log_scales=z(P, 3), d_quats=z(P, 4), d_opacity_logits=z(P),
+                     d_sh=z(P, g["sh"].shape[1], 3))
+        adc = dict(e1=z(P), e2=z(P), e_old=z(P), vis=z(P))
+        return grads, adc
+
+    def backward(self, dL_drgb, out=None, stream=None):
+        grads, adc = out if out is not None else self.alloc_backward()
+        Tf, nc = self._fwd
+        render_bwd(self.ctx, dL_drgb, Tf, nc, stream)
+        adc_stats(self.ctx, grads, adc, stream)
+        return grads, adc

@@ -1,0 +1,64 @@
+"""Shared helpers for the GPU parity tests: run the CUDA path through the C ABI
+on synth inputs and compare with the oracle under the DESIGN.md §5 rules."""
+import numpy as np
+import torch
+
+
+def to_dev(g, device="cuda"):
+    out = {k: torch.from_numpy(np.ascontiguousarray(v)).to(device) for k, v in g.items() if isinstance(v, np.ndarray)}
+    out["sh_degree"] = g["sh_degree"]
+    return out
+
+
+def run_gpu(g, cams, dLdC=None, bg=(0.0, 0.0, 0.0), max_pairs=0, max_entries=0, export=True):
+    from paper_2506_12727_b200 import mvgs
+    R = mvgs.Rasterizer(0, max_pairs, max_entries)
+    gd = to_dev(g)
+    R.preprocess(gd, cams, bg)
+    rgb, Tf, nc = R.forward()
+    out = dict(stats=R.stats)
+    if dLdC is not None:
+        grads, adc = R.backward(torch.from_numpy(np.ascontiguousarray(dLdC, np.float32)).cuda())
+        out.update({k: v.cpu().numpy() for k, v in grads.items()})
+        out.update({k: v.cpu().numpy() for k, v in adc.items()})
+    torch.cuda.synchronize()
+    out.update(rgb=rgb.cpu().numpy(), T_final=Tf.cpu().numpy(), n_contrib=nc.cpu().numpy())
+    if export:
+        st = R.stats
+        V, T = len(cams), st["tiles_x"] * st["tiles_y"]
+        Q, K = int(st["Q"]), int(st["K"])
+        rs = torch.empty(V * T + 1, dtype=torch.int64, device="cuda")
+        eg = torch.empty(max(K, 1), dtype=torch.int32, device="cuda")
+        mvgs.export_lists(R.ctx, rs, eg)
+        pid = torch.empty((max(Q, 1), 2), dtype=torch.int32, device="cuda")
+        pi = torch.empty((max(Q, 1), 8), dtype=torch.int32, device="cuda")
+        pf = torch.empty((max(Q, 1), 12), dtype=torch.float32, device="cuda")
+        pg = torch.empty((max(Q, 1), 10), dtype=torch.float32, device="cuda")
+        mvgs.export_pairs(R.ctx, pid, pi, pf, pg if dLdC is not None else None)
+        torch.cuda.synchronize()
+        out.update(range_start=rs.cpu().numpy(), entry_gid=eg.cpu().numpy()[:K], pair_ids=pid.cpu().numpy()[:Q],
+                   pair_i=pi.cpu().numpy()[:Q], pair_f=pf.cpu().numpy()[:Q],
+                   pair_g=pg.cpu().numpy()[:Q] if dLdC is not None else None)
+    del R
+    return out
+
+
+def assert_close_rel(got, ref, name, rtol=1e-3, floor=1e-6):
+    """per tensor ‖Δ‖/‖ref‖ ≤ rtol and per element
+    |Δ| ≤ rtol·|ref| + floor·max|ref|; reports the worst elements."""
+    got = np.asarray(got, np.float64).reshape(-1)
+    ref = np.asarray(ref, np.float64).reshape(-1)
+    assert got.shape == ref.shape, name
+    d = np.abs(got - ref)
+    nref = np.linalg.norm(ref)
+    mx = np.max(np.abs(ref)) if ref.size else 0.0
+    if nref == 0:
+        assert np.all(d <= 1e-30 + 1e-12), name
+        return
+    rel = np.linalg.norm(got - ref) / nref
+    lim = rtol * np.abs(ref) + floor * mx
+    bad = np.argsort(-(d - lim))[:10]
+    msg = f"{name}: tensor rel {rel:.3e}; worst " + ", ".join(
+        f"[{i}] got {got[i]:.6e} ref {ref[i]:.6e}" for i in bad[:5])
+    assert rel <= rtol, msg
+    assert np.all(d <= lim), msg
