@@ -52,6 +52,8 @@ def parse():
     ap.add_argument("--impl", default="mvgs", choices=["mvgs", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile", action="store_true",
+                    help="sizing pass + warmup + one step, nothing else (for ncu)")
     return ap.parse_args()
 
 
@@ -188,6 +190,11 @@ def run_mvgs(args):
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
+    if args.profile:
+        step()
+        torch.cuda.synchronize()
+        print(json.dumps({"profile": True, "stats": mvgs.query(R.ctx)}), flush=True)
+        return
     st = mvgs.query(R.ctx)  # structural stats of this workload (sync, untimed)
     mvgs.set_timing(R.ctx, True)
     mvgs.stage_times(R.ctx)  # clear

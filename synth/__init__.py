@@ -236,7 +236,9 @@ def _object360(cfg: Config, rng, stretch_x=1.0):
     th = rng.uniform(0, 2 * np.pi, n_vol)
     vpts = np.stack([rr * np.cos(th), rr * np.sin(th), rng.uniform(0, 4, n_vol)], 1)
     s_vol = 1.5 * 1.2 * math.sqrt(2 * math.pi * 6 * 4 / max(counts[2], 1))
-    vls = np.full((n_vol, 3), math.log(s_vol))
+    # near-isotropic (N(0, 0.1²) log-scale jitter): an exactly isotropic Gaussian has an
+    # identically-zero rotation gradient, a degenerate case tested on its own
+    vls = math.log(s_vol) + rng.normal(0, 0.1, size=(n_vol, 3))
     vq = _unit_quats(rng, n_vol)
     means = np.concatenate([pts, vpts])
     means[:, 0] *= stretch_x

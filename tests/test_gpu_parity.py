@@ -234,3 +234,20 @@ def test_batch_equals_single_views():
         dm += one["d_means"]
     assert_close_rel(full["e2"], e2, "E2(batch) vs Σ E_old(single)")
     assert_close_rel(full["d_means"], dm, "d_means additivity")
+
+
+def test_isotropic_rotation_gradient_is_zero():
+    """Exactly isotropic Gaussians: ∂L/∂q ≡ 0 analytically (the oracle gives ~1e-15);
+    the GPU's fp32 value must be at rounding level relative to the other gradients."""
+    rng = np.random.default_rng(9)
+    n = 300
+    means = rng.uniform(-0.4, 0.4, (n, 3)) + [0, 0, 2.5]
+    g = _scene(means, np.full((n, 3), math.log(0.05)), rng.uniform(-1, 2, n), rgb=rng.uniform(0, 1, (n, 3)))
+    g["quats"] = rng.normal(size=(n, 4)).astype(np.float32)
+    cam = synth.cams_array([synth.make_camera(np.eye(3), [0, 0, 0], 64, 48, 50.0)])
+    dL = synth.make_dLdC_scaled(1, 48, 64, 2)
+    ref = oracle.Oracle(g, cam).backward(dL)
+    gpu = run_gpu(g, cam, dL, export=False)
+    assert np.max(np.abs(ref["d_quats"])) < 1e-9 * np.max(np.abs(ref["d_log_scales"]))
+    assert np.max(np.abs(gpu["d_quats"])) < 1e-4 * np.max(np.abs(ref["d_log_scales"]))
+    assert_close_rel(gpu["d_log_scales"], ref["d_log_scales"], "d_log_scales")
