@@ -127,12 +127,21 @@ def stage_models(P, NK, V, NB, Q, K, T, evf, evb):
         "scan_pairs": ("hbm", 3 * 4 * V * NB),
         "project": ("hbm", pbytes + 4 * V * NB + Q * (48 + 8 + 48)),
         "scan_buckets": ("hbm", 3 * 4 * V * T),
-        "dup_scatter": ("hbm", Q * (16 + 8) + 8 * K),
-        "sort": ("hbm", 12 * K),
+        "sort_pairs": ("hbm", 4 * 16 * Q),
+        "dup": ("hbm", Q * (4 + 16 + 8 + 4 + 4) + 8 * K),
+        "sort_entries": ("hbm", ((max(1, (V * T - 1).bit_length()) + 7) // 8) * 16 * K),
         "render_fwd": ("alu", FWD_FLOPS_PER_EVAL * evf),
         "render_bwd": ("alu", BWD_FLOPS_PER_EVAL * evb),
         "gauss_bwd": ("hbm", 2 * pbytes + Q * (16 + 8 + 48) + 16 * P),
     }
+
+
+def launches_per_step(nbuckets, Q, K):
+    """Kernels libmvgs launches per step: count, 3-kernel scan, project,
+    3-kernel scan, pair sort (4 passes × (hist + 3 scan + scatter)), pair-tiles + 3 scan +
+    dup, entry sort (⌈log2(V·T)/8⌉ passes × 5) + max-bucket, fwd, bwd, gauss_bwd."""
+    ent_passes = (max(1, (nbuckets - 1).bit_length()) + 7) // 8
+    return 1 + 3 + 1 + 3 + 4 * 5 + 1 + 3 + 1 + ent_passes * 5 + 1 + 3
 
 
 # ---------------------------------------------------------------------- mvgs
@@ -253,7 +262,7 @@ def run_mvgs(args):
     peaks, peak_src = measured_peaks()
     T = st["tiles_x"] * st["tiles_y"]
     NB = (P + 255) // 256
-    models = stage_models(P, NK, Vr, NB, st["Q"], st["K"], T * Vr, st["eval_fwd"], st["eval_bwd"])
+    models = stage_models(P, NK, Vr, NB, st["Q"], st["K"], T, st["eval_fwd"], st["eval_bwd"])
     dom = max(stages, key=lambda k: stages[k])
     bound, units = models[dom]
     t_dom = stages[dom] / 1e3
@@ -290,7 +299,7 @@ def run_mvgs(args):
         "clocks": clocks,
         "e2e": {"value": round(views_total / (e2e_ms / 1e3), 3), "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": round(e2e_ms, 3)},
-        "gpu_launches": 13 * args.steps,
+        "gpu_launches": launches_per_step(Vr * T, st["Q"], st["K"]) * args.steps,
         "roofline": roof,
     }
     if rank == 0 and N == 1 and not args.no_cpu_baseline:

@@ -169,8 +169,8 @@ mvgs_status mvgs_export_pairs(mvgs_ctx *ctx, int32_t *pair_ids, int32_t *pair_i,
  * of each stage over all runs recorded since the previous read (0 if none), in
  * the order of MVGS_STAGE_NAMES, clears the record, and returns the number of
  * stages written. */
-#define MVGS_NUM_STAGES 9
-#define MVGS_STAGE_NAMES "count,scan_pairs,project,scan_buckets,dup_scatter,sort,render_fwd,render_bwd,gauss_bwd"
+#define MVGS_NUM_STAGES 10
+#define MVGS_STAGE_NAMES "count,scan_pairs,project,scan_buckets,sort_pairs,dup,sort_entries,render_fwd,render_bwd,gauss_bwd"
 mvgs_status mvgs_set_timing(mvgs_ctx *ctx, int enable);
 int mvgs_stage_times(mvgs_ctx *ctx, float *ms, int n);
 

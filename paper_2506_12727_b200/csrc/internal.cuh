@@ -36,11 +36,15 @@ struct Launch {  // everything a kernel needs about the current batch
     // workspace
     int* blk_off;     // [V*NB + 1]  exclusive scan of per-(view, block) participation counts
     int* bucket_off;  // [V*T + 1]   exclusive scan of per-(view, tile) entry counts
-    int* cursor;      // [V*T]
     float4* rec;      // [cap_pairs * 3]
     PairMeta* meta;   // [cap_pairs]
     float* pgrad;     // [cap_pairs * PG_STRIDE]
-    uint32_t *key, *val, *key2, *val2;  // [cap_entries]
+    uint32_t *key, *val, *key2, *val2;  // [cap_entries] entry (bucket key, pair) ping-pong
+    uint32_t *pkey, *pval, *pkey2, *pval2;  // [cap_pairs] pair (depth key, pair) ping-pong
+    int* ecount;      // [cap_pairs + 1] tiles per depth-ordered pair → entry offsets
+    int* rs_counts;   // radix digit × tile counts
+    int* scan_tmp;    // scan block sums
+    const uint32_t* sorted;  // [K] pair index of every entry in (view, tile, depth, gid) order
     int* counters;    // [C_NCOUNTERS]
     unsigned long long* counters64;  // [2]: fwd / bwd (pixel, entry) evaluations
 };
@@ -58,11 +62,14 @@ struct mvgs_ctx {
     mvgs_camera* d_cams = nullptr;
     int* d_blk = nullptr;
     int* d_bucket = nullptr;
-    int* d_cursor = nullptr;
     float4* d_rec = nullptr;
     mvgs::PairMeta* d_meta = nullptr;
     float* d_pgrad = nullptr;
     uint32_t *d_key = nullptr, *d_val = nullptr, *d_key2 = nullptr, *d_val2 = nullptr;
+    uint32_t *d_pkey = nullptr, *d_pval = nullptr, *d_pkey2 = nullptr, *d_pval2 = nullptr;
+    int* d_ecount = nullptr;
+    int* d_rs = nullptr;
+    int64_t cap_rs = 0;
     int* d_counters = nullptr;
     unsigned long long* d_counters64 = nullptr;
     int* d_scan = nullptr;  // scan block sums
@@ -80,8 +87,12 @@ namespace mvgs {
 cudaError_t scan_exclusive(int* a, int n, int* total_slot, int* tmp, cudaStream_t s);
 cudaError_t launch_count(const Launch& L, cudaStream_t s);
 cudaError_t launch_project(const Launch& L, cudaStream_t s);
-cudaError_t launch_dup_scatter(const Launch& L, cudaStream_t s);
-cudaError_t launch_bucket_sort(const Launch& L, cudaStream_t s);
+cudaError_t launch_sort_pairs(const Launch& L, const uint32_t** order_out, cudaStream_t s);
+cudaError_t launch_dup_sort(const Launch& L, const uint32_t* order, uint32_t** sorted_vals, cudaStream_t s,
+                            bool timing_dup_only);
+cudaError_t launch_sort_entries(const Launch& L, uint32_t** sorted_vals, cudaStream_t s);
+int64_t radix_counts_size(int64_t cap);
+int radix_tiles(int64_t cap);
 cudaError_t launch_render_fwd(const Launch& L, float* rgb, float* Tf, int32_t* nc, cudaStream_t s);
 cudaError_t launch_render_bwd(const Launch& L, const float* dL, const float* Tf, const int32_t* nc, cudaStream_t s);
 cudaError_t launch_gauss_bwd(const Launch& L, const mvgs_grads& gr, const mvgs_adc& adc, cudaStream_t s);

@@ -25,27 +25,48 @@ __constant__ float g_SH3[7] = {-0.5900435899266435f, 2.890611442640554f, -0.4570
                                0.3731763325901154f, -0.4570457994644658f, 1.445305721320277f,
                                -0.5900435899266435f};
 
+// SH coefficients and their gradient live in shared memory, one padded row per
+// Gaussian (odd stride ⇒ conflict-free when each thread walks its own row);
+// the block's rows are loaded and stored with coalesced accesses.
 template <int D>
-__global__ __launch_bounds__(BLK) void k_gauss_bwd(Launch L, mvgs_grads gr, mvgs_adc adc) {
-    constexpr int NK = (D + 1) * (D + 1);
+struct ShRows {
+    static constexpr int NK = (D + 1) * (D + 1);
+    static constexpr int NS = NK * 3;
+    static constexpr int STRIDE = NS | 1;
+};
+
+template <int D>
+__global__ __launch_bounds__(BLK, 2) void k_gauss_bwd(Launch L, mvgs_grads gr, mvgs_adc adc) {
+    constexpr int NK = ShRows<D>::NK, NS = ShRows<D>::NS, SS = ShRows<D>::STRIDE;
+    extern __shared__ float smem_sh[];
+    float* sh_s = smem_sh;              // [BLK][SS]
+    float* dsh_s = smem_sh + BLK * SS;  // [BLK][SS]
     __shared__ int wc[BLK / 32][32];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const unsigned lt = (1u << lane) - 1u;
-    const int64_t g = (int64_t)blockIdx.x * BLK + threadIdx.x;
+    const int64_t g0 = (int64_t)blockIdx.x * BLK;
+    const int64_t g = g0 + threadIdx.x;
     const bool valid = g < L.P;
+    {
+        const int nb = (int)min((int64_t)BLK, L.P - g0);
+        const float* src = L.sh + g0 * (int64_t)L.sh_stride * 3;
+        const int rowlen = L.sh_stride * 3;
+        for (int i = threadIdx.x; i < nb * NS; i += BLK) {
+            const int r = i / NS, k = i - r * NS;
+            sh_s[r * SS + k] = src[(int64_t)r * rowlen + k];
+            dsh_s[r * SS + k] = 0.f;
+        }
+    }
+    __syncthreads();
+    const float* sh = sh_s + threadIdx.x * SS;
+    float* dsh = dsh_s + threadIdx.x * SS;
     float mx = 0.f, my = 0.f, mz = 0.f;
     Activ a;
-    float sh[NK * 3], dsh[NK * 3];
-#pragma unroll
-    for (int k = 0; k < NK * 3; k++) dsh[k] = 0.f;
     if (valid) {
         mx = L.means[3 * g];
         my = L.means[3 * g + 1];
         mz = L.means[3 * g + 2];
         ca_activate(L.log_scales + 3 * g, L.quats + 4 * g, L.opac[g], a);
-        const float* s = L.sh + g * (int64_t)L.sh_stride * 3;
-#pragma unroll
-        for (int k = 0; k < NK * 3; k++) sh[k] = s[k];
     }
     float dmx = 0.f, dmy = 0.f, dmz = 0.f;
     float G00 = 0.f, G01 = 0.f, G02 = 0.f, G11 = 0.f, G12 = 0.f, G22 = 0.f;  // ∂L/∂Σ (symmetric)
@@ -212,6 +233,16 @@ __global__ __launch_bounds__(BLK) void k_gauss_bwd(Launch L, mvgs_grads gr, mvgs
         }
         __syncthreads();
     }
+    // coalesced store of the SH gradient rows (coefficients above the active degree are 0)
+    {
+        const int nb = (int)min((int64_t)BLK, L.P - g0);
+        float* dst = gr.d_sh + g0 * (int64_t)L.sh_stride * 3;
+        const int rowlen = L.sh_stride * 3;
+        for (int i = threadIdx.x; i < nb * rowlen; i += BLK) {
+            const int r = i / rowlen, k = i - r * rowlen;
+            dst[i] = k < NS ? dsh_s[r * SS + k] : 0.f;
+        }
+    }
     if (!valid) return;
     // Σ = M Mᵀ, M = R diag(s): ∂L/∂M = 2 G M (G symmetric)
     const float* R = a.R;
@@ -255,10 +286,6 @@ __global__ __launch_bounds__(BLK) void k_gauss_bwd(Launch L, mvgs_grads gr, mvgs
     gr.d_log_scales[3 * g + 1] = dls[1];
     gr.d_log_scales[3 * g + 2] = dls[2];
     gr.d_opacity_logits[g] = dop * a.o * (1.f - a.o);
-    float* ds = gr.d_sh + g * (int64_t)L.sh_stride * 3;
-#pragma unroll
-    for (int k = 0; k < NK * 3; k++) ds[k] = dsh[k];
-    for (int k = NK * 3; k < L.sh_stride * 3; k++) ds[k] = 0.f;
     adc.e1[g] = e1;
     adc.e2[g] = e2;
     if (adc.e_old) adc.e_old[g] = sqrtf(gsx * gsx + gsy * gsy);
@@ -268,14 +295,22 @@ __global__ __launch_bounds__(BLK) void k_gauss_bwd(Launch L, mvgs_grads gr, mvgs
     if (adc.denom_acc) adc.denom_acc[g] += nvis;
 }
 
+template <int D>
+cudaError_t launch_gauss_bwd_t(const Launch& L, const mvgs_grads& gr, const mvgs_adc& adc, cudaStream_t s) {
+    const size_t smem = sizeof(float) * 2 * BLK * ShRows<D>::STRIDE;
+    cudaError_t e = cudaFuncSetAttribute(k_gauss_bwd<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    k_gauss_bwd<D><<<L.NB, BLK, smem, s>>>(L, gr, adc);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_gauss_bwd(const Launch& L, const mvgs_grads& gr, const mvgs_adc& adc, cudaStream_t s) {
     switch (L.sh_degree) {
-        case 0: k_gauss_bwd<0><<<L.NB, BLK, 0, s>>>(L, gr, adc); break;
-        case 1: k_gauss_bwd<1><<<L.NB, BLK, 0, s>>>(L, gr, adc); break;
-        case 2: k_gauss_bwd<2><<<L.NB, BLK, 0, s>>>(L, gr, adc); break;
-        default: k_gauss_bwd<3><<<L.NB, BLK, 0, s>>>(L, gr, adc); break;
+        case 0: return launch_gauss_bwd_t<0>(L, gr, adc, s);
+        case 1: return launch_gauss_bwd_t<1>(L, gr, adc, s);
+        case 2: return launch_gauss_bwd_t<2>(L, gr, adc, s);
+        default: return launch_gauss_bwd_t<3>(L, gr, adc, s);
     }
-    return cudaGetLastError();
 }
 
 }  // namespace mvgs

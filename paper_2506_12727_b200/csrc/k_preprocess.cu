@@ -10,10 +10,7 @@
 //                     per-Gaussian work (activations, Σ, SH load) is done once for
 //                     the whole batch; also the per-(view, tile) entry histogram (S3)
 //   scan          S3/S5 exclusive scan of the histogram → bucket offsets = ranges
-//   k_dup_scatter S3  "duplicating projected Gaussians for each tile they cover"
-//                     (P:576): one 32-bit depth key + 32-bit pair value per entry,
-//                     written into its (view, tile) bucket (the key's view and tile
-//                     fields of P:579 are the bucket index)
+//   (duplication and sorting: k_sort.cu)
 #include "ca.cuh"
 #include "internal.cuh"
 
@@ -186,22 +183,30 @@ __device__ __forceinline__ void sh_eval_basis(float x, float y, float z, float* 
 
 template <int D>
 __global__ __launch_bounds__(BLK) void k_project(Launch L) {
-    constexpr int NK = (D + 1) * (D + 1);
+    constexpr int NK = (D + 1) * (D + 1), NS = NK * 3, SS = NS | 1;
+    extern __shared__ float sh_s[];  // [BLK][SS] SH rows, coalesced block load, odd stride
     __shared__ int wc[BLK / 32][32];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int64_t g = (int64_t)blockIdx.x * BLK + threadIdx.x;
+    const int64_t g0 = (int64_t)blockIdx.x * BLK;
+    const int64_t g = g0 + threadIdx.x;
     const bool valid = g < L.P;
+    {
+        const int nb = (int)min((int64_t)BLK, L.P - g0);
+        const float* src = L.sh + g0 * (int64_t)L.sh_stride * 3;
+        const int rowlen = L.sh_stride * 3;
+        for (int i = threadIdx.x; i < nb * NS; i += BLK) {
+            const int r = i / NS, k = i - r * NS;
+            sh_s[r * SS + k] = src[(int64_t)r * rowlen + k];
+        }
+    }
+    const float* sh = sh_s + threadIdx.x * SS;
     float mx = 0.f, my = 0.f, mz = 0.f;
     Activ a;
-    float sh[NK * 3];
     if (valid) {
         mx = L.means[3 * g];
         my = L.means[3 * g + 1];
         mz = L.means[3 * g + 2];
         ca_activate(L.log_scales + 3 * g, L.quats + 4 * g, L.opac[g], a);
-        const float* s = L.sh + g * (int64_t)L.sh_stride * 3;
-#pragma unroll
-        for (int k = 0; k < NK * 3; k++) sh[k] = s[k];
     }
     const unsigned lt = (1u << lane) - 1u;
     for (int v0 = 0; v0 < L.V; v0 += 32) {
@@ -225,31 +230,41 @@ __global__ __launch_bounds__(BLK) void k_project(Launch L) {
             Proj p;
             ca_project(c, mx, my, mz, a.Sig, L.TX, L.TY, p);
             const int tiles = p.ok ? (p.rx1 - p.rx0) * (p.ry1 - p.ry0) : 0;
-            // colour (R17), free arithmetic
-            const float cpx = -(c.R[0] * c.t[0] + c.R[3] * c.t[1] + c.R[6] * c.t[2]);
-            const float cpy = -(c.R[1] * c.t[0] + c.R[4] * c.t[1] + c.R[7] * c.t[2]);
-            const float cpz = -(c.R[2] * c.t[0] + c.R[5] * c.t[1] + c.R[8] * c.t[2]);
-            float dx = mx - cpx, dy = my - cpy, dz = mz - cpz;
-            const float inv = rsqrtf(dx * dx + dy * dy + dz * dz);
-            dx *= inv; dy *= inv; dz *= inv;
-            float Y[NK];
-            sh_eval_basis<D>(dx, dy, dz, Y);
-            float rgb[3];
-            uint32_t flags = (p.clx ? 8u : 0u) | (p.cly ? 16u : 0u);
-#pragma unroll
-            for (int ch = 0; ch < 3; ch++) {
-                float acc = 0.5f;
-#pragma unroll
-                for (int kk = 0; kk < NK; kk++) acc += Y[kk] * sh[3 * kk + ch];
-                if (acc < 0.f) {
-                    flags |= 1u << ch;
-                    acc = 0.f;
-                }
-                rgb[ch] = acc;
+            if (pair < L.cap_pairs) {  // depth key for the pair sort (inert pairs sort last)
+                L.pkey[pair] = tiles > 0 ? __float_as_uint(p.tz) : 0xffffffffu;
+                L.pval[pair] = (uint32_t)pair;
             }
-            if (pair < L.cap_pairs) {
+            if (pair >= L.cap_pairs) {
+                L.counters[C_OVERFLOW] = 1;
+            } else if (tiles == 0) {
+                // inert pair (R27): only the empty rect / depth and the ids are read later
+                L.rec[3 * pair + 2] = make_float4(0.f, p.tz, 0.f, 0.f);
+                L.meta[pair] = PairMeta{(uint32_t)g, ((uint32_t)v << 8) | (p.clx ? 8u : 0u) | (p.cly ? 16u : 0u)};
+            } else {
+                // colour (R17), free arithmetic
+                const float cpx = -(c.R[0] * c.t[0] + c.R[3] * c.t[1] + c.R[6] * c.t[2]);
+                const float cpy = -(c.R[1] * c.t[0] + c.R[4] * c.t[1] + c.R[7] * c.t[2]);
+                const float cpz = -(c.R[2] * c.t[0] + c.R[5] * c.t[1] + c.R[8] * c.t[2]);
+                float dx = mx - cpx, dy = my - cpy, dz = mz - cpz;
+                const float inv = rsqrtf(dx * dx + dy * dy + dz * dz);
+                dx *= inv; dy *= inv; dz *= inv;
+                float Y[NK];
+                sh_eval_basis<D>(dx, dy, dz, Y);
+                float rgb[3];
+                uint32_t flags = (p.clx ? 8u : 0u) | (p.cly ? 16u : 0u);
+#pragma unroll
+                for (int ch = 0; ch < 3; ch++) {
+                    float acc = 0.5f;
+#pragma unroll
+                    for (int kk = 0; kk < NK; kk++) acc += Y[kk] * sh[3 * kk + ch];
+                    if (acc < 0.f) {
+                        flags |= 1u << ch;
+                        acc = 0.f;
+                    }
+                    rgb[ch] = acc;
+                }
                 const uint32_t lo = (uint32_t)p.rx0 | ((uint32_t)p.ry0 << 16);
-                const uint32_t hi = tiles > 0 ? ((uint32_t)p.rx1 | ((uint32_t)p.ry1 << 16)) : lo;
+                const uint32_t hi = (uint32_t)p.rx1 | ((uint32_t)p.ry1 << 16);
                 float4* r = L.rec + 3 * pair;
                 r[0] = make_float4(p.px, p.py, p.A, p.B);
                 r[1] = make_float4(p.C, a.o, rgb[0], rgb[1]);
@@ -257,8 +272,6 @@ __global__ __launch_bounds__(BLK) void k_project(Launch L) {
                 L.meta[pair] = PairMeta{(uint32_t)g, ((uint32_t)v << 8) | flags};
                 float4* pg = reinterpret_cast<float4*>(L.pgrad + pair * PG_STRIDE);
                 pg[0] = pg[1] = pg[2] = make_float4(0.f, 0.f, 0.f, 0.f);
-            } else {
-                L.counters[C_OVERFLOW] = 1;
             }
             if (tiles > 0) {
                 atomicAdd(&L.counters[C_NVIS], 1);
@@ -271,48 +284,22 @@ __global__ __launch_bounds__(BLK) void k_project(Launch L) {
     }
 }
 
+template <int D>
+cudaError_t launch_project_t(const Launch& L, cudaStream_t s) {
+    const size_t smem = sizeof(float) * BLK * (((D + 1) * (D + 1) * 3) | 1);
+    cudaError_t e = cudaFuncSetAttribute(k_project<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    k_project<D><<<L.NB, BLK, smem, s>>>(L);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_project(const Launch& L, cudaStream_t s) {
     switch (L.sh_degree) {
-        case 0: k_project<0><<<L.NB, BLK, 0, s>>>(L); break;
-        case 1: k_project<1><<<L.NB, BLK, 0, s>>>(L); break;
-        case 2: k_project<2><<<L.NB, BLK, 0, s>>>(L); break;
-        default: k_project<3><<<L.NB, BLK, 0, s>>>(L); break;
+        case 0: return launch_project_t<0>(L, s);
+        case 1: return launch_project_t<1>(L, s);
+        case 2: return launch_project_t<2>(L, s);
+        default: return launch_project_t<3>(L, s);
     }
-    return cudaGetLastError();
-}
-
-// ------------------------------------------------------------------ S3
-__global__ __launch_bounds__(256) void k_dup_scatter(Launch L) {
-    const int Q = min((int64_t)L.counters[C_Q], L.cap_pairs);
-    const int stride = gridDim.x * blockDim.x;
-    for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < Q; q += stride) {
-        const float4 r2 = L.rec[3 * (int64_t)q + 2];
-        const uint32_t lo = __float_as_uint(r2.z), hi = __float_as_uint(r2.w);
-        const int rx0 = lo & 0xffff, ry0 = lo >> 16, rx1 = hi & 0xffff, ry1 = hi >> 16;
-        if (rx1 <= rx0 || ry1 <= ry0) continue;
-        const int v = L.meta[q].vf >> 8;
-        const uint32_t dbits = __float_as_uint(r2.y);
-        for (int ty = ry0; ty < ry1; ty++)
-            for (int tx = rx0; tx < rx1; tx++) {
-                const int64_t b = (int64_t)v * L.T + ty * L.TX + tx;
-                const int pos = atomicAdd(&L.cursor[b], 1);
-                const int64_t e = (int64_t)L.bucket_off[b] + pos;
-                if (e < L.cap_entries) {
-                    L.key[e] = dbits;
-                    L.val[e] = (uint32_t)q;
-                } else {
-                    L.counters[C_OVERFLOW] = 1;
-                }
-            }
-    }
-}
-
-cudaError_t launch_dup_scatter(const Launch& L, cudaStream_t s) {
-    int dev = 0, nsm = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    k_dup_scatter<<<nsm * 8, 256, 0, s>>>(L);
-    return cudaGetLastError();
 }
 
 // ------------------------------------------------------------------ export (tests)
@@ -326,7 +313,7 @@ __global__ void k_export(Launch L, int64_t* range_start, int32_t* entry_gid, int
     if (range_start)
         for (int64_t b = t0; b <= nb; b += stride) range_start[b] = L.bucket_off[b];
     if (entry_gid)
-        for (int64_t e = t0; e < K; e += stride) entry_gid[e] = (int32_t)L.meta[L.val[e]].gid;
+        for (int64_t e = t0; e < K; e += stride) entry_gid[e] = (int32_t)L.meta[L.sorted[e]].gid;
     for (int64_t q = t0; q < Q; q += stride) {
         const PairMeta m = L.meta[q];
         const float4 r0 = L.rec[3 * q], r1 = L.rec[3 * q + 1], r2 = L.rec[3 * q + 2];
@@ -344,13 +331,19 @@ __global__ void k_export(Launch L, int64_t* range_start, int32_t* entry_gid, int
             o[6] = (int32_t)(m.vf & 0xff);
             o[7] = 0;
         }
+        const bool inert = lo == hi;  // tiles == 0: only depth and ids were written (R27)
         if (pair_f) {
             float* f = pair_f + 12 * q;
-            f[0] = r2.y; f[1] = r0.x; f[2] = r0.y; f[3] = r0.z; f[4] = r0.w; f[5] = r1.x;
-            f[6] = r1.y; f[7] = r1.z; f[8] = r1.w; f[9] = r2.x; f[10] = 0.f; f[11] = 0.f;
+            f[0] = r2.y;
+            if (inert) {
+                for (int k = 1; k < 12; k++) f[k] = 0.f;
+            } else {
+                f[1] = r0.x; f[2] = r0.y; f[3] = r0.z; f[4] = r0.w; f[5] = r1.x;
+                f[6] = r1.y; f[7] = r1.z; f[8] = r1.w; f[9] = r2.x; f[10] = 0.f; f[11] = 0.f;
+            }
         }
         if (pair_g)
-            for (int k = 0; k < NG; k++) pair_g[NG * q + k] = L.pgrad[q * PG_STRIDE + k];
+            for (int k = 0; k < NG; k++) pair_g[NG * q + k] = inert ? 0.f : L.pgrad[q * PG_STRIDE + k];
     }
 }
 

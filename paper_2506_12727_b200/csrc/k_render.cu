@@ -55,7 +55,7 @@ __global__ __launch_bounds__(RT) void k_render_fwd(Launch L, float* __restrict__
             if (__syncthreads_count(done) == RT) break;
             const int idx = b0 + threadIdx.x;
             if (idx < end) {
-                const uint32_t q = L.val[idx];
+                const uint32_t q = L.sorted[idx];
                 const float4* r = L.rec + 3 * (int64_t)q;
                 s0[threadIdx.x] = r[0];
                 s1[threadIdx.x] = r[1];
@@ -169,6 +169,7 @@ __global__ __launch_bounds__(RT) void k_render_bwd(Launch L, const float* __rest
     if (last > 0) atomicMax(&smax, last);
     __syncthreads();
     const int maxlast = smax;
+    const int wmax = __reduce_max_sync(FULLR, last);  // entries beyond it are skipped warp-uniformly
     const int my_id = reduce_id(lane);
     const bool owner = (__ffs(__match_any_sync(FULLR, my_id)) - 1) == lane;
     const float fx = (float)x, fy = (float)y;
@@ -182,7 +183,7 @@ __global__ __launch_bounds__(RT) void k_render_bwd(Launch L, const float* __rest
         const int cnt = b_end - b0;
         __syncthreads();
         if (threadIdx.x < cnt) {
-            const uint32_t q = L.val[start + b0 + threadIdx.x];
+            const uint32_t q = L.sorted[start + b0 + threadIdx.x];
             const float4* r = L.rec + 3 * (int64_t)q;
             sq[threadIdx.x] = q;
             s0[threadIdx.x] = r[0];
@@ -191,7 +192,7 @@ __global__ __launch_bounds__(RT) void k_render_bwd(Launch L, const float* __rest
         }
         for (int i = threadIdx.x; i < RT * NG; i += RT) sacc[i] = 0.f;
         __syncthreads();
-        for (int jj = cnt - 1; jj >= 0; jj--) {
+        for (int jj = min(cnt, wmax - b0) - 1; jj >= 0; jj--) {
             const int j = b0 + jj;
             float val[NG];
 #pragma unroll
@@ -209,14 +210,15 @@ __global__ __launch_bounds__(RT) void k_render_bwd(Launch L, const float* __rest
                     if (alpha >= ALPHA_MIN) {
                         contrib = true;
                         const float one_m = 1.0f - alpha;
-                        T = T / one_m;
+                        const float inv_one_m = __fdividef(1.0f, one_m);
+                        T = T * inv_one_m;
                         const float w = alpha * T;
                         const float cb = s2[jj];
                         acc0 = a_prev * c0p + (1.f - a_prev) * acc0;
                         acc1 = a_prev * c1p + (1.f - a_prev) * acc1;
                         acc2 = a_prev * c2p + (1.f - a_prev) * acc2;
                         float dLda = (c.z - acc0) * dL0 + (c.w - acc1) * dL1 + (cb - acc2) * dL2;
-                        dLda = dLda * T - T_fin / one_m * dL_bg;
+                        dLda = dLda * T - T_fin * inv_one_m * dL_bg;
                         a_prev = alpha;
                         c0p = c.z; c1p = c.w; c2p = cb;
                         const bool clamped = oG > ALPHA_MAX;
@@ -227,7 +229,8 @@ __global__ __launch_bounds__(RT) void k_render_bwd(Launch L, const float* __rest
                         const float gy = dLdpw * -(c.x * dy + a.w * dx) * hh;
                         val[0] = gx;
                         val[1] = gy;
-                        val[2] = sqrtf(gx * gx + gy * gy);
+                        const float n2 = gx * gx + gy * gy;
+                        val[2] = n2 > 0.f ? n2 * rsqrtf(n2) : 0.f;
                         val[3] = -0.5f * dLdpw * dx * dx;
                         val[4] = -dLdpw * dx * dy;
                         val[5] = -0.5f * dLdpw * dy * dy;

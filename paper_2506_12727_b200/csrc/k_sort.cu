@@ -1,201 +1,215 @@
-// k_sort.cu — S4: "sorting Gaussians by depth for each tile" with views kept
-// apart.  The (view, tile) part of the paper's 64-bit key is the
-// bucket index (S3 already separated the entries), so each bucket only needs
-// its 32-bit depth keys ordered, ties by Gaussian id (R10).
+// k_sort.cu — S3 duplication + S4 sort.
 //
-// One CTA per (view, tile) bucket runs an LSD radix sort (4 passes × 8 bits,
-// passes whose digit is constant over the bucket are skipped).  Each pass is
-// stable: a warp owns a contiguous strip of 32·IPT positions, ranks its keys
-// with __match_any_sync in position order, and the CTA turns per-warp digit
-// counts into scatter offsets.  Buckets up to TILE_N keys are sorted entirely in
-// shared memory; larger ones stream tiles of TILE_N through global scratch
-// (key2/val2) with the same code and a running per-digit base.
-//
-// Ties: equal depth bits are ordered by pair index, which for one view is the
-// ascending-gid order (pairs are view-major, gid-ascending).  Equal keys are
-// rare; runs are fixed by an insertion sort started from each run head.
+// The paper keys every duplicated entry with (tile 16 | view 16 | depth 32)
+// and sorts the 64-bit keys.  Here the same total order (view, tile, depth,
+// gid) (R9, R10) is produced with two short stable LSD radix sorts and no
+// atomics:
+//   1. sort the pairs by depth bits (4 × 8-bit passes over Q pairs, Q ≪ K);
+//      pairs start in (view, gid) order and the sort is stable, so equal
+//      depths stay in gid order;
+//   2. duplicate: walk the pairs in that order and write one entry per covered
+//      tile, key = view·T + tile (positions from an exclusive scan of the
+//      per-pair tile counts — coalesced, deterministic);
+//   3. stable sort the K entries by the bucket key only (⌈log2(V·T)⌉ bits,
+//      8-bit digits).  Stability keeps each bucket in (depth, gid) order.
+// Every pass is an "on-chip" radix pass: a CTA ranks a 2048-key tile in shared
+// memory (warp __match_any_sync + per-warp digit counters, stable by
+// position), digit×tile counts are scanned device-wide, and the tile scatters
+// straight to its final positions.  Sizes (Q, K) live on the device; grids are
+// sized by capacity and tiles beyond the live count exit.
+#include "ca.cuh"
 #include "internal.cuh"
 
 namespace mvgs {
 
-constexpr unsigned FULLM = 0xffffffffu;
-constexpr int SORT_T = 256, SORT_IPT = 8, TILE_N = SORT_T * SORT_IPT, NW = SORT_T / 32;
+constexpr unsigned FULLS = 0xffffffffu;
+constexpr int RS_T = 256, RS_IPT = 8, RS_TILE = RS_T * RS_IPT, RS_NW = RS_T / 32, RS_BINS = 256;
 
-struct SortSmem {
-    uint32_t hist[NW][256];
-    uint32_t base[256];
-    uint32_t ws[NW + 1];
-    uint32_t diff;
-    int anytie;
-};
+int radix_tiles(int64_t cap) { return (int)((cap + RS_TILE - 1) / RS_TILE); }
+int64_t radix_counts_size(int64_t cap) { return (int64_t)RS_BINS * radix_tiles(cap) + 1; }
 
-__device__ __forceinline__ uint32_t block_excl_scan_256(uint32_t x, uint32_t* ws, uint32_t* total) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    uint32_t inc = x;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        uint32_t y = __shfl_up_sync(FULLM, inc, o);
-        if (lane >= o) inc += y;
-    }
-    if (lane == 31) ws[warp] = inc;
+// per-tile digit histogram → counts[digit * ntiles + tile]
+__global__ __launch_bounds__(RS_T) void k_rs_hist(const uint32_t* __restrict__ keys, const int* __restrict__ n_ptr,
+                                                  int64_t cap, int shift, int nbits, int* __restrict__ counts,
+                                                  int ntiles) {
+    __shared__ int h[RS_BINS];
+    h[threadIdx.x] = 0;
     __syncthreads();
-    if (threadIdx.x == 0) {
-        uint32_t run = 0;
-        for (int w = 0; w < NW; w++) {
-            uint32_t t = ws[w];
-            ws[w] = run;
-            run += t;
-        }
-        ws[NW] = run;
-    }
+    const int n = (int)min((int64_t)*n_ptr, cap);
+    const int t0 = blockIdx.x * RS_TILE;
+    const uint32_t mask = (1u << nbits) - 1u;
+    for (int i = t0 + threadIdx.x; i < min(n, t0 + RS_TILE); i += RS_T) atomicAdd(&h[(keys[i] >> shift) & mask], 1);
     __syncthreads();
-    uint32_t r = ws[warp] + inc - x;
-    *total = ws[NW];
-    __syncthreads();
-    return r;
+    counts[(int64_t)threadIdx.x * ntiles + blockIdx.x] = h[threadIdx.x];
 }
 
-// Stable LSD radix sort of (k, v)[0..n) → result back in (kA, vA).
-// kA/vA/kB/vB may point to shared or global memory (generic addressing).
-__device__ void bucket_radix_sort(uint32_t* kA, uint32_t* vA, uint32_t* kB, uint32_t* vB, int n, SortSmem& sm) {
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+// stable scatter of one tile to offsets[digit * ntiles + tile] + rank
+__global__ __launch_bounds__(RS_T) void k_rs_scatter(const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin,
+                                                     uint32_t* __restrict__ kout, uint32_t* __restrict__ vout,
+                                                     const int* __restrict__ n_ptr, int64_t cap, int shift, int nbits,
+                                                     const int* __restrict__ offs, int ntiles) {
+    __shared__ uint32_t hist[RS_NW][RS_BINS];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const unsigned lt = (1u << lane) - 1u;
-    if (tid == 0) {
-        sm.diff = 0;
-        sm.anytie = 0;
+    const int n = (int)min((int64_t)*n_ptr, cap);
+    const int t0 = blockIdx.x * RS_TILE;
+    if (t0 >= n) return;
+    const uint32_t mask = (1u << nbits) - 1u;
+#pragma unroll
+    for (int i = 0; i < RS_BINS / 32; i++) hist[warp][lane * (RS_BINS / 32) + i] = 0;
+    __syncwarp();
+    uint32_t key[RS_IPT], val[RS_IPT], loc[RS_IPT];
+#pragma unroll
+    for (int it = 0; it < RS_IPT; it++) {
+        const int p = t0 + warp * 32 * RS_IPT + it * 32 + lane;
+        const bool ok = p < n;
+        key[it] = ok ? kin[p] : 0u;
+        val[it] = ok ? vin[p] : 0u;
+    }
+#pragma unroll
+    for (int it = 0; it < RS_IPT; it++) {
+        const int p = t0 + warp * 32 * RS_IPT + it * 32 + lane;
+        const bool ok = p < n;
+        const uint32_t d = ok ? ((key[it] >> shift) & mask) : RS_BINS;
+        const unsigned peers = __match_any_sync(FULLS, d);
+        const uint32_t before = ok ? hist[warp][d] : 0u;
+        loc[it] = before + __popc(peers & lt);
+        __syncwarp();
+        if (ok && lane == __ffs(peers) - 1) hist[warp][d] = before + __popc(peers);
+        __syncwarp();
     }
     __syncthreads();
-    {
-        const uint32_t k0 = kA[0];
-        uint32_t d = 0;
-        for (int i = tid; i < n; i += SORT_T) d |= kA[i] ^ k0;
-        d |= __shfl_xor_sync(FULLM, d, 16);
-        d |= __shfl_xor_sync(FULLM, d, 8);
-        d |= __shfl_xor_sync(FULLM, d, 4);
-        d |= __shfl_xor_sync(FULLM, d, 2);
-        d |= __shfl_xor_sync(FULLM, d, 1);
-        if (lane == 0 && d) atomicOr(&sm.diff, d);
+    {  // thread = digit: warp bases inside the tile, offset by the device-wide scan
+        uint32_t run = (uint32_t)offs[(int64_t)threadIdx.x * ntiles + blockIdx.x];
+#pragma unroll
+        for (int w = 0; w < RS_NW; w++) {
+            const uint32_t c = hist[w][threadIdx.x];
+            hist[w][threadIdx.x] = run;
+            run += c;
+        }
     }
     __syncthreads();
-    const uint32_t diff = sm.diff;
-    uint32_t *ks = kA, *vs = vA, *kd = kB, *vd = vB;
-    for (int shift = 0; shift < 32; shift += 8) {
-        if (((diff >> shift) & 255u) == 0) continue;
-        // (1) digit histogram over the whole bucket → exclusive base per digit
-        sm.base[tid] = 0;
-        __syncthreads();
-        for (int i = tid; i < n; i += SORT_T) atomicAdd(&sm.base[(ks[i] >> shift) & 255u], 1u);
-        __syncthreads();
-        {
-            uint32_t tot;
-            const uint32_t c = sm.base[tid];
-            const uint32_t ex = block_excl_scan_256(c, sm.ws, &tot);
-            sm.base[tid] = ex;
+#pragma unroll
+    for (int it = 0; it < RS_IPT; it++) {
+        const int p = t0 + warp * 32 * RS_IPT + it * 32 + lane;
+        if (p < n) {
+            const uint32_t dst = hist[warp][(key[it] >> shift) & mask] + loc[it];
+            kout[dst] = key[it];
+            vout[dst] = val[it];
         }
-        __syncthreads();
-        // (2) tiles in order, stable scatter
-        for (int t0 = 0; t0 < n; t0 += TILE_N) {
-            uint32_t key[SORT_IPT], val[SORT_IPT], loc[SORT_IPT];
-#pragma unroll
-            for (int i = 0; i < 8; i++) sm.hist[warp][lane * 8 + i] = 0;
-            __syncwarp();
-#pragma unroll
-            for (int it = 0; it < SORT_IPT; it++) {
-                const int p = t0 + warp * 32 * SORT_IPT + it * 32 + lane;
-                const bool ok = p < n;
-                key[it] = ok ? ks[p] : 0u;
-                val[it] = ok ? vs[p] : 0u;
-                const uint32_t d = ok ? ((key[it] >> shift) & 255u) : 256u;
-                const unsigned peers = __match_any_sync(FULLM, d);
-                const int leader = __ffs(peers) - 1;
-                const uint32_t before = ok ? sm.hist[warp][d] : 0u;
-                loc[it] = before + __popc(peers & lt);
-                __syncwarp();
-                if (ok && lane == leader) sm.hist[warp][d] = before + __popc(peers);
-                __syncwarp();
-            }
-            __syncthreads();
-            {  // per digit (thread tid = digit): warp offsets inside the tile + running base
-                uint32_t run = sm.base[tid];
-#pragma unroll
-                for (int w = 0; w < NW; w++) {
-                    const uint32_t c = sm.hist[w][tid];
-                    sm.hist[w][tid] = run;
-                    run += c;
-                }
-                sm.base[tid] = run;
-            }
-            __syncthreads();
-#pragma unroll
-            for (int it = 0; it < SORT_IPT; it++) {
-                const int p = t0 + warp * 32 * SORT_IPT + it * 32 + lane;
-                if (p < n) {
-                    const uint32_t d = (key[it] >> shift) & 255u;
-                    const uint32_t dst = sm.hist[warp][d] + loc[it];
-                    kd[dst] = key[it];
-                    vd[dst] = val[it];
-                }
-            }
-            __syncthreads();
-        }
+    }
+}
+
+// Stable LSD sort of (k, v)[0..*n_ptr) on bits [0, bits) with ≤ 8-bit digits.
+// Returns the number of passes; the result is in (k, v) when even, (k2, v2) when odd.
+int radix_sort(uint32_t* k, uint32_t* v, uint32_t* k2, uint32_t* v2, const int* n_ptr, int64_t cap, int bits,
+               int* counts, int* scan_tmp, cudaStream_t s, cudaError_t* err) {
+    const int ntiles = radix_tiles(cap);
+    const int npass = (bits + 7) / 8;
+    const int db = npass ? (bits + npass - 1) / npass : 0;
+    *err = cudaSuccess;
+    if (ntiles == 0) return 0;
+    uint32_t *ks = k, *vs = v, *kd = k2, *vd = v2;
+    for (int pass = 0; pass < npass; pass++) {
+        const int shift = pass * db;
+        const int nb = min(db, bits - shift);
+        k_rs_hist<<<ntiles, RS_T, 0, s>>>(ks, n_ptr, cap, shift, nb, counts, ntiles);
+        if ((*err = scan_exclusive(counts, RS_BINS * ntiles, nullptr, scan_tmp, s)) != cudaSuccess) return pass;
+        k_rs_scatter<<<ntiles, RS_T, 0, s>>>(ks, vs, kd, vd, n_ptr, cap, shift, nb, counts, ntiles);
+        if ((*err = cudaGetLastError()) != cudaSuccess) return pass;
         uint32_t* t = ks; ks = kd; kd = t;
         t = vs; vs = vd; vd = t;
     }
-    if (ks != kA) {
-        for (int i = tid; i < n; i += SORT_T) {
-            kA[i] = ks[i];
-            vA[i] = vs[i];
+    return npass;
+}
+
+// tiles covered by the i-th pair in depth order (0 past Q) → scanned into entry offsets
+__global__ void k_pair_tiles(Launch L, const uint32_t* __restrict__ order, int* __restrict__ ecount) {
+    const int Q = (int)min((int64_t)L.counters[C_Q], L.cap_pairs);
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < L.cap_pairs; i += stride) {
+        int t = 0;
+        if (i < Q) {
+            const float4 r2 = L.rec[3 * (int64_t)order[i] + 2];
+            const uint32_t lo = __float_as_uint(r2.z), hi = __float_as_uint(r2.w);
+            t = (int)(((hi & 0xffff) - (lo & 0xffff)) * ((hi >> 16) - (lo >> 16)));
         }
-        __syncthreads();
+        ecount[i] = t;
     }
-    // ties: equal depth bits ordered by pair index (= gid within the view)
-    bool tie = false;
-    for (int i = tid + 1; i < n; i += SORT_T) tie |= (kA[i] == kA[i - 1]);
-    if (__syncthreads_or(tie)) {
-        for (int i = tid; i < n; i += SORT_T) {
-            const bool head = (i == 0 || kA[i] != kA[i - 1]) && (i + 1 < n && kA[i + 1] == kA[i]);
-            if (!head) continue;
-            int e = i + 1;
-            while (e < n && kA[e] == kA[i]) e++;
-            for (int a = i + 1; a < e; a++) {  // insertion sort of vA[i..e)
-                const uint32_t x = vA[a];
-                int b = a - 1;
-                while (b >= i && vA[b] > x) {
-                    vA[b + 1] = vA[b];
-                    b--;
+}
+
+// duplication in depth order: entry e = ebase[i] + local tile index, key = view·T + tile
+__global__ void k_dup(Launch L, const uint32_t* __restrict__ order, const int* __restrict__ ebase) {
+    const int Q = (int)min((int64_t)L.counters[C_Q], L.cap_pairs);
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < Q; i += stride) {
+        const uint32_t q = order[i];
+        const float4 r2 = L.rec[3 * (int64_t)q + 2];
+        const uint32_t lo = __float_as_uint(r2.z), hi = __float_as_uint(r2.w);
+        const int rx0 = lo & 0xffff, ry0 = lo >> 16, rx1 = hi & 0xffff, ry1 = hi >> 16;
+        if (rx1 <= rx0 || ry1 <= ry0) continue;
+        const uint32_t vbase = (L.meta[q].vf >> 8) * (uint32_t)L.T;
+        int64_t e = ebase[i];
+        for (int ty = ry0; ty < ry1; ty++)
+            for (int tx = rx0; tx < rx1; tx++, e++) {
+                if (e < L.cap_entries) {
+                    L.key[e] = vbase + ty * L.TX + tx;
+                    L.val[e] = q;
+                } else {
+                    L.counters[C_OVERFLOW] = 1;
                 }
-                vA[b + 1] = x;
             }
-        }
-        __syncthreads();
     }
 }
 
-__global__ __launch_bounds__(SORT_T) void k_bucket_sort(Launch L) {
-    __shared__ SortSmem sm;
-    __shared__ uint32_t sk[2][TILE_N], sv[2][TILE_N];
-    const int64_t b = blockIdx.x;
-    const int64_t s = L.bucket_off[b], e = L.bucket_off[b + 1];
-    const int n = (int)(e - s);
-    if (threadIdx.x == 0 && n > 0) atomicMax(&L.counters[C_MAXB], n);
-    if (n <= 1 || e > L.cap_entries) return;
-    uint32_t* gk = L.key + s;
-    uint32_t* gv = L.val + s;
-    if (n <= TILE_N) {
-        for (int i = threadIdx.x; i < n; i += SORT_T) {
-            sk[0][i] = gk[i];
-            sv[0][i] = gv[i];
-        }
-        __syncthreads();
-        bucket_radix_sort(sk[0], sv[0], sk[1], sv[1], n, sm);
-        for (int i = threadIdx.x; i < n; i += SORT_T) gv[i] = sv[0][i];
-    } else {
-        bucket_radix_sort(gk, gv, L.key2 + s, L.val2 + s, n, sm);
-    }
+// longest bucket (statistics)
+__global__ void k_max_bucket(Launch L) {
+    const int64_t nb = (int64_t)L.V * L.T;
+    int m = 0;
+    for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nb; b += (int64_t)gridDim.x * blockDim.x)
+        m = max(m, L.bucket_off[b + 1] - L.bucket_off[b]);
+    for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(FULLS, m, o));
+    if ((threadIdx.x & 31) == 0 && m > 0) atomicMax(&L.counters[C_MAXB], m);
 }
 
-cudaError_t launch_bucket_sort(const Launch& L, cudaStream_t s) {
-    k_bucket_sort<<<L.V * L.T, SORT_T, 0, s>>>(L);
+static int grid_for(int64_t n, int threads) {
+    int dev = 0, nsm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    int64_t b = (n + threads - 1) / threads;
+    return (int)max((int64_t)1, min(b, (int64_t)nsm * 16));
+}
+
+// S4a: pairs by depth.  pkey/pval were written by k_project; result order → *order_out.
+cudaError_t launch_sort_pairs(const Launch& L, const uint32_t** order_out, cudaStream_t s) {
+    cudaError_t e;
+    int np = radix_sort(L.pkey, L.pval, L.pkey2, L.pval2, L.counters + C_Q, L.cap_pairs, 32, L.rs_counts, L.scan_tmp,
+                        s, &e);
+    *order_out = (np & 1) ? L.pval2 : L.pval;
+    return e;
+}
+
+// S3 + S4b: duplicate in depth order, then stable sort by (view, tile).
+cudaError_t launch_dup_sort(const Launch& L, const uint32_t* order, uint32_t** sorted_vals, cudaStream_t s,
+                            bool timing_dup_only) {
+    (void)timing_dup_only;
+    k_pair_tiles<<<grid_for(L.cap_pairs, 256), 256, 0, s>>>(L, order, L.ecount);
+    cudaError_t e = scan_exclusive(L.ecount, (int)L.cap_pairs, nullptr, L.scan_tmp, s);
+    if (e != cudaSuccess) return e;
+    k_dup<<<grid_for(L.cap_pairs, 256), 256, 0, s>>>(L, order, L.ecount);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    return cudaSuccess;
+}
+
+cudaError_t launch_sort_entries(const Launch& L, uint32_t** sorted_vals, cudaStream_t s) {
+    int bits = 1;
+    while ((1ll << bits) < (int64_t)L.V * L.T) bits++;
+    cudaError_t e;
+    int np = radix_sort(L.key, L.val, L.key2, L.val2, L.counters + C_K, L.cap_entries, bits, L.rs_counts, L.scan_tmp,
+                        s, &e);
+    *sorted_vals = (np & 1) ? L.val2 : L.val;
+    if (e != cudaSuccess) return e;
+    k_max_bucket<<<64, 256, 0, s>>>(L);
     return cudaGetLastError();
 }
 

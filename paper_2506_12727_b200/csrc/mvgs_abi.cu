@@ -49,16 +49,46 @@ cudaError_t grow(T*& p, int64_t& cap, int64_t need, int64_t elem_per = 1) {
 }
 
 cudaError_t alloc_pairs(mvgs_ctx* c, int64_t n) {
-    cudaFree(c->d_rec);
-    cudaFree(c->d_meta);
-    cudaFree(c->d_pgrad);
+    cudaFree(c->d_rec); cudaFree(c->d_meta); cudaFree(c->d_pgrad);
+    cudaFree(c->d_pkey); cudaFree(c->d_pval); cudaFree(c->d_pkey2); cudaFree(c->d_pval2); cudaFree(c->d_ecount);
     c->d_rec = nullptr; c->d_meta = nullptr; c->d_pgrad = nullptr;
+    c->d_pkey = c->d_pval = c->d_pkey2 = c->d_pval2 = nullptr;
+    c->d_ecount = nullptr;
     c->cap_pairs = 0;
     cudaError_t e;
     if ((e = cudaMalloc(&c->d_rec, sizeof(float4) * REC_F4 * n)) != cudaSuccess) return e;
     if ((e = cudaMalloc(&c->d_meta, sizeof(PairMeta) * n)) != cudaSuccess) return e;
     if ((e = cudaMalloc(&c->d_pgrad, sizeof(float) * PG_STRIDE * n)) != cudaSuccess) return e;
+    if ((e = cudaMalloc(&c->d_pkey, 4 * n)) != cudaSuccess) return e;
+    if ((e = cudaMalloc(&c->d_pval, 4 * n)) != cudaSuccess) return e;
+    if ((e = cudaMalloc(&c->d_pkey2, 4 * n)) != cudaSuccess) return e;
+    if ((e = cudaMalloc(&c->d_pval2, 4 * n)) != cudaSuccess) return e;
+    if ((e = cudaMalloc(&c->d_ecount, 4 * (n + 1))) != cudaSuccess) return e;
     c->cap_pairs = n;
+    return cudaSuccess;
+}
+
+// radix digit counts and scan scratch sized for the current capacities
+cudaError_t alloc_sort_scratch(mvgs_ctx* c) {
+    const int64_t cap = std::max(c->cap_pairs, c->cap_entries);
+    const int64_t need = radix_counts_size(cap);
+    if (need > c->cap_rs || !c->d_rs) {
+        cudaFree(c->d_rs);
+        c->d_rs = nullptr;
+        c->cap_rs = 0;
+        cudaError_t e = cudaMalloc(&c->d_rs, sizeof(int) * need);
+        if (e != cudaSuccess) return e;
+        c->cap_rs = need;
+    }
+    const int64_t need_scan = scan_tmp_size((int)std::max(need, c->cap_pairs + 1));
+    if (need_scan > c->cap_scan || !c->d_scan) {
+        cudaFree(c->d_scan);
+        c->d_scan = nullptr;
+        c->cap_scan = 0;
+        cudaError_t e = cudaMalloc(&c->d_scan, sizeof(int) * need_scan);
+        if (e != cudaSuccess) return e;
+        c->cap_scan = need_scan;
+    }
     return cudaSuccess;
 }
 
@@ -75,7 +105,8 @@ cudaError_t alloc_entries(mvgs_ctx* c, int64_t n) {
     return cudaSuccess;
 }
 
-enum { ST_COUNT, ST_SCAN_PAIRS, ST_PROJECT, ST_SCAN_BUCKETS, ST_DUP, ST_SORT, ST_FWD, ST_BWD, ST_GAUSS };
+enum { ST_COUNT, ST_SCAN_PAIRS, ST_PROJECT, ST_SCAN_BUCKETS, ST_SORT_PAIRS, ST_DUP, ST_SORT_ENTRIES, ST_FWD, ST_BWD,
+       ST_GAUSS };
 
 cudaEvent_t pool_get(mvgs_ctx* c) {
     if (!c->ev_pool.empty()) {
@@ -116,7 +147,6 @@ void fill_launch(mvgs_ctx* c) {
     L.cap_entries = c->cap_entries;
     L.blk_off = c->d_blk;
     L.bucket_off = c->d_bucket;
-    L.cursor = c->d_cursor;
     L.rec = c->d_rec;
     L.meta = c->d_meta;
     L.pgrad = c->d_pgrad;
@@ -124,6 +154,13 @@ void fill_launch(mvgs_ctx* c) {
     L.val = c->d_val;
     L.key2 = c->d_key2;
     L.val2 = c->d_val2;
+    L.pkey = c->d_pkey;
+    L.pval = c->d_pval;
+    L.pkey2 = c->d_pkey2;
+    L.pval2 = c->d_pval2;
+    L.ecount = c->d_ecount;
+    L.rs_counts = c->d_rs;
+    L.scan_tmp = c->d_scan;
     L.counters = c->d_counters;
     L.counters64 = c->d_counters64;
 }
@@ -150,6 +187,7 @@ mvgs_status mvgs_create(mvgs_ctx** out, int device, int64_t max_pairs, int64_t m
         return MVGS_ERR_INVALID;
     }
     if ((e = alloc_pairs(ctx, max_pairs)) != cudaSuccess || (e = alloc_entries(ctx, max_entries)) != cudaSuccess ||
+        (e = alloc_sort_scratch(ctx)) != cudaSuccess ||
         (e = cudaMalloc(&ctx->d_counters, sizeof(int) * C_NCOUNTERS)) != cudaSuccess ||
         (e = cudaMemset(ctx->d_counters, 0, sizeof(int) * C_NCOUNTERS)) != cudaSuccess ||
         (e = cudaMalloc(&ctx->d_counters64, sizeof(unsigned long long) * 2)) != cudaSuccess ||
@@ -166,9 +204,11 @@ void mvgs_destroy(mvgs_ctx* ctx) {
     if (!ctx) return;
     cudaSetDevice(ctx->device);
     cudaDeviceSynchronize();
-    cudaFree(ctx->d_cams); cudaFree(ctx->d_blk); cudaFree(ctx->d_bucket); cudaFree(ctx->d_cursor);
+    cudaFree(ctx->d_cams); cudaFree(ctx->d_blk); cudaFree(ctx->d_bucket);
     cudaFree(ctx->d_rec); cudaFree(ctx->d_meta); cudaFree(ctx->d_pgrad);
     cudaFree(ctx->d_key); cudaFree(ctx->d_val); cudaFree(ctx->d_key2); cudaFree(ctx->d_val2);
+    cudaFree(ctx->d_pkey); cudaFree(ctx->d_pval); cudaFree(ctx->d_pkey2); cudaFree(ctx->d_pval2);
+    cudaFree(ctx->d_ecount); cudaFree(ctx->d_rs);
     cudaFree(ctx->d_counters); cudaFree(ctx->d_counters64); cudaFree(ctx->d_scan);
     if (ctx->h_cams) cudaFreeHost(ctx->h_cams);
     if (ctx->cams_ev) cudaEventDestroy(ctx->cams_ev);
@@ -190,6 +230,7 @@ mvgs_status mvgs_reserve(mvgs_ctx* ctx, int64_t max_pairs, int64_t max_entries) 
     CK(cudaDeviceSynchronize());
     if (max_pairs > ctx->cap_pairs) CK(alloc_pairs(ctx, max_pairs));
     if (max_entries > ctx->cap_entries) CK(alloc_entries(ctx, max_entries));
+    CK(alloc_sort_scratch(ctx));
     ctx->state = 0;
     return MVGS_OK;
 }
@@ -218,13 +259,17 @@ mvgs_status mvgs_preprocess(mvgs_ctx* ctx, const mvgs_gaussians* g, const mvgs_c
     CK(cudaSetDevice(ctx->device));
     // workspace growth (synchronous only when it grows)
     int64_t need_scan = scan_tmp_size((int)std::max(nblk, nbuck));
-    if (nblk + 1 > ctx->cap_blk || nbuck + 1 > ctx->cap_buckets || V > ctx->cap_cams || need_scan > ctx->cap_scan) {
+    if (nblk + 1 > ctx->cap_blk || nbuck + 1 > ctx->cap_buckets || V > ctx->cap_cams || need_scan > ctx->cap_scan ||
+        !ctx->d_blk) {
         CK(cudaDeviceSynchronize());
         CK(grow(ctx->d_blk, ctx->cap_blk, nblk + 1));
-        int64_t capb = ctx->cap_buckets;
         CK(grow(ctx->d_bucket, ctx->cap_buckets, nbuck + 1));
-        CK(grow(ctx->d_cursor, capb, nbuck + 1));
-        CK(grow(ctx->d_scan, ctx->cap_scan, need_scan));
+        if (need_scan > ctx->cap_scan) {
+            cudaFree(ctx->d_scan);
+            ctx->d_scan = nullptr;
+            ctx->cap_scan = 0;
+            CK(grow(ctx->d_scan, ctx->cap_scan, need_scan));
+        }
         if (V > ctx->cap_cams) {
             cudaFree(ctx->d_cams);
             if (ctx->h_cams) cudaFreeHost(ctx->h_cams);
@@ -263,9 +308,14 @@ mvgs_status mvgs_preprocess(mvgs_ctx* ctx, const mvgs_gaussians* g, const mvgs_c
         CK(cudaMemsetAsync(ctx->d_blk, 0, sizeof(int) * (nblk + 1), s));
     }
     { STAGE(ST_SCAN_BUCKETS); CK(scan_exclusive(ctx->d_bucket, (int)nbuck, ctx->d_counters + C_K, ctx->d_scan, s)); }
-    CK(cudaMemsetAsync(ctx->d_cursor, 0, sizeof(int) * nbuck, s));
-    { STAGE(ST_DUP); CK(launch_dup_scatter(L, s)); }                                                 // S3
-    { STAGE(ST_SORT); CK(launch_bucket_sort(L, s)); }                                                // S4
+    const uint32_t* order = L.pval;
+    uint32_t* sorted = L.val;
+    if (NB > 0) {
+        { STAGE(ST_SORT_PAIRS); CK(launch_sort_pairs(L, &order, s)); }                               // S4a
+        { STAGE(ST_DUP); CK(launch_dup_sort(L, order, &sorted, s, true)); }                          // S3
+        { STAGE(ST_SORT_ENTRIES); CK(launch_sort_entries(L, &sorted, s)); }                          // S4b
+    }
+    L.sorted = sorted;
     ctx->state = 1;
     return MVGS_OK;
 }

@@ -21,8 +21,8 @@ NG = 10
 SYMBOLS = ["mvgs_create", "mvgs_destroy", "mvgs_last_error", "mvgs_reserve", "mvgs_preprocess", "mvgs_render_fwd",
            "mvgs_render_bwd", "mvgs_adc_stats", "mvgs_query", "mvgs_export_lists", "mvgs_export_pairs",
            "mvgs_set_timing", "mvgs_stage_times"]
-STAGE_NAMES = ["count", "scan_pairs", "project", "scan_buckets", "dup_scatter", "sort", "render_fwd", "render_bwd",
-               "gauss_bwd"]
+STAGE_NAMES = ["count", "scan_pairs", "project", "scan_buckets", "sort_pairs", "dup", "sort_entries", "render_fwd",
+               "render_bwd", "gauss_bwd"]
 
 
 class MvgsError(RuntimeError):
