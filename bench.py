@@ -37,10 +37,12 @@ import synth  # noqa: E402
 METRIC = "views/sec fwd+bwd (N-view batch, 1/2/4/8 B200) and % HBM/L2 roofline"
 UNIT = "views/s"
 
-# algorithmic fp32 flops of one (pixel, entry) evaluation, counted from the CA
-# forms of DESIGN.md §4 (FMA = 2): see DESIGN.md §7
-FWD_FLOPS_PER_EVAL = 42
-BWD_FLOPS_PER_EVAL = 96
+# fp32 flops of one (pixel, entry) evaluation, counted from the CA forms of
+# DESIGN.md §4 (FMA = 2): every evaluation pays the offset + power + skip test
+# (13); those above the exact skip bound also pay the rest
+FLOPS_VISIT = 13
+FWD_FLOPS_REST = 29
+BWD_FLOPS_REST = 83
 
 
 def parse():
@@ -119,7 +121,7 @@ def measured_peaks():
     return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
 
 
-def stage_models(P, NK, V, NB, Q, K, T, evf, evb):
+def stage_models(P, NK, V, NB, Q, K, T, evf, evb, exf, exb):
     """(bound, algorithmic units per launch) per stage — DESIGN.md §7."""
     pbytes = 4 * (11 + 3 * NK) * P
     return {
@@ -130,8 +132,8 @@ def stage_models(P, NK, V, NB, Q, K, T, evf, evb):
         "sort_pairs": ("hbm", 4 * 16 * Q),
         "dup": ("hbm", Q * (4 + 16 + 8 + 4 + 4) + 8 * K),
         "sort_entries": ("hbm", ((max(1, (V * T - 1).bit_length()) + 7) // 8) * 16 * K),
-        "render_fwd": ("alu", FWD_FLOPS_PER_EVAL * evf),
-        "render_bwd": ("alu", BWD_FLOPS_PER_EVAL * evb),
+        "render_fwd": ("alu", FLOPS_VISIT * evf + FWD_FLOPS_REST * exf),
+        "render_bwd": ("alu", FLOPS_VISIT * evb + BWD_FLOPS_REST * exb),
         "gauss_bwd": ("hbm", 2 * pbytes + Q * (16 + 8 + 48) + 16 * P),
     }
 
@@ -262,7 +264,8 @@ def run_mvgs(args):
     peaks, peak_src = measured_peaks()
     T = st["tiles_x"] * st["tiles_y"]
     NB = (P + 255) // 256
-    models = stage_models(P, NK, Vr, NB, st["Q"], st["K"], T, st["eval_fwd"], st["eval_bwd"])
+    models = stage_models(P, NK, Vr, NB, st["Q"], st["K"], T, st["eval_fwd"], st["eval_bwd"], st["exp_fwd"],
+                          st["exp_bwd"])
     dom = max(stages, key=lambda k: stages[k])
     bound, units = models[dom]
     t_dom = stages[dom] / 1e3
@@ -295,7 +298,9 @@ def run_mvgs(args):
                                                                        if isinstance(v, np.ndarray)) / 1e6),
                    "Q": st["Q"], "K": st["K"], "max_bucket": st["max_bucket"], "n_visible": st["n_visible"],
                    "eval_fwd_per_px": round(st["eval_fwd"] / (Vr * cfg.W * cfg.H), 2),
-                   "eval_bwd_per_px": round(st["eval_bwd"] / (Vr * cfg.W * cfg.H), 2)},
+                   "eval_bwd_per_px": round(st["eval_bwd"] / (Vr * cfg.W * cfg.H), 2),
+                   "exp_fwd_per_px": round(st["exp_fwd"] / (Vr * cfg.W * cfg.H), 2),
+                   "exp_bwd_per_px": round(st["exp_bwd"] / (Vr * cfg.W * cfg.H), 2)},
         "clocks": clocks,
         "e2e": {"value": round(views_total / (e2e_ms / 1e3), 3), "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": round(e2e_ms, 3)},

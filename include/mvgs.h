@@ -106,6 +106,8 @@ typedef struct {
     int32_t V, tiles_x, tiles_y;
     int64_t eval_fwd;      /* (pixel, entry) evaluations of the last render_fwd (Alg. 2 work) */
     int64_t eval_bwd;      /* (pixel, entry) evaluations of the last render_bwd              */
+    int64_t exp_fwd;       /* of eval_fwd, those above the exact skip bound (G evaluated)    */
+    int64_t exp_bwd;       /* of eval_bwd, likewise                                          */
 } mvgs_stats;
 
 /* Create a context on `device` with initial capacities (0 = a small default).

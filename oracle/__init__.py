@@ -55,6 +55,8 @@ def lib():
         vp, i64 = C.c_void_p, C.c_int64
         L.oracle_create.restype = vp
         L.oracle_create.argtypes = [C.POINTER(_Scene), vp, C.c_int, vp, C.c_int]
+        L.oracle_create_masked.restype = vp
+        L.oracle_create_masked.argtypes = [C.POINTER(_Scene), vp, C.c_int, vp, C.c_int, vp]
         L.oracle_destroy.argtypes = [vp]
         L.oracle_forward.argtypes = [vp]
         L.oracle_backward.argtypes = [vp, vp]
@@ -97,7 +99,7 @@ class Oracle:
     ``forward()`` runs O5; ``backward(dLdC)`` runs O5–O8.
     """
 
-    def __init__(self, g: dict, cams: np.ndarray, bg=(0.0, 0.0, 0.0), flags: int = 0):
+    def __init__(self, g: dict, cams: np.ndarray, bg=(0.0, 0.0, 0.0), flags: int = 0, tile_mask=None):
         self._keep = {k: np.ascontiguousarray(g[k], np.float32)
                       for k in ("means", "log_scales", "quats", "opacity_logits", "sh")}
         self.P = int(self._keep["means"].shape[0])
@@ -112,7 +114,11 @@ class Oracle:
         self.bg = np.ascontiguousarray(bg, np.float32)
         sc = _Scene(self.P, self.sh_degree, self.sh_stride,
                     *[self._keep[k].ctypes.data for k in ("means", "log_scales", "quats", "opacity_logits", "sh")])
-        self._h = lib().oracle_create(C.byref(sc), self.cams.ctypes.data, self.V, _p(self.bg), flags)
+        self.tile_mask = None if tile_mask is None else np.ascontiguousarray(tile_mask, np.uint8).reshape(-1)
+        if self.tile_mask is not None:
+            assert self.tile_mask.size == self.V * self.T
+        self._h = lib().oracle_create_masked(C.byref(sc), self.cams.ctypes.data, self.V, _p(self.bg), flags,
+                                             _p(self.tile_mask))
         if not self._h:
             raise ValueError("oracle_create rejected the input")
         self.K = int(lib().oracle_num_entries(self._h))

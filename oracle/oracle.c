@@ -402,7 +402,9 @@ typedef struct {
     /* backward */
     double *pg;            /* [V*P*NG]                                       */
     int have_bwd;
+    uint8_t *mask;         /* [V*T] tiles to render (NULL = all) — sampled full-size checks */
     uint64_t dhash;        /* hash of every discrete decision (FD tests)     */
+    int64_t npg;           /* number of pairs with fp64 state (= rows of pg)  */
     double *d_means, *d_ls, *d_q, *d_op, *d_sh, *e1, *e2, *eold, *vis;
 } oracle_t;
 
@@ -426,14 +428,36 @@ void oracle_destroy(oracle_t *h)
 {
     if (!h) return;
     free(h->p32); free(h->o32); free(h->g64); free(h->p64); free(h->p64i); free(h->off); free(h->gid);
+    free(h->mask);
     free(h->img); free(h->Tfin); free(h->ncon); free(h->pg);
     free(h->d_means); free(h->d_ls); free(h->d_q); free(h->d_op); free(h->d_sh);
     free(h->e1); free(h->e2); free(h->eold); free(h->vis);
     free(h);
 }
 
+static int rect_hits_mask(const oracle_t *h, int v, const p32_t *p)
+{
+    if (!h->mask) return 1;
+    for (int ty = p->ry0; ty < p->ry1; ty++)
+        for (int tx = p->rx0; tx < p->rx1; tx++)
+            if (h->mask[(int64_t)v * h->T + ty * h->TX + tx]) return 1;
+    return 0;
+}
+
+oracle_t *oracle_create_masked(const og_scene *g, const og_cam *cams, int V, const float bg[3], int flags,
+                               const uint8_t *tile_mask);
+
 /* O1–O4: activations, projection, lists.  Returns NULL on invalid input. */
 oracle_t *oracle_create(const og_scene *g, const og_cam *cams, int V, const float bg[3], int flags)
+{
+    return oracle_create_masked(g, cams, V, bg, flags, NULL);
+}
+
+/* Same, restricted to the (view, tile) buckets with tile_mask[v*T + t] != 0: only
+ * those lists are built and only their pixels are composited (sampled checks at
+ * full size).  Participation, projection and vis are computed for every pair. */
+oracle_t *oracle_create_masked(const og_scene *g, const og_cam *cams, int V, const float bg[3], int flags,
+                               const uint8_t *tile_mask)
 {
     if (!g || !cams || V < 1 || g->sh_degree < 0 || g->sh_degree > 3) return NULL;
     for (int v = 1; v < V; v++)
@@ -449,6 +473,10 @@ oracle_t *oracle_create(const og_scene *g, const og_cam *cams, int V, const floa
     h->TX = (h->W + 15) / 16;
     h->TY = (h->H + 15) / 16;
     h->T = h->TX * h->TY;
+    if (tile_mask) {
+        h->mask = (uint8_t *)malloc((size_t)V * h->T);
+        memcpy(h->mask, tile_mask, (size_t)V * h->T);
+    }
     int64_t P = g->P;
     h->p32 = (p32_t *)calloc((size_t)V * P + 1, sizeof(p32_t));
     h->p64i = (int32_t *)malloc(sizeof(int32_t) * ((size_t)V * P + 1));
@@ -464,11 +492,12 @@ oracle_t *oracle_create(const og_scene *g, const og_cam *cams, int V, const floa
         for (int v = 0; v < V; v++) {
             p32_t *p = &h->p32[(size_t)v * P + i];
             project32(mu, Sig, &cams[v], p);
-            h->p64i[(size_t)v * P + i] = p->vis ? (int32_t)nvis++ : -1;
+            h->p64i[(size_t)v * P + i] = (p->vis && rect_hits_mask(h, v, p)) ? (int32_t)nvis++ : -1;
         }
     }
     /* O2 fp64 values for the visible pairs */
     h->p64 = (p64_t *)calloc((size_t)nvis + 1, sizeof(p64_t));
+    h->npg = nvis;
     for (int v = 0; v < V; v++)
         for (int64_t i = 0; i < P; i++) {
             int32_t k = h->p64i[(size_t)v * P + i];
@@ -482,7 +511,10 @@ oracle_t *oracle_create(const og_scene *g, const og_cam *cams, int V, const floa
             const p32_t *p = &h->p32[(size_t)v * P + i];
             if (!p->vis) continue;
             for (int ty = p->ry0; ty < p->ry1; ty++)
-                for (int tx = p->rx0; tx < p->rx1; tx++) h->off[(int64_t)v * h->T + ty * h->TX + tx + 1]++;
+                for (int tx = p->rx0; tx < p->rx1; tx++) {
+                    int64_t b = (int64_t)v * h->T + ty * h->TX + tx;
+                    if (!h->mask || h->mask[b]) h->off[b + 1]++;
+                }
         }
     for (int64_t b = 0; b < nb; b++) h->off[b + 1] += h->off[b];
     h->K = h->off[nb];
@@ -496,6 +528,7 @@ oracle_t *oracle_create(const og_scene *g, const og_cam *cams, int V, const floa
             for (int ty = p->ry0; ty < p->ry1; ty++)
                 for (int tx = p->rx0; tx < p->rx1; tx++) {
                     int64_t b = (int64_t)v * h->T + ty * h->TX + tx;
+                    if (h->mask && !h->mask[b]) continue;
                     ent[fill[b]].depth_bits = fbits(p->tz);
                     ent[fill[b]].gid = (int32_t)i;
                     fill[b]++;
@@ -536,6 +569,7 @@ static void composite(oracle_t *h, const float *dLdC)
         for (int y = 0; y < H; y++)
             for (int x = 0; x < W; x++) {
                 int64_t b = (int64_t)v * h->T + (y / 16) * h->TX + (x / 16);
+                if (h->mask && !h->mask[b]) continue;
                 /* ---- O5: forward.  Decisions fp32 (CA), values fp64. */
                 float T32 = 1.0f;
                 double T64 = 1.0, Cc[3] = {0, 0, 0};
@@ -592,7 +626,7 @@ static void composite(oracle_t *h, const float *dLdC)
                 for (int k = m - 1; k >= 0; k--) {
                     int32_t i = bl[k].gid;
                     const p64_t *q = &h->p64[h->p64i[(size_t)v * P + i]];
-                    double *pg = &h->pg[((size_t)v * P + i) * NG];
+                    double *pg = &h->pg[(size_t)h->p64i[(size_t)v * P + i] * NG];
                     double aT = bl[k].alpha * bl[k].T;
                     double dLda = 0;
                     for (int ch = 0; ch < 3; ch++) {
@@ -645,8 +679,9 @@ static void gauss_backward(oracle_t *h)
             ap[v].gx = ap[v].gy = ap[v].e1 = 0;
             if (!p->vis) continue;
             visc += 1;
+            if (h->p64i[(size_t)v * P + i] < 0) { present[v] = 0; continue; } /* outside the mask: no pixel */
             const p64_t *q = &h->p64[h->p64i[(size_t)v * P + i]];
-            const double *pg = &h->pg[((size_t)v * P + i) * NG];
+            const double *pg = &h->pg[(size_t)h->p64i[(size_t)v * P + i] * NG];
             const og_cam *cam = &h->cams[v];
             ap[v].gx = pg[0]; ap[v].gy = pg[1]; ap[v].e1 = pg[2];
             double Rv[3][3];
@@ -788,7 +823,7 @@ int oracle_backward(oracle_t *h, const float *dLdC)
     h->img = (double *)calloc(3 * npx, sizeof(double));
     h->Tfin = (double *)calloc(npx, sizeof(double));
     h->ncon = (int32_t *)calloc(npx, sizeof(int32_t));
-    h->pg = (double *)calloc((size_t)h->V * P * NG + 1, sizeof(double));
+    h->pg = (double *)calloc((size_t)h->npg * NG + 1, sizeof(double));
 #define ALLOC(f, n) do { free(h->f); h->f = (double *)calloc((size_t)(n) + 1, sizeof(double)); } while (0)
     ALLOC(d_means, 3 * P); ALLOC(d_ls, 3 * P); ALLOC(d_q, 4 * P); ALLOC(d_op, P);
     ALLOC(d_sh, (size_t)P * h->g.sh_stride * 3);
@@ -850,9 +885,13 @@ void oracle_get_opacity32(const oracle_t *h, float *o)
     memcpy(o, h->o32, sizeof(float) * h->g.P);
 }
 
-void oracle_get_pair_grads(const oracle_t *h, double *out)
+void oracle_get_pair_grads(const oracle_t *h, double *out) /* [V*P*NG], zero where no pair */
 {
-    if (h->have_bwd) memcpy(out, h->pg, sizeof(double) * (size_t)h->V * h->g.P * NG);
+    size_t n = (size_t)h->V * h->g.P;
+    memset(out, 0, sizeof(double) * n * NG);
+    if (!h->have_bwd) return;
+    for (size_t k = 0; k < n; k++)
+        if (h->p64i[k] >= 0) memcpy(out + k * NG, h->pg + (size_t)h->p64i[k] * NG, sizeof(double) * NG);
 }
 
 void oracle_get_grads(const oracle_t *h, double *d_means, double *d_ls, double *d_q, double *d_op,

@@ -41,6 +41,7 @@ struct Launch {  // everything a kernel needs about the current batch
     float* pgrad;     // [cap_pairs * PG_STRIDE]
     uint32_t *key, *val, *key2, *val2;  // [cap_entries] entry (bucket key, pair) ping-pong
     uint32_t *pkey, *pval, *pkey2, *pval2;  // [cap_pairs] pair (depth key, pair) ping-pong
+    uint2 *prect, *prect2;                  // [cap_pairs] packed tile rect carried through the pair sort
     int* ecount;      // [cap_pairs + 1] tiles per depth-ordered pair → entry offsets
     int* rs_counts;   // radix digit × tile counts
     int* scan_tmp;    // scan block sums
@@ -67,6 +68,7 @@ struct mvgs_ctx {
     float* d_pgrad = nullptr;
     uint32_t *d_key = nullptr, *d_val = nullptr, *d_key2 = nullptr, *d_val2 = nullptr;
     uint32_t *d_pkey = nullptr, *d_pval = nullptr, *d_pkey2 = nullptr, *d_pval2 = nullptr;
+    uint2 *d_prect = nullptr, *d_prect2 = nullptr;
     int* d_ecount = nullptr;
     int* d_rs = nullptr;
     int64_t cap_rs = 0;
@@ -87,9 +89,8 @@ namespace mvgs {
 cudaError_t scan_exclusive(int* a, int n, int* total_slot, int* tmp, cudaStream_t s);
 cudaError_t launch_count(const Launch& L, cudaStream_t s);
 cudaError_t launch_project(const Launch& L, cudaStream_t s);
-cudaError_t launch_sort_pairs(const Launch& L, const uint32_t** order_out, cudaStream_t s);
-cudaError_t launch_dup_sort(const Launch& L, const uint32_t* order, uint32_t** sorted_vals, cudaStream_t s,
-                            bool timing_dup_only);
+cudaError_t launch_sort_pairs(const Launch& L, const uint32_t** order_out, const uint2** rect_out, cudaStream_t s);
+cudaError_t launch_dup_sort(const Launch& L, const uint32_t* order, const uint2* rect, cudaStream_t s);
 cudaError_t launch_sort_entries(const Launch& L, uint32_t** sorted_vals, cudaStream_t s);
 int64_t radix_counts_size(int64_t cap);
 int radix_tiles(int64_t cap);

@@ -230,9 +230,12 @@ __global__ __launch_bounds__(BLK) void k_project(Launch L) {
             Proj p;
             ca_project(c, mx, my, mz, a.Sig, L.TX, L.TY, p);
             const int tiles = p.ok ? (p.rx1 - p.rx0) * (p.ry1 - p.ry0) : 0;
-            if (pair < L.cap_pairs) {  // depth key for the pair sort (inert pairs sort last)
+            if (pair < L.cap_pairs) {  // depth key + rect for the pair sort (inert pairs sort last)
                 L.pkey[pair] = tiles > 0 ? __float_as_uint(p.tz) : 0xffffffffu;
                 L.pval[pair] = (uint32_t)pair;
+                L.prect[pair] = tiles > 0 ? make_uint2((uint32_t)p.rx0 | ((uint32_t)p.ry0 << 16),
+                                                       (uint32_t)p.rx1 | ((uint32_t)p.ry1 << 16))
+                                          : make_uint2(0u, 0u);
             }
             if (pair >= L.cap_pairs) {
                 L.counters[C_OVERFLOW] = 1;

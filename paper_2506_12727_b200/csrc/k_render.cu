@@ -23,19 +23,34 @@ namespace mvgs {
 constexpr int RT = 256;
 constexpr unsigned FULLR = 0xffffffffu;
 
-// CTA-wide sum of a per-thread count → one 64-bit atomic per CTA.
-__device__ __forceinline__ void count_evals(unsigned long long* ctr, unsigned n, unsigned* sm) {
+// CTA-wide sums of two per-thread counts → one 64-bit atomic each per CTA.
+__device__ __forceinline__ void count_evals(unsigned long long* ctr0, unsigned long long* ctr1, unsigned n0,
+                                            unsigned n1, unsigned* sm) {
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) n += __shfl_xor_sync(FULLR, n, o);
-    if ((threadIdx.x & 31) == 0) atomicAdd(sm, n);
+    for (int o = 16; o > 0; o >>= 1) {
+        n0 += __shfl_xor_sync(FULLR, n0, o);
+        n1 += __shfl_xor_sync(FULLR, n1, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicAdd(sm, n0);
+        atomicAdd(sm + 1, n1);
+    }
     __syncthreads();
-    if (threadIdx.x == 0) atomicAdd(ctr, (unsigned long long)*sm);
+    if (threadIdx.x == 0) {
+        atomicAdd(ctr0, (unsigned long long)sm[0]);
+        atomicAdd(ctr1, (unsigned long long)sm[1]);
+    }
 }
+
+// Exact early skip: α = min(0.99, o·G) < 1/255 ⇔ power < −ln(255·o).
+// Below −ln(255·o) − SKIP_MARGIN the CA value o·G is < (1/255)·e^(−1e-3)·(1 + 1e-6),
+// so the CA decision is "skip" as well; the CA exp is only evaluated above this bound.
+constexpr float SKIP_MARGIN = 1e-3f;
+__device__ __forceinline__ float skip_power(float o) { return -logf(255.0f * o) - SKIP_MARGIN; }
 
 __global__ __launch_bounds__(RT) void k_render_fwd(Launch L, float* __restrict__ out_rgb, float* __restrict__ out_T,
                                                    int32_t* __restrict__ out_n) {
-    __shared__ float4 s0[RT], s1[RT];
-    __shared__ float s2[RT];
+    __shared__ float4 s0[RT], s1[RT], s2[RT];  // (x, y, A, B) (C, o, skip bound, -) (r, g, b, -)
     const int bucket = blockIdx.x;
     const int v = bucket / L.T, tile = bucket - v * L.T;
     const int ty = tile / L.TX, tx = tile - ty * L.TX;
@@ -45,9 +60,9 @@ __global__ __launch_bounds__(RT) void k_render_fwd(Launch L, float* __restrict__
     const float fx = (float)x, fy = (float)y;
     float T = 1.0f, C0 = 0.f, C1 = 0.f, C2 = 0.f;
     int last = 0;
-    unsigned nev = 0;
-    __shared__ unsigned sev;
-    if (threadIdx.x == 0) sev = 0;
+    unsigned nev = 0, nexp = 0;
+    __shared__ unsigned sev[2];
+    if (threadIdx.x == 0) sev[0] = sev[1] = 0;
     __syncthreads();
     bool done = !inside;
     if (end <= L.cap_entries) {
@@ -57,19 +72,21 @@ __global__ __launch_bounds__(RT) void k_render_fwd(Launch L, float* __restrict__
             if (idx < end) {
                 const uint32_t q = L.sorted[idx];
                 const float4* r = L.rec + 3 * (int64_t)q;
-                s0[threadIdx.x] = r[0];
-                s1[threadIdx.x] = r[1];
-                s2[threadIdx.x] = r[2].x;
+                const float4 r0 = r[0], r1 = r[1], r2 = r[2];
+                s0[threadIdx.x] = r0;
+                s1[threadIdx.x] = make_float4(r1.x, r1.y, skip_power(r1.y), 0.f);
+                s2[threadIdx.x] = make_float4(r1.z, r1.w, r2.x, 0.f);
             }
             __syncthreads();
             const int cnt = min(RT, end - b0);
             for (int j = 0; j < cnt && !done; j++) {
                 nev++;
                 const float4 a = s0[j];
-                const float dx = FSUB(a.x, fx), dy = FSUB(a.y, fy);
-                const float power = ca_power(a.z, a.w, s1[j].x, dx, dy);
-                if (power > 0.0f) continue;
                 const float4 c = s1[j];
+                const float dx = FSUB(a.x, fx), dy = FSUB(a.y, fy);
+                const float power = ca_power(a.z, a.w, c.x, dx, dy);
+                if (power > 0.0f || power < c.z) continue;
+                nexp++;
                 const float G = ca_exp(power);
                 const float alpha = fminf(ALPHA_MAX, FMUL(c.y, G));
                 if (alpha < ALPHA_MIN) continue;
@@ -79,15 +96,16 @@ __global__ __launch_bounds__(RT) void k_render_fwd(Launch L, float* __restrict__
                     break;
                 }
                 const float w = alpha * T;
-                C0 += c.z * w;
-                C1 += c.w * w;
-                C2 += s2[j] * w;
+                const float4 col = s2[j];
+                C0 += col.x * w;
+                C1 += col.y * w;
+                C2 += col.z * w;
                 T = Tn;
                 last = b0 - start + j + 1;
             }
         }
     }
-    count_evals(&L.counters64[0], nev, &sev);
+    count_evals(&L.counters64[0], &L.counters64[2], nev, nexp, sev);
     if (inside) {
         const int64_t HW = (int64_t)L.H * L.W, pix = (int64_t)y * L.W + x;
         out_rgb[(3 * (int64_t)v + 0) * HW + pix] = C0 + T * L.bg[0];
@@ -136,12 +154,11 @@ __device__ __forceinline__ int reduce_id(int lane) {
 
 __global__ __launch_bounds__(RT) void k_render_bwd(Launch L, const float* __restrict__ dL_drgb,
                                                    const float* __restrict__ in_T, const int32_t* __restrict__ in_n) {
-    __shared__ float4 s0[RT], s1[RT];
-    __shared__ float s2[RT];
+    __shared__ float4 s0[RT], s1[RT], s2[RT];  // as in the forward
     __shared__ uint32_t sq[RT];
     __shared__ float sacc[RT * NG];
     __shared__ int smax;
-    __shared__ unsigned sev;
+    __shared__ unsigned sev[2];
     const int lane = threadIdx.x & 31;
     const int bucket = blockIdx.x;
     const int v = bucket / L.T, tile = bucket - v * L.T;
@@ -162,10 +179,11 @@ __global__ __launch_bounds__(RT) void k_render_bwd(Launch L, const float* __rest
     }
     if (threadIdx.x == 0) {
         smax = 0;
-        sev = 0;
+        sev[0] = sev[1] = 0;
     }
     __syncthreads();
     const unsigned nev = (unsigned)last;  // entries this pixel walks back over
+    unsigned nexp = 0;
     if (last > 0) atomicMax(&smax, last);
     __syncthreads();
     const int maxlast = smax;
@@ -185,10 +203,11 @@ __global__ __launch_bounds__(RT) void k_render_bwd(Launch L, const float* __rest
         if (threadIdx.x < cnt) {
             const uint32_t q = L.sorted[start + b0 + threadIdx.x];
             const float4* r = L.rec + 3 * (int64_t)q;
+            const float4 r0 = r[0], r1 = r[1], r2 = r[2];
             sq[threadIdx.x] = q;
-            s0[threadIdx.x] = r[0];
-            s1[threadIdx.x] = r[1];
-            s2[threadIdx.x] = r[2].x;
+            s0[threadIdx.x] = r0;
+            s1[threadIdx.x] = make_float4(r1.x, r1.y, skip_power(r1.y), 0.f);
+            s2[threadIdx.x] = make_float4(r1.z, r1.w, r2.x, 0.f);
         }
         for (int i = threadIdx.x; i < RT * NG; i += RT) sacc[i] = 0.f;
         __syncthreads();
@@ -203,7 +222,8 @@ __global__ __launch_bounds__(RT) void k_render_bwd(Launch L, const float* __rest
                 const float4 c = s1[jj];
                 const float dx = FSUB(a.x, fx), dy = FSUB(a.y, fy);
                 const float power = ca_power(a.z, a.w, c.x, dx, dy);
-                if (power <= 0.0f) {
+                if (power <= 0.0f && power >= c.z) {
+                    nexp++;
                     const float G = ca_exp(power);
                     const float oG = FMUL(c.y, G);
                     const float alpha = fminf(ALPHA_MAX, oG);
@@ -213,14 +233,14 @@ __global__ __launch_bounds__(RT) void k_render_bwd(Launch L, const float* __rest
                         const float inv_one_m = __fdividef(1.0f, one_m);
                         T = T * inv_one_m;
                         const float w = alpha * T;
-                        const float cb = s2[jj];
+                        const float4 col = s2[jj];
                         acc0 = a_prev * c0p + (1.f - a_prev) * acc0;
                         acc1 = a_prev * c1p + (1.f - a_prev) * acc1;
                         acc2 = a_prev * c2p + (1.f - a_prev) * acc2;
-                        float dLda = (c.z - acc0) * dL0 + (c.w - acc1) * dL1 + (cb - acc2) * dL2;
+                        float dLda = (col.x - acc0) * dL0 + (col.y - acc1) * dL1 + (col.z - acc2) * dL2;
                         dLda = dLda * T - T_fin * inv_one_m * dL_bg;
                         a_prev = alpha;
-                        c0p = c.z; c1p = c.w; c2p = cb;
+                        c0p = col.x; c1p = col.y; c2p = col.z;
                         const bool clamped = oG > ALPHA_MAX;
                         const float dLdG = clamped ? 0.f : c.y * dLda;
                         const float dLdo = clamped ? 0.f : G * dLda;
@@ -255,7 +275,7 @@ __global__ __launch_bounds__(RT) void k_render_bwd(Launch L, const float* __rest
             }
         }
     }
-    count_evals(&L.counters64[1], nev, &sev);
+    count_evals(&L.counters64[1], &L.counters64[3], nev, nexp, sev);
 }
 
 cudaError_t launch_render_bwd(const Launch& L, const float* dL, const float* Tf, const int32_t* nc, cudaStream_t s) {

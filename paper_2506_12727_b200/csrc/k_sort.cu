@@ -4,16 +4,16 @@
 // and sorts the 64-bit keys.  Here the same total order (view, tile, depth,
 // gid) (R9, R10) is produced with two short stable LSD radix sorts and no
 // atomics:
-//   1. sort the pairs by depth bits (4 × 8-bit passes over Q pairs, Q ≪ K);
-//      pairs start in (view, gid) order and the sort is stable, so equal
-//      depths stay in gid order;
+//   1. sort the pairs by depth bits (4 × 8-bit passes over Q pairs, Q ≪ K),
+//      carrying each pair's packed tile rect; pairs start in (view, gid) order
+//      and the sort is stable, so equal depths stay in gid order;
 //   2. duplicate: walk the pairs in that order and write one entry per covered
 //      tile, key = view·T + tile (positions from an exclusive scan of the
 //      per-pair tile counts — coalesced, deterministic);
 //   3. stable sort the K entries by the bucket key only (⌈log2(V·T)⌉ bits,
 //      8-bit digits).  Stability keeps each bucket in (depth, gid) order.
 // Every pass is an "on-chip" radix pass: a CTA ranks a 2048-key tile in shared
-// memory (warp __match_any_sync + per-warp digit counters, stable by
+// memory (warp multisplit by 8 ballots + per-warp digit counters, stable by
 // position), digit×tile counts are scanned device-wide, and the tile scatters
 // straight to its final positions.  Sizes (Q, K) live on the device; grids are
 // sized by capacity and tiles beyond the live count exit.
@@ -43,9 +43,26 @@ __global__ __launch_bounds__(RS_T) void k_rs_hist(const uint32_t* __restrict__ k
     counts[(int64_t)threadIdx.x * ntiles + blockIdx.x] = h[threadIdx.x];
 }
 
-// stable scatter of one tile to offsets[digit * ntiles + tile] + rank
+// Warp multisplit ranking: lanes holding the same digit found with 8 ballots
+// (one per digit bit) instead of __match_any_sync, whose cost grows with the
+// number of distinct digits in the warp.
+__device__ __forceinline__ unsigned digit_peers(uint32_t d, bool ok) {
+    unsigned peers = __ballot_sync(FULLS, ok);
+#pragma unroll
+    for (int b = 0; b < 8; b++) {
+        const bool bit = (d >> b) & 1u;
+        const unsigned bal = __ballot_sync(FULLS, bit);
+        peers &= bit ? bal : ~bal;
+    }
+    return peers;
+}
+
+// stable scatter of one tile to offsets[digit * ntiles + tile] + rank; optionally
+// moves a 64-bit payload with each key
+template <bool PAYLOAD>
 __global__ __launch_bounds__(RS_T) void k_rs_scatter(const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin,
                                                      uint32_t* __restrict__ kout, uint32_t* __restrict__ vout,
+                                                     const uint2* __restrict__ pin, uint2* __restrict__ pout,
                                                      const int* __restrict__ n_ptr, int64_t cap, int shift, int nbits,
                                                      const int* __restrict__ offs, int ntiles) {
     __shared__ uint32_t hist[RS_NW][RS_BINS];
@@ -56,22 +73,24 @@ __global__ __launch_bounds__(RS_T) void k_rs_scatter(const uint32_t* __restrict_
     if (t0 >= n) return;
     const uint32_t mask = (1u << nbits) - 1u;
 #pragma unroll
-    for (int i = 0; i < RS_BINS / 32; i++) hist[warp][lane * (RS_BINS / 32) + i] = 0;
+    for (int i = 0; i < RS_BINS / 32; i++) hist[warp][lane + 32 * i] = 0;
     __syncwarp();
     uint32_t key[RS_IPT], val[RS_IPT], loc[RS_IPT];
+    uint2 pay[PAYLOAD ? RS_IPT : 1];
 #pragma unroll
     for (int it = 0; it < RS_IPT; it++) {
         const int p = t0 + warp * 32 * RS_IPT + it * 32 + lane;
         const bool ok = p < n;
         key[it] = ok ? kin[p] : 0u;
         val[it] = ok ? vin[p] : 0u;
+        if (PAYLOAD) pay[PAYLOAD ? it : 0] = ok ? pin[p] : make_uint2(0u, 0u);
     }
 #pragma unroll
     for (int it = 0; it < RS_IPT; it++) {
         const int p = t0 + warp * 32 * RS_IPT + it * 32 + lane;
         const bool ok = p < n;
-        const uint32_t d = ok ? ((key[it] >> shift) & mask) : RS_BINS;
-        const unsigned peers = __match_any_sync(FULLS, d);
+        const uint32_t d = (key[it] >> shift) & mask;
+        const unsigned peers = digit_peers(d, ok);
         const uint32_t before = ok ? hist[warp][d] : 0u;
         loc[it] = before + __popc(peers & lt);
         __syncwarp();
@@ -96,59 +115,77 @@ __global__ __launch_bounds__(RS_T) void k_rs_scatter(const uint32_t* __restrict_
             const uint32_t dst = hist[warp][(key[it] >> shift) & mask] + loc[it];
             kout[dst] = key[it];
             vout[dst] = val[it];
+            if (PAYLOAD) pout[dst] = pay[PAYLOAD ? it : 0];
         }
     }
 }
 
-// Stable LSD sort of (k, v)[0..*n_ptr) on bits [0, bits) with ≤ 8-bit digits.
-// Returns the number of passes; the result is in (k, v) when even, (k2, v2) when odd.
-int radix_sort(uint32_t* k, uint32_t* v, uint32_t* k2, uint32_t* v2, const int* n_ptr, int64_t cap, int bits,
-               int* counts, int* scan_tmp, cudaStream_t s, cudaError_t* err) {
+// Stable LSD sort of (k, v[, payload])[0..*n_ptr) on bits [0, bits) with ≤ 8-bit
+// digits.  Returns the number of passes; the result is in the first buffers when
+// even, in the second ones when odd.
+int radix_sort(uint32_t* k, uint32_t* v, uint32_t* k2, uint32_t* v2, uint2* pl, uint2* pl2, const int* n_ptr,
+               int64_t cap, int bits, int* counts, int* scan_tmp, cudaStream_t s, cudaError_t* err) {
     const int ntiles = radix_tiles(cap);
     const int npass = (bits + 7) / 8;
     const int db = npass ? (bits + npass - 1) / npass : 0;
     *err = cudaSuccess;
     if (ntiles == 0) return 0;
     uint32_t *ks = k, *vs = v, *kd = k2, *vd = v2;
+    uint2 *ps = pl, *pd = pl2;
     for (int pass = 0; pass < npass; pass++) {
         const int shift = pass * db;
         const int nb = min(db, bits - shift);
         k_rs_hist<<<ntiles, RS_T, 0, s>>>(ks, n_ptr, cap, shift, nb, counts, ntiles);
         if ((*err = scan_exclusive(counts, RS_BINS * ntiles, nullptr, scan_tmp, s)) != cudaSuccess) return pass;
-        k_rs_scatter<<<ntiles, RS_T, 0, s>>>(ks, vs, kd, vd, n_ptr, cap, shift, nb, counts, ntiles);
+        if (pl)
+            k_rs_scatter<true><<<ntiles, RS_T, 0, s>>>(ks, vs, kd, vd, ps, pd, n_ptr, cap, shift, nb, counts, ntiles);
+        else
+            k_rs_scatter<false><<<ntiles, RS_T, 0, s>>>(ks, vs, kd, vd, nullptr, nullptr, n_ptr, cap, shift, nb,
+                                                        counts, ntiles);
         if ((*err = cudaGetLastError()) != cudaSuccess) return pass;
         uint32_t* t = ks; ks = kd; kd = t;
         t = vs; vs = vd; vd = t;
+        uint2* tp = ps; ps = pd; pd = tp;
     }
     return npass;
 }
 
+// view of a pair from the view-major pair offsets (blk_off[v·NB] = first pair of view v)
+__device__ __forceinline__ int view_of_pair(const Launch& L, uint32_t q) {
+    int lo = 0, hi = L.V - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if ((uint32_t)L.blk_off[(int64_t)mid * L.NB] <= q) lo = mid;
+        else hi = mid - 1;
+    }
+    return lo;
+}
+
 // tiles covered by the i-th pair in depth order (0 past Q) → scanned into entry offsets
-__global__ void k_pair_tiles(Launch L, const uint32_t* __restrict__ order, int* __restrict__ ecount) {
+__global__ void k_pair_tiles(Launch L, const uint2* __restrict__ rect, int* __restrict__ ecount) {
     const int Q = (int)min((int64_t)L.counters[C_Q], L.cap_pairs);
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < L.cap_pairs; i += stride) {
         int t = 0;
         if (i < Q) {
-            const float4 r2 = L.rec[3 * (int64_t)order[i] + 2];
-            const uint32_t lo = __float_as_uint(r2.z), hi = __float_as_uint(r2.w);
-            t = (int)(((hi & 0xffff) - (lo & 0xffff)) * ((hi >> 16) - (lo >> 16)));
+            const uint2 r = rect[i];
+            t = (int)(((r.y & 0xffff) - (r.x & 0xffff)) * ((r.y >> 16) - (r.x >> 16)));
         }
         ecount[i] = t;
     }
 }
 
 // duplication in depth order: entry e = ebase[i] + local tile index, key = view·T + tile
-__global__ void k_dup(Launch L, const uint32_t* __restrict__ order, const int* __restrict__ ebase) {
+__global__ void k_dup(Launch L, const uint32_t* __restrict__ order, const uint2* __restrict__ rect,
+                      const int* __restrict__ ebase) {
     const int Q = (int)min((int64_t)L.counters[C_Q], L.cap_pairs);
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < Q; i += stride) {
-        const uint32_t q = order[i];
-        const float4 r2 = L.rec[3 * (int64_t)q + 2];
-        const uint32_t lo = __float_as_uint(r2.z), hi = __float_as_uint(r2.w);
-        const int rx0 = lo & 0xffff, ry0 = lo >> 16, rx1 = hi & 0xffff, ry1 = hi >> 16;
+        const uint2 r = rect[i];
+        const int rx0 = r.x & 0xffff, ry0 = r.x >> 16, rx1 = r.y & 0xffff, ry1 = r.y >> 16;
         if (rx1 <= rx0 || ry1 <= ry0) continue;
-        const uint32_t vbase = (L.meta[q].vf >> 8) * (uint32_t)L.T;
+        const uint32_t q = order[i];
+        const uint32_t vbase = (uint32_t)view_of_pair(L, q) * (uint32_t)L.T;
         int64_t e = ebase[i];
         for (int ty = ry0; ty < ry1; ty++)
             for (int tx = rx0; tx < rx1; tx++, e++) {
@@ -180,23 +217,23 @@ static int grid_for(int64_t n, int threads) {
     return (int)max((int64_t)1, min(b, (int64_t)nsm * 16));
 }
 
-// S4a: pairs by depth.  pkey/pval were written by k_project; result order → *order_out.
-cudaError_t launch_sort_pairs(const Launch& L, const uint32_t** order_out, cudaStream_t s) {
+// S4a: pairs by depth, carrying each pair's packed tile rect.  pkey/pval/prect were
+// written by k_project; the depth order and the rects in that order → *order_out, *rect_out.
+cudaError_t launch_sort_pairs(const Launch& L, const uint32_t** order_out, const uint2** rect_out, cudaStream_t s) {
     cudaError_t e;
-    int np = radix_sort(L.pkey, L.pval, L.pkey2, L.pval2, L.counters + C_Q, L.cap_pairs, 32, L.rs_counts, L.scan_tmp,
-                        s, &e);
+    int np = radix_sort(L.pkey, L.pval, L.pkey2, L.pval2, L.prect, L.prect2, L.counters + C_Q, L.cap_pairs, 32,
+                        L.rs_counts, L.scan_tmp, s, &e);
     *order_out = (np & 1) ? L.pval2 : L.pval;
+    *rect_out = (np & 1) ? L.prect2 : L.prect;
     return e;
 }
 
-// S3 + S4b: duplicate in depth order, then stable sort by (view, tile).
-cudaError_t launch_dup_sort(const Launch& L, const uint32_t* order, uint32_t** sorted_vals, cudaStream_t s,
-                            bool timing_dup_only) {
-    (void)timing_dup_only;
-    k_pair_tiles<<<grid_for(L.cap_pairs, 256), 256, 0, s>>>(L, order, L.ecount);
+// S3: duplicate in depth order (entry offsets from a scan of the tile counts).
+cudaError_t launch_dup_sort(const Launch& L, const uint32_t* order, const uint2* rect, cudaStream_t s) {
+    k_pair_tiles<<<grid_for(L.cap_pairs, 256), 256, 0, s>>>(L, rect, L.ecount);
     cudaError_t e = scan_exclusive(L.ecount, (int)L.cap_pairs, nullptr, L.scan_tmp, s);
     if (e != cudaSuccess) return e;
-    k_dup<<<grid_for(L.cap_pairs, 256), 256, 0, s>>>(L, order, L.ecount);
+    k_dup<<<grid_for(L.cap_pairs, 256), 256, 0, s>>>(L, order, rect, L.ecount);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     return cudaSuccess;
 }
@@ -205,8 +242,8 @@ cudaError_t launch_sort_entries(const Launch& L, uint32_t** sorted_vals, cudaStr
     int bits = 1;
     while ((1ll << bits) < (int64_t)L.V * L.T) bits++;
     cudaError_t e;
-    int np = radix_sort(L.key, L.val, L.key2, L.val2, L.counters + C_K, L.cap_entries, bits, L.rs_counts, L.scan_tmp,
-                        s, &e);
+    int np = radix_sort(L.key, L.val, L.key2, L.val2, nullptr, nullptr, L.counters + C_K, L.cap_entries, bits,
+                        L.rs_counts, L.scan_tmp, s, &e);
     *sorted_vals = (np & 1) ? L.val2 : L.val;
     if (e != cudaSuccess) return e;
     k_max_bucket<<<64, 256, 0, s>>>(L);

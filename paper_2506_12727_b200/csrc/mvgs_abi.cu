@@ -51,6 +51,8 @@ cudaError_t grow(T*& p, int64_t& cap, int64_t need, int64_t elem_per = 1) {
 cudaError_t alloc_pairs(mvgs_ctx* c, int64_t n) {
     cudaFree(c->d_rec); cudaFree(c->d_meta); cudaFree(c->d_pgrad);
     cudaFree(c->d_pkey); cudaFree(c->d_pval); cudaFree(c->d_pkey2); cudaFree(c->d_pval2); cudaFree(c->d_ecount);
+    cudaFree(c->d_prect); cudaFree(c->d_prect2);
+    c->d_prect = c->d_prect2 = nullptr;
     c->d_rec = nullptr; c->d_meta = nullptr; c->d_pgrad = nullptr;
     c->d_pkey = c->d_pval = c->d_pkey2 = c->d_pval2 = nullptr;
     c->d_ecount = nullptr;
@@ -64,6 +66,8 @@ cudaError_t alloc_pairs(mvgs_ctx* c, int64_t n) {
     if ((e = cudaMalloc(&c->d_pkey2, 4 * n)) != cudaSuccess) return e;
     if ((e = cudaMalloc(&c->d_pval2, 4 * n)) != cudaSuccess) return e;
     if ((e = cudaMalloc(&c->d_ecount, 4 * (n + 1))) != cudaSuccess) return e;
+    if ((e = cudaMalloc(&c->d_prect, sizeof(uint2) * n)) != cudaSuccess) return e;
+    if ((e = cudaMalloc(&c->d_prect2, sizeof(uint2) * n)) != cudaSuccess) return e;
     c->cap_pairs = n;
     return cudaSuccess;
 }
@@ -158,6 +162,8 @@ void fill_launch(mvgs_ctx* c) {
     L.pval = c->d_pval;
     L.pkey2 = c->d_pkey2;
     L.pval2 = c->d_pval2;
+    L.prect = c->d_prect;
+    L.prect2 = c->d_prect2;
     L.ecount = c->d_ecount;
     L.rs_counts = c->d_rs;
     L.scan_tmp = c->d_scan;
@@ -190,8 +196,8 @@ mvgs_status mvgs_create(mvgs_ctx** out, int device, int64_t max_pairs, int64_t m
         (e = alloc_sort_scratch(ctx)) != cudaSuccess ||
         (e = cudaMalloc(&ctx->d_counters, sizeof(int) * C_NCOUNTERS)) != cudaSuccess ||
         (e = cudaMemset(ctx->d_counters, 0, sizeof(int) * C_NCOUNTERS)) != cudaSuccess ||
-        (e = cudaMalloc(&ctx->d_counters64, sizeof(unsigned long long) * 2)) != cudaSuccess ||
-        (e = cudaMemset(ctx->d_counters64, 0, sizeof(unsigned long long) * 2)) != cudaSuccess ||
+        (e = cudaMalloc(&ctx->d_counters64, sizeof(unsigned long long) * 4)) != cudaSuccess ||
+        (e = cudaMemset(ctx->d_counters64, 0, sizeof(unsigned long long) * 4)) != cudaSuccess ||
         (e = cudaEventCreateWithFlags(&ctx->cams_ev, cudaEventDisableTiming)) != cudaSuccess) {
         mvgs_destroy(ctx);
         return MVGS_ERR_CUDA;
@@ -208,7 +214,7 @@ void mvgs_destroy(mvgs_ctx* ctx) {
     cudaFree(ctx->d_rec); cudaFree(ctx->d_meta); cudaFree(ctx->d_pgrad);
     cudaFree(ctx->d_key); cudaFree(ctx->d_val); cudaFree(ctx->d_key2); cudaFree(ctx->d_val2);
     cudaFree(ctx->d_pkey); cudaFree(ctx->d_pval); cudaFree(ctx->d_pkey2); cudaFree(ctx->d_pval2);
-    cudaFree(ctx->d_ecount); cudaFree(ctx->d_rs);
+    cudaFree(ctx->d_ecount); cudaFree(ctx->d_rs); cudaFree(ctx->d_prect); cudaFree(ctx->d_prect2);
     cudaFree(ctx->d_counters); cudaFree(ctx->d_counters64); cudaFree(ctx->d_scan);
     if (ctx->h_cams) cudaFreeHost(ctx->h_cams);
     if (ctx->cams_ev) cudaEventDestroy(ctx->cams_ev);
@@ -309,10 +315,11 @@ mvgs_status mvgs_preprocess(mvgs_ctx* ctx, const mvgs_gaussians* g, const mvgs_c
     }
     { STAGE(ST_SCAN_BUCKETS); CK(scan_exclusive(ctx->d_bucket, (int)nbuck, ctx->d_counters + C_K, ctx->d_scan, s)); }
     const uint32_t* order = L.pval;
+    const uint2* rect = L.prect;
     uint32_t* sorted = L.val;
     if (NB > 0) {
-        { STAGE(ST_SORT_PAIRS); CK(launch_sort_pairs(L, &order, s)); }                               // S4a
-        { STAGE(ST_DUP); CK(launch_dup_sort(L, order, &sorted, s, true)); }                          // S3
+        { STAGE(ST_SORT_PAIRS); CK(launch_sort_pairs(L, &order, &rect, s)); }                        // S4a
+        { STAGE(ST_DUP); CK(launch_dup_sort(L, order, rect, s)); }                                   // S3
         { STAGE(ST_SORT_ENTRIES); CK(launch_sort_entries(L, &sorted, s)); }                          // S4b
     }
     L.sorted = sorted;
@@ -328,6 +335,7 @@ mvgs_status mvgs_render_fwd(mvgs_ctx* ctx, float* rgb, float* T_final, int32_t* 
     ctx->last_stream = (cudaStream_t)stream;
     cudaStream_t s = (cudaStream_t)stream;
     CK(cudaMemsetAsync(ctx->d_counters64, 0, sizeof(unsigned long long), s));
+    CK(cudaMemsetAsync(ctx->d_counters64 + 2, 0, sizeof(unsigned long long), s));
     { STAGE(ST_FWD); CK(launch_render_fwd(ctx->L, rgb, T_final, n_contrib, s)); }  // S6
     ctx->state = 2;
     return MVGS_OK;
@@ -342,6 +350,7 @@ mvgs_status mvgs_render_bwd(mvgs_ctx* ctx, const float* dL_drgb, const float* T_
     ctx->last_stream = (cudaStream_t)stream;
     cudaStream_t s = (cudaStream_t)stream;
     CK(cudaMemsetAsync(ctx->d_counters64 + 1, 0, sizeof(unsigned long long), s));
+    CK(cudaMemsetAsync(ctx->d_counters64 + 3, 0, sizeof(unsigned long long), s));
     { STAGE(ST_BWD); CK(launch_render_bwd(ctx->L, dL_drgb, T_final, n_contrib, s)); }  // S7
     ctx->state = 3;
     return MVGS_OK;
@@ -366,7 +375,7 @@ mvgs_status mvgs_query(mvgs_ctx* ctx, mvgs_stats* out) {
     CK(cudaSetDevice(ctx->device));
     CK(cudaDeviceSynchronize());
     int h[C_NCOUNTERS];
-    unsigned long long h64[2];
+    unsigned long long h64[4];
     CK(cudaMemcpy(h, ctx->d_counters, sizeof(h), cudaMemcpyDeviceToHost));
     CK(cudaMemcpy(h64, ctx->d_counters64, sizeof(h64), cudaMemcpyDeviceToHost));
     memset(out, 0, sizeof(*out));
@@ -381,6 +390,8 @@ mvgs_status mvgs_query(mvgs_ctx* ctx, mvgs_stats* out) {
     out->tiles_y = ctx->L.TY;
     out->eval_fwd = (int64_t)h64[0];
     out->eval_bwd = (int64_t)h64[1];
+    out->exp_fwd = (int64_t)h64[2];
+    out->exp_bwd = (int64_t)h64[3];
     out->overflow = h[C_OVERFLOW] || out->Q > ctx->cap_pairs || out->K > ctx->cap_entries;
     if (out->overflow) return fail(ctx, MVGS_ERR_CAPACITY, "capacity exceeded: reserve stats.Q / stats.K and re-run");
     return MVGS_OK;

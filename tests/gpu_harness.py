@@ -68,12 +68,13 @@ def assert_close_rel(got, ref, name, rtol=1e-3, floor=1e-6, scale=None, ctol=1e-
     assert np.all(d <= lim), msg
 
 
-def per_view_scale(g, cams, dLdC, bg=(0.0, 0.0, 0.0)):
+def per_view_scale(g, cams, dLdC, bg=(0.0, 0.0, 0.0), tile_mask=None):
     """Σ_v |gradient of view v alone| for every output (the oracle, one view at a time)."""
     import oracle
     out = None
     for v in range(len(cams)):
-        r = oracle.Oracle(g, cams[v:v + 1], bg=bg).backward(dLdC[v:v + 1])
+        m = None if tile_mask is None else tile_mask[v:v + 1]
+        r = oracle.Oracle(g, cams[v:v + 1], bg=bg, tile_mask=m).backward(dLdC[v:v + 1])
         if out is None:
             out = {k: np.abs(x) for k, x in r.items()}
         else:

@@ -418,3 +418,35 @@ def test_P17_sh_basis_along_axes_and_diagonal():
             dd /= np.linalg.norm(dd)
             exp = np.maximum(0, _Y_textbook(k, dd) * np.array([0.3, -0.2, 0.1], np.float32).astype(float) + 0.5)
             np.testing.assert_allclose(o.pairs()["rgb"][0, 0], exp, atol=1e-7, err_msg=f"k={k} dir={dvec}")
+
+
+def test_tile_mask_mode_equals_full_run_on_the_mask():
+    """Masked oracle (used for sampled checks at full size): on the masked tiles it
+    reproduces the full run exactly; with ∂L/∂C zero outside them, every gradient and
+    E statistic equals the full run's."""
+    g, cams = synth.make_scene(synth.scaled(synth.CONFIGS["tiny"], P=600))
+    V, T = 4, 16
+    rng = np.random.default_rng(2)
+    mask = (rng.uniform(size=(V, T)) < 0.3).astype(np.uint8)
+    mask[0, :] = 0
+    mask[0, 5] = 1
+    pix = np.zeros((V, 64, 64), bool)
+    for v in range(V):
+        for t in range(T):
+            if mask[v, t]:
+                pix[v, (t // 4) * 16:(t // 4) * 16 + 16, (t % 4) * 16:(t % 4) * 16 + 16] = True
+    dL = synth.make_dLdC_scaled(V, 64, 64, 5) * pix[:, None]
+    full = oracle.Oracle(g, cams)
+    gf = full.backward(dL)
+    imf = full.image()
+    m = oracle.Oracle(g, cams, tile_mask=mask)
+    gm = m.backward(dL)
+    imm = m.image()
+    np.testing.assert_array_equal(imm["n_contrib"][pix], imf["n_contrib"][pix])
+    np.testing.assert_array_equal(imm["rgb"].transpose(0, 2, 3, 1)[pix], imf["rgb"].transpose(0, 2, 3, 1)[pix])
+    for k in gf:
+        np.testing.assert_allclose(gm[k], gf[k], rtol=1e-12, atol=1e-15, err_msg=k)
+    off_f, gid_f = full.lists()
+    off_m, gid_m = m.lists()
+    for b in np.nonzero(mask.reshape(-1))[0]:
+        np.testing.assert_array_equal(gid_m[off_m[b]:off_m[b + 1]], gid_f[off_f[b]:off_f[b + 1]])
