@@ -22,6 +22,23 @@ constexpr float ALPHA_MIN = 1.0f / 255.0f;  // R12
 constexpr float ALPHA_MAX = 0.99f;          // R11
 constexpr float T_EPS = 1e-4f;              // R13
 
+// §4.3 canonical exp, core for x ∈ [−87, 88] (no range checks).  The compositing
+// kernels only evaluate it for power ∈ [−ln(255)−1e-3, 0] (skip bound, §4.5), where it
+// is bit-identical to ca_exp.
+__device__ __forceinline__ float ca_exp_core(float x) {
+    float n = rintf(FMUL(x, 1.44269504f));
+    float r = FMA(n, -0.693145751953125f, x);
+    r = FMA(n, -1.428606765330187e-6f, r);
+    float p = (float)(1.0 / 720.0);
+    p = FMA(p, r, (float)(1.0 / 120.0));
+    p = FMA(p, r, (float)(1.0 / 24.0));
+    p = FMA(p, r, (float)(1.0 / 6.0));
+    p = FMA(p, r, 0.5f);
+    p = FMA(p, r, 1.0f);
+    p = FMA(p, r, 1.0f);
+    return FMUL(p, __int_as_float((__float2int_rn(n) + 127) << 23));
+}
+
 // §4.3 canonical exp.
 __device__ __forceinline__ float ca_exp(float x) {
     if (x < -87.0f) return 0.0f;

@@ -14,12 +14,13 @@ constexpr int BLK = 256;          // Gaussians per preprocessing block (pair-slo
 constexpr int NG = 10;            // per-pair gradient record: Σ∇x Σ∇y e1 ∂A ∂B ∂C ∂o ∂r ∂g ∂b
 constexpr int PG_STRIDE = 12;     // floats per pair-gradient slot (48 B, 16-B aligned)
 constexpr int REC_F4 = 3;         // float4 per pair render record (48 B)
+constexpr uint32_t PF_VISIBLE = 32u;
 
 // device counters (int32 slots in ctx->d_counters)
 enum { C_Q = 0, C_K = 1, C_OVERFLOW = 2, C_MAXB = 3, C_NVIS = 4, C_NCOUNTERS = 8 };
 
 // Per-pair meta: gid and (view << 8 | flags).  flags bit0..2: rgb clamped,
-// bit3: Jacobian x clamp, bit4: y clamp.
+// bit3: Jacobian x clamp, bit4: y clamp, bit5: tiles > 0 (visible).
 struct PairMeta {
     uint32_t gid;
     uint32_t vf;
@@ -38,6 +39,7 @@ struct Launch {  // everything a kernel needs about the current batch
     int* bucket_off;  // [V*T + 1]   exclusive scan of per-(view, tile) entry counts
     float4* rec;      // [cap_pairs * 3]
     PairMeta* meta;   // [cap_pairs]
+    uint32_t* pflag;  // [cap_pairs] bit0-2 rgb clamped, bit3-4 Jacobian clamps, bit5 tiles > 0
     float* pgrad;     // [cap_pairs * PG_STRIDE]
     uint32_t *key, *val, *key2, *val2;  // [cap_entries] entry (bucket key, pair) ping-pong
     uint32_t *pkey, *pval, *pkey2, *pval2;  // [cap_pairs] pair (depth key, pair) ping-pong
@@ -65,6 +67,7 @@ struct mvgs_ctx {
     int* d_bucket = nullptr;
     float4* d_rec = nullptr;
     mvgs::PairMeta* d_meta = nullptr;
+    uint32_t* d_pflag = nullptr;
     float* d_pgrad = nullptr;
     uint32_t *d_key = nullptr, *d_val = nullptr, *d_key2 = nullptr, *d_val2 = nullptr;
     uint32_t *d_pkey = nullptr, *d_pval = nullptr, *d_pkey2 = nullptr, *d_pval2 = nullptr;

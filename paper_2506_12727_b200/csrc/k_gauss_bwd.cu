@@ -81,22 +81,37 @@ __global__ __launch_bounds__(BLK, 2) void k_gauss_bwd(Launch L, mvgs_grads gr, m
             if (lane == 0) wc[warp][k] = __popc(bal);
         }
         __syncthreads();
-        for (int k = 0; k < nv; k++) {
-            const int v = v0 + k;
-            const mvgs_camera& c = L.cams[v];
-            const bool zvis = valid && ca_depth(c, mx, my, mz) > c.znear;
-            const unsigned bal = __ballot_sync(FULLG, zvis);
-            if (!zvis) continue;
-            int pre = 0;
-            for (int w = 0; w < warp; w++) pre += wc[w][k];
-            const int64_t pair = (int64_t)L.blk_off[(int64_t)v * L.NB + blockIdx.x] + pre + __popc(bal & lt);
-            if (pair >= L.cap_pairs) continue;
-            const float4 r2 = L.rec[3 * pair + 2];
-            if (__float_as_uint(r2.z) == __float_as_uint(r2.w)) continue;  // tiles == 0: inert (R27)
-            const uint32_t flags = L.meta[pair].vf & 0xffu;
-            const float4 pg0 = reinterpret_cast<const float4*>(L.pgrad + pair * PG_STRIDE)[0];
-            const float4 pg1 = reinterpret_cast<const float4*>(L.pgrad + pair * PG_STRIDE)[1];
-            const float4 pg2 = reinterpret_cast<const float4*>(L.pgrad + pair * PG_STRIDE)[2];
+        for (int k0 = 0; k0 < nv; k0 += 4) {
+            // issue the loads of up to 4 views first (memory-level parallelism), then the math
+            uint32_t fl[4];
+            float4 pga[4], pgb[4], pgc[4];
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                fl[u] = 0u;
+                const int k = k0 + u;
+                if (k >= nv) continue;  // warp-uniform
+                const mvgs_camera& c = L.cams[v0 + k];
+                const bool zvis = valid && ca_depth(c, mx, my, mz) > c.znear;
+                const unsigned bal = __ballot_sync(FULLG, zvis);
+                if (!zvis) continue;
+                int pre = 0;
+                for (int w = 0; w < warp; w++) pre += wc[w][k];
+                const int64_t pair = (int64_t)L.blk_off[(int64_t)(v0 + k) * L.NB + blockIdx.x] + pre + __popc(bal & lt);
+                if (pair >= L.cap_pairs) continue;
+                fl[u] = L.pflag[pair];
+                const float4* pgp = reinterpret_cast<const float4*>(L.pgrad + pair * PG_STRIDE);
+                if (fl[u] & PF_VISIBLE) {
+                    pga[u] = pgp[0];
+                    pgb[u] = pgp[1];
+                    pgc[u] = pgp[2];
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+            if (!(fl[u] & PF_VISIBLE)) continue;  // not participating, or tiles == 0: inert (R27)
+            const mvgs_camera& c = L.cams[v0 + k0 + u];
+            const uint32_t flags = fl[u];
+            const float4 pg0 = pga[u], pg1 = pgb[u], pg2 = pgc[u];
             // pg: (Σ∇x, Σ∇y, e1, ∂A) (∂B, ∂C, ∂o, ∂r) (∂g, ∂b, -, -)
             nvis += 1.f;
             e1 += pg0.z;
@@ -230,6 +245,7 @@ __global__ __launch_bounds__(BLK, 2) void k_gauss_bwd(Launch L, mvgs_grads gr, m
             dmx += (ddx - x * dd) * idn;
             dmy += (ddy - y * dd) * idn;
             dmz += (ddz - z * dd) * idn;
+            }
         }
         __syncthreads();
     }

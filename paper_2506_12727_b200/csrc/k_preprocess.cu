@@ -242,7 +242,9 @@ __global__ __launch_bounds__(BLK) void k_project(Launch L) {
             } else if (tiles == 0) {
                 // inert pair (R27): only the empty rect / depth and the ids are read later
                 L.rec[3 * pair + 2] = make_float4(0.f, p.tz, 0.f, 0.f);
-                L.meta[pair] = PairMeta{(uint32_t)g, ((uint32_t)v << 8) | (p.clx ? 8u : 0u) | (p.cly ? 16u : 0u)};
+                const uint32_t fl = (p.clx ? 8u : 0u) | (p.cly ? 16u : 0u);
+                L.meta[pair] = PairMeta{(uint32_t)g, ((uint32_t)v << 8) | fl};
+                L.pflag[pair] = fl;
             } else {
                 // colour (R17), free arithmetic
                 const float cpx = -(c.R[0] * c.t[0] + c.R[3] * c.t[1] + c.R[6] * c.t[2]);
@@ -273,6 +275,7 @@ __global__ __launch_bounds__(BLK) void k_project(Launch L) {
                 r[1] = make_float4(p.C, a.o, rgb[0], rgb[1]);
                 r[2] = make_float4(rgb[2], p.tz, __uint_as_float(lo), __uint_as_float(hi));
                 L.meta[pair] = PairMeta{(uint32_t)g, ((uint32_t)v << 8) | flags};
+                L.pflag[pair] = flags | PF_VISIBLE;
                 float4* pg = reinterpret_cast<float4*>(L.pgrad + pair * PG_STRIDE);
                 pg[0] = pg[1] = pg[2] = make_float4(0.f, 0.f, 0.f, 0.f);
             }

@@ -79,20 +79,21 @@ __global__ __launch_bounds__(RT) void k_render_fwd(Launch L, float* __restrict__
             }
             __syncthreads();
             const int cnt = min(RT, end - b0);
-            for (int j = 0; j < cnt && !done; j++) {
-                nev++;
+            int j = 0;
+            for (; j < cnt && !done; j++) {
                 const float4 a = s0[j];
                 const float4 c = s1[j];
                 const float dx = FSUB(a.x, fx), dy = FSUB(a.y, fy);
                 const float power = ca_power(a.z, a.w, c.x, dx, dy);
                 if (power > 0.0f || power < c.z) continue;
                 nexp++;
-                const float G = ca_exp(power);
+                const float G = ca_exp_core(power);
                 const float alpha = fminf(ALPHA_MAX, FMUL(c.y, G));
                 if (alpha < ALPHA_MIN) continue;
                 const float Tn = FMUL(T, FSUB(1.0f, alpha));
                 if (Tn < T_EPS) {
                     done = true;
+                    j++;  // the terminating entry was evaluated
                     break;
                 }
                 const float w = alpha * T;
@@ -103,6 +104,7 @@ __global__ __launch_bounds__(RT) void k_render_fwd(Launch L, float* __restrict__
                 T = Tn;
                 last = b0 - start + j + 1;
             }
+            nev += j;
         }
     }
     count_evals(&L.counters64[0], &L.counters64[2], nev, nexp, sev);
@@ -224,7 +226,7 @@ __global__ __launch_bounds__(RT) void k_render_bwd(Launch L, const float* __rest
                 const float power = ca_power(a.z, a.w, c.x, dx, dy);
                 if (power <= 0.0f && power >= c.z) {
                     nexp++;
-                    const float G = ca_exp(power);
+                    const float G = ca_exp_core(power);
                     const float oG = FMUL(c.y, G);
                     const float alpha = fminf(ALPHA_MAX, oG);
                     if (alpha >= ALPHA_MIN) {

@@ -43,6 +43,29 @@ __global__ __launch_bounds__(RS_T) void k_rs_hist(const uint32_t* __restrict__ k
     counts[(int64_t)threadIdx.x * ntiles + blockIdx.x] = h[threadIdx.x];
 }
 
+// exclusive scan over the 256 threads of a CTA (one value each)
+__device__ __forceinline__ uint32_t block_excl_scan_256_u(uint32_t x, uint32_t* total) {
+    __shared__ uint32_t wsum[RS_NW];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t inc = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(FULLS, inc, o);
+        if (lane >= o) inc += y;
+    }
+    if (lane == 31) wsum[warp] = inc;
+    __syncthreads();
+    uint32_t before = 0, all = 0;
+#pragma unroll
+    for (int w = 0; w < RS_NW; w++) {
+        const uint32_t t = wsum[w];
+        before += w < warp ? t : 0u;
+        all += t;
+    }
+    *total = all;
+    return before + inc - x;
+}
+
 // Warp multisplit ranking: lanes holding the same digit found with 8 ballots
 // (one per digit bit) instead of __match_any_sync, whose cost grows with the
 // number of distinct digits in the warp.
@@ -57,8 +80,11 @@ __device__ __forceinline__ unsigned digit_peers(uint32_t d, bool ok) {
     return peers;
 }
 
-// stable scatter of one tile to offsets[digit * ntiles + tile] + rank; optionally
-// moves a 64-bit payload with each key
+// Stable scatter of one tile.  Ranks are computed per warp (multisplit), the
+// tile is first re-ordered by digit in shared memory, then written out by
+// consecutive threads: every digit's run lands contiguously at
+// offsets[digit * ntiles + tile], so global writes are coalesced.
+// Optionally moves a 64-bit payload with each key.
 template <bool PAYLOAD>
 __global__ __launch_bounds__(RS_T) void k_rs_scatter(const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin,
                                                      uint32_t* __restrict__ kout, uint32_t* __restrict__ vout,
@@ -66,11 +92,16 @@ __global__ __launch_bounds__(RS_T) void k_rs_scatter(const uint32_t* __restrict_
                                                      const int* __restrict__ n_ptr, int64_t cap, int shift, int nbits,
                                                      const int* __restrict__ offs, int ntiles) {
     __shared__ uint32_t hist[RS_NW][RS_BINS];
+    __shared__ uint32_t dstart[RS_BINS];   // first local position of each digit
+    __shared__ uint32_t gdelta[RS_BINS];   // global offset − local start, per digit
+    __shared__ uint32_t sk[RS_TILE], sv[RS_TILE];
+    __shared__ uint2 sp[PAYLOAD ? RS_TILE : 1];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const unsigned lt = (1u << lane) - 1u;
     const int n = (int)min((int64_t)*n_ptr, cap);
     const int t0 = blockIdx.x * RS_TILE;
     if (t0 >= n) return;
+    const int nt = min(RS_TILE, n - t0);
     const uint32_t mask = (1u << nbits) - 1u;
 #pragma unroll
     for (int i = 0; i < RS_BINS / 32; i++) hist[warp][lane + 32 * i] = 0;
@@ -79,16 +110,16 @@ __global__ __launch_bounds__(RS_T) void k_rs_scatter(const uint32_t* __restrict_
     uint2 pay[PAYLOAD ? RS_IPT : 1];
 #pragma unroll
     for (int it = 0; it < RS_IPT; it++) {
-        const int p = t0 + warp * 32 * RS_IPT + it * 32 + lane;
-        const bool ok = p < n;
-        key[it] = ok ? kin[p] : 0u;
-        val[it] = ok ? vin[p] : 0u;
-        if (PAYLOAD) pay[PAYLOAD ? it : 0] = ok ? pin[p] : make_uint2(0u, 0u);
+        const int p = warp * 32 * RS_IPT + it * 32 + lane;
+        const bool ok = p < nt;
+        key[it] = ok ? kin[t0 + p] : 0u;
+        val[it] = ok ? vin[t0 + p] : 0u;
+        if (PAYLOAD) pay[PAYLOAD ? it : 0] = ok ? pin[t0 + p] : make_uint2(0u, 0u);
     }
 #pragma unroll
     for (int it = 0; it < RS_IPT; it++) {
-        const int p = t0 + warp * 32 * RS_IPT + it * 32 + lane;
-        const bool ok = p < n;
+        const int p = warp * 32 * RS_IPT + it * 32 + lane;
+        const bool ok = p < nt;
         const uint32_t d = (key[it] >> shift) & mask;
         const unsigned peers = digit_peers(d, ok);
         const uint32_t before = ok ? hist[warp][d] : 0u;
@@ -98,8 +129,15 @@ __global__ __launch_bounds__(RS_T) void k_rs_scatter(const uint32_t* __restrict_
         __syncwarp();
     }
     __syncthreads();
-    {  // thread = digit: warp bases inside the tile, offset by the device-wide scan
-        uint32_t run = (uint32_t)offs[(int64_t)threadIdx.x * ntiles + blockIdx.x];
+    {  // thread = digit: tile-local digit starts and warp bases
+        uint32_t tot = 0;
+#pragma unroll
+        for (int w = 0; w < RS_NW; w++) tot += hist[w][threadIdx.x];
+        uint32_t ws;
+        const uint32_t start = block_excl_scan_256_u(tot, &ws);
+        dstart[threadIdx.x] = start;
+        gdelta[threadIdx.x] = (uint32_t)offs[(int64_t)threadIdx.x * ntiles + blockIdx.x] - start;
+        uint32_t run = start;
 #pragma unroll
         for (int w = 0; w < RS_NW; w++) {
             const uint32_t c = hist[w][threadIdx.x];
@@ -110,13 +148,21 @@ __global__ __launch_bounds__(RS_T) void k_rs_scatter(const uint32_t* __restrict_
     __syncthreads();
 #pragma unroll
     for (int it = 0; it < RS_IPT; it++) {
-        const int p = t0 + warp * 32 * RS_IPT + it * 32 + lane;
-        if (p < n) {
-            const uint32_t dst = hist[warp][(key[it] >> shift) & mask] + loc[it];
-            kout[dst] = key[it];
-            vout[dst] = val[it];
-            if (PAYLOAD) pout[dst] = pay[PAYLOAD ? it : 0];
+        const int p = warp * 32 * RS_IPT + it * 32 + lane;
+        if (p < nt) {
+            const uint32_t l = hist[warp][(key[it] >> shift) & mask] + loc[it];
+            sk[l] = key[it];
+            sv[l] = val[it];
+            if (PAYLOAD) sp[PAYLOAD ? l : 0] = pay[PAYLOAD ? it : 0];
         }
+    }
+    __syncthreads();
+    for (int l = threadIdx.x; l < nt; l += RS_T) {
+        const uint32_t k = sk[l];
+        const uint32_t dst = gdelta[(k >> shift) & mask] + l;
+        kout[dst] = k;
+        vout[dst] = sv[l];
+        if (PAYLOAD) pout[dst] = sp[PAYLOAD ? l : 0];
     }
 }
 
@@ -175,27 +221,64 @@ __global__ void k_pair_tiles(Launch L, const uint2* __restrict__ rect, int* __re
     }
 }
 
-// duplication in depth order: entry e = ebase[i] + local tile index, key = view·T + tile
-__global__ void k_dup(Launch L, const uint32_t* __restrict__ order, const uint2* __restrict__ rect,
-                      const int* __restrict__ ebase) {
+// Duplication in depth order: pair i's entries are ebase[i] + (row-major tile index
+// in its rect), key = view·T + tile.  A warp takes 32 consecutive pairs and writes
+// their entries together: lane l handles entries l, l+32, … of the warp's run,
+// finding its pair by a search over the warp's inclusive tile-count prefix, so
+// consecutive lanes write consecutive addresses.
+__global__ __launch_bounds__(256) void k_dup(Launch L, const uint32_t* __restrict__ order,
+                                             const uint2* __restrict__ rect, const int* __restrict__ ebase) {
     const int Q = (int)min((int64_t)L.counters[C_Q], L.cap_pairs);
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < Q; i += stride) {
-        const uint2 r = rect[i];
+    const int lane = threadIdx.x & 31;
+    const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t w0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32; w0 < Q; w0 += nwarps * 32) {
+        const int64_t i = w0 + lane;
+        uint2 r = make_uint2(0u, 0u);
+        uint32_t q = 0;
+        if (i < Q) {
+            r = rect[i];
+            q = order[i];
+        }
         const int rx0 = r.x & 0xffff, ry0 = r.x >> 16, rx1 = r.y & 0xffff, ry1 = r.y >> 16;
-        if (rx1 <= rx0 || ry1 <= ry0) continue;
-        const uint32_t q = order[i];
-        const uint32_t vbase = (uint32_t)view_of_pair(L, q) * (uint32_t)L.T;
-        int64_t e = ebase[i];
-        for (int ty = ry0; ty < ry1; ty++)
-            for (int tx = rx0; tx < rx1; tx++, e++) {
+        const int w = rx1 - rx0;
+        const int cnt = (rx1 > rx0 && ry1 > ry0) ? w * (ry1 - ry0) : 0;
+        int inc = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(FULLS, inc, o);
+            if (lane >= o) inc += y;
+        }
+        const int total = __shfl_sync(FULLS, inc, 31);
+        const int64_t e0 = __shfl_sync(FULLS, (int64_t)(i < Q ? ebase[i] : 0), 0);
+        const uint32_t vb = (i < Q && cnt > 0) ? (uint32_t)view_of_pair(L, q) * (uint32_t)L.T : 0u;
+        for (int base = 0; base < total; base += 32) {  // warp-uniform rounds, all lanes active
+            const int k = base + lane;
+            // owner = first lane whose inclusive prefix exceeds k (monotone ⇒ binary search)
+            int lo = 0;
+#pragma unroll
+            for (int step = 16; step > 0; step >>= 1) {
+                const int cand = lo + step - 1;
+                if (__shfl_sync(FULLS, inc, cand) <= k) lo += step;
+            }
+            const int owner = min(lo, 31);
+            const int excl = __shfl_sync(FULLS, inc - cnt, owner);
+            const int ow = __shfl_sync(FULLS, w, owner);
+            const int ox = __shfl_sync(FULLS, rx0, owner);
+            const int oy = __shfl_sync(FULLS, ry0, owner);
+            const uint32_t ob = __shfl_sync(FULLS, vb, owner);
+            const uint32_t oq = __shfl_sync(FULLS, q, owner);
+            if (k < total) {
+                const int loc = k - excl;
+                const int ty = oy + loc / ow, tx = ox + loc % ow;
+                const int64_t e = e0 + k;
                 if (e < L.cap_entries) {
-                    L.key[e] = vbase + ty * L.TX + tx;
-                    L.val[e] = q;
+                    L.key[e] = ob + ty * L.TX + tx;
+                    L.val[e] = oq;
                 } else {
                     L.counters[C_OVERFLOW] = 1;
                 }
             }
+        }
     }
 }
 

@@ -51,8 +51,9 @@ cudaError_t grow(T*& p, int64_t& cap, int64_t need, int64_t elem_per = 1) {
 cudaError_t alloc_pairs(mvgs_ctx* c, int64_t n) {
     cudaFree(c->d_rec); cudaFree(c->d_meta); cudaFree(c->d_pgrad);
     cudaFree(c->d_pkey); cudaFree(c->d_pval); cudaFree(c->d_pkey2); cudaFree(c->d_pval2); cudaFree(c->d_ecount);
-    cudaFree(c->d_prect); cudaFree(c->d_prect2);
+    cudaFree(c->d_prect); cudaFree(c->d_prect2); cudaFree(c->d_pflag);
     c->d_prect = c->d_prect2 = nullptr;
+    c->d_pflag = nullptr;
     c->d_rec = nullptr; c->d_meta = nullptr; c->d_pgrad = nullptr;
     c->d_pkey = c->d_pval = c->d_pkey2 = c->d_pval2 = nullptr;
     c->d_ecount = nullptr;
@@ -67,6 +68,7 @@ cudaError_t alloc_pairs(mvgs_ctx* c, int64_t n) {
     if ((e = cudaMalloc(&c->d_pval2, 4 * n)) != cudaSuccess) return e;
     if ((e = cudaMalloc(&c->d_ecount, 4 * (n + 1))) != cudaSuccess) return e;
     if ((e = cudaMalloc(&c->d_prect, sizeof(uint2) * n)) != cudaSuccess) return e;
+    if ((e = cudaMalloc(&c->d_pflag, sizeof(uint32_t) * n)) != cudaSuccess) return e;
     if ((e = cudaMalloc(&c->d_prect2, sizeof(uint2) * n)) != cudaSuccess) return e;
     c->cap_pairs = n;
     return cudaSuccess;
@@ -153,6 +155,7 @@ void fill_launch(mvgs_ctx* c) {
     L.bucket_off = c->d_bucket;
     L.rec = c->d_rec;
     L.meta = c->d_meta;
+    L.pflag = c->d_pflag;
     L.pgrad = c->d_pgrad;
     L.key = c->d_key;
     L.val = c->d_val;
@@ -215,6 +218,7 @@ void mvgs_destroy(mvgs_ctx* ctx) {
     cudaFree(ctx->d_key); cudaFree(ctx->d_val); cudaFree(ctx->d_key2); cudaFree(ctx->d_val2);
     cudaFree(ctx->d_pkey); cudaFree(ctx->d_pval); cudaFree(ctx->d_pkey2); cudaFree(ctx->d_pval2);
     cudaFree(ctx->d_ecount); cudaFree(ctx->d_rs); cudaFree(ctx->d_prect); cudaFree(ctx->d_prect2);
+    cudaFree(ctx->d_pflag);
     cudaFree(ctx->d_counters); cudaFree(ctx->d_counters64); cudaFree(ctx->d_scan);
     if (ctx->h_cams) cudaFreeHost(ctx->h_cams);
     if (ctx->cams_ev) cudaEventDestroy(ctx->cams_ev);
