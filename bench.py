@@ -158,11 +158,13 @@ def run_mvgs(args):
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2506_12727_b200 import mvgs
+    from paper_2506_12727_b200.dist import GradBuffer, view_shard
 
     cfg = synth.CONFIGS[args.config]
     Vr = cfg.V if N == 1 else cfg.V  # views per rank (weak scaling: per-GPU batch fixed)
     g_np, cams_all = synth.make_scene(synth.scaled(cfg, V=Vr * N))
-    cams = synth.subset_views(cams_all, rank * Vr, (rank + 1) * Vr)
+    lo, hi = view_shard(Vr * N, N, rank)
+    cams = synth.subset_views(cams_all, lo, hi)
     P = g_np["means"].shape[0]
     NK = (g_np["sh_degree"] + 1) ** 2
     S = g_np["sh"].shape[1]
@@ -176,18 +178,8 @@ def run_mvgs(args):
     st0 = R.stats
     mvgs.reserve(R.ctx, int(st0["Q"] * 1.15) + 4096, int(st0["K"] * 1.15) + 65536)
     # one flat buffer for every output that is a sum over views (single all-reduce)
-    sizes = dict(d_means=3 * P, d_log_scales=3 * P, d_quats=4 * P, d_opacity_logits=P, d_sh=S * 3 * P,
-                 e1=P, e2=P, vis=P)
-    flat = torch.empty(sum(sizes.values()), dtype=torch.float32, device=dev)
-    views, off = {}, 0
-    shapes = dict(d_means=(P, 3), d_log_scales=(P, 3), d_quats=(P, 4), d_opacity_logits=(P,), d_sh=(P, S, 3),
-                  e1=(P,), e2=(P,), vis=(P,))
-    for k, n in sizes.items():
-        views[k] = flat[off:off + n].view(shapes[k])
-        off += n
-    e_old = torch.empty(P, dtype=torch.float32, device=dev)
-    grads = {k: views[k] for k in ("d_means", "d_log_scales", "d_quats", "d_opacity_logits", "d_sh")}
-    adc = dict(e1=views["e1"], e2=views["e2"], e_old=e_old, vis=views["vis"])
+    buf = GradBuffer(P, S, dev)
+    flat, grads, adc = buf.flat, buf.grads, buf.adc
     outs = R.alloc_forward()
 
     def step():
@@ -196,7 +188,7 @@ def run_mvgs(args):
         mvgs.render_bwd(R.ctx, dL, outs[1], outs[2])
         mvgs.adc_stats(R.ctx, grads, adc)
         if dist is not None:
-            dist.all_reduce(flat)
+            buf.allreduce()
 
     for _ in range(args.warmup):
         step()

@@ -42,6 +42,7 @@ __global__ __launch_bounds__(BLK, 2) void k_gauss_bwd(Launch L, mvgs_grads gr, m
     float* sh_s = smem_sh;              // [BLK][SS]
     float* dsh_s = smem_sh + BLK * SS;  // [BLK][SS]
     __shared__ int wc[BLK / 32][32];
+    __shared__ int sboff[32];  // first pair slot of this block in each view of the chunk
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const unsigned lt = (1u << lane) - 1u;
     const int64_t g0 = (int64_t)blockIdx.x * BLK;
@@ -80,6 +81,7 @@ __global__ __launch_bounds__(BLK, 2) void k_gauss_bwd(Launch L, mvgs_grads gr, m
             const unsigned bal = __ballot_sync(FULLG, vis);
             if (lane == 0) wc[warp][k] = __popc(bal);
         }
+        if (threadIdx.x < nv) sboff[threadIdx.x] = L.blk_off[(int64_t)(v0 + threadIdx.x) * L.NB + blockIdx.x];
         __syncthreads();
         for (int k0 = 0; k0 < nv; k0 += 4) {
             // issue the loads of up to 4 views first (memory-level parallelism), then the math
@@ -96,15 +98,14 @@ __global__ __launch_bounds__(BLK, 2) void k_gauss_bwd(Launch L, mvgs_grads gr, m
                 if (!zvis) continue;
                 int pre = 0;
                 for (int w = 0; w < warp; w++) pre += wc[w][k];
-                const int64_t pair = (int64_t)L.blk_off[(int64_t)(v0 + k) * L.NB + blockIdx.x] + pre + __popc(bal & lt);
+                const int64_t pair = (int64_t)sboff[k] + pre + __popc(bal & lt);
                 if (pair >= L.cap_pairs) continue;
+                // flags and gradient slot loaded together (the slot is ignored for inert pairs)
                 fl[u] = L.pflag[pair];
                 const float4* pgp = reinterpret_cast<const float4*>(L.pgrad + pair * PG_STRIDE);
-                if (fl[u] & PF_VISIBLE) {
-                    pga[u] = pgp[0];
-                    pgb[u] = pgp[1];
-                    pgc[u] = pgp[2];
-                }
+                pga[u] = pgp[0];
+                pgb[u] = pgp[1];
+                pgc[u] = pgp[2];
             }
 #pragma unroll
             for (int u = 0; u < 4; u++) {

@@ -12,9 +12,11 @@
 // n_contrib, reconstructing T by division.  Each entry's ten per-pixel terms
 // (Σ∇x, Σ∇y, ‖∇‖ for E1, ∂A, ∂B, ∂C, ∂o, ∂r, ∂g, ∂b) are reduced across the
 // warp with a transpose-reduce (12 shuffles for 10 values instead of 50; each
-// lane ends up owning one value's warp sum), added into a per-batch shared
-// accumulator, and the CTA's sums are flushed to the pair's gradient slot with
-// one global red.add per nonzero value after the batch.
+// lane ends up owning one value's warp sum), stored by that lane into the
+// warp's private slot for the entry (plain stores — shared-memory float atomics
+// would be CAS loops), and after the batch the 8 warp slots are summed in fixed
+// order and flushed to the pair's gradient slot with one global red.add per
+// nonzero value.
 #include "ca.cuh"
 #include "internal.cuh"
 
@@ -154,14 +156,16 @@ __device__ __forceinline__ int reduce_id(int lane) {
     return b2 ? x1 : x0;
 }
 
+constexpr int RB = 128;  // backward batch (entries staged per round)
+
 __global__ __launch_bounds__(RT) void k_render_bwd(Launch L, const float* __restrict__ dL_drgb,
                                                    const float* __restrict__ in_T, const int32_t* __restrict__ in_n) {
-    __shared__ float4 s0[RT], s1[RT], s2[RT];  // as in the forward
-    __shared__ uint32_t sq[RT];
-    __shared__ float sacc[RT * NG];
+    __shared__ float4 s0[RB], s1[RB], s2[RB];  // as in the forward
+    __shared__ uint32_t sq[RB];
+    __shared__ __align__(16) float sacc[RT / 32][RB * NG];  // per-warp partial sums, no atomics
     __shared__ int smax;
     __shared__ unsigned sev[2];
-    const int lane = threadIdx.x & 31;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int bucket = blockIdx.x;
     const int v = bucket / L.T, tile = bucket - v * L.T;
     const int ty = tile / L.TX, tx = tile - ty * L.TX;
@@ -192,14 +196,15 @@ __global__ __launch_bounds__(RT) void k_render_bwd(Launch L, const float* __rest
     const int wmax = __reduce_max_sync(FULLR, last);  // entries beyond it are skipped warp-uniformly
     const int my_id = reduce_id(lane);
     const bool owner = (__ffs(__match_any_sync(FULLR, my_id)) - 1) == lane;
+    float* wacc = sacc[warp];
     const float fx = (float)x, fy = (float)y;
     const float hw = 0.5f * (float)L.W, hh = 0.5f * (float)L.H;
     const float dL_bg = L.bg[0] * dL0 + L.bg[1] * dL1 + L.bg[2] * dL2;
     float T = T_fin;
     float acc0 = 0.f, acc1 = 0.f, acc2 = 0.f;   // colour behind the current entry
     float a_prev = 0.f, c0p = 0.f, c1p = 0.f, c2p = 0.f;
-    for (int b_end = maxlast; b_end > 0; b_end -= RT) {
-        const int b0 = max(0, b_end - RT);
+    for (int b_end = maxlast; b_end > 0; b_end -= RB) {
+        const int b0 = max(0, b_end - RB);
         const int cnt = b_end - b0;
         __syncthreads();
         if (threadIdx.x < cnt) {
@@ -211,7 +216,10 @@ __global__ __launch_bounds__(RT) void k_render_bwd(Launch L, const float* __rest
             s1[threadIdx.x] = make_float4(r1.x, r1.y, skip_power(r1.y), 0.f);
             s2[threadIdx.x] = make_float4(r1.z, r1.w, r2.x, 0.f);
         }
-        for (int i = threadIdx.x; i < RT * NG; i += RT) sacc[i] = 0.f;
+        {  // each warp clears its own slots
+            float4* w4 = reinterpret_cast<float4*>(wacc);
+            for (int i = lane; i < RB * NG / 4; i += 32) w4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
         __syncthreads();
         for (int jj = min(cnt, wmax - b0) - 1; jj >= 0; jj--) {
             const int j = b0 + jj;
@@ -265,12 +273,14 @@ __global__ __launch_bounds__(RT) void k_render_bwd(Launch L, const float* __rest
             }
             if (__any_sync(FULLR, contrib)) {
                 const float s = warp_transpose_reduce10(val, lane);
-                if (owner && s != 0.f) atomicAdd(&sacc[jj * NG + my_id], s);
+                if (owner) wacc[jj * NG + my_id] = s;
             }
         }
         __syncthreads();
         for (int i = threadIdx.x; i < cnt * NG; i += RT) {
-            const float s = sacc[i];
+            float s = 0.f;
+#pragma unroll
+            for (int w = 0; w < RT / 32; w++) s += sacc[w][i];
             if (s != 0.f) {
                 const int jj = i / NG, k = i - jj * NG;
                 atomicAdd(&L.pgrad[(int64_t)sq[jj] * PG_STRIDE + k], s);
