@@ -8,9 +8,8 @@
 //   k_project     S2  EWA projection, conic, radius, tile rect, SH colour per pair
 //                     (P:75), one thread per Gaussian looping its views so
 //                     per-Gaussian work (activations, Σ, SH load) is done once for
-//                     the whole batch; also the per-(view, tile) entry histogram (S3)
-//   scan          S3/S5 exclusive scan of the histogram → bucket offsets = ranges
-//   (duplication and sorting: k_sort.cu)
+//                     the whole batch; writes the pair-sort keys (depth, rect)
+//   (duplication, sorting and the per-(view, tile) ranges: k_sort.cu)
 #include "ca.cuh"
 #include "internal.cuh"
 
@@ -279,12 +278,7 @@ __global__ __launch_bounds__(BLK) void k_project(Launch L) {
                 float4* pg = reinterpret_cast<float4*>(L.pgrad + pair * PG_STRIDE);
                 pg[0] = pg[1] = pg[2] = make_float4(0.f, 0.f, 0.f, 0.f);
             }
-            if (tiles > 0) {
-                atomicAdd(&L.counters[C_NVIS], 1);
-                int* cnt = L.bucket_off + (int64_t)v * L.T;  // histogram, scanned in place afterwards
-                for (int ty = p.ry0; ty < p.ry1; ty++)
-                    for (int tx = p.rx0; tx < p.rx1; tx++) atomicAdd(&cnt[ty * L.TX + tx], 1);
-            }
+            if (tiles > 0) atomicAdd(&L.counters[C_NVIS], 1);  // warp-aggregated by ptxas
         }
         __syncthreads();
     }

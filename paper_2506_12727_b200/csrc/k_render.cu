@@ -1,28 +1,31 @@
 // k_render.cu — S6 forward compositing and S7 backward compositing + E1.
 //
 // Grid = one CTA per (view, tile) — "multiple blocks per tile, one block for
-// each viewpoint" — 256 threads, one pixel each (16×16 tile).  Entries
-// of the tile's depth-sorted list are staged into shared memory a batch of 256
-// at a time, each thread fetching one record, then every thread walks the
-// batch (Alg. 2).  A warp whose pixels have all terminated leaves
-// the batch loop at once (the loop condition is per-lane, so a fully-done warp
-// falls through); the CTA stops fetching when all 256 pixels are done.
+// each viewpoint".  A CTA has 128 threads for the 16×16 tile: each
+// thread owns TWO pixels (rows r and r+2 of its warp's 16×4 block), so every
+// staged record, loop step and — in the backward — every warp reduction is
+// shared by two pixels.  Entries of the tile's depth-sorted list are staged in
+// shared memory a batch of 128 at a time, one record per thread, then every
+// thread walks the batch (Alg. 2).  A warp whose pixels have all
+// terminated leaves the batch loop at once; the CTA stops fetching when all
+// its pixels are done.
 //
 // Backward (adjoint of Eq. (1)): back to front from each pixel's
-// n_contrib, reconstructing T by division.  Each entry's ten per-pixel terms
-// (Σ∇x, Σ∇y, ‖∇‖ for E1, ∂A, ∂B, ∂C, ∂o, ∂r, ∂g, ∂b) are reduced across the
-// warp with a transpose-reduce (12 shuffles for 10 values instead of 50; each
-// lane ends up owning one value's warp sum), stored by that lane into the
-// warp's private slot for the entry (plain stores — shared-memory float atomics
-// would be CAS loops), and after the batch the 8 warp slots are summed in fixed
-// order and flushed to the pair's gradient slot with one global red.add per
-// nonzero value.
+// n_contrib, reconstructing T by division.  For each entry a thread adds its
+// two pixels' ten terms (Σ∇x, Σ∇y, ‖∇‖ for E1, ∂A, ∂B, ∂C, ∂o, ∂r, ∂g, ∂b;
+// ‖∇‖ is taken per pixel before adding — "norm and add"), the warp
+// transpose-reduces them (12 shuffles for 10 values; each lane ends up owning
+// one value's warp sum) into the warp's private slot for the entry (plain
+// stores — shared-memory float atomics would be CAS loops), and after the
+// batch the 4 warp slots are summed in fixed order and flushed to the pair's
+// gradient slot with one global red.add per nonzero value.
 #include "ca.cuh"
 #include "internal.cuh"
 
 namespace mvgs {
 
-constexpr int RT = 256;
+constexpr int RT = 128;            // threads per CTA = entries per staged batch
+constexpr int NWR = RT / 32;       // warps per CTA
 constexpr unsigned FULLR = 0xffffffffu;
 
 // CTA-wide sums of two per-thread counts → one 64-bit atomic each per CTA.
@@ -50,73 +53,97 @@ __device__ __forceinline__ void count_evals(unsigned long long* ctr0, unsigned l
 constexpr float SKIP_MARGIN = 1e-3f;
 __device__ __forceinline__ float skip_power(float o) { return -logf(255.0f * o) - SKIP_MARGIN; }
 
+// pixel coordinates of this thread's two pixels: warp w covers rows 4w..4w+3
+__device__ __forceinline__ void pixel_pair(int tx, int ty, int& x, int& y0, int& y1) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    x = tx * TILE + (lane & 15);
+    y0 = ty * TILE + 4 * warp + (lane >> 4);
+    y1 = y0 + 2;
+}
+
+// stage one record: (x, y, A, B) (C, o, skip bound, -) (r, g, b, -)
+__device__ __forceinline__ void stage(const Launch& L, uint32_t q, float4* s0, float4* s1, float4* s2, int i) {
+    const float4* r = L.rec + 3 * (int64_t)q;
+    const float4 r0 = r[0], r1 = r[1], r2 = r[2];
+    s0[i] = r0;
+    s1[i] = make_float4(r1.x, r1.y, skip_power(r1.y), 0.f);
+    s2[i] = make_float4(r1.z, r1.w, r2.x, 0.f);
+}
+
 __global__ __launch_bounds__(RT) void k_render_fwd(Launch L, float* __restrict__ out_rgb, float* __restrict__ out_T,
                                                    int32_t* __restrict__ out_n) {
-    __shared__ float4 s0[RT], s1[RT], s2[RT];  // (x, y, A, B) (C, o, skip bound, -) (r, g, b, -)
+    __shared__ float4 s0[RT], s1[RT], s2[RT];
+    __shared__ unsigned sev[2];
     const int bucket = blockIdx.x;
     const int v = bucket / L.T, tile = bucket - v * L.T;
     const int ty = tile / L.TX, tx = tile - ty * L.TX;
-    const int x = tx * TILE + (threadIdx.x & 15), y = ty * TILE + (threadIdx.x >> 4);
-    const bool inside = x < L.W && y < L.H;
+    int x, y[2];
+    pixel_pair(tx, ty, x, y[0], y[1]);
     const int start = L.bucket_off[bucket], end = L.bucket_off[bucket + 1];
-    const float fx = (float)x, fy = (float)y;
-    float T = 1.0f, C0 = 0.f, C1 = 0.f, C2 = 0.f;
-    int last = 0;
+    const float fx = (float)x;
+    float fy[2], T[2], C0[2], C1[2], C2[2];
+    int last[2];
+    bool done[2];
+#pragma unroll
+    for (int p = 0; p < 2; p++) {
+        fy[p] = (float)y[p];
+        T[p] = 1.0f;
+        C0[p] = C1[p] = C2[p] = 0.f;
+        last[p] = 0;
+        done[p] = !(x < L.W && y[p] < L.H);
+    }
     unsigned nev = 0, nexp = 0;
-    __shared__ unsigned sev[2];
     if (threadIdx.x == 0) sev[0] = sev[1] = 0;
     __syncthreads();
-    bool done = !inside;
     if (end <= L.cap_entries) {
         for (int b0 = start; b0 < end; b0 += RT) {
-            if (__syncthreads_count(done) == RT) break;
+            if (__syncthreads_count(done[0] && done[1]) == RT) break;
             const int idx = b0 + threadIdx.x;
-            if (idx < end) {
-                const uint32_t q = L.sorted[idx];
-                const float4* r = L.rec + 3 * (int64_t)q;
-                const float4 r0 = r[0], r1 = r[1], r2 = r[2];
-                s0[threadIdx.x] = r0;
-                s1[threadIdx.x] = make_float4(r1.x, r1.y, skip_power(r1.y), 0.f);
-                s2[threadIdx.x] = make_float4(r1.z, r1.w, r2.x, 0.f);
-            }
+            if (idx < end) stage(L, L.sorted[idx], s0, s1, s2, threadIdx.x);
             __syncthreads();
             const int cnt = min(RT, end - b0);
-            int j = 0;
-            for (; j < cnt && !done; j++) {
+            for (int j = 0; j < cnt && !(done[0] && done[1]); j++) {
                 const float4 a = s0[j];
                 const float4 c = s1[j];
-                const float dx = FSUB(a.x, fx), dy = FSUB(a.y, fy);
-                const float power = ca_power(a.z, a.w, c.x, dx, dy);
-                if (power > 0.0f || power < c.z) continue;
-                nexp++;
-                const float G = ca_exp_core(power);
-                const float alpha = fminf(ALPHA_MAX, FMUL(c.y, G));
-                if (alpha < ALPHA_MIN) continue;
-                const float Tn = FMUL(T, FSUB(1.0f, alpha));
-                if (Tn < T_EPS) {
-                    done = true;
-                    j++;  // the terminating entry was evaluated
-                    break;
+                const float dx = FSUB(a.x, fx);
+#pragma unroll
+                for (int p = 0; p < 2; p++) {
+                    if (done[p]) continue;
+                    nev++;
+                    const float dy = FSUB(a.y, fy[p]);
+                    const float power = ca_power(a.z, a.w, c.x, dx, dy);
+                    if (power > 0.0f || power < c.z) continue;
+                    nexp++;
+                    const float G = ca_exp_core(power);
+                    const float alpha = fminf(ALPHA_MAX, FMUL(c.y, G));
+                    if (alpha < ALPHA_MIN) continue;
+                    const float Tn = FMUL(T[p], FSUB(1.0f, alpha));
+                    if (Tn < T_EPS) {
+                        done[p] = true;
+                        continue;
+                    }
+                    const float w = alpha * T[p];
+                    const float4 col = s2[j];
+                    C0[p] += col.x * w;
+                    C1[p] += col.y * w;
+                    C2[p] += col.z * w;
+                    T[p] = Tn;
+                    last[p] = b0 - start + j + 1;
                 }
-                const float w = alpha * T;
-                const float4 col = s2[j];
-                C0 += col.x * w;
-                C1 += col.y * w;
-                C2 += col.z * w;
-                T = Tn;
-                last = b0 - start + j + 1;
             }
-            nev += j;
         }
     }
     count_evals(&L.counters64[0], &L.counters64[2], nev, nexp, sev);
-    if (inside) {
-        const int64_t HW = (int64_t)L.H * L.W, pix = (int64_t)y * L.W + x;
-        out_rgb[(3 * (int64_t)v + 0) * HW + pix] = C0 + T * L.bg[0];
-        out_rgb[(3 * (int64_t)v + 1) * HW + pix] = C1 + T * L.bg[1];
-        out_rgb[(3 * (int64_t)v + 2) * HW + pix] = C2 + T * L.bg[2];
-        out_T[v * HW + pix] = T;
-        out_n[v * HW + pix] = last;
+    const int64_t HW = (int64_t)L.H * L.W;
+#pragma unroll
+    for (int p = 0; p < 2; p++) {
+        if (!(x < L.W && y[p] < L.H)) continue;
+        const int64_t pix = (int64_t)y[p] * L.W + x;
+        out_rgb[(3 * (int64_t)v + 0) * HW + pix] = C0[p] + T[p] * L.bg[0];
+        out_rgb[(3 * (int64_t)v + 1) * HW + pix] = C1[p] + T[p] * L.bg[1];
+        out_rgb[(3 * (int64_t)v + 2) * HW + pix] = C2[p] + T[p] * L.bg[2];
+        out_T[v * HW + pix] = T[p];
+        out_n[v * HW + pix] = last[p];
     }
 }
 
@@ -156,131 +183,143 @@ __device__ __forceinline__ int reduce_id(int lane) {
     return b2 ? x1 : x0;
 }
 
-constexpr int RB = 128;  // backward batch (entries staged per round)
+// per-pixel backward state
+struct BwdPix {
+    float dL0, dL1, dL2, T_fin, T, dL_bg;
+    float acc0, acc1, acc2, a_prev, c0p, c1p, c2p;
+    int last;
+};
 
 __global__ __launch_bounds__(RT) void k_render_bwd(Launch L, const float* __restrict__ dL_drgb,
                                                    const float* __restrict__ in_T, const int32_t* __restrict__ in_n) {
-    __shared__ float4 s0[RB], s1[RB], s2[RB];  // as in the forward
-    __shared__ uint32_t sq[RB];
-    __shared__ __align__(16) float sacc[RT / 32][RB * NG];  // per-warp partial sums, no atomics
+    __shared__ float4 s0[RT], s1[RT], s2[RT];
+    __shared__ uint32_t sq[RT];
+    __shared__ __align__(16) float sacc[NWR][RT * NG];  // per-warp partial sums, no atomics
     __shared__ int smax;
     __shared__ unsigned sev[2];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int bucket = blockIdx.x;
     const int v = bucket / L.T, tile = bucket - v * L.T;
     const int ty = tile / L.TX, tx = tile - ty * L.TX;
-    const int x = tx * TILE + (threadIdx.x & 15), y = ty * TILE + (threadIdx.x >> 4);
-    const bool inside = x < L.W && y < L.H;
+    int x, y[2];
+    pixel_pair(tx, ty, x, y[0], y[1]);
     const int start = L.bucket_off[bucket], end = L.bucket_off[bucket + 1];
     if (end > L.cap_entries) return;
-    const int64_t HW = (int64_t)L.H * L.W, pix = (int64_t)y * L.W + x;
-    float dL0 = 0.f, dL1 = 0.f, dL2 = 0.f, T_fin = 1.f;
-    int last = 0;
-    if (inside) {
-        dL0 = dL_drgb[(3 * (int64_t)v + 0) * HW + pix];
-        dL1 = dL_drgb[(3 * (int64_t)v + 1) * HW + pix];
-        dL2 = dL_drgb[(3 * (int64_t)v + 2) * HW + pix];
-        T_fin = in_T[v * HW + pix];
-        last = in_n[v * HW + pix];
+    const int64_t HW = (int64_t)L.H * L.W;
+    BwdPix px[2];
+    int mylast = 0;
+#pragma unroll
+    for (int p = 0; p < 2; p++) {
+        BwdPix& s = px[p];
+        s.dL0 = s.dL1 = s.dL2 = 0.f;
+        s.T_fin = 1.f;
+        s.last = 0;
+        if (x < L.W && y[p] < L.H) {
+            const int64_t pix = (int64_t)y[p] * L.W + x;
+            s.dL0 = dL_drgb[(3 * (int64_t)v + 0) * HW + pix];
+            s.dL1 = dL_drgb[(3 * (int64_t)v + 1) * HW + pix];
+            s.dL2 = dL_drgb[(3 * (int64_t)v + 2) * HW + pix];
+            s.T_fin = in_T[v * HW + pix];
+            s.last = in_n[v * HW + pix];
+        }
+        s.T = s.T_fin;
+        s.dL_bg = L.bg[0] * s.dL0 + L.bg[1] * s.dL1 + L.bg[2] * s.dL2;
+        s.acc0 = s.acc1 = s.acc2 = 0.f;  // colour behind the current entry
+        s.a_prev = s.c0p = s.c1p = s.c2p = 0.f;
+        mylast = max(mylast, s.last);
     }
     if (threadIdx.x == 0) {
         smax = 0;
         sev[0] = sev[1] = 0;
     }
     __syncthreads();
-    const unsigned nev = (unsigned)last;  // entries this pixel walks back over
+    const unsigned nev = (unsigned)(px[0].last + px[1].last);  // entries the two pixels walk back over
     unsigned nexp = 0;
-    if (last > 0) atomicMax(&smax, last);
+    if (mylast > 0) atomicMax(&smax, mylast);
     __syncthreads();
     const int maxlast = smax;
-    const int wmax = __reduce_max_sync(FULLR, last);  // entries beyond it are skipped warp-uniformly
+    const int wmax = __reduce_max_sync(FULLR, mylast);  // entries beyond it are skipped warp-uniformly
     const int my_id = reduce_id(lane);
     const bool owner = (__ffs(__match_any_sync(FULLR, my_id)) - 1) == lane;
     float* wacc = sacc[warp];
-    const float fx = (float)x, fy = (float)y;
+    const float fx = (float)x;
+    const float fy0 = (float)y[0], fy1 = (float)y[1];
     const float hw = 0.5f * (float)L.W, hh = 0.5f * (float)L.H;
-    const float dL_bg = L.bg[0] * dL0 + L.bg[1] * dL1 + L.bg[2] * dL2;
-    float T = T_fin;
-    float acc0 = 0.f, acc1 = 0.f, acc2 = 0.f;   // colour behind the current entry
-    float a_prev = 0.f, c0p = 0.f, c1p = 0.f, c2p = 0.f;
-    for (int b_end = maxlast; b_end > 0; b_end -= RB) {
-        const int b0 = max(0, b_end - RB);
+    for (int b_end = maxlast; b_end > 0; b_end -= RT) {
+        const int b0 = max(0, b_end - RT);
         const int cnt = b_end - b0;
         __syncthreads();
         if (threadIdx.x < cnt) {
             const uint32_t q = L.sorted[start + b0 + threadIdx.x];
-            const float4* r = L.rec + 3 * (int64_t)q;
-            const float4 r0 = r[0], r1 = r[1], r2 = r[2];
             sq[threadIdx.x] = q;
-            s0[threadIdx.x] = r0;
-            s1[threadIdx.x] = make_float4(r1.x, r1.y, skip_power(r1.y), 0.f);
-            s2[threadIdx.x] = make_float4(r1.z, r1.w, r2.x, 0.f);
+            stage(L, q, s0, s1, s2, threadIdx.x);
         }
         {  // each warp clears its own slots
             float4* w4 = reinterpret_cast<float4*>(wacc);
-            for (int i = lane; i < RB * NG / 4; i += 32) w4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int i = lane; i < RT * NG / 4; i += 32) w4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
         }
         __syncthreads();
         for (int jj = min(cnt, wmax - b0) - 1; jj >= 0; jj--) {
             const int j = b0 + jj;
+            const float4 a = s0[jj];
+            const float4 c = s1[jj];
+            const float dx = FSUB(a.x, fx);
             float val[NG];
 #pragma unroll
             for (int k = 0; k < NG; k++) val[k] = 0.f;
             bool contrib = false;
-            if (j < last) {
-                const float4 a = s0[jj];
-                const float4 c = s1[jj];
-                const float dx = FSUB(a.x, fx), dy = FSUB(a.y, fy);
+#pragma unroll
+            for (int p = 0; p < 2; p++) {
+                BwdPix& s = px[p];
+                if (j >= s.last) continue;
+                const float dy = FSUB(a.y, p ? fy1 : fy0);
                 const float power = ca_power(a.z, a.w, c.x, dx, dy);
-                if (power <= 0.0f && power >= c.z) {
-                    nexp++;
-                    const float G = ca_exp_core(power);
-                    const float oG = FMUL(c.y, G);
-                    const float alpha = fminf(ALPHA_MAX, oG);
-                    if (alpha >= ALPHA_MIN) {
-                        contrib = true;
-                        const float one_m = 1.0f - alpha;
-                        const float inv_one_m = __fdividef(1.0f, one_m);
-                        T = T * inv_one_m;
-                        const float w = alpha * T;
-                        const float4 col = s2[jj];
-                        acc0 = a_prev * c0p + (1.f - a_prev) * acc0;
-                        acc1 = a_prev * c1p + (1.f - a_prev) * acc1;
-                        acc2 = a_prev * c2p + (1.f - a_prev) * acc2;
-                        float dLda = (col.x - acc0) * dL0 + (col.y - acc1) * dL1 + (col.z - acc2) * dL2;
-                        dLda = dLda * T - T_fin * inv_one_m * dL_bg;
-                        a_prev = alpha;
-                        c0p = col.x; c1p = col.y; c2p = col.z;
-                        const bool clamped = oG > ALPHA_MAX;
-                        const float dLdG = clamped ? 0.f : c.y * dLda;
-                        const float dLdo = clamped ? 0.f : G * dLda;
-                        const float dLdpw = G * dLdG;
-                        const float gx = dLdpw * -(a.z * dx + a.w * dy) * hw;
-                        const float gy = dLdpw * -(c.x * dy + a.w * dx) * hh;
-                        val[0] = gx;
-                        val[1] = gy;
-                        const float n2 = gx * gx + gy * gy;
-                        val[2] = n2 > 0.f ? n2 * rsqrtf(n2) : 0.f;
-                        val[3] = -0.5f * dLdpw * dx * dx;
-                        val[4] = -dLdpw * dx * dy;
-                        val[5] = -0.5f * dLdpw * dy * dy;
-                        val[6] = dLdo;
-                        val[7] = w * dL0;
-                        val[8] = w * dL1;
-                        val[9] = w * dL2;
-                    }
-                }
+                if (power > 0.0f || power < c.z) continue;
+                nexp++;
+                const float G = ca_exp_core(power);
+                const float oG = FMUL(c.y, G);
+                const float alpha = fminf(ALPHA_MAX, oG);
+                if (alpha < ALPHA_MIN) continue;
+                contrib = true;
+                const float inv_one_m = __fdividef(1.0f, 1.0f - alpha);
+                s.T = s.T * inv_one_m;
+                const float w = alpha * s.T;
+                const float4 col = s2[jj];
+                s.acc0 = s.a_prev * s.c0p + (1.f - s.a_prev) * s.acc0;
+                s.acc1 = s.a_prev * s.c1p + (1.f - s.a_prev) * s.acc1;
+                s.acc2 = s.a_prev * s.c2p + (1.f - s.a_prev) * s.acc2;
+                float dLda = (col.x - s.acc0) * s.dL0 + (col.y - s.acc1) * s.dL1 + (col.z - s.acc2) * s.dL2;
+                dLda = dLda * s.T - s.T_fin * inv_one_m * s.dL_bg;
+                s.a_prev = alpha;
+                s.c0p = col.x; s.c1p = col.y; s.c2p = col.z;
+                const bool clamped = oG > ALPHA_MAX;
+                const float dLdG = clamped ? 0.f : c.y * dLda;
+                const float dLdo = clamped ? 0.f : G * dLda;
+                const float dLdpw = G * dLdG;
+                const float gx = dLdpw * -(a.z * dx + a.w * dy) * hw;
+                const float gy = dLdpw * -(c.x * dy + a.w * dx) * hh;
+                val[0] += gx;
+                val[1] += gy;
+                const float n2 = gx * gx + gy * gy;
+                val[2] += n2 > 0.f ? n2 * rsqrtf(n2) : 0.f;
+                val[3] += -0.5f * dLdpw * dx * dx;
+                val[4] += -dLdpw * dx * dy;
+                val[5] += -0.5f * dLdpw * dy * dy;
+                val[6] += dLdo;
+                val[7] += w * s.dL0;
+                val[8] += w * s.dL1;
+                val[9] += w * s.dL2;
             }
             if (__any_sync(FULLR, contrib)) {
-                const float s = warp_transpose_reduce10(val, lane);
-                if (owner) wacc[jj * NG + my_id] = s;
+                const float sum = warp_transpose_reduce10(val, lane);
+                if (owner) wacc[jj * NG + my_id] = sum;
             }
         }
         __syncthreads();
         for (int i = threadIdx.x; i < cnt * NG; i += RT) {
             float s = 0.f;
 #pragma unroll
-            for (int w = 0; w < RT / 32; w++) s += sacc[w][i];
+            for (int w = 0; w < NWR; w++) s += sacc[w][i];
             if (s != 0.f) {
                 const int jj = i / NG, k = i - jj * NG;
                 atomicAdd(&L.pgrad[(int64_t)sq[jj] * PG_STRIDE + k], s);

@@ -222,16 +222,21 @@ __global__ void k_pair_tiles(Launch L, const uint2* __restrict__ rect, int* __re
 }
 
 // Duplication in depth order: pair i's entries are ebase[i] + (row-major tile index
-// in its rect), key = view·T + tile.  A warp takes 32 consecutive pairs and writes
-// their entries together: lane l handles entries l, l+32, … of the warp's run,
-// finding its pair by a search over the warp's inclusive tile-count prefix, so
-// consecutive lanes write consecutive addresses.
+// in its rect), key = view·T + tile.  A warp takes 32 consecutive pairs, whose
+// entries form one contiguous run; each lane writes its own pair's entries into a
+// per-warp shared buffer (a row-major walk of its rect, no division) a chunk of
+// DUP_CHUNK entries at a time, and the warp copies each chunk out with coalesced
+// stores.
+constexpr int DUP_CHUNK = 256;
+
 __global__ __launch_bounds__(256) void k_dup(Launch L, const uint32_t* __restrict__ order,
                                              const uint2* __restrict__ rect, const int* __restrict__ ebase) {
+    __shared__ uint2 buf[8][DUP_CHUNK];
     const int Q = (int)min((int64_t)L.counters[C_Q], L.cap_pairs);
-    const int lane = threadIdx.x & 31;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    uint2* wb = buf[wid];
     const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
-    for (int64_t w0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32; w0 < Q; w0 += nwarps * 32) {
+    for (int64_t w0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + wid) * 32; w0 < Q; w0 += nwarps * 32) {
         const int64_t i = w0 + lane;
         uint2 r = make_uint2(0u, 0u);
         uint32_t q = 0;
@@ -240,45 +245,54 @@ __global__ __launch_bounds__(256) void k_dup(Launch L, const uint32_t* __restric
             q = order[i];
         }
         const int rx0 = r.x & 0xffff, ry0 = r.x >> 16, rx1 = r.y & 0xffff, ry1 = r.y >> 16;
-        const int w = rx1 - rx0;
-        const int cnt = (rx1 > rx0 && ry1 > ry0) ? w * (ry1 - ry0) : 0;
+        const int cnt = (rx1 > rx0 && ry1 > ry0) ? (rx1 - rx0) * (ry1 - ry0) : 0;
         int inc = cnt;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const int y = __shfl_up_sync(FULLS, inc, o);
             if (lane >= o) inc += y;
         }
+        const int excl = inc - cnt;
         const int total = __shfl_sync(FULLS, inc, 31);
         const int64_t e0 = __shfl_sync(FULLS, (int64_t)(i < Q ? ebase[i] : 0), 0);
-        const uint32_t vb = (i < Q && cnt > 0) ? (uint32_t)view_of_pair(L, q) * (uint32_t)L.T : 0u;
-        for (int base = 0; base < total; base += 32) {  // warp-uniform rounds, all lanes active
-            const int k = base + lane;
-            // owner = first lane whose inclusive prefix exceeds k (monotone ⇒ binary search)
-            int lo = 0;
-#pragma unroll
-            for (int step = 16; step > 0; step >>= 1) {
-                const int cand = lo + step - 1;
-                if (__shfl_sync(FULLS, inc, cand) <= k) lo += step;
+        const uint32_t vb = cnt > 0 ? (uint32_t)view_of_pair(L, q) * (uint32_t)L.T : 0u;
+        // this lane's walk position (row-major in its rect), advanced chunk by chunk
+        int t = 0, tx = rx0, ty = ry0;
+        for (int c0 = 0; c0 < total; c0 += DUP_CHUNK) {
+            const int c1 = min(total, c0 + DUP_CHUNK);
+            for (; t < cnt && excl + t < c1; t++) {
+                wb[excl + t - c0] = make_uint2(vb + ty * L.TX + tx, q);
+                if (++tx == rx1) {
+                    tx = rx0;
+                    ty++;
+                }
             }
-            const int owner = min(lo, 31);
-            const int excl = __shfl_sync(FULLS, inc - cnt, owner);
-            const int ow = __shfl_sync(FULLS, w, owner);
-            const int ox = __shfl_sync(FULLS, rx0, owner);
-            const int oy = __shfl_sync(FULLS, ry0, owner);
-            const uint32_t ob = __shfl_sync(FULLS, vb, owner);
-            const uint32_t oq = __shfl_sync(FULLS, q, owner);
-            if (k < total) {
-                const int loc = k - excl;
-                const int ty = oy + loc / ow, tx = ox + loc % ow;
-                const int64_t e = e0 + k;
+            __syncwarp();
+            for (int k = lane; k < c1 - c0; k += 32) {
+                const int64_t e = e0 + c0 + k;
+                const uint2 kv = wb[k];
                 if (e < L.cap_entries) {
-                    L.key[e] = ob + ty * L.TX + tx;
-                    L.val[e] = oq;
+                    L.key[e] = kv.x;
+                    L.val[e] = kv.y;
                 } else {
                     L.counters[C_OVERFLOW] = 1;
                 }
             }
+            __syncwarp();
         }
+    }
+}
+
+// S5 ranges from the sorted bucket keys: bucket b = [off[b], off[b+1]).  Entry e
+// opens every bucket in (key[e−1], key[e]]; the end closes the rest.
+__global__ void k_ranges(Launch L, const uint32_t* __restrict__ keys) {
+    const int64_t K = min((int64_t)L.counters[C_K], L.cap_entries);
+    const int64_t nb = (int64_t)L.V * L.T;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e <= K; e += stride) {
+        const int64_t hi = e < K ? (int64_t)keys[e] : nb;           // buckets up to hi start at e
+        const int64_t lo = e > 0 ? (int64_t)keys[e - 1] + 1 : 0;    // first bucket not yet opened
+        for (int64_t b = lo; b <= hi; b++) L.bucket_off[b] = (int)e;
     }
 }
 
@@ -314,7 +328,7 @@ cudaError_t launch_sort_pairs(const Launch& L, const uint32_t** order_out, const
 // S3: duplicate in depth order (entry offsets from a scan of the tile counts).
 cudaError_t launch_dup_sort(const Launch& L, const uint32_t* order, const uint2* rect, cudaStream_t s) {
     k_pair_tiles<<<grid_for(L.cap_pairs, 256), 256, 0, s>>>(L, rect, L.ecount);
-    cudaError_t e = scan_exclusive(L.ecount, (int)L.cap_pairs, nullptr, L.scan_tmp, s);
+    cudaError_t e = scan_exclusive(L.ecount, (int)L.cap_pairs, L.counters + C_K, L.scan_tmp, s);  // K
     if (e != cudaSuccess) return e;
     k_dup<<<grid_for(L.cap_pairs, 256), 256, 0, s>>>(L, order, rect, L.ecount);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
@@ -329,6 +343,7 @@ cudaError_t launch_sort_entries(const Launch& L, uint32_t** sorted_vals, cudaStr
                         L.rs_counts, L.scan_tmp, s, &e);
     *sorted_vals = (np & 1) ? L.val2 : L.val;
     if (e != cudaSuccess) return e;
+    k_ranges<<<grid_for(L.cap_entries + 1, 256), 256, 0, s>>>(L, (np & 1) ? L.key2 : L.key);
     k_max_bucket<<<64, 256, 0, s>>>(L);
     return cudaGetLastError();
 }

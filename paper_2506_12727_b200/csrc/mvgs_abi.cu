@@ -309,7 +309,6 @@ mvgs_status mvgs_preprocess(mvgs_ctx* ctx, const mvgs_gaussians* g, const mvgs_c
     ctx->last_stream = s;
 
     CK(cudaMemsetAsync(ctx->d_counters, 0, sizeof(int) * C_NCOUNTERS, s));
-    CK(cudaMemsetAsync(ctx->d_bucket, 0, sizeof(int) * (nbuck + 1), s));
     if (NB > 0) {
         { STAGE(ST_COUNT); CK(launch_count(L, s)); }                                                 // S1
         { STAGE(ST_SCAN_PAIRS); CK(scan_exclusive(ctx->d_blk, (int)nblk, ctx->d_counters + C_Q, ctx->d_scan, s)); }
@@ -317,14 +316,15 @@ mvgs_status mvgs_preprocess(mvgs_ctx* ctx, const mvgs_gaussians* g, const mvgs_c
     } else {
         CK(cudaMemsetAsync(ctx->d_blk, 0, sizeof(int) * (nblk + 1), s));
     }
-    { STAGE(ST_SCAN_BUCKETS); CK(scan_exclusive(ctx->d_bucket, (int)nbuck, ctx->d_counters + C_K, ctx->d_scan, s)); }
     const uint32_t* order = L.pval;
     const uint2* rect = L.prect;
     uint32_t* sorted = L.val;
     if (NB > 0) {
         { STAGE(ST_SORT_PAIRS); CK(launch_sort_pairs(L, &order, &rect, s)); }                        // S4a
         { STAGE(ST_DUP); CK(launch_dup_sort(L, order, rect, s)); }                                   // S3
-        { STAGE(ST_SORT_ENTRIES); CK(launch_sort_entries(L, &sorted, s)); }                          // S4b
+        { STAGE(ST_SORT_ENTRIES); CK(launch_sort_entries(L, &sorted, s)); }                          // S4b + S5
+    } else {
+        CK(cudaMemsetAsync(ctx->d_bucket, 0, sizeof(int) * (nbuck + 1), s));
     }
     L.sorted = sorted;
     ctx->state = 1;
