@@ -49,7 +49,7 @@ struct Launch {  // everything a kernel needs about the current batch
     int* scan_tmp;    // scan block sums
     const uint32_t* sorted;  // [K] pair index of every entry in (view, tile, depth, gid) order
     int* counters;    // [C_NCOUNTERS]
-    unsigned long long* counters64;  // [2]: fwd / bwd (pixel, entry) evaluations
+    unsigned long long* counters64;  // [8]: fwd/bwd evaluations, fwd/bwd exps, entries needed
 };
 
 }  // namespace mvgs

@@ -185,18 +185,17 @@ __global__ __launch_bounds__(BLK) void k_project(Launch L) {
     constexpr int NK = (D + 1) * (D + 1), NS = NK * 3, SS = NS | 1;
     extern __shared__ float sh_s[];  // [BLK][SS] SH rows, coalesced block load, odd stride
     __shared__ int wc[BLK / 32][32];
+    __shared__ int sboff[32];  // first pair slot of this block in each view of the chunk
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t g0 = (int64_t)blockIdx.x * BLK;
     const int64_t g = g0 + threadIdx.x;
     const bool valid = g < L.P;
-    {
+    {  // coalesced row loads: warp w takes rows w, w+8, …; lanes walk the row
         const int nb = (int)min((int64_t)BLK, L.P - g0);
         const float* src = L.sh + g0 * (int64_t)L.sh_stride * 3;
         const int rowlen = L.sh_stride * 3;
-        for (int i = threadIdx.x; i < nb * NS; i += BLK) {
-            const int r = i / NS, k = i - r * NS;
-            sh_s[r * SS + k] = src[(int64_t)r * rowlen + k];
-        }
+        for (int r = warp; r < nb; r += BLK / 32)
+            for (int k = lane; k < NS; k += 32) sh_s[r * SS + k] = src[(int64_t)r * rowlen + k];
     }
     const float* sh = sh_s + threadIdx.x * SS;
     float mx = 0.f, my = 0.f, mz = 0.f;
@@ -208,6 +207,7 @@ __global__ __launch_bounds__(BLK) void k_project(Launch L) {
         ca_activate(L.log_scales + 3 * g, L.quats + 4 * g, L.opac[g], a);
     }
     const unsigned lt = (1u << lane) - 1u;
+    unsigned long long my_tiles = 0;  // entries this Gaussian needs (K needed, capacity-independent)
     for (int v0 = 0; v0 < L.V; v0 += 32) {
         const int nv = min(32, L.V - v0);
         for (int k = 0; k < nv; k++) {
@@ -216,6 +216,7 @@ __global__ __launch_bounds__(BLK) void k_project(Launch L) {
             const unsigned bal = __ballot_sync(FULL, vis);
             if (lane == 0) wc[warp][k] = __popc(bal);
         }
+        if (threadIdx.x < nv) sboff[threadIdx.x] = L.blk_off[(int64_t)(v0 + threadIdx.x) * L.NB + blockIdx.x];
         __syncthreads();
         for (int k = 0; k < nv; k++) {
             const int v = v0 + k;
@@ -225,7 +226,7 @@ __global__ __launch_bounds__(BLK) void k_project(Launch L) {
             if (!vis) continue;
             int pre = 0;
             for (int w = 0; w < warp; w++) pre += wc[w][k];
-            const int64_t pair = (int64_t)L.blk_off[(int64_t)v * L.NB + blockIdx.x] + pre + __popc(bal & lt);
+            const int64_t pair = (int64_t)sboff[k] + pre + __popc(bal & lt);
             Proj p;
             ca_project(c, mx, my, mz, a.Sig, L.TX, L.TY, p);
             const int tiles = p.ok ? (p.rx1 - p.rx0) * (p.ry1 - p.ry0) : 0;
@@ -279,9 +280,13 @@ __global__ __launch_bounds__(BLK) void k_project(Launch L) {
                 pg[0] = pg[1] = pg[2] = make_float4(0.f, 0.f, 0.f, 0.f);
             }
             if (tiles > 0) atomicAdd(&L.counters[C_NVIS], 1);  // warp-aggregated by ptxas
+            my_tiles += (unsigned long long)tiles;
         }
         __syncthreads();
     }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) my_tiles += __shfl_xor_sync(FULL, my_tiles, o);
+    if (lane == 0 && my_tiles) atomicAdd(&L.counters64[4], my_tiles);
 }
 
 template <int D>

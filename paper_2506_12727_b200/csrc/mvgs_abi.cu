@@ -199,8 +199,8 @@ mvgs_status mvgs_create(mvgs_ctx** out, int device, int64_t max_pairs, int64_t m
         (e = alloc_sort_scratch(ctx)) != cudaSuccess ||
         (e = cudaMalloc(&ctx->d_counters, sizeof(int) * C_NCOUNTERS)) != cudaSuccess ||
         (e = cudaMemset(ctx->d_counters, 0, sizeof(int) * C_NCOUNTERS)) != cudaSuccess ||
-        (e = cudaMalloc(&ctx->d_counters64, sizeof(unsigned long long) * 4)) != cudaSuccess ||
-        (e = cudaMemset(ctx->d_counters64, 0, sizeof(unsigned long long) * 4)) != cudaSuccess ||
+        (e = cudaMalloc(&ctx->d_counters64, sizeof(unsigned long long) * 8)) != cudaSuccess ||
+        (e = cudaMemset(ctx->d_counters64, 0, sizeof(unsigned long long) * 8)) != cudaSuccess ||
         (e = cudaEventCreateWithFlags(&ctx->cams_ev, cudaEventDisableTiming)) != cudaSuccess) {
         mvgs_destroy(ctx);
         return MVGS_ERR_CUDA;
@@ -309,6 +309,7 @@ mvgs_status mvgs_preprocess(mvgs_ctx* ctx, const mvgs_gaussians* g, const mvgs_c
     ctx->last_stream = s;
 
     CK(cudaMemsetAsync(ctx->d_counters, 0, sizeof(int) * C_NCOUNTERS, s));
+    CK(cudaMemsetAsync(ctx->d_counters64 + 4, 0, sizeof(unsigned long long), s));
     if (NB > 0) {
         { STAGE(ST_COUNT); CK(launch_count(L, s)); }                                                 // S1
         { STAGE(ST_SCAN_PAIRS); CK(scan_exclusive(ctx->d_blk, (int)nblk, ctx->d_counters + C_Q, ctx->d_scan, s)); }
@@ -379,12 +380,12 @@ mvgs_status mvgs_query(mvgs_ctx* ctx, mvgs_stats* out) {
     CK(cudaSetDevice(ctx->device));
     CK(cudaDeviceSynchronize());
     int h[C_NCOUNTERS];
-    unsigned long long h64[4];
+    unsigned long long h64[5];
     CK(cudaMemcpy(h, ctx->d_counters, sizeof(h), cudaMemcpyDeviceToHost));
     CK(cudaMemcpy(h64, ctx->d_counters64, sizeof(h64), cudaMemcpyDeviceToHost));
     memset(out, 0, sizeof(*out));
     out->Q = h[C_Q];
-    out->K = h[C_K];
+    out->K = std::max((int64_t)h[C_K], (int64_t)h64[4]);  // entries needed, even past a pair overflow
     out->cap_pairs = ctx->cap_pairs;
     out->cap_entries = ctx->cap_entries;
     out->max_bucket = h[C_MAXB];

@@ -209,10 +209,14 @@ class Rasterizer:
         preprocess(self.ctx, g, self.cams, bg, stream)
         if auto_reserve:
             st = query(self.ctx, raise_on_capacity=False)
-            if st["overflow"]:
+            for _ in range(3):
+                if not st["overflow"]:
+                    break
                 reserve(self.ctx, int(st["Q"] * 1.1) + 1024, int(st["K"] * 1.1) + 4096)
                 preprocess(self.ctx, g, self.cams, bg, stream)
-                st = query(self.ctx)
+                st = query(self.ctx, raise_on_capacity=False)
+            if st["overflow"]:
+                query(self.ctx)  # raises with the library's message
             self.stats = st
 
     def alloc_forward(self):
