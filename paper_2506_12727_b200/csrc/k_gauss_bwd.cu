@@ -48,15 +48,29 @@ __global__ __launch_bounds__(BLK, 2) void k_gauss_bwd(Launch L, mvgs_grads gr, m
     const int64_t g0 = (int64_t)blockIdx.x * BLK;
     const int64_t g = g0 + threadIdx.x;
     const bool valid = g < L.P;
-    {  // coalesced row loads: warp w takes rows w, w+8, …; lanes walk the row
+    {  // coalesced block load, 8 loads in flight per thread before the stores
         const int nb = (int)min((int64_t)BLK, L.P - g0);
         const float* src = L.sh + g0 * (int64_t)L.sh_stride * 3;
         const int rowlen = L.sh_stride * 3;
-        for (int r = warp; r < nb; r += BLK / 32)
-            for (int k = lane; k < NS; k += 32) {
-                sh_s[r * SS + k] = src[(int64_t)r * rowlen + k];
-                dsh_s[r * SS + k] = 0.f;
+        const int n = nb * NS;
+        for (int i0 = threadIdx.x; i0 < n; i0 += 8 * BLK) {
+            float t[8];
+#pragma unroll
+            for (int u = 0; u < 8; u++) {
+                const int i = i0 + u * BLK;
+                const int r = i / NS, k = i - r * NS;  // NS constexpr: mul-shift
+                t[u] = i < n ? src[(int64_t)r * rowlen + k] : 0.f;
             }
+#pragma unroll
+            for (int u = 0; u < 8; u++) {
+                const int i = i0 + u * BLK;
+                const int r = i / NS, k = i - r * NS;
+                if (i < n) {
+                    sh_s[r * SS + k] = t[u];
+                    dsh_s[r * SS + k] = 0.f;
+                }
+            }
+        }
     }
     __syncthreads();
     const float* sh = sh_s + threadIdx.x * SS;
@@ -255,8 +269,10 @@ __global__ __launch_bounds__(BLK, 2) void k_gauss_bwd(Launch L, mvgs_grads gr, m
         const int nb = (int)min((int64_t)BLK, L.P - g0);
         float* dst = gr.d_sh + g0 * (int64_t)L.sh_stride * 3;
         const int rowlen = L.sh_stride * 3;
-        for (int r = warp; r < nb; r += BLK / 32)
-            for (int k = lane; k < rowlen; k += 32) dst[(int64_t)r * rowlen + k] = k < NS ? dsh_s[r * SS + k] : 0.f;
+        for (int i = threadIdx.x; i < nb * rowlen; i += BLK) {
+            const int r = i / rowlen, k = i - r * rowlen;
+            dst[i] = k < NS ? dsh_s[r * SS + k] : 0.f;
+        }
     }
     if (!valid) return;
     // Σ = M Mᵀ, M = R diag(s): ∂L/∂M = 2 G M (G symmetric)

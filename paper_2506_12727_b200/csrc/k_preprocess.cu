@@ -190,12 +190,26 @@ __global__ __launch_bounds__(BLK) void k_project(Launch L) {
     const int64_t g0 = (int64_t)blockIdx.x * BLK;
     const int64_t g = g0 + threadIdx.x;
     const bool valid = g < L.P;
-    {  // coalesced row loads: warp w takes rows w, w+8, …; lanes walk the row
+    {  // coalesced block load, 8 loads in flight per thread before the stores
         const int nb = (int)min((int64_t)BLK, L.P - g0);
         const float* src = L.sh + g0 * (int64_t)L.sh_stride * 3;
         const int rowlen = L.sh_stride * 3;
-        for (int r = warp; r < nb; r += BLK / 32)
-            for (int k = lane; k < NS; k += 32) sh_s[r * SS + k] = src[(int64_t)r * rowlen + k];
+        const int n = nb * NS;
+        for (int i0 = threadIdx.x; i0 < n; i0 += 8 * BLK) {
+            float t[8];
+#pragma unroll
+            for (int u = 0; u < 8; u++) {
+                const int i = i0 + u * BLK;
+                const int r = i / NS, k = i - r * NS;  // NS constexpr: mul-shift
+                t[u] = i < n ? src[(int64_t)r * rowlen + k] : 0.f;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; u++) {
+                const int i = i0 + u * BLK;
+                const int r = i / NS, k = i - r * NS;
+                if (i < n) sh_s[r * SS + k] = t[u];
+            }
+        }
     }
     const float* sh = sh_s + threadIdx.x * SS;
     float mx = 0.f, my = 0.f, mz = 0.f;

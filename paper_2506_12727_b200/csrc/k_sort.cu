@@ -222,21 +222,16 @@ __global__ void k_pair_tiles(Launch L, const uint2* __restrict__ rect, int* __re
 }
 
 // Duplication in depth order: pair i's entries are ebase[i] + (row-major tile index
-// in its rect), key = view·T + tile.  A warp takes 32 consecutive pairs, whose
-// entries form one contiguous run; each lane writes its own pair's entries into a
-// per-warp shared buffer (a row-major walk of its rect, no division) a chunk of
-// DUP_CHUNK entries at a time, and the warp copies each chunk out with coalesced
-// stores.
-constexpr int DUP_CHUNK = 256;
-
+// in its rect), key = view·T + tile.  A warp takes 32 consecutive pairs and writes
+// their entries together: lane l handles entries l, l+32, … of the warp's run,
+// finding its pair by a search over the warp's inclusive tile-count prefix, so
+// consecutive lanes write consecutive addresses.
 __global__ __launch_bounds__(256) void k_dup(Launch L, const uint32_t* __restrict__ order,
                                              const uint2* __restrict__ rect, const int* __restrict__ ebase) {
-    __shared__ uint2 buf[8][DUP_CHUNK];
     const int Q = (int)min((int64_t)L.counters[C_Q], L.cap_pairs);
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    uint2* wb = buf[wid];
+    const int lane = threadIdx.x & 31;
     const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
-    for (int64_t w0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + wid) * 32; w0 < Q; w0 += nwarps * 32) {
+    for (int64_t w0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32; w0 < Q; w0 += nwarps * 32) {
         const int64_t i = w0 + lane;
         uint2 r = make_uint2(0u, 0u);
         uint32_t q = 0;
@@ -245,40 +240,44 @@ __global__ __launch_bounds__(256) void k_dup(Launch L, const uint32_t* __restric
             q = order[i];
         }
         const int rx0 = r.x & 0xffff, ry0 = r.x >> 16, rx1 = r.y & 0xffff, ry1 = r.y >> 16;
-        const int cnt = (rx1 > rx0 && ry1 > ry0) ? (rx1 - rx0) * (ry1 - ry0) : 0;
+        const int w = rx1 - rx0;
+        const int cnt = (rx1 > rx0 && ry1 > ry0) ? w * (ry1 - ry0) : 0;
         int inc = cnt;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const int y = __shfl_up_sync(FULLS, inc, o);
             if (lane >= o) inc += y;
         }
-        const int excl = inc - cnt;
         const int total = __shfl_sync(FULLS, inc, 31);
         const int64_t e0 = __shfl_sync(FULLS, (int64_t)(i < Q ? ebase[i] : 0), 0);
-        const uint32_t vb = cnt > 0 ? (uint32_t)view_of_pair(L, q) * (uint32_t)L.T : 0u;
-        // this lane's walk position (row-major in its rect), advanced chunk by chunk
-        int t = 0, tx = rx0, ty = ry0;
-        for (int c0 = 0; c0 < total; c0 += DUP_CHUNK) {
-            const int c1 = min(total, c0 + DUP_CHUNK);
-            for (; t < cnt && excl + t < c1; t++) {
-                wb[excl + t - c0] = make_uint2(vb + ty * L.TX + tx, q);
-                if (++tx == rx1) {
-                    tx = rx0;
-                    ty++;
-                }
+        const uint32_t vb = (i < Q && cnt > 0) ? (uint32_t)view_of_pair(L, q) * (uint32_t)L.T : 0u;
+        for (int base = 0; base < total; base += 32) {  // warp-uniform rounds, all lanes active
+            const int k = base + lane;
+            // owner = first lane whose inclusive prefix exceeds k (monotone ⇒ binary search)
+            int lo = 0;
+#pragma unroll
+            for (int step = 16; step > 0; step >>= 1) {
+                const int cand = lo + step - 1;
+                if (__shfl_sync(FULLS, inc, cand) <= k) lo += step;
             }
-            __syncwarp();
-            for (int k = lane; k < c1 - c0; k += 32) {
-                const int64_t e = e0 + c0 + k;
-                const uint2 kv = wb[k];
+            const int owner = min(lo, 31);
+            const int excl = __shfl_sync(FULLS, inc - cnt, owner);
+            const int ow = __shfl_sync(FULLS, w, owner);
+            const int ox = __shfl_sync(FULLS, rx0, owner);
+            const int oy = __shfl_sync(FULLS, ry0, owner);
+            const uint32_t ob = __shfl_sync(FULLS, vb, owner);
+            const uint32_t oq = __shfl_sync(FULLS, q, owner);
+            if (k < total) {
+                const int loc = k - excl;
+                const int ty = oy + loc / ow, tx = ox + loc % ow;
+                const int64_t e = e0 + k;
                 if (e < L.cap_entries) {
-                    L.key[e] = kv.x;
-                    L.val[e] = kv.y;
+                    L.key[e] = ob + ty * L.TX + tx;
+                    L.val[e] = oq;
                 } else {
                     L.counters[C_OVERFLOW] = 1;
                 }
             }
-            __syncwarp();
         }
     }
 }
