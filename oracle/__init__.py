@@ -62,6 +62,7 @@ def lib():
         L.oracle_backward.argtypes = [vp, vp]
         L.oracle_num_entries.restype = i64
         L.oracle_num_entries.argtypes = [vp]
+        L.oracle_phase_times.argtypes = [vp, vp]
         L.oracle_decision_hash.restype = C.c_uint64
         L.oracle_decision_hash.argtypes = [vp]
         for name, n in [("oracle_get_image", 3), ("oracle_get_lists", 2), ("oracle_get_pairs", 3),
@@ -132,6 +133,12 @@ class Oracle:
     def forward(self):
         lib().oracle_forward(self._h)
         return self.image()
+
+    def phase_times(self):
+        """Seconds: (projection O1–O2, lists O3–O4, per-pixel O5–O6, per-Gaussian O7–O8)."""
+        out = np.zeros(4)
+        lib().oracle_phase_times(self._h, _p(out))
+        return out
 
     def decision_hash(self) -> int:
         return int(lib().oracle_decision_hash(self._h))

@@ -33,8 +33,10 @@
  * Compile: gcc -O2 -std=c11 -ffp-contract=off -fno-fast-math -fPIC -shared
  * (no contraction, IEEE float on SSE, denormals kept).
  */
+#define _POSIX_C_SOURCE 199309L
 #include <math.h>
 #include <stdint.h>
+#include <time.h>
 #include <stdlib.h>
 #include <string.h>
 
@@ -405,6 +407,7 @@ typedef struct {
     uint8_t *mask;         /* [V*T] tiles to render (NULL = all) — sampled full-size checks */
     uint64_t dhash;        /* hash of every discrete decision (FD tests)     */
     int64_t npg;           /* number of pairs with fp64 state (= rows of pg)  */
+    double t_phase[4];     /* seconds: O1–O2 projection, O3–O4 lists, O5–O6 per pixel, O7–O8 per Gaussian */
     double *d_means, *d_ls, *d_q, *d_op, *d_sh, *e1, *e2, *eold, *vis;
 } oracle_t;
 
@@ -433,6 +436,13 @@ void oracle_destroy(oracle_t *h)
     free(h->d_means); free(h->d_ls); free(h->d_q); free(h->d_op); free(h->d_sh);
     free(h->e1); free(h->e2); free(h->eold); free(h->vis);
     free(h);
+}
+
+static double now_s(void)
+{
+    struct timespec ts;
+    clock_gettime(CLOCK_MONOTONIC, &ts);
+    return ts.tv_sec + 1e-9 * ts.tv_nsec;
 }
 
 static int rect_hits_mask(const oracle_t *h, int v, const p32_t *p)
@@ -478,6 +488,7 @@ oracle_t *oracle_create_masked(const og_scene *g, const og_cam *cams, int V, con
         memcpy(h->mask, tile_mask, (size_t)V * h->T);
     }
     int64_t P = g->P;
+    double t0 = now_s();
     h->p32 = (p32_t *)calloc((size_t)V * P + 1, sizeof(p32_t));
     h->p64i = (int32_t *)malloc(sizeof(int32_t) * ((size_t)V * P + 1));
     h->o32 = (float *)calloc(P + 1, sizeof(float));
@@ -503,6 +514,8 @@ oracle_t *oracle_create_masked(const og_scene *g, const og_cam *cams, int V, con
             int32_t k = h->p64i[(size_t)v * P + i];
             if (k >= 0) project64(g, i, &h->g64[i], &cams[v], &h->p64[k]);
         }
+    double t1 = now_s();
+    h->t_phase[0] = t1 - t0;
     /* O3: count, offsets, fill; O4: sort each list */
     int64_t nb = (int64_t)V * h->T;
     h->off = (int64_t *)calloc(nb + 1, sizeof(int64_t));
@@ -540,6 +553,7 @@ oracle_t *oracle_create_masked(const og_scene *g, const og_cam *cams, int V, con
     for (int64_t k = 0; k < h->K; k++) h->gid[k] = ent[k].gid;
     free(ent);
     free(fill);
+    h->t_phase[1] = now_s() - t1;
     return h;
 }
 
@@ -829,8 +843,12 @@ int oracle_backward(oracle_t *h, const float *dLdC)
     ALLOC(d_sh, (size_t)P * h->g.sh_stride * 3);
     ALLOC(e1, P); ALLOC(e2, P); ALLOC(eold, P); ALLOC(vis, P);
 #undef ALLOC
+    double t0 = now_s();
     composite(h, dLdC);
+    double t1 = now_s();
     gauss_backward(h);
+    h->t_phase[2] = t1 - t0;
+    h->t_phase[3] = now_s() - t1;
     h->have_bwd = 1;
     return 0;
 }
@@ -842,6 +860,12 @@ int64_t oracle_num_entries(const oracle_t *h) { return h->K; }
  * and colour clamps of blended pairs).  Equal hashes ⇒ the fp64 value chain is one
  * smooth function between two runs (used to screen finite differences). */
 uint64_t oracle_decision_hash(const oracle_t *h) { return h->dhash; }
+
+/* Wall-clock seconds of the phases of the last run (timing the CPU baseline). */
+void oracle_phase_times(const oracle_t *h, double out[4])
+{
+    for (int k = 0; k < 4; k++) out[k] = h->t_phase[k];
+}
 
 void oracle_get_image(const oracle_t *h, double *rgb, double *Tfin, int32_t *ncon)
 {

@@ -25,6 +25,75 @@ __constant__ float g_SH3[7] = {-0.5900435899266435f, 2.890611442640554f, -0.4570
                                0.3731763325901154f, -0.4570457994644658f, 1.445305721320277f,
                                -0.5900435899266435f};
 
+// Values-only recomputation for the chain rule (no decision depends on them: the
+// Jacobian clamps come from the pair flags written by k_project), so fast
+// reciprocal / exp / rsqrt are used instead of the canonical arithmetic.
+struct FastActiv {
+    float o, s[3], q[4], inv_norm, R[9], Sig[6];
+};
+
+__device__ __forceinline__ void fast_activate(const float* __restrict__ ls, const float* __restrict__ qr, float logit,
+                                              FastActiv& a) {
+    a.o = 1.f / (1.f + __expf(-logit));
+    a.s[0] = __expf(ls[0]);
+    a.s[1] = __expf(ls[1]);
+    a.s[2] = __expf(ls[2]);
+    float w = qr[0], x = qr[1], y = qr[2], z = qr[3];
+    const float inv = rsqrtf(w * w + x * x + y * y + z * z);
+    a.inv_norm = inv;
+    w *= inv; x *= inv; y *= inv; z *= inv;
+    a.q[0] = w; a.q[1] = x; a.q[2] = y; a.q[3] = z;
+    float* R = a.R;
+    R[0] = 1.f - 2.f * (y * y + z * z); R[1] = 2.f * (x * y - w * z); R[2] = 2.f * (x * z + w * y);
+    R[3] = 2.f * (x * y + w * z); R[4] = 1.f - 2.f * (x * x + z * z); R[5] = 2.f * (y * z - w * x);
+    R[6] = 2.f * (x * z - w * y); R[7] = 2.f * (y * z + w * x); R[8] = 1.f - 2.f * (x * x + y * y);
+    float M[9];
+#pragma unroll
+    for (int r = 0; r < 3; r++)
+#pragma unroll
+        for (int c = 0; c < 3; c++) M[3 * r + c] = R[3 * r + c] * a.s[c];
+    a.Sig[0] = M[0] * M[0] + M[1] * M[1] + M[2] * M[2];
+    a.Sig[1] = M[0] * M[3] + M[1] * M[4] + M[2] * M[5];
+    a.Sig[2] = M[0] * M[6] + M[1] * M[7] + M[2] * M[8];
+    a.Sig[3] = M[3] * M[3] + M[4] * M[4] + M[5] * M[5];
+    a.Sig[4] = M[3] * M[6] + M[4] * M[7] + M[5] * M[8];
+    a.Sig[5] = M[6] * M[6] + M[7] * M[7] + M[8] * M[8];
+}
+
+struct FastProj {
+    float tx, ty, tz, itz, uxc, uyc, T0[3], T1[3], a, b, c, det;
+};
+
+__device__ __forceinline__ void fast_project(const mvgs_camera& cam, float mx, float my, float mz, const float Sig[6],
+                                             uint32_t flags, FastProj& p) {
+    const float* R = cam.R;
+    p.tx = R[0] * mx + R[1] * my + R[2] * mz + cam.t[0];
+    p.ty = R[3] * mx + R[4] * my + R[5] * mz + cam.t[1];
+    p.tz = R[6] * mx + R[7] * my + R[8] * mz + cam.t[2];
+    p.itz = __frcp_rn(p.tz);
+    const float ux = p.tx * p.itz, uy = p.ty * p.itz;
+    const float limx = 0.65f * (float)cam.width / cam.fx, limy = 0.65f * (float)cam.height / cam.fy;
+    p.uxc = (flags & 8u) ? fminf(limx, fmaxf(-limx, ux)) : ux;   // clamp decisions from k_project (R4)
+    p.uyc = (flags & 16u) ? fminf(limy, fmaxf(-limy, uy)) : uy;
+    const float J00 = cam.fx * p.itz, J02 = -cam.fx * p.uxc * p.itz;
+    const float J11 = cam.fy * p.itz, J12 = -cam.fy * p.uyc * p.itz;
+#pragma unroll
+    for (int j = 0; j < 3; j++) {
+        p.T0[j] = J00 * R[j] + J02 * R[6 + j];
+        p.T1[j] = J11 * R[3 + j] + J12 * R[6 + j];
+    }
+    const float U00 = p.T0[0] * Sig[0] + p.T0[1] * Sig[1] + p.T0[2] * Sig[2];
+    const float U01 = p.T0[0] * Sig[1] + p.T0[1] * Sig[3] + p.T0[2] * Sig[4];
+    const float U02 = p.T0[0] * Sig[2] + p.T0[1] * Sig[4] + p.T0[2] * Sig[5];
+    const float U10 = p.T1[0] * Sig[0] + p.T1[1] * Sig[1] + p.T1[2] * Sig[2];
+    const float U11 = p.T1[0] * Sig[1] + p.T1[1] * Sig[3] + p.T1[2] * Sig[4];
+    const float U12 = p.T1[0] * Sig[2] + p.T1[1] * Sig[4] + p.T1[2] * Sig[5];
+    p.a = U00 * p.T0[0] + U01 * p.T0[1] + U02 * p.T0[2] + 0.3f;
+    p.b = U00 * p.T1[0] + U01 * p.T1[1] + U02 * p.T1[2];
+    p.c = U10 * p.T1[0] + U11 * p.T1[1] + U12 * p.T1[2] + 0.3f;
+    p.det = p.a * p.c - p.b * p.b;
+}
+
 // SH coefficients and their gradient live in shared memory, one padded row per
 // Gaussian (odd stride ⇒ conflict-free when each thread walks its own row);
 // the block's rows are loaded and stored with coalesced accesses.
@@ -76,12 +145,14 @@ __global__ __launch_bounds__(BLK, 2) void k_gauss_bwd(Launch L, mvgs_grads gr, m
     const float* sh = sh_s + threadIdx.x * SS;
     float* dsh = dsh_s + threadIdx.x * SS;
     float mx = 0.f, my = 0.f, mz = 0.f;
-    Activ a;
+    FastActiv a;
     if (valid) {
         mx = L.means[3 * g];
         my = L.means[3 * g + 1];
         mz = L.means[3 * g + 2];
-        ca_activate(L.log_scales + 3 * g, L.quats + 4 * g, L.opac[g], a);
+        fast_activate(L.log_scales + 3 * g, L.quats + 4 * g, L.opac[g], a);
+    } else {
+        fast_activate(L.log_scales, L.quats, 0.f, a);  // any finite values; unused
     }
     float dmx = 0.f, dmy = 0.f, dmz = 0.f;
     float G00 = 0.f, G01 = 0.f, G02 = 0.f, G11 = 0.f, G12 = 0.f, G22 = 0.f;  // ∂L/∂Σ (symmetric)
@@ -134,9 +205,9 @@ __global__ __launch_bounds__(BLK, 2) void k_gauss_bwd(Launch L, mvgs_grads gr, m
             gsx += pg0.x;
             gsy += pg0.y;
             dop += pg1.z;
-            Proj p;
-            ca_project(c, mx, my, mz, a.Sig, L.TX, L.TY, p);
-            const float tz = p.tz, itz = 1.f / tz, itz2 = itz * itz;
+            FastProj p;
+            fast_project(c, mx, my, mz, a.Sig, flags, p);
+            const float itz = p.itz, itz2 = itz * itz;
             // μ' (pixels) = (fx·tx/tz + cx, fy·ty/tz + cy); ∂L/∂μ' = Σ∇·(2/W, 2/H) (R2)
             const float dpx = pg0.x * sW, dpy = pg0.y * sH;
             float dtx = c.fx * itz * dpx;
@@ -144,7 +215,7 @@ __global__ __launch_bounds__(BLK, 2) void k_gauss_bwd(Launch L, mvgs_grads gr, m
             float dtz = -(c.fx * p.tx * itz2) * dpx - (c.fy * p.ty * itz2) * dpy;
             // conic (A,B,C) = (c,−b,a)/det → Σ' entries (a,b,c)
             const float dA = pg0.w, dB = pg1.x, dC = pg1.y;
-            const float id2 = 1.f / (p.det * p.det);
+            const float id2 = __frcp_rn(p.det * p.det);
             const float da = (-p.c * p.c * dA + p.b * p.c * dB - p.b * p.b * dC) * id2;
             const float dc = (-p.b * p.b * dA + p.a * p.b * dB - p.a * p.a * dC) * id2;
             const float db = (2.f * p.b * p.c * dA - (p.det + 2.f * p.b * p.b) * dB + 2.f * p.a * p.b * dC) * id2;

@@ -61,37 +61,13 @@ __device__ __forceinline__ void pixel_pair(int tx, int ty, int& x, int& y0, int&
     y1 = y0 + 2;
 }
 
-// Warp-level culling.  Per-pixel skip ⇔ ½ dᵀQd > Λ with Q the conic and
-// Λ = −skip_power(o).  Pixels outside the bounding box of {dᵀQd ≤ 2(Λ + 1e-3)} have exact power
-// below the skip bound by > 1e-3, so the per-pixel test (fp32 error ≪ 1e-3) skips them too;
-// the box half-widths are sqrt(2Λ'·(Q⁻¹)_xx) and sqrt(2Λ'·(Q⁻¹)_yy), enlarged by 1e-4
-// relative.  A warp skips an entry when its whole pixel block is outside the box.
-__device__ __forceinline__ void cull_box(float A, float B, float C, float bound, float& hx, float& hy) {
-    const float lam = -bound + 1e-3f;
-    const float det = A * C - B * B;
-    if (!(lam > 0.f) || !(det > 0.f)) {  // never visible (o < 1/255) / degenerate: no culling
-        hx = hy = lam > 0.f ? 3.0e38f : -1.0f;
-        return;
-    }
-    hx = sqrtf(2.f * lam * C / det) * 1.0001f + 1e-3f;
-    hy = sqrtf(2.f * lam * A / det) * 1.0001f + 1e-3f;
-}
-
-// stage one record: (x, y, A, B) (C, o, skip bound, box hx) (r, g, b, box hy)
+// stage one record: (x, y, A, B) (C, o, skip bound, -) (r, g, b, -)
 __device__ __forceinline__ void stage(const Launch& L, uint32_t q, float4* s0, float4* s1, float4* s2, int i) {
     const float4* r = L.rec + 3 * (int64_t)q;
     const float4 r0 = r[0], r1 = r[1], r2 = r[2];
-    const float bound = skip_power(r1.y);
-    float hx, hy;
-    cull_box(r0.z, r0.w, r1.x, bound, hx, hy);
     s0[i] = r0;
-    s1[i] = make_float4(r1.x, r1.y, bound, hx);
-    s2[i] = make_float4(r1.z, r1.w, r2.x, hy);
-}
-
-// true when the warp's 16×4 pixel block (centre (cx, cy)) lies outside the entry's box
-__device__ __forceinline__ bool warp_culled(const float4& a, const float4& c, float hy, float cx, float cy) {
-    return fabsf(a.x - cx) > c.w + 7.5f || fabsf(a.y - cy) > hy + 1.5f;
+    s1[i] = make_float4(r1.x, r1.y, skip_power(r1.y), 0.f);
+    s2[i] = make_float4(r1.z, r1.w, r2.x, 0.f);
 }
 
 __global__ __launch_bounds__(RT) void k_render_fwd(Launch L, float* __restrict__ out_rgb, float* __restrict__ out_T,
@@ -105,7 +81,6 @@ __global__ __launch_bounds__(RT) void k_render_fwd(Launch L, float* __restrict__
     pixel_pair(tx, ty, x, y[0], y[1]);
     const int start = L.bucket_off[bucket], end = L.bucket_off[bucket + 1];
     const float fx = (float)x;
-    const float wcx = (float)(tx * TILE) + 7.5f, wcy = (float)(ty * TILE + 4 * (threadIdx.x >> 5)) + 1.5f;
     float fy[2], T[2], C0[2], C1[2], C2[2];
     int last[2];
     bool done[2];
@@ -130,10 +105,6 @@ __global__ __launch_bounds__(RT) void k_render_fwd(Launch L, float* __restrict__
             for (int j = 0; j < cnt && !(done[0] && done[1]); j++) {
                 const float4 a = s0[j];
                 const float4 c = s1[j];
-                if (warp_culled(a, c, s2[j].w, wcx, wcy)) {  // warp-uniform
-                    nev += (unsigned)(!done[0]) + (unsigned)(!done[1]);
-                    continue;
-                }
                 const float dx = FSUB(a.x, fx);
 #pragma unroll
                 for (int p = 0; p < 2; p++) {
@@ -273,7 +244,6 @@ __global__ __launch_bounds__(RT) void k_render_bwd(Launch L, const float* __rest
     float* wacc = sacc[warp];
     const float fx = (float)x;
     const float fy0 = (float)y[0], fy1 = (float)y[1];
-    const float wcx = (float)(tx * TILE) + 7.5f, wcy = (float)(ty * TILE + 4 * warp) + 1.5f;
     const float hw = 0.5f * (float)L.W, hh = 0.5f * (float)L.H;
     for (int b_end = maxlast; b_end > 0; b_end -= RT) {
         const int b0 = max(0, b_end - RT);
@@ -293,7 +263,6 @@ __global__ __launch_bounds__(RT) void k_render_bwd(Launch L, const float* __rest
             const int j = b0 + jj;
             const float4 a = s0[jj];
             const float4 c = s1[jj];
-            if (warp_culled(a, c, s2[jj].w, wcx, wcy)) continue;  // warp-uniform
             const float dx = FSUB(a.x, fx);
             float val[NG];
 #pragma unroll
