@@ -190,32 +190,42 @@ struct BwdPix {
     int last;
 };
 
-__global__ __launch_bounds__(RT) void k_render_bwd(Launch L, const float* __restrict__ dL_drgb,
-                                                   const float* __restrict__ in_T, const int32_t* __restrict__ in_n) {
-    __shared__ float4 s0[RT], s1[RT], s2[RT];
-    __shared__ uint32_t sq[RT];
-    __shared__ __align__(16) float sacc[NWR][RT * NG];  // per-warp partial sums, no atomics
+// NPX pixels per thread: a CTA of 256/NPX threads covers the 16×16 tile; warp w
+// covers rows (32·NPX/16)·w …, lane l column l & 15, rows r, r+2, r+4, …
+template <int NPX>
+__global__ __launch_bounds__(256 / NPX) void k_render_bwd(Launch L, const float* __restrict__ dL_drgb,
+                                                          const float* __restrict__ in_T,
+                                                          const int32_t* __restrict__ in_n) {
+    constexpr int NT = 256 / NPX;         // threads
+    constexpr int NW = NT / 32;           // warps
+    constexpr int RB = 128;               // entries per staged batch
+    constexpr int ROWS = 2 * NPX;         // rows per warp
+    __shared__ float4 s0[RB], s1[RB], s2[RB];
+    __shared__ uint32_t sq[RB];
+    __shared__ __align__(16) float sacc[NW][RB * NG];  // per-warp partial sums, no atomics
     __shared__ int smax;
     __shared__ unsigned sev[2];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int bucket = blockIdx.x;
     const int v = bucket / L.T, tile = bucket - v * L.T;
     const int ty = tile / L.TX, tx = tile - ty * L.TX;
-    int x, y[2];
-    pixel_pair(tx, ty, x, y[0], y[1]);
+    const int x = tx * TILE + (lane & 15);
+    const int y0 = ty * TILE + ROWS * warp + (lane >> 4);
     const int start = L.bucket_off[bucket], end = L.bucket_off[bucket + 1];
     if (end > L.cap_entries) return;
     const int64_t HW = (int64_t)L.H * L.W;
-    BwdPix px[2];
+    BwdPix px[NPX];
     int mylast = 0;
+    unsigned nev = 0;
 #pragma unroll
-    for (int p = 0; p < 2; p++) {
+    for (int p = 0; p < NPX; p++) {
         BwdPix& s = px[p];
+        const int y = y0 + 2 * p;
         s.dL0 = s.dL1 = s.dL2 = 0.f;
         s.T_fin = 1.f;
         s.last = 0;
-        if (x < L.W && y[p] < L.H) {
-            const int64_t pix = (int64_t)y[p] * L.W + x;
+        if (x < L.W && y < L.H) {
+            const int64_t pix = (int64_t)y * L.W + x;
             s.dL0 = dL_drgb[(3 * (int64_t)v + 0) * HW + pix];
             s.dL1 = dL_drgb[(3 * (int64_t)v + 1) * HW + pix];
             s.dL2 = dL_drgb[(3 * (int64_t)v + 2) * HW + pix];
@@ -227,13 +237,13 @@ __global__ __launch_bounds__(RT) void k_render_bwd(Launch L, const float* __rest
         s.acc0 = s.acc1 = s.acc2 = 0.f;  // colour behind the current entry
         s.a_prev = s.c0p = s.c1p = s.c2p = 0.f;
         mylast = max(mylast, s.last);
+        nev += (unsigned)s.last;  // entries this pixel walks back over
     }
     if (threadIdx.x == 0) {
         smax = 0;
         sev[0] = sev[1] = 0;
     }
     __syncthreads();
-    const unsigned nev = (unsigned)(px[0].last + px[1].last);  // entries the two pixels walk back over
     unsigned nexp = 0;
     if (mylast > 0) atomicMax(&smax, mylast);
     __syncthreads();
@@ -243,20 +253,20 @@ __global__ __launch_bounds__(RT) void k_render_bwd(Launch L, const float* __rest
     const bool owner = (__ffs(__match_any_sync(FULLR, my_id)) - 1) == lane;
     float* wacc = sacc[warp];
     const float fx = (float)x;
-    const float fy0 = (float)y[0], fy1 = (float)y[1];
+    const float fy0 = (float)y0;
     const float hw = 0.5f * (float)L.W, hh = 0.5f * (float)L.H;
-    for (int b_end = maxlast; b_end > 0; b_end -= RT) {
-        const int b0 = max(0, b_end - RT);
+    for (int b_end = maxlast; b_end > 0; b_end -= RB) {
+        const int b0 = max(0, b_end - RB);
         const int cnt = b_end - b0;
         __syncthreads();
-        if (threadIdx.x < cnt) {
-            const uint32_t q = L.sorted[start + b0 + threadIdx.x];
-            sq[threadIdx.x] = q;
-            stage(L, q, s0, s1, s2, threadIdx.x);
+        for (int t = threadIdx.x; t < cnt; t += NT) {
+            const uint32_t q = L.sorted[start + b0 + t];
+            sq[t] = q;
+            stage(L, q, s0, s1, s2, t);
         }
         {  // each warp clears its own slots
             float4* w4 = reinterpret_cast<float4*>(wacc);
-            for (int i = lane; i < RT * NG / 4; i += 32) w4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int i = lane; i < RB * NG / 4; i += 32) w4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
         }
         __syncthreads();
         for (int jj = min(cnt, wmax - b0) - 1; jj >= 0; jj--) {
@@ -269,10 +279,10 @@ __global__ __launch_bounds__(RT) void k_render_bwd(Launch L, const float* __rest
             for (int k = 0; k < NG; k++) val[k] = 0.f;
             bool contrib = false;
 #pragma unroll
-            for (int p = 0; p < 2; p++) {
+            for (int p = 0; p < NPX; p++) {
                 BwdPix& s = px[p];
                 if (j >= s.last) continue;
-                const float dy = FSUB(a.y, p ? fy1 : fy0);
+                const float dy = FSUB(a.y, fy0 + (float)(2 * p));
                 const float power = ca_power(a.z, a.w, c.x, dx, dy);
                 if (power > 0.0f || power < c.z) continue;
                 nexp++;
@@ -316,10 +326,10 @@ __global__ __launch_bounds__(RT) void k_render_bwd(Launch L, const float* __rest
             }
         }
         __syncthreads();
-        for (int i = threadIdx.x; i < cnt * NG; i += RT) {
+        for (int i = threadIdx.x; i < cnt * NG; i += NT) {
             float s = 0.f;
 #pragma unroll
-            for (int w = 0; w < NWR; w++) s += sacc[w][i];
+            for (int w = 0; w < NW; w++) s += sacc[w][i];
             if (s != 0.f) {
                 const int jj = i / NG, k = i - jj * NG;
                 atomicAdd(&L.pgrad[(int64_t)sq[jj] * PG_STRIDE + k], s);
@@ -329,8 +339,12 @@ __global__ __launch_bounds__(RT) void k_render_bwd(Launch L, const float* __rest
     count_evals(&L.counters64[1], &L.counters64[3], nev, nexp, sev);
 }
 
+#ifndef MVGS_BWD_NPX
+#define MVGS_BWD_NPX 4
+#endif
+
 cudaError_t launch_render_bwd(const Launch& L, const float* dL, const float* Tf, const int32_t* nc, cudaStream_t s) {
-    k_render_bwd<<<L.V * L.T, RT, 0, s>>>(L, dL, Tf, nc);
+    k_render_bwd<MVGS_BWD_NPX><<<L.V * L.T, 256 / MVGS_BWD_NPX, 0, s>>>(L, dL, Tf, nc);
     return cudaGetLastError();
 }
 

@@ -222,16 +222,27 @@ __global__ void k_pair_tiles(Launch L, const uint2* __restrict__ rect, int* __re
 }
 
 // Duplication in depth order: pair i's entries are ebase[i] + (row-major tile index
-// in its rect), key = view·T + tile.  A warp takes 32 consecutive pairs and writes
-// their entries together: lane l handles entries l, l+32, … of the warp's run,
-// finding its pair by a search over the warp's inclusive tile-count prefix, so
-// consecutive lanes write consecutive addresses.
+// in its rect), key = view·T + tile.  A warp takes 32 consecutive pairs, whose
+// entries form one contiguous run, and writes them together: lane l handles
+// entries l, l+32, … of the run, finding its pair by a binary search over the
+// warp's inclusive tile-count prefix kept in shared memory, so consecutive lanes
+// write consecutive addresses.  The row/column split uses a float reciprocal of
+// the rect width (exact: (k + 0.5)/w for integers k < 2^20, w < 2^12 never
+// rounds across an integer).
+struct DupDesc {  // one pair of the warp's 32
+    int x0, y0, w, excl;
+    float inv_w;
+    uint32_t vb, q, pad;
+};
+
 __global__ __launch_bounds__(256) void k_dup(Launch L, const uint32_t* __restrict__ order,
                                              const uint2* __restrict__ rect, const int* __restrict__ ebase) {
+    __shared__ int pref[8][32];
+    __shared__ DupDesc desc[8][32];
     const int Q = (int)min((int64_t)L.counters[C_Q], L.cap_pairs);
-    const int lane = threadIdx.x & 31;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
-    for (int64_t w0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32; w0 < Q; w0 += nwarps * 32) {
+    for (int64_t w0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + wid) * 32; w0 < Q; w0 += nwarps * 32) {
         const int64_t i = w0 + lane;
         uint2 r = make_uint2(0u, 0u);
         uint32_t q = 0;
@@ -250,35 +261,36 @@ __global__ __launch_bounds__(256) void k_dup(Launch L, const uint32_t* __restric
         }
         const int total = __shfl_sync(FULLS, inc, 31);
         const int64_t e0 = __shfl_sync(FULLS, (int64_t)(i < Q ? ebase[i] : 0), 0);
-        const uint32_t vb = (i < Q && cnt > 0) ? (uint32_t)view_of_pair(L, q) * (uint32_t)L.T : 0u;
-        for (int base = 0; base < total; base += 32) {  // warp-uniform rounds, all lanes active
-            const int k = base + lane;
-            // owner = first lane whose inclusive prefix exceeds k (monotone ⇒ binary search)
-            int lo = 0;
+        pref[wid][lane] = inc;
+        DupDesc d;
+        d.x0 = rx0;
+        d.y0 = ry0;
+        d.w = w;
+        d.excl = inc - cnt;
+        d.inv_w = cnt > 0 ? 1.0f / (float)w : 0.f;
+        d.vb = cnt > 0 ? (uint32_t)view_of_pair(L, q) * (uint32_t)L.T : 0u;
+        d.q = q;
+        d.pad = 0;
+        desc[wid][lane] = d;
+        __syncwarp();
+        for (int k = lane; k < total; k += 32) {
+            int lo = 0;  // owner = number of lanes whose inclusive prefix is ≤ k
 #pragma unroll
-            for (int step = 16; step > 0; step >>= 1) {
-                const int cand = lo + step - 1;
-                if (__shfl_sync(FULLS, inc, cand) <= k) lo += step;
-            }
-            const int owner = min(lo, 31);
-            const int excl = __shfl_sync(FULLS, inc - cnt, owner);
-            const int ow = __shfl_sync(FULLS, w, owner);
-            const int ox = __shfl_sync(FULLS, rx0, owner);
-            const int oy = __shfl_sync(FULLS, ry0, owner);
-            const uint32_t ob = __shfl_sync(FULLS, vb, owner);
-            const uint32_t oq = __shfl_sync(FULLS, q, owner);
-            if (k < total) {
-                const int loc = k - excl;
-                const int ty = oy + loc / ow, tx = ox + loc % ow;
-                const int64_t e = e0 + k;
-                if (e < L.cap_entries) {
-                    L.key[e] = ob + ty * L.TX + tx;
-                    L.val[e] = oq;
-                } else {
-                    L.counters[C_OVERFLOW] = 1;
-                }
+            for (int step = 16; step > 0; step >>= 1)
+                if (pref[wid][lo + step - 1] <= k) lo += step;
+            const DupDesc& o = desc[wid][lo];
+            const int loc = k - o.excl;
+            const int row = __float2int_rz(((float)loc + 0.5f) * o.inv_w);
+            const int col = loc - row * o.w;
+            const int64_t e = e0 + k;
+            if (e < L.cap_entries) {
+                L.key[e] = o.vb + (o.y0 + row) * L.TX + o.x0 + col;
+                L.val[e] = o.q;
+            } else {
+                L.counters[C_OVERFLOW] = 1;
             }
         }
+        __syncwarp();
     }
 }
 

@@ -12,7 +12,7 @@ import numpy as np
 import torch
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libmvgs.so")
+LIB_PATH = os.environ.get("MVGS_LIB", os.path.join(HERE, "libmvgs.so"))  # override: experiments only
 
 MVGS_OK, MVGS_ERR_INVALID, MVGS_ERR_CAPACITY, MVGS_ERR_STATE, MVGS_ERR_CUDA = 0, -1, -2, -3, -4
 NG = 10
