@@ -193,4 +193,12 @@ __device__ __forceinline__ float ca_power(float A, float B, float C, float dx, f
     return FMA(-0.5f, FMA(FMUL(A, dx), dx, FMUL(FMUL(C, dy), dy)), -FMUL(FMUL(B, dx), dy));
 }
 
+// 4-byte global→shared async copy (LDGSTS), completion via cp_async_wait_all().
+__device__ __forceinline__ void cp_async4(float* smem_dst, const float* gmem_src) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(d), "l"(gmem_src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
 }  // namespace mvgs

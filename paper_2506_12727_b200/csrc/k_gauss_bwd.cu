@@ -117,31 +117,18 @@ __global__ __launch_bounds__(BLK, 2) void k_gauss_bwd(Launch L, mvgs_grads gr, m
     const int64_t g0 = (int64_t)blockIdx.x * BLK;
     const int64_t g = g0 + threadIdx.x;
     const bool valid = g < L.P;
-    {  // coalesced block load, 8 loads in flight per thread before the stores
+    {  // SH rows: coalesced async copies (no registers, all in flight), waited on before first use
         const int nb = (int)min((int64_t)BLK, L.P - g0);
         const float* src = L.sh + g0 * (int64_t)L.sh_stride * 3;
         const int rowlen = L.sh_stride * 3;
         const int n = nb * NS;
-        for (int i0 = threadIdx.x; i0 < n; i0 += 8 * BLK) {
-            float t[8];
-#pragma unroll
-            for (int u = 0; u < 8; u++) {
-                const int i = i0 + u * BLK;
-                const int r = i / NS, k = i - r * NS;  // NS constexpr: mul-shift
-                t[u] = i < n ? src[(int64_t)r * rowlen + k] : 0.f;
-            }
-#pragma unroll
-            for (int u = 0; u < 8; u++) {
-                const int i = i0 + u * BLK;
-                const int r = i / NS, k = i - r * NS;
-                if (i < n) {
-                    sh_s[r * SS + k] = t[u];
-                    dsh_s[r * SS + k] = 0.f;
-                }
-            }
+        for (int i = threadIdx.x; i < n; i += BLK) {
+            const int r = i / NS, k = i - r * NS;  // NS constexpr: mul-shift
+            cp_async4(&sh_s[r * SS + k], src + (int64_t)r * rowlen + k);
+            dsh_s[r * SS + k] = 0.f;
         }
+        cp_async_commit();
     }
-    __syncthreads();
     const float* sh = sh_s + threadIdx.x * SS;
     float* dsh = dsh_s + threadIdx.x * SS;
     float mx = 0.f, my = 0.f, mz = 0.f;
@@ -158,6 +145,7 @@ __global__ __launch_bounds__(BLK, 2) void k_gauss_bwd(Launch L, mvgs_grads gr, m
     float G00 = 0.f, G01 = 0.f, G02 = 0.f, G11 = 0.f, G12 = 0.f, G22 = 0.f;  // ∂L/∂Σ (symmetric)
     float dop = 0.f, e1 = 0.f, e2 = 0.f, gsx = 0.f, gsy = 0.f, nvis = 0.f;
     const float sW = 2.0f / (float)L.W, sH = 2.0f / (float)L.H;
+    bool sh_ready = false;  // SH rows arrive asynchronously; waited on after the first view loads
     for (int v0 = 0; v0 < L.V; v0 += 32) {
         const int nv = min(32, L.V - v0);
         for (int k = 0; k < nv; k++) {
@@ -191,6 +179,11 @@ __global__ __launch_bounds__(BLK, 2) void k_gauss_bwd(Launch L, mvgs_grads gr, m
                 pga[u] = pgp[0];
                 pgb[u] = pgp[1];
                 pgc[u] = pgp[2];
+            }
+            if (!sh_ready) {  // block-uniform: overlap the SH copy with the first pair loads
+                cp_async_wait_all();
+                __syncthreads();
+                sh_ready = true;
             }
 #pragma unroll
             for (int u = 0; u < 4; u++) {
@@ -333,6 +326,10 @@ __global__ __launch_bounds__(BLK, 2) void k_gauss_bwd(Launch L, mvgs_grads gr, m
             dmz += (ddz - z * dd) * idn;
             }
         }
+        __syncthreads();
+    }
+    if (!sh_ready) {  // no view chunk ran (V == 0 cannot happen, but keep the copy complete)
+        cp_async_wait_all();
         __syncthreads();
     }
     // coalesced store of the SH gradient rows (coefficients above the active degree are 0)

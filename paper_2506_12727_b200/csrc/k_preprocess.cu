@@ -190,26 +190,16 @@ __global__ __launch_bounds__(BLK) void k_project(Launch L) {
     const int64_t g0 = (int64_t)blockIdx.x * BLK;
     const int64_t g = g0 + threadIdx.x;
     const bool valid = g < L.P;
-    {  // coalesced block load, 8 loads in flight per thread before the stores
+    {  // SH rows: coalesced async copies (no registers, all in flight), waited on before first use
         const int nb = (int)min((int64_t)BLK, L.P - g0);
         const float* src = L.sh + g0 * (int64_t)L.sh_stride * 3;
         const int rowlen = L.sh_stride * 3;
         const int n = nb * NS;
-        for (int i0 = threadIdx.x; i0 < n; i0 += 8 * BLK) {
-            float t[8];
-#pragma unroll
-            for (int u = 0; u < 8; u++) {
-                const int i = i0 + u * BLK;
-                const int r = i / NS, k = i - r * NS;  // NS constexpr: mul-shift
-                t[u] = i < n ? src[(int64_t)r * rowlen + k] : 0.f;
-            }
-#pragma unroll
-            for (int u = 0; u < 8; u++) {
-                const int i = i0 + u * BLK;
-                const int r = i / NS, k = i - r * NS;
-                if (i < n) sh_s[r * SS + k] = t[u];
-            }
+        for (int i = threadIdx.x; i < n; i += BLK) {
+            const int r = i / NS, k = i - r * NS;  // NS constexpr: mul-shift
+            cp_async4(&sh_s[r * SS + k], src + (int64_t)r * rowlen + k);
         }
+        cp_async_commit();
     }
     const float* sh = sh_s + threadIdx.x * SS;
     float mx = 0.f, my = 0.f, mz = 0.f;
@@ -231,6 +221,7 @@ __global__ __launch_bounds__(BLK) void k_project(Launch L) {
             if (lane == 0) wc[warp][k] = __popc(bal);
         }
         if (threadIdx.x < nv) sboff[threadIdx.x] = L.blk_off[(int64_t)(v0 + threadIdx.x) * L.NB + blockIdx.x];
+        cp_async_wait_all();
         __syncthreads();
         for (int k = 0; k < nv; k++) {
             const int v = v0 + k;

@@ -340,7 +340,7 @@ __global__ __launch_bounds__(256 / NPX) void k_render_bwd(Launch L, const float*
 }
 
 #ifndef MVGS_BWD_NPX
-#define MVGS_BWD_NPX 4
+#define MVGS_BWD_NPX 2
 #endif
 
 cudaError_t launch_render_bwd(const Launch& L, const float* dL, const float* Tf, const int32_t* nc, cudaStream_t s) {
