@@ -26,6 +26,11 @@ struct PairMeta {
     uint32_t vf;
 };
 
+struct RadixScratch {
+    unsigned long long* status;  // [256 × tiles] look-back words (epoch-tagged)
+    uint32_t* small;             // digit totals, bases, tile counters, device pass epoch
+};
+
 struct Launch {  // everything a kernel needs about the current batch
     int64_t P;
     int V, W, H, TX, TY, T, NB;
@@ -45,7 +50,8 @@ struct Launch {  // everything a kernel needs about the current batch
     uint32_t *pkey, *pval, *pkey2, *pval2;  // [cap_pairs] pair (depth key, pair) ping-pong
     uint2 *prect, *prect2;                  // [cap_pairs] packed tile rect carried through the pair sort
     int* ecount;      // [cap_pairs + 1] tiles per depth-ordered pair → entry offsets
-    int* rs_counts;   // radix digit × tile counts
+    int* rs_counts;   // (unused) radix digit × tile counts
+    RadixScratch rs;  // onesweep radix scratch
     int* scan_tmp;    // scan block sums
     const uint32_t* sorted;  // [K] pair index of every entry in (view, tile, depth, gid) order
     int* counters;    // [C_NCOUNTERS]
@@ -75,6 +81,9 @@ struct mvgs_ctx {
     int* d_ecount = nullptr;
     int* d_rs = nullptr;
     int64_t cap_rs = 0;
+    unsigned long long* d_rs_status = nullptr;
+    uint32_t* d_rs_small = nullptr;
+    uint32_t rs_epoch = 0;
     int* d_counters = nullptr;
     unsigned long long* d_counters64 = nullptr;
     int* d_scan = nullptr;  // scan block sums

@@ -284,7 +284,7 @@ __global__ __launch_bounds__(BLK) void k_project(Launch L) {
                 float4* pg = reinterpret_cast<float4*>(L.pgrad + pair * PG_STRIDE);
                 pg[0] = pg[1] = pg[2] = make_float4(0.f, 0.f, 0.f, 0.f);
             }
-            if (tiles > 0) atomicAdd(&L.counters[C_NVIS], 1);  // warp-aggregated by ptxas
+            if (tiles > 0 && pair < L.cap_pairs) atomicAdd(&L.counters[C_NVIS], 1);  // stored visible pairs
             my_tiles += (unsigned long long)tiles;
         }
         __syncthreads();

@@ -28,19 +28,12 @@ constexpr int RS_T = 256, RS_IPT = 8, RS_TILE = RS_T * RS_IPT, RS_NW = RS_T / 32
 int radix_tiles(int64_t cap) { return (int)((cap + RS_TILE - 1) / RS_TILE); }
 int64_t radix_counts_size(int64_t cap) { return (int64_t)RS_BINS * radix_tiles(cap) + 1; }
 
-// per-tile digit histogram → counts[digit * ntiles + tile]
-__global__ __launch_bounds__(RS_T) void k_rs_hist(const uint32_t* __restrict__ keys, const int* __restrict__ n_ptr,
-                                                  int64_t cap, int shift, int nbits, int* __restrict__ counts,
-                                                  int ntiles) {
-    __shared__ int h[RS_BINS];
-    h[threadIdx.x] = 0;
-    __syncthreads();
-    const int n = (int)min((int64_t)*n_ptr, cap);
-    const int t0 = blockIdx.x * RS_TILE;
-    const uint32_t mask = (1u << nbits) - 1u;
-    for (int i = t0 + threadIdx.x; i < min(n, t0 + RS_TILE); i += RS_T) atomicAdd(&h[(keys[i] >> shift) & mask], 1);
-    __syncthreads();
-    counts[(int64_t)threadIdx.x * ntiles + blockIdx.x] = h[threadIdx.x];
+static int grid_for(int64_t n, int threads) {
+    int dev = 0, nsm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    int64_t b = (n + threads - 1) / threads;
+    return (int)max((int64_t)1, min(b, (int64_t)nsm * 16));
 }
 
 // exclusive scan over the 256 threads of a CTA (one value each)
@@ -80,27 +73,85 @@ __device__ __forceinline__ unsigned digit_peers(uint32_t d, bool ok) {
     return peers;
 }
 
-// Stable scatter of one tile.  Ranks are computed per warp (multisplit), the
-// tile is first re-ordered by digit in shared memory, then written out by
-// consecutive threads: every digit's run lands contiguously at
-// offsets[digit * ntiles + tile], so global writes are coalesced.
-// Optionally moves a 64-bit payload with each key.
+// ---------------------------------------------------------------- onesweep
+// Stable LSD radix sort, one kernel per pass.  The digit totals of every pass are
+// counted once up front (the key multiset never changes between passes); within a
+// pass each tile takes a dynamic id, ranks its keys on chip, publishes its per-digit
+// counts and obtains its exclusive per-digit prefix by decoupled look-back over the
+// preceding tiles (status words tagged with a per-pass epoch, so nothing is cleared
+// between passes).  The first pass can drop "inert" keys (0xffffffff), compacting
+// the pairs with no tile before the remaining passes.
+constexpr uint32_t INERT = 0xffffffffu;
+constexpr unsigned long long ST_AGG = 1ull << 32, ST_PRE = 2ull << 32;
+
+__global__ __launch_bounds__(256) void k_rs_upsweep(const uint32_t* __restrict__ keys, const int* __restrict__ n_ptr,
+                                                    int64_t cap, int npass, int db, int bits, int drop_inert,
+                                                    uint32_t* __restrict__ totals) {
+    __shared__ uint32_t h[4][RS_BINS];
+    for (int i = threadIdx.x; i < 4 * RS_BINS; i += blockDim.x) (&h[0][0])[i] = 0;
+    __syncthreads();
+    const int n = (int)min((int64_t)*n_ptr, cap);
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const uint32_t k = keys[i];
+        if (drop_inert && k == INERT) continue;
+        for (int p = 0; p < npass; p++) {
+            const int sh = p * db, nb = min(db, bits - sh);
+            atomicAdd(&h[p][(k >> sh) & ((1u << nb) - 1u)], 1u);
+        }
+    }
+    __syncthreads();
+    for (int p = 0; p < npass; p++)
+        if (h[p][threadIdx.x]) atomicAdd(&totals[p * RS_BINS + threadIdx.x], h[p][threadIdx.x]);
+}
+
+// also advances the device-side pass epoch (graph replays never see stale words)
+__global__ __launch_bounds__(256) void k_rs_bases(const uint32_t* __restrict__ totals, uint32_t* __restrict__ gbase,
+                                                  int npass, uint32_t* __restrict__ epoch) {
+    if (threadIdx.x == 0) {
+        epoch[1] = epoch[0] + 1;  // epoch of pass 0
+        epoch[0] += (uint32_t)npass;
+    }
+    for (int p = 0; p < npass; p++) {
+        uint32_t tot;
+        const uint32_t ex = block_excl_scan_256_u(totals[p * RS_BINS + threadIdx.x], &tot);
+        gbase[p * RS_BINS + threadIdx.x] = ex;
+        __syncthreads();
+    }
+}
+
+__device__ __forceinline__ void st_status(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;\n" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_status(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];\n" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
 template <bool PAYLOAD>
-__global__ __launch_bounds__(RS_T) void k_rs_scatter(const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin,
-                                                     uint32_t* __restrict__ kout, uint32_t* __restrict__ vout,
-                                                     const uint2* __restrict__ pin, uint2* __restrict__ pout,
-                                                     const int* __restrict__ n_ptr, int64_t cap, int shift, int nbits,
-                                                     const int* __restrict__ offs, int ntiles) {
+__global__ __launch_bounds__(RS_T) void k_rs_onesweep(const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin,
+                                                      uint32_t* __restrict__ kout, uint32_t* __restrict__ vout,
+                                                      const uint2* __restrict__ pin, uint2* __restrict__ pout,
+                                                      const int* __restrict__ n_ptr, int64_t cap, int shift, int nbits,
+                                                      int drop_inert, const uint32_t* __restrict__ gbase,
+                                                      unsigned long long* __restrict__ status,
+                                                      const uint32_t* __restrict__ epoch_base, int pass,
+                                                      int* __restrict__ tile_ctr) {
     __shared__ uint32_t hist[RS_NW][RS_BINS];
-    __shared__ uint32_t dstart[RS_BINS];   // first local position of each digit
-    __shared__ uint32_t gdelta[RS_BINS];   // global offset − local start, per digit
+    __shared__ uint32_t gdelta[RS_BINS];  // global offset − local start, per digit
     __shared__ uint32_t sk[RS_TILE], sv[RS_TILE];
     __shared__ uint2 sp[PAYLOAD ? RS_TILE : 1];
+    __shared__ int s_tile;
+    __shared__ uint32_t s_total;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const unsigned lt = (1u << lane) - 1u;
+    if (threadIdx.x == 0) s_tile = atomicAdd(tile_ctr, 1);  // dynamic ids: predecessors are running
+    __syncthreads();
+    const int tile = s_tile;
+    const uint32_t epoch = (epoch_base[1] + (uint32_t)pass) & 0x3fffffffu;  // 30-bit tag
     const int n = (int)min((int64_t)*n_ptr, cap);
-    const int t0 = blockIdx.x * RS_TILE;
-    if (t0 >= n) return;
+    const int t0 = tile * RS_TILE;
+    if (t0 >= n) return;  // every later tile is past n as well
     const int nt = min(RS_TILE, n - t0);
     const uint32_t mask = (1u << nbits) - 1u;
 #pragma unroll
@@ -112,44 +163,61 @@ __global__ __launch_bounds__(RS_T) void k_rs_scatter(const uint32_t* __restrict_
     for (int it = 0; it < RS_IPT; it++) {
         const int p = warp * 32 * RS_IPT + it * 32 + lane;
         const bool ok = p < nt;
-        key[it] = ok ? kin[t0 + p] : 0u;
+        key[it] = ok ? kin[t0 + p] : INERT;
         val[it] = ok ? vin[t0 + p] : 0u;
         if (PAYLOAD) pay[PAYLOAD ? it : 0] = ok ? pin[t0 + p] : make_uint2(0u, 0u);
     }
 #pragma unroll
     for (int it = 0; it < RS_IPT; it++) {
         const int p = warp * 32 * RS_IPT + it * 32 + lane;
-        const bool ok = p < nt;
+        const bool ok = p < nt && !(drop_inert && key[it] == INERT);
         const uint32_t d = (key[it] >> shift) & mask;
         const unsigned peers = digit_peers(d, ok);
         const uint32_t before = ok ? hist[warp][d] : 0u;
-        loc[it] = before + __popc(peers & lt);
+        loc[it] = ok ? before + __popc(peers & lt) : 0xffffffffu;
         __syncwarp();
         if (ok && lane == __ffs(peers) - 1) hist[warp][d] = before + __popc(peers);
         __syncwarp();
     }
     __syncthreads();
-    {  // thread = digit: tile-local digit starts and warp bases
+    {  // thread = digit: publish, look back, tile-local starts and warp bases
+        const int d = threadIdx.x;
         uint32_t tot = 0;
 #pragma unroll
-        for (int w = 0; w < RS_NW; w++) tot += hist[w][threadIdx.x];
-        uint32_t ws;
-        const uint32_t start = block_excl_scan_256_u(tot, &ws);
-        dstart[threadIdx.x] = start;
-        gdelta[threadIdx.x] = (uint32_t)offs[(int64_t)threadIdx.x * ntiles + blockIdx.x] - start;
+        for (int w = 0; w < RS_NW; w++) tot += hist[w][d];
+        unsigned long long* st = status + (size_t)tile * RS_BINS + d;
+        const unsigned long long ep = (unsigned long long)epoch << 34;
+        uint32_t excl = 0;
+        if (tile == 0) {
+            st_status(st, ep | ST_PRE | tot);
+        } else {
+            st_status(st, ep | ST_AGG | tot);
+            for (int p = tile - 1; p >= 0; p--) {
+                unsigned long long w;
+                do {
+                    w = ld_status(status + (size_t)p * RS_BINS + d);
+                } while ((w >> 34) != epoch || !(w & (ST_AGG | ST_PRE)));
+                excl += (uint32_t)w;
+                if (w & ST_PRE) break;
+            }
+            st_status(st, ep | ST_PRE | (excl + tot));
+        }
+        uint32_t all;
+        const uint32_t start = block_excl_scan_256_u(tot, &all);
+        if (d == 0) s_total = all;
+        gdelta[d] = gbase[d] + excl - start;
         uint32_t run = start;
 #pragma unroll
         for (int w = 0; w < RS_NW; w++) {
-            const uint32_t c = hist[w][threadIdx.x];
-            hist[w][threadIdx.x] = run;
+            const uint32_t c = hist[w][d];
+            hist[w][d] = run;
             run += c;
         }
     }
     __syncthreads();
 #pragma unroll
     for (int it = 0; it < RS_IPT; it++) {
-        const int p = warp * 32 * RS_IPT + it * 32 + lane;
-        if (p < nt) {
+        if (loc[it] != 0xffffffffu) {
             const uint32_t l = hist[warp][(key[it] >> shift) & mask] + loc[it];
             sk[l] = key[it];
             sv[l] = val[it];
@@ -157,7 +225,8 @@ __global__ __launch_bounds__(RS_T) void k_rs_scatter(const uint32_t* __restrict_
         }
     }
     __syncthreads();
-    for (int l = threadIdx.x; l < nt; l += RS_T) {
+    const int nout = (int)s_total;
+    for (int l = threadIdx.x; l < nout; l += RS_T) {
         const uint32_t k = sk[l];
         const uint32_t dst = gdelta[(k >> shift) & mask] + l;
         kout[dst] = k;
@@ -167,27 +236,38 @@ __global__ __launch_bounds__(RS_T) void k_rs_scatter(const uint32_t* __restrict_
 }
 
 // Stable LSD sort of (k, v[, payload])[0..*n_ptr) on bits [0, bits) with ≤ 8-bit
-// digits.  Returns the number of passes; the result is in the first buffers when
-// even, in the second ones when odd.
+// digits; with drop_inert the first pass removes keys equal to 0xffffffff and the
+// later passes run on *n_after elements.  Returns the number of passes; the result
+// is in the first buffers when even, in the second ones when odd.
 int radix_sort(uint32_t* k, uint32_t* v, uint32_t* k2, uint32_t* v2, uint2* pl, uint2* pl2, const int* n_ptr,
-               int64_t cap, int bits, int* counts, int* scan_tmp, cudaStream_t s, cudaError_t* err) {
+               const int* n_after, int64_t cap, int bits, bool drop_inert, const RadixScratch& rs, cudaStream_t s,
+               cudaError_t* err) {
     const int ntiles = radix_tiles(cap);
     const int npass = (bits + 7) / 8;
     const int db = npass ? (bits + npass - 1) / npass : 0;
     *err = cudaSuccess;
-    if (ntiles == 0) return 0;
+    if (ntiles == 0 || npass == 0) return 0;
+    uint32_t* totals = rs.small;                      // [4][256]
+    uint32_t* gbase = rs.small + 4 * RS_BINS;         // [4][256]
+    int* tctr = (int*)(rs.small + 8 * RS_BINS);       // [4]
+    uint32_t* epoch = rs.small + 8 * RS_BINS + 8;     // [2] device pass epoch (never cleared)
+    if ((*err = cudaMemsetAsync(rs.small, 0, sizeof(uint32_t) * (8 * RS_BINS + 4), s)) != cudaSuccess) return 0;
+    k_rs_upsweep<<<grid_for(cap, 256), 256, 0, s>>>(k, n_ptr, cap, npass, db, bits, drop_inert ? 1 : 0, totals);
+    k_rs_bases<<<1, 256, 0, s>>>(totals, gbase, npass, epoch);
     uint32_t *ks = k, *vs = v, *kd = k2, *vd = v2;
     uint2 *ps = pl, *pd = pl2;
     for (int pass = 0; pass < npass; pass++) {
         const int shift = pass * db;
         const int nb = min(db, bits - shift);
-        k_rs_hist<<<ntiles, RS_T, 0, s>>>(ks, n_ptr, cap, shift, nb, counts, ntiles);
-        if ((*err = scan_exclusive(counts, RS_BINS * ntiles, nullptr, scan_tmp, s)) != cudaSuccess) return pass;
+        const int* np = (pass == 0) ? n_ptr : (drop_inert ? n_after : n_ptr);
         if (pl)
-            k_rs_scatter<true><<<ntiles, RS_T, 0, s>>>(ks, vs, kd, vd, ps, pd, n_ptr, cap, shift, nb, counts, ntiles);
+            k_rs_onesweep<true><<<ntiles, RS_T, 0, s>>>(ks, vs, kd, vd, ps, pd, np, cap, shift, nb,
+                                                        (drop_inert && pass == 0) ? 1 : 0, gbase + pass * RS_BINS,
+                                                        rs.status, epoch, pass, tctr + pass);
         else
-            k_rs_scatter<false><<<ntiles, RS_T, 0, s>>>(ks, vs, kd, vd, nullptr, nullptr, n_ptr, cap, shift, nb,
-                                                        counts, ntiles);
+            k_rs_onesweep<false><<<ntiles, RS_T, 0, s>>>(ks, vs, kd, vd, nullptr, nullptr, np, cap, shift, nb,
+                                                         (drop_inert && pass == 0) ? 1 : 0, gbase + pass * RS_BINS,
+                                                         rs.status, epoch, pass, tctr + pass);
         if ((*err = cudaGetLastError()) != cudaSuccess) return pass;
         uint32_t* t = ks; ks = kd; kd = t;
         t = vs; vs = vd; vd = t;
@@ -209,7 +289,7 @@ __device__ __forceinline__ int view_of_pair(const Launch& L, uint32_t q) {
 
 // tiles covered by the i-th pair in depth order (0 past Q) → scanned into entry offsets
 __global__ void k_pair_tiles(Launch L, const uint2* __restrict__ rect, int* __restrict__ ecount) {
-    const int Q = (int)min((int64_t)L.counters[C_Q], L.cap_pairs);
+    const int Q = (int)min((int64_t)L.counters[C_NVIS], L.cap_pairs);  // visible pairs (compacted by the sort)
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < L.cap_pairs; i += stride) {
         int t = 0;
@@ -239,7 +319,7 @@ __global__ __launch_bounds__(256) void k_dup(Launch L, const uint32_t* __restric
                                              const uint2* __restrict__ rect, const int* __restrict__ ebase) {
     __shared__ int pref[8][32];
     __shared__ DupDesc desc[8][32];
-    const int Q = (int)min((int64_t)L.counters[C_Q], L.cap_pairs);
+    const int Q = (int)min((int64_t)L.counters[C_NVIS], L.cap_pairs);  // visible pairs (compacted by the sort)
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
     for (int64_t w0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + wid) * 32; w0 < Q; w0 += nwarps * 32) {
@@ -317,20 +397,13 @@ __global__ void k_max_bucket(Launch L) {
     if ((threadIdx.x & 31) == 0 && m > 0) atomicMax(&L.counters[C_MAXB], m);
 }
 
-static int grid_for(int64_t n, int threads) {
-    int dev = 0, nsm = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    int64_t b = (n + threads - 1) / threads;
-    return (int)max((int64_t)1, min(b, (int64_t)nsm * 16));
-}
 
 // S4a: pairs by depth, carrying each pair's packed tile rect.  pkey/pval/prect were
 // written by k_project; the depth order and the rects in that order → *order_out, *rect_out.
 cudaError_t launch_sort_pairs(const Launch& L, const uint32_t** order_out, const uint2** rect_out, cudaStream_t s) {
     cudaError_t e;
-    int np = radix_sort(L.pkey, L.pval, L.pkey2, L.pval2, L.prect, L.prect2, L.counters + C_Q, L.cap_pairs, 32,
-                        L.rs_counts, L.scan_tmp, s, &e);
+    int np = radix_sort(L.pkey, L.pval, L.pkey2, L.pval2, L.prect, L.prect2, L.counters + C_Q, L.counters + C_NVIS,
+                        L.cap_pairs, 32, true, L.rs, s, &e);
     *order_out = (np & 1) ? L.pval2 : L.pval;
     *rect_out = (np & 1) ? L.prect2 : L.prect;
     return e;
@@ -350,8 +423,8 @@ cudaError_t launch_sort_entries(const Launch& L, uint32_t** sorted_vals, cudaStr
     int bits = 1;
     while ((1ll << bits) < (int64_t)L.V * L.T) bits++;
     cudaError_t e;
-    int np = radix_sort(L.key, L.val, L.key2, L.val2, nullptr, nullptr, L.counters + C_K, L.cap_entries, bits,
-                        L.rs_counts, L.scan_tmp, s, &e);
+    int np = radix_sort(L.key, L.val, L.key2, L.val2, nullptr, nullptr, L.counters + C_K, nullptr, L.cap_entries,
+                        bits, false, L.rs, s, &e);
     *sorted_vals = (np & 1) ? L.val2 : L.val;
     if (e != cudaSuccess) return e;
     k_ranges<<<grid_for(L.cap_entries + 1, 256), 256, 0, s>>>(L, (np & 1) ? L.key2 : L.key);
