@@ -141,10 +141,10 @@ def stage_models(P, NK, V, NB, Q, K, T, evf, evb, exf, exb):
 def launches_per_step(nbuckets, Q, K):
     """Kernels libmvgs launches per step: count + 3-kernel scan, project,
     pair sort (upsweep + bases + 4 onesweep passes), pair-tiles + 3-kernel scan + dup,
-    entry sort (upsweep + bases + ⌈log2(V·T)/8⌉ passes), ranges + max-bucket, fwd, bwd,
-    gauss_bwd."""
+    entry sort (⌈log2(V·T)/8⌉ passes × (histogram + 3-kernel scan + scatter)),
+    ranges + max-bucket, fwd, bwd, gauss_bwd."""
     ent_passes = (max(1, (nbuckets - 1).bit_length()) + 7) // 8
-    return (1 + 3) + 1 + (2 + 4) + (1 + 3 + 1) + (2 + ent_passes) + 2 + 3
+    return (1 + 3) + 1 + (2 + 4) + (1 + 3 + 1) + 5 * ent_passes + 2 + 3
 
 
 # ---------------------------------------------------------------------- mvgs

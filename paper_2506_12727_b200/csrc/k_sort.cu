@@ -73,6 +73,139 @@ __device__ __forceinline__ unsigned digit_peers(uint32_t d, bool ok) {
     return peers;
 }
 
+// per-tile digit histogram → counts[digit * ntiles + tile]
+__global__ __launch_bounds__(RS_T) void k_rs_hist(const uint32_t* __restrict__ keys, const int* __restrict__ n_ptr,
+                                                  int64_t cap, int shift, int nbits, int* __restrict__ counts,
+                                                  int ntiles) {
+    __shared__ int h[RS_BINS];
+    h[threadIdx.x] = 0;
+    __syncthreads();
+    const int n = (int)min((int64_t)*n_ptr, cap);
+    const int t0 = blockIdx.x * RS_TILE;
+    const uint32_t mask = (1u << nbits) - 1u;
+    for (int i = t0 + threadIdx.x; i < min(n, t0 + RS_TILE); i += RS_T) atomicAdd(&h[(keys[i] >> shift) & mask], 1);
+    __syncthreads();
+    counts[(int64_t)threadIdx.x * ntiles + blockIdx.x] = h[threadIdx.x];
+}
+
+// Stable scatter of one tile.  Ranks are computed per warp (multisplit), the
+// tile is first re-ordered by digit in shared memory, then written out by
+// consecutive threads: every digit's run lands contiguously at
+// offsets[digit * ntiles + tile], so global writes are coalesced.
+// Optionally moves a 64-bit payload with each key.
+template <bool PAYLOAD>
+__global__ __launch_bounds__(RS_T) void k_rs_scatter(const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin,
+                                                     uint32_t* __restrict__ kout, uint32_t* __restrict__ vout,
+                                                     const uint2* __restrict__ pin, uint2* __restrict__ pout,
+                                                     const int* __restrict__ n_ptr, int64_t cap, int shift, int nbits,
+                                                     const int* __restrict__ offs, int ntiles) {
+    __shared__ uint32_t hist[RS_NW][RS_BINS];
+    __shared__ uint32_t dstart[RS_BINS];   // first local position of each digit
+    __shared__ uint32_t gdelta[RS_BINS];   // global offset − local start, per digit
+    __shared__ uint32_t sk[RS_TILE], sv[RS_TILE];
+    __shared__ uint2 sp[PAYLOAD ? RS_TILE : 1];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const unsigned lt = (1u << lane) - 1u;
+    const int n = (int)min((int64_t)*n_ptr, cap);
+    const int t0 = blockIdx.x * RS_TILE;
+    if (t0 >= n) return;
+    const int nt = min(RS_TILE, n - t0);
+    const uint32_t mask = (1u << nbits) - 1u;
+#pragma unroll
+    for (int i = 0; i < RS_BINS / 32; i++) hist[warp][lane + 32 * i] = 0;
+    __syncwarp();
+    uint32_t key[RS_IPT], val[RS_IPT], loc[RS_IPT];
+    uint2 pay[PAYLOAD ? RS_IPT : 1];
+#pragma unroll
+    for (int it = 0; it < RS_IPT; it++) {
+        const int p = warp * 32 * RS_IPT + it * 32 + lane;
+        const bool ok = p < nt;
+        key[it] = ok ? kin[t0 + p] : 0u;
+        val[it] = ok ? vin[t0 + p] : 0u;
+        if (PAYLOAD) pay[PAYLOAD ? it : 0] = ok ? pin[t0 + p] : make_uint2(0u, 0u);
+    }
+#pragma unroll
+    for (int it = 0; it < RS_IPT; it++) {
+        const int p = warp * 32 * RS_IPT + it * 32 + lane;
+        const bool ok = p < nt;
+        const uint32_t d = (key[it] >> shift) & mask;
+        const unsigned peers = digit_peers(d, ok);
+        const uint32_t before = ok ? hist[warp][d] : 0u;
+        loc[it] = before + __popc(peers & lt);
+        __syncwarp();
+        if (ok && lane == __ffs(peers) - 1) hist[warp][d] = before + __popc(peers);
+        __syncwarp();
+    }
+    __syncthreads();
+    {  // thread = digit: tile-local digit starts and warp bases
+        uint32_t tot = 0;
+#pragma unroll
+        for (int w = 0; w < RS_NW; w++) tot += hist[w][threadIdx.x];
+        uint32_t ws;
+        const uint32_t start = block_excl_scan_256_u(tot, &ws);
+        dstart[threadIdx.x] = start;
+        gdelta[threadIdx.x] = (uint32_t)offs[(int64_t)threadIdx.x * ntiles + blockIdx.x] - start;
+        uint32_t run = start;
+#pragma unroll
+        for (int w = 0; w < RS_NW; w++) {
+            const uint32_t c = hist[w][threadIdx.x];
+            hist[w][threadIdx.x] = run;
+            run += c;
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int it = 0; it < RS_IPT; it++) {
+        const int p = warp * 32 * RS_IPT + it * 32 + lane;
+        if (p < nt) {
+            const uint32_t l = hist[warp][(key[it] >> shift) & mask] + loc[it];
+            sk[l] = key[it];
+            sv[l] = val[it];
+            if (PAYLOAD) sp[PAYLOAD ? l : 0] = pay[PAYLOAD ? it : 0];
+        }
+    }
+    __syncthreads();
+    for (int l = threadIdx.x; l < nt; l += RS_T) {
+        const uint32_t k = sk[l];
+        const uint32_t dst = gdelta[(k >> shift) & mask] + l;
+        kout[dst] = k;
+        vout[dst] = sv[l];
+        if (PAYLOAD) pout[dst] = sp[PAYLOAD ? l : 0];
+    }
+}
+
+// Three-kernel variant (per-tile histogram, device-wide scan, scatter) — used for the
+// entries, whose many small tiles make onesweep look-back chains long.
+// Stable LSD sort of (k, v[, payload])[0..*n_ptr) on bits [0, bits) with ≤ 8-bit
+// digits.  Returns the number of passes; the result is in the first buffers when
+// even, in the second ones when odd.
+int radix_sort_3k(uint32_t* k, uint32_t* v, uint32_t* k2, uint32_t* v2, uint2* pl, uint2* pl2, const int* n_ptr,
+               int64_t cap, int bits, int* counts, int* scan_tmp, cudaStream_t s, cudaError_t* err) {
+    const int ntiles = radix_tiles(cap);
+    const int npass = (bits + 7) / 8;
+    const int db = npass ? (bits + npass - 1) / npass : 0;
+    *err = cudaSuccess;
+    if (ntiles == 0) return 0;
+    uint32_t *ks = k, *vs = v, *kd = k2, *vd = v2;
+    uint2 *ps = pl, *pd = pl2;
+    for (int pass = 0; pass < npass; pass++) {
+        const int shift = pass * db;
+        const int nb = min(db, bits - shift);
+        k_rs_hist<<<ntiles, RS_T, 0, s>>>(ks, n_ptr, cap, shift, nb, counts, ntiles);
+        if ((*err = scan_exclusive(counts, RS_BINS * ntiles, nullptr, scan_tmp, s)) != cudaSuccess) return pass;
+        if (pl)
+            k_rs_scatter<true><<<ntiles, RS_T, 0, s>>>(ks, vs, kd, vd, ps, pd, n_ptr, cap, shift, nb, counts, ntiles);
+        else
+            k_rs_scatter<false><<<ntiles, RS_T, 0, s>>>(ks, vs, kd, vd, nullptr, nullptr, n_ptr, cap, shift, nb,
+                                                        counts, ntiles);
+        if ((*err = cudaGetLastError()) != cudaSuccess) return pass;
+        uint32_t* t = ks; ks = kd; kd = t;
+        t = vs; vs = vd; vd = t;
+        uint2* tp = ps; ps = pd; pd = tp;
+    }
+    return npass;
+}
+
 // ---------------------------------------------------------------- onesweep
 // Stable LSD radix sort, one kernel per pass.  The digit totals of every pass are
 // counted once up front (the key multiset never changes between passes); within a
@@ -423,8 +556,8 @@ cudaError_t launch_sort_entries(const Launch& L, uint32_t** sorted_vals, cudaStr
     int bits = 1;
     while ((1ll << bits) < (int64_t)L.V * L.T) bits++;
     cudaError_t e;
-    int np = radix_sort(L.key, L.val, L.key2, L.val2, nullptr, nullptr, L.counters + C_K, nullptr, L.cap_entries,
-                        bits, false, L.rs, s, &e);
+    int np = radix_sort_3k(L.key, L.val, L.key2, L.val2, nullptr, nullptr, L.counters + C_K, L.cap_entries, bits,
+                           L.rs_counts, L.scan_tmp, s, &e);
     *sorted_vals = (np & 1) ? L.val2 : L.val;
     if (e != cudaSuccess) return e;
     k_ranges<<<grid_for(L.cap_entries + 1, 256), 256, 0, s>>>(L, (np & 1) ? L.key2 : L.key);

@@ -13,7 +13,7 @@ import subprocess
 import sys
 from collections import OrderedDict
 
-STAGE_OF = [("k_count", "count"), ("k_project", "project"), ("k_rs_scatter<1>", "sort_pairs"),
+STAGE_OF = [("k_count", "count"), ("k_project", "project"), ("k_rs_onesweep<1>", "sort_pairs"),
             ("k_dup", "dup"), ("k_rs_scatter<0>", "sort_entries"), ("k_render_fwd", "render_fwd"),
             ("k_render_bwd", "render_bwd"), ("k_gauss_bwd", "gauss_bwd")]
 
@@ -63,7 +63,7 @@ def traffic(path, out):
     h, units, rows = _raw(path)
     res = {}
     for r in rows:
-        name = r[h.index("Kernel Name")]
+        name = r[h.index("Kernel Name")].replace("mvgs::", "").replace("void ", "")
         for pat, stage in STAGE_OF:
             if name.startswith(pat.split("<")[0]) and (("<" not in pat) or pat.split("<")[1].split(">")[0] in name):
                 rd = _num(r[h.index("dram__bytes_read.sum")])
@@ -85,7 +85,7 @@ def launches(path):
         k.setdefault(r[ii], {"name": r[ki]})[r[mi]] = r[vi]
     items = list(k.values())
     # the last step: from the last k_count onwards
-    last = max(i for i, it in enumerate(items) if it["name"].startswith("k_count"))
+    last = max(i for i, it in enumerate(items) if "k_count" in it["name"])
     step = items[last:]
     tot = sum(_num(it.get("gpu__time_duration.sum", "0")) for it in step)
     print(f"# ncu launch list (--clock-control none, serialised, cold cache) of one step: {path}")
@@ -93,7 +93,8 @@ def launches(path):
     print(f"{'kernel':60s} {'us':>9s} {'share':>6s} {'DRAM rd':>12s} {'DRAM wr':>12s}")
     for it in step:
         t = _num(it.get("gpu__time_duration.sum", "0"))
-        print(f"{it['name'][:60]:60s} {t / 1e3:9.1f} {100 * t / tot:5.1f}% {it.get('dram__bytes_read.sum', ''):>12s} "
+        nm = it["name"].replace("mvgs::", "").replace("void ", "")
+        print(f"{nm[:60]:60s} {t / 1e3:9.1f} {100 * t / tot:5.1f}% {it.get('dram__bytes_read.sum', ''):>12s} "
               f"{it.get('dram__bytes_write.sum', ''):>12s}")
 
 
