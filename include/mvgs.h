@@ -165,6 +165,28 @@ mvgs_status mvgs_export_lists(mvgs_ctx *ctx, int64_t *range_start, int32_t *entr
 mvgs_status mvgs_export_pairs(mvgs_ctx *ctx, int32_t *pair_ids, int32_t *pair_i, float *pair_f, float *pair_g,
                               void *stream);
 
+/* NEXT-1: partial rendering (Alg. 3).  Each (view, tile)
+ * renders only the S pixels listed in `pix` — the index array A of Alg. 3 —
+ * so a V-view batch can render one image's worth of pixels.
+ *   pix   [V, T, S] int32, local pixel index 0..255 inside the 16×16 tile
+ *         (row-major); a listed pixel outside the image is skipped ("isValid").
+ *         T = tiles_x·tiles_y of the preceding preprocess.
+ *   mode  MVGS_PARTIAL_THREAD_EFFICIENT: one block of ⌈S/32⌉·32 threads per
+ *         (view, tile), thread i renders pix[.., i] (Alg. 3);
+ *         MVGS_PARTIAL_MASKED: one 256-thread block per (view, tile) with the
+ *         unlisted pixels masked off (the binary-mask baseline).
+ *   rgb [V,T,S,3], T_final [V,T,S], n_contrib [V,T,S] per listed pixel; the
+ *   values equal the full render's at those pixels.  render_bwd_partial takes
+ *   dL_drgb [V,T,S,3] and accumulates the same per-pair records as
+ *   mvgs_render_bwd (adc_stats follows as usual).  Same ordering rules as the
+ *   full calls (fwd after preprocess, bwd after fwd). */
+#define MVGS_PARTIAL_THREAD_EFFICIENT 0
+#define MVGS_PARTIAL_MASKED 1
+mvgs_status mvgs_render_fwd_partial(mvgs_ctx *ctx, const int32_t *pix, int32_t S, int32_t mode, float *rgb,
+                                    float *T_final, int32_t *n_contrib, void *stream);
+mvgs_status mvgs_render_bwd_partial(mvgs_ctx *ctx, const int32_t *pix, int32_t S, int32_t mode, const float *dL_drgb,
+                                    const float *T_final, const int32_t *n_contrib, void *stream);
+
 /* Stage timing (measurement).  While enabled, every call records a pair of
  * CUDA events on its stream around each kernel stage.  mvgs_stage_times
  * synchronises on them, writes into ms[0..n) the AVERAGE milliseconds per run

@@ -108,6 +108,10 @@ int64_t radix_counts_size(int64_t cap);
 int radix_tiles(int64_t cap);
 cudaError_t launch_render_fwd(const Launch& L, float* rgb, float* Tf, int32_t* nc, cudaStream_t s);
 cudaError_t launch_render_bwd(const Launch& L, const float* dL, const float* Tf, const int32_t* nc, cudaStream_t s);
+cudaError_t launch_render_fwd_partial(const Launch& L, const int32_t* pix, int S, int mode, float* rgb, float* Tf,
+                                      int32_t* nc, cudaStream_t s);
+cudaError_t launch_render_bwd_partial(const Launch& L, const int32_t* pix, int S, int mode, const float* dL,
+                                      const float* Tf, const int32_t* nc, cudaStream_t s);
 cudaError_t launch_gauss_bwd(const Launch& L, const mvgs_grads& gr, const mvgs_adc& adc, cudaStream_t s);
 cudaError_t launch_export(const Launch& L, int64_t* range_start, int32_t* entry_gid, int32_t* pair_ids,
                           int32_t* pair_i, float* pair_f, float* pair_g, cudaStream_t s);

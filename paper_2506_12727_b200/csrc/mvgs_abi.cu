@@ -372,6 +372,36 @@ mvgs_status mvgs_render_bwd(mvgs_ctx* ctx, const float* dL_drgb, const float* T_
     return MVGS_OK;
 }
 
+mvgs_status mvgs_render_fwd_partial(mvgs_ctx* ctx, const int32_t* pix, int32_t S, int32_t mode, float* rgb,
+                                    float* T_final, int32_t* n_contrib, void* stream) {
+    if (!ctx) return MVGS_ERR_INVALID;
+    if (ctx->state < 1) return fail(ctx, MVGS_ERR_STATE, "render_fwd_partial before preprocess");
+    if (!pix || !rgb || !T_final || !n_contrib || S < 1 || S > 256 ||
+        (mode != MVGS_PARTIAL_THREAD_EFFICIENT && mode != MVGS_PARTIAL_MASKED))
+        return fail(ctx, MVGS_ERR_INVALID, "partial: null pointer, S outside [1, 256] or unknown mode");
+    CK(cudaSetDevice(ctx->device));
+    cudaStream_t s = (cudaStream_t)stream;
+    ctx->last_stream = s;
+    { STAGE(ST_FWD); CK(launch_render_fwd_partial(ctx->L, pix, S, mode, rgb, T_final, n_contrib, s)); }
+    ctx->state = 2;
+    return MVGS_OK;
+}
+
+mvgs_status mvgs_render_bwd_partial(mvgs_ctx* ctx, const int32_t* pix, int32_t S, int32_t mode, const float* dL_drgb,
+                                    const float* T_final, const int32_t* n_contrib, void* stream) {
+    if (!ctx) return MVGS_ERR_INVALID;
+    if (ctx->state != 2) return fail(ctx, MVGS_ERR_STATE, "render_bwd_partial needs a render_fwd of a fresh preprocess");
+    if (!pix || !dL_drgb || !T_final || !n_contrib || S < 1 || S > 256 ||
+        (mode != MVGS_PARTIAL_THREAD_EFFICIENT && mode != MVGS_PARTIAL_MASKED))
+        return fail(ctx, MVGS_ERR_INVALID, "partial: null pointer, S outside [1, 256] or unknown mode");
+    CK(cudaSetDevice(ctx->device));
+    cudaStream_t s = (cudaStream_t)stream;
+    ctx->last_stream = s;
+    { STAGE(ST_BWD); CK(launch_render_bwd_partial(ctx->L, pix, S, mode, dL_drgb, T_final, n_contrib, s)); }
+    ctx->state = 3;
+    return MVGS_OK;
+}
+
 mvgs_status mvgs_adc_stats(mvgs_ctx* ctx, const mvgs_grads* grads, const mvgs_adc* adc, void* stream) {
     if (!ctx) return MVGS_ERR_INVALID;
     if (ctx->state != 3) return fail(ctx, MVGS_ERR_STATE, "adc_stats needs a preceding render_bwd");

@@ -20,7 +20,8 @@ NG = 10
 # the exported symbols include/mvgs.h declares (checked by tests/test_abi.py)
 SYMBOLS = ["mvgs_create", "mvgs_destroy", "mvgs_last_error", "mvgs_reserve", "mvgs_preprocess", "mvgs_render_fwd",
            "mvgs_render_bwd", "mvgs_adc_stats", "mvgs_query", "mvgs_export_lists", "mvgs_export_pairs",
-           "mvgs_set_timing", "mvgs_stage_times"]
+           "mvgs_set_timing", "mvgs_stage_times", "mvgs_render_fwd_partial", "mvgs_render_bwd_partial"]
+PARTIAL_THREAD_EFFICIENT, PARTIAL_MASKED = 0, 1
 STAGE_NAMES = ["count", "scan_pairs", "project", "scan_buckets", "sort_pairs", "dup", "sort_entries", "render_fwd",
                "render_bwd", "gauss_bwd"]
 
@@ -74,6 +75,8 @@ def _load():
     L.mvgs_export_lists.argtypes = [vp, vp, vp, vp]
     L.mvgs_export_pairs.argtypes = [vp, vp, vp, vp, vp, vp]
     L.mvgs_set_timing.argtypes = [vp, C.c_int]
+    L.mvgs_render_fwd_partial.argtypes = [vp, vp, C.c_int32, C.c_int32, vp, vp, vp, vp]
+    L.mvgs_render_bwd_partial.argtypes = [vp, vp, C.c_int32, C.c_int32, vp, vp, vp, vp]
     L.mvgs_stage_times.argtypes = [vp, C.POINTER(C.c_float), C.c_int]
     L.mvgs_stage_times.restype = C.c_int
     for n in SYMBOLS:
@@ -148,6 +151,17 @@ def render_fwd(ctx, rgb, T_final, n_contrib, stream=None):
 
 def render_bwd(ctx, dL_drgb, T_final, n_contrib, stream=None):
     _check(ctx, _lib.mvgs_render_bwd(ctx, _ptr(dL_drgb), _ptr(T_final), _ptr(n_contrib), _stream(stream)))
+
+
+def render_fwd_partial(ctx, pix, S: int, mode: int, rgb, T_final, n_contrib, stream=None):
+    """NEXT-1 (Alg. 3): render only the listed pixels (pix [V,T,S] int32, local 0..255)."""
+    _check(ctx, _lib.mvgs_render_fwd_partial(ctx, _ptr(pix), int(S), int(mode), _ptr(rgb), _ptr(T_final),
+                                             _ptr(n_contrib), _stream(stream)))
+
+
+def render_bwd_partial(ctx, pix, S: int, mode: int, dL_drgb, T_final, n_contrib, stream=None):
+    _check(ctx, _lib.mvgs_render_bwd_partial(ctx, _ptr(pix), int(S), int(mode), _ptr(dL_drgb), _ptr(T_final),
+                                             _ptr(n_contrib), _stream(stream)))
 
 
 def adc_stats(ctx, grads: dict, adc: dict, stream=None):
