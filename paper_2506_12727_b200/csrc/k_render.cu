@@ -286,8 +286,15 @@ __global__ __launch_bounds__(256 / NPX) void k_render_bwd(Launch L, const float*
                 const float power = ca_power(a.z, a.w, c.x, dx, dy);
                 if (power > 0.0f || power < c.z) continue;
                 nexp++;
-                const float G = ca_exp_core(power);
-                const float oG = FMUL(c.y, G);
+                // Decisions (α ≥ 1/255, α clamp) must be the forward's: take them from the
+                // hardware exp unless o·G is within 1e-5 (relative) of a threshold, where the
+                // canonical exp decides.  Values use the hardware exp.
+                float G = exp2f(power * 1.4426950408889634f);
+                float oG = c.y * G;
+                if (fabsf(oG - ALPHA_MIN) < 1e-5f * ALPHA_MIN || fabsf(oG - ALPHA_MAX) < 1e-5f * ALPHA_MAX) {
+                    G = ca_exp_core(power);
+                    oG = FMUL(c.y, G);
+                }
                 const float alpha = fminf(ALPHA_MAX, oG);
                 if (alpha < ALPHA_MIN) continue;
                 contrib = true;
