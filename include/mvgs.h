@@ -134,6 +134,11 @@ mvgs_status mvgs_preprocess(mvgs_ctx *ctx, const mvgs_gaussians *g, const mvgs_c
  *   T_final   [V,H,W]    final transmittance
  *   n_contrib [V,H,W]    1 + index of the last blended entry of the pixel's list (R14) */
 mvgs_status mvgs_render_fwd(mvgs_ctx *ctx, float *rgb, float *T_final, int32_t *n_contrib, void *stream);
+/* Same, also writing the rasterizer's predicted depth (NEXT-2): the
+ * alpha-weighted expected camera depth depth[V,H,W] = Σ dᵢ αᵢ Tᵢ over the
+ * blended entries (no background term).  depth may be NULL. */
+mvgs_status mvgs_render_fwd_depth(mvgs_ctx *ctx, float *rgb, float *T_final, int32_t *n_contrib, float *depth,
+                                  void *stream);
 
 /* S7: back-to-front adjoint of Eq. (1) for every (view, tile) given
  * dL_drgb [V,3,H,W] and the T_final / n_contrib written by render_fwd.
@@ -147,6 +152,27 @@ mvgs_status mvgs_render_bwd(mvgs_ctx *ctx, const float *dL_drgb, const float *T_
  * and the ADC statistics E1, E2, E_old, vis.  `grads` and `adc`
  * are host structs of device pointers.  Requires a preceding render_bwd. */
 mvgs_status mvgs_adc_stats(mvgs_ctx *ctx, const mvgs_grads *grads, const mvgs_adc *adc, void *stream);
+
+/* NEXT-2: the 3D distance-aware D-SSIM loss and its gradient.
+ *   SSIM = (2μ1μ2 + C1)(2τ12 + C2) / ((μ1² + μ2² + C1)(τ1² + τ2² + C2))
+ * with the moments μ, τ taken under the 3D kernel
+ *   K*_σ(u, v) ∝ exp(−‖X_uv − X_c‖² / 2σ²)
+ * where X is a pixel's camera-space point from `depth` (render_fwd_depth).
+ * Readings: 11×11 windows, C1 = 0.01², C2 = 0.03²; weights
+ * renormalised over in-image pixels that are not background (T_final > 0.999);
+ * a background centre uses the plain 2D Gaussian (σ = sigma_px); σ at a centre
+ * c is sigma_px·depth_c/fx; depth and T_final are constants of the loss.
+ *   cams     host array [V] (only fx, fy, cx, cy are read; copied into the launch)
+ *   img, target         device [V,3,H,W] fp32 (rendered / ground-truth image)
+ *   depth, T_final      device [V,H,W] fp32
+ *   loss     device [1] fp32: 1 − mean SSIM over V·3·H·W (window centre, channel)
+ *   dL_dimg  device [V,3,H,W] or NULL: ∂loss/∂img, ready for mvgs_render_bwd
+ * Independent of preprocess state; grows context scratch of 48·V·H·W bytes
+ * (synchronising when it does).  MVGS_ERR_INVALID on null inputs, V ∉
+ * [1, 65535], H, W < 1, sigma_px ≤ 0 or fx, fy ≤ 0. */
+mvgs_status mvgs_dssim3d(mvgs_ctx *ctx, const mvgs_camera *cams, int32_t V, int32_t H, int32_t W, const float *img,
+                         const float *target, const float *depth, const float *T_final, float sigma_px, float *loss,
+                         float *dL_dimg, void *stream);
 
 /* Synchronise and report sizes and the capacity flag of the last preprocess.
  * Returns MVGS_ERR_CAPACITY if it overflowed. */
@@ -193,8 +219,8 @@ mvgs_status mvgs_render_bwd_partial(mvgs_ctx *ctx, const int32_t *pix, int32_t S
  * of each stage over all runs recorded since the previous read (0 if none), in
  * the order of MVGS_STAGE_NAMES, clears the record, and returns the number of
  * stages written. */
-#define MVGS_NUM_STAGES 10
-#define MVGS_STAGE_NAMES "count,scan_pairs,project,scan_buckets,sort_pairs,dup,sort_entries,render_fwd,render_bwd,gauss_bwd"
+#define MVGS_NUM_STAGES 11
+#define MVGS_STAGE_NAMES "count,scan_pairs,project,scan_buckets,sort_pairs,dup,sort_entries,render_fwd,render_bwd,gauss_bwd,dssim"
 mvgs_status mvgs_set_timing(mvgs_ctx *ctx, int enable);
 int mvgs_stage_times(mvgs_ctx *ctx, float *ms, int n);
 

@@ -400,6 +400,7 @@ typedef struct {
     int64_t K;
     /* forward */
     double *img, *Tfin;    /* [V,3,H,W], [V,H,W]                             */
+    double *dep;           /* [V,H,W] alpha-weighted expected depth (NEXT-2)  */
     int32_t *ncon;         /* [V,H,W]                                        */
     /* backward */
     double *pg;            /* [V*P*NG]                                       */
@@ -432,7 +433,7 @@ void oracle_destroy(oracle_t *h)
     if (!h) return;
     free(h->p32); free(h->o32); free(h->g64); free(h->p64); free(h->p64i); free(h->off); free(h->gid);
     free(h->mask);
-    free(h->img); free(h->Tfin); free(h->ncon); free(h->pg);
+    free(h->img); free(h->Tfin); free(h->ncon); free(h->pg); free(h->dep);
     free(h->d_means); free(h->d_ls); free(h->d_q); free(h->d_op); free(h->d_sh);
     free(h->e1); free(h->e2); free(h->eold); free(h->vis);
     free(h);
@@ -586,7 +587,7 @@ static void composite(oracle_t *h, const float *dLdC)
                 if (h->mask && !h->mask[b]) continue;
                 /* ---- O5: forward.  Decisions fp32 (CA), values fp64. */
                 float T32 = 1.0f;
-                double T64 = 1.0, Cc[3] = {0, 0, 0};
+                double T64 = 1.0, Cc[3] = {0, 0, 0}, Dd = 0.0;
                 int last = 0, m = 0;
                 const float fxp = (float)x, fyp = (float)y;
                 for (int64_t j = h->off[b]; j < h->off[b + 1]; j++) {
@@ -609,6 +610,7 @@ static void composite(oracle_t *h, const float *dLdC)
                     int clamped = oG > 0.99f;
                     double a64 = clamped ? 0.99 : h->g64[i].o * G;
                     for (int ch = 0; ch < 3; ch++) Cc[ch] += q->rgb[ch] * a64 * T64;
+                    Dd += q->t[2] * a64 * T64; /* predicted depth Σ dᵢαᵢTᵢ */
                     h->dhash = mix(h->dhash, ((uint64_t)j << 20) ^ ((uint64_t)(y * W + x) << 1) ^ (uint64_t)clamped);
                     h->dhash = mix(h->dhash, (uint64_t)(q->clx | q->cly << 1 | q->rgb_clamped[0] << 2
                                                         | q->rgb_clamped[1] << 3 | q->rgb_clamped[2] << 4));
@@ -628,6 +630,7 @@ static void composite(oracle_t *h, const float *dLdC)
                 for (int ch = 0; ch < 3; ch++)
                     h->img[((size_t)v * 3 + ch) * H * W + pix] = Cc[ch] + T64 * h->bg[ch];
                 h->Tfin[(size_t)v * H * W + pix] = T64;
+                h->dep[(size_t)v * H * W + pix] = Dd;
                 h->ncon[(size_t)v * H * W + pix] = last;
                 if (!dLdC) continue;
                 /* ---- O6: adjoint of Eq. (1) for this pixel, from its definition:
@@ -824,6 +827,8 @@ int oracle_forward(oracle_t *h)
     h->img = (double *)calloc(3 * npx, sizeof(double));
     h->Tfin = (double *)calloc(npx, sizeof(double));
     h->ncon = (int32_t *)calloc(npx, sizeof(int32_t));
+    free(h->dep);
+    h->dep = (double *)calloc(npx, sizeof(double));
     composite(h, NULL);
     return 0;
 }
@@ -838,6 +843,8 @@ int oracle_backward(oracle_t *h, const float *dLdC)
     h->Tfin = (double *)calloc(npx, sizeof(double));
     h->ncon = (int32_t *)calloc(npx, sizeof(int32_t));
     h->pg = (double *)calloc((size_t)h->npg * NG + 1, sizeof(double));
+    free(h->dep);
+    h->dep = (double *)calloc(npx, sizeof(double));
 #define ALLOC(f, n) do { free(h->f); h->f = (double *)calloc((size_t)(n) + 1, sizeof(double)); } while (0)
     ALLOC(d_means, 3 * P); ALLOC(d_ls, 3 * P); ALLOC(d_q, 4 * P); ALLOC(d_op, P);
     ALLOC(d_sh, (size_t)P * h->g.sh_stride * 3);
@@ -873,6 +880,11 @@ void oracle_get_image(const oracle_t *h, double *rgb, double *Tfin, int32_t *nco
     if (rgb) memcpy(rgb, h->img, 3 * npx * sizeof(double));
     if (Tfin) memcpy(Tfin, h->Tfin, npx * sizeof(double));
     if (ncon) memcpy(ncon, h->ncon, npx * sizeof(int32_t));
+}
+
+void oracle_get_depth(const oracle_t *h, double *dep)
+{
+    memcpy(dep, h->dep, sizeof(double) * (size_t)h->V * h->W * h->H);
 }
 
 void oracle_get_lists(const oracle_t *h, int64_t *off, int32_t *gid)

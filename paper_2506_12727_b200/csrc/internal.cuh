@@ -87,6 +87,10 @@ struct mvgs_ctx {
     int* d_counters = nullptr;
     unsigned long long* d_counters64 = nullptr;
     int* d_scan = nullptr;  // scan block sums
+    float* d_dssim_coef = nullptr;   // [V,H,W,12] NEXT-2 backward coefficients
+    int64_t cap_dssim_coef = 0;
+    double* d_dssim_part = nullptr;  // per-block SSIM sums
+    int64_t cap_dssim_part = 0;
     mvgs_camera* h_cams = nullptr;  // pinned staging
     cudaEvent_t cams_ev = nullptr;
     cudaStream_t last_stream = nullptr;
@@ -106,7 +110,10 @@ cudaError_t launch_dup_sort(const Launch& L, const uint32_t* order, const uint2*
 cudaError_t launch_sort_entries(const Launch& L, uint32_t** sorted_vals, cudaStream_t s);
 int64_t radix_counts_size(int64_t cap);
 int radix_tiles(int64_t cap);
-cudaError_t launch_render_fwd(const Launch& L, float* rgb, float* Tf, int32_t* nc, cudaStream_t s);
+cudaError_t launch_render_fwd(const Launch& L, float* rgb, float* Tf, int32_t* nc, float* depth, cudaStream_t s);
+cudaError_t launch_dssim3d(const mvgs_camera* h_cams, int V, int H, int W, const float* img, const float* tgt,
+                           const float* depth, const float* Tf, float sigma_px, float* loss, float* grad, float* coef,
+                           double* partial, cudaStream_t s);
 cudaError_t launch_render_bwd(const Launch& L, const float* dL, const float* Tf, const int32_t* nc, cudaStream_t s);
 cudaError_t launch_render_fwd_partial(const Launch& L, const int32_t* pix, int S, int mode, float* rgb, float* Tf,
                                       int32_t* nc, cudaStream_t s);

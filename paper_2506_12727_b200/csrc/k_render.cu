@@ -61,17 +61,19 @@ __device__ __forceinline__ void pixel_pair(int tx, int ty, int& x, int& y0, int&
     y1 = y0 + 2;
 }
 
-// stage one record: (x, y, A, B) (C, o, skip bound, -) (r, g, b, -)
+// stage one record: (x, y, A, B) (C, o, skip bound, -) (r, g, b, depth)
 __device__ __forceinline__ void stage(const Launch& L, uint32_t q, float4* s0, float4* s1, float4* s2, int i) {
     const float4* r = L.rec + 3 * (int64_t)q;
     const float4 r0 = r[0], r1 = r[1], r2 = r[2];
     s0[i] = r0;
     s1[i] = make_float4(r1.x, r1.y, skip_power(r1.y), 0.f);
-    s2[i] = make_float4(r1.z, r1.w, r2.x, 0.f);
+    s2[i] = make_float4(r1.z, r1.w, r2.x, r2.y);
 }
 
+// DEPTH: also accumulate the alpha-weighted expected depth Σ dᵢ αᵢ Tᵢ (NEXT-2)
+template <bool DEPTH>
 __global__ __launch_bounds__(RT) void k_render_fwd(Launch L, float* __restrict__ out_rgb, float* __restrict__ out_T,
-                                                   int32_t* __restrict__ out_n) {
+                                                   int32_t* __restrict__ out_n, float* __restrict__ out_D) {
     __shared__ float4 s0[RT], s1[RT], s2[RT];
     __shared__ unsigned sev[2];
     const int bucket = blockIdx.x;
@@ -81,14 +83,14 @@ __global__ __launch_bounds__(RT) void k_render_fwd(Launch L, float* __restrict__
     pixel_pair(tx, ty, x, y[0], y[1]);
     const int start = L.bucket_off[bucket], end = L.bucket_off[bucket + 1];
     const float fx = (float)x;
-    float fy[2], T[2], C0[2], C1[2], C2[2];
+    float fy[2], T[2], C0[2], C1[2], C2[2], D[2];
     int last[2];
     bool done[2];
 #pragma unroll
     for (int p = 0; p < 2; p++) {
         fy[p] = (float)y[p];
         T[p] = 1.0f;
-        C0[p] = C1[p] = C2[p] = 0.f;
+        C0[p] = C1[p] = C2[p] = D[p] = 0.f;
         last[p] = 0;
         done[p] = !(x < L.W && y[p] < L.H);
     }
@@ -127,6 +129,7 @@ __global__ __launch_bounds__(RT) void k_render_fwd(Launch L, float* __restrict__
                     C0[p] += col.x * w;
                     C1[p] += col.y * w;
                     C2[p] += col.z * w;
+                    if (DEPTH) D[p] += col.w * w;
                     T[p] = Tn;
                     last[p] = b0 - start + j + 1;
                 }
@@ -144,11 +147,15 @@ __global__ __launch_bounds__(RT) void k_render_fwd(Launch L, float* __restrict__
         out_rgb[(3 * (int64_t)v + 2) * HW + pix] = C2[p] + T[p] * L.bg[2];
         out_T[v * HW + pix] = T[p];
         out_n[v * HW + pix] = last[p];
+        if (DEPTH) out_D[v * HW + pix] = D[p];
     }
 }
 
-cudaError_t launch_render_fwd(const Launch& L, float* rgb, float* Tf, int32_t* nc, cudaStream_t s) {
-    k_render_fwd<<<L.V * L.T, RT, 0, s>>>(L, rgb, Tf, nc);
+cudaError_t launch_render_fwd(const Launch& L, float* rgb, float* Tf, int32_t* nc, float* depth, cudaStream_t s) {
+    if (depth)
+        k_render_fwd<true><<<L.V * L.T, RT, 0, s>>>(L, rgb, Tf, nc, depth);
+    else
+        k_render_fwd<false><<<L.V * L.T, RT, 0, s>>>(L, rgb, Tf, nc, nullptr);
     return cudaGetLastError();
 }
 

@@ -122,7 +122,7 @@ cudaError_t alloc_entries(mvgs_ctx* c, int64_t n) {
 }
 
 enum { ST_COUNT, ST_SCAN_PAIRS, ST_PROJECT, ST_SCAN_BUCKETS, ST_SORT_PAIRS, ST_DUP, ST_SORT_ENTRIES, ST_FWD, ST_BWD,
-       ST_GAUSS };
+       ST_GAUSS, ST_DSSIM };
 
 cudaEvent_t pool_get(mvgs_ctx* c) {
     if (!c->ev_pool.empty()) {
@@ -231,6 +231,7 @@ void mvgs_destroy(mvgs_ctx* ctx) {
     cudaFree(ctx->d_ecount); cudaFree(ctx->d_rs); cudaFree(ctx->d_rs_status); cudaFree(ctx->d_rs_small); cudaFree(ctx->d_prect); cudaFree(ctx->d_prect2);
     cudaFree(ctx->d_pflag);
     cudaFree(ctx->d_counters); cudaFree(ctx->d_counters64); cudaFree(ctx->d_scan);
+    cudaFree(ctx->d_dssim_coef); cudaFree(ctx->d_dssim_part);
     if (ctx->h_cams) cudaFreeHost(ctx->h_cams);
     if (ctx->cams_ev) cudaEventDestroy(ctx->cams_ev);
     for (int i = 0; i < MVGS_NUM_STAGES; i++)
@@ -344,6 +345,11 @@ mvgs_status mvgs_preprocess(mvgs_ctx* ctx, const mvgs_gaussians* g, const mvgs_c
 }
 
 mvgs_status mvgs_render_fwd(mvgs_ctx* ctx, float* rgb, float* T_final, int32_t* n_contrib, void* stream) {
+    return mvgs_render_fwd_depth(ctx, rgb, T_final, n_contrib, nullptr, stream);
+}
+
+mvgs_status mvgs_render_fwd_depth(mvgs_ctx* ctx, float* rgb, float* T_final, int32_t* n_contrib, float* depth,
+                                  void* stream) {
     if (!ctx) return MVGS_ERR_INVALID;
     if (ctx->state < 1) return fail(ctx, MVGS_ERR_STATE, "render_fwd before preprocess");
     if (!rgb || !T_final || !n_contrib) return fail(ctx, MVGS_ERR_INVALID, "null output");
@@ -352,7 +358,7 @@ mvgs_status mvgs_render_fwd(mvgs_ctx* ctx, float* rgb, float* T_final, int32_t* 
     cudaStream_t s = (cudaStream_t)stream;
     CK(cudaMemsetAsync(ctx->d_counters64, 0, sizeof(unsigned long long), s));
     CK(cudaMemsetAsync(ctx->d_counters64 + 2, 0, sizeof(unsigned long long), s));
-    { STAGE(ST_FWD); CK(launch_render_fwd(ctx->L, rgb, T_final, n_contrib, s)); }  // S6
+    { STAGE(ST_FWD); CK(launch_render_fwd(ctx->L, rgb, T_final, n_contrib, depth, s)); }  // S6
     ctx->state = 2;
     return MVGS_OK;
 }
@@ -461,6 +467,30 @@ mvgs_status mvgs_export_pairs(mvgs_ctx* ctx, int32_t* pair_ids, int32_t* pair_i,
 mvgs_status mvgs_set_timing(mvgs_ctx* ctx, int enable) {
     if (!ctx) return MVGS_ERR_INVALID;
     ctx->timing = enable != 0;
+    return MVGS_OK;
+}
+
+mvgs_status mvgs_dssim3d(mvgs_ctx* ctx, const mvgs_camera* cams, int32_t V, int32_t H, int32_t W, const float* img,
+                         const float* target, const float* depth, const float* T_final, float sigma_px, float* loss,
+                         float* dL_dimg, void* stream) {
+    if (!ctx) return MVGS_ERR_INVALID;
+    if (!cams || !img || !target || !depth || !T_final || !loss)
+        return fail(ctx, MVGS_ERR_INVALID, "dssim3d: null argument");
+    if (V < 1 || V > 65535 || H < 1 || W < 1 || !(sigma_px > 0.f))
+        return fail(ctx, MVGS_ERR_INVALID, "dssim3d: V, H, W must be positive and sigma_px > 0");
+    for (int v = 0; v < V; v++)
+        if (!(cams[v].fx > 0.f) || !(cams[v].fy > 0.f)) return fail(ctx, MVGS_ERR_INVALID, "dssim3d: fx, fy must be > 0");
+    CK(cudaSetDevice(ctx->device));
+    cudaStream_t s = (cudaStream_t)stream;
+    const int64_t npx = (int64_t)V * H * W;
+    const int64_t nblk = (int64_t)V * ((W + 15) / 16) * ((H + 15) / 16);
+    if (npx * 12 > ctx->cap_dssim_coef || nblk > ctx->cap_dssim_part) {
+        CK(cudaDeviceSynchronize());
+        CK(grow(ctx->d_dssim_coef, ctx->cap_dssim_coef, npx * 12));
+        CK(grow(ctx->d_dssim_part, ctx->cap_dssim_part, nblk));
+    }
+    { STAGE(ST_DSSIM); CK(launch_dssim3d(cams, V, H, W, img, target, depth, T_final, sigma_px, loss, dL_dimg,
+                                         ctx->d_dssim_coef, ctx->d_dssim_part, s)); }
     return MVGS_OK;
 }
 

@@ -20,10 +20,11 @@ NG = 10
 # the exported symbols include/mvgs.h declares (checked by tests/test_abi.py)
 SYMBOLS = ["mvgs_create", "mvgs_destroy", "mvgs_last_error", "mvgs_reserve", "mvgs_preprocess", "mvgs_render_fwd",
            "mvgs_render_bwd", "mvgs_adc_stats", "mvgs_query", "mvgs_export_lists", "mvgs_export_pairs",
-           "mvgs_set_timing", "mvgs_stage_times", "mvgs_render_fwd_partial", "mvgs_render_bwd_partial"]
+           "mvgs_set_timing", "mvgs_stage_times", "mvgs_render_fwd_partial", "mvgs_render_bwd_partial",
+           "mvgs_render_fwd_depth", "mvgs_dssim3d"]
 PARTIAL_THREAD_EFFICIENT, PARTIAL_MASKED = 0, 1
 STAGE_NAMES = ["count", "scan_pairs", "project", "scan_buckets", "sort_pairs", "dup", "sort_entries", "render_fwd",
-               "render_bwd", "gauss_bwd"]
+               "render_bwd", "gauss_bwd", "dssim"]
 
 
 class MvgsError(RuntimeError):
@@ -69,6 +70,7 @@ def _load():
     L.mvgs_reserve.argtypes = [vp, i64, i64]
     L.mvgs_preprocess.argtypes = [vp, C.POINTER(Gaussians), vp, C.c_int32, vp, vp]
     L.mvgs_render_fwd.argtypes = [vp, vp, vp, vp, vp]
+    L.mvgs_render_fwd_depth.argtypes = [vp, vp, vp, vp, vp, vp]
     L.mvgs_render_bwd.argtypes = [vp, vp, vp, vp, vp]
     L.mvgs_adc_stats.argtypes = [vp, C.POINTER(Grads), C.POINTER(Adc), vp]
     L.mvgs_query.argtypes = [vp, C.POINTER(Stats)]
@@ -77,6 +79,7 @@ def _load():
     L.mvgs_set_timing.argtypes = [vp, C.c_int]
     L.mvgs_render_fwd_partial.argtypes = [vp, vp, C.c_int32, C.c_int32, vp, vp, vp, vp]
     L.mvgs_render_bwd_partial.argtypes = [vp, vp, C.c_int32, C.c_int32, vp, vp, vp, vp]
+    L.mvgs_dssim3d.argtypes = [vp, vp, C.c_int32, C.c_int32, C.c_int32, vp, vp, vp, vp, C.c_float, vp, vp, vp]
     L.mvgs_stage_times.argtypes = [vp, C.POINTER(C.c_float), C.c_int]
     L.mvgs_stage_times.restype = C.c_int
     for n in SYMBOLS:
@@ -147,6 +150,22 @@ def preprocess(ctx, g: dict, cams: np.ndarray, bg=(0.0, 0.0, 0.0), stream=None):
 
 def render_fwd(ctx, rgb, T_final, n_contrib, stream=None):
     _check(ctx, _lib.mvgs_render_fwd(ctx, _ptr(rgb), _ptr(T_final), _ptr(n_contrib), _stream(stream)))
+
+
+def render_fwd_depth(ctx, rgb, T_final, n_contrib, depth, stream=None):
+    _check(ctx, _lib.mvgs_render_fwd_depth(ctx, _ptr(rgb), _ptr(T_final), _ptr(n_contrib), _ptr(depth),
+                                           _stream(stream)))
+
+
+def dssim3d(ctx, cams: np.ndarray, img, target, depth, T_final, loss, dL_dimg=None, sigma_px: float = 1.5,
+            stream=None):
+    """NEXT-2: 3D distance-aware D-SSIM.  img/target [V,3,H,W],
+    depth/T_final [V,H,W], loss [1] (device fp32); dL_dimg [V,3,H,W] or None."""
+    cams = np.ascontiguousarray(cams)
+    assert cams.dtype.itemsize == CAM_BYTES
+    V, _, H, W = img.shape
+    _check(ctx, _lib.mvgs_dssim3d(ctx, cams.ctypes.data, V, H, W, _ptr(img), _ptr(target), _ptr(depth), _ptr(T_final),
+                                  float(sigma_px), _ptr(loss), _ptr(dL_dimg), _stream(stream)))
 
 
 def render_bwd(ctx, dL_drgb, T_final, n_contrib, stream=None):

@@ -340,3 +340,37 @@ def make_dLdC_scaled(V: int, H: int, W: int, seed: int) -> np.ndarray:
 
 def subset_views(cams: np.ndarray, lo: int, hi: int) -> np.ndarray:
     return np.ascontiguousarray(cams[lo:hi])
+
+
+def make_dssim_inputs(V: int, H: int, W: int, seed: int, bg_frac: float = 0.15):
+    """Seeded inputs for the NEXT-2 D-SSIM (DESIGN.md §14 recipe): a rendered-like
+    image (smooth colour ramps + texture, in [0, 1]), a target = image + noise,
+    a depth map of two slanted planes with a step edge between them (2–7 units,
+    the object360 depth range) and a background region (T_final = 1, depth 0)
+    in a corner disc; foreground T_final ∈ [0, 0.3].  Returns float32 arrays
+    img, target [V,3,H,W], depth, T_final [V,H,W] and a cams array (f = 0.9·W)."""
+    rng = np.random.Generator(np.random.PCG64(seed + 500))
+    y, x = np.mgrid[0:H, 0:W].astype(np.float64)
+    img = np.empty((V, 3, H, W))
+    depth = np.empty((V, H, W))
+    Tf = np.empty((V, H, W))
+    cams = []
+    for v in range(V):
+        for c in range(3):
+            a, b, ph = rng.uniform(-1, 1, 3)
+            img[v, c] = 0.5 + 0.25 * (a * x / W + b * y / H) + 0.15 * np.sin(ph * 6 + x * 0.7 + y * 0.3 * (c + 1))
+        img[v] += rng.normal(0, 0.05, (3, H, W))
+        edge = rng.uniform(0.35, 0.65) * W
+        near = 2.0 + rng.uniform(0, 1) + 0.01 * (x - W / 2) + 0.005 * y
+        far = 5.0 + rng.uniform(0, 1) - 0.008 * y
+        depth[v] = np.where(x < edge + 0.2 * (y - H / 2), near, far)
+        r = np.hypot(x - W, y - H)
+        bgm = r < np.sqrt(bg_frac * 4 * W * H / np.pi)
+        Tf[v] = rng.uniform(0.0, 0.3, (H, W))
+        Tf[v][bgm] = 1.0
+        depth[v][bgm] = 0.0
+        cams.append(make_camera(np.eye(3), [0, 0, 0], W, H, 0.9 * W))
+    img = np.clip(img, 0, 1)
+    tgt = np.clip(img + rng.normal(0, 0.08, img.shape), 0, 1)
+    return (img.astype(np.float32), tgt.astype(np.float32), depth.astype(np.float32), Tf.astype(np.float32),
+            cams_array(cams))

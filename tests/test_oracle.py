@@ -450,3 +450,17 @@ def test_tile_mask_mode_equals_full_run_on_the_mask():
     off_m, gid_m = m.lists()
     for b in np.nonzero(mask.reshape(-1))[0]:
         np.testing.assert_array_equal(gid_m[off_m[b]:off_m[b + 1]], gid_f[off_f[b]:off_f[b + 1]])
+
+
+def test_predicted_depth_single_gaussian():
+    """NEXT-2 predicted depth Σ dᵢαᵢTᵢ: one Gaussian at depth z ⇒ z·α on its
+    footprint, 0 elsewhere; two co-centred terms ⇒ z₁α₁ + z₂α₂(1−α₁)."""
+    s, z, f, W = 0.06, 2.0, 40.0, 32
+    g = scene([0, 0, z], log_scales=np.full(3, math.log(s)), logits=[0.3])
+    o = oracle.Oracle(g, cam_identity(W=W, H=W, f=f))
+    im = o.forward()
+    np.testing.assert_allclose(o.depth()[0], z * (1 - im["T_final"][0]), atol=1e-12)
+    g2 = scene([[0, 0, 2.0], [0, 0, 3.0]], log_scales=np.full((2, 3), math.log(0.05)), logits=[0.0, math.log(9.0)])
+    o2 = oracle.Oracle(g2, cam_identity(W=33, H=33, f=40.0))
+    o2.forward()
+    assert abs(o2.depth()[0, 16, 16] - (2.0 * 0.5 + 3.0 * 0.9 * 0.5)) < 1e-6
