@@ -111,6 +111,7 @@ cudaError_t launch_sort_entries(const Launch& L, uint32_t** sorted_vals, cudaStr
 int64_t radix_counts_size(int64_t cap);
 int radix_tiles(int64_t cap);
 cudaError_t launch_render_fwd(const Launch& L, float* rgb, float* Tf, int32_t* nc, float* depth, cudaStream_t s);
+int64_t dssim_partials(int V, int H, int W);
 cudaError_t launch_dssim3d(const mvgs_camera* h_cams, int V, int H, int W, const float* img, const float* tgt,
                            const float* depth, const float* Tf, float sigma_px, float* loss, float* grad, float* coef,
                            double* partial, cudaStream_t s);

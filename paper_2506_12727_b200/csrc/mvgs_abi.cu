@@ -483,7 +483,7 @@ mvgs_status mvgs_dssim3d(mvgs_ctx* ctx, const mvgs_camera* cams, int32_t V, int3
     CK(cudaSetDevice(ctx->device));
     cudaStream_t s = (cudaStream_t)stream;
     const int64_t npx = (int64_t)V * H * W;
-    const int64_t nblk = (int64_t)V * ((W + 15) / 16) * ((H + 15) / 16);
+    const int64_t nblk = dssim_partials(V, H, W);
     if (npx * 12 > ctx->cap_dssim_coef || nblk > ctx->cap_dssim_part) {
         CK(cudaDeviceSynchronize());
         CK(grow(ctx->d_dssim_coef, ctx->cap_dssim_coef, npx * 12));
