@@ -374,3 +374,26 @@ def make_dssim_inputs(V: int, H: int, W: int, seed: int, bg_frac: float = 0.15):
     tgt = np.clip(img + rng.normal(0, 0.08, img.shape), 0, 1)
     return (img.astype(np.float32), tgt.astype(np.float32), depth.astype(np.float32), Tf.astype(np.float32),
             cams_array(cams))
+
+
+def make_adc_inputs(P: int, seed: int, N: int = 2, sh_degree: int = 3, iters: int = 100, B: int = 4):
+    """Seeded inputs for the NEXT-3 ADC step (DESIGN.md §15 recipe): Gaussians from the
+    object360 generator's distributions (log-scales around ln 0.01, opacities U[0.002, 0.95]),
+    running accumulators of `iters` steps of B views — denom ~ integer U[0, B·iters] with 10%
+    never visible, per-visibility mean E1 log-normal around 2e-4, E2 = E1·U[0.3, 1],
+    E_old = E2·U[0, 1] (the triangle-inequality order E1 ≥ E2 ≥ E_old) — and the split noise
+    n ~ N(0, I) [P, N, 3]."""
+    rng = np.random.Generator(np.random.PCG64(seed + 900))
+    means = rng.normal(0, 1.0, (P, 3))
+    log_scales = np.log(0.01) + rng.normal(0, 0.8, (P, 3))
+    quats = _unit_quats(rng, P)
+    op = rng.uniform(0.002, 0.95, P)
+    g = _finish(rng, means, log_scales, quats, np.log(op / (1 - op)), sh_degree)
+    den = rng.integers(0, B * iters + 1, P).astype(np.float32)
+    den[rng.uniform(0, 1, P) < 0.1] = 0
+    e1 = (den * np.exp(rng.normal(np.log(2e-4), 0.7, P))).astype(np.float32)
+    e2 = (e1 * rng.uniform(0.3, 1.0, P)).astype(np.float32)
+    eo = (e2 * rng.uniform(0.0, 1.0, P)).astype(np.float32)
+    acc = dict(e1=e1, e2=e2, e_old=eo, denom=den)
+    noise = rng.normal(0, 1, (P, N, 3)).astype(np.float32)
+    return g, acc, noise
