@@ -93,6 +93,7 @@ typedef struct {
     float *e1_acc;    /* [P] nullable, += e1  */
     float *e2_acc;    /* [P] nullable, += e2  */
     float *denom_acc; /* [P] nullable, += vis */
+    float *e_old_acc; /* [P] nullable, += e_old (single-view ADC metric, NEXT-3 mode 0) */
 } mvgs_adc;
 
 typedef struct {
@@ -173,6 +174,66 @@ mvgs_status mvgs_adc_stats(mvgs_ctx *ctx, const mvgs_grads *grads, const mvgs_ad
 mvgs_status mvgs_dssim3d(mvgs_ctx *ctx, const mvgs_camera *cams, int32_t V, int32_t H, int32_t W, const float *img,
                          const float *target, const float *depth, const float *T_final, float sigma_px, float *loss,
                          float *dL_dimg, void *stream);
+
+/* ---- NEXT-3: the multi-view ADC step (P:4) --------------------------- */
+
+/* Per-interval densification policy.  Readings R35–R42. */
+typedef struct {
+    float grad_threshold_split; /* τ on the mean of E1 (mode 1) or E_old (mode 0): split if ≥ and large */
+    float grad_threshold_clone; /* τ on the mean of E2 (mode 1) or E_old (mode 0): clone if ≥ and small */
+    float size_threshold;       /* world units, > 0: "large" ⟺ max scale > size_threshold          */
+    float split_factor;         /* > 0: children get scale / split_factor (3DGS 1.6)                 */
+    int32_t split_count;        /* N ∈ [2, 8] children per split                                      */
+    float prune_opacity;        /* prune if opacity < prune_opacity × batch_views, ∈ (0, 1)   */
+    float prune_scale_max;      /* prune if max scale > this (world units); ≤ 0 disables             */
+    int32_t metric_mode;        /* 0: E_old for both (single-view ADC), 1: E1 split / E2 clone */
+    int32_t batch_views;        /* B ≥ 1, images per iteration                                       */
+} mvgs_adc_config;
+
+/* Running accumulators (device [P]; the *_acc outputs of mvgs_adc_stats). e_old_acc is read in
+ * mode 0 only, e1/e2 in mode 1 only; the unused ones may be NULL. */
+typedef struct {
+    const float *e1_acc, *e2_acc, *e_old_acc, *denom_acc;
+} mvgs_adc_accum;
+
+/* Output Gaussian arrays (device), `capacity` rows each; sh_stride must equal the input's. */
+typedef struct {
+    int64_t capacity;
+    int32_t sh_stride;
+    float *means, *log_scales, *quats, *opacity_logits, *sh;
+} mvgs_gaussians_out;
+
+typedef struct {
+    int64_t n_split;  /* parents split (each replaced by split_count children)           */
+    int64_t n_clone;  /* parents cloned                                                    */
+    int64_t n_pruned; /* emitted Gaussians (kept, clones, children) removed by the prune  */
+    int64_t P_new;    /* rows written = P + (N−1)·n_split + n_clone − n_pruned             */
+} mvgs_adc_report;
+
+/* One ADC event.  Per Gaussian g, with Ē = acc/denom in fp32 (0 where denom = 0):
+ *   split ⟺ Ē_split ≥ τ_split ∧ max log_scale > fp32(ln size_threshold)
+ *   clone ⟺ Ē_clone ≥ τ_clone ∧ ¬large
+ * Emitted in canonical order — for g = 0..P−1: g itself unless split, its clone, its N children
+ * (child k: mean + R(q̂)·(exp(log_scale) ⊙ noise[g,k]), log_scale − fp32(ln split_factor), other
+ * parameters copied) — then every emitted row with opacity logit < fp32(logit(prune_opacity·B))
+ * or max log_scale > fp32(ln prune_scale_max) is dropped (prune-compaction).
+ *   noise   device [P, split_count, 3] standard normals (the step's random draw, an input)
+ *   origin  device [capacity] int32: the input row each output row derives from
+ *   kind    device [capacity] uint8: 0 kept, 1 clone, 2 split child
+ *   report  host; filled on success and on MVGS_ERR_CAPACITY (P_new > out->capacity, nothing
+ *           written).  Synchronises the stream once (the new count is needed on the host).
+ * quats and sh (input and output) must be 16-byte aligned.
+ * MVGS_ERR_INVALID on null pointers, P < 0, sh_stride mismatch, misalignment or a config
+ * outside its range. */
+mvgs_status mvgs_adc_step(mvgs_ctx *ctx, const mvgs_gaussians *g, const mvgs_adc_accum *acc, const float *noise,
+                          const mvgs_adc_config *cfg, const mvgs_gaussians_out *out, int32_t *origin, uint8_t *kind,
+                          mvgs_adc_report *report, void *stream);
+
+/* Optimiser-state resize after mvgs_adc_step: dst[i, :] = src[origin[i], :] for kept rows, 0 for
+ * clones and split children (new Gaussians start with zero moments).  src [P, width],
+ * dst [P_new, width] device fp32, distinct buffers. */
+mvgs_status mvgs_adc_remap(mvgs_ctx *ctx, const float *src, float *dst, int64_t width, const int32_t *origin,
+                           const uint8_t *kind, int64_t P_new, void *stream);
 
 /* Synchronise and report sizes and the capacity flag of the last preprocess.
  * Returns MVGS_ERR_CAPACITY if it overflowed. */

@@ -91,6 +91,14 @@ struct mvgs_ctx {
     int64_t cap_dssim_coef = 0;
     double* d_dssim_part = nullptr;  // per-block SSIM sums
     int64_t cap_dssim_part = 0;
+    int* d_adc_cnt = nullptr;        // NEXT-3 per-Gaussian emitted-row counts → offsets
+    int64_t cap_adc_cnt = 0;
+    uint8_t* d_adc_flags = nullptr;
+    int64_t cap_adc_flags = 0;
+    int* d_adc_tmp = nullptr;        // scan block sums
+    int64_t cap_adc_tmp = 0;
+    unsigned long long* d_adc_rep = nullptr;  // [4] split, clone, pruned, total
+    long long* h_adc_rep = nullptr;           // pinned mirror
     mvgs_camera* h_cams = nullptr;  // pinned staging
     cudaEvent_t cams_ev = nullptr;
     cudaStream_t last_stream = nullptr;
@@ -112,6 +120,17 @@ int64_t radix_counts_size(int64_t cap);
 int radix_tiles(int64_t cap);
 cudaError_t launch_render_fwd(const Launch& L, float* rgb, float* Tf, int32_t* nc, float* depth, cudaStream_t s);
 int64_t dssim_partials(int V, int H, int W);
+struct AdcParamsHost {
+    float tau_split, tau_clone, ln_size, ln_split, logit_prune, ln_prune_scale;
+    int N, mode;
+};
+cudaError_t launch_adc_decide(const mvgs_gaussians& g, const mvgs_adc_accum& acc, const AdcParamsHost& h, int* cnt,
+                              uint8_t* flags, unsigned long long* rep, cudaStream_t s);
+cudaError_t launch_adc_emit(const mvgs_gaussians& g, const uint8_t* flags, const int* offs, const float* noise,
+                            const AdcParamsHost& h, const mvgs_gaussians_out& out, int32_t* origin, uint8_t* kind,
+                            cudaStream_t s);
+cudaError_t launch_adc_remap(const float* src, float* dst, int64_t width, const int32_t* origin, const uint8_t* kind,
+                             int64_t P_new, cudaStream_t s);
 cudaError_t launch_dssim3d(const mvgs_camera* h_cams, int V, int H, int W, const float* img, const float* tgt,
                            const float* depth, const float* Tf, float sigma_px, float* loss, float* grad, float* coef,
                            double* partial, cudaStream_t s);

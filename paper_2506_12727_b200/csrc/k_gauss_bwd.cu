@@ -387,7 +387,11 @@ __global__ __launch_bounds__(BLK, 2) void k_gauss_bwd(Launch L, mvgs_grads gr, m
     gr.d_opacity_logits[g] = dop * a.o * (1.f - a.o);
     adc.e1[g] = e1;
     adc.e2[g] = e2;
-    if (adc.e_old) adc.e_old[g] = sqrtf(gsx * gsx + gsy * gsy);
+    if (adc.e_old || adc.e_old_acc) {
+        const float eo = sqrtf(gsx * gsx + gsy * gsy);
+        if (adc.e_old) adc.e_old[g] = eo;
+        if (adc.e_old_acc) adc.e_old_acc[g] += eo;
+    }
     adc.vis[g] = nvis;
     if (adc.e1_acc) adc.e1_acc[g] += e1;
     if (adc.e2_acc) adc.e2_acc[g] += e2;

@@ -3,6 +3,7 @@
 // the method lives here; every step runs in the kernels of k_*.cu.
 #include <algorithm>
 #include <cstdio>
+#include <cmath>
 #include <cstring>
 #include <new>
 #include "ca.cuh"
@@ -232,6 +233,8 @@ void mvgs_destroy(mvgs_ctx* ctx) {
     cudaFree(ctx->d_pflag);
     cudaFree(ctx->d_counters); cudaFree(ctx->d_counters64); cudaFree(ctx->d_scan);
     cudaFree(ctx->d_dssim_coef); cudaFree(ctx->d_dssim_part);
+    cudaFree(ctx->d_adc_cnt); cudaFree(ctx->d_adc_flags); cudaFree(ctx->d_adc_tmp); cudaFree(ctx->d_adc_rep);
+    if (ctx->h_adc_rep) cudaFreeHost(ctx->h_adc_rep);
     if (ctx->h_cams) cudaFreeHost(ctx->h_cams);
     if (ctx->cams_ev) cudaEventDestroy(ctx->cams_ev);
     for (int i = 0; i < MVGS_NUM_STAGES; i++)
@@ -491,6 +494,83 @@ mvgs_status mvgs_dssim3d(mvgs_ctx* ctx, const mvgs_camera* cams, int32_t V, int3
     }
     { STAGE(ST_DSSIM); CK(launch_dssim3d(cams, V, H, W, img, target, depth, T_final, sigma_px, loss, dL_dimg,
                                          ctx->d_dssim_coef, ctx->d_dssim_part, s)); }
+    return MVGS_OK;
+}
+
+static bool aligned16(const void* p) { return ((uintptr_t)p & 15) == 0; }
+
+mvgs_status mvgs_adc_step(mvgs_ctx* ctx, const mvgs_gaussians* g, const mvgs_adc_accum* acc, const float* noise,
+                          const mvgs_adc_config* cfg, const mvgs_gaussians_out* out, int32_t* origin, uint8_t* kind,
+                          mvgs_adc_report* report, void* stream) {
+    if (!ctx) return MVGS_ERR_INVALID;
+    if (!g || !acc || !cfg || !out || !origin || !kind || !report)
+        return fail(ctx, MVGS_ERR_INVALID, "adc_step: null argument");
+    if (g->P < 0 || g->P >= (int64_t)INT32_MAX / 10) return fail(ctx, MVGS_ERR_INVALID, "adc_step: P out of range");
+    if (g->P > 0 && (!g->means || !g->log_scales || !g->quats || !g->opacity_logits || !g->sh || !noise ||
+                     !acc->denom_acc || (cfg->metric_mode == 1 && (!acc->e1_acc || !acc->e2_acc)) ||
+                     (cfg->metric_mode == 0 && !acc->e_old_acc)))
+        return fail(ctx, MVGS_ERR_INVALID, "adc_step: null input array");
+    if (!out->means || !out->log_scales || !out->quats || !out->opacity_logits || !out->sh || out->capacity < 0)
+        return fail(ctx, MVGS_ERR_INVALID, "adc_step: null output array");
+    if (out->sh_stride != g->sh_stride || g->sh_stride < 1)
+        return fail(ctx, MVGS_ERR_INVALID, "adc_step: sh_stride mismatch");
+    if (!aligned16(g->quats) || !aligned16(out->quats) || !aligned16(g->sh) || !aligned16(out->sh))
+        return fail(ctx, MVGS_ERR_INVALID, "adc_step: quats / sh not 16-B aligned");
+    if (cfg->split_count < 2 || cfg->split_count > 8 || !(cfg->size_threshold > 0.f) || !(cfg->split_factor > 0.f) ||
+        !(cfg->prune_opacity > 0.f && cfg->prune_opacity < 1.f) || cfg->batch_views < 1 ||
+        (cfg->metric_mode != 0 && cfg->metric_mode != 1))
+        return fail(ctx, MVGS_ERR_INVALID, "adc_step: config out of range");
+    CK(cudaSetDevice(ctx->device));
+    cudaStream_t s = (cudaStream_t)stream;
+    const int64_t P = g->P;
+    // host thresholds: fp64 math rounded once to fp32 (the oracle rounds identically)
+    mvgs::AdcParamsHost h{};
+    h.tau_split = cfg->grad_threshold_split;
+    h.tau_clone = cfg->grad_threshold_clone;
+    h.ln_size = (float)std::log((double)cfg->size_threshold);
+    h.ln_split = (float)std::log((double)cfg->split_factor);
+    const double p = (double)cfg->prune_opacity * cfg->batch_views;
+    h.logit_prune = p >= 1.0 ? INFINITY : (float)std::log(p / (1.0 - p));
+    h.ln_prune_scale = cfg->prune_scale_max > 0.f ? (float)std::log((double)cfg->prune_scale_max) : INFINITY;
+    h.N = cfg->split_count;
+    h.mode = cfg->metric_mode;
+    const int64_t ntmp = scan_tmp_size((int)std::max<int64_t>(P, 1));
+    if (P + 1 > ctx->cap_adc_cnt || P > ctx->cap_adc_flags || ntmp > ctx->cap_adc_tmp || !ctx->d_adc_rep) {
+        CK(cudaDeviceSynchronize());
+        CK(grow(ctx->d_adc_cnt, ctx->cap_adc_cnt, P + 1));  // scan writes the total at [P]
+        CK(grow(ctx->d_adc_flags, ctx->cap_adc_flags, std::max<int64_t>(P, 1)));
+        CK(grow(ctx->d_adc_tmp, ctx->cap_adc_tmp, ntmp));
+        if (!ctx->d_adc_rep) {
+            CK(cudaMalloc(&ctx->d_adc_rep, 4 * sizeof(unsigned long long)));
+            CK(cudaMallocHost(&ctx->h_adc_rep, 4 * sizeof(long long)));
+        }
+    }
+    CK(cudaMemsetAsync(ctx->d_adc_rep, 0, 4 * sizeof(unsigned long long), s));
+    CK(launch_adc_decide(*g, *acc, h, ctx->d_adc_cnt, ctx->d_adc_flags, ctx->d_adc_rep, s));
+    if (P > 0) CK(scan_exclusive(ctx->d_adc_cnt, (int)P, (int*)(ctx->d_adc_rep + 3), ctx->d_adc_tmp, s));
+    CK(cudaMemcpyAsync(ctx->h_adc_rep, ctx->d_adc_rep, 4 * sizeof(long long), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    report->n_split = ctx->h_adc_rep[0];
+    report->n_clone = ctx->h_adc_rep[1];
+    report->n_pruned = ctx->h_adc_rep[2];
+    report->P_new = P > 0 ? (int64_t)(int)(ctx->h_adc_rep[3] & 0xffffffffLL) : 0;
+    if (report->P_new > out->capacity) {
+        char msg[128];
+        snprintf(msg, sizeof msg, "adc_step: %lld rows needed, capacity %lld", (long long)report->P_new,
+                 (long long)out->capacity);
+        return fail(ctx, MVGS_ERR_CAPACITY, msg);
+    }
+    CK(launch_adc_emit(*g, ctx->d_adc_flags, ctx->d_adc_cnt, noise, h, *out, origin, kind, s));
+    return MVGS_OK;
+}
+
+mvgs_status mvgs_adc_remap(mvgs_ctx* ctx, const float* src, float* dst, int64_t width, const int32_t* origin,
+                           const uint8_t* kind, int64_t P_new, void* stream) {
+    if (!ctx) return MVGS_ERR_INVALID;
+    if (width < 1 || P_new < 0 || (P_new > 0 && (!src || !dst || !origin || !kind)) || (P_new > 0 && src == dst))
+        return fail(ctx, MVGS_ERR_INVALID, "adc_remap: bad arguments");
+    CK(cudaSetDevice(ctx->device));
+    CK(launch_adc_remap(src, dst, width, origin, kind, P_new, (cudaStream_t)stream));
     return MVGS_OK;
 }
 

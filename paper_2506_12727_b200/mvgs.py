@@ -21,7 +21,7 @@ NG = 10
 SYMBOLS = ["mvgs_create", "mvgs_destroy", "mvgs_last_error", "mvgs_reserve", "mvgs_preprocess", "mvgs_render_fwd",
            "mvgs_render_bwd", "mvgs_adc_stats", "mvgs_query", "mvgs_export_lists", "mvgs_export_pairs",
            "mvgs_set_timing", "mvgs_stage_times", "mvgs_render_fwd_partial", "mvgs_render_bwd_partial",
-           "mvgs_render_fwd_depth", "mvgs_dssim3d"]
+           "mvgs_render_fwd_depth", "mvgs_dssim3d", "mvgs_adc_step", "mvgs_adc_remap"]
 PARTIAL_THREAD_EFFICIENT, PARTIAL_MASKED = 0, 1
 STAGE_NAMES = ["count", "scan_pairs", "project", "scan_buckets", "sort_pairs", "dup", "sort_entries", "render_fwd",
                "render_bwd", "gauss_bwd", "dssim"]
@@ -44,7 +44,27 @@ class Grads(C.Structure):
 
 
 class Adc(C.Structure):
-    _fields_ = [(k, C.c_void_p) for k in ("e1", "e2", "e_old", "vis", "e1_acc", "e2_acc", "denom_acc")]
+    _fields_ = [(k, C.c_void_p) for k in ("e1", "e2", "e_old", "vis", "e1_acc", "e2_acc", "denom_acc", "e_old_acc")]
+
+
+class AdcConfig(C.Structure):
+    _fields_ = [("grad_threshold_split", C.c_float), ("grad_threshold_clone", C.c_float),
+                ("size_threshold", C.c_float), ("split_factor", C.c_float), ("split_count", C.c_int32),
+                ("prune_opacity", C.c_float), ("prune_scale_max", C.c_float), ("metric_mode", C.c_int32),
+                ("batch_views", C.c_int32)]
+
+
+class AdcAccum(C.Structure):
+    _fields_ = [(k, C.c_void_p) for k in ("e1_acc", "e2_acc", "e_old_acc", "denom_acc")]
+
+
+class GaussiansOut(C.Structure):
+    _fields_ = [("capacity", C.c_int64), ("sh_stride", C.c_int32), ("means", C.c_void_p), ("log_scales", C.c_void_p),
+                ("quats", C.c_void_p), ("opacity_logits", C.c_void_p), ("sh", C.c_void_p)]
+
+
+class AdcReport(C.Structure):
+    _fields_ = [(k, C.c_int64) for k in ("n_split", "n_clone", "n_pruned", "P_new")]
 
 
 class Stats(C.Structure):
@@ -80,6 +100,8 @@ def _load():
     L.mvgs_render_fwd_partial.argtypes = [vp, vp, C.c_int32, C.c_int32, vp, vp, vp, vp]
     L.mvgs_render_bwd_partial.argtypes = [vp, vp, C.c_int32, C.c_int32, vp, vp, vp, vp]
     L.mvgs_dssim3d.argtypes = [vp, vp, C.c_int32, C.c_int32, C.c_int32, vp, vp, vp, vp, C.c_float, vp, vp, vp]
+    L.mvgs_adc_step.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]
+    L.mvgs_adc_remap.argtypes = [vp, vp, vp, i64, vp, vp, i64, vp]
     L.mvgs_stage_times.argtypes = [vp, C.POINTER(C.c_float), C.c_int]
     L.mvgs_stage_times.restype = C.c_int
     for n in SYMBOLS:
@@ -185,8 +207,48 @@ def render_bwd_partial(ctx, pix, S: int, mode: int, dL_drgb, T_final, n_contrib,
 
 def adc_stats(ctx, grads: dict, adc: dict, stream=None):
     gr = Grads(*[_ptr(grads[k]) for k in ("d_means", "d_log_scales", "d_quats", "d_opacity_logits", "d_sh")])
-    ad = Adc(*[_ptr(adc.get(k)) for k in ("e1", "e2", "e_old", "vis", "e1_acc", "e2_acc", "denom_acc")])
+    ad = Adc(*[_ptr(adc.get(k)) for k in ("e1", "e2", "e_old", "vis", "e1_acc", "e2_acc", "denom_acc", "e_old_acc")])
     _check(ctx, _lib.mvgs_adc_stats(ctx, C.byref(gr), C.byref(ad), _stream(stream)))
+
+
+ADC_DEFAULTS = dict(grad_threshold_split=2e-4, grad_threshold_clone=2e-4, size_threshold=0.01, split_factor=1.6,
+                    split_count=2, prune_opacity=0.005, prune_scale_max=0.0, metric_mode=1, batch_views=1)
+
+
+def alloc_gaussians(capacity: int, sh_stride: int, device) -> dict:
+    f = dict(dtype=torch.float32, device=device)
+    return dict(means=torch.empty((capacity, 3), **f), log_scales=torch.empty((capacity, 3), **f),
+                quats=torch.empty((capacity, 4), **f), opacity_logits=torch.empty((capacity,), **f),
+                sh=torch.empty((capacity, sh_stride, 3), **f))
+
+
+def adc_step(ctx, g: dict, acc: dict, noise, cfg: dict, out: dict, origin, kind, stream=None) -> dict:
+    """NEXT-3 (P:4): one ADC event.  `acc` holds e1_acc / e2_acc / e_old_acc /
+    denom_acc device tensors, `noise` [P, N, 3] standard normals, `out` arrays from
+    alloc_gaussians(capacity, ...).  Returns the report; raises MvgsError (status −2) when the
+    new count exceeds the capacity (the report is attached as .report)."""
+    c = dict(ADC_DEFAULTS)
+    c.update(cfg)
+    conf = AdcConfig(**c)
+    gs = gaussians_struct(g)
+    ac = AdcAccum(*[_ptr(acc.get(k)) for k in ("e1_acc", "e2_acc", "e_old_acc", "denom_acc")])
+    o = GaussiansOut(int(out["means"].shape[0]), int(out["sh"].shape[1]), _ptr(out["means"]), _ptr(out["log_scales"]),
+                     _ptr(out["quats"]), _ptr(out["opacity_logits"]), _ptr(out["sh"]))
+    rep = AdcReport()
+    st = _lib.mvgs_adc_step(ctx, C.byref(gs), C.byref(ac), _ptr(noise), C.byref(conf), C.byref(o), _ptr(origin),
+                            _ptr(kind), C.byref(rep), _stream(stream))
+    r = {k: getattr(rep, k) for k, _ in AdcReport._fields_}
+    if st != MVGS_OK:
+        e = MvgsError(st, _lib.mvgs_last_error(ctx).decode())
+        e.report = r
+        raise e
+    return r
+
+
+def adc_remap(ctx, src, dst, origin, kind, P_new: int, stream=None):
+    width = int(src[0].numel()) if src.dim() > 1 else 1
+    _check(ctx, _lib.mvgs_adc_remap(ctx, _ptr(src), _ptr(dst), width, _ptr(origin), _ptr(kind), int(P_new),
+                                    _stream(stream)))
 
 
 def query(ctx, raise_on_capacity: bool = True) -> dict:

@@ -378,20 +378,20 @@ def make_dssim_inputs(V: int, H: int, W: int, seed: int, bg_frac: float = 0.15):
 
 def make_adc_inputs(P: int, seed: int, N: int = 2, sh_degree: int = 3, iters: int = 100, B: int = 4):
     """Seeded inputs for the NEXT-3 ADC step (DESIGN.md §15 recipe): Gaussians from the
-    object360 generator's distributions (log-scales around ln 0.01, opacities U[0.002, 0.95]),
+    object360 generator's distributions (log-scales around ln 0.005, about half "large" at 0.01, opacities U[0.002, 0.95]),
     running accumulators of `iters` steps of B views — denom ~ integer U[0, B·iters] with 10%
-    never visible, per-visibility mean E1 log-normal around 2e-4, E2 = E1·U[0.3, 1],
+    never visible, per-visibility mean E1 log-normal around 1e-4 (≈16% above the 3DGS 2e-4), E2 = E1·U[0.3, 1],
     E_old = E2·U[0, 1] (the triangle-inequality order E1 ≥ E2 ≥ E_old) — and the split noise
     n ~ N(0, I) [P, N, 3]."""
     rng = np.random.Generator(np.random.PCG64(seed + 900))
     means = rng.normal(0, 1.0, (P, 3))
-    log_scales = np.log(0.01) + rng.normal(0, 0.8, (P, 3))
+    log_scales = np.log(0.005) + rng.normal(0, 0.8, (P, 3))
     quats = _unit_quats(rng, P)
     op = rng.uniform(0.002, 0.95, P)
     g = _finish(rng, means, log_scales, quats, np.log(op / (1 - op)), sh_degree)
     den = rng.integers(0, B * iters + 1, P).astype(np.float32)
     den[rng.uniform(0, 1, P) < 0.1] = 0
-    e1 = (den * np.exp(rng.normal(np.log(2e-4), 0.7, P))).astype(np.float32)
+    e1 = (den * np.exp(rng.normal(np.log(1e-4), 0.7, P))).astype(np.float32)
     e2 = (e1 * rng.uniform(0.3, 1.0, P)).astype(np.float32)
     eo = (e2 * rng.uniform(0.0, 1.0, P)).astype(np.float32)
     acc = dict(e1=e1, e2=e2, e_old=eo, denom=den)
