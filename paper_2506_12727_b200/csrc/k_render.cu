@@ -353,12 +353,228 @@ __global__ __launch_bounds__(256 / NPX) void k_render_bwd(Launch L, const float*
     count_evals(&L.counters64[1], &L.counters64[3], nev, nexp, sev);
 }
 
+// ---------------------------------------------------------------------------------------
+// Packed backward (default).  Same mapping as k_render_bwd<2> (128 threads, pixels at rows r
+// and r+2 of the thread's column), but the two pixels of a thread are the two lanes of FP32x2
+// registers: every per-pixel operation is one FFMA2/FMUL2/FADD2 for both pixels.  The body is
+// branch-free per pixel — a pixel that does not blend the entry (beyond its n_contrib, skip
+// bound, α < 1/255) gets α = 0 and a zero gradient weight, which leaves T and the colour
+// behind it unchanged exactly (÷(1 − 0), 0·c + 1·acc) — and only warp-uniform tests branch.
+// Decisions are the same as the scalar kernel's: the CA power with per-lane RN operations
+// (bit-identical to ca_power), the hardware exp with the CA fallback band.
+// The colour behind the current entry is updated eagerly after the entry (the same
+// expression the lazy form evaluates one entry later), so no previous-entry state is kept.
+struct BwdConsts {
+    float4 xy;   // (x, x, y, y)
+    float4 ab;   // (A, A, B, B)
+    float4 cnb;  // (C, C, −B, −B)
+    float4 os;   // (o, o, skip bound, skip bound)
+    float4 rg;   // (r, r, g, g)
+    float2 bb;   // (b, b)
+};
+
+__device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
+__device__ __forceinline__ float ex2_approx(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ float sqrt_approx(float x) {
+    float y;
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ float rcp_approx(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+// G and o·G of one lane: hardware exp, CA exp when o·G is within 1e-5 (relative) of a threshold
+__device__ __forceinline__ void bwd_exp(float power, float o, float& G, float& oG) {
+    G = ex2_approx(power * 1.4426950408889634f);
+    oG = o * G;
+    if (fabsf(oG - ALPHA_MIN) < 1e-5f * ALPHA_MIN || fabsf(oG - ALPHA_MAX) < 1e-5f * ALPHA_MAX) {
+        G = ca_exp_core(power);
+        oG = FMUL(o, G);
+    }
+}
+
+__global__ __launch_bounds__(128) void k_render_bwd_p(Launch L, const float* __restrict__ dL_drgb,
+                                                      const float* __restrict__ in_T,
+                                                      const int32_t* __restrict__ in_n) {
+    constexpr int NT = 128, NW = 4, RB = 128;
+    __shared__ BwdConsts sc[RB];
+    __shared__ uint32_t sq[RB];
+    __shared__ __align__(16) float sacc[NW][RB * NG];
+    __shared__ int smax;
+    __shared__ unsigned sev[2];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int bucket = blockIdx.x;
+    const int v = bucket / L.T, tile = bucket - v * L.T;
+    const int ty = tile / L.TX, tx = tile - ty * L.TX;
+    const int x = tx * TILE + (lane & 15);
+    const int y0 = ty * TILE + 4 * warp + (lane >> 4);
+    const int start = L.bucket_off[bucket], end = L.bucket_off[bucket + 1];
+    if (end > L.cap_entries) return;
+    const int64_t HW = (int64_t)L.H * L.W;
+    float dL[2][3], Tfin[2];
+    int last[2];
+    unsigned nev = 0;
+#pragma unroll
+    for (int p = 0; p < 2; p++) {
+        const int y = y0 + 2 * p;
+        dL[p][0] = dL[p][1] = dL[p][2] = 0.f;
+        Tfin[p] = 1.f;
+        last[p] = 0;
+        if (x < L.W && y < L.H) {
+            const int64_t pix = (int64_t)y * L.W + x;
+            dL[p][0] = dL_drgb[(3 * (int64_t)v + 0) * HW + pix];
+            dL[p][1] = dL_drgb[(3 * (int64_t)v + 1) * HW + pix];
+            dL[p][2] = dL_drgb[(3 * (int64_t)v + 2) * HW + pix];
+            Tfin[p] = in_T[v * HW + pix];
+            last[p] = in_n[v * HW + pix];
+        }
+        nev += (unsigned)last[p];
+    }
+    const float2 dLr = f2(dL[0][0], dL[1][0]), dLg = f2(dL[0][1], dL[1][1]), dLb = f2(dL[0][2], dL[1][2]);
+    // −T_final·(∂L/∂C · bg): the background term of ∂L/∂α, scaled by 1/(1 − α) per entry
+    const float2 nTbg = f2(-Tfin[0] * (L.bg[0] * dL[0][0] + L.bg[1] * dL[0][1] + L.bg[2] * dL[0][2]),
+                           -Tfin[1] * (L.bg[0] * dL[1][0] + L.bg[1] * dL[1][1] + L.bg[2] * dL[1][2]));
+    float2 T = f2(Tfin[0], Tfin[1]);
+    float2 accr = f2(0.f, 0.f), accg = accr, accb = accr;  // colour behind the current entry
+    const int mylast = max(last[0], last[1]);
+    if (threadIdx.x == 0) {
+        smax = 0;
+        sev[0] = sev[1] = 0;
+    }
+    __syncthreads();
+    unsigned nexp = 0;
+    if (mylast > 0) atomicMax(&smax, mylast);
+    __syncthreads();
+    const int maxlast = smax;
+    const int wmax = __reduce_max_sync(FULLR, mylast);
+    const int my_id = reduce_id(lane);
+    const bool owner = (__ffs(__match_any_sync(FULLR, my_id)) - 1) == lane;
+    const float hw = 0.5f * (float)L.W, hh = 0.5f * (float)L.H;
+    // per-value scale applied by the owner after the reduction (see the V terms below)
+    const float oscale = my_id == 0 ? -hw : my_id == 1 ? -hh : (my_id == 3 || my_id == 5) ? -0.5f : my_id == 4 ? -1.f : 1.f;
+    float* wacc = sacc[warp];
+    const float2 nfx = f2(-(float)x, -(float)x), nfy = f2(-(float)y0, -(float)(y0 + 2));
+    const float2 one = f2(1.f, 1.f), mone = f2(-1.f, -1.f), mhalf = f2(-0.5f, -0.5f);
+    const float2 hw2 = f2(hw * hw, hw * hw), hh2 = f2(hh * hh, hh * hh);
+    for (int b_end = maxlast; b_end > 0; b_end -= RB) {
+        const int b0 = max(0, b_end - RB);
+        const int cnt = b_end - b0;
+        __syncthreads();
+        for (int t = threadIdx.x; t < cnt; t += NT) {
+            const uint32_t q = L.sorted[start + b0 + t];
+            sq[t] = q;
+            const float4* r = L.rec + 3 * (int64_t)q;
+            const float4 r0 = r[0], r1 = r[1], r2 = r[2];
+            BwdConsts k;
+            k.xy = make_float4(r0.x, r0.x, r0.y, r0.y);
+            k.ab = make_float4(r0.z, r0.z, r0.w, r0.w);
+            k.cnb = make_float4(r1.x, r1.x, -r0.w, -r0.w);
+            const float sb = skip_power(r1.y);
+            k.os = make_float4(r1.y, r1.y, sb, sb);
+            k.rg = make_float4(r1.z, r1.z, r1.w, r1.w);
+            k.bb = f2(r2.x, r2.x);
+            sc[t] = k;
+        }
+        {
+            float4* w4 = reinterpret_cast<float4*>(wacc);
+            for (int i = lane; i < RB * NG / 4; i += 32) w4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        __syncthreads();
+        for (int jj = min(cnt, wmax - b0) - 1; jj >= 0; jj--) {
+            const int j = b0 + jj;
+            const float4 xy = sc[jj].xy, ab = sc[jj].ab, cnb = sc[jj].cnb, os = sc[jj].os;
+            const float2 dx = __fadd2_rn(f2(xy.x, xy.y), nfx);
+            const float2 dy = __fadd2_rn(f2(xy.z, xy.w), nfy);
+            // ca_power per lane: FMA(−0.5, FMA(A·dx, dx, (C·dy)·dy), −(B·dx)·dy)
+            const float2 Adx = __fmul2_rn(f2(ab.x, ab.y), dx);
+            const float2 CdyDy = __fmul2_rn(__fmul2_rn(f2(cnb.x, cnb.y), dy), dy);
+            const float2 inner = __ffma2_rn(Adx, dx, CdyDy);
+            const float2 nBdxdy = __fmul2_rn(__fmul2_rn(f2(cnb.z, cnb.w), dx), dy);
+            const float2 power = __ffma2_rn(mhalf, inner, nBdxdy);
+            const bool in0 = j < last[0] && !(power.x > 0.f) && !(power.x < os.z);
+            const bool in1 = j < last[1] && !(power.y > 0.f) && !(power.y < os.z);
+            if (!__any_sync(FULLR, in0 || in1)) continue;
+            nexp += (unsigned)in0 + (unsigned)in1;
+            float G0, G1, oG0, oG1;
+            bwd_exp(power.x, os.x, G0, oG0);
+            bwd_exp(power.y, os.y, G1, oG1);
+            const float al0 = fminf(ALPHA_MAX, oG0), al1 = fminf(ALPHA_MAX, oG1);
+            const bool v0 = in0 && !(al0 < ALPHA_MIN), v1 = in1 && !(al1 < ALPHA_MIN);
+            if (!__any_sync(FULLR, v0 || v1)) continue;
+            const float2 alpha = f2(v0 ? al0 : 0.f, v1 ? al1 : 0.f);
+            // o·G for ∂/∂G and ∂/∂o; zero where clamped (α = 0.99 has zero gradient, R11)
+            const float2 Gc = f2(v0 && !(oG0 > ALPHA_MAX) ? G0 : 0.f, v1 && !(oG1 > ALPHA_MAX) ? G1 : 0.f);
+            const float2 om = __ffma2_rn(alpha, mone, one);
+            const float2 inv = f2(rcp_approx(om.x), rcp_approx(om.y));
+            T = __fmul2_rn(T, inv);
+            const float2 w = __fmul2_rn(alpha, T);
+            const float4 rg = sc[jj].rg;
+            const float2 bb = sc[jj].bb;
+            const float2 cr = f2(rg.x, rg.y), cg = f2(rg.z, rg.w);
+            float2 dLda = __fmul2_rn(__ffma2_rn(accr, mone, cr), dLr);
+            dLda = __ffma2_rn(__ffma2_rn(accg, mone, cg), dLg, dLda);
+            dLda = __ffma2_rn(__ffma2_rn(accb, mone, bb), dLb, dLda);
+            dLda = __ffma2_rn(dLda, T, __fmul2_rn(nTbg, inv));
+            // colour behind the next (nearer) entry: α·c + (1 − α)·acc
+            accr = __ffma2_rn(alpha, cr, __fmul2_rn(om, accr));
+            accg = __ffma2_rn(alpha, cg, __fmul2_rn(om, accg));
+            accb = __ffma2_rn(alpha, bb, __fmul2_rn(om, accb));
+            const float2 dLdo = __fmul2_rn(Gc, dLda);
+            const float2 dLdpw = __fmul2_rn(__fmul2_rn(Gc, f2(os.x, os.y)), dLda);
+            const float2 d = __fmul2_rn(dLdpw, dx), e = __fmul2_rn(dLdpw, dy);
+            // ∂L/∂p' (pixels → NDC): gx = −hw·(A d + B e), gy = −hh·(C e + B d)
+            const float2 gxr = __ffma2_rn(f2(ab.x, ab.y), d, __fmul2_rn(f2(ab.z, ab.w), e));
+            const float2 gyr = __ffma2_rn(f2(cnb.x, cnb.y), e, __fmul2_rn(f2(ab.z, ab.w), d));
+            const float2 n2 = __ffma2_rn(__fmul2_rn(gxr, gxr), hw2, __fmul2_rn(__fmul2_rn(gyr, gyr), hh2));
+            float val[NG];
+            val[0] = gxr.x + gxr.y;
+            val[1] = gyr.x + gyr.y;
+            val[2] = sqrt_approx(n2.x) + sqrt_approx(n2.y);  // ‖∇_{p_i}L‖ per pixel, then add
+            const float2 dd = __fmul2_rn(d, dx), de = __fmul2_rn(d, dy), ee = __fmul2_rn(e, dy);
+            val[3] = dd.x + dd.y;
+            val[4] = de.x + de.y;
+            val[5] = ee.x + ee.y;
+            val[6] = dLdo.x + dLdo.y;
+            const float2 wr = __fmul2_rn(w, dLr), wg = __fmul2_rn(w, dLg), wb = __fmul2_rn(w, dLb);
+            val[7] = wr.x + wr.y;
+            val[8] = wg.x + wg.y;
+            val[9] = wb.x + wb.y;
+            const float sum = warp_transpose_reduce10(val, lane);
+            if (owner) wacc[jj * NG + my_id] = sum * oscale;
+        }
+        __syncthreads();
+        for (int i = threadIdx.x; i < cnt * NG; i += NT) {
+            float s = 0.f;
+#pragma unroll
+            for (int w = 0; w < NW; w++) s += sacc[w][i];
+            if (s != 0.f) {
+                const int jj = i / NG, k = i - jj * NG;
+                atomicAdd(&L.pgrad[(int64_t)sq[jj] * PG_STRIDE + k], s);
+            }
+        }
+    }
+    count_evals(&L.counters64[1], &L.counters64[3], nev, nexp, sev);
+}
+
+#ifndef MVGS_BWD_PACKED
+#define MVGS_BWD_PACKED 1
+#endif
+
 #ifndef MVGS_BWD_NPX
 #define MVGS_BWD_NPX 2
 #endif
 
 cudaError_t launch_render_bwd(const Launch& L, const float* dL, const float* Tf, const int32_t* nc, cudaStream_t s) {
-    k_render_bwd<MVGS_BWD_NPX><<<L.V * L.T, 256 / MVGS_BWD_NPX, 0, s>>>(L, dL, Tf, nc);
+    if (MVGS_BWD_PACKED)
+        k_render_bwd_p<<<L.V * L.T, 128, 0, s>>>(L, dL, Tf, nc);
+    else
+        k_render_bwd<MVGS_BWD_NPX><<<L.V * L.T, 256 / MVGS_BWD_NPX, 0, s>>>(L, dL, Tf, nc);
     return cudaGetLastError();
 }
 
