@@ -151,11 +151,151 @@ __global__ __launch_bounds__(RT) void k_render_fwd(Launch L, float* __restrict__
     }
 }
 
+// ---------------------------------------------------------------------------------------
+// Packed forward (default): the thread's two pixels are the lanes of FP32x2 registers; every
+// CA operation (power, canonical exp, α, T·(1 − α)) is the per-lane RN operation of the
+// scalar kernel, so decisions, T_final and n_contrib are bit-identical to k_render_fwd.
+// A lane that does not blend the entry gets weight 0 and keeps its T.
+struct FwdConsts {
+    float4 xy;   // (x, x, y, y)
+    float4 ab;   // (A, A, −B, −B)
+    float4 cs;   // (C, C, skip bound, skip bound)
+    float4 orr;  // (o, o, r, r)
+    float4 gb;   // (g, g, b, b)
+    float2 dd;   // (depth, depth)
+};
+
+__device__ __forceinline__ float2 ff2(float a, float b) { return make_float2(a, b); }
+
+// ca_exp_core per lane, packed (same RN / FMA sequence)
+__device__ __forceinline__ float2 ca_exp_core2(float2 x) {
+    const float2 t = __fmul2_rn(x, ff2(1.44269504f, 1.44269504f));
+    const float2 n = ff2(rintf(t.x), rintf(t.y));
+    float2 r = __ffma2_rn(n, ff2(-0.693145751953125f, -0.693145751953125f), x);
+    r = __ffma2_rn(n, ff2(-1.428606765330187e-6f, -1.428606765330187e-6f), r);
+    const float c6 = (float)(1.0 / 720.0), c5 = (float)(1.0 / 120.0), c4 = (float)(1.0 / 24.0),
+                c3 = (float)(1.0 / 6.0);
+    float2 p = __ffma2_rn(ff2(c6, c6), r, ff2(c5, c5));
+    p = __ffma2_rn(p, r, ff2(c4, c4));
+    p = __ffma2_rn(p, r, ff2(c3, c3));
+    p = __ffma2_rn(p, r, ff2(0.5f, 0.5f));
+    p = __ffma2_rn(p, r, ff2(1.f, 1.f));
+    p = __ffma2_rn(p, r, ff2(1.f, 1.f));
+    const float2 sc = ff2(__int_as_float((__float2int_rn(n.x) + 127) << 23),
+                          __int_as_float((__float2int_rn(n.y) + 127) << 23));
+    return __fmul2_rn(p, sc);
+}
+
+template <bool DEPTH>
+__global__ __launch_bounds__(RT) void k_render_fwd_p(Launch L, float* __restrict__ out_rgb,
+                                                     float* __restrict__ out_T, int32_t* __restrict__ out_n,
+                                                     float* __restrict__ out_D) {
+    __shared__ FwdConsts sf[RT];
+    __shared__ unsigned sev[2];
+    const int bucket = blockIdx.x;
+    const int v = bucket / L.T, tile = bucket - v * L.T;
+    const int ty = tile / L.TX, tx = tile - ty * L.TX;
+    int x, y[2];
+    pixel_pair(tx, ty, x, y[0], y[1]);
+    const int start = L.bucket_off[bucket], end = L.bucket_off[bucket + 1];
+    const float2 nfx = ff2(-(float)x, -(float)x), nfy = ff2(-(float)y[0], -(float)y[1]);
+    const float2 one = ff2(1.f, 1.f), mone = ff2(-1.f, -1.f), mhalf = ff2(-0.5f, -0.5f);
+    float2 T = one, C0 = ff2(0.f, 0.f), C1 = C0, C2 = C0, D = C0;
+    int last0 = 0, last1 = 0;
+    bool done0 = !(x < L.W && y[0] < L.H), done1 = !(x < L.W && y[1] < L.H);
+    unsigned nev = 0, nexp = 0;
+    if (threadIdx.x == 0) sev[0] = sev[1] = 0;
+    __syncthreads();
+    if (end <= L.cap_entries) {
+        for (int b0 = start; b0 < end; b0 += RT) {
+            if (__syncthreads_count(done0 && done1) == RT) break;
+            const int idx = b0 + threadIdx.x;
+            if (idx < end) {
+                const float4* r = L.rec + 3 * (int64_t)L.sorted[idx];
+                const float4 r0 = r[0], r1 = r[1], r2 = r[2];
+                FwdConsts k;
+                k.xy = make_float4(r0.x, r0.x, r0.y, r0.y);
+                k.ab = make_float4(r0.z, r0.z, -r0.w, -r0.w);
+                const float sb = skip_power(r1.y);
+                k.cs = make_float4(r1.x, r1.x, sb, sb);
+                k.orr = make_float4(r1.y, r1.y, r1.z, r1.z);
+                k.gb = make_float4(r1.w, r1.w, r2.x, r2.x);
+                k.dd = ff2(r2.y, r2.y);
+                sf[threadIdx.x] = k;
+            }
+            __syncthreads();
+            const int cnt = min(RT, end - b0);
+            for (int j = 0; j < cnt && !(done0 && done1); j++) {
+                nev += (unsigned)!done0 + (unsigned)!done1;
+                const float4 xy = sf[j].xy, ab = sf[j].ab, cs = sf[j].cs;
+                const float2 dx = __fadd2_rn(ff2(xy.x, xy.y), nfx);
+                const float2 dy = __fadd2_rn(ff2(xy.z, xy.w), nfy);
+                const float2 Adx = __fmul2_rn(ff2(ab.x, ab.y), dx);
+                const float2 CdyDy = __fmul2_rn(__fmul2_rn(ff2(cs.x, cs.y), dy), dy);
+                const float2 inner = __ffma2_rn(Adx, dx, CdyDy);
+                const float2 nBdxdy = __fmul2_rn(__fmul2_rn(ff2(ab.z, ab.w), dx), dy);
+                const float2 power = __ffma2_rn(mhalf, inner, nBdxdy);
+                const bool in0 = !done0 && !(power.x > 0.f) && !(power.x < cs.z);
+                const bool in1 = !done1 && !(power.y > 0.f) && !(power.y < cs.z);
+                if (!(in0 || in1)) continue;
+                nexp += (unsigned)in0 + (unsigned)in1;
+                const float4 orr = sf[j].orr;
+                const float2 G = ca_exp_core2(power);
+                const float2 oG = __fmul2_rn(ff2(orr.x, orr.y), G);
+                const float2 alpha = ff2(fminf(ALPHA_MAX, oG.x), fminf(ALPHA_MAX, oG.y));
+                const bool ok0 = in0 && !(alpha.x < ALPHA_MIN), ok1 = in1 && !(alpha.y < ALPHA_MIN);
+                if (!(ok0 || ok1)) continue;
+                const float2 Tn = __fmul2_rn(T, __ffma2_rn(alpha, mone, one));  // T·(1 − α), CA
+                const bool term0 = ok0 && Tn.x < T_EPS, term1 = ok1 && Tn.y < T_EPS;
+                const bool bl0 = ok0 && !term0, bl1 = ok1 && !term1;
+                done0 |= term0;
+                done1 |= term1;
+                const float2 w = __fmul2_rn(ff2(bl0 ? alpha.x : 0.f, bl1 ? alpha.y : 0.f), T);
+                const float4 gb = sf[j].gb;
+                C0 = __ffma2_rn(ff2(orr.z, orr.w), w, C0);
+                C1 = __ffma2_rn(ff2(gb.x, gb.y), w, C1);
+                C2 = __ffma2_rn(ff2(gb.z, gb.w), w, C2);
+                if (DEPTH) D = __ffma2_rn(sf[j].dd, w, D);
+                T = ff2(bl0 ? Tn.x : T.x, bl1 ? Tn.y : T.y);
+                const int jn = b0 - start + j + 1;
+                last0 = bl0 ? jn : last0;
+                last1 = bl1 ? jn : last1;
+            }
+        }
+    }
+    count_evals(&L.counters64[0], &L.counters64[2], nev, nexp, sev);
+    const int64_t HW = (int64_t)L.H * L.W;
+    const float Cs[2][3] = {{C0.x, C1.x, C2.x}, {C0.y, C1.y, C2.y}};
+    const float Ts[2] = {T.x, T.y}, Ds[2] = {D.x, D.y};
+    const int ls[2] = {last0, last1};
+#pragma unroll
+    for (int p = 0; p < 2; p++) {
+        if (!(x < L.W && y[p] < L.H)) continue;
+        const int64_t pix = (int64_t)y[p] * L.W + x;
+        out_rgb[(3 * (int64_t)v + 0) * HW + pix] = Cs[p][0] + Ts[p] * L.bg[0];
+        out_rgb[(3 * (int64_t)v + 1) * HW + pix] = Cs[p][1] + Ts[p] * L.bg[1];
+        out_rgb[(3 * (int64_t)v + 2) * HW + pix] = Cs[p][2] + Ts[p] * L.bg[2];
+        out_T[v * HW + pix] = Ts[p];
+        out_n[v * HW + pix] = ls[p];
+        if (DEPTH) out_D[v * HW + pix] = Ds[p];
+    }
+}
+
+#ifndef MVGS_FWD_PACKED
+#define MVGS_FWD_PACKED 1
+#endif
+
 cudaError_t launch_render_fwd(const Launch& L, float* rgb, float* Tf, int32_t* nc, float* depth, cudaStream_t s) {
-    if (depth)
+    if (MVGS_FWD_PACKED) {
+        if (depth)
+            k_render_fwd_p<true><<<L.V * L.T, RT, 0, s>>>(L, rgb, Tf, nc, depth);
+        else
+            k_render_fwd_p<false><<<L.V * L.T, RT, 0, s>>>(L, rgb, Tf, nc, nullptr);
+    } else if (depth) {
         k_render_fwd<true><<<L.V * L.T, RT, 0, s>>>(L, rgb, Tf, nc, depth);
-    else
+    } else {
         k_render_fwd<false><<<L.V * L.T, RT, 0, s>>>(L, rgb, Tf, nc, nullptr);
+    }
     return cudaGetLastError();
 }
 
