@@ -95,19 +95,23 @@ __device__ __forceinline__ void fast_project(const mvgs_camera& cam, float mx, f
 }
 
 // SH coefficients and their gradient live in shared memory, one padded row per
-// Gaussian (odd stride ⇒ conflict-free when each thread walks its own row);
-// the block's rows are loaded and stored with coalesced accesses.
+// Gaussian, walked by its thread with 16-byte accesses: the row stride is an odd
+// number of float4 ⇒ every LDS.128/STS.128 of a warp is 4 conflict-free wavefronts.
+// The block's rows are loaded (cp.async, 16 B when the global rows allow) and stored
+// with coalesced accesses.
 template <int D>
 struct ShRows {
     static constexpr int NK = (D + 1) * (D + 1);
     static constexpr int NS = NK * 3;
-    static constexpr int STRIDE = NS | 1;
+    static constexpr int NS4 = (NS + 3) / 4;  // float4 per row
+    static constexpr int STRIDE = 4 * (NS4 | 1);
 };
 
 template <int D>
 __global__ __launch_bounds__(BLK, 2) void k_gauss_bwd(Launch L, mvgs_grads gr, mvgs_adc adc) {
     constexpr int NK = ShRows<D>::NK, NS = ShRows<D>::NS, SS = ShRows<D>::STRIDE;
-    extern __shared__ float smem_sh[];
+    extern __shared__ float4 smem_sh4[];  // 16-byte aligned base
+    float* smem_sh = reinterpret_cast<float*>(smem_sh4);
     float* sh_s = smem_sh;              // [BLK][SS]
     float* dsh_s = smem_sh + BLK * SS;  // [BLK][SS]
     __shared__ int wc[BLK / 32][32];
@@ -121,13 +125,21 @@ __global__ __launch_bounds__(BLK, 2) void k_gauss_bwd(Launch L, mvgs_grads gr, m
         const int nb = (int)min((int64_t)BLK, L.P - g0);
         const float* src = L.sh + g0 * (int64_t)L.sh_stride * 3;
         const int rowlen = L.sh_stride * 3;
-        const int n = nb * NS;
-        for (int i = threadIdx.x; i < n; i += BLK) {
-            const int r = i / NS, k = i - r * NS;  // NS constexpr: mul-shift
-            cp_async4(&sh_s[r * SS + k], src + (int64_t)r * rowlen + k);
-            dsh_s[r * SS + k] = 0.f;
+        if ((rowlen & 3) == 0 && (NS & 3) == 0 && ((uintptr_t)src & 15) == 0) {
+            constexpr int NS4 = NS / 4;
+            for (int i = threadIdx.x; i < nb * NS4; i += BLK) {
+                const int r = i / NS4, k = 4 * (i - r * NS4);
+                cp_async16(&sh_s[r * SS + k], src + (int64_t)r * rowlen + k);
+            }
+        } else {
+            for (int i = threadIdx.x; i < nb * NS; i += BLK) {
+                const int r = i / NS, k = i - r * NS;  // NS constexpr: mul-shift
+                cp_async4(&sh_s[r * SS + k], src + (int64_t)r * rowlen + k);
+            }
         }
         cp_async_commit();
+        float4* z4 = reinterpret_cast<float4*>(dsh_s);
+        for (int i = threadIdx.x; i < BLK * SS / 4; i += BLK) z4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
     const float* sh = sh_s + threadIdx.x * SS;
     float* dsh = dsh_s + threadIdx.x * SS;
@@ -156,6 +168,15 @@ __global__ __launch_bounds__(BLK, 2) void k_gauss_bwd(Launch L, mvgs_grads gr, m
         }
         if (threadIdx.x < nv) sboff[threadIdx.x] = L.blk_off[(int64_t)(v0 + threadIdx.x) * L.NB + blockIdx.x];
         __syncthreads();
+        if (threadIdx.x < nv) {  // exclusive prefix over warps, per view: wc[w][k] ← Σ_{w' < w}
+            int run = 0;
+            for (int w = 0; w < BLK / 32; w++) {
+                const int c = wc[w][threadIdx.x];
+                wc[w][threadIdx.x] = run;
+                run += c;
+            }
+        }
+        __syncthreads();
         for (int k0 = 0; k0 < nv; k0 += 4) {
             // issue the loads of up to 4 views first (memory-level parallelism), then the math
             uint32_t fl[4];
@@ -169,11 +190,10 @@ __global__ __launch_bounds__(BLK, 2) void k_gauss_bwd(Launch L, mvgs_grads gr, m
                 const bool zvis = valid && ca_depth(c, mx, my, mz) > c.znear;
                 const unsigned bal = __ballot_sync(FULLG, zvis);
                 if (!zvis) continue;
-                int pre = 0;
-                for (int w = 0; w < warp; w++) pre += wc[w][k];
-                const int64_t pair = (int64_t)sboff[k] + pre + __popc(bal & lt);
+                const int64_t pair = (int64_t)sboff[k] + wc[warp][k] + __popc(bal & lt);
                 if (pair >= L.cap_pairs) continue;
-                // flags and gradient slot loaded together (the slot is ignored for inert pairs)
+                // flags and gradient slot loaded together (the slot is ignored for inert pairs;
+                // loading it only after the flag was measured slower: one more dependent trip)
                 fl[u] = L.pflag[pair];
                 const float4* pgp = reinterpret_cast<const float4*>(L.pgrad + pair * PG_STRIDE);
                 pga[u] = pgp[0];
@@ -272,9 +292,23 @@ __global__ __launch_bounds__(BLK, 2) void k_gauss_bwd(Launch L, mvgs_grads gr, m
             float x = mx - cpx, y = my - cpy, z = mz - cpz;
             const float dn = sqrtf(x * x + y * y + z * z), idn = 1.f / dn;
             x *= idn; y *= idn; z *= idn;
-            float wk[NK];
+            float wk[NK];  // Σ_c sh[k][c]·∂L/∂rgb_c, read as float4 chunks of the row
 #pragma unroll
-            for (int kk = 0; kk < NK; kk++) wk[kk] = sh[3 * kk] * dr0 + sh[3 * kk + 1] * dr1 + sh[3 * kk + 2] * dr2;
+            for (int kk = 0; kk < NK; kk++) wk[kk] = 0.f;
+            {
+                const float drc[3] = {dr0, dr1, dr2};
+                const float4* sh4 = reinterpret_cast<const float4*>(sh);
+#pragma unroll
+                for (int i4 = 0; i4 < ShRows<D>::NS4; i4++) {
+                    const float4 q = sh4[i4];
+                    const float qe[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+                    for (int e = 0; e < 4; e++) {
+                        const int f = 4 * i4 + e;
+                        if (f < NS) wk[f / 3] += qe[e] * drc[f % 3];
+                    }
+                }
+            }
             float Y[NK];
             Y[0] = 0.28209479177387814f;
             float ddx = 0.f, ddy = 0.f, ddz = 0.f;
@@ -314,11 +348,20 @@ __global__ __launch_bounds__(BLK, 2) void k_gauss_bwd(Launch L, mvgs_grads gr, m
                          + g_SH3[5] * (xx - yy) * wk[14];
                 }
             }
+            {
+                const float drc[3] = {dr0, dr1, dr2};
+                float4* dsh4 = reinterpret_cast<float4*>(dsh);
 #pragma unroll
-            for (int kk = 0; kk < NK; kk++) {
-                dsh[3 * kk] += Y[kk] * dr0;
-                dsh[3 * kk + 1] += Y[kk] * dr1;
-                dsh[3 * kk + 2] += Y[kk] * dr2;
+                for (int i4 = 0; i4 < ShRows<D>::NS4; i4++) {
+                    float4 q = dsh4[i4];
+                    float* qe = reinterpret_cast<float*>(&q);
+#pragma unroll
+                    for (int e = 0; e < 4; e++) {
+                        const int f = 4 * i4 + e;
+                        if (f < NS) qe[e] += Y[f / 3] * drc[f % 3];
+                    }
+                    dsh4[i4] = q;
+                }
             }
             const float dd = x * ddx + y * ddy + z * ddz;
             dmx += (ddx - x * dd) * idn;
@@ -337,9 +380,14 @@ __global__ __launch_bounds__(BLK, 2) void k_gauss_bwd(Launch L, mvgs_grads gr, m
         const int nb = (int)min((int64_t)BLK, L.P - g0);
         float* dst = gr.d_sh + g0 * (int64_t)L.sh_stride * 3;
         const int rowlen = L.sh_stride * 3;
-        for (int i = threadIdx.x; i < nb * rowlen; i += BLK) {
-            const int r = i / rowlen, k = i - r * rowlen;
-            dst[i] = k < NS ? dsh_s[r * SS + k] : 0.f;
+        if (rowlen == NS) {  // rows hold exactly the active coefficients: constant divisor
+            for (int i = threadIdx.x; i < nb * NS; i += BLK) {
+                const int r = i / NS, k = i - r * NS;
+                dst[i] = dsh_s[r * SS + k];
+            }
+        } else {
+            for (int r = warp; r < nb; r += BLK / 32)
+                for (int k = lane; k < rowlen; k += 32) dst[(int64_t)r * rowlen + k] = k < NS ? dsh_s[r * SS + k] : 0.f;
         }
     }
     if (!valid) return;
