@@ -91,6 +91,9 @@ struct mvgs_ctx {
     int64_t cap_dssim_coef = 0;
     double* d_dssim_part = nullptr;  // per-block SSIM sums
     int64_t cap_dssim_part = 0;
+    unsigned long long* d_ent64 = nullptr;  // [cap_entries] bucket-sort keys (depth << 32 | pair)
+    int* d_bcur = nullptr;                  // [V*T] bucket cursors
+    int64_t cap_bcur = 0;
     int* d_adc_cnt = nullptr;        // NEXT-3 per-Gaussian emitted-row counts → offsets
     int64_t cap_adc_cnt = 0;
     uint8_t* d_adc_flags = nullptr;
@@ -134,6 +137,16 @@ cudaError_t launch_adc_remap(const float* src, float* dst, int64_t width, const 
 cudaError_t launch_dssim3d(const mvgs_camera* h_cams, int V, int H, int W, const float* img, const float* tgt,
                            const float* depth, const float* Tf, float sigma_px, float* loss, float* grad, float* coef,
                            double* partial, cudaStream_t s);
+#ifndef MVGS_SORT_BUCKET
+// 1: S3–S5 as count / scatter / per-bucket bitonic sort (k_bucket.cu) — exact, but measured
+// 2.9 ms vs 1.26 ms for the pair sort + dup + entry sort path at garden scale (scattered 8-B
+// writes, log² shared-memory traffic); kept as an experiment, off by default.
+#define MVGS_SORT_BUCKET 0
+#endif
+cudaError_t launch_bucket_count(const Launch& L, int* gcnt, cudaStream_t s);
+cudaError_t launch_bucket_scatter(const Launch& L, int* gcur, unsigned long long* ent, cudaStream_t s);
+cudaError_t launch_bucket_sort(const Launch& L, unsigned long long* ent, uint32_t* sorted, cudaStream_t s);
+cudaError_t launch_max_bucket(const Launch& L, cudaStream_t s);
 cudaError_t launch_render_bwd(const Launch& L, const float* dL, const float* Tf, const int32_t* nc, cudaStream_t s);
 cudaError_t launch_render_fwd_partial(const Launch& L, const int32_t* pix, int S, int mode, float* rgb, float* Tf,
                                       int32_t* nc, cudaStream_t s);

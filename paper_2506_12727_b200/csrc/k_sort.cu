@@ -566,3 +566,10 @@ cudaError_t launch_sort_entries(const Launch& L, uint32_t** sorted_vals, cudaStr
 }
 
 }  // namespace mvgs
+
+namespace mvgs {
+cudaError_t launch_max_bucket(const Launch& L, cudaStream_t s) {
+    k_max_bucket<<<64, 256, 0, s>>>(L);
+    return cudaGetLastError();
+}
+}  // namespace mvgs

@@ -110,10 +110,12 @@ cudaError_t alloc_sort_scratch(mvgs_ctx* c) {
 }
 
 cudaError_t alloc_entries(mvgs_ctx* c, int64_t n) {
-    cudaFree(c->d_key); cudaFree(c->d_val); cudaFree(c->d_key2); cudaFree(c->d_val2);
+    cudaFree(c->d_key); cudaFree(c->d_val); cudaFree(c->d_key2); cudaFree(c->d_val2); cudaFree(c->d_ent64);
     c->d_key = c->d_val = c->d_key2 = c->d_val2 = nullptr;
+    c->d_ent64 = nullptr;
     c->cap_entries = 0;
     cudaError_t e;
+    if (MVGS_SORT_BUCKET && (e = cudaMalloc(&c->d_ent64, 8 * n)) != cudaSuccess) return e;
     if ((e = cudaMalloc(&c->d_key, 4 * n)) != cudaSuccess) return e;
     if ((e = cudaMalloc(&c->d_val, 4 * n)) != cudaSuccess) return e;
     if ((e = cudaMalloc(&c->d_key2, 4 * n)) != cudaSuccess) return e;
@@ -233,6 +235,7 @@ void mvgs_destroy(mvgs_ctx* ctx) {
     cudaFree(ctx->d_pflag);
     cudaFree(ctx->d_counters); cudaFree(ctx->d_counters64); cudaFree(ctx->d_scan);
     cudaFree(ctx->d_dssim_coef); cudaFree(ctx->d_dssim_part);
+    cudaFree(ctx->d_bcur); cudaFree(ctx->d_ent64);
     cudaFree(ctx->d_adc_cnt); cudaFree(ctx->d_adc_flags); cudaFree(ctx->d_adc_tmp); cudaFree(ctx->d_adc_rep);
     if (ctx->h_adc_rep) cudaFreeHost(ctx->h_adc_rep);
     if (ctx->h_cams) cudaFreeHost(ctx->h_cams);
@@ -289,6 +292,7 @@ mvgs_status mvgs_preprocess(mvgs_ctx* ctx, const mvgs_gaussians* g, const mvgs_c
         CK(cudaDeviceSynchronize());
         CK(grow(ctx->d_blk, ctx->cap_blk, nblk + 1));
         CK(grow(ctx->d_bucket, ctx->cap_buckets, nbuck + 1));
+        CK(grow(ctx->d_bcur, ctx->cap_bcur, nbuck + 1));
         if (need_scan > ctx->cap_scan) {
             cudaFree(ctx->d_scan);
             ctx->d_scan = nullptr;
@@ -335,7 +339,21 @@ mvgs_status mvgs_preprocess(mvgs_ctx* ctx, const mvgs_gaussians* g, const mvgs_c
     const uint32_t* order = L.pval;
     const uint2* rect = L.prect;
     uint32_t* sorted = L.val;
-    if (NB > 0) {
+    if (NB > 0 && MVGS_SORT_BUCKET) {
+        // S3 counts + S5 ranges, S3 duplication into buckets, S4 per-bucket depth sort (k_bucket.cu)
+        {
+            STAGE(ST_SORT_PAIRS);
+            CK(launch_bucket_count(L, ctx->d_bucket, s));
+            CK(scan_exclusive(ctx->d_bucket, (int)nbuck, ctx->d_counters + C_K, ctx->d_scan, s));
+        }
+        { STAGE(ST_DUP); CK(launch_bucket_scatter(L, ctx->d_bcur, ctx->d_ent64, s)); }
+        {
+            STAGE(ST_SORT_ENTRIES);
+            CK(launch_bucket_sort(L, ctx->d_ent64, L.val, s));
+            CK(launch_max_bucket(L, s));
+        }
+        sorted = L.val;
+    } else if (NB > 0) {
         { STAGE(ST_SORT_PAIRS); CK(launch_sort_pairs(L, &order, &rect, s)); }                        // S4a
         { STAGE(ST_DUP); CK(launch_dup_sort(L, order, rect, s)); }                                   // S3
         { STAGE(ST_SORT_ENTRIES); CK(launch_sort_entries(L, &sorted, s)); }                          // S4b + S5
