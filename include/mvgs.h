@@ -235,6 +235,25 @@ mvgs_status mvgs_adc_step(mvgs_ctx *ctx, const mvgs_gaussians *g, const mvgs_adc
 mvgs_status mvgs_adc_remap(mvgs_ctx *ctx, const float *src, float *dst, int64_t width, const int32_t *origin,
                            const uint8_t *kind, int64_t P_new, void *stream);
 
+/* ---- NEXT-4: mini-batch gradient-variance laboratory ------------------------- */
+
+/* Per-pixel loss gradient of a rendered batch: mode 0 (ℓ1) dL = scale·sign(C − C*),
+ * mode 1 (ℓ2) dL = 2·scale·(C − C*); `loss` (device [1] fp64, nullable) receives Σ|C − C*| or
+ * Σ(C − C*)² (multiply by `scale` for the mean).  rgb, target, dL_drgb device [n] fp32
+ * (normally [V,3,H,W] with scale = 1/(3·V·H·W)).  Deterministic fixed-order reduction. */
+mvgs_status mvgs_loss_grad(mvgs_ctx *ctx, const float *rgb, const float *target, int64_t n, int32_t mode, float scale,
+                           float *dL_drgb, double *loss, void *stream);
+
+/* Monte-Carlo accumulators of the variance estimator of §4.2 for one mini-batch
+ * gradient g (device [n] fp32, e.g. the ∂L/∂means of mvgs_adc_stats):
+ *   sum[i] += g[i]  (device [n] fp64),   *sumsq += ‖g‖²  (device [1] fp64). */
+mvgs_status mvgs_grad_moments(mvgs_ctx *ctx, const float *g, int64_t n, double *sum, double *sumsq, void *stream);
+
+/* 𝕍 ≈ (1/K)Σ_k‖g_k‖² − ‖(1/K)Σ_k g_k‖² from the accumulators after K mini-batches
+ * (P:152–156); `variance` device [1] fp64, distinct from sumsq. */
+mvgs_status mvgs_grad_variance(mvgs_ctx *ctx, const double *sum, int64_t n, const double *sumsq, int64_t K,
+                               double *variance, void *stream);
+
 /* Synchronise and report sizes and the capacity flag of the last preprocess.
  * Returns MVGS_ERR_CAPACITY if it overflowed. */
 mvgs_status mvgs_query(mvgs_ctx *ctx, mvgs_stats *out);

@@ -94,6 +94,7 @@ struct mvgs_ctx {
     unsigned long long* d_ent64 = nullptr;  // [cap_entries] bucket-sort keys (depth << 32 | pair)
     int* d_bcur = nullptr;                  // [V*T] bucket cursors
     int64_t cap_bcur = 0;
+    double* d_lab_part = nullptr;           // NEXT-4 per-CTA fp64 partials
     int* d_adc_cnt = nullptr;        // NEXT-3 per-Gaussian emitted-row counts → offsets
     int64_t cap_adc_cnt = 0;
     uint8_t* d_adc_flags = nullptr;
@@ -147,6 +148,12 @@ cudaError_t launch_bucket_count(const Launch& L, int* gcnt, cudaStream_t s);
 cudaError_t launch_bucket_scatter(const Launch& L, int* gcur, unsigned long long* ent, cudaStream_t s);
 cudaError_t launch_bucket_sort(const Launch& L, unsigned long long* ent, uint32_t* sorted, cudaStream_t s);
 cudaError_t launch_max_bucket(const Launch& L, cudaStream_t s);
+int lab_partials();
+cudaError_t launch_loss_grad(const float* rgb, const float* tgt, int64_t n, int mode, float scale, float* dL,
+                             double* loss, double* part, cudaStream_t s);
+cudaError_t launch_moments(const float* g, int64_t n, double* sum, double* sumsq, double* part, cudaStream_t s);
+cudaError_t launch_variance(const double* sum, int64_t n, const double* sumsq, int64_t K, double* out, double* part,
+                            cudaStream_t s);
 cudaError_t launch_render_bwd(const Launch& L, const float* dL, const float* Tf, const int32_t* nc, cudaStream_t s);
 cudaError_t launch_render_fwd_partial(const Launch& L, const int32_t* pix, int S, int mode, float* rgb, float* Tf,
                                       int32_t* nc, cudaStream_t s);

@@ -215,6 +215,7 @@ mvgs_status mvgs_create(mvgs_ctx** out, int device, int64_t max_pairs, int64_t m
         (e = cudaMemset(ctx->d_counters, 0, sizeof(int) * C_NCOUNTERS)) != cudaSuccess ||
         (e = cudaMalloc(&ctx->d_counters64, sizeof(unsigned long long) * 8)) != cudaSuccess ||
         (e = cudaMemset(ctx->d_counters64, 0, sizeof(unsigned long long) * 8)) != cudaSuccess ||
+        (e = cudaMalloc(&ctx->d_lab_part, sizeof(double) * lab_partials())) != cudaSuccess ||
         (e = cudaEventCreateWithFlags(&ctx->cams_ev, cudaEventDisableTiming)) != cudaSuccess) {
         mvgs_destroy(ctx);
         return MVGS_ERR_CUDA;
@@ -235,7 +236,7 @@ void mvgs_destroy(mvgs_ctx* ctx) {
     cudaFree(ctx->d_pflag);
     cudaFree(ctx->d_counters); cudaFree(ctx->d_counters64); cudaFree(ctx->d_scan);
     cudaFree(ctx->d_dssim_coef); cudaFree(ctx->d_dssim_part);
-    cudaFree(ctx->d_bcur); cudaFree(ctx->d_ent64);
+    cudaFree(ctx->d_bcur); cudaFree(ctx->d_ent64); cudaFree(ctx->d_lab_part);
     cudaFree(ctx->d_adc_cnt); cudaFree(ctx->d_adc_flags); cudaFree(ctx->d_adc_tmp); cudaFree(ctx->d_adc_rep);
     if (ctx->h_adc_rep) cudaFreeHost(ctx->h_adc_rep);
     if (ctx->h_cams) cudaFreeHost(ctx->h_cams);
@@ -589,6 +590,34 @@ mvgs_status mvgs_adc_remap(mvgs_ctx* ctx, const float* src, float* dst, int64_t 
         return fail(ctx, MVGS_ERR_INVALID, "adc_remap: bad arguments");
     CK(cudaSetDevice(ctx->device));
     CK(launch_adc_remap(src, dst, width, origin, kind, P_new, (cudaStream_t)stream));
+    return MVGS_OK;
+}
+
+mvgs_status mvgs_loss_grad(mvgs_ctx* ctx, const float* rgb, const float* target, int64_t n, int32_t mode, float scale,
+                           float* dL_drgb, double* loss, void* stream) {
+    if (!ctx) return MVGS_ERR_INVALID;
+    if (n < 0 || (n > 0 && (!rgb || !target || !dL_drgb)) || (mode != 0 && mode != 1))
+        return fail(ctx, MVGS_ERR_INVALID, "loss_grad: bad arguments");
+    CK(cudaSetDevice(ctx->device));
+    CK(launch_loss_grad(rgb, target, n, mode, scale, dL_drgb, loss, ctx->d_lab_part, (cudaStream_t)stream));
+    return MVGS_OK;
+}
+
+mvgs_status mvgs_grad_moments(mvgs_ctx* ctx, const float* g, int64_t n, double* sum, double* sumsq, void* stream) {
+    if (!ctx) return MVGS_ERR_INVALID;
+    if (n < 0 || !sumsq || (n > 0 && (!g || !sum))) return fail(ctx, MVGS_ERR_INVALID, "grad_moments: bad arguments");
+    CK(cudaSetDevice(ctx->device));
+    CK(launch_moments(g, n, sum, sumsq, ctx->d_lab_part, (cudaStream_t)stream));
+    return MVGS_OK;
+}
+
+mvgs_status mvgs_grad_variance(mvgs_ctx* ctx, const double* sum, int64_t n, const double* sumsq, int64_t K,
+                               double* variance, void* stream) {
+    if (!ctx) return MVGS_ERR_INVALID;
+    if (n < 0 || K < 1 || !sumsq || !variance || (n > 0 && !sum) || variance == sumsq)
+        return fail(ctx, MVGS_ERR_INVALID, "grad_variance: bad arguments");
+    CK(cudaSetDevice(ctx->device));
+    CK(launch_variance(sum, n, sumsq, K, variance, ctx->d_lab_part, (cudaStream_t)stream));
     return MVGS_OK;
 }
 

@@ -21,7 +21,8 @@ NG = 10
 SYMBOLS = ["mvgs_create", "mvgs_destroy", "mvgs_last_error", "mvgs_reserve", "mvgs_preprocess", "mvgs_render_fwd",
            "mvgs_render_bwd", "mvgs_adc_stats", "mvgs_query", "mvgs_export_lists", "mvgs_export_pairs",
            "mvgs_set_timing", "mvgs_stage_times", "mvgs_render_fwd_partial", "mvgs_render_bwd_partial",
-           "mvgs_render_fwd_depth", "mvgs_dssim3d", "mvgs_adc_step", "mvgs_adc_remap"]
+           "mvgs_render_fwd_depth", "mvgs_dssim3d", "mvgs_adc_step", "mvgs_adc_remap",
+           "mvgs_loss_grad", "mvgs_grad_moments", "mvgs_grad_variance"]
 PARTIAL_THREAD_EFFICIENT, PARTIAL_MASKED = 0, 1
 STAGE_NAMES = ["count", "scan_pairs", "project", "scan_buckets", "sort_pairs", "dup", "sort_entries", "render_fwd",
                "render_bwd", "gauss_bwd", "dssim"]
@@ -102,6 +103,9 @@ def _load():
     L.mvgs_dssim3d.argtypes = [vp, vp, C.c_int32, C.c_int32, C.c_int32, vp, vp, vp, vp, C.c_float, vp, vp, vp]
     L.mvgs_adc_step.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]
     L.mvgs_adc_remap.argtypes = [vp, vp, vp, i64, vp, vp, i64, vp]
+    L.mvgs_loss_grad.argtypes = [vp, vp, vp, i64, C.c_int32, C.c_float, vp, vp, vp]
+    L.mvgs_grad_moments.argtypes = [vp, vp, i64, vp, vp, vp]
+    L.mvgs_grad_variance.argtypes = [vp, vp, i64, vp, i64, vp, vp]
     L.mvgs_stage_times.argtypes = [vp, C.POINTER(C.c_float), C.c_int]
     L.mvgs_stage_times.restype = C.c_int
     for n in SYMBOLS:
@@ -249,6 +253,28 @@ def adc_remap(ctx, src, dst, origin, kind, P_new: int, stream=None):
     width = int(src[0].numel()) if src.dim() > 1 else 1
     _check(ctx, _lib.mvgs_adc_remap(ctx, _ptr(src), _ptr(dst), width, _ptr(origin), _ptr(kind), int(P_new),
                                     _stream(stream)))
+
+
+LOSS_L1, LOSS_L2 = 0, 1
+
+
+def loss_grad(ctx, rgb, target, dL, mode: int = LOSS_L1, scale: float | None = None, loss=None, stream=None):
+    """NEXT-4: ∂loss/∂C of a rendered batch (ℓ1 or ℓ2, mean over all elements by default)."""
+    n = int(rgb.numel())
+    sc = 1.0 / n if scale is None else scale
+    _check(ctx, _lib.mvgs_loss_grad(ctx, _ptr(rgb), _ptr(target), n, int(mode), float(sc), _ptr(dL), _ptr(loss),
+                                    _stream(stream)))
+
+
+def grad_moments(ctx, g, acc_sum, acc_sumsq, stream=None):
+    """NEXT-4 (P:152–156): acc_sum (fp64 [n]) += g, acc_sumsq (fp64 [1]) += ‖g‖²."""
+    _check(ctx, _lib.mvgs_grad_moments(ctx, _ptr(g), int(g.numel()), _ptr(acc_sum), _ptr(acc_sumsq), _stream(stream)))
+
+
+def grad_variance(ctx, acc_sum, acc_sumsq, K: int, out, stream=None):
+    """NEXT-4: 𝕍 = (1/K)Σ‖g_k‖² − ‖(1/K)Σ g_k‖² into out (fp64 [1])."""
+    _check(ctx, _lib.mvgs_grad_variance(ctx, _ptr(acc_sum), int(acc_sum.numel()), _ptr(acc_sumsq), int(K), _ptr(out),
+                                        _stream(stream)))
 
 
 def query(ctx, raise_on_capacity: bool = True) -> dict:

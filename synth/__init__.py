@@ -397,3 +397,17 @@ def make_adc_inputs(P: int, seed: int, N: int = 2, sh_degree: int = 3, iters: in
     acc = dict(e1=e1, e2=e2, e_old=eo, denom=den)
     noise = rng.normal(0, 1, (P, N, 3)).astype(np.float32)
     return g, acc, noise
+
+
+def make_lab_targets(V: int, H: int, W: int, seed: int) -> np.ndarray:
+    """Seeded target photos for the NEXT-4 variance lab: per view a smooth
+    colour field (random linear ramps + low-frequency sinusoids) in [0, 1], float32 [V,3,H,W].
+    Independent of any scene: the lab only needs a fixed per-view loss landscape."""
+    rng = np.random.Generator(np.random.PCG64(seed + 1300))
+    y, x = np.mgrid[0:H, 0:W].astype(np.float64)
+    out = np.empty((V, 3, H, W))
+    for v in range(V):
+        for c in range(3):
+            a, b, f1, f2, ph = rng.uniform(-1, 1, 5)
+            out[v, c] = 0.4 + 0.2 * (a * x / W + b * y / H) + 0.2 * np.sin(2 * np.pi * (f1 * x / W + f2 * y / H) + 3 * ph)
+    return np.clip(out, 0, 1).astype(np.float32)
