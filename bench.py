@@ -52,7 +52,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="garden", choices=list(synth.CONFIGS))
     ap.add_argument("--impl", default="mvgs", choices=["mvgs", "reference"])
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=8)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile", action="store_true",
                     help="sizing pass + warmup + one step, nothing else (for ncu)")
@@ -121,20 +121,21 @@ def measured_peaks():
     return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
 
 
-def stage_models(P, NK, V, NB, Q, K, T, evf, evb, exf, exb):
-    """(bound, algorithmic units per launch) per stage — DESIGN.md §7."""
+def stage_models(P, NK, V, NB, Q, K, T, evf, evb, exf, exb, Qv):
+    """(bound, algorithmic units per launch) per stage — DESIGN.md §7.  Qv = pairs with
+    tiles > 0 (the rest are inert: only their depth, flags and sort key are written)."""
     pbytes = 4 * (11 + 3 * NK) * P
     return {
         "count": ("hbm", 12 * P + 4 * V * NB),
         "scan_pairs": ("hbm", 3 * 4 * V * NB),
-        "project": ("hbm", pbytes + 4 * V * NB + Q * (48 + 8 + 48)),
+        "project": ("hbm", pbytes + 4 * V * NB + Qv * (48 + 4 + 4 + 8) + (Q - Qv) * (16 + 4 + 4)),
         "scan_buckets": ("hbm", 3 * 4 * V * T),
         "sort_pairs": ("hbm", 4 * 16 * Q),
         "dup": ("hbm", Q * (4 + 16 + 8 + 4 + 4) + 8 * K),
         "sort_entries": ("hbm", ((max(1, (V * T - 1).bit_length()) + 7) // 8) * 16 * K),
         "render_fwd": ("alu", FLOPS_VISIT * evf + FWD_FLOPS_REST * exf),
         "render_bwd": ("alu", FLOPS_VISIT * evb + BWD_FLOPS_REST * exb),
-        "gauss_bwd": ("hbm", 2 * pbytes + Q * (16 + 8 + 48) + 16 * P),
+        "gauss_bwd": ("hbm", 2 * pbytes + 4 * Q + 48 * Qv + 16 * P),
     }
 
 
@@ -142,9 +143,9 @@ def launches_per_step(nbuckets, Q, K):
     """Kernels libmvgs launches per step: count + 3-kernel scan, project,
     pair sort (upsweep + bases + 4 onesweep passes), pair-tiles + 3-kernel scan + dup,
     entry sort (⌈log2(V·T)/8⌉ passes × (histogram + 3-kernel scan + scatter)),
-    ranges + max-bucket, fwd, bwd, gauss_bwd."""
+    ranges close-up (the bucket starts come out of the last entry pass), fwd, bwd, gauss_bwd."""
     ent_passes = (max(1, (nbuckets - 1).bit_length()) + 7) // 8
-    return (1 + 3) + 1 + (2 + 4) + (1 + 3 + 1) + 5 * ent_passes + 2 + 3
+    return (1 + 3) + 1 + (2 + 4) + (1 + 3 + 1) + 5 * ent_passes + 1 + 3
 
 
 # ---------------------------------------------------------------------- mvgs
@@ -227,25 +228,61 @@ def run_mvgs(args):
     views_total = Vr * N
     value = views_total / (ms / 1e3)
 
-    # ---- e2e: the same step through the public API with HOST buffers:
-    # pinned host params + dL/dC copied in, gradients + ADC stats copied out.
+    # ---- e2e: the same step through the public API with HOST buffers: every step copies
+    # its inputs (pinned host params + dL/dC) in and its result (gradients + ADC stats)
+    # out.  Copies run on their own streams, double-buffered on the device, so step i+1's
+    # upload and step i−1's download overlap step i's kernels (PCIe is full duplex; the
+    # two directions use separate copy engines).  Timed from the first upload to the
+    # last download on the device.
     host_in = {k: torch.from_numpy(v).pin_memory() for k, v in g_np.items() if isinstance(v, np.ndarray)}
     host_dL = dL.cpu().pin_memory()
-    host_out = torch.empty_like(flat, device="cpu").pin_memory()
+    host_out = [torch.empty_like(flat, device="cpu").pin_memory() for _ in range(2)]
     h2d = sum(t.numel() * 4 for t in host_in.values()) + host_dL.numel() * 4
-    d2h = host_out.numel() * 4
+    d2h = host_out[0].numel() * 4
+    g_slots = [g, {k: (torch.empty_like(v) if torch.is_tensor(v) else v) for k, v in g.items()}]
+    dL_slots = [dL, torch.empty_like(dL)]
+    bufs = [buf, GradBuffer(P, S, dev)]
+    comp = torch.cuda.current_stream()
+    s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
+    mk = lambda: [torch.cuda.Event() for _ in range(2)]  # noqa: E731
+    in_ready, in_free, out_ready, out_free = mk(), mk(), mk(), mk()
+
+    def e2e_step(i):
+        b = i % 2
+        if i >= 2:
+            s_in.wait_event(in_free[b])
+        with torch.cuda.stream(s_in):
+            for k, t in host_in.items():
+                g_slots[b][k].copy_(t, non_blocking=True)
+            dL_slots[b].copy_(host_dL, non_blocking=True)
+        in_ready[b].record(s_in)
+        comp.wait_event(in_ready[b])
+        if i >= 2:
+            comp.wait_event(out_free[b])
+        ob = bufs[b]
+        mvgs.preprocess(R.ctx, g_slots[b], R.cams)
+        mvgs.render_fwd(R.ctx, *outs)
+        mvgs.render_bwd(R.ctx, dL_slots[b], outs[1], outs[2])
+        mvgs.adc_stats(R.ctx, ob.grads, ob.adc)
+        if dist is not None:
+            ob.allreduce()
+        in_free[b].record(comp)
+        out_ready[b].record(comp)
+        s_out.wait_event(out_ready[b])
+        with torch.cuda.stream(s_out):
+            host_out[b].copy_(ob.flat, non_blocking=True)
+        out_free[b].record(s_out)
+
     if dist is not None:
         dist.barrier()
     torch.cuda.synchronize()
     e0, e1_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(args.e2e_steps):
-        for k, t in host_in.items():
-            g[k].copy_(t, non_blocking=True)
-        dL.copy_(host_dL, non_blocking=True)
-        step()
-        host_out.copy_(flat, non_blocking=True)
-    e1_.record()
+    e0.record(comp)
+    s_in.wait_event(e0)
+    for i in range(args.e2e_steps):
+        e2e_step(i)
+    comp.wait_event(out_free[(args.e2e_steps - 1) % 2])
+    e1_.record(comp)
     torch.cuda.synchronize()
     e2e_ms = e0.elapsed_time(e1_) / args.e2e_steps
     if dist is not None:
@@ -258,7 +295,7 @@ def run_mvgs(args):
     T = st["tiles_x"] * st["tiles_y"]
     NB = (P + 255) // 256
     models = stage_models(P, NK, Vr, NB, st["Q"], st["K"], T, st["eval_fwd"], st["eval_bwd"], st["exp_fwd"],
-                          st["exp_bwd"])
+                          st["exp_bwd"], st["n_visible"])
     dom = max(stages, key=lambda k: stages[k])
     bound, units = models[dom]
     t_dom = stages[dom] / 1e3

@@ -19,13 +19,6 @@ constexpr uint32_t PF_VISIBLE = 32u;
 // device counters (int32 slots in ctx->d_counters)
 enum { C_Q = 0, C_K = 1, C_OVERFLOW = 2, C_MAXB = 3, C_NVIS = 4, C_NCOUNTERS = 8 };
 
-// Per-pair meta: gid and (view << 8 | flags).  flags bit0..2: rgb clamped,
-// bit3: Jacobian x clamp, bit4: y clamp, bit5: tiles > 0 (visible).
-struct PairMeta {
-    uint32_t gid;
-    uint32_t vf;
-};
-
 struct RadixScratch {
     unsigned long long* status;  // [256 × tiles] look-back words (epoch-tagged)
     uint32_t* small;             // digit totals, bases, tile counters, device pass epoch
@@ -43,7 +36,6 @@ struct Launch {  // everything a kernel needs about the current batch
     int* blk_off;     // [V*NB + 1]  exclusive scan of per-(view, block) participation counts
     int* bucket_off;  // [V*T + 1]   exclusive scan of per-(view, tile) entry counts
     float4* rec;      // [cap_pairs * 3]
-    PairMeta* meta;   // [cap_pairs]
     uint32_t* pflag;  // [cap_pairs] bit0-2 rgb clamped, bit3-4 Jacobian clamps, bit5 tiles > 0
     float* pgrad;     // [cap_pairs * PG_STRIDE]
     uint32_t *key, *val, *key2, *val2;  // [cap_entries] entry (bucket key, pair) ping-pong
@@ -57,6 +49,21 @@ struct Launch {  // everything a kernel needs about the current batch
     int* counters;    // [C_NCOUNTERS]
     unsigned long long* counters64;  // [8]: fwd/bwd evaluations, fwd/bwd exps, entries needed
 };
+
+#ifdef __CUDACC__
+// Every forward launch clears the per-pair gradient slots [0, Q) that the following
+// backward accumulates into (red.add).  The forward kernels are compute-bound with
+// little DRAM traffic, so these fire-and-forget stores ride along instead of costing
+// the HBM-bound projection 48 B per pair; each CTA clears one grid-strided slice.
+__device__ __forceinline__ void zero_pgrad_slice(const Launch& L) {
+    const int64_t Q = min((int64_t)L.counters[C_Q], L.cap_pairs);
+    float4* p4 = reinterpret_cast<float4*>(L.pgrad);
+    const int64_t n4 = Q * (PG_STRIDE / 4);
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride)
+        p4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+}
+#endif
 
 }  // namespace mvgs
 
@@ -72,7 +79,6 @@ struct mvgs_ctx {
     int* d_blk = nullptr;
     int* d_bucket = nullptr;
     float4* d_rec = nullptr;
-    mvgs::PairMeta* d_meta = nullptr;
     uint32_t* d_pflag = nullptr;
     float* d_pgrad = nullptr;
     uint32_t *d_key = nullptr, *d_val = nullptr, *d_key2 = nullptr, *d_val2 = nullptr;
@@ -114,7 +120,7 @@ struct mvgs_ctx {
 
 namespace mvgs {
 // launchers (return cudaGetLastError())
-cudaError_t scan_exclusive(int* a, int n, int* total_slot, int* tmp, cudaStream_t s);
+cudaError_t scan_exclusive(int* a, int n, int* total_slot, int* tmp, cudaStream_t s, const int* n_live = nullptr);
 cudaError_t launch_count(const Launch& L, cudaStream_t s);
 cudaError_t launch_project(const Launch& L, cudaStream_t s);
 cudaError_t launch_sort_pairs(const Launch& L, const uint32_t** order_out, const uint2** rect_out, cudaStream_t s);

@@ -55,6 +55,7 @@ __global__ __launch_bounds__(256) void k_render_fwd_list(Launch L, const int32_t
                                                          int32_t* __restrict__ out_n) {
     __shared__ float4 s0[PRB], s1[PRB], s2[PRB];
     __shared__ int slot_of[256];
+    zero_pgrad_slice(L);
     const int bucket = blockIdx.x;
     const int tile = bucket % L.T;
     const int ty = tile / L.TX, tx = tile - ty * L.TX;

@@ -50,8 +50,18 @@ __device__ __forceinline__ int block_exclusive_scan_1024(int x, int* sm /*[32]*/
     return r;
 }
 
-__global__ __launch_bounds__(SCAN_T) void k_scan_reduce(const int* __restrict__ a, int n, int* __restrict__ tmp) {
+// n_live (device, nullable): only a[0, min(*n_live, n)) is scanned and the total goes to
+// a[min(*n_live, n)]; blocks past the live count exit at once.
+__device__ __forceinline__ int scan_n(int n, const int* n_live) { return n_live ? min(*n_live, n) : n; }
+
+__global__ __launch_bounds__(SCAN_T) void k_scan_reduce(const int* __restrict__ a, int n, int* __restrict__ tmp,
+                                                        const int* __restrict__ n_live) {
     __shared__ int sm[33];
+    n = scan_n(n, n_live);
+    if ((int)blockIdx.x * SCAN_TILE >= n && blockIdx.x > 0) {
+        if (threadIdx.x == 0) tmp[blockIdx.x] = 0;
+        return;
+    }
     int base = blockIdx.x * SCAN_TILE + threadIdx.x * SCAN_IPT;
     int s = 0;
 #pragma unroll
@@ -78,8 +88,12 @@ __global__ __launch_bounds__(SCAN_T) void k_scan_top(int* __restrict__ tmp, int 
     }
 }
 
-__global__ __launch_bounds__(SCAN_T) void k_scan_apply(int* __restrict__ a, int n, const int* __restrict__ tmp, int nb) {
+__global__ __launch_bounds__(SCAN_T) void k_scan_apply(int* __restrict__ a, int n, const int* __restrict__ tmp, int nb,
+                                                       const int* __restrict__ n_live) {
     __shared__ int sm[33];
+    n = scan_n(n, n_live);
+    const int last_blk = min(n / SCAN_TILE, nb - 1);  // the block that writes a[n]
+    if ((int)blockIdx.x > last_blk) return;
     int base = blockIdx.x * SCAN_TILE + threadIdx.x * SCAN_IPT;
     int v[SCAN_IPT];
     int s = 0;
@@ -95,16 +109,17 @@ __global__ __launch_bounds__(SCAN_T) void k_scan_apply(int* __restrict__ a, int 
         if (base + i < n) a[base + i] = ex;
         ex += v[i];
     }
-    if (blockIdx.x == nb - 1 && threadIdx.x == 0) a[n] = tmp[nb];
+    if ((int)blockIdx.x == last_blk && threadIdx.x == 0) a[n] = tmp[nb];
 }
 
-// Exclusive scan of a[0..n) in place; a[n] and *total_slot receive the total.
-cudaError_t scan_exclusive(int* a, int n, int* total_slot, int* tmp, cudaStream_t s) {
+// Exclusive scan of a[0..n) in place; a[n] and *total_slot receive the total.  With
+// n_live (device) only the first min(*n_live, n) elements take part (see k_scan_reduce).
+cudaError_t scan_exclusive(int* a, int n, int* total_slot, int* tmp, cudaStream_t s, const int* n_live) {
     int nb = (n + SCAN_TILE - 1) / SCAN_TILE;
     if (nb == 0) nb = 1;
-    k_scan_reduce<<<nb, SCAN_T, 0, s>>>(a, n, tmp);
+    k_scan_reduce<<<nb, SCAN_T, 0, s>>>(a, n, tmp, n_live);
     k_scan_top<<<1, SCAN_T, 0, s>>>(tmp, nb, total_slot);
-    k_scan_apply<<<nb, SCAN_T, 0, s>>>(a, n, tmp, nb);
+    k_scan_apply<<<nb, SCAN_T, 0, s>>>(a, n, tmp, nb, n_live);
     return cudaGetLastError();
 }
 
@@ -212,6 +227,7 @@ __global__ __launch_bounds__(BLK) void k_project(Launch L) {
     }
     const unsigned lt = (1u << lane) - 1u;
     unsigned long long my_tiles = 0;  // entries this Gaussian needs (K needed, capacity-independent)
+    unsigned my_vis = 0;              // stored visible pairs of this Gaussian
     for (int v0 = 0; v0 < L.V; v0 += 32) {
         const int nv = min(32, L.V - v0);
         for (int k = 0; k < nv; k++) {
@@ -235,21 +251,18 @@ __global__ __launch_bounds__(BLK) void k_project(Launch L) {
             Proj p;
             ca_project(c, mx, my, mz, a.Sig, L.TX, L.TY, p);
             const int tiles = p.ok ? (p.rx1 - p.rx0) * (p.ry1 - p.ry0) : 0;
-            if (pair < L.cap_pairs) {  // depth key + rect for the pair sort (inert pairs sort last)
+            if (pair < L.cap_pairs) {  // depth key + rect for the pair sort (the value is the slot itself)
                 L.pkey[pair] = tiles > 0 ? __float_as_uint(p.tz) : 0xffffffffu;
-                L.pval[pair] = (uint32_t)pair;
-                L.prect[pair] = tiles > 0 ? make_uint2((uint32_t)p.rx0 | ((uint32_t)p.ry0 << 16),
-                                                       (uint32_t)p.rx1 | ((uint32_t)p.ry1 << 16))
-                                          : make_uint2(0u, 0u);
+                if (tiles > 0)  // inert keys are dropped by the first sort pass: no rect needed
+                    L.prect[pair] = make_uint2((uint32_t)p.rx0 | ((uint32_t)p.ry0 << 16),
+                                               (uint32_t)p.rx1 | ((uint32_t)p.ry1 << 16));
             }
             if (pair >= L.cap_pairs) {
                 L.counters[C_OVERFLOW] = 1;
             } else if (tiles == 0) {
                 // inert pair (R27): only the empty rect / depth and the ids are read later
                 L.rec[3 * pair + 2] = make_float4(0.f, p.tz, 0.f, 0.f);
-                const uint32_t fl = (p.clx ? 8u : 0u) | (p.cly ? 16u : 0u);
-                L.meta[pair] = PairMeta{(uint32_t)g, ((uint32_t)v << 8) | fl};
-                L.pflag[pair] = fl;
+                L.pflag[pair] = (p.clx ? 8u : 0u) | (p.cly ? 16u : 0u);
             } else {
                 // colour (R17), free arithmetic
                 const float cpx = -(c.R[0] * c.t[0] + c.R[3] * c.t[1] + c.R[6] * c.t[2]);
@@ -279,19 +292,38 @@ __global__ __launch_bounds__(BLK) void k_project(Launch L) {
                 r[0] = make_float4(p.px, p.py, p.A, p.B);
                 r[1] = make_float4(p.C, a.o, rgb[0], rgb[1]);
                 r[2] = make_float4(rgb[2], p.tz, __uint_as_float(lo), __uint_as_float(hi));
-                L.meta[pair] = PairMeta{(uint32_t)g, ((uint32_t)v << 8) | flags};
-                L.pflag[pair] = flags | PF_VISIBLE;
-                float4* pg = reinterpret_cast<float4*>(L.pgrad + pair * PG_STRIDE);
-                pg[0] = pg[1] = pg[2] = make_float4(0.f, 0.f, 0.f, 0.f);
+                L.pflag[pair] = flags | PF_VISIBLE;  // (its gradient slot is cleared by the forward)
             }
-            if (tiles > 0 && pair < L.cap_pairs) atomicAdd(&L.counters[C_NVIS], 1);  // stored visible pairs
+            my_vis += (tiles > 0 && pair < L.cap_pairs) ? 1u : 0u;
             my_tiles += (unsigned long long)tiles;
         }
         __syncthreads();
     }
+    // CTA totals, then one atomic per counter per CTA: same-address atomics serialise in one
+    // L2 slice (per-warp ones cost ≈ 1 ns each, i.e. ~0.1 ms per 94k warps per view)
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) my_tiles += __shfl_xor_sync(FULL, my_tiles, o);
-    if (lane == 0 && my_tiles) atomicAdd(&L.counters64[4], my_tiles);
+    for (int o = 16; o > 0; o >>= 1) {
+        my_tiles += __shfl_xor_sync(FULL, my_tiles, o);
+        my_vis += __shfl_xor_sync(FULL, my_vis, o);
+    }
+    __shared__ unsigned long long s_tiles[BLK / 32];
+    __shared__ unsigned s_vis[BLK / 32];
+    if (lane == 0) {
+        s_tiles[warp] = my_tiles;
+        s_vis[warp] = my_vis;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long t = 0;
+        unsigned nv = 0;
+#pragma unroll
+        for (int w = 0; w < BLK / 32; w++) {
+            t += s_tiles[w];
+            nv += s_vis[w];
+        }
+        if (t) atomicAdd(&L.counters64[4], t);
+        if (nv) atomicAdd(&L.counters[C_NVIS], (int)nv);
+    }
 }
 
 template <int D>
@@ -313,6 +345,29 @@ cudaError_t launch_project(const Launch& L, cudaStream_t s) {
 }
 
 // ------------------------------------------------------------------ export (tests)
+// (view, gid) of pair slot q, recomputed from the slot allocation (no per-pair ids are
+// stored by the path): the view and 256-Gaussian block by binary search over the scanned
+// per-(view, block) offsets, then the rank among the block's z-visible Gaussians.
+__device__ void slot_ids(const Launch& L, int64_t q, int& view, int64_t& gid) {
+    int lo = 0, hi = L.V * L.NB - 1;  // last (view, block) index with blk_off ≤ q (skips empty ones)
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if ((int64_t)L.blk_off[mid] <= q) lo = mid;
+        else hi = mid - 1;
+    }
+    view = lo / L.NB;
+    const int b = lo - view * L.NB;
+    int r = (int)(q - L.blk_off[lo]);
+    const mvgs_camera& c = L.cams[view];
+    gid = -1;
+    for (int64_t g = (int64_t)b * BLK; g < min(L.P, (int64_t)(b + 1) * BLK); g++) {
+        if (ca_depth(c, L.means[3 * g], L.means[3 * g + 1], L.means[3 * g + 2]) > c.znear && r-- == 0) {
+            gid = g;
+            break;
+        }
+    }
+}
+
 __global__ void k_export(Launch L, int64_t* range_start, int32_t* entry_gid, int32_t* pair_ids, int32_t* pair_i,
                          float* pair_f, float* pair_g) {
     const int Q = min((int64_t)L.counters[C_Q], L.cap_pairs);
@@ -323,14 +378,21 @@ __global__ void k_export(Launch L, int64_t* range_start, int32_t* entry_gid, int
     if (range_start)
         for (int64_t b = t0; b <= nb; b += stride) range_start[b] = L.bucket_off[b];
     if (entry_gid)
-        for (int64_t e = t0; e < K; e += stride) entry_gid[e] = (int32_t)L.meta[L.sorted[e]].gid;
+        for (int64_t e = t0; e < K; e += stride) {
+            int v;
+            int64_t gid;
+            slot_ids(L, L.sorted[e], v, gid);
+            entry_gid[e] = (int32_t)gid;
+        }
     for (int64_t q = t0; q < Q; q += stride) {
-        const PairMeta m = L.meta[q];
+        int view = 0;
+        int64_t gid = 0;
+        if (pair_ids) slot_ids(L, q, view, gid);
         const float4 r0 = L.rec[3 * q], r1 = L.rec[3 * q + 1], r2 = L.rec[3 * q + 2];
         const uint32_t lo = __float_as_uint(r2.z), hi = __float_as_uint(r2.w);
         if (pair_ids) {
-            pair_ids[2 * q] = (int32_t)(m.vf >> 8);
-            pair_ids[2 * q + 1] = (int32_t)m.gid;
+            pair_ids[2 * q] = (int32_t)view;
+            pair_ids[2 * q + 1] = (int32_t)gid;
         }
         if (pair_i) {
             const int rx0 = lo & 0xffff, ry0 = lo >> 16, rx1 = hi & 0xffff, ry1 = hi >> 16;
@@ -338,7 +400,7 @@ __global__ void k_export(Launch L, int64_t* range_start, int32_t* entry_gid, int
             o[0] = 0;  // radius is not kept by the path; tests compare the rect
             o[1] = rx0; o[2] = ry0; o[3] = rx1; o[4] = ry1;
             o[5] = (rx1 - rx0) * (ry1 - ry0);
-            o[6] = (int32_t)(m.vf & 0xff);
+            o[6] = (int32_t)(L.pflag[q] & 0x1fu);
             o[7] = 0;
         }
         const bool inert = lo == hi;  // tiles == 0: only depth and ids were written (R27)

@@ -76,6 +76,7 @@ __global__ __launch_bounds__(RT) void k_render_fwd(Launch L, float* __restrict__
                                                    int32_t* __restrict__ out_n, float* __restrict__ out_D) {
     __shared__ float4 s0[RT], s1[RT], s2[RT];
     __shared__ unsigned sev[2];
+    zero_pgrad_slice(L);
     const int bucket = blockIdx.x;
     const int v = bucket / L.T, tile = bucket - v * L.T;
     const int ty = tile / L.TX, tx = tile - ty * L.TX;
@@ -192,6 +193,7 @@ __global__ __launch_bounds__(RT) void k_render_fwd_p(Launch L, float* __restrict
                                                      float* __restrict__ out_D) {
     __shared__ FwdConsts sf[RT];
     __shared__ unsigned sev[2];
+    zero_pgrad_slice(L);
     const int bucket = blockIdx.x;
     const int v = bucket / L.T, tile = bucket - v * L.T;
     const int ty = tile / L.TX, tx = tile - ty * L.TX;

@@ -85,7 +85,7 @@ __global__ __launch_bounds__(RS_T) void k_rs_hist(const uint32_t* __restrict__ k
     const uint32_t mask = (1u << nbits) - 1u;
     for (int i = t0 + threadIdx.x; i < min(n, t0 + RS_TILE); i += RS_T) atomicAdd(&h[(keys[i] >> shift) & mask], 1);
     __syncthreads();
-    counts[(int64_t)threadIdx.x * ntiles + blockIdx.x] = h[threadIdx.x];
+    if (threadIdx.x <= mask) counts[(int64_t)threadIdx.x * ntiles + blockIdx.x] = h[threadIdx.x];
 }
 
 // Stable scatter of one tile.  Ranks are computed per warp (multisplit), the
@@ -98,7 +98,8 @@ __global__ __launch_bounds__(RS_T) void k_rs_scatter(const uint32_t* __restrict_
                                                      uint32_t* __restrict__ kout, uint32_t* __restrict__ vout,
                                                      const uint2* __restrict__ pin, uint2* __restrict__ pout,
                                                      const int* __restrict__ n_ptr, int64_t cap, int shift, int nbits,
-                                                     const int* __restrict__ offs, int ntiles) {
+                                                     const int* __restrict__ offs, int ntiles,
+                                                     int* __restrict__ range_min) {
     __shared__ uint32_t hist[RS_NW][RS_BINS];
     __shared__ uint32_t dstart[RS_BINS];   // first local position of each digit
     __shared__ uint32_t gdelta[RS_BINS];   // global offset − local start, per digit
@@ -144,7 +145,7 @@ __global__ __launch_bounds__(RS_T) void k_rs_scatter(const uint32_t* __restrict_
         uint32_t ws;
         const uint32_t start = block_excl_scan_256_u(tot, &ws);
         dstart[threadIdx.x] = start;
-        gdelta[threadIdx.x] = (uint32_t)offs[(int64_t)threadIdx.x * ntiles + blockIdx.x] - start;
+        gdelta[threadIdx.x] = threadIdx.x <= mask ? (uint32_t)offs[(int64_t)threadIdx.x * ntiles + blockIdx.x] - start : 0u;
         uint32_t run = start;
 #pragma unroll
         for (int w = 0; w < RS_NW; w++) {
@@ -165,6 +166,19 @@ __global__ __launch_bounds__(RS_T) void k_rs_scatter(const uint32_t* __restrict_
         }
     }
     __syncthreads();
+    if (range_min) {
+        // Last pass (S5 fused): the tile is now ordered by the FULL key (its input was sorted by
+        // the lower digits and this pass is stable), so each local run start of a key is a
+        // candidate bucket start; the global start is the minimum over tiles.  The sorted keys
+        // themselves are not needed afterwards and are not written.
+        for (int l = threadIdx.x; l < nt; l += RS_T) {
+            const uint32_t k = sk[l];
+            const uint32_t dst = gdelta[(k >> shift) & mask] + l;
+            vout[dst] = sv[l];
+            if (l == 0 || sk[l - 1] != k) atomicMin(&range_min[k], (int)dst);
+        }
+        return;
+    }
     for (int l = threadIdx.x; l < nt; l += RS_T) {
         const uint32_t k = sk[l];
         const uint32_t dst = gdelta[(k >> shift) & mask] + l;
@@ -179,8 +193,12 @@ __global__ __launch_bounds__(RS_T) void k_rs_scatter(const uint32_t* __restrict_
 // Stable LSD sort of (k, v[, payload])[0..*n_ptr) on bits [0, bits) with ≤ 8-bit
 // digits.  Returns the number of passes; the result is in the first buffers when
 // even, in the second ones when odd.
+// With range_min (entries: keys < 2^bits are bucket ids) the last pass also writes each
+// bucket's first position (atomicMin; the caller fills range_min with INT_MAX first and
+// closes empty buckets afterwards) and skips writing the sorted keys.
 int radix_sort_3k(uint32_t* k, uint32_t* v, uint32_t* k2, uint32_t* v2, uint2* pl, uint2* pl2, const int* n_ptr,
-               int64_t cap, int bits, int* counts, int* scan_tmp, cudaStream_t s, cudaError_t* err) {
+               int64_t cap, int bits, int* counts, int* scan_tmp, cudaStream_t s, cudaError_t* err,
+               int* range_min = nullptr) {
     const int ntiles = radix_tiles(cap);
     const int npass = (bits + 7) / 8;
     const int db = npass ? (bits + npass - 1) / npass : 0;
@@ -192,12 +210,15 @@ int radix_sort_3k(uint32_t* k, uint32_t* v, uint32_t* k2, uint32_t* v2, uint2* p
         const int shift = pass * db;
         const int nb = min(db, bits - shift);
         k_rs_hist<<<ntiles, RS_T, 0, s>>>(ks, n_ptr, cap, shift, nb, counts, ntiles);
-        if ((*err = scan_exclusive(counts, RS_BINS * ntiles, nullptr, scan_tmp, s)) != cudaSuccess) return pass;
+        // only the live digits' counts (digit-major layout): a 7-bit pass scans half the table
+        if ((*err = scan_exclusive(counts, (1 << nb) * ntiles, nullptr, scan_tmp, s)) != cudaSuccess) return pass;
+        int* rm = (pass == npass - 1) ? range_min : nullptr;
         if (pl)
-            k_rs_scatter<true><<<ntiles, RS_T, 0, s>>>(ks, vs, kd, vd, ps, pd, n_ptr, cap, shift, nb, counts, ntiles);
+            k_rs_scatter<true><<<ntiles, RS_T, 0, s>>>(ks, vs, kd, vd, ps, pd, n_ptr, cap, shift, nb, counts, ntiles,
+                                                       rm);
         else
             k_rs_scatter<false><<<ntiles, RS_T, 0, s>>>(ks, vs, kd, vd, nullptr, nullptr, n_ptr, cap, shift, nb,
-                                                        counts, ntiles);
+                                                        counts, ntiles, rm);
         if ((*err = cudaGetLastError()) != cudaSuccess) return pass;
         uint32_t* t = ks; ks = kd; kd = t;
         t = vs; vs = vd; vd = t;
@@ -297,7 +318,7 @@ __global__ __launch_bounds__(RS_T) void k_rs_onesweep(const uint32_t* __restrict
         const int p = warp * 32 * RS_IPT + it * 32 + lane;
         const bool ok = p < nt;
         key[it] = ok ? kin[t0 + p] : INERT;
-        val[it] = ok ? vin[t0 + p] : 0u;
+        val[it] = vin ? (ok ? vin[t0 + p] : 0u) : (uint32_t)(t0 + p);  // no vin: the identity
         if (PAYLOAD) pay[PAYLOAD ? it : 0] = ok ? pin[t0 + p] : make_uint2(0u, 0u);
     }
 #pragma unroll
@@ -370,11 +391,12 @@ __global__ __launch_bounds__(RS_T) void k_rs_onesweep(const uint32_t* __restrict
 
 // Stable LSD sort of (k, v[, payload])[0..*n_ptr) on bits [0, bits) with ≤ 8-bit
 // digits; with drop_inert the first pass removes keys equal to 0xffffffff and the
-// later passes run on *n_after elements.  Returns the number of passes; the result
+// later passes run on *n_after elements; with identity_vals the first pass takes the
+// values to be the input positions (v is not read).  Returns the number of passes; the result
 // is in the first buffers when even, in the second ones when odd.
 int radix_sort(uint32_t* k, uint32_t* v, uint32_t* k2, uint32_t* v2, uint2* pl, uint2* pl2, const int* n_ptr,
-               const int* n_after, int64_t cap, int bits, bool drop_inert, const RadixScratch& rs, cudaStream_t s,
-               cudaError_t* err) {
+               const int* n_after, int64_t cap, int bits, bool drop_inert, bool identity_vals, const RadixScratch& rs,
+               cudaStream_t s, cudaError_t* err) {
     const int ntiles = radix_tiles(cap);
     const int npass = (bits + 7) / 8;
     const int db = npass ? (bits + npass - 1) / npass : 0;
@@ -393,12 +415,13 @@ int radix_sort(uint32_t* k, uint32_t* v, uint32_t* k2, uint32_t* v2, uint2* pl, 
         const int shift = pass * db;
         const int nb = min(db, bits - shift);
         const int* np = (pass == 0) ? n_ptr : (drop_inert ? n_after : n_ptr);
+        const uint32_t* vin = (pass == 0 && identity_vals) ? nullptr : vs;
         if (pl)
-            k_rs_onesweep<true><<<ntiles, RS_T, 0, s>>>(ks, vs, kd, vd, ps, pd, np, cap, shift, nb,
+            k_rs_onesweep<true><<<ntiles, RS_T, 0, s>>>(ks, vin, kd, vd, ps, pd, np, cap, shift, nb,
                                                         (drop_inert && pass == 0) ? 1 : 0, gbase + pass * RS_BINS,
                                                         rs.status, epoch, pass, tctr + pass);
         else
-            k_rs_onesweep<false><<<ntiles, RS_T, 0, s>>>(ks, vs, kd, vd, nullptr, nullptr, np, cap, shift, nb,
+            k_rs_onesweep<false><<<ntiles, RS_T, 0, s>>>(ks, vin, kd, vd, nullptr, nullptr, np, cap, shift, nb,
                                                          (drop_inert && pass == 0) ? 1 : 0, gbase + pass * RS_BINS,
                                                          rs.status, epoch, pass, tctr + pass);
         if ((*err = cudaGetLastError()) != cudaSuccess) return pass;
@@ -420,32 +443,35 @@ __device__ __forceinline__ int view_of_pair(const Launch& L, uint32_t q) {
     return lo;
 }
 
-// tiles covered by the i-th pair in depth order (0 past Q) → scanned into entry offsets
+// tiles covered by the i-th visible pair in depth order → scanned into entry offsets
 __global__ void k_pair_tiles(Launch L, const uint2* __restrict__ rect, int* __restrict__ ecount) {
     const int Q = (int)min((int64_t)L.counters[C_NVIS], L.cap_pairs);  // visible pairs (compacted by the sort)
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < L.cap_pairs; i += stride) {
-        int t = 0;
-        if (i < Q) {
-            const uint2 r = rect[i];
-            t = (int)(((r.y & 0xffff) - (r.x & 0xffff)) * ((r.y >> 16) - (r.x >> 16)));
-        }
-        ecount[i] = t;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < Q; i += stride) {
+        const uint2 r = rect[i];
+        ecount[i] = (int)(((r.y & 0xffff) - (r.x & 0xffff)) * ((r.y >> 16) - (r.x >> 16)));
     }
 }
 
 // Duplication in depth order: pair i's entries are ebase[i] + (row-major tile index
-// in its rect), key = view·T + tile.  A warp takes 32 consecutive pairs, whose
-// entries form one contiguous run, and writes them together: lane l handles
-// entries l, l+32, … of the run, finding its pair by a binary search over the
-// warp's inclusive tile-count prefix kept in shared memory, so consecutive lanes
-// write consecutive addresses.  The row/column split uses a float reciprocal of
-// the rect width (exact: (k + 0.5)/w for integers k < 2^20, w < 2^12 never
-// rounds across an integer).
+// in its rect), key = view·T + tile.  Work is balanced over ENTRIES, not pairs: the
+// depth order puts the nearest — largest — footprints first, so a warp owning 32
+// consecutive pairs could face 10^5 entries while its neighbours had a few (measured:
+// half the SMs idle for half of the kernel).  A warp takes a chunk of DUP_CH
+// consecutive entries, finds the pair holding its first entry with a 32-ary search
+// over the entry offsets, and walks the chunk's pairs 32 at a time: lanes load one
+// pair each, a warp scan of their in-chunk counts gives a contiguous run of entries,
+// and lane l writes entries l, l+32, … of the run (coalesced), finding its pair by a
+// binary search over the 32 inclusive prefixes in shared memory.  The row/column split
+// uses a float reciprocal of the rect width (exact: (k + 0.5)/w for integers k < 2^20,
+// w < 2^12 never rounds across an integer).
+constexpr int DUP_CH = 1024;
+
 struct DupDesc {  // one pair of the warp's 32
-    int x0, y0, w, excl;
+    int x0, y0, w, excl;  // rect origin and width, exclusive prefix of in-chunk counts
     float inv_w;
-    uint32_t vb, q, pad;
+    uint32_t vb, q;       // view·T, pair slot
+    int off0;             // pair-local index of the pair's first in-chunk entry
 };
 
 __global__ __launch_bounds__(256) void k_dup(Launch L, const uint32_t* __restrict__ order,
@@ -453,70 +479,123 @@ __global__ __launch_bounds__(256) void k_dup(Launch L, const uint32_t* __restric
     __shared__ int pref[8][32];
     __shared__ DupDesc desc[8][32];
     const int Q = (int)min((int64_t)L.counters[C_NVIS], L.cap_pairs);  // visible pairs (compacted by the sort)
+    const int64_t Kall = L.counters[C_K];
+    const int Kw = (int)min(Kall, L.cap_entries);  // entries written (the rest is a capacity overflow)
+    if (blockIdx.x == 0 && threadIdx.x == 0 && Kall > L.cap_entries) L.counters[C_OVERFLOW] = 1;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
-    for (int64_t w0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + wid) * 32; w0 < Q; w0 += nwarps * 32) {
-        const int64_t i = w0 + lane;
-        uint2 r = make_uint2(0u, 0u);
-        uint32_t q = 0;
-        if (i < Q) {
-            r = rect[i];
-            q = order[i];
+    const int nwarps = gridDim.x * (blockDim.x >> 5);
+    const int nchunks = (Kw + DUP_CH - 1) / DUP_CH;
+    for (int c = blockIdx.x * (blockDim.x >> 5) + wid; c < nchunks; c += nwarps) {
+        const int e0 = c * DUP_CH, e1 = min(e0 + DUP_CH, Kw);
+        // largest i < Q with ebase[i] ≤ e0 (ebase[Q] = K > e0): 32-ary search
+        int lo = 0, hi = Q;
+        while (hi - lo > 1) {
+            const int step = (hi - lo + 31) >> 5;
+            const int p = lo + lane * step;
+            const unsigned bal = __ballot_sync(FULLS, p < hi && ebase[p] <= e0);
+            lo += (31 - __clz(bal)) * step;  // lane 0 probes lo itself: bal ≠ 0
+            hi = min(hi, lo + step);
         }
-        const int rx0 = r.x & 0xffff, ry0 = r.x >> 16, rx1 = r.y & 0xffff, ry1 = r.y >> 16;
-        const int w = rx1 - rx0;
-        const int cnt = (rx1 > rx0 && ry1 > ry0) ? w * (ry1 - ry0) : 0;
-        int inc = cnt;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int y = __shfl_up_sync(FULLS, inc, o);
-            if (lane >= o) inc += y;
-        }
-        const int total = __shfl_sync(FULLS, inc, 31);
-        const int64_t e0 = __shfl_sync(FULLS, (int64_t)(i < Q ? ebase[i] : 0), 0);
-        pref[wid][lane] = inc;
-        DupDesc d;
-        d.x0 = rx0;
-        d.y0 = ry0;
-        d.w = w;
-        d.excl = inc - cnt;
-        d.inv_w = cnt > 0 ? 1.0f / (float)w : 0.f;
-        d.vb = cnt > 0 ? (uint32_t)view_of_pair(L, q) * (uint32_t)L.T : 0u;
-        d.q = q;
-        d.pad = 0;
-        desc[wid][lane] = d;
-        __syncwarp();
-        for (int k = lane; k < total; k += 32) {
-            int lo = 0;  // owner = number of lanes whose inclusive prefix is ≤ k
-#pragma unroll
-            for (int step = 16; step > 0; step >>= 1)
-                if (pref[wid][lo + step - 1] <= k) lo += step;
-            const DupDesc& o = desc[wid][lo];
-            const int loc = k - o.excl;
-            const int row = __float2int_rz(((float)loc + 0.5f) * o.inv_w);
-            const int col = loc - row * o.w;
-            const int64_t e = e0 + k;
-            if (e < L.cap_entries) {
-                L.key[e] = o.vb + (o.y0 + row) * L.TX + o.x0 + col;
-                L.val[e] = o.q;
-            } else {
-                L.counters[C_OVERFLOW] = 1;
+        for (int i0 = lo; i0 < Q;) {
+            const int i = i0 + lane;
+            uint2 r = make_uint2(0u, 0u);
+            uint32_t q = 0;
+            int eb = Kw, en = Kw;
+            if (i < Q) {
+                r = rect[i];
+                q = order[i];
+                eb = ebase[i];
+                en = ebase[i + 1];
             }
+            const int s0 = max(eb, e0), s1 = min(en, e1);
+            const int cnt = max(0, s1 - s0);
+            int inc = cnt;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(FULLS, inc, o);
+                if (lane >= o) inc += y;
+            }
+            const int total = __shfl_sync(FULLS, inc, 31);
+            const int ebeg = __shfl_sync(FULLS, s0, 0);  // the run's first entry
+            const int enext = __shfl_sync(FULLS, en, 31);  // first entry after these 32 pairs
+            const int rx0 = r.x & 0xffff, ry0 = r.x >> 16, rx1 = r.y & 0xffff;
+            const int w = rx1 - rx0;
+            pref[wid][lane] = inc;
+            DupDesc d;
+            d.x0 = rx0;
+            d.y0 = ry0;
+            d.w = w;
+            d.excl = inc - cnt;
+            d.inv_w = cnt > 0 ? 1.0f / (float)w : 0.f;
+            d.vb = cnt > 0 ? (uint32_t)view_of_pair(L, q) * (uint32_t)L.T : 0u;
+            d.q = q;
+            d.off0 = s0 - eb;
+            desc[wid][lane] = d;
+            __syncwarp();
+            for (int k = lane; k < total; k += 32) {
+                int o = 0;  // owner = number of lanes whose inclusive prefix is ≤ k
+#pragma unroll
+                for (int step = 16; step > 0; step >>= 1)
+                    if (pref[wid][o + step - 1] <= k) o += step;
+                const DupDesc& od = desc[wid][o];
+                const int loc = od.off0 + (k - od.excl);
+                const int row = __float2int_rz(((float)loc + 0.5f) * od.inv_w);
+                const int col = loc - row * od.w;
+                const int e = ebeg + k;
+                L.key[e] = od.vb + (od.y0 + row) * L.TX + od.x0 + col;
+                L.val[e] = od.q;
+            }
+            __syncwarp();
+            if (enext >= e1) break;  // warp-uniform
+            i0 += 32;
         }
-        __syncwarp();
     }
 }
 
-// S5 ranges from the sorted bucket keys: bucket b = [off[b], off[b+1]).  Entry e
-// opens every bucket in (key[e−1], key[e]]; the end closes the rest.
-__global__ void k_ranges(Launch L, const uint32_t* __restrict__ keys) {
-    const int64_t K = min((int64_t)L.counters[C_K], L.cap_entries);
-    const int64_t nb = (int64_t)L.V * L.T;
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e <= K; e += stride) {
-        const int64_t hi = e < K ? (int64_t)keys[e] : nb;           // buckets up to hi start at e
-        const int64_t lo = e > 0 ? (int64_t)keys[e - 1] + 1 : 0;    // first bucket not yet opened
-        for (int64_t b = lo; b <= hi; b++) L.bucket_off[b] = (int)e;
+// Closes the ranges written by the last entry-sort pass: off[nb] = K, and an empty bucket
+// (still INT_MAX) starts where the next one does — a suffix minimum over the V·T buckets,
+// one CTA.  Also records the longest bucket (statistics).
+constexpr int RC_T = 1024;
+__global__ __launch_bounds__(RC_T) void k_ranges_close(Launch L) {
+    __shared__ int wmin[RC_T / 32];
+    __shared__ int wmax[RC_T / 32];
+    const int K = (int)min((int64_t)L.counters[C_K], L.cap_entries);
+    const int nb = L.V * L.T;
+    const int per = (nb + RC_T - 1) / RC_T;
+    const int lo = min(nb, (int)threadIdx.x * per), hi = min(nb, lo + per);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    // this thread's chunk minimum, then an exclusive suffix-min over later threads
+    int m = K;
+    for (int b = lo; b < hi; b++) m = min(m, L.bucket_off[b]);
+    int inc = m;  // inclusive suffix min within the warp (lanes ≥ this one)
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_down_sync(FULLS, inc, o);
+        if (lane + o < 32) inc = min(inc, y);
+    }
+    if (lane == 0) wmin[warp] = inc;
+    __syncthreads();
+    int after = K;  // min over all later threads
+    for (int w = warp + 1; w < RC_T / 32; w++) after = min(after, wmin[w]);
+    const int nxt = __shfl_down_sync(FULLS, inc, 1);
+    if (lane < 31) after = min(after, nxt);
+    int mx = 0;
+    int cur = after;  // start of the next bucket
+    for (int b = hi - 1; b >= lo; b--) {
+        const int o = min(L.bucket_off[b], cur);
+        L.bucket_off[b] = o;
+        mx = max(mx, cur - o);
+        cur = o;
+    }
+    if (threadIdx.x == 0) L.bucket_off[nb] = K;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(FULLS, mx, o));
+    if (lane == 0) wmax[warp] = mx;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int t = 0;
+        for (int w = 0; w < RC_T / 32; w++) t = max(t, wmax[w]);
+        atomicMax(&L.counters[C_MAXB], t);
     }
 }
 
@@ -531,12 +610,12 @@ __global__ void k_max_bucket(Launch L) {
 }
 
 
-// S4a: pairs by depth, carrying each pair's packed tile rect.  pkey/pval/prect were
-// written by k_project; the depth order and the rects in that order → *order_out, *rect_out.
+// S4a: pairs by depth, carrying each pair's packed tile rect.  pkey/prect were written
+// by k_project (the values start as the pair slots themselves); the depth order and the rects in that order → *order_out, *rect_out.
 cudaError_t launch_sort_pairs(const Launch& L, const uint32_t** order_out, const uint2** rect_out, cudaStream_t s) {
     cudaError_t e;
     int np = radix_sort(L.pkey, L.pval, L.pkey2, L.pval2, L.prect, L.prect2, L.counters + C_Q, L.counters + C_NVIS,
-                        L.cap_pairs, 32, true, L.rs, s, &e);
+                        L.cap_pairs, 32, true, true, L.rs, s, &e);
     *order_out = (np & 1) ? L.pval2 : L.pval;
     *rect_out = (np & 1) ? L.prect2 : L.prect;
     return e;
@@ -545,9 +624,16 @@ cudaError_t launch_sort_pairs(const Launch& L, const uint32_t** order_out, const
 // S3: duplicate in depth order (entry offsets from a scan of the tile counts).
 cudaError_t launch_dup_sort(const Launch& L, const uint32_t* order, const uint2* rect, cudaStream_t s) {
     k_pair_tiles<<<grid_for(L.cap_pairs, 256), 256, 0, s>>>(L, rect, L.ecount);
-    cudaError_t e = scan_exclusive(L.ecount, (int)L.cap_pairs, L.counters + C_K, L.scan_tmp, s);  // K
+    cudaError_t e = scan_exclusive(L.ecount, (int)L.cap_pairs, L.counters + C_K, L.scan_tmp, s,
+                                   L.counters + C_NVIS);  // entry offsets of the visible pairs; K
     if (e != cudaSuccess) return e;
-    k_dup<<<grid_for(L.cap_pairs, 256), 256, 0, s>>>(L, order, rect, L.ecount);
+    {  // one full wave of resident CTAs; chunks are grid-strided over warps
+        int dev = 0, nsm = 148, per = 1;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_dup, 256, 0);
+        k_dup<<<nsm * max(per, 1), 256, 0, s>>>(L, order, rect, L.ecount);
+    }
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     return cudaSuccess;
 }
@@ -556,12 +642,13 @@ cudaError_t launch_sort_entries(const Launch& L, uint32_t** sorted_vals, cudaStr
     int bits = 1;
     while ((1ll << bits) < (int64_t)L.V * L.T) bits++;
     cudaError_t e;
+    // bucket starts come out of the last pass (atomicMin): fill with INT_MAX first
+    if ((e = cudaMemsetAsync(L.bucket_off, 0x7f, sizeof(int) * ((size_t)L.V * L.T + 1), s)) != cudaSuccess) return e;
     int np = radix_sort_3k(L.key, L.val, L.key2, L.val2, nullptr, nullptr, L.counters + C_K, L.cap_entries, bits,
-                           L.rs_counts, L.scan_tmp, s, &e);
+                           L.rs_counts, L.scan_tmp, s, &e, L.bucket_off);
     *sorted_vals = (np & 1) ? L.val2 : L.val;
     if (e != cudaSuccess) return e;
-    k_ranges<<<grid_for(L.cap_entries + 1, 256), 256, 0, s>>>(L, (np & 1) ? L.key2 : L.key);
-    k_max_bucket<<<64, 256, 0, s>>>(L);
+    k_ranges_close<<<1, RC_T, 0, s>>>(L);
     return cudaGetLastError();
 }
 

@@ -50,18 +50,17 @@ cudaError_t grow(T*& p, int64_t& cap, int64_t need, int64_t elem_per = 1) {
 }
 
 cudaError_t alloc_pairs(mvgs_ctx* c, int64_t n) {
-    cudaFree(c->d_rec); cudaFree(c->d_meta); cudaFree(c->d_pgrad);
+    cudaFree(c->d_rec); cudaFree(c->d_pgrad);
     cudaFree(c->d_pkey); cudaFree(c->d_pval); cudaFree(c->d_pkey2); cudaFree(c->d_pval2); cudaFree(c->d_ecount);
     cudaFree(c->d_prect); cudaFree(c->d_prect2); cudaFree(c->d_pflag);
     c->d_prect = c->d_prect2 = nullptr;
     c->d_pflag = nullptr;
-    c->d_rec = nullptr; c->d_meta = nullptr; c->d_pgrad = nullptr;
+    c->d_rec = nullptr; c->d_pgrad = nullptr;
     c->d_pkey = c->d_pval = c->d_pkey2 = c->d_pval2 = nullptr;
     c->d_ecount = nullptr;
     c->cap_pairs = 0;
     cudaError_t e;
     if ((e = cudaMalloc(&c->d_rec, sizeof(float4) * REC_F4 * n)) != cudaSuccess) return e;
-    if ((e = cudaMalloc(&c->d_meta, sizeof(PairMeta) * n)) != cudaSuccess) return e;
     if ((e = cudaMalloc(&c->d_pgrad, sizeof(float) * PG_STRIDE * n)) != cudaSuccess) return e;
     if ((e = cudaMalloc(&c->d_pkey, 4 * n)) != cudaSuccess) return e;
     if ((e = cudaMalloc(&c->d_pval, 4 * n)) != cudaSuccess) return e;
@@ -167,7 +166,6 @@ void fill_launch(mvgs_ctx* c) {
     L.blk_off = c->d_blk;
     L.bucket_off = c->d_bucket;
     L.rec = c->d_rec;
-    L.meta = c->d_meta;
     L.pflag = c->d_pflag;
     L.pgrad = c->d_pgrad;
     L.key = c->d_key;
@@ -229,7 +227,7 @@ void mvgs_destroy(mvgs_ctx* ctx) {
     cudaSetDevice(ctx->device);
     cudaDeviceSynchronize();
     cudaFree(ctx->d_cams); cudaFree(ctx->d_blk); cudaFree(ctx->d_bucket);
-    cudaFree(ctx->d_rec); cudaFree(ctx->d_meta); cudaFree(ctx->d_pgrad);
+    cudaFree(ctx->d_rec); cudaFree(ctx->d_pgrad);
     cudaFree(ctx->d_key); cudaFree(ctx->d_val); cudaFree(ctx->d_key2); cudaFree(ctx->d_val2);
     cudaFree(ctx->d_pkey); cudaFree(ctx->d_pval); cudaFree(ctx->d_pkey2); cudaFree(ctx->d_pval2);
     cudaFree(ctx->d_ecount); cudaFree(ctx->d_rs); cudaFree(ctx->d_rs_status); cudaFree(ctx->d_rs_small); cudaFree(ctx->d_prect); cudaFree(ctx->d_prect2);
