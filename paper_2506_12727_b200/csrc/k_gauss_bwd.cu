@@ -25,6 +25,19 @@ __constant__ float g_SH3[7] = {-0.5900435899266435f, 2.890611442640554f, -0.4570
                                0.3731763325901154f, -0.4570457994644658f, 1.445305721320277f,
                                -0.5900435899266435f};
 
+// Hardware approximations for values that decide nothing: MUFU.RCP /
+// MUFU.SQRT (≤ 2 ulp) instead of the multi-instruction IEEE sequences.
+__device__ __forceinline__ float g_rcp(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ float g_sqrt(float x) {
+    float y;
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
 // Values-only recomputation for the chain rule (no decision depends on them: the
 // Jacobian clamps come from the pair flags written by k_project), so fast
 // reciprocal / exp / rsqrt are used instead of the canonical arithmetic.
@@ -34,7 +47,7 @@ struct FastActiv {
 
 __device__ __forceinline__ void fast_activate(const float* __restrict__ ls, const float* __restrict__ qr, float logit,
                                               FastActiv& a) {
-    a.o = 1.f / (1.f + __expf(-logit));
+    a.o = g_rcp(1.f + __expf(-logit));
     a.s[0] = __expf(ls[0]);
     a.s[1] = __expf(ls[1]);
     a.s[2] = __expf(ls[2]);
@@ -70,9 +83,9 @@ __device__ __forceinline__ void fast_project(const mvgs_camera& cam, float mx, f
     p.tx = R[0] * mx + R[1] * my + R[2] * mz + cam.t[0];
     p.ty = R[3] * mx + R[4] * my + R[5] * mz + cam.t[1];
     p.tz = R[6] * mx + R[7] * my + R[8] * mz + cam.t[2];
-    p.itz = __frcp_rn(p.tz);
+    p.itz = g_rcp(p.tz);
     const float ux = p.tx * p.itz, uy = p.ty * p.itz;
-    const float limx = 0.65f * (float)cam.width / cam.fx, limy = 0.65f * (float)cam.height / cam.fy;
+    const float limx = 0.65f * (float)cam.width * g_rcp(cam.fx), limy = 0.65f * (float)cam.height * g_rcp(cam.fy);
     p.uxc = (flags & 8u) ? fminf(limx, fmaxf(-limx, ux)) : ux;   // clamp decisions from k_project (R4)
     p.uyc = (flags & 16u) ? fminf(limy, fmaxf(-limy, uy)) : uy;
     const float J00 = cam.fx * p.itz, J02 = -cam.fx * p.uxc * p.itz;
@@ -106,6 +119,10 @@ struct ShRows {
     static constexpr int NS4 = (NS + 3) / 4;  // float4 per row
     static constexpr int STRIDE = 4 * (NS4 | 1);
 };
+
+#ifndef GB_VB
+#define GB_VB 2  // views whose pair loads are issued together (4: more loads in flight, more spills)
+#endif
 
 template <int D>
 __global__ __launch_bounds__(BLK, 2) void k_gauss_bwd(Launch L, mvgs_grads gr, mvgs_adc adc) {
@@ -177,12 +194,12 @@ __global__ __launch_bounds__(BLK, 2) void k_gauss_bwd(Launch L, mvgs_grads gr, m
             }
         }
         __syncthreads();
-        for (int k0 = 0; k0 < nv; k0 += 4) {
-            // issue the loads of up to 4 views first (memory-level parallelism), then the math
-            uint32_t fl[4];
-            float4 pga[4], pgb[4], pgc[4];
+        for (int k0 = 0; k0 < nv; k0 += GB_VB) {
+            // issue the loads of up to GB_VB views first (memory-level parallelism), then the math
+            uint32_t fl[GB_VB];
+            float4 pga[GB_VB], pgb[GB_VB], pgc[GB_VB];
 #pragma unroll
-            for (int u = 0; u < 4; u++) {
+            for (int u = 0; u < GB_VB; u++) {
                 fl[u] = 0u;
                 const int k = k0 + u;
                 if (k >= nv) continue;  // warp-uniform
@@ -206,7 +223,7 @@ __global__ __launch_bounds__(BLK, 2) void k_gauss_bwd(Launch L, mvgs_grads gr, m
                 sh_ready = true;
             }
 #pragma unroll
-            for (int u = 0; u < 4; u++) {
+            for (int u = 0; u < GB_VB; u++) {
             if (!(fl[u] & PF_VISIBLE)) continue;  // not participating, or tiles == 0: inert (R27)
             const mvgs_camera& c = L.cams[v0 + k0 + u];
             const uint32_t flags = fl[u];
@@ -214,7 +231,7 @@ __global__ __launch_bounds__(BLK, 2) void k_gauss_bwd(Launch L, mvgs_grads gr, m
             // pg: (Σ∇x, Σ∇y, e1, ∂A) (∂B, ∂C, ∂o, ∂r) (∂g, ∂b, -, -)
             nvis += 1.f;
             e1 += pg0.z;
-            e2 += sqrtf(pg0.x * pg0.x + pg0.y * pg0.y);
+            e2 += g_sqrt(pg0.x * pg0.x + pg0.y * pg0.y);
             gsx += pg0.x;
             gsy += pg0.y;
             dop += pg1.z;
@@ -228,7 +245,7 @@ __global__ __launch_bounds__(BLK, 2) void k_gauss_bwd(Launch L, mvgs_grads gr, m
             float dtz = -(c.fx * p.tx * itz2) * dpx - (c.fy * p.ty * itz2) * dpy;
             // conic (A,B,C) = (c,−b,a)/det → Σ' entries (a,b,c)
             const float dA = pg0.w, dB = pg1.x, dC = pg1.y;
-            const float id2 = __frcp_rn(p.det * p.det);
+            const float id2 = g_rcp(p.det * p.det);
             const float da = (-p.c * p.c * dA + p.b * p.c * dB - p.b * p.b * dC) * id2;
             const float dc = (-p.b * p.b * dA + p.a * p.b * dB - p.a * p.a * dC) * id2;
             const float db = (2.f * p.b * p.c * dA - (p.det + 2.f * p.b * p.b) * dB + 2.f * p.a * p.b * dC) * id2;
@@ -290,7 +307,7 @@ __global__ __launch_bounds__(BLK, 2) void k_gauss_bwd(Launch L, mvgs_grads gr, m
             const float cpy = -(R[1] * c.t[0] + R[4] * c.t[1] + R[7] * c.t[2]);
             const float cpz = -(R[2] * c.t[0] + R[5] * c.t[1] + R[8] * c.t[2]);
             float x = mx - cpx, y = my - cpy, z = mz - cpz;
-            const float dn = sqrtf(x * x + y * y + z * z), idn = 1.f / dn;
+            const float idn = rsqrtf(x * x + y * y + z * z);
             x *= idn; y *= idn; z *= idn;
             float wk[NK];  // Σ_c sh[k][c]·∂L/∂rgb_c, read as float4 chunks of the row
 #pragma unroll
@@ -380,7 +397,14 @@ __global__ __launch_bounds__(BLK, 2) void k_gauss_bwd(Launch L, mvgs_grads gr, m
         const int nb = (int)min((int64_t)BLK, L.P - g0);
         float* dst = gr.d_sh + g0 * (int64_t)L.sh_stride * 3;
         const int rowlen = L.sh_stride * 3;
-        if (rowlen == NS) {  // rows hold exactly the active coefficients: constant divisor
+        if (rowlen == NS && (NS & 3) == 0 && ((uintptr_t)dst & 15) == 0) {  // float4 rows, constant divisor
+            constexpr int NS4 = NS / 4;
+            float4* dst4 = reinterpret_cast<float4*>(dst);
+            for (int i = threadIdx.x; i < nb * NS4; i += BLK) {
+                const int r = i / NS4, k4 = i - r * NS4;
+                dst4[i] = *reinterpret_cast<const float4*>(&dsh_s[r * SS + 4 * k4]);
+            }
+        } else if (rowlen == NS) {  // rows hold exactly the active coefficients: constant divisor
             for (int i = threadIdx.x; i < nb * NS; i += BLK) {
                 const int r = i / NS, k = i - r * NS;
                 dst[i] = dsh_s[r * SS + k];

@@ -61,6 +61,47 @@ __device__ __forceinline__ void pixel_pair(int tx, int ty, int& x, int& y0, int&
     y1 = y0 + 2;
 }
 
+// Exact warp-block culling.  A pixel can pass the skip test only if
+// power ≥ sb, i.e. inside the ellipse dᵀMd ≤ L = −2·sb, M = [[A, B], [B, C]]; that
+// ellipse lies in the box |dx| ≤ √(L·C/det), |dy| ≤ √(L·A/det).  An entry whose box
+// (inflated by 1 % + 0.01 in L and 0.01 px) misses a warp's 16×4 pixel block is never
+// evaluated by that warp.  The margins must also cover the fp32 rounding of the CA
+// power that takes the real decision: with B² ≤ 0.9·A·C the power's terms are within
+// 40× of dᵀMd near the ellipse, so its rounding error (≲ 1e-4) is far below the slack;
+// more correlated (near-degenerate) conics, L ≤ 0.01 and det ≤ 0 are never culled.
+// Bit j of the result: the entry may touch warp j's rows 4j … 4j+3 of the tile.
+__device__ __forceinline__ unsigned warp_block_mask(float px, float py, float A, float B, float C, float sb,
+                                                    float X0, float Y0) {
+    const float L = -2.0f * sb;
+    const double det = (double)A * (double)C - (double)B * (double)B;
+    if (!(L > 0.01f) || !(det > 0.0) || (double)B * (double)B > 0.9 * (double)A * (double)C) return 0xfu;
+    const double Lm = (double)L * 1.01 + 0.01;
+    const float hx = (float)sqrt(Lm * (double)C / det) + 0.01f;
+    const float hy = (float)sqrt(Lm * (double)A / det) + 0.01f;
+    if (!(px + hx >= X0 && px - hx <= X0 + 15.0f)) return 0u;
+    unsigned m = 0;
+#pragma unroll
+    for (int w = 0; w < 4; w++) {
+        const float ylo = Y0 + 4.0f * w, yhi = ylo + 3.0f;
+        if (py + hy >= ylo && py - hy <= yhi) m |= 1u << w;
+    }
+    return m;
+}
+
+// Per-warp compacted batch: the indices j < cnt whose mask has this warp's bit, ascending.
+__device__ __forceinline__ int warp_batch_list(const uint8_t* smask, int cnt, int warp, int lane, uint8_t* list) {
+    int n = 0;
+    for (int c = 0; c < cnt; c += 32) {
+        const int j = c + lane;
+        const bool in = j < cnt && ((smask[j] >> warp) & 1u);
+        const unsigned bal = __ballot_sync(0xffffffffu, in);
+        if (in) list[n + __popc(bal & ((1u << lane) - 1u))] = (uint8_t)j;
+        n += __popc(bal);
+    }
+    __syncwarp();
+    return n;
+}
+
 // stage one record: (x, y, A, B) (C, o, skip bound, -) (r, g, b, depth)
 __device__ __forceinline__ void stage(const Launch& L, uint32_t q, float4* s0, float4* s1, float4* s2, int i) {
     const float4* r = L.rec + 3 * (int64_t)q;
@@ -192,6 +233,8 @@ __global__ __launch_bounds__(RT) void k_render_fwd_p(Launch L, float* __restrict
                                                      float* __restrict__ out_T, int32_t* __restrict__ out_n,
                                                      float* __restrict__ out_D) {
     __shared__ FwdConsts sf[RT];
+    __shared__ uint8_t smask[RT];
+    __shared__ uint8_t slist[RT / 32][RT];
     __shared__ unsigned sev[2];
     zero_pgrad_slice(L);
     const int bucket = blockIdx.x;
@@ -224,10 +267,15 @@ __global__ __launch_bounds__(RT) void k_render_fwd_p(Launch L, float* __restrict
                 k.gb = make_float4(r1.w, r1.w, r2.x, r2.x);
                 k.dd = ff2(r2.y, r2.y);
                 sf[threadIdx.x] = k;
+                smask[threadIdx.x] = (uint8_t)warp_block_mask(r0.x, r0.y, r0.z, r0.w, r1.x, sb, (float)(tx * TILE),
+                                                              (float)(ty * TILE));
             }
             __syncthreads();
             const int cnt = min(RT, end - b0);
-            for (int j = 0; j < cnt && !(done0 && done1); j++) {
+            const int wl = threadIdx.x >> 5;
+            const int nl = warp_batch_list(smask, cnt, wl, threadIdx.x & 31, slist[wl]);
+            for (int u = 0; u < nl && !(done0 && done1); u++) {
+                const int j = slist[wl][u];
                 nev += (unsigned)!done0 + (unsigned)!done1;
                 const float4 xy = sf[j].xy, ab = sf[j].ab, cs = sf[j].cs;
                 const float2 dx = __fadd2_rn(ff2(xy.x, xy.y), nfx);
@@ -541,7 +589,7 @@ __device__ __forceinline__ void bwd_exp(float power, float o, float& G, float& o
     }
 }
 
-__global__ __launch_bounds__(128) void k_render_bwd_p(Launch L, const float* __restrict__ dL_drgb,
+__global__ __launch_bounds__(128, 6) void k_render_bwd_p(Launch L, const float* __restrict__ dL_drgb,
                                                       const float* __restrict__ in_T,
                                                       const int32_t* __restrict__ in_n) {
     constexpr int NT = 128, NW = 4, RB = 128;
@@ -550,6 +598,8 @@ __global__ __launch_bounds__(128) void k_render_bwd_p(Launch L, const float* __r
     __shared__ __align__(16) float sacc[NW][RB * NG];
     __shared__ int smax;
     __shared__ unsigned sev[2];
+    __shared__ uint8_t smask[RB];
+    __shared__ uint8_t slist[NW][RB];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int bucket = blockIdx.x;
     const int v = bucket / L.T, tile = bucket - v * L.T;
@@ -576,7 +626,6 @@ __global__ __launch_bounds__(128) void k_render_bwd_p(Launch L, const float* __r
             Tfin[p] = in_T[v * HW + pix];
             last[p] = in_n[v * HW + pix];
         }
-        nev += (unsigned)last[p];
     }
     const float2 dLr = f2(dL[0][0], dL[1][0]), dLg = f2(dL[0][1], dL[1][1]), dLb = f2(dL[0][2], dL[1][2]);
     // −T_final·(∂L/∂C · bg): the background term of ∂L/∂α, scaled by 1/(1 − α) per entry
@@ -622,14 +671,19 @@ __global__ __launch_bounds__(128) void k_render_bwd_p(Launch L, const float* __r
             k.rg = make_float4(r1.z, r1.z, r1.w, r1.w);
             k.bb = f2(r2.x, r2.x);
             sc[t] = k;
+            smask[t] = (uint8_t)warp_block_mask(r0.x, r0.y, r0.z, r0.w, r1.x, sb, (float)(tx * TILE), (float)(ty * TILE));
         }
         {
             float4* w4 = reinterpret_cast<float4*>(wacc);
             for (int i = lane; i < RB * NG / 4; i += 32) w4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
         }
         __syncthreads();
-        for (int jj = min(cnt, wmax - b0) - 1; jj >= 0; jj--) {
+        // this warp's entries of the batch (culled by its pixel block), walked back to front
+        const int nl = warp_batch_list(smask, min(cnt, wmax - b0), warp, lane, slist[warp]);
+        for (int u = nl - 1; u >= 0; u--) {
+            const int jj = slist[warp][u];
             const int j = b0 + jj;
+            nev += (unsigned)(j < last[0]) + (unsigned)(j < last[1]);
             const float4 xy = sc[jj].xy, ab = sc[jj].ab, cnb = sc[jj].cnb, os = sc[jj].os;
             const float2 dx = __fadd2_rn(f2(xy.x, xy.y), nfx);
             const float2 dy = __fadd2_rn(f2(xy.z, xy.w), nfy);

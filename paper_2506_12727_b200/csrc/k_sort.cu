@@ -62,10 +62,11 @@ __device__ __forceinline__ uint32_t block_excl_scan_256_u(uint32_t x, uint32_t* 
 // Warp multisplit ranking: lanes holding the same digit found with 8 ballots
 // (one per digit bit) instead of __match_any_sync, whose cost grows with the
 // number of distinct digits in the warp.
-__device__ __forceinline__ unsigned digit_peers(uint32_t d, bool ok) {
+__device__ __forceinline__ unsigned digit_peers(uint32_t d, bool ok, int nbits) {
     unsigned peers = __ballot_sync(FULLS, ok);
 #pragma unroll
     for (int b = 0; b < 8; b++) {
+        if (b >= nbits) break;  // uniform: a 7-bit pass needs 7 ballots
         const bool bit = (d >> b) & 1u;
         const unsigned bal = __ballot_sync(FULLS, bit);
         peers &= bit ? bal : ~bal;
@@ -130,7 +131,7 @@ __global__ __launch_bounds__(RS_T) void k_rs_scatter(const uint32_t* __restrict_
         const int p = warp * 32 * RS_IPT + it * 32 + lane;
         const bool ok = p < nt;
         const uint32_t d = (key[it] >> shift) & mask;
-        const unsigned peers = digit_peers(d, ok);
+        const unsigned peers = digit_peers(d, ok, nbits);
         const uint32_t before = ok ? hist[warp][d] : 0u;
         loc[it] = before + __popc(peers & lt);
         __syncwarp();
@@ -326,7 +327,7 @@ __global__ __launch_bounds__(RS_T) void k_rs_onesweep(const uint32_t* __restrict
         const int p = warp * 32 * RS_IPT + it * 32 + lane;
         const bool ok = p < nt && !(drop_inert && key[it] == INERT);
         const uint32_t d = (key[it] >> shift) & mask;
-        const unsigned peers = digit_peers(d, ok);
+        const unsigned peers = digit_peers(d, ok, nbits);
         const uint32_t before = ok ? hist[warp][d] : 0u;
         loc[it] = ok ? before + __popc(peers & lt) : 0xffffffffu;
         __syncwarp();
