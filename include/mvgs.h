@@ -304,6 +304,14 @@ mvgs_status mvgs_render_bwd_partial(mvgs_ctx *ctx, const int32_t *pix, int32_t S
 mvgs_status mvgs_set_timing(mvgs_ctx *ctx, int enable);
 int mvgs_stage_times(mvgs_ctx *ctx, float *ms, int n);
 
+/* Evaluation counting (statistics).  While enabled (the default), the full-image
+ * compositing kernels count their (pixel, entry) evaluations and canonical-exp
+ * evaluations; mvgs_query reports them (eval_fwd, eval_bwd, exp_fwd, exp_bwd) for
+ * the last preprocess → fwd → bwd sequence.  Disabling it removes the counting
+ * from the kernels' inner loops (the counts then read 0); results are unchanged.
+ * Returns MVGS_ERR_INVALID for a NULL ctx. */
+mvgs_status mvgs_set_eval_counting(mvgs_ctx *ctx, int enable);
+
 #ifdef __cplusplus
 }
 #endif

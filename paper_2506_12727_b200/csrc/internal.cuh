@@ -28,6 +28,7 @@ struct Launch {  // everything a kernel needs about the current batch
     int64_t P;
     int V, W, H, TX, TY, T, NB;
     int sh_degree, sh_stride;
+    int count_evals;  // compositing kernels count (pixel, entry) evaluations (statistics)
     float bg[3];
     const mvgs_camera* cams;  // device [V]
     const float *means, *log_scales, *quats, *opac, *sh;
@@ -113,6 +114,7 @@ struct mvgs_ctx {
     cudaEvent_t cams_ev = nullptr;
     cudaStream_t last_stream = nullptr;
     bool timing = false;
+    bool count_evals = true;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_rec[MVGS_NUM_STAGES];  // recorded since last read
     std::vector<cudaEvent_t> ev_pool;
     std::string err;

@@ -228,7 +228,7 @@ __device__ __forceinline__ float2 ca_exp_core2(float2 x) {
     return __fmul2_rn(p, sc);
 }
 
-template <bool DEPTH>
+template <bool DEPTH, bool CNT>
 __global__ __launch_bounds__(RT) void k_render_fwd_p(Launch L, float* __restrict__ out_rgb,
                                                      float* __restrict__ out_T, int32_t* __restrict__ out_n,
                                                      float* __restrict__ out_D) {
@@ -276,7 +276,7 @@ __global__ __launch_bounds__(RT) void k_render_fwd_p(Launch L, float* __restrict
             const int nl = warp_batch_list(smask, cnt, wl, threadIdx.x & 31, slist[wl]);
             for (int u = 0; u < nl && !(done0 && done1); u++) {
                 const int j = slist[wl][u];
-                nev += (unsigned)!done0 + (unsigned)!done1;
+                if (CNT) nev += (unsigned)!done0 + (unsigned)!done1;
                 const float4 xy = sf[j].xy, ab = sf[j].ab, cs = sf[j].cs;
                 const float2 dx = __fadd2_rn(ff2(xy.x, xy.y), nfx);
                 const float2 dy = __fadd2_rn(ff2(xy.z, xy.w), nfy);
@@ -288,7 +288,7 @@ __global__ __launch_bounds__(RT) void k_render_fwd_p(Launch L, float* __restrict
                 const bool in0 = !done0 && !(power.x > 0.f) && !(power.x < cs.z);
                 const bool in1 = !done1 && !(power.y > 0.f) && !(power.y < cs.z);
                 if (!(in0 || in1)) continue;
-                nexp += (unsigned)in0 + (unsigned)in1;
+                if (CNT) nexp += (unsigned)in0 + (unsigned)in1;
                 const float4 orr = sf[j].orr;
                 const float2 G = ca_exp_core2(power);
                 const float2 oG = __fmul2_rn(ff2(orr.x, orr.y), G);
@@ -313,7 +313,7 @@ __global__ __launch_bounds__(RT) void k_render_fwd_p(Launch L, float* __restrict
             }
         }
     }
-    count_evals(&L.counters64[0], &L.counters64[2], nev, nexp, sev);
+    if (CNT) count_evals(&L.counters64[0], &L.counters64[2], nev, nexp, sev);
     const int64_t HW = (int64_t)L.H * L.W;
     const float Cs[2][3] = {{C0.x, C1.x, C2.x}, {C0.y, C1.y, C2.y}};
     const float Ts[2] = {T.x, T.y}, Ds[2] = {D.x, D.y};
@@ -338,9 +338,11 @@ __global__ __launch_bounds__(RT) void k_render_fwd_p(Launch L, float* __restrict
 cudaError_t launch_render_fwd(const Launch& L, float* rgb, float* Tf, int32_t* nc, float* depth, cudaStream_t s) {
     if (MVGS_FWD_PACKED) {
         if (depth)
-            k_render_fwd_p<true><<<L.V * L.T, RT, 0, s>>>(L, rgb, Tf, nc, depth);
+            k_render_fwd_p<true, true><<<L.V * L.T, RT, 0, s>>>(L, rgb, Tf, nc, depth);
+        else if (L.count_evals)
+            k_render_fwd_p<false, true><<<L.V * L.T, RT, 0, s>>>(L, rgb, Tf, nc, nullptr);
         else
-            k_render_fwd_p<false><<<L.V * L.T, RT, 0, s>>>(L, rgb, Tf, nc, nullptr);
+            k_render_fwd_p<false, false><<<L.V * L.T, RT, 0, s>>>(L, rgb, Tf, nc, nullptr);
     } else if (depth) {
         k_render_fwd<true><<<L.V * L.T, RT, 0, s>>>(L, rgb, Tf, nc, depth);
     } else {
@@ -589,6 +591,7 @@ __device__ __forceinline__ void bwd_exp(float power, float o, float& G, float& o
     }
 }
 
+template <bool CNT>
 __global__ __launch_bounds__(128, 6) void k_render_bwd_p(Launch L, const float* __restrict__ dL_drgb,
                                                       const float* __restrict__ in_T,
                                                       const int32_t* __restrict__ in_n) {
@@ -683,7 +686,7 @@ __global__ __launch_bounds__(128, 6) void k_render_bwd_p(Launch L, const float* 
         for (int u = nl - 1; u >= 0; u--) {
             const int jj = slist[warp][u];
             const int j = b0 + jj;
-            nev += (unsigned)(j < last[0]) + (unsigned)(j < last[1]);
+            if (CNT) nev += (unsigned)(j < last[0]) + (unsigned)(j < last[1]);
             const float4 xy = sc[jj].xy, ab = sc[jj].ab, cnb = sc[jj].cnb, os = sc[jj].os;
             const float2 dx = __fadd2_rn(f2(xy.x, xy.y), nfx);
             const float2 dy = __fadd2_rn(f2(xy.z, xy.w), nfy);
@@ -696,7 +699,7 @@ __global__ __launch_bounds__(128, 6) void k_render_bwd_p(Launch L, const float* 
             const bool in0 = j < last[0] && !(power.x > 0.f) && !(power.x < os.z);
             const bool in1 = j < last[1] && !(power.y > 0.f) && !(power.y < os.z);
             if (!__any_sync(FULLR, in0 || in1)) continue;
-            nexp += (unsigned)in0 + (unsigned)in1;
+            if (CNT) nexp += (unsigned)in0 + (unsigned)in1;
             float G0, G1, oG0, oG1;
             bwd_exp(power.x, os.x, G0, oG0);
             bwd_exp(power.y, os.y, G1, oG1);
@@ -755,7 +758,7 @@ __global__ __launch_bounds__(128, 6) void k_render_bwd_p(Launch L, const float* 
             }
         }
     }
-    count_evals(&L.counters64[1], &L.counters64[3], nev, nexp, sev);
+    if (CNT) count_evals(&L.counters64[1], &L.counters64[3], nev, nexp, sev);
 }
 
 #ifndef MVGS_BWD_PACKED
@@ -768,7 +771,10 @@ __global__ __launch_bounds__(128, 6) void k_render_bwd_p(Launch L, const float* 
 
 cudaError_t launch_render_bwd(const Launch& L, const float* dL, const float* Tf, const int32_t* nc, cudaStream_t s) {
     if (MVGS_BWD_PACKED)
-        k_render_bwd_p<<<L.V * L.T, 128, 0, s>>>(L, dL, Tf, nc);
+        if (L.count_evals)
+            k_render_bwd_p<true><<<L.V * L.T, 128, 0, s>>>(L, dL, Tf, nc);
+        else
+            k_render_bwd_p<false><<<L.V * L.T, 128, 0, s>>>(L, dL, Tf, nc);
     else
         k_render_bwd<MVGS_BWD_NPX><<<L.V * L.T, 256 / MVGS_BWD_NPX, 0, s>>>(L, dL, Tf, nc);
     return cudaGetLastError();

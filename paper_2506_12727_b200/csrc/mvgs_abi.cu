@@ -321,6 +321,7 @@ mvgs_status mvgs_preprocess(mvgs_ctx* ctx, const mvgs_gaussians* g, const mvgs_c
     L.V = V; L.W = W; L.H = H; L.TX = TX; L.TY = TY; L.T = TX * TY; L.NB = NB;
     L.sh_degree = g->sh_degree;
     L.sh_stride = g->sh_stride;
+    L.count_evals = ctx->count_evals ? 1 : 0;
     for (int k = 0; k < 3; k++) L.bg[k] = bg ? bg[k] : 0.f;
     L.means = g->means; L.log_scales = g->log_scales; L.quats = g->quats; L.opac = g->opacity_logits; L.sh = g->sh;
     fill_launch(ctx);
@@ -487,6 +488,13 @@ mvgs_status mvgs_export_pairs(mvgs_ctx* ctx, int32_t* pair_ids, int32_t* pair_i,
 mvgs_status mvgs_set_timing(mvgs_ctx* ctx, int enable) {
     if (!ctx) return MVGS_ERR_INVALID;
     ctx->timing = enable != 0;
+    return MVGS_OK;
+}
+
+mvgs_status mvgs_set_eval_counting(mvgs_ctx* ctx, int enable) {
+    if (!ctx) return MVGS_ERR_INVALID;
+    ctx->count_evals = enable != 0;
+    ctx->L.count_evals = enable != 0;
     return MVGS_OK;
 }
 

@@ -20,7 +20,7 @@ NG = 10
 # the exported symbols include/mvgs.h declares (checked by tests/test_abi.py)
 SYMBOLS = ["mvgs_create", "mvgs_destroy", "mvgs_last_error", "mvgs_reserve", "mvgs_preprocess", "mvgs_render_fwd",
            "mvgs_render_bwd", "mvgs_adc_stats", "mvgs_query", "mvgs_export_lists", "mvgs_export_pairs",
-           "mvgs_set_timing", "mvgs_stage_times", "mvgs_render_fwd_partial", "mvgs_render_bwd_partial",
+           "mvgs_set_timing", "mvgs_stage_times", "mvgs_set_eval_counting", "mvgs_render_fwd_partial", "mvgs_render_bwd_partial",
            "mvgs_render_fwd_depth", "mvgs_dssim3d", "mvgs_adc_step", "mvgs_adc_remap",
            "mvgs_loss_grad", "mvgs_grad_moments", "mvgs_grad_variance"]
 PARTIAL_THREAD_EFFICIENT, PARTIAL_MASKED = 0, 1
@@ -98,6 +98,7 @@ def _load():
     L.mvgs_export_lists.argtypes = [vp, vp, vp, vp]
     L.mvgs_export_pairs.argtypes = [vp, vp, vp, vp, vp, vp]
     L.mvgs_set_timing.argtypes = [vp, C.c_int]
+    L.mvgs_set_eval_counting.argtypes = [vp, C.c_int]
     L.mvgs_render_fwd_partial.argtypes = [vp, vp, C.c_int32, C.c_int32, vp, vp, vp, vp]
     L.mvgs_render_bwd_partial.argtypes = [vp, vp, C.c_int32, C.c_int32, vp, vp, vp, vp]
     L.mvgs_dssim3d.argtypes = [vp, vp, C.c_int32, C.c_int32, C.c_int32, vp, vp, vp, vp, C.c_float, vp, vp, vp]
@@ -296,6 +297,10 @@ def export_pairs(ctx, pair_ids=None, pair_i=None, pair_f=None, pair_g=None, stre
 
 def set_timing(ctx, enable: bool):
     _check(ctx, _lib.mvgs_set_timing(ctx, int(bool(enable))))
+
+
+def set_eval_counting(ctx, enable: bool):
+    _check(ctx, _lib.mvgs_set_eval_counting(ctx, int(bool(enable))))
 
 
 def stage_times(ctx) -> dict:
