@@ -78,14 +78,13 @@ struct FastProj {
 };
 
 __device__ __forceinline__ void fast_project(const mvgs_camera& cam, float mx, float my, float mz, const float Sig[6],
-                                             uint32_t flags, FastProj& p) {
+                                             uint32_t flags, float limx, float limy, FastProj& p) {
     const float* R = cam.R;
     p.tx = R[0] * mx + R[1] * my + R[2] * mz + cam.t[0];
     p.ty = R[3] * mx + R[4] * my + R[5] * mz + cam.t[1];
     p.tz = R[6] * mx + R[7] * my + R[8] * mz + cam.t[2];
     p.itz = g_rcp(p.tz);
     const float ux = p.tx * p.itz, uy = p.ty * p.itz;
-    const float limx = 0.65f * (float)cam.width * g_rcp(cam.fx), limy = 0.65f * (float)cam.height * g_rcp(cam.fy);
     p.uxc = (flags & 8u) ? fminf(limx, fmaxf(-limx, ux)) : ux;   // clamp decisions from k_project (R4)
     p.uyc = (flags & 16u) ? fminf(limy, fmaxf(-limy, uy)) : uy;
     const float J00 = cam.fx * p.itz, J02 = -cam.fx * p.uxc * p.itz;
@@ -123,22 +122,32 @@ struct ShRows {
 #ifndef GB_VB
 #define GB_VB 2  // views whose pair loads are issued together (4: more loads in flight, more spills)
 #endif
+#ifndef GB_VB_SHG
+#define GB_VB_SHG 1  // the same for the 3-CTA variant (80 registers)
+#endif
 
-template <int D>
-__global__ __launch_bounds__(BLK, 2) void k_gauss_bwd(Launch L, mvgs_grads gr, mvgs_adc adc) {
+// SHG: the thread reads its SH row straight from global memory (16-byte loads through L1,
+// rows 16-byte aligned) instead of a staged shared-memory copy.  Only the SH-gradient rows
+// stay in shared memory, which with the smaller live state (Σ only in the view loop; R, s,
+// q recomputed at the end) lets three 256-thread CTAs share an SM instead of two.
+template <int D, bool SHG>
+__global__ __launch_bounds__(BLK, SHG ? 3 : 2) void k_gauss_bwd(Launch L, mvgs_grads gr, mvgs_adc adc) {
     constexpr int NK = ShRows<D>::NK, NS = ShRows<D>::NS, SS = ShRows<D>::STRIDE;
+    constexpr int VB = SHG ? GB_VB_SHG : GB_VB;
     extern __shared__ float4 smem_sh4[];  // 16-byte aligned base
     float* smem_sh = reinterpret_cast<float*>(smem_sh4);
-    float* sh_s = smem_sh;              // [BLK][SS]
-    float* dsh_s = smem_sh + BLK * SS;  // [BLK][SS]
+    float* dsh_s = smem_sh;                              // [BLK][SS]
+    float* sh_s = SHG ? nullptr : smem_sh + BLK * SS;    // [BLK][SS] (staged rows, !SHG)
     __shared__ int wc[BLK / 32][32];
+    __shared__ float4 scam[32];  // per view of the chunk: camera centre (x, y, z), Jacobian clamp limit x
+    __shared__ float scl[32];    // clamp limit y
     __shared__ int sboff[32];  // first pair slot of this block in each view of the chunk
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const unsigned lt = (1u << lane) - 1u;
     const int64_t g0 = (int64_t)blockIdx.x * BLK;
     const int64_t g = g0 + threadIdx.x;
     const bool valid = g < L.P;
-    {  // SH rows: coalesced async copies (no registers, all in flight), waited on before first use
+    if (!SHG) {  // SH rows: coalesced async copies (no registers, all in flight), waited on before first use
         const int nb = (int)min((int64_t)BLK, L.P - g0);
         const float* src = L.sh + g0 * (int64_t)L.sh_stride * 3;
         const int rowlen = L.sh_stride * 3;
@@ -155,20 +164,28 @@ __global__ __launch_bounds__(BLK, 2) void k_gauss_bwd(Launch L, mvgs_grads gr, m
             }
         }
         cp_async_commit();
+    }
+    {
         float4* z4 = reinterpret_cast<float4*>(dsh_s);
         for (int i = threadIdx.x; i < BLK * SS / 4; i += BLK) z4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
-    const float* sh = sh_s + threadIdx.x * SS;
+    // SH row of this Gaussian: staged copy, or global (16-byte aligned: checked by the launcher)
+    const float* sh = SHG ? L.sh + (valid ? g : 0) * (int64_t)L.sh_stride * 3 : sh_s + threadIdx.x * SS;
     float* dsh = dsh_s + threadIdx.x * SS;
     float mx = 0.f, my = 0.f, mz = 0.f;
-    FastActiv a;
-    if (valid) {
-        mx = L.means[3 * g];
-        my = L.means[3 * g + 1];
-        mz = L.means[3 * g + 2];
-        fast_activate(L.log_scales + 3 * g, L.quats + 4 * g, L.opac[g], a);
-    } else {
-        fast_activate(L.log_scales, L.quats, 0.f, a);  // any finite values; unused
+    float Sg[6];  // Σ (only Σ is needed in the view loop)
+    {
+        FastActiv a;
+        if (valid) {
+            mx = L.means[3 * g];
+            my = L.means[3 * g + 1];
+            mz = L.means[3 * g + 2];
+            fast_activate(L.log_scales + 3 * g, L.quats + 4 * g, L.opac[g], a);
+        } else {
+            fast_activate(L.log_scales, L.quats, 0.f, a);  // any finite values; unused
+        }
+#pragma unroll
+        for (int k = 0; k < 6; k++) Sg[k] = a.Sig[k];
     }
     float dmx = 0.f, dmy = 0.f, dmz = 0.f;
     float G00 = 0.f, G01 = 0.f, G02 = 0.f, G11 = 0.f, G12 = 0.f, G22 = 0.f;  // ∂L/∂Σ (symmetric)
@@ -183,7 +200,16 @@ __global__ __launch_bounds__(BLK, 2) void k_gauss_bwd(Launch L, mvgs_grads gr, m
             const unsigned bal = __ballot_sync(FULLG, vis);
             if (lane == 0) wc[warp][k] = __popc(bal);
         }
-        if (threadIdx.x < nv) sboff[threadIdx.x] = L.blk_off[(int64_t)(v0 + threadIdx.x) * L.NB + blockIdx.x];
+        if (threadIdx.x < nv) {
+            sboff[threadIdx.x] = L.blk_off[(int64_t)(v0 + threadIdx.x) * L.NB + blockIdx.x];
+            const mvgs_camera& c = L.cams[v0 + threadIdx.x];
+            const float* R = c.R;  // centre −Rᵀt and the clamp limits 0.65·W/fx, 0.65·H/fy (R4)
+            scam[threadIdx.x] = make_float4(-(R[0] * c.t[0] + R[3] * c.t[1] + R[6] * c.t[2]),
+                                            -(R[1] * c.t[0] + R[4] * c.t[1] + R[7] * c.t[2]),
+                                            -(R[2] * c.t[0] + R[5] * c.t[1] + R[8] * c.t[2]),
+                                            0.65f * (float)c.width / c.fx);
+            scl[threadIdx.x] = 0.65f * (float)c.height / c.fy;
+        }
         __syncthreads();
         if (threadIdx.x < nv) {  // exclusive prefix over warps, per view: wc[w][k] ← Σ_{w' < w}
             int run = 0;
@@ -194,12 +220,12 @@ __global__ __launch_bounds__(BLK, 2) void k_gauss_bwd(Launch L, mvgs_grads gr, m
             }
         }
         __syncthreads();
-        for (int k0 = 0; k0 < nv; k0 += GB_VB) {
+        for (int k0 = 0; k0 < nv; k0 += VB) {
             // issue the loads of up to GB_VB views first (memory-level parallelism), then the math
-            uint32_t fl[GB_VB];
-            float4 pga[GB_VB], pgb[GB_VB], pgc[GB_VB];
+            uint32_t fl[VB];
+            float4 pga[VB], pgb[VB], pgc[VB];
 #pragma unroll
-            for (int u = 0; u < GB_VB; u++) {
+            for (int u = 0; u < VB; u++) {
                 fl[u] = 0u;
                 const int k = k0 + u;
                 if (k >= nv) continue;  // warp-uniform
@@ -217,13 +243,13 @@ __global__ __launch_bounds__(BLK, 2) void k_gauss_bwd(Launch L, mvgs_grads gr, m
                 pgb[u] = pgp[1];
                 pgc[u] = pgp[2];
             }
-            if (!sh_ready) {  // block-uniform: overlap the SH copy with the first pair loads
+            if (!SHG && !sh_ready) {  // block-uniform: overlap the SH copy with the first pair loads
                 cp_async_wait_all();
                 __syncthreads();
                 sh_ready = true;
             }
 #pragma unroll
-            for (int u = 0; u < GB_VB; u++) {
+            for (int u = 0; u < VB; u++) {
             if (!(fl[u] & PF_VISIBLE)) continue;  // not participating, or tiles == 0: inert (R27)
             const mvgs_camera& c = L.cams[v0 + k0 + u];
             const uint32_t flags = fl[u];
@@ -235,8 +261,9 @@ __global__ __launch_bounds__(BLK, 2) void k_gauss_bwd(Launch L, mvgs_grads gr, m
             gsx += pg0.x;
             gsy += pg0.y;
             dop += pg1.z;
+            const float4 cam4 = scam[k0 + u];  // camera centre, clamp limit x
             FastProj p;
-            fast_project(c, mx, my, mz, a.Sig, flags, p);
+            fast_project(c, mx, my, mz, Sg, flags, cam4.w, scl[k0 + u], p);
             const float itz = p.itz, itz2 = itz * itz;
             // μ' (pixels) = (fx·tx/tz + cx, fy·ty/tz + cy); ∂L/∂μ' = Σ∇·(2/W, 2/H) (R2)
             const float dpx = pg0.x * sW, dpy = pg0.y * sH;
@@ -266,7 +293,7 @@ __global__ __launch_bounds__(BLK, 2) void k_gauss_bwd(Launch L, mvgs_grads gr, m
             G12 += T0[1] * GT0[2] + T1[1] * GT1[2];
             G22 += T0[2] * GT0[2] + T1[2] * GT1[2];
             // ∂L/∂T = 2 (Gs T) Σ
-            const float* S = a.Sig;
+            const float* S = Sg;
             float dT0[3], dT1[3];
             dT0[0] = 2.f * (GT0[0] * S[0] + GT0[1] * S[1] + GT0[2] * S[2]);
             dT0[1] = 2.f * (GT0[0] * S[1] + GT0[1] * S[3] + GT0[2] * S[4]);
@@ -303,10 +330,7 @@ __global__ __launch_bounds__(BLK, 2) void k_gauss_bwd(Launch L, mvgs_grads gr, m
             const float dr0 = (flags & 1u) ? 0.f : pg1.w;
             const float dr1 = (flags & 2u) ? 0.f : pg2.x;
             const float dr2 = (flags & 4u) ? 0.f : pg2.y;
-            const float cpx = -(R[0] * c.t[0] + R[3] * c.t[1] + R[6] * c.t[2]);
-            const float cpy = -(R[1] * c.t[0] + R[4] * c.t[1] + R[7] * c.t[2]);
-            const float cpz = -(R[2] * c.t[0] + R[5] * c.t[1] + R[8] * c.t[2]);
-            float x = mx - cpx, y = my - cpy, z = mz - cpz;
+            float x = mx - cam4.x, y = my - cam4.y, z = mz - cam4.z;
             const float idn = rsqrtf(x * x + y * y + z * z);
             x *= idn; y *= idn; z *= idn;
             float wk[NK];  // Σ_c sh[k][c]·∂L/∂rgb_c, read as float4 chunks of the row
@@ -317,7 +341,7 @@ __global__ __launch_bounds__(BLK, 2) void k_gauss_bwd(Launch L, mvgs_grads gr, m
                 const float4* sh4 = reinterpret_cast<const float4*>(sh);
 #pragma unroll
                 for (int i4 = 0; i4 < ShRows<D>::NS4; i4++) {
-                    const float4 q = sh4[i4];
+                    const float4 q = SHG ? __ldg(sh4 + i4) : sh4[i4];
                     const float qe[4] = {q.x, q.y, q.z, q.w};
 #pragma unroll
                     for (int e = 0; e < 4; e++) {
@@ -388,7 +412,7 @@ __global__ __launch_bounds__(BLK, 2) void k_gauss_bwd(Launch L, mvgs_grads gr, m
         }
         __syncthreads();
     }
-    if (!sh_ready) {  // no view chunk ran (V == 0 cannot happen, but keep the copy complete)
+    if (!SHG && !sh_ready) {  // no view chunk ran (V == 0 cannot happen, but keep the copy complete)
         cp_async_wait_all();
         __syncthreads();
     }
@@ -415,6 +439,8 @@ __global__ __launch_bounds__(BLK, 2) void k_gauss_bwd(Launch L, mvgs_grads gr, m
         }
     }
     if (!valid) return;
+    FastActiv a;  // recomputed: R, s, q are not kept live through the view loop
+    fast_activate(L.log_scales + 3 * g, L.quats + 4 * g, L.opac[g], a);
     // Σ = M Mᵀ, M = R diag(s): ∂L/∂M = 2 G M (G symmetric)
     const float* R = a.R;
     const float Gm[9] = {G00, G01, G02, G01, G11, G12, G02, G12, G22};
@@ -470,13 +496,24 @@ __global__ __launch_bounds__(BLK, 2) void k_gauss_bwd(Launch L, mvgs_grads gr, m
     if (adc.denom_acc) adc.denom_acc[g] += nvis;
 }
 
+template <int D, bool SHG>
+cudaError_t launch_gauss_bwd_v(const Launch& L, const mvgs_grads& gr, const mvgs_adc& adc, cudaStream_t s) {
+    const size_t smem = sizeof(float) * (SHG ? 1 : 2) * BLK * ShRows<D>::STRIDE;
+    cudaError_t e = cudaFuncSetAttribute(k_gauss_bwd<D, SHG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    k_gauss_bwd<D, SHG><<<L.NB, BLK, smem, s>>>(L, gr, adc);
+    return cudaGetLastError();
+}
+
+#ifndef GB_SH_GLOBAL
+#define GB_SH_GLOBAL 0  // 1 measured slower (0.71 vs 0.61 ms at garden): 3 CTAs of rows thrash L1
+#endif
+
 template <int D>
 cudaError_t launch_gauss_bwd_t(const Launch& L, const mvgs_grads& gr, const mvgs_adc& adc, cudaStream_t s) {
-    const size_t smem = sizeof(float) * 2 * BLK * ShRows<D>::STRIDE;
-    cudaError_t e = cudaFuncSetAttribute(k_gauss_bwd<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    k_gauss_bwd<D><<<L.NB, BLK, smem, s>>>(L, gr, adc);
-    return cudaGetLastError();
+    // rows read as float4 from global: row length and base must keep every row 16-byte aligned
+    const bool shg = GB_SH_GLOBAL && ((L.sh_stride * 3) & 3) == 0 && ((uintptr_t)L.sh & 15) == 0;
+    return shg ? launch_gauss_bwd_v<D, true>(L, gr, adc, s) : launch_gauss_bwd_v<D, false>(L, gr, adc, s);
 }
 
 cudaError_t launch_gauss_bwd(const Launch& L, const mvgs_grads& gr, const mvgs_adc& adc, cudaStream_t s) {
