@@ -3,8 +3,10 @@
 
 One step = the whole hot path on one batch:
 preprocess (S1–S5) → render_fwd (S6) → render_bwd (S7) → adc_stats (S8–S9),
-plus, with N > 1 GPUs, one NCCL all-reduce of the flat [param grads | E1 | E2 |
-vis] buffer (every output is a sum over views).
+plus, with N > 1 GPUs, the NCCL all-reduce of the flat [param grads | E1 | E2 | vis]
+buffer (every output is a sum over views), issued per Gaussian chunk
+as soon as that chunk's S8–S9 kernel is enqueued (MVGS_AR_CHUNKS, default 4) so the
+collective overlaps the rest of the per-Gaussian kernel.
 
 Workload: BASELINE.json configs[1], the Mip-NeRF-360 garden-shaped scene
 (3 M Gaussians, SH degree 3, 4 views of 1237×822) per GPU; with N GPUs each rank
@@ -160,7 +162,7 @@ def run_mvgs(args):
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2506_12727_b200 import mvgs
-    from paper_2506_12727_b200.dist import GradBuffer, view_shard
+    from paper_2506_12727_b200.dist import GradBuffer, adc_stats_allreduce, view_shard
 
     cfg = synth.CONFIGS[args.config]
     Vr = cfg.V if N == 1 else cfg.V  # views per rank (weak scaling: per-GPU batch fixed)
@@ -180,17 +182,25 @@ def run_mvgs(args):
     st0 = R.stats
     mvgs.reserve(R.ctx, int(st0["Q"] * 1.15) + 4096, int(st0["K"] * 1.15) + 65536)
     # one flat buffer for every output that is a sum over views (single all-reduce)
-    buf = GradBuffer(P, S, dev)
-    flat, grads, adc = buf.flat, buf.grads, buf.adc
+    # with N > 1, chunk-major so each chunk's all-reduce overlaps the next chunk's kernel
+    CHUNKS = int(os.environ.get("MVGS_AR_CHUNKS", "4")) if dist is not None else 1
+    buf = GradBuffer(P, S, dev, chunks=CHUNKS)
+    flat = buf.flat
     outs = R.alloc_forward()
+
+    def grads_out(b):
+        mvgs.render_bwd(R.ctx, dL_cur[0], outs[1], outs[2])
+        if dist is None:
+            mvgs.adc_stats(R.ctx, b.grads, b.adc)
+        else:
+            adc_stats_allreduce(R.ctx, b)
+
+    dL_cur = [dL]
 
     def step():
         mvgs.preprocess(R.ctx, g, R.cams)
         mvgs.render_fwd(R.ctx, *outs)
-        mvgs.render_bwd(R.ctx, dL, outs[1], outs[2])
-        mvgs.adc_stats(R.ctx, grads, adc)
-        if dist is not None:
-            buf.allreduce()
+        grads_out(buf)
 
     for _ in range(args.warmup):
         step()
@@ -243,7 +253,7 @@ def run_mvgs(args):
     d2h = host_out[0].numel() * 4
     g_slots = [g, {k: (torch.empty_like(v) if torch.is_tensor(v) else v) for k, v in g.items()}]
     dL_slots = [dL, torch.empty_like(dL)]
-    bufs = [buf, GradBuffer(P, S, dev)]
+    bufs = [buf, GradBuffer(P, S, dev, chunks=CHUNKS)]
     comp = torch.cuda.current_stream()
     s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
     mk = lambda: [torch.cuda.Event() for _ in range(2)]  # noqa: E731
@@ -264,10 +274,8 @@ def run_mvgs(args):
         ob = bufs[b]
         mvgs.preprocess(R.ctx, g_slots[b], R.cams)
         mvgs.render_fwd(R.ctx, *outs)
-        mvgs.render_bwd(R.ctx, dL_slots[b], outs[1], outs[2])
-        mvgs.adc_stats(R.ctx, ob.grads, ob.adc)
-        if dist is not None:
-            ob.allreduce()
+        dL_cur[0] = dL_slots[b]
+        grads_out(ob)
         in_free[b].record(comp)
         out_ready[b].record(comp)
         s_out.wait_event(out_ready[b])
@@ -326,6 +334,7 @@ def run_mvgs(args):
         "vs_baseline": None, "dtype": "f32", "data": "synthetic (mvgs-synth v1, seeded; DESIGN.md §6)",
         "config": {"workload": f"{cfg.name}: {P} Gaussians SH{cfg.sh_degree}, {Vr} views/GPU at {cfg.W}x{cfg.H}",
                    "views_per_step": views_total, "global_batch_views": views_total, "parallelism": f"views dp{N}",
+                   "allreduce_chunks": CHUNKS,
                    "l2": "inputs larger than L2 (params %.0f MB)" % (sum(v.nbytes for v in g_np.values()
                                                                        if isinstance(v, np.ndarray)) / 1e6),
                    "Q": st["Q"], "K": st["K"], "max_bucket": st["max_bucket"], "n_visible": st["n_visible"],

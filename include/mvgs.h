@@ -154,6 +154,17 @@ mvgs_status mvgs_render_bwd(mvgs_ctx *ctx, const float *dL_drgb, const float *T_
  * are host structs of device pointers.  Requires a preceding render_bwd. */
 mvgs_status mvgs_adc_stats(mvgs_ctx *ctx, const mvgs_grads *grads, const mvgs_adc *adc, void *stream);
 
+/* The same for the Gaussians [g_begin, g_end) only, g_begin a multiple of 256
+ * (the pair-slot block size): every pointer in `grads` and `adc` addresses the
+ * row of Gaussian g_begin (row g − g_begin of each output).  Chunks may be
+ * issued in any order and number after one render_bwd; a multi-GPU caller
+ * all-reduces each finished chunk while the next one computes (SURVEY §8(e)
+ * lever 1).  mvgs_adc_stats ≡ range [0, P).  MVGS_ERR_INVALID
+ * for g_begin % 256 ≠ 0, g_begin < 0, g_end < g_begin, g_end > P or a null
+ * output pointer of a non-empty range; MVGS_ERR_STATE without a render_bwd. */
+mvgs_status mvgs_adc_stats_range(mvgs_ctx *ctx, int64_t g_begin, int64_t g_end, const mvgs_grads *grads,
+                                 const mvgs_adc *adc, void *stream);
+
 /* NEXT-2: the 3D distance-aware D-SSIM loss and its gradient.
  *   SSIM = (2μ1μ2 + C1)(2τ12 + C2) / ((μ1² + μ2² + C1)(τ1² + τ2² + C2))
  * with the moments μ, τ taken under the 3D kernel

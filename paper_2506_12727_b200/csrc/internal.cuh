@@ -167,7 +167,8 @@ cudaError_t launch_render_fwd_partial(const Launch& L, const int32_t* pix, int S
                                       int32_t* nc, cudaStream_t s);
 cudaError_t launch_render_bwd_partial(const Launch& L, const int32_t* pix, int S, int mode, const float* dL,
                                       const float* Tf, const int32_t* nc, cudaStream_t s);
-cudaError_t launch_gauss_bwd(const Launch& L, const mvgs_grads& gr, const mvgs_adc& adc, cudaStream_t s);
+cudaError_t launch_gauss_bwd(const Launch& L, const mvgs_grads& gr, const mvgs_adc& adc, int64_t gb, int64_t ge,
+                             cudaStream_t s);
 cudaError_t launch_export(const Launch& L, int64_t* range_start, int32_t* entry_gid, int32_t* pair_ids,
                           int32_t* pair_i, float* pair_f, float* pair_g, cudaStream_t s);
 int scan_tmp_size(int n);

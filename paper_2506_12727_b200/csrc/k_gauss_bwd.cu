@@ -131,7 +131,10 @@ struct ShRows {
 // stay in shared memory, which with the smaller live state (Σ only in the view loop; R, s,
 // q recomputed at the end) lets three 256-thread CTAs share an SM instead of two.
 template <int D, bool SHG>
-__global__ __launch_bounds__(BLK, SHG ? 3 : 2) void k_gauss_bwd(Launch L, mvgs_grads gr, mvgs_adc adc) {
+// Gaussians [gbeg, gend) only (gbeg a multiple of BLK): outputs are addressed relative to gbeg,
+// so a caller can reduce each finished chunk while the next one computes.
+__global__ __launch_bounds__(BLK, SHG ? 3 : 2) void k_gauss_bwd(Launch L, mvgs_grads gr, mvgs_adc adc, int64_t gbeg,
+                                                                 int64_t gend) {
     constexpr int NK = ShRows<D>::NK, NS = ShRows<D>::NS, SS = ShRows<D>::STRIDE;
     constexpr int VB = SHG ? GB_VB_SHG : GB_VB;
     extern __shared__ float4 smem_sh4[];  // 16-byte aligned base
@@ -144,11 +147,13 @@ __global__ __launch_bounds__(BLK, SHG ? 3 : 2) void k_gauss_bwd(Launch L, mvgs_g
     __shared__ int sboff[32];  // first pair slot of this block in each view of the chunk
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const unsigned lt = (1u << lane) - 1u;
-    const int64_t g0 = (int64_t)blockIdx.x * BLK;
+    const int blk = blockIdx.x + (int)(gbeg / BLK);  // 256-Gaussian block of the pair-slot allocation
+    const int64_t g0 = (int64_t)blk * BLK;
     const int64_t g = g0 + threadIdx.x;
-    const bool valid = g < L.P;
+    const int64_t o = g - gbeg;  // output row
+    const bool valid = g < gend;
     if (!SHG) {  // SH rows: coalesced async copies (no registers, all in flight), waited on before first use
-        const int nb = (int)min((int64_t)BLK, L.P - g0);
+        const int nb = (int)min((int64_t)BLK, gend - g0);
         const float* src = L.sh + g0 * (int64_t)L.sh_stride * 3;
         const int rowlen = L.sh_stride * 3;
         if ((rowlen & 3) == 0 && (NS & 3) == 0 && ((uintptr_t)src & 15) == 0) {
@@ -201,7 +206,7 @@ __global__ __launch_bounds__(BLK, SHG ? 3 : 2) void k_gauss_bwd(Launch L, mvgs_g
             if (lane == 0) wc[warp][k] = __popc(bal);
         }
         if (threadIdx.x < nv) {
-            sboff[threadIdx.x] = L.blk_off[(int64_t)(v0 + threadIdx.x) * L.NB + blockIdx.x];
+            sboff[threadIdx.x] = L.blk_off[(int64_t)(v0 + threadIdx.x) * L.NB + blk];
             const mvgs_camera& c = L.cams[v0 + threadIdx.x];
             const float* R = c.R;  // centre −Rᵀt and the clamp limits 0.65·W/fx, 0.65·H/fy (R4)
             scam[threadIdx.x] = make_float4(-(R[0] * c.t[0] + R[3] * c.t[1] + R[6] * c.t[2]),
@@ -418,8 +423,8 @@ __global__ __launch_bounds__(BLK, SHG ? 3 : 2) void k_gauss_bwd(Launch L, mvgs_g
     }
     // coalesced store of the SH gradient rows (coefficients above the active degree are 0)
     {
-        const int nb = (int)min((int64_t)BLK, L.P - g0);
-        float* dst = gr.d_sh + g0 * (int64_t)L.sh_stride * 3;
+        const int nb = (int)min((int64_t)BLK, gend - g0);
+        float* dst = gr.d_sh + (g0 - gbeg) * (int64_t)L.sh_stride * 3;
         const int rowlen = L.sh_stride * 3;
         if (rowlen == NS && (NS & 3) == 0 && ((uintptr_t)dst & 15) == 0) {  // float4 rows, constant divisor
             constexpr int NS4 = NS / 4;
@@ -475,33 +480,35 @@ __global__ __launch_bounds__(BLK, SHG ? 3 : 2) void k_gauss_bwd(Launch L, mvgs_g
     const float qd = w * dq[0] + x * dq[1] + y * dq[2] + z * dq[3];
     // q̂ = q/‖q‖ ⇒ ∂L/∂q = (∂q̂ − q̂(q̂·∂q̂))/‖q‖
 #pragma unroll
-    for (int k = 0; k < 4; k++) gr.d_quats[4 * g + k] = (dq[k] - a.q[k] * qd) * a.inv_norm;
-    gr.d_means[3 * g] = dmx;
-    gr.d_means[3 * g + 1] = dmy;
-    gr.d_means[3 * g + 2] = dmz;
-    gr.d_log_scales[3 * g] = dls[0];
-    gr.d_log_scales[3 * g + 1] = dls[1];
-    gr.d_log_scales[3 * g + 2] = dls[2];
-    gr.d_opacity_logits[g] = dop * a.o * (1.f - a.o);
-    adc.e1[g] = e1;
-    adc.e2[g] = e2;
+    for (int k = 0; k < 4; k++) gr.d_quats[4 * o + k] = (dq[k] - a.q[k] * qd) * a.inv_norm;
+    gr.d_means[3 * o] = dmx;
+    gr.d_means[3 * o + 1] = dmy;
+    gr.d_means[3 * o + 2] = dmz;
+    gr.d_log_scales[3 * o] = dls[0];
+    gr.d_log_scales[3 * o + 1] = dls[1];
+    gr.d_log_scales[3 * o + 2] = dls[2];
+    gr.d_opacity_logits[o] = dop * a.o * (1.f - a.o);
+    adc.e1[o] = e1;
+    adc.e2[o] = e2;
     if (adc.e_old || adc.e_old_acc) {
         const float eo = sqrtf(gsx * gsx + gsy * gsy);
-        if (adc.e_old) adc.e_old[g] = eo;
-        if (adc.e_old_acc) adc.e_old_acc[g] += eo;
+        if (adc.e_old) adc.e_old[o] = eo;
+        if (adc.e_old_acc) adc.e_old_acc[o] += eo;
     }
-    adc.vis[g] = nvis;
-    if (adc.e1_acc) adc.e1_acc[g] += e1;
-    if (adc.e2_acc) adc.e2_acc[g] += e2;
-    if (adc.denom_acc) adc.denom_acc[g] += nvis;
+    adc.vis[o] = nvis;
+    if (adc.e1_acc) adc.e1_acc[o] += e1;
+    if (adc.e2_acc) adc.e2_acc[o] += e2;
+    if (adc.denom_acc) adc.denom_acc[o] += nvis;
 }
 
 template <int D, bool SHG>
-cudaError_t launch_gauss_bwd_v(const Launch& L, const mvgs_grads& gr, const mvgs_adc& adc, cudaStream_t s) {
+cudaError_t launch_gauss_bwd_v(const Launch& L, const mvgs_grads& gr, const mvgs_adc& adc, int64_t gb, int64_t ge,
+                               cudaStream_t s) {
     const size_t smem = sizeof(float) * (SHG ? 1 : 2) * BLK * ShRows<D>::STRIDE;
     cudaError_t e = cudaFuncSetAttribute(k_gauss_bwd<D, SHG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    k_gauss_bwd<D, SHG><<<L.NB, BLK, smem, s>>>(L, gr, adc);
+    const int nblk = (int)((ge - gb + BLK - 1) / BLK);
+    if (nblk > 0) k_gauss_bwd<D, SHG><<<nblk, BLK, smem, s>>>(L, gr, adc, gb, ge);
     return cudaGetLastError();
 }
 
@@ -510,18 +517,20 @@ cudaError_t launch_gauss_bwd_v(const Launch& L, const mvgs_grads& gr, const mvgs
 #endif
 
 template <int D>
-cudaError_t launch_gauss_bwd_t(const Launch& L, const mvgs_grads& gr, const mvgs_adc& adc, cudaStream_t s) {
+cudaError_t launch_gauss_bwd_t(const Launch& L, const mvgs_grads& gr, const mvgs_adc& adc, int64_t gb, int64_t ge,
+                               cudaStream_t s) {
     // rows read as float4 from global: row length and base must keep every row 16-byte aligned
     const bool shg = GB_SH_GLOBAL && ((L.sh_stride * 3) & 3) == 0 && ((uintptr_t)L.sh & 15) == 0;
-    return shg ? launch_gauss_bwd_v<D, true>(L, gr, adc, s) : launch_gauss_bwd_v<D, false>(L, gr, adc, s);
+    return shg ? launch_gauss_bwd_v<D, true>(L, gr, adc, gb, ge, s) : launch_gauss_bwd_v<D, false>(L, gr, adc, gb, ge, s);
 }
 
-cudaError_t launch_gauss_bwd(const Launch& L, const mvgs_grads& gr, const mvgs_adc& adc, cudaStream_t s) {
+cudaError_t launch_gauss_bwd(const Launch& L, const mvgs_grads& gr, const mvgs_adc& adc, int64_t gb, int64_t ge,
+                             cudaStream_t s) {
     switch (L.sh_degree) {
-        case 0: return launch_gauss_bwd_t<0>(L, gr, adc, s);
-        case 1: return launch_gauss_bwd_t<1>(L, gr, adc, s);
-        case 2: return launch_gauss_bwd_t<2>(L, gr, adc, s);
-        default: return launch_gauss_bwd_t<3>(L, gr, adc, s);
+        case 0: return launch_gauss_bwd_t<0>(L, gr, adc, gb, ge, s);
+        case 1: return launch_gauss_bwd_t<1>(L, gr, adc, gb, ge, s);
+        case 2: return launch_gauss_bwd_t<2>(L, gr, adc, gb, ge, s);
+        default: return launch_gauss_bwd_t<3>(L, gr, adc, gb, ge, s);
     }
 }
 

@@ -197,8 +197,11 @@ __device__ __forceinline__ void sh_eval_basis(float x, float y, float z, float* 
 
 template <int D>
 __global__ __launch_bounds__(BLK) void k_project(Launch L) {
-    constexpr int NK = (D + 1) * (D + 1), NS = NK * 3, SS = NS | 1;
-    extern __shared__ float sh_s[];  // [BLK][SS] SH rows, coalesced block load, odd stride
+    // SH rows in shared memory with an odd number of float4 per row: 16-byte copies in, and
+    // the colour loop walks its row with conflict-free LDS.128 (8 lanes per wavefront)
+    constexpr int NK = (D + 1) * (D + 1), NS = NK * 3, NS4 = (NS + 3) / 4, SS = 4 * (NS4 | 1);
+    extern __shared__ float4 sh_s4[];  // [BLK][SS] SH rows
+    float* sh_s = reinterpret_cast<float*>(sh_s4);
     __shared__ int wc[BLK / 32][32];
     __shared__ int sboff[32];  // first pair slot of this block in each view of the chunk
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -209,10 +212,16 @@ __global__ __launch_bounds__(BLK) void k_project(Launch L) {
         const int nb = (int)min((int64_t)BLK, L.P - g0);
         const float* src = L.sh + g0 * (int64_t)L.sh_stride * 3;
         const int rowlen = L.sh_stride * 3;
-        const int n = nb * NS;
-        for (int i = threadIdx.x; i < n; i += BLK) {
-            const int r = i / NS, k = i - r * NS;  // NS constexpr: mul-shift
-            cp_async4(&sh_s[r * SS + k], src + (int64_t)r * rowlen + k);
+        if ((rowlen & 3) == 0 && (NS & 3) == 0 && ((uintptr_t)src & 15) == 0) {
+            for (int i = threadIdx.x; i < nb * NS4; i += BLK) {
+                const int r = i / NS4, k = 4 * (i - r * NS4);  // NS4 constexpr: mul-shift
+                cp_async16(&sh_s[r * SS + k], src + (int64_t)r * rowlen + k);
+            }
+        } else {
+            for (int i = threadIdx.x; i < nb * NS; i += BLK) {
+                const int r = i / NS, k = i - r * NS;
+                cp_async4(&sh_s[r * SS + k], src + (int64_t)r * rowlen + k);
+            }
         }
         cp_async_commit();
     }
@@ -275,11 +284,23 @@ __global__ __launch_bounds__(BLK) void k_project(Launch L) {
                 sh_eval_basis<D>(dx, dy, dz, Y);
                 float rgb[3];
                 uint32_t flags = (p.clx ? 8u : 0u) | (p.cly ? 16u : 0u);
+                float accs[3] = {0.5f, 0.5f, 0.5f};
+                {  // Σ_k Y_k·sh[k][ch], the row read as float4 chunks (same per-channel order)
+                    const float4* sh4 = reinterpret_cast<const float4*>(sh);
+#pragma unroll
+                    for (int i4 = 0; i4 < NS4; i4++) {
+                        const float4 q = sh4[i4];
+                        const float qe[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+                        for (int e = 0; e < 4; e++) {
+                            const int f = 4 * i4 + e;
+                            if (f < NS) accs[f % 3] += Y[f / 3] * qe[e];
+                        }
+                    }
+                }
 #pragma unroll
                 for (int ch = 0; ch < 3; ch++) {
-                    float acc = 0.5f;
-#pragma unroll
-                    for (int kk = 0; kk < NK; kk++) acc += Y[kk] * sh[3 * kk + ch];
+                    float acc = accs[ch];
                     if (acc < 0.f) {
                         flags |= 1u << ch;
                         acc = 0.f;
@@ -328,7 +349,7 @@ __global__ __launch_bounds__(BLK) void k_project(Launch L) {
 
 template <int D>
 cudaError_t launch_project_t(const Launch& L, cudaStream_t s) {
-    const size_t smem = sizeof(float) * BLK * (((D + 1) * (D + 1) * 3) | 1);
+    const size_t smem = sizeof(float) * BLK * 4 * ((((D + 1) * (D + 1) * 3 + 3) / 4) | 1);
     cudaError_t e = cudaFuncSetAttribute(k_project<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     k_project<D><<<L.NB, BLK, smem, s>>>(L);

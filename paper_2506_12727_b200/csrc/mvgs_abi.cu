@@ -429,18 +429,26 @@ mvgs_status mvgs_render_bwd_partial(mvgs_ctx* ctx, const int32_t* pix, int32_t S
     return MVGS_OK;
 }
 
-mvgs_status mvgs_adc_stats(mvgs_ctx* ctx, const mvgs_grads* grads, const mvgs_adc* adc, void* stream) {
+mvgs_status mvgs_adc_stats_range(mvgs_ctx* ctx, int64_t g_begin, int64_t g_end, const mvgs_grads* grads,
+                                 const mvgs_adc* adc, void* stream) {
     if (!ctx) return MVGS_ERR_INVALID;
     if (ctx->state != 3) return fail(ctx, MVGS_ERR_STATE, "adc_stats needs a preceding render_bwd");
     if (!grads || !adc) return fail(ctx, MVGS_ERR_INVALID, "null grads/adc");
-    if (ctx->L.P > 0 && (!grads->d_means || !grads->d_log_scales || !grads->d_quats || !grads->d_opacity_logits ||
-                         !grads->d_sh || !adc->e1 || !adc->e2 || !adc->vis))
+    if (g_begin < 0 || g_end < g_begin || g_end > ctx->L.P || (g_begin % BLK) != 0)
+        return fail(ctx, MVGS_ERR_INVALID, "adc_stats_range: need 0 <= g_begin <= g_end <= P, g_begin % 256 == 0");
+    if (g_end > g_begin && (!grads->d_means || !grads->d_log_scales || !grads->d_quats || !grads->d_opacity_logits ||
+                            !grads->d_sh || !adc->e1 || !adc->e2 || !adc->vis))
         return fail(ctx, MVGS_ERR_INVALID, "null output pointer");
     CK(cudaSetDevice(ctx->device));
     ctx->last_stream = (cudaStream_t)stream;
     cudaStream_t s = (cudaStream_t)stream;
-    if (ctx->L.NB > 0) { STAGE(ST_GAUSS); CK(launch_gauss_bwd(ctx->L, *grads, *adc, s)); }  // S8 + S9
+    if (g_end > g_begin) { STAGE(ST_GAUSS); CK(launch_gauss_bwd(ctx->L, *grads, *adc, g_begin, g_end, s)); }  // S8 + S9
     return MVGS_OK;
+}
+
+mvgs_status mvgs_adc_stats(mvgs_ctx* ctx, const mvgs_grads* grads, const mvgs_adc* adc, void* stream) {
+    if (!ctx) return MVGS_ERR_INVALID;
+    return mvgs_adc_stats_range(ctx, 0, ctx->L.P, grads, adc, stream);
 }
 
 mvgs_status mvgs_query(mvgs_ctx* ctx, mvgs_stats* out) {

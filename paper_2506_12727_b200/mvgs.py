@@ -19,7 +19,7 @@ NG = 10
 
 # the exported symbols include/mvgs.h declares (checked by tests/test_abi.py)
 SYMBOLS = ["mvgs_create", "mvgs_destroy", "mvgs_last_error", "mvgs_reserve", "mvgs_preprocess", "mvgs_render_fwd",
-           "mvgs_render_bwd", "mvgs_adc_stats", "mvgs_query", "mvgs_export_lists", "mvgs_export_pairs",
+           "mvgs_render_bwd", "mvgs_adc_stats", "mvgs_adc_stats_range", "mvgs_query", "mvgs_export_lists", "mvgs_export_pairs",
            "mvgs_set_timing", "mvgs_stage_times", "mvgs_set_eval_counting", "mvgs_render_fwd_partial", "mvgs_render_bwd_partial",
            "mvgs_render_fwd_depth", "mvgs_dssim3d", "mvgs_adc_step", "mvgs_adc_remap",
            "mvgs_loss_grad", "mvgs_grad_moments", "mvgs_grad_variance"]
@@ -94,6 +94,7 @@ def _load():
     L.mvgs_render_fwd_depth.argtypes = [vp, vp, vp, vp, vp, vp]
     L.mvgs_render_bwd.argtypes = [vp, vp, vp, vp, vp]
     L.mvgs_adc_stats.argtypes = [vp, C.POINTER(Grads), C.POINTER(Adc), vp]
+    L.mvgs_adc_stats_range.argtypes = [vp, C.c_int64, C.c_int64, C.POINTER(Grads), C.POINTER(Adc), vp]
     L.mvgs_query.argtypes = [vp, C.POINTER(Stats)]
     L.mvgs_export_lists.argtypes = [vp, vp, vp, vp]
     L.mvgs_export_pairs.argtypes = [vp, vp, vp, vp, vp, vp]
@@ -214,6 +215,13 @@ def adc_stats(ctx, grads: dict, adc: dict, stream=None):
     gr = Grads(*[_ptr(grads[k]) for k in ("d_means", "d_log_scales", "d_quats", "d_opacity_logits", "d_sh")])
     ad = Adc(*[_ptr(adc.get(k)) for k in ("e1", "e2", "e_old", "vis", "e1_acc", "e2_acc", "denom_acc", "e_old_acc")])
     _check(ctx, _lib.mvgs_adc_stats(ctx, C.byref(gr), C.byref(ad), _stream(stream)))
+
+
+def adc_stats_range(ctx, g_begin: int, g_end: int, grads: dict, adc: dict, stream=None):
+    """S8–S9 for Gaussians [g_begin, g_end) (g_begin % 256 == 0); the tensors hold rows g_begin.. ."""
+    gr = Grads(*[_ptr(grads[k]) for k in ("d_means", "d_log_scales", "d_quats", "d_opacity_logits", "d_sh")])
+    ad = Adc(*[_ptr(adc.get(k)) for k in ("e1", "e2", "e_old", "vis", "e1_acc", "e2_acc", "denom_acc", "e_old_acc")])
+    _check(ctx, _lib.mvgs_adc_stats_range(ctx, int(g_begin), int(g_end), C.byref(gr), C.byref(ad), _stream(stream)))
 
 
 ADC_DEFAULTS = dict(grad_threshold_split=2e-4, grad_threshold_clone=2e-4, size_threshold=0.01, split_factor=1.6,

@@ -66,11 +66,11 @@ def traffic(path, out):
         name = r[h.index("Kernel Name")].replace("mvgs::", "").replace("void ", "")
         for pat, stage in STAGE_OF:
             if name.startswith(pat.split("<")[0]) and (("<" not in pat) or pat.split("<")[1].split(">")[0] in name):
-                rd = _num(r[h.index("dram__bytes_read.sum")])
-                wr = _num(r[h.index("dram__bytes_write.sum")])
-                ur = units[h.index("dram__bytes_read.sum")]
-                scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(ur, 1)
-                res[stage] = (rd + wr) * scale
+                sc = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+                tot = 0.0
+                for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"):  # units differ per metric
+                    tot += _num(r[h.index(m)]) * sc.get(units[h.index(m)], 1)
+                res[stage] = tot
     json.dump(res, open(out, "w"), indent=1)
     print(json.dumps(res, indent=1))
 

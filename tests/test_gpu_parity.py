@@ -253,3 +253,42 @@ def test_isotropic_rotation_gradient_is_zero():
     assert np.max(np.abs(ref["d_quats"])) < 1e-9 * np.max(np.abs(ref["d_log_scales"]))
     assert np.max(np.abs(gpu["d_quats"])) < 1e-4 * np.max(np.abs(ref["d_log_scales"]))
     assert_close_rel(gpu["d_log_scales"], ref["d_log_scales"], "d_log_scales")
+
+
+def test_adc_stats_range_chunks_equal_full_call():
+    """mvgs_adc_stats_range over 256-aligned chunks of a chunk-major GradBuffer (the
+    overlapped multi-GPU schedule) gives bit-identical gradients and E statistics to one
+    mvgs_adc_stats call: every Gaussian's chain runs in one thread either way."""
+    import torch
+    from paper_2506_12727_b200 import mvgs
+    from paper_2506_12727_b200.dist import GradBuffer
+    from gpu_harness import to_dev
+    g, cams = synth.make_scene(synth.scaled(synth.CONFIGS["garden"], P=3_000, V=3, W=203, H=137))
+    V, H, W = len(cams), int(cams[0]["height"]), int(cams[0]["width"])
+    dL = torch.from_numpy(synth.make_dLdC_scaled(V, H, W, 5)).cuda()
+    R = mvgs.Rasterizer(0)
+    R.preprocess(to_dev(g), cams)
+    R.forward()
+    full_g, full_a = R.backward(dL)
+    P, S = g["means"].shape[0], g["sh"].shape[1]
+    for chunks in (2, 5):
+        buf = GradBuffer(P, S, "cuda", chunks=chunks)
+        assert len(buf.bounds) > 1 and buf.bounds[-1][1] == P
+        R.preprocess(to_dev(g), cams)
+        R.forward()
+        mvgs.render_bwd(R.ctx, dL, *R._fwd)
+        for c in reversed(range(len(buf.bounds))):  # any order
+            lo, hi, gr, ad = buf.chunk_outputs(c)
+            mvgs.adc_stats_range(R.ctx, lo, hi, gr, ad)
+        torch.cuda.synchronize()
+        v = buf.views
+        for k in ("d_means", "d_log_scales", "d_quats", "d_opacity_logits", "d_sh"):
+            assert torch.equal(v[k], full_g[k]), k
+        for k in ("e1", "e2", "vis"):
+            assert torch.equal(v[k], full_a[k]), k
+        assert torch.equal(buf.e_old, full_a["e_old"])
+    lo, hi, gr, ad = buf.chunk_outputs(0)
+    for a, b in ((1, 10), (-256, 10), (0, P + 1), (512, 256)):
+        with pytest.raises(mvgs.MvgsError) as e:
+            mvgs.adc_stats_range(R.ctx, a, b, gr, ad)
+        assert e.value.status == mvgs.MVGS_ERR_INVALID
