@@ -462,8 +462,8 @@ __global__ void k_pair_tiles(Launch L, const uint2* __restrict__ rect, int* __re
 // consecutive entries, finds the pair holding its first entry with a 32-ary search
 // over the entry offsets, and walks the chunk's pairs 32 at a time: lanes load one
 // pair each, a warp scan of their in-chunk counts gives a contiguous run of entries,
-// and lane l writes entries l, l+32, … of the run (coalesced), finding its pair by a
-// binary search over the 32 inclusive prefixes in shared memory.  The row/column split
+// and lane l writes entries l, l+32, … of the run (coalesced), finding its pair from a
+// ballot of the run starts inside its 32-entry window (highest start ≤ its entry).  The row/column split
 // uses a float reciprocal of the rect width (exact: (k + 0.5)/w for integers k < 2^20,
 // w < 2^12 never rounds across an integer).
 constexpr int DUP_CH = 1024;
@@ -477,7 +477,7 @@ struct DupDesc {  // one pair of the warp's 32
 
 __global__ __launch_bounds__(256) void k_dup(Launch L, const uint32_t* __restrict__ order,
                                              const uint2* __restrict__ rect, const int* __restrict__ ebase) {
-    __shared__ int pref[8][32];
+    __shared__ uint8_t spos[8][32];
     __shared__ DupDesc desc[8][32];
     const int Q = (int)min((int64_t)L.counters[C_NVIS], L.cap_pairs);  // visible pairs (compacted by the sort)
     const int64_t Kall = L.counters[C_K];
@@ -521,7 +521,6 @@ __global__ __launch_bounds__(256) void k_dup(Launch L, const uint32_t* __restric
             const int enext = __shfl_sync(FULLS, en, 31);  // first entry after these 32 pairs
             const int rx0 = r.x & 0xffff, ry0 = r.x >> 16, rx1 = r.y & 0xffff;
             const int w = rx1 - rx0;
-            pref[wid][lane] = inc;
             DupDesc d;
             d.x0 = rx0;
             d.y0 = ry0;
@@ -533,18 +532,31 @@ __global__ __launch_bounds__(256) void k_dup(Launch L, const uint32_t* __restric
             d.off0 = s0 - eb;
             desc[wid][lane] = d;
             __syncwarp();
-            for (int k = lane; k < total; k += 32) {
-                int o = 0;  // owner = number of lanes whose inclusive prefix is ≤ k
-#pragma unroll
-                for (int step = 16; step > 0; step >>= 1)
-                    if (pref[wid][o + step - 1] <= k) o += step;
-                const DupDesc& od = desc[wid][o];
-                const int loc = od.off0 + (k - od.excl);
-                const int row = __float2int_rz(((float)loc + 0.5f) * od.inv_w);
-                const int col = loc - row * od.w;
-                const int e = ebeg + k;
-                L.key[e] = od.vb + (od.y0 + row) * L.TX + od.x0 + col;
-                L.val[e] = od.q;
+            // Entries in windows of 32: the owner of entry k is the last lane whose run starts at
+            // or before k.  Lanes with entries have distinct, lane-ordered run starts, so a lane
+            // starting inside the window marks its bit (and records itself at that position);
+            // entry k takes the highest marked bit ≤ k, or the window's carried-in owner.
+            const int my_excl = inc - cnt;
+            int carry = 0;
+            for (int k0 = 0; k0 < total; k0 += 32) {
+                const bool st = cnt > 0 && my_excl >= k0 && my_excl < k0 + 32;
+                if (st) spos[wid][my_excl - k0] = (uint8_t)lane;
+                const unsigned W = __ballot_sync(FULLS, st);
+                __syncwarp();
+                const unsigned le = W & (0xffffffffu >> (31 - lane));  // starts at positions 0..lane
+                const int o = le ? (int)spos[wid][31 - __clz(le)] : carry;
+                carry = __shfl_sync(FULLS, o, 31);
+                __syncwarp();  // spos is rewritten by the next window
+                const int k = k0 + lane;
+                if (k < total) {
+                    const DupDesc& od = desc[wid][o];
+                    const int loc = od.off0 + (k - od.excl);
+                    const int row = __float2int_rz(((float)loc + 0.5f) * od.inv_w);
+                    const int col = loc - row * od.w;
+                    const int e = ebeg + k;
+                    L.key[e] = od.vb + (od.y0 + row) * L.TX + od.x0 + col;
+                    L.val[e] = od.q;
+                }
             }
             __syncwarp();
             if (enext >= e1) break;  // warp-uniform

@@ -267,16 +267,16 @@ def test_adc_stats_range_chunks_equal_full_call():
     V, H, W = len(cams), int(cams[0]["height"]), int(cams[0]["width"])
     dL = torch.from_numpy(synth.make_dLdC_scaled(V, H, W, 5)).cuda()
     R = mvgs.Rasterizer(0)
-    R.preprocess(to_dev(g), cams)
-    R.forward()
-    full_g, full_a = R.backward(dL)
     P, S = g["means"].shape[0], g["sh"].shape[1]
     for chunks in (2, 5):
         buf = GradBuffer(P, S, "cuda", chunks=chunks)
         assert len(buf.bounds) > 1 and buf.bounds[-1][1] == P
         R.preprocess(to_dev(g), cams)
         R.forward()
+        # one render_bwd (its per-pair sums are atomics: compare both calls on the same records)
         mvgs.render_bwd(R.ctx, dL, *R._fwd)
+        full_g, full_a = R.alloc_backward()
+        mvgs.adc_stats(R.ctx, full_g, full_a)
         for c in reversed(range(len(buf.bounds))):  # any order
             lo, hi, gr, ad = buf.chunk_outputs(c)
             mvgs.adc_stats_range(R.ctx, lo, hi, gr, ad)
