@@ -541,7 +541,7 @@ __global__ __launch_bounds__(256) void k_dup(Launch L, const uint32_t* __restric
             for (int k0 = 0; k0 < total; k0 += 32) {
                 const bool st = cnt > 0 && my_excl >= k0 && my_excl < k0 + 32;
                 if (st) spos[wid][my_excl - k0] = (uint8_t)lane;
-                const unsigned W = __ballot_sync(FULLS, st);
+                const unsigned W = __reduce_or_sync(FULLS, st ? 1u << (my_excl - k0) : 0u);  // start positions
                 __syncwarp();
                 const unsigned le = W & (0xffffffffu >> (31 - lane));  // starts at positions 0..lane
                 const int o = le ? (int)spos[wid][31 - __clz(le)] : carry;
