@@ -246,20 +246,12 @@ __global__ __launch_bounds__(256) void k_rs_upsweep(const uint32_t* __restrict__
     for (int i = threadIdx.x; i < 4 * RS_BINS; i += blockDim.x) (&h[0][0])[i] = 0;
     __syncthreads();
     const int n = (int)min((int64_t)*n_ptr, cap);
-    // Warp-uniform trip count; lanes with the same digit add once (the high depth digits take
-    // few distinct values, so unaggregated shared atomics serialise on a handful of bins).
-    const int stride = gridDim.x * blockDim.x;
-    for (int i0 = blockIdx.x * blockDim.x + (threadIdx.x & ~31); i0 < n; i0 += stride) {
-        const int i = i0 + (threadIdx.x & 31);
-        const uint32_t k = i < n ? keys[i] : INERT;
-        const bool ok = i < n && !(drop_inert && k == INERT);
-        const unsigned act = __ballot_sync(FULLS, ok);
-        if (!act) continue;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const uint32_t k = keys[i];
+        if (drop_inert && k == INERT) continue;
         for (int p = 0; p < npass; p++) {
             const int sh = p * db, nb = min(db, bits - sh);
-            const uint32_t dg = (k >> sh) & ((1u << nb) - 1u);
-            const unsigned peers = __match_any_sync(FULLS, ok ? dg : 0xffffffffu) & act;
-            if (ok && (threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&h[p][dg], (uint32_t)__popc(peers));
+            atomicAdd(&h[p][(k >> sh) & ((1u << nb) - 1u)], 1u);
         }
     }
     __syncthreads();
@@ -292,7 +284,7 @@ __device__ __forceinline__ unsigned long long ld_status(const unsigned long long
 }
 
 template <bool PAYLOAD>
-__global__ __launch_bounds__(RS_T, 4) void k_rs_onesweep(const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin,
+__global__ __launch_bounds__(RS_T) void k_rs_onesweep(const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin,
                                                       uint32_t* __restrict__ kout, uint32_t* __restrict__ vout,
                                                       const uint2* __restrict__ pin, uint2* __restrict__ pout,
                                                       const int* __restrict__ n_ptr, int64_t cap, int shift, int nbits,
@@ -355,28 +347,13 @@ __global__ __launch_bounds__(RS_T, 4) void k_rs_onesweep(const uint32_t* __restr
             st_status(st, ep | ST_PRE | tot);
         } else {
             st_status(st, ep | ST_AGG | tot);
-            // Windowed look-back: the status words of up to LB predecessors are loaded together
-            // (independent loads in flight instead of one dependent L2 trip per predecessor),
-            // then consumed in order until an inclusive prefix; a predecessor that has not
-            // published yet is re-polled (with the window behind it) — same sums as one at a time.
-            constexpr int LB = 8;
-            int p = tile - 1;
-            bool found = false;
-            while (!found) {
-                unsigned long long w[LB];
-#pragma unroll
-                for (int i = 0; i < LB; i++) w[i] = p - i >= 0 ? ld_status(status + (size_t)(p - i) * RS_BINS + d) : 0ull;
-                int used = 0;
-#pragma unroll
-                for (int i = 0; i < LB; i++) {
-                    if (found || used < i || p - i < 0) continue;  // consumed in order only
-                    const unsigned long long v = w[i];
-                    if ((v >> 34) != epoch || !(v & (ST_AGG | ST_PRE))) continue;  // not ready: re-poll
-                    excl += (uint32_t)v;
-                    used = i + 1;
-                    found = (v & ST_PRE) != 0;
-                }
-                p -= used;
+            for (int p = tile - 1; p >= 0; p--) {
+                unsigned long long w;
+                do {
+                    w = ld_status(status + (size_t)p * RS_BINS + d);
+                } while ((w >> 34) != epoch || !(w & (ST_AGG | ST_PRE)));
+                excl += (uint32_t)w;
+                if (w & ST_PRE) break;
             }
             st_status(st, ep | ST_PRE | (excl + tot));
         }
