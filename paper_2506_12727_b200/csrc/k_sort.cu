@@ -75,16 +75,18 @@ __device__ __forceinline__ unsigned digit_peers(uint32_t d, bool ok, int nbits) 
 }
 
 // per-tile digit histogram → counts[digit * ntiles + tile]
+template <int IPT>
 __global__ __launch_bounds__(RS_T) void k_rs_hist(const uint32_t* __restrict__ keys, const int* __restrict__ n_ptr,
                                                   int64_t cap, int shift, int nbits, int* __restrict__ counts,
                                                   int ntiles) {
+    constexpr int TILE = RS_T * IPT;
     __shared__ int h[RS_BINS];
     h[threadIdx.x] = 0;
     __syncthreads();
     const int n = (int)min((int64_t)*n_ptr, cap);
-    const int t0 = blockIdx.x * RS_TILE;
+    const int t0 = blockIdx.x * TILE;
     const uint32_t mask = (1u << nbits) - 1u;
-    for (int i = t0 + threadIdx.x; i < min(n, t0 + RS_TILE); i += RS_T) atomicAdd(&h[(keys[i] >> shift) & mask], 1);
+    for (int i = t0 + threadIdx.x; i < min(n, t0 + TILE); i += RS_T) atomicAdd(&h[(keys[i] >> shift) & mask], 1);
     __syncthreads();
     if (threadIdx.x <= mask) counts[(int64_t)threadIdx.x * ntiles + blockIdx.x] = h[threadIdx.x];
 }
@@ -94,41 +96,42 @@ __global__ __launch_bounds__(RS_T) void k_rs_hist(const uint32_t* __restrict__ k
 // consecutive threads: every digit's run lands contiguously at
 // offsets[digit * ntiles + tile], so global writes are coalesced.
 // Optionally moves a 64-bit payload with each key.
-template <bool PAYLOAD>
+template <bool PAYLOAD, int IPT>
 __global__ __launch_bounds__(RS_T) void k_rs_scatter(const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin,
                                                      uint32_t* __restrict__ kout, uint32_t* __restrict__ vout,
                                                      const uint2* __restrict__ pin, uint2* __restrict__ pout,
                                                      const int* __restrict__ n_ptr, int64_t cap, int shift, int nbits,
                                                      const int* __restrict__ offs, int ntiles,
                                                      int* __restrict__ range_min) {
+    constexpr int TILE = RS_T * IPT;
     __shared__ uint32_t hist[RS_NW][RS_BINS];
     __shared__ uint32_t dstart[RS_BINS];   // first local position of each digit
     __shared__ uint32_t gdelta[RS_BINS];   // global offset − local start, per digit
-    __shared__ uint32_t sk[RS_TILE], sv[RS_TILE];
-    __shared__ uint2 sp[PAYLOAD ? RS_TILE : 1];
+    __shared__ uint32_t sk[TILE], sv[TILE];
+    __shared__ uint2 sp[PAYLOAD ? TILE : 1];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const unsigned lt = (1u << lane) - 1u;
     const int n = (int)min((int64_t)*n_ptr, cap);
-    const int t0 = blockIdx.x * RS_TILE;
+    const int t0 = blockIdx.x * TILE;
     if (t0 >= n) return;
-    const int nt = min(RS_TILE, n - t0);
+    const int nt = min(TILE, n - t0);
     const uint32_t mask = (1u << nbits) - 1u;
 #pragma unroll
     for (int i = 0; i < RS_BINS / 32; i++) hist[warp][lane + 32 * i] = 0;
     __syncwarp();
-    uint32_t key[RS_IPT], val[RS_IPT], loc[RS_IPT];
-    uint2 pay[PAYLOAD ? RS_IPT : 1];
+    uint32_t key[IPT], val[IPT], loc[IPT];
+    uint2 pay[PAYLOAD ? IPT : 1];
 #pragma unroll
-    for (int it = 0; it < RS_IPT; it++) {
-        const int p = warp * 32 * RS_IPT + it * 32 + lane;
+    for (int it = 0; it < IPT; it++) {
+        const int p = warp * 32 * IPT + it * 32 + lane;
         const bool ok = p < nt;
         key[it] = ok ? kin[t0 + p] : 0u;
         val[it] = ok ? vin[t0 + p] : 0u;
         if (PAYLOAD) pay[PAYLOAD ? it : 0] = ok ? pin[t0 + p] : make_uint2(0u, 0u);
     }
 #pragma unroll
-    for (int it = 0; it < RS_IPT; it++) {
-        const int p = warp * 32 * RS_IPT + it * 32 + lane;
+    for (int it = 0; it < IPT; it++) {
+        const int p = warp * 32 * IPT + it * 32 + lane;
         const bool ok = p < nt;
         const uint32_t d = (key[it] >> shift) & mask;
         const unsigned peers = digit_peers(d, ok, nbits);
@@ -157,8 +160,8 @@ __global__ __launch_bounds__(RS_T) void k_rs_scatter(const uint32_t* __restrict_
     }
     __syncthreads();
 #pragma unroll
-    for (int it = 0; it < RS_IPT; it++) {
-        const int p = warp * 32 * RS_IPT + it * 32 + lane;
+    for (int it = 0; it < IPT; it++) {
+        const int p = warp * 32 * IPT + it * 32 + lane;
         if (p < nt) {
             const uint32_t l = hist[warp][(key[it] >> shift) & mask] + loc[it];
             sk[l] = key[it];
@@ -197,10 +200,16 @@ __global__ __launch_bounds__(RS_T) void k_rs_scatter(const uint32_t* __restrict_
 // With range_min (entries: keys < 2^bits are bucket ids) the last pass also writes each
 // bucket's first position (atomicMin; the caller fills range_min with INT_MAX first and
 // closes empty buckets afterwards) and skips writing the sorted keys.
-int radix_sort_3k(uint32_t* k, uint32_t* v, uint32_t* k2, uint32_t* v2, uint2* pl, uint2* pl2, const int* n_ptr,
+#ifndef MVGS_RS3_IPT
+#define MVGS_RS3_IPT 8  // keys per thread of the three-kernel passes' tiles
+#endif
+constexpr int RS3_IPT = MVGS_RS3_IPT;
+
+template <int IPT>
+static int radix_sort_3k_t(uint32_t* k, uint32_t* v, uint32_t* k2, uint32_t* v2, uint2* pl, uint2* pl2, const int* n_ptr,
                int64_t cap, int bits, int* counts, int* scan_tmp, cudaStream_t s, cudaError_t* err,
-               int* range_min = nullptr) {
-    const int ntiles = radix_tiles(cap);
+               int* range_min) {
+    const int ntiles = (int)((cap + RS_T * IPT - 1) / (RS_T * IPT));  // ≤ radix_tiles(cap): counts fit
     const int npass = (bits + 7) / 8;
     const int db = npass ? (bits + npass - 1) / npass : 0;
     *err = cudaSuccess;
@@ -210,15 +219,20 @@ int radix_sort_3k(uint32_t* k, uint32_t* v, uint32_t* k2, uint32_t* v2, uint2* p
     for (int pass = 0; pass < npass; pass++) {
         const int shift = pass * db;
         const int nb = min(db, bits - shift);
-        k_rs_hist<<<ntiles, RS_T, 0, s>>>(ks, n_ptr, cap, shift, nb, counts, ntiles);
+        k_rs_hist<IPT><<<ntiles, RS_T, 0, s>>>(ks, n_ptr, cap, shift, nb, counts, ntiles);
         // only the live digits' counts (digit-major layout): a 7-bit pass scans half the table
         if ((*err = scan_exclusive(counts, (1 << nb) * ntiles, nullptr, scan_tmp, s)) != cudaSuccess) return pass;
         int* rm = (pass == npass - 1) ? range_min : nullptr;
-        if (pl)
-            k_rs_scatter<true><<<ntiles, RS_T, 0, s>>>(ks, vs, kd, vd, ps, pd, n_ptr, cap, shift, nb, counts, ntiles,
-                                                       rm);
-        else
-            k_rs_scatter<false><<<ntiles, RS_T, 0, s>>>(ks, vs, kd, vd, nullptr, nullptr, n_ptr, cap, shift, nb,
+        bool launched = false;
+        if constexpr (IPT == 8) {  // payload tiles only at 8 keys per thread (static shared memory)
+            if (pl) {
+                k_rs_scatter<true, IPT><<<ntiles, RS_T, 0, s>>>(ks, vs, kd, vd, ps, pd, n_ptr, cap, shift, nb, counts,
+                                                               ntiles, rm);
+                launched = true;
+            }
+        }
+        if (!launched)
+            k_rs_scatter<false, IPT><<<ntiles, RS_T, 0, s>>>(ks, vs, kd, vd, nullptr, nullptr, n_ptr, cap, shift, nb,
                                                         counts, ntiles, rm);
         if ((*err = cudaGetLastError()) != cudaSuccess) return pass;
         uint32_t* t = ks; ks = kd; kd = t;
@@ -226,6 +240,14 @@ int radix_sort_3k(uint32_t* k, uint32_t* v, uint32_t* k2, uint32_t* v2, uint2* p
         uint2* tp = ps; ps = pd; pd = tp;
     }
     return npass;
+}
+
+int radix_sort_3k(uint32_t* k, uint32_t* v, uint32_t* k2, uint32_t* v2, uint2* pl, uint2* pl2, const int* n_ptr,
+               int64_t cap, int bits, int* counts, int* scan_tmp, cudaStream_t s, cudaError_t* err,
+               int* range_min = nullptr) {
+    // payload tiles stay at 8 keys per thread (static shared memory); key/value tiles take RS3_IPT
+    return pl ? radix_sort_3k_t<8>(k, v, k2, v2, pl, pl2, n_ptr, cap, bits, counts, scan_tmp, s, err, range_min)
+              : radix_sort_3k_t<RS3_IPT>(k, v, k2, v2, pl, pl2, n_ptr, cap, bits, counts, scan_tmp, s, err, range_min);
 }
 
 // ---------------------------------------------------------------- onesweep
