@@ -24,6 +24,13 @@
 
 namespace mvgs {
 
+#ifndef MVGS_FWD_UNROLL
+#define MVGS_FWD_UNROLL 1  // inner entry loops (experiment knobs)
+#endif
+#ifndef MVGS_BWD_UNROLL
+#define MVGS_BWD_UNROLL 1
+#endif
+constexpr int kFwdUnroll = MVGS_FWD_UNROLL, kBwdUnroll = MVGS_BWD_UNROLL;
 constexpr int RT = 128;            // threads per CTA = entries per staged batch
 constexpr int NWR = RT / 32;       // warps per CTA
 constexpr unsigned FULLR = 0xffffffffu;
@@ -274,6 +281,7 @@ __global__ __launch_bounds__(RT) void k_render_fwd_p(Launch L, float* __restrict
             const int cnt = min(RT, end - b0);
             const int wl = threadIdx.x >> 5;
             const int nl = warp_batch_list(smask, cnt, wl, threadIdx.x & 31, slist[wl]);
+#pragma unroll(kFwdUnroll)
             for (int u = 0; u < nl && !(done0 && done1); u++) {
                 const int j = slist[wl][u];
                 if (CNT) nev += (unsigned)!done0 + (unsigned)!done1;
@@ -683,6 +691,7 @@ __global__ __launch_bounds__(128, 6) void k_render_bwd_p(Launch L, const float* 
         __syncthreads();
         // this warp's entries of the batch (culled by its pixel block), walked back to front
         const int nl = warp_batch_list(smask, min(cnt, wmax - b0), warp, lane, slist[warp]);
+#pragma unroll(kBwdUnroll)
         for (int u = nl - 1; u >= 0; u--) {
             const int jj = slist[warp][u];
             const int j = b0 + jj;
