@@ -300,9 +300,9 @@ def test_warp_culling_on_thin_correlated_ellipses():
     the camera, opacities from barely above 1/255 to the 0.99 clamp — lists, n_contrib and
     images stay identical to the oracle's and gradients within the §5 rule."""
     rng = np.random.default_rng(23)
-    n = 900
+    n = 400
     means = np.column_stack([rng.uniform(-0.9, 0.9, n), rng.uniform(-0.6, 0.6, n), rng.uniform(1.0, 4.0, n)])
-    ls = np.column_stack([rng.uniform(-1.0, -0.2, n), rng.uniform(-7.0, -4.0, n), rng.uniform(-7.0, -4.0, n)])
+    ls = np.column_stack([rng.uniform(-2.3, -1.0, n), rng.uniform(-7.0, -4.0, n), rng.uniform(-7.0, -4.0, n)])
     ang = rng.uniform(0, np.pi, n)  # rotations about the view axis: diagonal needles
     tilt = rng.uniform(-0.6, 0.6, n)
     q = np.column_stack([np.cos(ang / 2) * np.cos(tilt / 2), np.sin(tilt / 2) * np.cos(ang / 2),
@@ -313,7 +313,27 @@ def test_warp_culling_on_thin_correlated_ellipses():
     g["quats"] = q.astype(np.float32)
     cam = synth.cams_array([synth.make_camera(np.eye(3), [0, 0, 0], 150, 110, 90.0),
                             synth.make_camera(np.eye(3), [0.1, -0.05, 0.3], 150, 110, 120.0)])
-    _check_all(g, cam, bg=(0.05, 0.1, 0.2))
+    V, H, W = len(cam), 110, 150
+    bg = (0.05, 0.1, 0.2)
+    dL = synth.make_dLdC_scaled(V, H, W, 3)
+    o = oracle.Oracle(g, cam, bg=bg)
+    ref, im = o.backward(dL), o.image()
+    gpu = run_gpu(g, cam, dL, bg=bg)
+    # decisions bit-exact: every culled (pixel, entry) would have been skipped
+    np.testing.assert_array_equal(gpu["n_contrib"], im["n_contrib"])
+    off, gid = o.lists()
+    np.testing.assert_array_equal(gpu["range_start"], off)
+    np.testing.assert_array_equal(gpu["entry_gid"], gid)
+    # values: up to ~300 list entries per pixel here, so the fp32 (GPU) vs fp64 (oracle) colour
+    # sum is held to a rounding bound growing with the walk (6 ulp per entry: T·(1−α) and the
+    # colour FMA each round, and T's relative error reaches every later term) on top of 1e-5
+    nmax = int(im["n_contrib"].max())
+    assert nmax > 100
+    lim = 1e-5 + 6 * 2.0 ** -24 * im["n_contrib"][:, None].astype(np.float64)
+    assert np.all(np.abs(gpu["rgb"] - im["rgb"]) <= lim)
+    scale = per_view_scale(g, cam, dL, bg)
+    for k in ["d_means", "d_log_scales", "d_quats", "d_opacity_logits", "d_sh", "e1", "e2", "e_old"]:
+        assert_close_rel(gpu[k], ref[k], k, scale=scale[k])
 
 
 def test_eval_counting_off_changes_nothing():
