@@ -133,6 +133,7 @@ class Oracle:
 
     def forward(self):
         lib().oracle_forward(self._h)
+        self._rendered = True
         return self.image()
 
     def phase_times(self):
@@ -148,9 +149,12 @@ class Oracle:
         d = np.ascontiguousarray(dLdC, np.float32)
         assert d.shape == (self.V, 3, self.H, self.W)
         lib().oracle_backward(self._h, _p(d))
+        self._rendered = True
         return self.grads()
 
     def image(self):
+        if not getattr(self, "_rendered", False):
+            raise RuntimeError("Oracle.image() before forward()/backward()")
         rgb = np.zeros((self.V, 3, self.H, self.W))
         Tf = np.zeros((self.V, self.H, self.W))
         nc = np.zeros((self.V, self.H, self.W), np.int32)
