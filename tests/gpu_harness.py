@@ -45,13 +45,26 @@ def run_gpu(g, cams, dLdC=None, bg=(0.0, 0.0, 0.0), max_pairs=0, max_entries=0, 
 
 def assert_close_rel(got, ref, name, rtol=1e-3, floor=1e-6, scale=None, ctol=1e-4):
     """per tensor ‖Δ‖/‖ref‖ ≤ rtol and per element
-    |Δ| ≤ rtol·|ref| + ctol·scale + floor·max|ref|, where `scale` (optional) is the
-    magnitude of the per-view terms the element sums (Σ_v |ref_v|): an element that
-    is a cancellation of larger per-view terms is held to fp32 accuracy of those
-    terms, not of the cancelled result.  Reports the worst elements."""
-    got = np.asarray(got, np.float64).reshape(-1)
-    ref = np.asarray(ref, np.float64).reshape(-1)
-    sc = np.zeros_like(ref) if scale is None else np.asarray(scale, np.float64).reshape(-1)
+    |Δ| ≤ rtol·|ref| + ctol·(scale + ‖scale row‖) + floor·max|ref|, where `scale`
+    (optional, default |ref|) is the magnitude of the per-view terms the element sums
+    (Σ_v |ref_v|): an element that is a cancellation of larger per-view terms is held to
+    fp32 accuracy of those terms, not of the cancelled result; and a component of a
+    Gaussian's gradient row (its 3 mean components, 4 quaternion components, SH
+    coefficients …, axis 0 = Gaussian) is held to that accuracy relative to the row's
+    norm, since the chain rule mixes the row's components through rotations and
+    Jacobians (a component that cancels to ~1e-5 of its row carries the row's rounding).
+    Reports the worst elements."""
+    g0 = np.asarray(got, np.float64)
+    r0 = np.asarray(ref, np.float64)
+    s0 = np.abs(r0) if scale is None else np.asarray(scale, np.float64)
+    if r0.ndim >= 2 and r0.shape[0] > 0:
+        rown = np.linalg.norm(s0.reshape(r0.shape[0], -1), axis=1)
+        rown = np.broadcast_to(rown.reshape((-1,) + (1,) * (r0.ndim - 1)), r0.shape).reshape(-1)
+    else:
+        rown = np.zeros(r0.size)
+    got = g0.reshape(-1)
+    ref = r0.reshape(-1)
+    sc = (np.zeros_like(ref) if scale is None else s0.reshape(-1)) + rown
     assert got.shape == ref.shape, name
     d = np.abs(got - ref)
     nref = np.linalg.norm(ref)
@@ -63,7 +76,7 @@ def assert_close_rel(got, ref, name, rtol=1e-3, floor=1e-6, scale=None, ctol=1e-
     lim = rtol * np.abs(ref) + ctol * sc + floor * mx
     bad = np.argsort(-(d - lim))[:10]
     msg = f"{name}: tensor rel {rel:.3e}; worst " + ", ".join(
-        f"[{i}] got {got[i]:.6e} ref {ref[i]:.6e}" for i in bad[:5])
+        f"[{i}] got {got[i]:.6e} ref {ref[i]:.6e} lim {lim[i]:.3e}" for i in bad[:5])
     assert rel <= rtol, msg
     assert np.all(d <= lim), msg
 
