@@ -79,6 +79,9 @@ __device__ __forceinline__ void pixel_pair(int tx, int ty, int& x, int& y0, int&
 // Bit j of the result: the entry may touch warp j's rows 4j … 4j+3 of the tile.
 __device__ __forceinline__ unsigned warp_block_mask(float px, float py, float A, float B, float C, float sb,
                                                     float X0, float Y0) {
+#ifdef MVGS_NO_CULL
+    return 0xfu;  // experiment / diagnosis: every warp walks every entry
+#endif
     const float L = -2.0f * sb;
     const double det = (double)A * (double)C - (double)B * (double)B;
     if (!(L > 0.01f) || !(det > 0.0) || (double)B * (double)B > 0.9 * (double)A * (double)C) return 0xfu;
