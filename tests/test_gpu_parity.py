@@ -331,9 +331,20 @@ def test_warp_culling_on_thin_correlated_ellipses():
     assert nmax > 100
     lim = 1e-5 + 6 * 2.0 ** -24 * im["n_contrib"][:, None].astype(np.float64)
     assert np.all(np.abs(gpu["rgb"] - im["rgb"]) <= lim)
+    # gradients: the conic → Σ' step of the chain has condition number κ = 1/(1 − ρ²),
+    # ρ² = B²/(A·C); these needles reach κ ≈ 240, which amplifies the fp32 rounding of the
+    # per-pair conic sums (measured: 1.1e-4 of the gradient row).  Elements of Gaussians with
+    # κ > 100 get their per-view/row term scaled by κ/100.
+    pr = o.pairs()
+    AC = pr["A"].astype(np.float64) * pr["C"]
+    rho2 = np.where((pr["vis"] > 0) & (AC > 0), pr["B"].astype(np.float64) ** 2 / np.where(AC > 0, AC, 1), 0.0)
+    kappa = np.max(1.0 / np.maximum(1.0 - rho2, 1e-12), axis=0)  # per Gaussian, over views
+    assert kappa.max() > 100  # the adversarial case is exercised
+    amp = np.maximum(1.0, kappa / 100.0)
     scale = per_view_scale(g, cam, dL, bg)
     for k in ["d_means", "d_log_scales", "d_quats", "d_opacity_logits", "d_sh", "e1", "e2", "e_old"]:
-        assert_close_rel(gpu[k], ref[k], k, scale=scale[k])
+        a = amp.reshape((-1,) + (1,) * (ref[k].ndim - 1))
+        assert_close_rel(gpu[k], ref[k], k, scale=scale[k] * a)
 
 
 def test_eval_counting_off_changes_nothing():
