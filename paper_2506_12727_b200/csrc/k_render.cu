@@ -68,32 +68,51 @@ __device__ __forceinline__ void pixel_pair(int tx, int ty, int& x, int& y0, int&
     y1 = y0 + 2;
 }
 
-// Exact warp-block culling.  A pixel can pass the skip test only if
-// power ≥ sb, i.e. inside the ellipse dᵀMd ≤ L = −2·sb, M = [[A, B], [B, C]]; that
-// ellipse lies in the box |dx| ≤ √(L·C/det), |dy| ≤ √(L·A/det).  An entry whose box
-// (inflated by 1 % + 0.01 in L and 0.01 px) misses a warp's 16×4 pixel block is never
-// evaluated by that warp.  The margins must also cover the fp32 rounding of the CA
-// power that takes the real decision: with B² ≤ 0.9·A·C the power's terms are within
-// 40× of dᵀMd near the ellipse, so its rounding error (≲ 1e-4) is far below the slack;
-// more correlated (near-degenerate) conics, L ≤ 0.01 and det ≤ 0 are never culled.
-// Bit j of the result: the entry may touch warp j's rows 4j … 4j+3 of the tile.
-__device__ __forceinline__ unsigned warp_block_mask(float px, float py, float A, float B, float C, float sb,
-                                                    float X0, float Y0) {
+// Exact warp-block culling.  A pixel reaches the canonical exp only if
+// its CA power ≥ sb.  With d = μ' − p and q(d) = dᵀMd, M = [[A, B], [B, C]] (the stored
+// fp32 conic), the exact power is −q/2 and the CA value differs from it by at most
+// ε·T(d), T(d) = A·dx² + C·dy² + 2|B·dx·dy|, ε = 8·2⁻²⁴ (a few fp32 roundings).  q_min, the
+// minimum of q over a warp's 16×4 block (0 if μ' lies in it, else the smallest of q on the
+// four edges, each a 1-D quadratic taken at its clamped minimiser), is evaluated in fp32
+// with an error below another ε·T_max (evaluating at a rounded minimiser only raises q by
+// C·δ², δ ~ 1e-7·|t|, far inside the 0.01 slack).  No pixel of the block can pass when
+//   q_min > 1.01·L + 0.01 + 3ε·T_max,   L = −2·sb,  T_max ≥ T over the block.
+// Conics that are not positive definite are never culled.  Bit j: the entry may touch
+// warp j's rows 4j … 4j+3 of the tile.
+__device__ __forceinline__ float q_edge(float A, float B, float C, float fixed, float lo, float hi, bool fix_x) {
+    if (fix_x) {  // dx fixed, dy clamped to [lo, hi] at the 1-D minimiser
+        const float t = fminf(hi, fmaxf(lo, -B * fixed / C));
+        return A * fixed * fixed + 2.0f * B * fixed * t + C * t * t;
+    }
+    const float t = fminf(hi, fmaxf(lo, -B * fixed / A));
+    return A * t * t + 2.0f * B * t * fixed + C * fixed * fixed;
+}
+
+__device__ __noinline__ unsigned warp_block_mask(float px, float py, float A, float B, float C, float sb, float X0,
+                                                 float Y0) {
 #ifdef MVGS_NO_CULL
     return 0xfu;  // experiment / diagnosis: every warp walks every entry
 #endif
     const float L = -2.0f * sb;
-    const double det = (double)A * (double)C - (double)B * (double)B;
-    if (!(L > 0.01f) || !(det > 0.0) || (double)B * (double)B > 0.9 * (double)A * (double)C) return 0xfu;
-    const double Lm = (double)L * 1.01 + 0.01;
-    const float hx = (float)sqrt(Lm * (double)C / det) + 0.01f;
-    const float hy = (float)sqrt(Lm * (double)A / det) + 0.01f;
-    if (!(px + hx >= X0 && px - hx <= X0 + 15.0f)) return 0u;
+    if (!(A > 0.0f) || !(C > 0.0f) || !((double)A * (double)C - (double)B * (double)B > 0.0) || !(L > 0.0f))
+        return 0xfu;
+    const float eps3 = 3.0f * 8.0f * 5.9604644775390625e-8f;
+    const float Lm = L * 1.01f + 0.01f;
+    const float dxlo = px - (X0 + 15.0f), dxhi = px - X0;  // d = μ' − p over the block (exact: small integers)
+    const float dxm = fmaxf(fabsf(dxlo), fabsf(dxhi));
     unsigned m = 0;
 #pragma unroll
     for (int w = 0; w < 4; w++) {
-        const float ylo = Y0 + 4.0f * w, yhi = ylo + 3.0f;
-        if (py + hy >= ylo && py - hy <= yhi) m |= 1u << w;
+        const float y0 = Y0 + 4.0f * w;
+        const float dylo = py - (y0 + 3.0f), dyhi = py - y0;
+        const float dym = fmaxf(fabsf(dylo), fabsf(dyhi));
+        float qmin = 0.0f;
+        if (!(dxlo <= 0.0f && dxhi >= 0.0f && dylo <= 0.0f && dyhi >= 0.0f)) {  // centre outside the block
+            qmin = fminf(fminf(q_edge(A, B, C, dxlo, dylo, dyhi, true), q_edge(A, B, C, dxhi, dylo, dyhi, true)),
+                         fminf(q_edge(A, B, C, dylo, dxlo, dxhi, false), q_edge(A, B, C, dyhi, dxlo, dxhi, false)));
+        }
+        const float tmax = A * dxm * dxm + C * dym * dym + 2.0f * fabsf(B) * dxm * dym;
+        if (!(qmin > Lm + eps3 * tmax)) m |= 1u << w;
     }
     return m;
 }
