@@ -30,6 +30,9 @@ namespace mvgs {
 #ifndef MVGS_BWD_UNROLL
 #define MVGS_BWD_UNROLL 1
 #endif
+#ifndef MVGS_BWD_MINB
+#define MVGS_BWD_MINB 6  // resident CTAs per SM asked of the packed backward (register cap 65536/(128·MINB))
+#endif
 constexpr int kFwdUnroll = MVGS_FWD_UNROLL, kBwdUnroll = MVGS_BWD_UNROLL;
 constexpr int RT = 128;            // threads per CTA = entries per staged batch
 constexpr int NWR = RT / 32;       // warps per CTA
@@ -596,6 +599,9 @@ struct BwdConsts {
 };
 
 __device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
+__device__ __forceinline__ void st_shared_f32(uint32_t addr, float v) {
+    asm volatile("st.shared.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
+}
 __device__ __forceinline__ float ex2_approx(float x) {
     float y;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -622,7 +628,7 @@ __device__ __forceinline__ void bwd_exp(float power, float o, float& G, float& o
 }
 
 template <bool CNT>
-__global__ __launch_bounds__(128, 6) void k_render_bwd_p(Launch L, const float* __restrict__ dL_drgb,
+__global__ __launch_bounds__(128, MVGS_BWD_MINB) void k_render_bwd_p(Launch L, const float* __restrict__ dL_drgb,
                                                       const float* __restrict__ in_T,
                                                       const int32_t* __restrict__ in_n) {
     constexpr int NT = 128, NW = 4, RB = 128;
@@ -683,6 +689,9 @@ __global__ __launch_bounds__(128, 6) void k_render_bwd_p(Launch L, const float* 
     // per-value scale applied by the owner after the reduction (see the V terms below)
     const float oscale = my_id == 0 ? -hw : my_id == 1 ? -hh : (my_id == 3 || my_id == 5) ? -0.5f : my_id == 4 ? -1.f : 1.f;
     float* wacc = sacc[warp];
+    // 32-bit shared address of this lane's value slot: the owner store is one STS per entry
+    // (a generic pointer here is rematerialised every iteration under the register cap)
+    const uint32_t wslot = (uint32_t)__cvta_generic_to_shared(wacc + my_id);
     const float2 nfx = f2(-(float)x, -(float)x), nfy = f2(-(float)y0, -(float)(y0 + 2));
     const float2 one = f2(1.f, 1.f), mone = f2(-1.f, -1.f), mhalf = f2(-0.5f, -0.5f);
     const float2 hw2 = f2(hw * hw, hw * hw), hh2 = f2(hh * hh, hh * hh);
@@ -776,7 +785,7 @@ __global__ __launch_bounds__(128, 6) void k_render_bwd_p(Launch L, const float* 
             val[8] = wg.x + wg.y;
             val[9] = wb.x + wb.y;
             const float sum = warp_transpose_reduce10(val, lane);
-            if (owner) wacc[jj * NG + my_id] = sum * oscale;
+            if (owner) st_shared_f32(wslot + 4u * (uint32_t)(jj * NG), sum * oscale);
         }
         __syncthreads();
         for (int i = threadIdx.x; i < cnt * NG; i += NT) {
