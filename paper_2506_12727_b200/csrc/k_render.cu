@@ -689,9 +689,6 @@ __global__ __launch_bounds__(128, MVGS_BWD_MINB) void k_render_bwd_p(Launch L, c
     // per-value scale applied by the owner after the reduction (see the V terms below)
     const float oscale = my_id == 0 ? -hw : my_id == 1 ? -hh : (my_id == 3 || my_id == 5) ? -0.5f : my_id == 4 ? -1.f : 1.f;
     float* wacc = sacc[warp];
-    // 32-bit shared address of this lane's value slot: the owner store is one STS per entry
-    // (a generic pointer here is rematerialised every iteration under the register cap)
-    const uint32_t wslot = (uint32_t)__cvta_generic_to_shared(wacc + my_id);
     const float2 nfx = f2(-(float)x, -(float)x), nfy = f2(-(float)y0, -(float)(y0 + 2));
     const float2 one = f2(1.f, 1.f), mone = f2(-1.f, -1.f), mhalf = f2(-0.5f, -0.5f);
     const float2 hw2 = f2(hw * hw, hw * hw), hh2 = f2(hh * hh, hh * hh);
@@ -785,7 +782,7 @@ __global__ __launch_bounds__(128, MVGS_BWD_MINB) void k_render_bwd_p(Launch L, c
             val[8] = wg.x + wg.y;
             val[9] = wb.x + wb.y;
             const float sum = warp_transpose_reduce10(val, lane);
-            if (owner) st_shared_f32(wslot + 4u * (uint32_t)(jj * NG), sum * oscale);
+            if (owner) wacc[jj * NG + my_id] = sum * oscale;
         }
         __syncthreads();
         for (int i = threadIdx.x; i < cnt * NG; i += NT) {
