@@ -53,6 +53,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="garden", choices=list(synth.CONFIGS))
+    ap.add_argument("--views", type=int, default=0,
+                    help="views per GPU per step (default: the config's batch); the views-per-batch sweep")
     ap.add_argument("--impl", default="mvgs", choices=["mvgs", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=8)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -165,7 +167,7 @@ def run_mvgs(args):
     from paper_2506_12727_b200.dist import GradBuffer, adc_stats_allreduce, view_shard
 
     cfg = synth.CONFIGS[args.config]
-    Vr = cfg.V if N == 1 else cfg.V  # views per rank (weak scaling: per-GPU batch fixed)
+    Vr = args.views or cfg.V  # views per rank (weak scaling: the per-GPU batch is fixed)
     g_np, cams_all = synth.make_scene(synth.scaled(cfg, V=Vr * N))
     lo, hi = view_shard(Vr * N, N, rank)
     cams = synth.subset_views(cams_all, lo, hi)
@@ -338,6 +340,9 @@ def run_mvgs(args):
                    "l2": "inputs larger than L2 (params %.0f MB)" % (sum(v.nbytes for v in g_np.values()
                                                                        if isinstance(v, np.ndarray)) / 1e6),
                    "Q": st["Q"], "K": st["K"], "max_bucket": st["max_bucket"], "n_visible": st["n_visible"],
+                   # structural statistics: ρ = Q/(V·P), κ = K/Q_visible, mean list length
+                   "rho": round(st["Q"] / max(1, Vr * P), 4), "kappa": round(st["K"] / max(1, st["n_visible"]), 3),
+                   "mean_bucket": round(st["K"] / max(1, Vr * st["tiles_x"] * st["tiles_y"]), 1),
                    "eval_fwd_per_px": round(st["eval_fwd"] / (Vr * cfg.W * cfg.H), 2),
                    "eval_bwd_per_px": round(st["eval_bwd"] / (Vr * cfg.W * cfg.H), 2),
                    "exp_fwd_per_px": round(st["exp_fwd"] / (Vr * cfg.W * cfg.H), 2),
