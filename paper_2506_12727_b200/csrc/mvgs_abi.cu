@@ -309,11 +309,15 @@ mvgs_status mvgs_preprocess(mvgs_ctx* ctx, const mvgs_gaussians* g, const mvgs_c
             ctx->cap_cams = n;
         }
     }
-    // cameras: host → pinned staging (after the previous copy drained) → device
-    CK(cudaEventSynchronize(ctx->cams_ev));
+    // cameras: host → pinned staging (after the previous copy drained) → device.  Under CUDA
+    // graph capture there is no previous copy to wait for: the captured copy reads the staging
+    // buffer at every replay, i.e. the cameras given here.
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    CK(cudaStreamIsCapturing(s, &cap));
+    if (cap == cudaStreamCaptureStatusNone) CK(cudaEventSynchronize(ctx->cams_ev));
     memcpy(ctx->h_cams, cams, sizeof(mvgs_camera) * V);
     CK(cudaMemcpyAsync(ctx->d_cams, ctx->h_cams, sizeof(mvgs_camera) * V, cudaMemcpyHostToDevice, s));
-    CK(cudaEventRecord(ctx->cams_ev, s));
+    if (cap == cudaStreamCaptureStatusNone) CK(cudaEventRecord(ctx->cams_ev, s));
 
     ctx->g = *g;
     Launch& L = ctx->L;

@@ -362,3 +362,49 @@ def test_eval_counting_off_changes_nothing():
         assert torch.equal(x, y)
     st = mvgs.query(R.ctx)
     assert st["eval_fwd"] == 0 and st["exp_fwd"] == 0
+
+
+def test_step_captures_in_a_cuda_graph():
+    """preprocess → render_fwd → render_bwd → adc_stats is capturable in one CUDA graph once
+    capacities are reserved (mvgs.h ordering rules): replays reproduce the eager step —
+    images and counts bit-exact, gradients to the §5 rule (the backward's per-pair sums are
+    atomics, so their order may differ)."""
+    import torch
+    from paper_2506_12727_b200 import mvgs
+    from gpu_harness import to_dev
+    (g, cams), kw = CASES["object360_small"]
+    V, H, W = len(cams), int(cams[0]["height"]), int(cams[0]["width"])
+    dL = torch.from_numpy(synth.make_dLdC_scaled(V, H, W, 9)).cuda()
+    gd = to_dev(g)
+    R = mvgs.Rasterizer(0)
+    R.preprocess(gd, cams, kw["bg"])  # sizes and reserves
+    outs = R.alloc_forward()
+    grads, adc = R.alloc_backward()
+
+    def step():
+        mvgs.preprocess(R.ctx, gd, R.cams, kw["bg"])
+        mvgs.render_fwd(R.ctx, *outs)
+        mvgs.render_bwd(R.ctx, dL, outs[1], outs[2])
+        mvgs.adc_stats(R.ctx, grads, adc)
+
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        step()  # warm-up on the capture stream
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    eager = [t.clone() for t in outs] + [grads[k].clone() for k in sorted(grads)] + [adc[k].clone() for k in sorted(adc)]
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        step()
+    for t in list(outs) + list(grads.values()) + list(adc.values()):
+        t.zero_()
+    graph.replay()
+    graph.replay()
+    torch.cuda.synchronize()
+    for a, b in zip(eager[:3], outs):
+        assert torch.equal(a, b)
+    for a, k in zip(eager[3:3 + len(grads)], sorted(grads)):
+        assert_close_rel(grads[k].cpu().numpy(), a.cpu().numpy(), k)
+    for a, k in zip(eager[3 + len(grads):], sorted(adc)):
+        assert_close_rel(adc[k].cpu().numpy(), a.cpu().numpy(), k)
