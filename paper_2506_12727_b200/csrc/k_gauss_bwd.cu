@@ -126,6 +126,242 @@ struct ShRows {
 #define GB_VB_SHG 1  // the same for the 3-CTA variant (80 registers)
 #endif
 
+// One visible (Gaussian, view) pair of the chain rule (S8) and its ADC terms (S9), added into
+// the Gaussian's accumulators; the SH-gradient row is updated in shared memory.
+struct GAcc {
+    float dmx = 0.f, dmy = 0.f, dmz = 0.f;
+    float G00 = 0.f, G01 = 0.f, G02 = 0.f, G11 = 0.f, G12 = 0.f, G22 = 0.f;  // ∂L/∂Σ (symmetric)
+    float dop = 0.f, e1 = 0.f, e2 = 0.f, gsx = 0.f, gsy = 0.f, nvis = 0.f;
+};
+
+template <int D, bool SHG>
+__device__ __forceinline__ void pair_chain(const mvgs_camera& c, float4 cam4, float limy, uint32_t flags, float4 pg0,
+                                           float4 pg1, float4 pg2, float mx, float my, float mz, const float* Sg,
+                                           const float* sh, float* dsh, float sW, float sH, GAcc& A) {
+    constexpr int NK = ShRows<D>::NK, NS = ShRows<D>::NS;
+    float& dmx = A.dmx; float& dmy = A.dmy; float& dmz = A.dmz;
+    float& G00 = A.G00; float& G01 = A.G01; float& G02 = A.G02;
+    float& G11 = A.G11; float& G12 = A.G12; float& G22 = A.G22;
+    float& dop = A.dop; float& e1 = A.e1; float& e2 = A.e2;
+    float& gsx = A.gsx; float& gsy = A.gsy; float& nvis = A.nvis;
+    // pg: (Σ∇x, Σ∇y, e1, ∂A) (∂B, ∂C, ∂o, ∂r) (∂g, ∂b, -, -)
+    nvis += 1.f;
+    e1 += pg0.z;
+    e2 += g_sqrt(pg0.x * pg0.x + pg0.y * pg0.y);
+    gsx += pg0.x;
+    gsy += pg0.y;
+    dop += pg1.z;
+    FastProj p;
+    fast_project(c, mx, my, mz, Sg, flags, cam4.w, limy, p);
+    const float itz = p.itz, itz2 = itz * itz;
+    // μ' (pixels) = (fx·tx/tz + cx, fy·ty/tz + cy); ∂L/∂μ' = Σ∇·(2/W, 2/H) (R2)
+    const float dpx = pg0.x * sW, dpy = pg0.y * sH;
+    float dtx = c.fx * itz * dpx;
+    float dty = c.fy * itz * dpy;
+    float dtz = -(c.fx * p.tx * itz2) * dpx - (c.fy * p.ty * itz2) * dpy;
+    // conic (A,B,C) = (c,−b,a)/det → Σ' entries (a,b,c)
+    const float dA = pg0.w, dB = pg1.x, dC = pg1.y;
+    const float id2 = g_rcp(p.det * p.det);
+    const float da = (-p.c * p.c * dA + p.b * p.c * dB - p.b * p.b * dC) * id2;
+    const float dc = (-p.b * p.b * dA + p.a * p.b * dB - p.a * p.a * dC) * id2;
+    const float db = (2.f * p.b * p.c * dA - (p.det + 2.f * p.b * p.b) * dB + 2.f * p.a * p.b * dC) * id2;
+    const float hb = 0.5f * db;
+    // ∂L/∂Σ += Tᵀ Gs T,  Gs = [[da, hb], [hb, dc]]
+    const float* T0 = p.T0;
+    const float* T1 = p.T1;
+    float GT0[3], GT1[3];  // Gs·T rows
+#pragma unroll
+    for (int j = 0; j < 3; j++) {
+        GT0[j] = da * T0[j] + hb * T1[j];
+        GT1[j] = hb * T0[j] + dc * T1[j];
+    }
+    G00 += T0[0] * GT0[0] + T1[0] * GT1[0];
+    G01 += T0[0] * GT0[1] + T1[0] * GT1[1];
+    G02 += T0[0] * GT0[2] + T1[0] * GT1[2];
+    G11 += T0[1] * GT0[1] + T1[1] * GT1[1];
+    G12 += T0[1] * GT0[2] + T1[1] * GT1[2];
+    G22 += T0[2] * GT0[2] + T1[2] * GT1[2];
+    // ∂L/∂T = 2 (Gs T) Σ
+    const float* S = Sg;
+    float dT0[3], dT1[3];
+    dT0[0] = 2.f * (GT0[0] * S[0] + GT0[1] * S[1] + GT0[2] * S[2]);
+    dT0[1] = 2.f * (GT0[0] * S[1] + GT0[1] * S[3] + GT0[2] * S[4]);
+    dT0[2] = 2.f * (GT0[0] * S[2] + GT0[1] * S[4] + GT0[2] * S[5]);
+    dT1[0] = 2.f * (GT1[0] * S[0] + GT1[1] * S[1] + GT1[2] * S[2]);
+    dT1[1] = 2.f * (GT1[0] * S[1] + GT1[1] * S[3] + GT1[2] * S[4]);
+    dT1[2] = 2.f * (GT1[0] * S[2] + GT1[1] * S[4] + GT1[2] * S[5]);
+    // T = J R_v ⇒ ∂L/∂J = ∂L/∂T R_vᵀ (only the non-constant entries of J)
+    const float* R = c.R;
+    const float dJ00 = dT0[0] * R[0] + dT0[1] * R[1] + dT0[2] * R[2];
+    const float dJ02 = dT0[0] * R[6] + dT0[1] * R[7] + dT0[2] * R[8];
+    const float dJ11 = dT1[0] * R[3] + dT1[1] * R[4] + dT1[2] * R[5];
+    const float dJ12 = dT1[0] * R[6] + dT1[1] * R[7] + dT1[2] * R[8];
+    dtz += -c.fx * itz2 * dJ00 - c.fy * itz2 * dJ11;
+    // J02 = −fx·ũx/tz: ũx = tx/tz unclamped (∂/∂tx = −fx/tz², ∂/∂tz = 2fx·ux/tz²),
+    // constant when clamped (∂/∂tz = fx·ũx/tz²) — R4
+    if (!(flags & 8u)) {
+        dtx += -c.fx * itz2 * dJ02;
+        dtz += 2.f * c.fx * p.uxc * itz2 * dJ02;
+    } else {
+        dtz += c.fx * p.uxc * itz2 * dJ02;
+    }
+    if (!(flags & 16u)) {
+        dty += -c.fy * itz2 * dJ12;
+        dtz += 2.f * c.fy * p.uyc * itz2 * dJ12;
+    } else {
+        dtz += c.fy * p.uyc * itz2 * dJ12;
+    }
+    // t = R_v μ + t_v
+    dmx += R[0] * dtx + R[3] * dty + R[6] * dtz;
+    dmy += R[1] * dtx + R[4] * dty + R[7] * dtz;
+    dmz += R[2] * dtx + R[5] * dty + R[8] * dtz;
+    // colour: rgb = max(0, Σ Y_k(dir) sh_k + 0.5), dir = (μ − c_v)/‖μ − c_v‖
+    const float dr0 = (flags & 1u) ? 0.f : pg1.w;
+    const float dr1 = (flags & 2u) ? 0.f : pg2.x;
+    const float dr2 = (flags & 4u) ? 0.f : pg2.y;
+    float x = mx - cam4.x, y = my - cam4.y, z = mz - cam4.z;
+    const float idn = rsqrtf(x * x + y * y + z * z);
+    x *= idn; y *= idn; z *= idn;
+    float wk[NK];  // Σ_c sh[k][c]·∂L/∂rgb_c, read as float4 chunks of the row
+#pragma unroll
+    for (int kk = 0; kk < NK; kk++) wk[kk] = 0.f;
+    {
+        const float drc[3] = {dr0, dr1, dr2};
+        const float4* sh4 = reinterpret_cast<const float4*>(sh);
+#pragma unroll
+        for (int i4 = 0; i4 < ShRows<D>::NS4; i4++) {
+            const float4 q = SHG ? __ldg(sh4 + i4) : sh4[i4];
+            const float qe[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+            for (int e = 0; e < 4; e++) {
+                const int f = 4 * i4 + e;
+                if (f < NS) wk[f / 3] += qe[e] * drc[f % 3];
+            }
+        }
+    }
+    float Y[NK];
+    Y[0] = 0.28209479177387814f;
+    float ddx = 0.f, ddy = 0.f, ddz = 0.f;
+    if (D >= 1) {
+        Y[1] = -g_SH1 * y; Y[2] = g_SH1 * z; Y[3] = -g_SH1 * x;
+        ddx += -g_SH1 * wk[3];
+        ddy += -g_SH1 * wk[1];
+        ddz += g_SH1 * wk[2];
+    }
+    if (D >= 2) {
+        const float xx = x * x, yy = y * y, zz = z * z;
+        Y[4] = g_SH2[0] * x * y;
+        Y[5] = g_SH2[1] * y * z;
+        Y[6] = g_SH2[2] * (2.f * zz - xx - yy);
+        Y[7] = g_SH2[3] * x * z;
+        Y[8] = g_SH2[4] * (xx - yy);
+        ddx += g_SH2[0] * y * wk[4] - 2.f * g_SH2[2] * x * wk[6] + g_SH2[3] * z * wk[7] + 2.f * g_SH2[4] * x * wk[8];
+        ddy += g_SH2[0] * x * wk[4] + g_SH2[1] * z * wk[5] - 2.f * g_SH2[2] * y * wk[6] - 2.f * g_SH2[4] * y * wk[8];
+        ddz += g_SH2[1] * y * wk[5] + 4.f * g_SH2[2] * z * wk[6] + g_SH2[3] * x * wk[7];
+        if (D >= 3) {
+            Y[9] = g_SH3[0] * y * (3.f * xx - yy);
+            Y[10] = g_SH3[1] * x * y * z;
+            Y[11] = g_SH3[2] * y * (4.f * zz - xx - yy);
+            Y[12] = g_SH3[3] * z * (2.f * zz - 3.f * xx - 3.f * yy);
+            Y[13] = g_SH3[4] * x * (4.f * zz - xx - yy);
+            Y[14] = g_SH3[5] * z * (xx - yy);
+            Y[15] = g_SH3[6] * x * (xx - 3.f * yy);
+            ddx += g_SH3[0] * 6.f * x * y * wk[9] + g_SH3[1] * y * z * wk[10] - g_SH3[2] * 2.f * x * y * wk[11]
+                 - g_SH3[3] * 6.f * x * z * wk[12] + g_SH3[4] * (4.f * zz - 3.f * xx - yy) * wk[13]
+                 + g_SH3[5] * 2.f * x * z * wk[14] + g_SH3[6] * (3.f * xx - 3.f * yy) * wk[15];
+            ddy += g_SH3[0] * (3.f * xx - 3.f * yy) * wk[9] + g_SH3[1] * x * z * wk[10]
+                 + g_SH3[2] * (4.f * zz - xx - 3.f * yy) * wk[11] - g_SH3[3] * 6.f * y * z * wk[12]
+                 - g_SH3[4] * 2.f * x * y * wk[13] - g_SH3[5] * 2.f * y * z * wk[14]
+                 - g_SH3[6] * 6.f * x * y * wk[15];
+            ddz += g_SH3[1] * x * y * wk[10] + g_SH3[2] * 8.f * y * z * wk[11]
+                 + g_SH3[3] * (6.f * zz - 3.f * xx - 3.f * yy) * wk[12] + g_SH3[4] * 8.f * x * z * wk[13]
+                 + g_SH3[5] * (xx - yy) * wk[14];
+        }
+    }
+    {
+        const float drc[3] = {dr0, dr1, dr2};
+        float4* dsh4 = reinterpret_cast<float4*>(dsh);
+#pragma unroll
+        for (int i4 = 0; i4 < ShRows<D>::NS4; i4++) {
+            float4 q = dsh4[i4];
+            float* qe = reinterpret_cast<float*>(&q);
+#pragma unroll
+            for (int e = 0; e < 4; e++) {
+                const int f = 4 * i4 + e;
+                if (f < NS) qe[e] += Y[f / 3] * drc[f % 3];
+            }
+            dsh4[i4] = q;
+        }
+    }
+    const float dd = x * ddx + y * ddy + z * ddz;
+    dmx += (ddx - x * dd) * idn;
+    dmy += (ddy - y * dd) * idn;
+    dmz += (ddz - z * dd) * idn;
+}
+
+// Σ → (scale, rotation) and the output writes of one Gaussian (row o of the outputs).
+__device__ __forceinline__ void finish_gaussian(const Launch& L, const mvgs_grads& gr, const mvgs_adc& adc, int64_t g,
+                                                int64_t o, const GAcc& A) {
+    const float dmx = A.dmx, dmy = A.dmy, dmz = A.dmz;
+    const float G00 = A.G00, G01 = A.G01, G02 = A.G02, G11 = A.G11, G12 = A.G12, G22 = A.G22;
+    const float dop = A.dop, e1 = A.e1, e2 = A.e2, gsx = A.gsx, gsy = A.gsy, nvis = A.nvis;
+    FastActiv a;  // recomputed: R, s, q are not kept live through the view loop
+    fast_activate(L.log_scales + 3 * g, L.quats + 4 * g, L.opac[g], a);
+    // Σ = M Mᵀ, M = R diag(s): ∂L/∂M = 2 G M (G symmetric)
+    const float* R = a.R;
+    const float Gm[9] = {G00, G01, G02, G01, G11, G12, G02, G12, G22};
+    float dM[9];
+#pragma unroll
+    for (int r = 0; r < 3; r++)
+#pragma unroll
+        for (int cc = 0; cc < 3; cc++) {
+            const float Mkc0 = R[0 * 3 + cc] * a.s[cc], Mkc1 = R[1 * 3 + cc] * a.s[cc], Mkc2 = R[2 * 3 + cc] * a.s[cc];
+            dM[3 * r + cc] = 2.f * (Gm[3 * r] * Mkc0 + Gm[3 * r + 1] * Mkc1 + Gm[3 * r + 2] * Mkc2);
+        }
+    float dR[9], dls[3];
+#pragma unroll
+    for (int cc = 0; cc < 3; cc++) {
+        float ds = 0.f;
+#pragma unroll
+        for (int r = 0; r < 3; r++) {
+            ds += dM[3 * r + cc] * R[3 * r + cc];
+            dR[3 * r + cc] = dM[3 * r + cc] * a.s[cc];
+        }
+        dls[cc] = ds * a.s[cc];  // s = exp(λ)
+    }
+    const float w = a.q[0], x = a.q[1], y = a.q[2], z = a.q[3];
+    float dq[4];
+    dq[0] = -2.f * z * dR[1] + 2.f * y * dR[2] + 2.f * z * dR[3] - 2.f * x * dR[5] - 2.f * y * dR[6] + 2.f * x * dR[7];
+    dq[1] = 2.f * y * dR[1] + 2.f * z * dR[2] + 2.f * y * dR[3] - 4.f * x * dR[4] - 2.f * w * dR[5] + 2.f * z * dR[6]
+          + 2.f * w * dR[7] - 4.f * x * dR[8];
+    dq[2] = -4.f * y * dR[0] + 2.f * x * dR[1] + 2.f * w * dR[2] + 2.f * x * dR[3] + 2.f * z * dR[5] - 2.f * w * dR[6]
+          + 2.f * z * dR[7] - 4.f * y * dR[8];
+    dq[3] = -4.f * z * dR[0] - 2.f * w * dR[1] + 2.f * x * dR[2] + 2.f * w * dR[3] - 4.f * z * dR[4] + 2.f * y * dR[5]
+          + 2.f * x * dR[6] + 2.f * y * dR[7];
+    const float qd = w * dq[0] + x * dq[1] + y * dq[2] + z * dq[3];
+    // q̂ = q/‖q‖ ⇒ ∂L/∂q = (∂q̂ − q̂(q̂·∂q̂))/‖q‖
+#pragma unroll
+    for (int k = 0; k < 4; k++) gr.d_quats[4 * o + k] = (dq[k] - a.q[k] * qd) * a.inv_norm;
+    gr.d_means[3 * o] = dmx;
+    gr.d_means[3 * o + 1] = dmy;
+    gr.d_means[3 * o + 2] = dmz;
+    gr.d_log_scales[3 * o] = dls[0];
+    gr.d_log_scales[3 * o + 1] = dls[1];
+    gr.d_log_scales[3 * o + 2] = dls[2];
+    gr.d_opacity_logits[o] = dop * a.o * (1.f - a.o);
+    adc.e1[o] = e1;
+    adc.e2[o] = e2;
+    if (adc.e_old || adc.e_old_acc) {
+        const float eo = sqrtf(gsx * gsx + gsy * gsy);
+        if (adc.e_old) adc.e_old[o] = eo;
+        if (adc.e_old_acc) adc.e_old_acc[o] += eo;
+    }
+    adc.vis[o] = nvis;
+    if (adc.e1_acc) adc.e1_acc[o] += e1;
+    if (adc.e2_acc) adc.e2_acc[o] += e2;
+    if (adc.denom_acc) adc.denom_acc[o] += nvis;
+}
+
 // SHG: the thread reads its SH row straight from global memory (16-byte loads through L1,
 // rows 16-byte aligned) instead of a staged shared-memory copy.  Only the SH-gradient rows
 // stay in shared memory, which with the smaller live state (Σ only in the view loop; R, s,
@@ -192,9 +428,7 @@ __global__ __launch_bounds__(BLK, SHG ? 3 : 2) void k_gauss_bwd(Launch L, mvgs_g
 #pragma unroll
         for (int k = 0; k < 6; k++) Sg[k] = a.Sig[k];
     }
-    float dmx = 0.f, dmy = 0.f, dmz = 0.f;
-    float G00 = 0.f, G01 = 0.f, G02 = 0.f, G11 = 0.f, G12 = 0.f, G22 = 0.f;  // ∂L/∂Σ (symmetric)
-    float dop = 0.f, e1 = 0.f, e2 = 0.f, gsx = 0.f, gsy = 0.f, nvis = 0.f;
+    GAcc A;
     const float sW = 2.0f / (float)L.W, sH = 2.0f / (float)L.H;
     bool sh_ready = false;  // SH rows arrive asynchronously; waited on after the first view loads
     for (int v0 = 0; v0 < L.V; v0 += 32) {
@@ -259,160 +493,7 @@ __global__ __launch_bounds__(BLK, SHG ? 3 : 2) void k_gauss_bwd(Launch L, mvgs_g
             const mvgs_camera& c = L.cams[v0 + k0 + u];
             const uint32_t flags = fl[u];
             const float4 pg0 = pga[u], pg1 = pgb[u], pg2 = pgc[u];
-            // pg: (Σ∇x, Σ∇y, e1, ∂A) (∂B, ∂C, ∂o, ∂r) (∂g, ∂b, -, -)
-            nvis += 1.f;
-            e1 += pg0.z;
-            e2 += g_sqrt(pg0.x * pg0.x + pg0.y * pg0.y);
-            gsx += pg0.x;
-            gsy += pg0.y;
-            dop += pg1.z;
-            const float4 cam4 = scam[k0 + u];  // camera centre, clamp limit x
-            FastProj p;
-            fast_project(c, mx, my, mz, Sg, flags, cam4.w, scl[k0 + u], p);
-            const float itz = p.itz, itz2 = itz * itz;
-            // μ' (pixels) = (fx·tx/tz + cx, fy·ty/tz + cy); ∂L/∂μ' = Σ∇·(2/W, 2/H) (R2)
-            const float dpx = pg0.x * sW, dpy = pg0.y * sH;
-            float dtx = c.fx * itz * dpx;
-            float dty = c.fy * itz * dpy;
-            float dtz = -(c.fx * p.tx * itz2) * dpx - (c.fy * p.ty * itz2) * dpy;
-            // conic (A,B,C) = (c,−b,a)/det → Σ' entries (a,b,c)
-            const float dA = pg0.w, dB = pg1.x, dC = pg1.y;
-            const float id2 = g_rcp(p.det * p.det);
-            const float da = (-p.c * p.c * dA + p.b * p.c * dB - p.b * p.b * dC) * id2;
-            const float dc = (-p.b * p.b * dA + p.a * p.b * dB - p.a * p.a * dC) * id2;
-            const float db = (2.f * p.b * p.c * dA - (p.det + 2.f * p.b * p.b) * dB + 2.f * p.a * p.b * dC) * id2;
-            const float hb = 0.5f * db;
-            // ∂L/∂Σ += Tᵀ Gs T,  Gs = [[da, hb], [hb, dc]]
-            const float* T0 = p.T0;
-            const float* T1 = p.T1;
-            float GT0[3], GT1[3];  // Gs·T rows
-#pragma unroll
-            for (int j = 0; j < 3; j++) {
-                GT0[j] = da * T0[j] + hb * T1[j];
-                GT1[j] = hb * T0[j] + dc * T1[j];
-            }
-            G00 += T0[0] * GT0[0] + T1[0] * GT1[0];
-            G01 += T0[0] * GT0[1] + T1[0] * GT1[1];
-            G02 += T0[0] * GT0[2] + T1[0] * GT1[2];
-            G11 += T0[1] * GT0[1] + T1[1] * GT1[1];
-            G12 += T0[1] * GT0[2] + T1[1] * GT1[2];
-            G22 += T0[2] * GT0[2] + T1[2] * GT1[2];
-            // ∂L/∂T = 2 (Gs T) Σ
-            const float* S = Sg;
-            float dT0[3], dT1[3];
-            dT0[0] = 2.f * (GT0[0] * S[0] + GT0[1] * S[1] + GT0[2] * S[2]);
-            dT0[1] = 2.f * (GT0[0] * S[1] + GT0[1] * S[3] + GT0[2] * S[4]);
-            dT0[2] = 2.f * (GT0[0] * S[2] + GT0[1] * S[4] + GT0[2] * S[5]);
-            dT1[0] = 2.f * (GT1[0] * S[0] + GT1[1] * S[1] + GT1[2] * S[2]);
-            dT1[1] = 2.f * (GT1[0] * S[1] + GT1[1] * S[3] + GT1[2] * S[4]);
-            dT1[2] = 2.f * (GT1[0] * S[2] + GT1[1] * S[4] + GT1[2] * S[5]);
-            // T = J R_v ⇒ ∂L/∂J = ∂L/∂T R_vᵀ (only the non-constant entries of J)
-            const float* R = c.R;
-            const float dJ00 = dT0[0] * R[0] + dT0[1] * R[1] + dT0[2] * R[2];
-            const float dJ02 = dT0[0] * R[6] + dT0[1] * R[7] + dT0[2] * R[8];
-            const float dJ11 = dT1[0] * R[3] + dT1[1] * R[4] + dT1[2] * R[5];
-            const float dJ12 = dT1[0] * R[6] + dT1[1] * R[7] + dT1[2] * R[8];
-            dtz += -c.fx * itz2 * dJ00 - c.fy * itz2 * dJ11;
-            // J02 = −fx·ũx/tz: ũx = tx/tz unclamped (∂/∂tx = −fx/tz², ∂/∂tz = 2fx·ux/tz²),
-            // constant when clamped (∂/∂tz = fx·ũx/tz²) — R4
-            if (!(flags & 8u)) {
-                dtx += -c.fx * itz2 * dJ02;
-                dtz += 2.f * c.fx * p.uxc * itz2 * dJ02;
-            } else {
-                dtz += c.fx * p.uxc * itz2 * dJ02;
-            }
-            if (!(flags & 16u)) {
-                dty += -c.fy * itz2 * dJ12;
-                dtz += 2.f * c.fy * p.uyc * itz2 * dJ12;
-            } else {
-                dtz += c.fy * p.uyc * itz2 * dJ12;
-            }
-            // t = R_v μ + t_v
-            dmx += R[0] * dtx + R[3] * dty + R[6] * dtz;
-            dmy += R[1] * dtx + R[4] * dty + R[7] * dtz;
-            dmz += R[2] * dtx + R[5] * dty + R[8] * dtz;
-            // colour: rgb = max(0, Σ Y_k(dir) sh_k + 0.5), dir = (μ − c_v)/‖μ − c_v‖
-            const float dr0 = (flags & 1u) ? 0.f : pg1.w;
-            const float dr1 = (flags & 2u) ? 0.f : pg2.x;
-            const float dr2 = (flags & 4u) ? 0.f : pg2.y;
-            float x = mx - cam4.x, y = my - cam4.y, z = mz - cam4.z;
-            const float idn = rsqrtf(x * x + y * y + z * z);
-            x *= idn; y *= idn; z *= idn;
-            float wk[NK];  // Σ_c sh[k][c]·∂L/∂rgb_c, read as float4 chunks of the row
-#pragma unroll
-            for (int kk = 0; kk < NK; kk++) wk[kk] = 0.f;
-            {
-                const float drc[3] = {dr0, dr1, dr2};
-                const float4* sh4 = reinterpret_cast<const float4*>(sh);
-#pragma unroll
-                for (int i4 = 0; i4 < ShRows<D>::NS4; i4++) {
-                    const float4 q = SHG ? __ldg(sh4 + i4) : sh4[i4];
-                    const float qe[4] = {q.x, q.y, q.z, q.w};
-#pragma unroll
-                    for (int e = 0; e < 4; e++) {
-                        const int f = 4 * i4 + e;
-                        if (f < NS) wk[f / 3] += qe[e] * drc[f % 3];
-                    }
-                }
-            }
-            float Y[NK];
-            Y[0] = 0.28209479177387814f;
-            float ddx = 0.f, ddy = 0.f, ddz = 0.f;
-            if (D >= 1) {
-                Y[1] = -g_SH1 * y; Y[2] = g_SH1 * z; Y[3] = -g_SH1 * x;
-                ddx += -g_SH1 * wk[3];
-                ddy += -g_SH1 * wk[1];
-                ddz += g_SH1 * wk[2];
-            }
-            if (D >= 2) {
-                const float xx = x * x, yy = y * y, zz = z * z;
-                Y[4] = g_SH2[0] * x * y;
-                Y[5] = g_SH2[1] * y * z;
-                Y[6] = g_SH2[2] * (2.f * zz - xx - yy);
-                Y[7] = g_SH2[3] * x * z;
-                Y[8] = g_SH2[4] * (xx - yy);
-                ddx += g_SH2[0] * y * wk[4] - 2.f * g_SH2[2] * x * wk[6] + g_SH2[3] * z * wk[7] + 2.f * g_SH2[4] * x * wk[8];
-                ddy += g_SH2[0] * x * wk[4] + g_SH2[1] * z * wk[5] - 2.f * g_SH2[2] * y * wk[6] - 2.f * g_SH2[4] * y * wk[8];
-                ddz += g_SH2[1] * y * wk[5] + 4.f * g_SH2[2] * z * wk[6] + g_SH2[3] * x * wk[7];
-                if (D >= 3) {
-                    Y[9] = g_SH3[0] * y * (3.f * xx - yy);
-                    Y[10] = g_SH3[1] * x * y * z;
-                    Y[11] = g_SH3[2] * y * (4.f * zz - xx - yy);
-                    Y[12] = g_SH3[3] * z * (2.f * zz - 3.f * xx - 3.f * yy);
-                    Y[13] = g_SH3[4] * x * (4.f * zz - xx - yy);
-                    Y[14] = g_SH3[5] * z * (xx - yy);
-                    Y[15] = g_SH3[6] * x * (xx - 3.f * yy);
-                    ddx += g_SH3[0] * 6.f * x * y * wk[9] + g_SH3[1] * y * z * wk[10] - g_SH3[2] * 2.f * x * y * wk[11]
-                         - g_SH3[3] * 6.f * x * z * wk[12] + g_SH3[4] * (4.f * zz - 3.f * xx - yy) * wk[13]
-                         + g_SH3[5] * 2.f * x * z * wk[14] + g_SH3[6] * (3.f * xx - 3.f * yy) * wk[15];
-                    ddy += g_SH3[0] * (3.f * xx - 3.f * yy) * wk[9] + g_SH3[1] * x * z * wk[10]
-                         + g_SH3[2] * (4.f * zz - xx - 3.f * yy) * wk[11] - g_SH3[3] * 6.f * y * z * wk[12]
-                         - g_SH3[4] * 2.f * x * y * wk[13] - g_SH3[5] * 2.f * y * z * wk[14]
-                         - g_SH3[6] * 6.f * x * y * wk[15];
-                    ddz += g_SH3[1] * x * y * wk[10] + g_SH3[2] * 8.f * y * z * wk[11]
-                         + g_SH3[3] * (6.f * zz - 3.f * xx - 3.f * yy) * wk[12] + g_SH3[4] * 8.f * x * z * wk[13]
-                         + g_SH3[5] * (xx - yy) * wk[14];
-                }
-            }
-            {
-                const float drc[3] = {dr0, dr1, dr2};
-                float4* dsh4 = reinterpret_cast<float4*>(dsh);
-#pragma unroll
-                for (int i4 = 0; i4 < ShRows<D>::NS4; i4++) {
-                    float4 q = dsh4[i4];
-                    float* qe = reinterpret_cast<float*>(&q);
-#pragma unroll
-                    for (int e = 0; e < 4; e++) {
-                        const int f = 4 * i4 + e;
-                        if (f < NS) qe[e] += Y[f / 3] * drc[f % 3];
-                    }
-                    dsh4[i4] = q;
-                }
-            }
-            const float dd = x * ddx + y * ddy + z * ddz;
-            dmx += (ddx - x * dd) * idn;
-            dmy += (ddy - y * dd) * idn;
-            dmz += (ddz - z * dd) * idn;
+            pair_chain<D, SHG>(c, scam[k0 + u], scl[k0 + u], flags, pg0, pg1, pg2, mx, my, mz, Sg, sh, dsh, sW, sH, A);
             }
         }
         __syncthreads();
@@ -444,61 +525,7 @@ __global__ __launch_bounds__(BLK, SHG ? 3 : 2) void k_gauss_bwd(Launch L, mvgs_g
         }
     }
     if (!valid) return;
-    FastActiv a;  // recomputed: R, s, q are not kept live through the view loop
-    fast_activate(L.log_scales + 3 * g, L.quats + 4 * g, L.opac[g], a);
-    // Σ = M Mᵀ, M = R diag(s): ∂L/∂M = 2 G M (G symmetric)
-    const float* R = a.R;
-    const float Gm[9] = {G00, G01, G02, G01, G11, G12, G02, G12, G22};
-    float dM[9];
-#pragma unroll
-    for (int r = 0; r < 3; r++)
-#pragma unroll
-        for (int cc = 0; cc < 3; cc++) {
-            const float Mkc0 = R[0 * 3 + cc] * a.s[cc], Mkc1 = R[1 * 3 + cc] * a.s[cc], Mkc2 = R[2 * 3 + cc] * a.s[cc];
-            dM[3 * r + cc] = 2.f * (Gm[3 * r] * Mkc0 + Gm[3 * r + 1] * Mkc1 + Gm[3 * r + 2] * Mkc2);
-        }
-    float dR[9], dls[3];
-#pragma unroll
-    for (int cc = 0; cc < 3; cc++) {
-        float ds = 0.f;
-#pragma unroll
-        for (int r = 0; r < 3; r++) {
-            ds += dM[3 * r + cc] * R[3 * r + cc];
-            dR[3 * r + cc] = dM[3 * r + cc] * a.s[cc];
-        }
-        dls[cc] = ds * a.s[cc];  // s = exp(λ)
-    }
-    const float w = a.q[0], x = a.q[1], y = a.q[2], z = a.q[3];
-    float dq[4];
-    dq[0] = -2.f * z * dR[1] + 2.f * y * dR[2] + 2.f * z * dR[3] - 2.f * x * dR[5] - 2.f * y * dR[6] + 2.f * x * dR[7];
-    dq[1] = 2.f * y * dR[1] + 2.f * z * dR[2] + 2.f * y * dR[3] - 4.f * x * dR[4] - 2.f * w * dR[5] + 2.f * z * dR[6]
-          + 2.f * w * dR[7] - 4.f * x * dR[8];
-    dq[2] = -4.f * y * dR[0] + 2.f * x * dR[1] + 2.f * w * dR[2] + 2.f * x * dR[3] + 2.f * z * dR[5] - 2.f * w * dR[6]
-          + 2.f * z * dR[7] - 4.f * y * dR[8];
-    dq[3] = -4.f * z * dR[0] - 2.f * w * dR[1] + 2.f * x * dR[2] + 2.f * w * dR[3] - 4.f * z * dR[4] + 2.f * y * dR[5]
-          + 2.f * x * dR[6] + 2.f * y * dR[7];
-    const float qd = w * dq[0] + x * dq[1] + y * dq[2] + z * dq[3];
-    // q̂ = q/‖q‖ ⇒ ∂L/∂q = (∂q̂ − q̂(q̂·∂q̂))/‖q‖
-#pragma unroll
-    for (int k = 0; k < 4; k++) gr.d_quats[4 * o + k] = (dq[k] - a.q[k] * qd) * a.inv_norm;
-    gr.d_means[3 * o] = dmx;
-    gr.d_means[3 * o + 1] = dmy;
-    gr.d_means[3 * o + 2] = dmz;
-    gr.d_log_scales[3 * o] = dls[0];
-    gr.d_log_scales[3 * o + 1] = dls[1];
-    gr.d_log_scales[3 * o + 2] = dls[2];
-    gr.d_opacity_logits[o] = dop * a.o * (1.f - a.o);
-    adc.e1[o] = e1;
-    adc.e2[o] = e2;
-    if (adc.e_old || adc.e_old_acc) {
-        const float eo = sqrtf(gsx * gsx + gsy * gsy);
-        if (adc.e_old) adc.e_old[o] = eo;
-        if (adc.e_old_acc) adc.e_old_acc[o] += eo;
-    }
-    adc.vis[o] = nvis;
-    if (adc.e1_acc) adc.e1_acc[o] += e1;
-    if (adc.e2_acc) adc.e2_acc[o] += e2;
-    if (adc.denom_acc) adc.denom_acc[o] += nvis;
+    finish_gaussian(L, gr, adc, g, o, A);
 }
 
 template <int D, bool SHG>
