@@ -528,180 +528,6 @@ __global__ __launch_bounds__(BLK, SHG ? 3 : 2) void k_gauss_bwd(Launch L, mvgs_g
     finish_gaussian(L, gr, adc, g, o, A);
 }
 
-// Visibility-grouped variant (V ≤ GRP_VMAX views).  With one thread per Gaussian walking
-// its views, a warp executes a view's chain whenever ANY of its 32 Gaussians is visible
-// there; at ~50 % visibility per (Gaussian, view) half the lanes idle.  Here the block first
-// learns every Gaussian's visible-view mask (z-test ballots, then the pair flags), counting-
-// sorts its 256 Gaussians by mask, and thread t processes Gaussian perm[t]: warps hold
-// Gaussians with the same mask and walk only their visible views.  Each Gaussian is still
-// handled by one thread, so results are identical to k_gauss_bwd's; pair slots come from
-// the stored per-view ballots; cameras come from shared memory (lanes of a warp can be at
-// different views at a mask boundary).
-constexpr int GRP_VMAX = 8;
-
-template <int D>
-__global__ __launch_bounds__(BLK, 2) void k_gauss_bwd_grp(Launch L, mvgs_grads gr, mvgs_adc adc, int64_t gbeg,
-                                                          int64_t gend) {
-    constexpr int NS = ShRows<D>::NS, SS = ShRows<D>::STRIDE;
-    extern __shared__ float4 smem_sh4[];
-    float* smem_sh = reinterpret_cast<float*>(smem_sh4);
-    float* dsh_s = smem_sh;             // [BLK][SS]
-    float* sh_s = smem_sh + BLK * SS;   // [BLK][SS]
-    __shared__ unsigned sbal[BLK / 32][GRP_VMAX];  // z-visibility ballots per (warp, view)
-    __shared__ int wc[BLK / 32][GRP_VMAX];         // exclusive prefix of their counts over warps
-    __shared__ int sboff[GRP_VMAX];
-    __shared__ mvgs_camera scams[GRP_VMAX];
-    __shared__ float4 scam[GRP_VMAX];
-    __shared__ float scl[GRP_VMAX];
-    __shared__ uint8_t smask[BLK];
-    __shared__ int hist[1 << GRP_VMAX];
-    __shared__ uint8_t perm[BLK];
-    const int V = L.V;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int blk = blockIdx.x + (int)(gbeg / BLK);
-    const int64_t g0 = (int64_t)blk * BLK;
-    const int nb = (int)min((int64_t)BLK, gend - g0);
-    {  // SH rows (async, waited on before the view loop)
-        const float* src = L.sh + g0 * (int64_t)L.sh_stride * 3;
-        const int rowlen = L.sh_stride * 3;
-        if ((rowlen & 3) == 0 && (NS & 3) == 0 && ((uintptr_t)src & 15) == 0) {
-            constexpr int NS4 = NS / 4;
-            for (int i = threadIdx.x; i < nb * NS4; i += BLK) {
-                const int r = i / NS4, q = 4 * (i - r * NS4);
-                cp_async16(&sh_s[r * SS + q], src + (int64_t)r * rowlen + q);
-            }
-        } else {
-            for (int i = threadIdx.x; i < nb * NS; i += BLK) {
-                const int r = i / NS, q = i - r * NS;
-                cp_async4(&sh_s[r * SS + q], src + (int64_t)r * rowlen + q);
-            }
-        }
-        cp_async_commit();
-        float4* z4 = reinterpret_cast<float4*>(dsh_s);
-        for (int i = threadIdx.x; i < BLK * SS / 4; i += BLK) z4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-    }
-    for (int i = threadIdx.x; i < (1 << GRP_VMAX); i += BLK) hist[i] = 0;
-    if (threadIdx.x < V) {
-        const int v = threadIdx.x;
-        sboff[v] = L.blk_off[(int64_t)v * L.NB + blk];
-        const mvgs_camera& c = L.cams[v];
-        scams[v] = c;
-        const float* R = c.R;
-        scam[v] = make_float4(-(R[0] * c.t[0] + R[3] * c.t[1] + R[6] * c.t[2]),
-                              -(R[1] * c.t[0] + R[4] * c.t[1] + R[7] * c.t[2]),
-                              -(R[2] * c.t[0] + R[5] * c.t[1] + R[8] * c.t[2]), 0.65f * (float)c.width / c.fx);
-        scl[v] = 0.65f * (float)c.height / c.fy;
-    }
-    // phase A (natural order): z-test ballots, pair slots, visible mask from the pair flags
-    {
-        const int64_t g = g0 + threadIdx.x;
-        const bool valid = threadIdx.x < nb;
-        float mx = 0.f, my = 0.f, mz = 0.f;
-        if (valid) {
-            mx = L.means[3 * g];
-            my = L.means[3 * g + 1];
-            mz = L.means[3 * g + 2];
-        }
-        unsigned zm = 0;
-        for (int v = 0; v < V; v++) {
-            const mvgs_camera& c = L.cams[v];
-            const bool zv = valid && ca_depth(c, mx, my, mz) > c.znear;
-            const unsigned bal = __ballot_sync(FULLG, zv);
-            if (lane == 0) {
-                sbal[warp][v] = bal;
-                wc[warp][v] = __popc(bal);
-            }
-            zm |= zv ? 1u << v : 0u;
-        }
-        __syncthreads();
-        if (threadIdx.x < V) {
-            int run = 0;
-            for (int w = 0; w < BLK / 32; w++) {
-                const int c = wc[w][threadIdx.x];
-                wc[w][threadIdx.x] = run;
-                run += c;
-            }
-        }
-        __syncthreads();
-        unsigned vm = 0;
-        const unsigned lt = (1u << lane) - 1u;
-        for (int v = 0; v < V; v++) {
-            if (!((zm >> v) & 1u)) continue;
-            const int64_t pair = (int64_t)sboff[v] + wc[warp][v] + __popc(sbal[warp][v] & lt);
-            if (pair < L.cap_pairs && (L.pflag[pair] & PF_VISIBLE)) vm |= 1u << v;
-        }
-        smask[threadIdx.x] = (uint8_t)vm;
-        if (valid) atomicAdd(&hist[vm], 1);
-    }
-    __syncthreads();
-    if (warp == 0) {  // exclusive scan of the mask histogram → bucket cursors
-        constexpr int PER = (1 << GRP_VMAX) / 32;
-        int loc[PER], t = 0;
-#pragma unroll
-        for (int q = 0; q < PER; q++) {
-            loc[q] = t;
-            t += hist[lane * PER + q];
-        }
-        int inc = t;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int y = __shfl_up_sync(FULLG, inc, o);
-            if (lane >= o) inc += y;
-        }
-        const int ex = inc - t;
-#pragma unroll
-        for (int q = 0; q < PER; q++) hist[lane * PER + q] = ex + loc[q];
-    }
-    __syncthreads();
-    if (threadIdx.x < nb) perm[atomicAdd(&hist[smask[threadIdx.x]], 1)] = (uint8_t)threadIdx.x;
-    cp_async_wait_all();
-    __syncthreads();
-    // phase B: thread t takes Gaussian j = perm[t] and walks its visible views only
-    if (threadIdx.x < nb) {
-        const int j = perm[threadIdx.x];
-        const int64_t g = g0 + j;
-        const int jw = j >> 5;
-        const unsigned jlt = (1u << (j & 31)) - 1u;
-        const float mx = L.means[3 * g], my = L.means[3 * g + 1], mz = L.means[3 * g + 2];
-        float Sg[6];
-        {
-            FastActiv a;
-            fast_activate(L.log_scales + 3 * g, L.quats + 4 * g, L.opac[g], a);
-#pragma unroll
-            for (int q = 0; q < 6; q++) Sg[q] = a.Sig[q];
-        }
-        const float sW = 2.0f / (float)L.W, sH = 2.0f / (float)L.H;
-        const float* sh = sh_s + j * SS;
-        float* dsh = dsh_s + j * SS;
-        GAcc A;
-        for (unsigned mm = smask[j]; mm; mm &= mm - 1u) {
-            const int v = __ffs(mm) - 1;
-            const int64_t pair = (int64_t)sboff[v] + wc[jw][v] + __popc(sbal[jw][v] & jlt);
-            const uint32_t flags = L.pflag[pair];
-            const float4* pgp = reinterpret_cast<const float4*>(L.pgrad + pair * PG_STRIDE);
-            pair_chain<D, false>(scams[v], scam[v], scl[v], flags, pgp[0], pgp[1], pgp[2], mx, my, mz, Sg, sh, dsh,
-                                 sW, sH, A);
-        }
-        finish_gaussian(L, gr, adc, g, g - gbeg, A);
-    }
-    __syncthreads();
-    {  // coalesced store of the SH gradient rows
-        float* dst = gr.d_sh + (g0 - gbeg) * (int64_t)L.sh_stride * 3;
-        const int rowlen = L.sh_stride * 3;
-        if (rowlen == NS && (NS & 3) == 0 && ((uintptr_t)dst & 15) == 0) {
-            constexpr int NS4 = NS / 4;
-            float4* dst4 = reinterpret_cast<float4*>(dst);
-            for (int i = threadIdx.x; i < nb * NS4; i += BLK) {
-                const int r = i / NS4, k4 = i - r * NS4;
-                dst4[i] = *reinterpret_cast<const float4*>(&dsh_s[r * SS + 4 * k4]);
-            }
-        } else {
-            for (int r = warp; r < nb; r += BLK / 32)
-                for (int q = lane; q < rowlen; q += 32) dst[(int64_t)r * rowlen + q] = q < NS ? dsh_s[r * SS + q] : 0.f;
-        }
-    }
-}
-
 template <int D, bool SHG>
 cudaError_t launch_gauss_bwd_v(const Launch& L, const mvgs_grads& gr, const mvgs_adc& adc, int64_t gb, int64_t ge,
                                cudaStream_t s) {
@@ -717,21 +543,9 @@ cudaError_t launch_gauss_bwd_v(const Launch& L, const mvgs_grads& gr, const mvgs
 #define GB_SH_GLOBAL 0  // 1 measured slower (0.71 vs 0.61 ms at garden): 3 CTAs of rows thrash L1
 #endif
 
-#ifndef GB_GROUPED
-#define GB_GROUPED 1
-#endif
-
 template <int D>
 cudaError_t launch_gauss_bwd_t(const Launch& L, const mvgs_grads& gr, const mvgs_adc& adc, int64_t gb, int64_t ge,
                                cudaStream_t s) {
-    if (GB_GROUPED && L.V <= GRP_VMAX) {
-        const size_t smem = sizeof(float) * 2 * BLK * ShRows<D>::STRIDE;
-        cudaError_t e = cudaFuncSetAttribute(k_gauss_bwd_grp<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        const int nblk = (int)((ge - gb + BLK - 1) / BLK);
-        if (nblk > 0) k_gauss_bwd_grp<D><<<nblk, BLK, smem, s>>>(L, gr, adc, gb, ge);
-        return cudaGetLastError();
-    }
     // rows read as float4 from global: row length and base must keep every row 16-byte aligned
     const bool shg = GB_SH_GLOBAL && ((L.sh_stride * 3) & 3) == 0 && ((uintptr_t)L.sh & 15) == 0;
     return shg ? launch_gauss_bwd_v<D, true>(L, gr, adc, gb, ge, s) : launch_gauss_bwd_v<D, false>(L, gr, adc, gb, ge, s);
