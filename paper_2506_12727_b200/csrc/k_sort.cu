@@ -208,7 +208,7 @@ constexpr int RS3_IPT = MVGS_RS3_IPT;
 template <int IPT>
 static int radix_sort_3k_t(uint32_t* k, uint32_t* v, uint32_t* k2, uint32_t* v2, uint2* pl, uint2* pl2, const int* n_ptr,
                int64_t cap, int bits, int* counts, int* scan_tmp, cudaStream_t s, cudaError_t* err,
-               int* range_min) {
+               int* range_min, bool first_counted) {
     const int ntiles = (int)((cap + RS_T * IPT - 1) / (RS_T * IPT));  // ≤ radix_tiles(cap): counts fit
     const int npass = (bits + 7) / 8;
     const int db = npass ? (bits + npass - 1) / npass : 0;
@@ -219,7 +219,8 @@ static int radix_sort_3k_t(uint32_t* k, uint32_t* v, uint32_t* k2, uint32_t* v2,
     for (int pass = 0; pass < npass; pass++) {
         const int shift = pass * db;
         const int nb = min(db, bits - shift);
-        k_rs_hist<IPT><<<ntiles, RS_T, 0, s>>>(ks, n_ptr, cap, shift, nb, counts, ntiles);
+        if (!(pass == 0 && first_counted))  // the producer of the keys may have counted pass 0 already
+            k_rs_hist<IPT><<<ntiles, RS_T, 0, s>>>(ks, n_ptr, cap, shift, nb, counts, ntiles);
         // only the live digits' counts (digit-major layout): a 7-bit pass scans half the table
         if ((*err = scan_exclusive(counts, (1 << nb) * ntiles, nullptr, scan_tmp, s)) != cudaSuccess) return pass;
         int* rm = (pass == npass - 1) ? range_min : nullptr;
@@ -244,10 +245,20 @@ static int radix_sort_3k_t(uint32_t* k, uint32_t* v, uint32_t* k2, uint32_t* v2,
 
 int radix_sort_3k(uint32_t* k, uint32_t* v, uint32_t* k2, uint32_t* v2, uint2* pl, uint2* pl2, const int* n_ptr,
                int64_t cap, int bits, int* counts, int* scan_tmp, cudaStream_t s, cudaError_t* err,
-               int* range_min = nullptr) {
+               int* range_min = nullptr, bool first_counted = false) {
     // payload tiles stay at 8 keys per thread (static shared memory); key/value tiles take RS3_IPT
-    return pl ? radix_sort_3k_t<8>(k, v, k2, v2, pl, pl2, n_ptr, cap, bits, counts, scan_tmp, s, err, range_min)
-              : radix_sort_3k_t<RS3_IPT>(k, v, k2, v2, pl, pl2, n_ptr, cap, bits, counts, scan_tmp, s, err, range_min);
+    return pl ? radix_sort_3k_t<8>(k, v, k2, v2, pl, pl2, n_ptr, cap, bits, counts, scan_tmp, s, err, range_min, false)
+              : radix_sort_3k_t<RS3_IPT>(k, v, k2, v2, pl, pl2, n_ptr, cap, bits, counts, scan_tmp, s, err, range_min,
+                                         first_counted);
+}
+
+// digit width of the entry sort's passes (keys view·T + tile < V·T)
+static void entry_digits(const Launch& L, int* bits, int* db) {
+    int b = 1;
+    while ((1ll << b) < (int64_t)L.V * L.T) b++;
+    const int np = (b + 7) / 8;
+    *bits = b;
+    *db = (b + np - 1) / np;
 }
 
 // ---------------------------------------------------------------- onesweep
@@ -488,7 +499,7 @@ __global__ void k_pair_tiles(Launch L, const uint2* __restrict__ rect, int* __re
 // ballot of the run starts inside its 32-entry window (highest start ≤ its entry).  The row/column split
 // uses a float reciprocal of the rect width (exact: (k + 0.5)/w for integers k < 2^20,
 // w < 2^12 never rounds across an integer).
-constexpr int DUP_CH = 1024;
+constexpr int DUP_CH = RS_T * RS3_IPT;  // one chunk = one tile of the entry sort's first pass
 
 struct DupDesc {  // one pair of the warp's 32
     int x0, y0, w, excl;  // rect origin and width, exclusive prefix of in-chunk counts
@@ -497,10 +508,15 @@ struct DupDesc {  // one pair of the warp's 32
     int off0;             // pair-local index of the pair's first in-chunk entry
 };
 
+// Since a chunk is exactly one tile of the entry sort's first radix pass, the warp also counts
+// that pass's digits of the keys it writes (counts[digit·ntiles + chunk]): the pass needs no
+// histogram kernel re-reading the K keys.
 __global__ __launch_bounds__(256) void k_dup(Launch L, const uint32_t* __restrict__ order,
-                                             const uint2* __restrict__ rect, const int* __restrict__ ebase) {
+                                             const uint2* __restrict__ rect, const int* __restrict__ ebase,
+                                             int* __restrict__ counts, int ntiles, uint32_t dmask) {
     __shared__ uint8_t spos[8][32];
     __shared__ DupDesc desc[8][32];
+    __shared__ int dh[8][RS_BINS];
     const int Q = (int)min((int64_t)L.counters[C_NVIS], L.cap_pairs);  // visible pairs (compacted by the sort)
     const int64_t Kall = L.counters[C_K];
     const int Kw = (int)min(Kall, L.cap_entries);  // entries written (the rest is a capacity overflow)
@@ -510,6 +526,8 @@ __global__ __launch_bounds__(256) void k_dup(Launch L, const uint32_t* __restric
     const int nchunks = (Kw + DUP_CH - 1) / DUP_CH;
     for (int c = blockIdx.x * (blockDim.x >> 5) + wid; c < nchunks; c += nwarps) {
         const int e0 = c * DUP_CH, e1 = min(e0 + DUP_CH, Kw);
+        for (int d = lane; d <= (int)dmask; d += 32) dh[wid][d] = 0;
+        __syncwarp();
         // largest i < Q with ebase[i] ≤ e0 (ebase[Q] = K > e0): 32-ary search
         int lo = 0, hi = Q;
         while (hi - lo > 1) {
@@ -576,15 +594,23 @@ __global__ __launch_bounds__(256) void k_dup(Launch L, const uint32_t* __restric
                     const int row = __float2int_rz(((float)loc + 0.5f) * od.inv_w);
                     const int col = loc - row * od.w;
                     const int e = ebeg + k;
-                    L.key[e] = od.vb + (od.y0 + row) * L.TX + od.x0 + col;
+                    const uint32_t key = od.vb + (od.y0 + row) * L.TX + od.x0 + col;
+                    L.key[e] = key;
                     L.val[e] = od.q;
+                    atomicAdd(&dh[wid][key & dmask], 1);
                 }
             }
             __syncwarp();
             if (enext >= e1) break;  // warp-uniform
             i0 += 32;
         }
+        __syncwarp();
+        for (int d = lane; d <= (int)dmask; d += 32) counts[(int64_t)d * ntiles + c] = dh[wid][d];
+        __syncwarp();
     }
+    // tiles past the written entries (capacity slack) count nothing
+    for (int c = nchunks + blockIdx.x * (blockDim.x >> 5) + wid; c < ntiles; c += nwarps)
+        for (int d = lane; d <= (int)dmask; d += 32) counts[(int64_t)d * ntiles + c] = 0;
 }
 
 // Closes the ranges written by the last entry-sort pass: off[nb] = K, and an empty bucket
@@ -601,7 +627,8 @@ __global__ __launch_bounds__(RC_T) void k_ranges_close(Launch L) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     // this thread's chunk minimum, then an exclusive suffix-min over later threads
     int m = K;
-    for (int b = lo; b < hi; b++) m = min(m, L.bucket_off[b]);
+#pragma unroll 8
+    for (int b = lo; b < hi; b++) m = min(m, L.bucket_off[b]);  // independent loads, unrolled
     int inc = m;  // inclusive suffix min within the warp (lanes ≥ this one)
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -616,6 +643,7 @@ __global__ __launch_bounds__(RC_T) void k_ranges_close(Launch L) {
     if (lane < 31) after = min(after, nxt);
     int mx = 0;
     int cur = after;  // start of the next bucket
+#pragma unroll 8
     for (int b = hi - 1; b >= lo; b--) {
         const int o = min(L.bucket_off[b], cur);
         L.bucket_off[b] = o;
@@ -667,20 +695,24 @@ cudaError_t launch_dup_sort(const Launch& L, const uint32_t* order, const uint2*
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_dup, 256, 0);
-        k_dup<<<nsm * max(per, 1), 256, 0, s>>>(L, order, rect, L.ecount);
+        int bits, db;
+        entry_digits(L, &bits, &db);
+        const int ntiles = (int)((L.cap_entries + DUP_CH - 1) / DUP_CH);
+        k_dup<<<nsm * max(per, 1), 256, 0, s>>>(L, order, rect, L.ecount, L.rs_counts, ntiles, (1u << db) - 1u);
     }
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     return cudaSuccess;
 }
 
 cudaError_t launch_sort_entries(const Launch& L, uint32_t** sorted_vals, cudaStream_t s) {
-    int bits = 1;
-    while ((1ll << bits) < (int64_t)L.V * L.T) bits++;
+    int bits, db;
+    entry_digits(L, &bits, &db);
     cudaError_t e;
     // bucket starts come out of the last pass (atomicMin): fill with INT_MAX first
     if ((e = cudaMemsetAsync(L.bucket_off, 0x7f, sizeof(int) * ((size_t)L.V * L.T + 1), s)) != cudaSuccess) return e;
+    // the first pass's digit counts were written by k_dup
     int np = radix_sort_3k(L.key, L.val, L.key2, L.val2, nullptr, nullptr, L.counters + C_K, L.cap_entries, bits,
-                           L.rs_counts, L.scan_tmp, s, &e, L.bucket_off);
+                           L.rs_counts, L.scan_tmp, s, &e, L.bucket_off, true);
     *sorted_vals = (np & 1) ? L.val2 : L.val;
     if (e != cudaSuccess) return e;
     k_ranges_close<<<1, RC_T, 0, s>>>(L);
