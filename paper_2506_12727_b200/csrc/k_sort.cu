@@ -614,50 +614,73 @@ __global__ __launch_bounds__(256) void k_dup(Launch L, const uint32_t* __restric
 }
 
 // Closes the ranges written by the last entry-sort pass: off[nb] = K, and an empty bucket
-// (still INT_MAX) starts where the next one does — a suffix minimum over the V·T buckets,
-// one CTA.  Also records the longest bucket (statistics).
+// (still INT_MAX) starts where the next one does — a suffix minimum over the V·T buckets.
+// Two small kernels over segments of RC_T buckets: the segment minima, then per segment the
+// minimum of all later segments, a shared-memory suffix scan and the writes (coalesced).
+// The second also records the longest bucket (statistics).
 constexpr int RC_T = 1024;
-__global__ __launch_bounds__(RC_T) void k_ranges_close(Launch L) {
-    __shared__ int wmin[RC_T / 32];
-    __shared__ int wmax[RC_T / 32];
+
+__global__ __launch_bounds__(RC_T) void k_ranges_segmin(Launch L, int* __restrict__ segmin) {
+    __shared__ int wm[RC_T / 32];
     const int K = (int)min((int64_t)L.counters[C_K], L.cap_entries);
     const int nb = L.V * L.T;
-    const int per = (nb + RC_T - 1) / RC_T;
-    const int lo = min(nb, (int)threadIdx.x * per), hi = min(nb, lo + per);
+    const int b = blockIdx.x * RC_T + threadIdx.x;
+    int m = b < nb ? min(K, L.bucket_off[b]) : K;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = min(m, __shfl_xor_sync(FULLS, m, o));
+    if ((threadIdx.x & 31) == 0) wm[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        m = wm[threadIdx.x];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) m = min(m, __shfl_xor_sync(FULLS, m, o));
+        if (threadIdx.x == 0) segmin[blockIdx.x] = m;
+    }
+}
+
+__global__ __launch_bounds__(RC_T) void k_ranges_close(Launch L, const int* __restrict__ segmin) {
+    __shared__ int wm[RC_T / 32];
+    __shared__ int s_after;
+    const int K = (int)min((int64_t)L.counters[C_K], L.cap_entries);
+    const int nb = L.V * L.T;
+    const int nseg = (nb + RC_T - 1) / RC_T;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    // this thread's chunk minimum, then an exclusive suffix-min over later threads
-    int m = K;
-#pragma unroll 8
-    for (int b = lo; b < hi; b++) m = min(m, L.bucket_off[b]);  // independent loads, unrolled
-    int inc = m;  // inclusive suffix min within the warp (lanes ≥ this one)
+    if (warp == 0) {  // minimum over the later segments
+        int a = K;
+        for (int q = blockIdx.x + 1 + lane; q < nseg; q += 32) a = min(a, segmin[q]);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) a = min(a, __shfl_xor_sync(FULLS, a, o));
+        if (lane == 0) s_after = a;
+    }
+    const int b = blockIdx.x * RC_T + threadIdx.x;
+    const int v = b < nb ? min(K, L.bucket_off[b]) : K;
+    // inclusive suffix minimum over the segment (this bucket and the later ones in it)
+    int inc = v;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
         const int y = __shfl_down_sync(FULLS, inc, o);
         if (lane + o < 32) inc = min(inc, y);
     }
-    if (lane == 0) wmin[warp] = inc;
+    if (lane == 0) wm[warp] = inc;
     __syncthreads();
-    int after = K;  // min over all later threads
-    for (int w = warp + 1; w < RC_T / 32; w++) after = min(after, wmin[w]);
-    const int nxt = __shfl_down_sync(FULLS, inc, 1);
-    if (lane < 31) after = min(after, nxt);
+    int later = s_after;
+    for (int w = warp + 1; w < RC_T / 32; w++) later = min(later, wm[w]);
+    const int o = min(inc, later);  // start of this bucket (an empty one takes the next start)
+    const int nxt = __shfl_down_sync(FULLS, o, 1);  // start of bucket b + 1 (lane 31: `later`)
     int mx = 0;
-    int cur = after;  // start of the next bucket
-#pragma unroll 8
-    for (int b = hi - 1; b >= lo; b--) {
-        const int o = min(L.bucket_off[b], cur);
+    if (b < nb) {
         L.bucket_off[b] = o;
-        mx = max(mx, cur - o);
-        cur = o;
+        mx = (lane < 31 ? nxt : later) - o;
     }
-    if (threadIdx.x == 0) L.bucket_off[nb] = K;
+    if (b == 0) L.bucket_off[nb] = K;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(FULLS, mx, o));
-    if (lane == 0) wmax[warp] = mx;
+    for (int q = 16; q > 0; q >>= 1) mx = max(mx, __shfl_xor_sync(FULLS, mx, q));
+    __syncthreads();
+    if (lane == 0) wm[warp] = mx;
     __syncthreads();
     if (threadIdx.x == 0) {
         int t = 0;
-        for (int w = 0; w < RC_T / 32; w++) t = max(t, wmax[w]);
+        for (int w = 0; w < RC_T / 32; w++) t = max(t, wm[w]);
         atomicMax(&L.counters[C_MAXB], t);
     }
 }
@@ -715,7 +738,9 @@ cudaError_t launch_sort_entries(const Launch& L, uint32_t** sorted_vals, cudaStr
                            L.rs_counts, L.scan_tmp, s, &e, L.bucket_off, true);
     *sorted_vals = (np & 1) ? L.val2 : L.val;
     if (e != cudaSuccess) return e;
-    k_ranges_close<<<1, RC_T, 0, s>>>(L);
+    const int nseg = (L.V * L.T + RC_T - 1) / RC_T;
+    k_ranges_segmin<<<nseg, RC_T, 0, s>>>(L, L.scan_tmp);  // (scan scratch: free after the last pass)
+    k_ranges_close<<<nseg, RC_T, 0, s>>>(L, L.scan_tmp);
     return cudaGetLastError();
 }
 

@@ -285,7 +285,8 @@ mvgs_status mvgs_preprocess(mvgs_ctx* ctx, const mvgs_gaussians* g, const mvgs_c
     cudaStream_t s = (cudaStream_t)stream;
     CK(cudaSetDevice(ctx->device));
     // workspace growth (synchronous only when it grows)
-    int64_t need_scan = scan_tmp_size((int)std::max(nblk, nbuck));
+    // scan block sums, and the ranges close-up's per-1024-bucket minima (k_sort.cu)
+    int64_t need_scan = std::max<int64_t>(scan_tmp_size((int)std::max(nblk, nbuck)), nbuck / 1024 + 2);
     if (nblk + 1 > ctx->cap_blk || nbuck + 1 > ctx->cap_buckets || V > ctx->cap_cams || need_scan > ctx->cap_scan ||
         !ctx->d_blk) {
         CK(cudaDeviceSynchronize());
