@@ -18,11 +18,17 @@ namespace mvgs {
 constexpr unsigned FULL = 0xffffffffu;
 
 // ------------------------------------------------------------------ scan
+// Single-pass exclusive scan with decoupled look-back: one kernel per scan.  A CTA takes a
+// dynamic tile id (4096 ints), scans it, publishes its aggregate, and warp 0 looks back over
+// up to 32 predecessors at a time for the nearest inclusive prefix.  The status words and
+// the tile counter are cleared by a memset before every scan (no epochs: graph replays are
+// safe).  tmp layout (ints): [0] tile counter, [1] pad, [2 …] u64 status per tile.
 constexpr int SCAN_T = 1024, SCAN_IPT = 4, SCAN_TILE = SCAN_T * SCAN_IPT;
+constexpr unsigned long long SC_AGG = 1ull << 32, SC_PRE = 2ull << 32;
 
-int scan_tmp_size(int n) { return (n + SCAN_TILE - 1) / SCAN_TILE + 2; }
+int scan_tmp_size(int n) { return 2 * ((n + SCAN_TILE - 1) / SCAN_TILE + 1) + 4; }
 
-__device__ __forceinline__ int block_exclusive_scan_1024(int x, int* sm /*[32]*/, int* total) {
+__device__ __forceinline__ int block_exclusive_scan_1024(int x, int* sm /*[33]*/, int* total) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     int inc = x;
 #pragma unroll
@@ -50,76 +56,99 @@ __device__ __forceinline__ int block_exclusive_scan_1024(int x, int* sm /*[32]*/
     return r;
 }
 
+__device__ __forceinline__ void scan_st(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;\n" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long scan_ld(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];\n" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
 // n_live (device, nullable): only a[0, min(*n_live, n)) is scanned and the total goes to
-// a[min(*n_live, n)]; blocks past the live count exit at once.
-__device__ __forceinline__ int scan_n(int n, const int* n_live) { return n_live ? min(*n_live, n) : n; }
-
-__global__ __launch_bounds__(SCAN_T) void k_scan_reduce(const int* __restrict__ a, int n, int* __restrict__ tmp,
-                                                        const int* __restrict__ n_live) {
+// a[min(*n_live, n)]; CTAs past the live tiles exit at once.
+__global__ __launch_bounds__(SCAN_T) void k_scan_1p(int* __restrict__ a, int n, int* __restrict__ total_slot,
+                                                    int* __restrict__ tmp, const int* __restrict__ n_live) {
     __shared__ int sm[33];
-    n = scan_n(n, n_live);
-    if ((int)blockIdx.x * SCAN_TILE >= n && blockIdx.x > 0) {
-        if (threadIdx.x == 0) tmp[blockIdx.x] = 0;
-        return;
-    }
-    int base = blockIdx.x * SCAN_TILE + threadIdx.x * SCAN_IPT;
-    int s = 0;
-#pragma unroll
-    for (int i = 0; i < SCAN_IPT; i++) s += (base + i < n) ? a[base + i] : 0;
-    int tot;
-    block_exclusive_scan_1024(s, sm, &tot);
-    if (threadIdx.x == 0) tmp[blockIdx.x] = tot;
-}
-
-__global__ __launch_bounds__(SCAN_T) void k_scan_top(int* __restrict__ tmp, int nb, int* __restrict__ total_slot) {
-    __shared__ int sm[33];
-    int carry = 0;
-    for (int c0 = 0; c0 < nb; c0 += SCAN_T) {
-        int i = c0 + threadIdx.x;
-        int x = i < nb ? tmp[i] : 0;
-        int tot;
-        int ex = block_exclusive_scan_1024(x, sm, &tot);
-        if (i < nb) tmp[i] = ex + carry;
-        carry += tot;
-    }
-    if (threadIdx.x == 0) {
-        tmp[nb] = carry;
-        if (total_slot) *total_slot = carry;
-    }
-}
-
-__global__ __launch_bounds__(SCAN_T) void k_scan_apply(int* __restrict__ a, int n, const int* __restrict__ tmp, int nb,
-                                                       const int* __restrict__ n_live) {
-    __shared__ int sm[33];
-    n = scan_n(n, n_live);
-    const int last_blk = min(n / SCAN_TILE, nb - 1);  // the block that writes a[n]
-    if ((int)blockIdx.x > last_blk) return;
-    int base = blockIdx.x * SCAN_TILE + threadIdx.x * SCAN_IPT;
+    __shared__ int s_tile, s_pre;
+    if (n_live) n = min(*n_live, n);
+    if (threadIdx.x == 0) s_tile = atomicAdd(tmp, 1);
+    __syncthreads();
+    const int tile = s_tile;
+    const int ntiles = max(1, (n + SCAN_TILE - 1) / SCAN_TILE);
+    if (tile >= ntiles) return;
+    unsigned long long* status = reinterpret_cast<unsigned long long*>(tmp + 2);
+    const int base = tile * SCAN_TILE + threadIdx.x * SCAN_IPT;
     int v[SCAN_IPT];
-    int s = 0;
+    if (base + SCAN_IPT <= n) {
+        const int4 q = *reinterpret_cast<const int4*>(a + base);
+        v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
+    } else {
 #pragma unroll
-    for (int i = 0; i < SCAN_IPT; i++) {
-        v[i] = (base + i < n) ? a[base + i] : 0;
-        s += v[i];
+        for (int i = 0; i < SCAN_IPT; i++) v[i] = base + i < n ? a[base + i] : 0;
     }
+    const int sum = v[0] + v[1] + v[2] + v[3];
     int tot;
-    int ex = block_exclusive_scan_1024(s, sm, &tot) + tmp[blockIdx.x];
+    const int ex = block_exclusive_scan_1024(sum, sm, &tot);
+    if (threadIdx.x < 32) {
+        const int lane = threadIdx.x;
+        int excl = 0;
+        if (tile == 0) {
+            if (lane == 0) scan_st(status, SC_PRE | (unsigned)tot);
+        } else {
+            if (lane == 0) scan_st(status + tile, SC_AGG | (unsigned)tot);
+            int p = tile - 1;  // nearest predecessor not yet accounted for
+            while (true) {
+                const int q = p - lane;
+                const unsigned long long w = q >= 0 ? scan_ld(status + q) : (SC_PRE | 0ull);
+                const bool ready = (w & (SC_AGG | SC_PRE)) != 0;
+                const unsigned nr = ~__ballot_sync(FULL, ready);
+                const int first_nr = nr ? __ffs(nr) - 1 : 32;  // lanes before it are all ready
+                const unsigned pre = __ballot_sync(FULL, ready && (w & SC_PRE)) &
+                                     (first_nr == 32 ? 0xffffffffu : ((1u << first_nr) - 1u));
+                const int upto = pre ? __ffs(pre) - 1 : first_nr - 1;  // last lane to add
+                int val = lane <= upto ? (int)(unsigned)(w & 0xffffffffull) : 0;
 #pragma unroll
-    for (int i = 0; i < SCAN_IPT; i++) {
-        if (base + i < n) a[base + i] = ex;
-        ex += v[i];
+                for (int o = 16; o > 0; o >>= 1) val += __shfl_xor_sync(FULL, val, o);
+                excl += val;
+                if (pre) break;
+                p -= first_nr;  // 0 when the nearest is not ready: poll again
+            }
+            if (lane == 0) scan_st(status + tile, SC_PRE | (unsigned)(excl + tot));
+        }
+        if (lane == 0) s_pre = excl;
     }
-    if ((int)blockIdx.x == last_blk && threadIdx.x == 0) a[n] = tmp[nb];
+    __syncthreads();
+    int run = s_pre + ex;
+    if (base + SCAN_IPT <= n) {
+        int4 q;
+        q.x = run; run += v[0];
+        q.y = run; run += v[1];
+        q.z = run; run += v[2];
+        q.w = run;
+        *reinterpret_cast<int4*>(a + base) = q;
+    } else {
+#pragma unroll
+        for (int i = 0; i < SCAN_IPT; i++) {
+            if (base + i < n) a[base + i] = run;
+            run += v[i];
+        }
+    }
+    if (tile == ntiles - 1 && threadIdx.x == 0) {
+        a[n] = s_pre + tot;
+        if (total_slot) *total_slot = s_pre + tot;
+    }
 }
 
 // Exclusive scan of a[0..n) in place; a[n] and *total_slot receive the total.  With
-// n_live (device) only the first min(*n_live, n) elements take part (see k_scan_reduce).
+// n_live (device) only the first min(*n_live, n) elements take part.  `tmp` holds
+// scan_tmp_size(n) ints.
 cudaError_t scan_exclusive(int* a, int n, int* total_slot, int* tmp, cudaStream_t s, const int* n_live) {
-    int nb = (n + SCAN_TILE - 1) / SCAN_TILE;
-    if (nb == 0) nb = 1;
-    k_scan_reduce<<<nb, SCAN_T, 0, s>>>(a, n, tmp, n_live);
-    k_scan_top<<<1, SCAN_T, 0, s>>>(tmp, nb, total_slot);
-    k_scan_apply<<<nb, SCAN_T, 0, s>>>(a, n, tmp, nb, n_live);
+    int nt = (n + SCAN_TILE - 1) / SCAN_TILE;
+    if (nt == 0) nt = 1;
+    cudaError_t e = cudaMemsetAsync(tmp, 0, sizeof(int) * (2 + 2 * (size_t)nt), s);
+    if (e != cudaSuccess) return e;
+    k_scan_1p<<<nt, SCAN_T, 0, s>>>(a, n, total_slot, tmp, n_live);
     return cudaGetLastError();
 }
 
