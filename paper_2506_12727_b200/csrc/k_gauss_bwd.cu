@@ -122,9 +122,6 @@ struct ShRows {
 #ifndef GB_VB
 #define GB_VB 2  // views whose pair loads are issued together (4: more loads in flight, more spills)
 #endif
-#ifndef GB_VB_SHG
-#define GB_VB_SHG 1  // the same for the 3-CTA variant (80 registers)
-#endif
 
 // One visible (Gaussian, view) pair of the chain rule (S8) and its ADC terms (S9), added into
 // the Gaussian's accumulators; the SH-gradient row is updated in shared memory.
@@ -134,7 +131,7 @@ struct GAcc {
     float dop = 0.f, e1 = 0.f, e2 = 0.f, gsx = 0.f, gsy = 0.f, nvis = 0.f;
 };
 
-template <int D, bool SHG>
+template <int D>
 __device__ __forceinline__ void pair_chain(const mvgs_camera& c, float4 cam4, float limy, uint32_t flags, float4 pg0,
                                            float4 pg1, float4 pg2, float mx, float my, float mz, const float* Sg,
                                            const float* sh, float* dsh, float sW, float sH, GAcc& A) {
@@ -230,7 +227,7 @@ __device__ __forceinline__ void pair_chain(const mvgs_camera& c, float4 cam4, fl
         const float4* sh4 = reinterpret_cast<const float4*>(sh);
 #pragma unroll
         for (int i4 = 0; i4 < ShRows<D>::NS4; i4++) {
-            const float4 q = SHG ? __ldg(sh4 + i4) : sh4[i4];
+            const float4 q = sh4[i4];
             const float qe[4] = {q.x, q.y, q.z, q.w};
 #pragma unroll
             for (int e = 0; e < 4; e++) {
@@ -362,21 +359,18 @@ __device__ __forceinline__ void finish_gaussian(const Launch& L, const mvgs_grad
     if (adc.denom_acc) adc.denom_acc[o] += nvis;
 }
 
-// SHG: the thread reads its SH row straight from global memory (16-byte loads through L1,
-// rows 16-byte aligned) instead of a staged shared-memory copy.  Only the SH-gradient rows
-// stay in shared memory, which with the smaller live state (Σ only in the view loop; R, s,
-// q recomputed at the end) lets three 256-thread CTAs share an SM instead of two.
-template <int D, bool SHG>
+template <int D>
 // Gaussians [gbeg, gend) only (gbeg a multiple of BLK): outputs are addressed relative to gbeg,
 // so a caller can reduce each finished chunk while the next one computes.
-__global__ __launch_bounds__(BLK, SHG ? 3 : 2) void k_gauss_bwd(Launch L, mvgs_grads gr, mvgs_adc adc, int64_t gbeg,
+__global__ __launch_bounds__(BLK, 2) void k_gauss_bwd(Launch L, mvgs_grads gr, mvgs_adc adc, int64_t gbeg,
                                                                  int64_t gend) {
-    constexpr int NK = ShRows<D>::NK, NS = ShRows<D>::NS, SS = ShRows<D>::STRIDE;
-    constexpr int VB = SHG ? GB_VB_SHG : GB_VB;
+    constexpr int NS = ShRows<D>::NS, SS = ShRows<D>::STRIDE;
+    constexpr int VB = GB_VB;
+    constexpr int NS4 = NS / 4 > 0 ? NS / 4 : 1;  // float4 per row when NS % 4 == 0
     extern __shared__ float4 smem_sh4[];  // 16-byte aligned base
     float* smem_sh = reinterpret_cast<float*>(smem_sh4);
     float* dsh_s = smem_sh;                              // [BLK][SS]
-    float* sh_s = SHG ? nullptr : smem_sh + BLK * SS;    // [BLK][SS] (staged rows, !SHG)
+    float* sh_s = smem_sh + BLK * SS;                    // [BLK][SS] staged SH rows
     __shared__ int wc[BLK / 32][32];
     __shared__ float4 scam[32];  // per view of the chunk: camera centre (x, y, z), Jacobian clamp limit x
     __shared__ float scl[32];    // clamp limit y
@@ -388,12 +382,11 @@ __global__ __launch_bounds__(BLK, SHG ? 3 : 2) void k_gauss_bwd(Launch L, mvgs_g
     const int64_t g = g0 + threadIdx.x;
     const int64_t o = g - gbeg;  // output row
     const bool valid = g < gend;
-    if (!SHG) {  // SH rows: coalesced async copies (no registers, all in flight), waited on before first use
+    {  // SH rows: coalesced async copies (no registers, all in flight), waited on before first use
         const int nb = (int)min((int64_t)BLK, gend - g0);
         const float* src = L.sh + g0 * (int64_t)L.sh_stride * 3;
         const int rowlen = L.sh_stride * 3;
         if ((rowlen & 3) == 0 && (NS & 3) == 0 && ((uintptr_t)src & 15) == 0) {
-            constexpr int NS4 = NS / 4;
             for (int i = threadIdx.x; i < nb * NS4; i += BLK) {
                 const int r = i / NS4, k = 4 * (i - r * NS4);
                 cp_async16(&sh_s[r * SS + k], src + (int64_t)r * rowlen + k);
@@ -411,7 +404,7 @@ __global__ __launch_bounds__(BLK, SHG ? 3 : 2) void k_gauss_bwd(Launch L, mvgs_g
         for (int i = threadIdx.x; i < BLK * SS / 4; i += BLK) z4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
     // SH row of this Gaussian: staged copy, or global (16-byte aligned: checked by the launcher)
-    const float* sh = SHG ? L.sh + (valid ? g : 0) * (int64_t)L.sh_stride * 3 : sh_s + threadIdx.x * SS;
+    const float* sh = sh_s + threadIdx.x * SS;
     float* dsh = dsh_s + threadIdx.x * SS;
     float mx = 0.f, my = 0.f, mz = 0.f;
     float Sg[6];  // Σ (only Σ is needed in the view loop)
@@ -482,7 +475,7 @@ __global__ __launch_bounds__(BLK, SHG ? 3 : 2) void k_gauss_bwd(Launch L, mvgs_g
                 pgb[u] = pgp[1];
                 pgc[u] = pgp[2];
             }
-            if (!SHG && !sh_ready) {  // block-uniform: overlap the SH copy with the first pair loads
+            if (!sh_ready) {  // block-uniform: overlap the SH copy with the first pair loads
                 cp_async_wait_all();
                 __syncthreads();
                 sh_ready = true;
@@ -493,12 +486,12 @@ __global__ __launch_bounds__(BLK, SHG ? 3 : 2) void k_gauss_bwd(Launch L, mvgs_g
             const mvgs_camera& c = L.cams[v0 + k0 + u];
             const uint32_t flags = fl[u];
             const float4 pg0 = pga[u], pg1 = pgb[u], pg2 = pgc[u];
-            pair_chain<D, SHG>(c, scam[k0 + u], scl[k0 + u], flags, pg0, pg1, pg2, mx, my, mz, Sg, sh, dsh, sW, sH, A);
+            pair_chain<D>(c, scam[k0 + u], scl[k0 + u], flags, pg0, pg1, pg2, mx, my, mz, Sg, sh, dsh, sW, sH, A);
             }
         }
         __syncthreads();
     }
-    if (!SHG && !sh_ready) {  // no view chunk ran (V == 0 cannot happen, but keep the copy complete)
+    if (!sh_ready) {  // no view chunk ran (V == 0 cannot happen, but keep the copy complete)
         cp_async_wait_all();
         __syncthreads();
     }
@@ -508,7 +501,6 @@ __global__ __launch_bounds__(BLK, SHG ? 3 : 2) void k_gauss_bwd(Launch L, mvgs_g
         float* dst = gr.d_sh + (g0 - gbeg) * (int64_t)L.sh_stride * 3;
         const int rowlen = L.sh_stride * 3;
         if (rowlen == NS && (NS & 3) == 0 && ((uintptr_t)dst & 15) == 0) {  // float4 rows, constant divisor
-            constexpr int NS4 = NS / 4;
             float4* dst4 = reinterpret_cast<float4*>(dst);
             for (int i = threadIdx.x; i < nb * NS4; i += BLK) {
                 const int r = i / NS4, k4 = i - r * NS4;
@@ -528,27 +520,15 @@ __global__ __launch_bounds__(BLK, SHG ? 3 : 2) void k_gauss_bwd(Launch L, mvgs_g
     finish_gaussian(L, gr, adc, g, o, A);
 }
 
-template <int D, bool SHG>
-cudaError_t launch_gauss_bwd_v(const Launch& L, const mvgs_grads& gr, const mvgs_adc& adc, int64_t gb, int64_t ge,
-                               cudaStream_t s) {
-    const size_t smem = sizeof(float) * (SHG ? 1 : 2) * BLK * ShRows<D>::STRIDE;
-    cudaError_t e = cudaFuncSetAttribute(k_gauss_bwd<D, SHG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    const int nblk = (int)((ge - gb + BLK - 1) / BLK);
-    if (nblk > 0) k_gauss_bwd<D, SHG><<<nblk, BLK, smem, s>>>(L, gr, adc, gb, ge);
-    return cudaGetLastError();
-}
-
-#ifndef GB_SH_GLOBAL
-#define GB_SH_GLOBAL 0  // 1 measured slower (0.71 vs 0.61 ms at garden): 3 CTAs of rows thrash L1
-#endif
-
 template <int D>
 cudaError_t launch_gauss_bwd_t(const Launch& L, const mvgs_grads& gr, const mvgs_adc& adc, int64_t gb, int64_t ge,
                                cudaStream_t s) {
-    // rows read as float4 from global: row length and base must keep every row 16-byte aligned
-    const bool shg = GB_SH_GLOBAL && ((L.sh_stride * 3) & 3) == 0 && ((uintptr_t)L.sh & 15) == 0;
-    return shg ? launch_gauss_bwd_v<D, true>(L, gr, adc, gb, ge, s) : launch_gauss_bwd_v<D, false>(L, gr, adc, gb, ge, s);
+    const size_t smem = sizeof(float) * 2 * BLK * ShRows<D>::STRIDE;
+    cudaError_t e = cudaFuncSetAttribute(k_gauss_bwd<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    const int nblk = (int)((ge - gb + BLK - 1) / BLK);
+    if (nblk > 0) k_gauss_bwd<D><<<nblk, BLK, smem, s>>>(L, gr, adc, gb, ge);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_gauss_bwd(const Launch& L, const mvgs_grads& gr, const mvgs_adc& adc, int64_t gb, int64_t ge,

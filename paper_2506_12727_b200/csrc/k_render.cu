@@ -35,7 +35,6 @@ namespace mvgs {
 #endif
 constexpr int kFwdUnroll = MVGS_FWD_UNROLL, kBwdUnroll = MVGS_BWD_UNROLL;
 constexpr int RT = 128;            // threads per CTA = entries per staged batch
-constexpr int NWR = RT / 32;       // warps per CTA
 constexpr unsigned FULLR = 0xffffffffu;
 
 // CTA-wide sums of two per-thread counts → one 64-bit atomic each per CTA.
