@@ -406,7 +406,7 @@ __global__ __launch_bounds__(BLK, 2) void k_gauss_bwd(Launch L, mvgs_grads gr, m
     // SH row of this Gaussian: staged copy, or global (16-byte aligned: checked by the launcher)
     const float* sh = sh_s + threadIdx.x * SS;
     float* dsh = dsh_s + threadIdx.x * SS;
-    float mx = 0.f, my = 0.f, mz = 0.f;
+    float mx = 0.f, my = 0.f, mz = 0.f, smax = 0.f;
     float Sg[6];  // Σ (only Σ is needed in the view loop)
     {
         FastActiv a;
@@ -414,6 +414,7 @@ __global__ __launch_bounds__(BLK, 2) void k_gauss_bwd(Launch L, mvgs_grads gr, m
             mx = L.means[3 * g];
             my = L.means[3 * g + 1];
             mz = L.means[3 * g + 2];
+            smax = participation_smax(L.log_scales[3 * g], L.log_scales[3 * g + 1], L.log_scales[3 * g + 2]);
             fast_activate(L.log_scales + 3 * g, L.quats + 4 * g, L.opac[g], a);
         } else {
             fast_activate(L.log_scales, L.quats, 0.f, a);  // any finite values; unused
@@ -428,7 +429,7 @@ __global__ __launch_bounds__(BLK, 2) void k_gauss_bwd(Launch L, mvgs_grads gr, m
         const int nv = min(32, L.V - v0);
         for (int k = 0; k < nv; k++) {
             const mvgs_camera& c = L.cams[v0 + k];
-            const bool vis = valid && ca_depth(c, mx, my, mz) > c.znear;
+            const bool vis = valid && ca_participates(c, mx, my, mz, smax, L.TX, L.TY);
             const unsigned bal = __ballot_sync(FULLG, vis);
             if (lane == 0) wc[warp][k] = __popc(bal);
         }
@@ -462,7 +463,7 @@ __global__ __launch_bounds__(BLK, 2) void k_gauss_bwd(Launch L, mvgs_grads gr, m
                 const int k = k0 + u;
                 if (k >= nv) continue;  // warp-uniform
                 const mvgs_camera& c = L.cams[v0 + k];
-                const bool zvis = valid && ca_depth(c, mx, my, mz) > c.znear;
+                const bool zvis = valid && ca_participates(c, mx, my, mz, smax, L.TX, L.TY);
                 const unsigned bal = __ballot_sync(FULLG, zvis);
                 if (!zvis) continue;
                 const int64_t pair = (int64_t)sboff[k] + wc[warp][k] + __popc(bal & lt);

@@ -158,17 +158,18 @@ __global__ __launch_bounds__(BLK) void k_count(Launch L) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t g = (int64_t)blockIdx.x * BLK + threadIdx.x;
     const bool valid = g < L.P;
-    float mx = 0.f, my = 0.f, mz = 0.f;
+    float mx = 0.f, my = 0.f, mz = 0.f, smax = 0.f;
     if (valid) {
         mx = L.means[3 * g];
         my = L.means[3 * g + 1];
         mz = L.means[3 * g + 2];
+        smax = participation_smax(L.log_scales[3 * g], L.log_scales[3 * g + 1], L.log_scales[3 * g + 2]);
     }
     for (int v0 = 0; v0 < L.V; v0 += 32) {
         const int nv = min(32, L.V - v0);
         for (int k = 0; k < nv; k++) {
             const mvgs_camera& c = L.cams[v0 + k];
-            const bool vis = valid && ca_depth(c, mx, my, mz) > c.znear;
+            const bool vis = valid && ca_participates(c, mx, my, mz, smax, L.TX, L.TY);
             const unsigned bal = __ballot_sync(FULL, vis);
             if (lane == 0) wc[warp][k] = __popc(bal);
         }
@@ -255,12 +256,13 @@ __global__ __launch_bounds__(BLK) void k_project(Launch L) {
         cp_async_commit();
     }
     const float* sh = sh_s + threadIdx.x * SS;
-    float mx = 0.f, my = 0.f, mz = 0.f;
+    float mx = 0.f, my = 0.f, mz = 0.f, smax = 0.f;
     Activ a;
     if (valid) {
         mx = L.means[3 * g];
         my = L.means[3 * g + 1];
         mz = L.means[3 * g + 2];
+        smax = participation_smax(L.log_scales[3 * g], L.log_scales[3 * g + 1], L.log_scales[3 * g + 2]);
         ca_activate(L.log_scales + 3 * g, L.quats + 4 * g, L.opac[g], a);
     }
     const unsigned lt = (1u << lane) - 1u;
@@ -270,7 +272,7 @@ __global__ __launch_bounds__(BLK) void k_project(Launch L) {
         const int nv = min(32, L.V - v0);
         for (int k = 0; k < nv; k++) {
             const mvgs_camera& c = L.cams[v0 + k];
-            const bool vis = valid && ca_depth(c, mx, my, mz) > c.znear;
+            const bool vis = valid && ca_participates(c, mx, my, mz, smax, L.TX, L.TY);
             const unsigned bal = __ballot_sync(FULL, vis);
             if (lane == 0) wc[warp][k] = __popc(bal);
         }
@@ -280,7 +282,7 @@ __global__ __launch_bounds__(BLK) void k_project(Launch L) {
         for (int k = 0; k < nv; k++) {
             const int v = v0 + k;
             const mvgs_camera& c = L.cams[v];
-            const bool vis = valid && ca_depth(c, mx, my, mz) > c.znear;
+            const bool vis = valid && ca_participates(c, mx, my, mz, smax, L.TX, L.TY);
             const unsigned bal = __ballot_sync(FULL, vis);
             if (!vis) continue;
             int pre = 0;
@@ -397,7 +399,7 @@ cudaError_t launch_project(const Launch& L, cudaStream_t s) {
 // ------------------------------------------------------------------ export (tests)
 // (view, gid) of pair slot q, recomputed from the slot allocation (no per-pair ids are
 // stored by the path): the view and 256-Gaussian block by binary search over the scanned
-// per-(view, block) offsets, then the rank among the block's z-visible Gaussians.
+// per-(view, block) offsets, then the rank among the block's participating Gaussians.
 __device__ void slot_ids(const Launch& L, int64_t q, int& view, int64_t& gid) {
     int lo = 0, hi = L.V * L.NB - 1;  // last (view, block) index with blk_off ≤ q (skips empty ones)
     while (lo < hi) {
@@ -411,7 +413,8 @@ __device__ void slot_ids(const Launch& L, int64_t q, int& view, int64_t& gid) {
     const mvgs_camera& c = L.cams[view];
     gid = -1;
     for (int64_t g = (int64_t)b * BLK; g < min(L.P, (int64_t)(b + 1) * BLK); g++) {
-        if (ca_depth(c, L.means[3 * g], L.means[3 * g + 1], L.means[3 * g + 2]) > c.znear && r-- == 0) {
+        const float sm = participation_smax(L.log_scales[3 * g], L.log_scales[3 * g + 1], L.log_scales[3 * g + 2]);
+        if (ca_participates(c, L.means[3 * g], L.means[3 * g + 1], L.means[3 * g + 2], sm, L.TX, L.TY) && r-- == 0) {
             gid = g;
             break;
         }
