@@ -117,29 +117,42 @@ __device__ __forceinline__ float ca_depth(const mvgs_camera& c, float mx, float 
 // (DESIGN.md §4.9).  With r ≤ ⌈3·√(a + c + 0.32)⌉ and a + c ≤ ‖J‖²_F·s²_max + 0.6 (Σ' = JWΣWᵀJᵀ
 // + 0.3·I, W a rotation, λ_max(Σ) = s²_max), rect x is empty when px + r < 1 or
 // px − r ≥ 16·TX (same for y); the bound is inflated by 0.1 % and 2 px.  Every operation is an
-// explicit RN intrinsic (no contraction) so each kernel that re-derives the pair slots takes
-// the same decision.  smax = participation_smax(log_scales).
+// explicit intrinsic (RN arithmetic, MUFU approximations; no contraction), so each kernel that
+// re-derives the pair slots takes the same decision.  smax = participation_smax(log_scales).
 __device__ __forceinline__ float participation_smax(float l0, float l1, float l2) {
     return FMUL(__expf(fmaxf(l0, fmaxf(l1, l2))), 1.001f);
 }
 
+__device__ __forceinline__ float pt_rcp(float x) {  // MUFU.RCP: deterministic, ≤ 1 ulp
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ float pt_sqrt(float x) {
+    float y;
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
 __device__ __forceinline__ bool ca_participates(const mvgs_camera& c, float mx, float my, float mz, float smax,
                                                 int TX, int TY) {
-    const float tz = FMA(c.R[8], mz, FMA(c.R[7], my, FMA(c.R[6], mx, c.t[2])));
+    const float tz = FMA(c.R[8], mz, FMA(c.R[7], my, FMA(c.R[6], mx, c.t[2])));  // the CA z-test (R27)
     if (!(tz > c.znear)) return false;
+    // the bound: approximate but deterministic operations; their errors (≲ 1e-6 relative)
+    // sit far inside the 0.1 % + 2 px slack
     const float tx = FMA(c.R[2], mz, FMA(c.R[1], my, FMA(c.R[0], mx, c.t[0])));
     const float ty = FMA(c.R[5], mz, FMA(c.R[4], my, FMA(c.R[3], mx, c.t[1])));
-    const float ux = FDIV(tx, tz), uy = FDIV(ty, tz);
+    const float itz = pt_rcp(tz);
+    const float ux = FMUL(tx, itz), uy = FMUL(ty, itz);
     const float px = FMA(c.fx, ux, c.cx), py = FMA(c.fy, uy, c.cy);
-    const float limx = FDIV(FMUL(0.65f, __int2float_rn(c.width)), c.fx);
-    const float limy = FDIV(FMUL(0.65f, __int2float_rn(c.height)), c.fy);
+    const float limx = FMUL(FMUL(0.65f, __int2float_rn(c.width)), pt_rcp(c.fx));
+    const float limy = FMUL(FMUL(0.65f, __int2float_rn(c.height)), pt_rcp(c.fy));
     const float cux = fminf(fabsf(ux), limx), cuy = fminf(fabsf(uy), limy);
-    const float jf = FDIV(FADD(FMUL(FMUL(c.fx, c.fx), FADD(1.0f, FMUL(cux, cux))),
-                               FMUL(FMUL(c.fy, c.fy), FADD(1.0f, FMUL(cuy, cuy)))),
-                          FMUL(tz, tz));  // ‖J‖²_F
-    const float tr = FADD(FMUL(FMUL(jf, FMUL(smax, smax)), 1.001f), 0.92f);
-    const float rub = FADD(FMUL(3.0f, FSQRT(tr)), 2.0f);  // > r, incl. the ceil
-    if (!(rub < 1e30f)) return true;                      // overflow / NaN: keep the pair
+    const float jf = FMUL(FADD(FMUL(FMUL(c.fx, c.fx), FMA(cux, cux, 1.0f)), FMUL(FMUL(c.fy, c.fy), FMA(cuy, cuy, 1.0f))),
+                          FMUL(itz, itz));  // ‖J‖²_F
+    const float tr = FMA(FMUL(jf, FMUL(smax, smax)), 1.001f, 0.92f);
+    const float rub = FMA(3.0f, pt_sqrt(tr), 2.0f);  // > r, incl. the ceil
+    if (!(rub < 1e30f)) return true;                 // overflow / NaN: keep the pair
     if (FADD(px, rub) < 1.0f || FSUB(px, rub) > 16.0f * (float)TX) return false;
     if (FADD(py, rub) < 1.0f || FSUB(py, rub) > 16.0f * (float)TY) return false;
     return true;

@@ -427,9 +427,11 @@ __global__ __launch_bounds__(BLK, 2) void k_gauss_bwd(Launch L, mvgs_grads gr, m
     bool sh_ready = false;  // SH rows arrive asynchronously; waited on after the first view loads
     for (int v0 = 0; v0 < L.V; v0 += 32) {
         const int nv = min(32, L.V - v0);
+        unsigned pm = 0;  // participation in the chunk's views (evaluated once, as in k_project)
         for (int k = 0; k < nv; k++) {
             const mvgs_camera& c = L.cams[v0 + k];
             const bool vis = valid && ca_participates(c, mx, my, mz, smax, L.TX, L.TY);
+            pm |= vis ? 1u << k : 0u;
             const unsigned bal = __ballot_sync(FULLG, vis);
             if (lane == 0) wc[warp][k] = __popc(bal);
         }
@@ -462,8 +464,7 @@ __global__ __launch_bounds__(BLK, 2) void k_gauss_bwd(Launch L, mvgs_grads gr, m
                 fl[u] = 0u;
                 const int k = k0 + u;
                 if (k >= nv) continue;  // warp-uniform
-                const mvgs_camera& c = L.cams[v0 + k];
-                const bool zvis = valid && ca_participates(c, mx, my, mz, smax, L.TX, L.TY);
+                const bool zvis = (pm >> k) & 1u;
                 const unsigned bal = __ballot_sync(FULLG, zvis);
                 if (!zvis) continue;
                 const int64_t pair = (int64_t)sboff[k] + wc[warp][k] + __popc(bal & lt);

@@ -270,9 +270,11 @@ __global__ __launch_bounds__(BLK) void k_project(Launch L) {
     unsigned my_vis = 0;              // stored visible pairs of this Gaussian
     for (int v0 = 0; v0 < L.V; v0 += 32) {
         const int nv = min(32, L.V - v0);
+        unsigned pm = 0;  // participation of this Gaussian in the chunk's views (evaluated once)
         for (int k = 0; k < nv; k++) {
             const mvgs_camera& c = L.cams[v0 + k];
             const bool vis = valid && ca_participates(c, mx, my, mz, smax, L.TX, L.TY);
+            pm |= vis ? 1u << k : 0u;
             const unsigned bal = __ballot_sync(FULL, vis);
             if (lane == 0) wc[warp][k] = __popc(bal);
         }
@@ -282,7 +284,7 @@ __global__ __launch_bounds__(BLK) void k_project(Launch L) {
         for (int k = 0; k < nv; k++) {
             const int v = v0 + k;
             const mvgs_camera& c = L.cams[v];
-            const bool vis = valid && ca_participates(c, mx, my, mz, smax, L.TX, L.TY);
+            const bool vis = (pm >> k) & 1u;
             const unsigned bal = __ballot_sync(FULL, vis);
             if (!vis) continue;
             int pre = 0;
