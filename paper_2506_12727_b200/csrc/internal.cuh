@@ -29,6 +29,7 @@ struct Launch {  // everything a kernel needs about the current batch
     int V, W, H, TX, TY, T, NB;
     int sh_degree, sh_stride;
     int count_evals;  // compositing kernels count (pixel, entry) evaluations (statistics)
+    uint32_t* pmask;  // [P] participation bits per view (V ≤ 32; written by k_count), else null
     float bg[3];
     const mvgs_camera* cams;  // device [V]
     const float *means, *log_scales, *quats, *opac, *sh;
@@ -101,6 +102,8 @@ struct mvgs_ctx {
     unsigned long long* d_ent64 = nullptr;  // [cap_entries] bucket-sort keys (depth << 32 | pair)
     int* d_bcur = nullptr;                  // [V*T] bucket cursors
     int64_t cap_bcur = 0;
+    uint32_t* d_pmask = nullptr;            // [P] participation bits (V ≤ 32)
+    int64_t cap_pmask = 0;
     double* d_lab_part = nullptr;           // NEXT-4 per-CTA fp64 partials
     int* d_adc_cnt = nullptr;        // NEXT-3 per-Gaussian emitted-row counts → offsets
     int64_t cap_adc_cnt = 0;

@@ -427,12 +427,16 @@ __global__ __launch_bounds__(BLK, 2) void k_gauss_bwd(Launch L, mvgs_grads gr, m
     bool sh_ready = false;  // SH rows arrive asynchronously; waited on after the first view loads
     for (int v0 = 0; v0 < L.V; v0 += 32) {
         const int nv = min(32, L.V - v0);
-        unsigned pm = 0;  // participation in the chunk's views (evaluated once, as in k_project)
+        // participation in the chunk's views: k_count's bits when stored (as in k_project)
+        unsigned pm = 0;
+        if (L.pmask) {
+            pm = valid ? L.pmask[g] : 0u;
+        } else {
+            for (int k = 0; k < nv; k++)
+                pm |= (valid && ca_participates(L.cams[v0 + k], mx, my, mz, smax, L.TX, L.TY)) ? 1u << k : 0u;
+        }
         for (int k = 0; k < nv; k++) {
-            const mvgs_camera& c = L.cams[v0 + k];
-            const bool vis = valid && ca_participates(c, mx, my, mz, smax, L.TX, L.TY);
-            pm |= vis ? 1u << k : 0u;
-            const unsigned bal = __ballot_sync(FULLG, vis);
+            const unsigned bal = __ballot_sync(FULLG, (pm >> k) & 1u);
             if (lane == 0) wc[warp][k] = __popc(bal);
         }
         if (threadIdx.x < nv) {

@@ -167,12 +167,15 @@ __global__ __launch_bounds__(BLK) void k_count(Launch L) {
     }
     for (int v0 = 0; v0 < L.V; v0 += 32) {
         const int nv = min(32, L.V - v0);
+        unsigned pm = 0;
         for (int k = 0; k < nv; k++) {
             const mvgs_camera& c = L.cams[v0 + k];
             const bool vis = valid && ca_participates(c, mx, my, mz, smax, L.TX, L.TY);
+            pm |= vis ? 1u << k : 0u;
             const unsigned bal = __ballot_sync(FULL, vis);
             if (lane == 0) wc[warp][k] = __popc(bal);
         }
+        if (L.pmask && valid) L.pmask[g] = pm;  // V ≤ 32: one chunk; project and gauss_bwd reuse it
         __syncthreads();
         if (threadIdx.x < nv) {
             int s = 0;
@@ -270,12 +273,16 @@ __global__ __launch_bounds__(BLK) void k_project(Launch L) {
     unsigned my_vis = 0;              // stored visible pairs of this Gaussian
     for (int v0 = 0; v0 < L.V; v0 += 32) {
         const int nv = min(32, L.V - v0);
-        unsigned pm = 0;  // participation of this Gaussian in the chunk's views (evaluated once)
+        // participation of this Gaussian in the chunk's views: k_count's bits when stored
+        unsigned pm = 0;
+        if (L.pmask) {
+            pm = valid ? L.pmask[g] : 0u;
+        } else {
+            for (int k = 0; k < nv; k++)
+                pm |= (valid && ca_participates(L.cams[v0 + k], mx, my, mz, smax, L.TX, L.TY)) ? 1u << k : 0u;
+        }
         for (int k = 0; k < nv; k++) {
-            const mvgs_camera& c = L.cams[v0 + k];
-            const bool vis = valid && ca_participates(c, mx, my, mz, smax, L.TX, L.TY);
-            pm |= vis ? 1u << k : 0u;
-            const unsigned bal = __ballot_sync(FULL, vis);
+            const unsigned bal = __ballot_sync(FULL, (pm >> k) & 1u);
             if (lane == 0) wc[warp][k] = __popc(bal);
         }
         if (threadIdx.x < nv) sboff[threadIdx.x] = L.blk_off[(int64_t)(v0 + threadIdx.x) * L.NB + blockIdx.x];

@@ -234,7 +234,7 @@ void mvgs_destroy(mvgs_ctx* ctx) {
     cudaFree(ctx->d_pflag);
     cudaFree(ctx->d_counters); cudaFree(ctx->d_counters64); cudaFree(ctx->d_scan);
     cudaFree(ctx->d_dssim_coef); cudaFree(ctx->d_dssim_part);
-    cudaFree(ctx->d_bcur); cudaFree(ctx->d_ent64); cudaFree(ctx->d_lab_part);
+    cudaFree(ctx->d_bcur); cudaFree(ctx->d_ent64); cudaFree(ctx->d_lab_part); cudaFree(ctx->d_pmask);
     cudaFree(ctx->d_adc_cnt); cudaFree(ctx->d_adc_flags); cudaFree(ctx->d_adc_tmp); cudaFree(ctx->d_adc_rep);
     if (ctx->h_adc_rep) cudaFreeHost(ctx->h_adc_rep);
     if (ctx->h_cams) cudaFreeHost(ctx->h_cams);
@@ -287,9 +287,11 @@ mvgs_status mvgs_preprocess(mvgs_ctx* ctx, const mvgs_gaussians* g, const mvgs_c
     // workspace growth (synchronous only when it grows)
     // scan block sums, and the ranges close-up's per-1024-bucket minima (k_sort.cu)
     int64_t need_scan = std::max<int64_t>(scan_tmp_size((int)std::max(nblk, nbuck)), nbuck / 1024 + 2);
+    const int64_t need_pmask = V <= 32 ? std::max<int64_t>(g->P, 1) : 1;  // participation masks (V ≤ 32)
     if (nblk + 1 > ctx->cap_blk || nbuck + 1 > ctx->cap_buckets || V > ctx->cap_cams || need_scan > ctx->cap_scan ||
-        !ctx->d_blk) {
+        need_pmask > ctx->cap_pmask || !ctx->d_blk) {
         CK(cudaDeviceSynchronize());
+        CK(grow(ctx->d_pmask, ctx->cap_pmask, need_pmask));
         CK(grow(ctx->d_blk, ctx->cap_blk, nblk + 1));
         CK(grow(ctx->d_bucket, ctx->cap_buckets, nbuck + 1));
         CK(grow(ctx->d_bcur, ctx->cap_bcur, nbuck + 1));
@@ -327,6 +329,7 @@ mvgs_status mvgs_preprocess(mvgs_ctx* ctx, const mvgs_gaussians* g, const mvgs_c
     L.sh_degree = g->sh_degree;
     L.sh_stride = g->sh_stride;
     L.count_evals = ctx->count_evals ? 1 : 0;
+    L.pmask = V <= 32 ? ctx->d_pmask : nullptr;  // k_count stores each Gaussian's participation bits
     for (int k = 0; k < 3; k++) L.bg[k] = bg ? bg[k] : 0.f;
     L.means = g->means; L.log_scales = g->log_scales; L.quats = g->quats; L.opac = g->opacity_logits; L.sh = g->sh;
     fill_launch(ctx);
