@@ -420,3 +420,31 @@ def test_step_captures_in_a_cuda_graph():
         assert_close_rel(grads[k].cpu().numpy(), a.cpu().numpy(), k)
     for a, k in zip(eager[3 + len(grads):], sorted(adc)):
         assert_close_rel(adc[k].cpu().numpy(), a.cpu().numpy(), k)
+
+
+def test_participation_bound_at_the_image_border():
+    """§4.9: Gaussians centred just outside every border, with footprints that end just
+    inside or just outside the image, large Jacobian-clamped ones far off-screen, and
+    anisotropic ones — the conservative off-screen test must keep every pair whose rect is
+    non-empty (checked against the oracle's z-test set), and lists / images stay exact."""
+    rng = np.random.default_rng(41)
+    W, H, f = 96, 72, 80.0
+    n = 1500
+    z = rng.uniform(0.5, 6.0, n)
+    side = rng.integers(0, 4, n)
+    # pixel position just outside a border, then back-projected
+    off = rng.uniform(0.0, 40.0, n)
+    px = np.where(side == 0, -off, np.where(side == 1, W - 1 + off, rng.uniform(0, W - 1, n)))
+    py = np.where(side == 2, -off, np.where(side == 3, H - 1 + off, rng.uniform(0, H - 1, n)))
+    far = rng.random(n) < 0.1  # some far off-screen (clamped Jacobian)
+    px = np.where(far, px + np.sign(px - W / 2) * rng.uniform(200, 2000, n), px)
+    means = np.column_stack([(px - (W - 1) / 2) / f * z, (py - (H - 1) / 2) / f * z, z])
+    ls = np.log(rng.uniform(0.003, 0.3, (n, 3)) * z[:, None] / 3)
+    g = _scene(means, ls, rng.uniform(-2, 4, n), rgb=rng.uniform(0, 1, (n, 3)))
+    q = rng.normal(size=(n, 4))
+    g["quats"] = (q / np.linalg.norm(q, axis=1, keepdims=True)).astype(np.float32)
+    cam = synth.cams_array([synth.make_camera(np.eye(3), [0, 0, 0], W, H, f)])
+    gpu, o = _check_all(g, cam, bg=(0.2, 0.1, 0.0))
+    p, zv, zg = _gpu_pairs_in_oracle(o, gpu)
+    inert_z = int(p["zvis"].sum() - p["vis"].sum())
+    assert inert_z > 100 and gpu["stats"]["Q"] < int(p["zvis"].sum())  # the bound dropped some pairs
