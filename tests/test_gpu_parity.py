@@ -439,7 +439,7 @@ def test_participation_bound_at_the_image_border():
     far = rng.random(n) < 0.1  # some far off-screen (clamped Jacobian)
     px = np.where(far, px + np.sign(px - W / 2) * rng.uniform(200, 2000, n), px)
     means = np.column_stack([(px - (W - 1) / 2) / f * z, (py - (H - 1) / 2) / f * z, z])
-    ls = np.log(rng.uniform(0.003, 0.3, (n, 3)) * z[:, None] / 3)
+    ls = np.log(rng.uniform(0.003, 0.1, (n, 3)) * z[:, None] / 3)
     g = _scene(means, ls, rng.uniform(-2, 4, n), rgb=rng.uniform(0, 1, (n, 3)))
     q = rng.normal(size=(n, 4))
     g["quats"] = (q / np.linalg.norm(q, axis=1, keepdims=True)).astype(np.float32)
