@@ -56,7 +56,7 @@ def parse():
     ap.add_argument("--views", type=int, default=0,
                     help="views per GPU per step (default: the config's batch); the views-per-batch sweep")
     ap.add_argument("--impl", default="mvgs", choices=["mvgs", "reference"])
-    ap.add_argument("--e2e-steps", type=int, default=8)
+    ap.add_argument("--e2e-steps", type=int, default=16)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile", action="store_true",
                     help="sizing pass + warmup + one step, nothing else (for ncu)")
