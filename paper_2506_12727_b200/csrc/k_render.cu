@@ -627,31 +627,6 @@ __device__ __forceinline__ void bwd_exp(float power, float o, float& G, float& o
     }
 }
 
-// Both pixels' G and o·G (packed): hardware exp, and the CA exp for a lane whose o·G is within
-// 1e-5 (relative) of a threshold — the band test of bwd_exp with packed subtractions.
-__device__ __forceinline__ void bwd_exp2(float2 power, float2 o, float& G0, float& G1, float& oG0, float& oG1) {
-    const float2 pl = __fmul2_rn(power, f2(1.4426950408889634f, 1.4426950408889634f));
-    G0 = ex2_approx(pl.x);
-    G1 = ex2_approx(pl.y);
-    const float2 oG = __fmul2_rn(o, f2(G0, G1));
-    oG0 = oG.x;
-    oG1 = oG.y;
-    const float2 d1 = __fadd2_rn(oG, f2(-ALPHA_MIN, -ALPHA_MIN));
-    const float2 d2 = __fadd2_rn(oG, f2(-ALPHA_MAX, -ALPHA_MAX));
-    const bool b0 = fabsf(d1.x) < 1e-5f * ALPHA_MIN || fabsf(d2.x) < 1e-5f * ALPHA_MAX;
-    const bool b1 = fabsf(d1.y) < 1e-5f * ALPHA_MIN || fabsf(d2.y) < 1e-5f * ALPHA_MAX;
-    if (b0 || b1) {  // rare
-        if (b0) {
-            G0 = ca_exp_core(power.x);
-            oG0 = FMUL(o.x, G0);
-        }
-        if (b1) {
-            G1 = ca_exp_core(power.y);
-            oG1 = FMUL(o.y, G1);
-        }
-    }
-}
-
 template <bool CNT>
 __global__ __launch_bounds__(128, MVGS_BWD_MINB) void k_render_bwd_p(Launch L, const float* __restrict__ dL_drgb,
                                                       const float* __restrict__ in_T,
@@ -763,7 +738,8 @@ __global__ __launch_bounds__(128, MVGS_BWD_MINB) void k_render_bwd_p(Launch L, c
             if (!__any_sync(FULLR, in0 || in1)) continue;
             if (CNT) nexp += (unsigned)in0 + (unsigned)in1;
             float G0, G1, oG0, oG1;
-            bwd_exp2(power, f2(os.x, os.y), G0, G1, oG0, oG1);
+            bwd_exp(power.x, os.x, G0, oG0);
+            bwd_exp(power.y, os.y, G1, oG1);
             const float al0 = fminf(ALPHA_MAX, oG0), al1 = fminf(ALPHA_MAX, oG1);
             const bool v0 = in0 && !(al0 < ALPHA_MIN), v1 = in1 && !(al1 < ALPHA_MIN);
             if (!__any_sync(FULLR, v0 || v1)) continue;
