@@ -269,6 +269,10 @@ static void entry_digits(const Launch& L, int* bits, int* db) {
 // preceding tiles (status words tagged with a per-pass epoch, so nothing is cleared
 // between passes).  The first pass can drop "inert" keys (0xffffffff), compacting
 // the pairs with no tile before the remaining passes.
+#ifndef MVGS_OS_IPT
+#define MVGS_OS_IPT 8  // keys per thread of the onesweep tiles (dynamic shared memory)
+#endif
+constexpr int OS_IPT = MVGS_OS_IPT;
 constexpr uint32_t INERT = 0xffffffffu;
 constexpr unsigned long long ST_AGG = 1ull << 32, ST_PRE = 2ull << 32;
 
@@ -316,7 +320,7 @@ __device__ __forceinline__ unsigned long long ld_status(const unsigned long long
     return v;
 }
 
-template <bool PAYLOAD>
+template <bool PAYLOAD, int IPT>
 __global__ __launch_bounds__(RS_T) void k_rs_onesweep(const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin,
                                                       uint32_t* __restrict__ kout, uint32_t* __restrict__ vout,
                                                       const uint2* __restrict__ pin, uint2* __restrict__ pout,
@@ -327,8 +331,11 @@ __global__ __launch_bounds__(RS_T) void k_rs_onesweep(const uint32_t* __restrict
                                                       int* __restrict__ tile_ctr) {
     __shared__ uint32_t hist[RS_NW][RS_BINS];
     __shared__ uint32_t gdelta[RS_BINS];  // global offset − local start, per digit
-    __shared__ uint32_t sk[RS_TILE], sv[RS_TILE];
-    __shared__ uint2 sp[PAYLOAD ? RS_TILE : 1];
+    constexpr int TILE = RS_T * IPT;
+    extern __shared__ uint2 os_dyn[];  // sp[TILE] (payload), then sk[TILE], sv[TILE]
+    uint2* sp = os_dyn;
+    uint32_t* sk = reinterpret_cast<uint32_t*>(os_dyn + (PAYLOAD ? TILE : 0));
+    uint32_t* sv = sk + TILE;
     __shared__ int s_tile;
     __shared__ uint32_t s_total;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -338,26 +345,26 @@ __global__ __launch_bounds__(RS_T) void k_rs_onesweep(const uint32_t* __restrict
     const int tile = s_tile;
     const uint32_t epoch = (epoch_base[1] + (uint32_t)pass) & 0x3fffffffu;  // 30-bit tag
     const int n = (int)min((int64_t)*n_ptr, cap);
-    const int t0 = tile * RS_TILE;
+    const int t0 = tile * TILE;
     if (t0 >= n) return;  // every later tile is past n as well
-    const int nt = min(RS_TILE, n - t0);
+    const int nt = min(TILE, n - t0);
     const uint32_t mask = (1u << nbits) - 1u;
 #pragma unroll
     for (int i = 0; i < RS_BINS / 32; i++) hist[warp][lane + 32 * i] = 0;
     __syncwarp();
-    uint32_t key[RS_IPT], val[RS_IPT], loc[RS_IPT];
-    uint2 pay[PAYLOAD ? RS_IPT : 1];
+    uint32_t key[IPT], val[IPT], loc[IPT];
+    uint2 pay[PAYLOAD ? IPT : 1];
 #pragma unroll
-    for (int it = 0; it < RS_IPT; it++) {
-        const int p = warp * 32 * RS_IPT + it * 32 + lane;
+    for (int it = 0; it < IPT; it++) {
+        const int p = warp * 32 * IPT + it * 32 + lane;
         const bool ok = p < nt;
         key[it] = ok ? kin[t0 + p] : INERT;
         val[it] = vin ? (ok ? vin[t0 + p] : 0u) : (uint32_t)(t0 + p);  // no vin: the identity
         if (PAYLOAD) pay[PAYLOAD ? it : 0] = ok ? pin[t0 + p] : make_uint2(0u, 0u);
     }
 #pragma unroll
-    for (int it = 0; it < RS_IPT; it++) {
-        const int p = warp * 32 * RS_IPT + it * 32 + lane;
+    for (int it = 0; it < IPT; it++) {
+        const int p = warp * 32 * IPT + it * 32 + lane;
         const bool ok = p < nt && !(drop_inert && key[it] == INERT);
         const uint32_t d = (key[it] >> shift) & mask;
         const unsigned peers = digit_peers(d, ok, nbits);
@@ -404,7 +411,7 @@ __global__ __launch_bounds__(RS_T) void k_rs_onesweep(const uint32_t* __restrict
     }
     __syncthreads();
 #pragma unroll
-    for (int it = 0; it < RS_IPT; it++) {
+    for (int it = 0; it < IPT; it++) {
         if (loc[it] != 0xffffffffu) {
             const uint32_t l = hist[warp][(key[it] >> shift) & mask] + loc[it];
             sk[l] = key[it];
@@ -450,12 +457,17 @@ int radix_sort(uint32_t* k, uint32_t* v, uint32_t* k2, uint32_t* v2, uint2* pl, 
         const int nb = min(db, bits - shift);
         const int* np = (pass == 0) ? n_ptr : (drop_inert ? n_after : n_ptr);
         const uint32_t* vin = (pass == 0 && identity_vals) ? nullptr : vs;
+        constexpr int OT = RS_T * OS_IPT;
+        const int otiles = (int)((cap + OT - 1) / OT);
+        const size_t osm = (size_t)OT * ((pl ? 8 : 0) + 8);
+        if (pl) cudaFuncSetAttribute(k_rs_onesweep<true, OS_IPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)osm);
+        else cudaFuncSetAttribute(k_rs_onesweep<false, OS_IPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)osm);
         if (pl)
-            k_rs_onesweep<true><<<ntiles, RS_T, 0, s>>>(ks, vin, kd, vd, ps, pd, np, cap, shift, nb,
+            k_rs_onesweep<true, OS_IPT><<<otiles, RS_T, osm, s>>>(ks, vin, kd, vd, ps, pd, np, cap, shift, nb,
                                                         (drop_inert && pass == 0) ? 1 : 0, gbase + pass * RS_BINS,
                                                         rs.status, epoch, pass, tctr + pass);
         else
-            k_rs_onesweep<false><<<ntiles, RS_T, 0, s>>>(ks, vin, kd, vd, nullptr, nullptr, np, cap, shift, nb,
+            k_rs_onesweep<false, OS_IPT><<<otiles, RS_T, osm, s>>>(ks, vin, kd, vd, nullptr, nullptr, np, cap, shift, nb,
                                                          (drop_inert && pass == 0) ? 1 : 0, gbase + pass * RS_BINS,
                                                          rs.status, epoch, pass, tctr + pass);
         if ((*err = cudaGetLastError()) != cudaSuccess) return pass;
