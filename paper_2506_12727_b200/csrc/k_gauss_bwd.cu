@@ -18,12 +18,20 @@ namespace mvgs {
 
 constexpr unsigned FULLG = 0xffffffffu;
 
-__constant__ float g_SH1 = 0.4886025119029199f;
-__constant__ float g_SH2[5] = {1.0925484305920792f, -1.0925484305920792f, 0.31539156525252005f,
-                               -1.0925484305920792f, 0.5462742152960396f};
-__constant__ float g_SH3[7] = {-0.5900435899266435f, 2.890611442640554f, -0.4570457994644658f,
-                               0.3731763325901154f, -0.4570457994644658f, 1.445305721320277f,
-                               -0.5900435899266435f};
+// real SH constants [3DGS] as compile-time values (folded into the products)
+constexpr float g_SH1 = 0.4886025119029199f;
+constexpr float g_SH2_0 = 1.0925484305920792f;
+constexpr float g_SH2_1 = -1.0925484305920792f;
+constexpr float g_SH2_2 = 0.31539156525252005f;
+constexpr float g_SH2_3 = -1.0925484305920792f;
+constexpr float g_SH2_4 = 0.5462742152960396f;
+constexpr float g_SH3_0 = -0.5900435899266435f;
+constexpr float g_SH3_1 = 2.890611442640554f;
+constexpr float g_SH3_2 = -0.4570457994644658f;
+constexpr float g_SH3_3 = 0.3731763325901154f;
+constexpr float g_SH3_4 = -0.4570457994644658f;
+constexpr float g_SH3_5 = 1.445305721320277f;
+constexpr float g_SH3_6 = -0.5900435899266435f;
 
 // Hardware approximations for values that decide nothing: MUFU.RCP /
 // MUFU.SQRT (≤ 2 ulp) instead of the multi-instruction IEEE sequences.
@@ -247,32 +255,32 @@ __device__ __forceinline__ void pair_chain(const mvgs_camera& c, float4 cam4, fl
     }
     if (D >= 2) {
         const float xx = x * x, yy = y * y, zz = z * z;
-        Y[4] = g_SH2[0] * x * y;
-        Y[5] = g_SH2[1] * y * z;
-        Y[6] = g_SH2[2] * (2.f * zz - xx - yy);
-        Y[7] = g_SH2[3] * x * z;
-        Y[8] = g_SH2[4] * (xx - yy);
-        ddx += g_SH2[0] * y * wk[4] - 2.f * g_SH2[2] * x * wk[6] + g_SH2[3] * z * wk[7] + 2.f * g_SH2[4] * x * wk[8];
-        ddy += g_SH2[0] * x * wk[4] + g_SH2[1] * z * wk[5] - 2.f * g_SH2[2] * y * wk[6] - 2.f * g_SH2[4] * y * wk[8];
-        ddz += g_SH2[1] * y * wk[5] + 4.f * g_SH2[2] * z * wk[6] + g_SH2[3] * x * wk[7];
+        Y[4] = g_SH2_0 * x * y;
+        Y[5] = g_SH2_1 * y * z;
+        Y[6] = g_SH2_2 * (2.f * zz - xx - yy);
+        Y[7] = g_SH2_3 * x * z;
+        Y[8] = g_SH2_4 * (xx - yy);
+        ddx += g_SH2_0 * y * wk[4] - 2.f * g_SH2_2 * x * wk[6] + g_SH2_3 * z * wk[7] + 2.f * g_SH2_4 * x * wk[8];
+        ddy += g_SH2_0 * x * wk[4] + g_SH2_1 * z * wk[5] - 2.f * g_SH2_2 * y * wk[6] - 2.f * g_SH2_4 * y * wk[8];
+        ddz += g_SH2_1 * y * wk[5] + 4.f * g_SH2_2 * z * wk[6] + g_SH2_3 * x * wk[7];
         if (D >= 3) {
-            Y[9] = g_SH3[0] * y * (3.f * xx - yy);
-            Y[10] = g_SH3[1] * x * y * z;
-            Y[11] = g_SH3[2] * y * (4.f * zz - xx - yy);
-            Y[12] = g_SH3[3] * z * (2.f * zz - 3.f * xx - 3.f * yy);
-            Y[13] = g_SH3[4] * x * (4.f * zz - xx - yy);
-            Y[14] = g_SH3[5] * z * (xx - yy);
-            Y[15] = g_SH3[6] * x * (xx - 3.f * yy);
-            ddx += g_SH3[0] * 6.f * x * y * wk[9] + g_SH3[1] * y * z * wk[10] - g_SH3[2] * 2.f * x * y * wk[11]
-                 - g_SH3[3] * 6.f * x * z * wk[12] + g_SH3[4] * (4.f * zz - 3.f * xx - yy) * wk[13]
-                 + g_SH3[5] * 2.f * x * z * wk[14] + g_SH3[6] * (3.f * xx - 3.f * yy) * wk[15];
-            ddy += g_SH3[0] * (3.f * xx - 3.f * yy) * wk[9] + g_SH3[1] * x * z * wk[10]
-                 + g_SH3[2] * (4.f * zz - xx - 3.f * yy) * wk[11] - g_SH3[3] * 6.f * y * z * wk[12]
-                 - g_SH3[4] * 2.f * x * y * wk[13] - g_SH3[5] * 2.f * y * z * wk[14]
-                 - g_SH3[6] * 6.f * x * y * wk[15];
-            ddz += g_SH3[1] * x * y * wk[10] + g_SH3[2] * 8.f * y * z * wk[11]
-                 + g_SH3[3] * (6.f * zz - 3.f * xx - 3.f * yy) * wk[12] + g_SH3[4] * 8.f * x * z * wk[13]
-                 + g_SH3[5] * (xx - yy) * wk[14];
+            Y[9] = g_SH3_0 * y * (3.f * xx - yy);
+            Y[10] = g_SH3_1 * x * y * z;
+            Y[11] = g_SH3_2 * y * (4.f * zz - xx - yy);
+            Y[12] = g_SH3_3 * z * (2.f * zz - 3.f * xx - 3.f * yy);
+            Y[13] = g_SH3_4 * x * (4.f * zz - xx - yy);
+            Y[14] = g_SH3_5 * z * (xx - yy);
+            Y[15] = g_SH3_6 * x * (xx - 3.f * yy);
+            ddx += g_SH3_0 * 6.f * x * y * wk[9] + g_SH3_1 * y * z * wk[10] - g_SH3_2 * 2.f * x * y * wk[11]
+                 - g_SH3_3 * 6.f * x * z * wk[12] + g_SH3_4 * (4.f * zz - 3.f * xx - yy) * wk[13]
+                 + g_SH3_5 * 2.f * x * z * wk[14] + g_SH3_6 * (3.f * xx - 3.f * yy) * wk[15];
+            ddy += g_SH3_0 * (3.f * xx - 3.f * yy) * wk[9] + g_SH3_1 * x * z * wk[10]
+                 + g_SH3_2 * (4.f * zz - xx - 3.f * yy) * wk[11] - g_SH3_3 * 6.f * y * z * wk[12]
+                 - g_SH3_4 * 2.f * x * y * wk[13] - g_SH3_5 * 2.f * y * z * wk[14]
+                 - g_SH3_6 * 6.f * x * y * wk[15];
+            ddz += g_SH3_1 * x * y * wk[10] + g_SH3_2 * 8.f * y * z * wk[11]
+                 + g_SH3_3 * (6.f * zz - 3.f * xx - 3.f * yy) * wk[12] + g_SH3_4 * 8.f * x * z * wk[13]
+                 + g_SH3_5 * (xx - yy) * wk[14];
         }
     }
     {

@@ -193,12 +193,20 @@ cudaError_t launch_count(const Launch& L, cudaStream_t s) {
 }
 
 // ------------------------------------------------------------------ S2
-__constant__ float c_SH1 = 0.4886025119029199f;
-__constant__ float c_SH2[5] = {1.0925484305920792f, -1.0925484305920792f, 0.31539156525252005f,
-                               -1.0925484305920792f, 0.5462742152960396f};
-__constant__ float c_SH3[7] = {-0.5900435899266435f, 2.890611442640554f, -0.4570457994644658f,
-                               0.3731763325901154f, -0.4570457994644658f, 1.445305721320277f,
-                               -0.5900435899266435f};
+// real SH constants [3DGS] as compile-time values (folded into the products)
+constexpr float c_SH1 = 0.4886025119029199f;
+constexpr float c_SH2_0 = 1.0925484305920792f;
+constexpr float c_SH2_1 = -1.0925484305920792f;
+constexpr float c_SH2_2 = 0.31539156525252005f;
+constexpr float c_SH2_3 = -1.0925484305920792f;
+constexpr float c_SH2_4 = 0.5462742152960396f;
+constexpr float c_SH3_0 = -0.5900435899266435f;
+constexpr float c_SH3_1 = 2.890611442640554f;
+constexpr float c_SH3_2 = -0.4570457994644658f;
+constexpr float c_SH3_3 = 0.3731763325901154f;
+constexpr float c_SH3_4 = -0.4570457994644658f;
+constexpr float c_SH3_5 = 1.445305721320277f;
+constexpr float c_SH3_6 = -0.5900435899266435f;
 
 // Real SH basis (R17), degree D, direction (x,y,z) unit.
 template <int D>
@@ -211,19 +219,19 @@ __device__ __forceinline__ void sh_eval_basis(float x, float y, float z, float* 
     }
     if (D >= 2) {
         const float xx = x * x, yy = y * y, zz = z * z;
-        Y[4] = c_SH2[0] * x * y;
-        Y[5] = c_SH2[1] * y * z;
-        Y[6] = c_SH2[2] * (2.f * zz - xx - yy);
-        Y[7] = c_SH2[3] * x * z;
-        Y[8] = c_SH2[4] * (xx - yy);
+        Y[4] = c_SH2_0 * x * y;
+        Y[5] = c_SH2_1 * y * z;
+        Y[6] = c_SH2_2 * (2.f * zz - xx - yy);
+        Y[7] = c_SH2_3 * x * z;
+        Y[8] = c_SH2_4 * (xx - yy);
         if (D >= 3) {
-            Y[9] = c_SH3[0] * y * (3.f * xx - yy);
-            Y[10] = c_SH3[1] * x * y * z;
-            Y[11] = c_SH3[2] * y * (4.f * zz - xx - yy);
-            Y[12] = c_SH3[3] * z * (2.f * zz - 3.f * xx - 3.f * yy);
-            Y[13] = c_SH3[4] * x * (4.f * zz - xx - yy);
-            Y[14] = c_SH3[5] * z * (xx - yy);
-            Y[15] = c_SH3[6] * x * (xx - 3.f * yy);
+            Y[9] = c_SH3_0 * y * (3.f * xx - yy);
+            Y[10] = c_SH3_1 * x * y * z;
+            Y[11] = c_SH3_2 * y * (4.f * zz - xx - yy);
+            Y[12] = c_SH3_3 * z * (2.f * zz - 3.f * xx - 3.f * yy);
+            Y[13] = c_SH3_4 * x * (4.f * zz - xx - yy);
+            Y[14] = c_SH3_5 * z * (xx - yy);
+            Y[15] = c_SH3_6 * x * (xx - 3.f * yy);
         }
     }
 }
