@@ -128,7 +128,7 @@ struct ShRows {
 };
 
 #ifndef GB_VB
-#define GB_VB 2  // views whose pair loads are issued together (4: more loads in flight, more spills)
+#define GB_VB 1  // views whose pair loads are issued together (measured: 1 → 0.60 ms, 2 → 0.61, 4 → 0.67)
 #endif
 
 // One visible (Gaussian, view) pair of the chain rule (S8) and its ADC terms (S9), added into
