@@ -30,6 +30,9 @@ namespace mvgs {
 #ifndef MVGS_BWD_UNROLL
 #define MVGS_BWD_UNROLL 1
 #endif
+#ifndef MVGS_FWD_BATCH
+#define MVGS_FWD_BATCH 1  // forward staged batch = 128 × this entries
+#endif
 #ifndef MVGS_BWD_MINB
 #define MVGS_BWD_MINB 6  // resident CTAs per SM asked of the packed backward (register cap 65536/(128·MINB))
 #endif
@@ -263,9 +266,11 @@ template <bool DEPTH, bool CNT>
 __global__ __launch_bounds__(RT) void k_render_fwd_p(Launch L, float* __restrict__ out_rgb,
                                                      float* __restrict__ out_T, int32_t* __restrict__ out_n,
                                                      float* __restrict__ out_D) {
-    __shared__ FwdConsts sf[RT];
-    __shared__ uint8_t smask[RT];
-    __shared__ uint8_t slist[RT / 32][RT];
+    constexpr int FB = RT * MVGS_FWD_BATCH;  // entries per staged batch (≤ 256: uint8 list indices)
+    static_assert(FB <= 256, "list indices are bytes");
+    __shared__ FwdConsts sf[FB];
+    __shared__ uint8_t smask[FB];
+    __shared__ uint8_t slist[RT / 32][FB];
     __shared__ unsigned sev[2];
     zero_pgrad_slice(L);
     const int bucket = blockIdx.x;
@@ -283,10 +288,10 @@ __global__ __launch_bounds__(RT) void k_render_fwd_p(Launch L, float* __restrict
     if (threadIdx.x == 0) sev[0] = sev[1] = 0;
     __syncthreads();
     if (end <= L.cap_entries) {
-        for (int b0 = start; b0 < end; b0 += RT) {
+        for (int b0 = start; b0 < end; b0 += FB) {
             if (__syncthreads_count(done0 && done1) == RT) break;
-            const int idx = b0 + threadIdx.x;
-            if (idx < end) {
+            for (int t = threadIdx.x; t < FB && b0 + t < end; t += RT) {
+                const int idx = b0 + t;
                 const float4* r = L.rec + 3 * (int64_t)L.sorted[idx];
                 const float4 r0 = r[0], r1 = r[1], r2 = r[2];
                 FwdConsts k;
@@ -297,12 +302,12 @@ __global__ __launch_bounds__(RT) void k_render_fwd_p(Launch L, float* __restrict
                 k.orr = make_float4(r1.y, r1.y, r1.z, r1.z);
                 k.gb = make_float4(r1.w, r1.w, r2.x, r2.x);
                 k.dd = ff2(r2.y, r2.y);
-                sf[threadIdx.x] = k;
-                smask[threadIdx.x] = (uint8_t)warp_block_mask(r0.x, r0.y, r0.z, r0.w, r1.x, sb, (float)(tx * TILE),
-                                                              (float)(ty * TILE));
+                sf[t] = k;
+                smask[t] = (uint8_t)warp_block_mask(r0.x, r0.y, r0.z, r0.w, r1.x, sb, (float)(tx * TILE),
+                                                    (float)(ty * TILE));
             }
             __syncthreads();
-            const int cnt = min(RT, end - b0);
+            const int cnt = min(FB, end - b0);
             const int wl = threadIdx.x >> 5;
             const int jbase = b0 - start + 1;  // list index + 1 of batch entry 0
             const int nl = warp_batch_list(smask, cnt, wl, threadIdx.x & 31, slist[wl]);
