@@ -30,6 +30,9 @@ namespace mvgs {
 #ifndef MVGS_BWD_UNROLL
 #define MVGS_BWD_UNROLL 1
 #endif
+#ifndef MVGS_BWD_RED4
+#define MVGS_BWD_RED4 1  // backward flush with 16-byte vector reductions
+#endif
 #ifndef MVGS_FWD_BATCH
 #define MVGS_FWD_BATCH 1  // forward staged batch = 128 × this entries
 #endif
@@ -604,6 +607,12 @@ struct BwdConsts {
 };
 
 __device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
+// 16-byte vector reduction into global memory (sm_90+): the four floats are added atomically
+// element-wise; the address must be 16-byte aligned (pair gradient slots are 48 B).
+__device__ __forceinline__ void red_add_v4(float* p, float a, float b, float c, float d) {
+    asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(d)
+                 : "memory");
+}
 __device__ __forceinline__ void st_shared_f32(uint32_t addr, float v) {
     asm volatile("st.shared.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
 }
@@ -790,6 +799,25 @@ __global__ __launch_bounds__(128, MVGS_BWD_MINB) void k_render_bwd_p(Launch L, c
             if (owner) wacc[jj * NG + my_id] = sum * oscale;
         }
         __syncthreads();
+#if MVGS_BWD_RED4
+        // one 16-byte vector reduction per (entry, quarter of its slot): 3 instead of ≤ 10
+        for (int i = threadIdx.x; i < cnt * 3; i += NT) {
+            const int jj = i / 3, qd = i - jj * 3;
+            float a[4];
+#pragma unroll
+            for (int e = 0; e < 4; e++) {
+                const int k = 4 * qd + e;
+                float sum = 0.f;
+                if (k < NG) {
+#pragma unroll
+                    for (int w = 0; w < NW; w++) sum += sacc[w][jj * NG + k];
+                }
+                a[e] = sum;
+            }
+            if (a[0] != 0.f || a[1] != 0.f || a[2] != 0.f || a[3] != 0.f)
+                red_add_v4(L.pgrad + (int64_t)sq[jj] * PG_STRIDE + 4 * qd, a[0], a[1], a[2], a[3]);
+        }
+#else
         for (int i = threadIdx.x; i < cnt * NG; i += NT) {
             float s = 0.f;
 #pragma unroll
@@ -799,6 +827,7 @@ __global__ __launch_bounds__(128, MVGS_BWD_MINB) void k_render_bwd_p(Launch L, c
                 atomicAdd(&L.pgrad[(int64_t)sq[jj] * PG_STRIDE + k], s);
             }
         }
+#endif
     }
     if (CNT) count_evals(&L.counters64[1], &L.counters64[3], nev, nexp, sev);
 }
