@@ -31,7 +31,7 @@ namespace mvgs {
 #define MVGS_BWD_UNROLL 1
 #endif
 #ifndef MVGS_BWD_RED4
-#define MVGS_BWD_RED4 1  // backward flush with 16-byte vector reductions
+#define MVGS_BWD_RED4 0  // 1: backward flush with 16-byte vector reductions (measured: no gain)
 #endif
 #ifndef MVGS_FWD_BATCH
 #define MVGS_FWD_BATCH 1  // forward staged batch = 128 × this entries
