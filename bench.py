@@ -259,35 +259,21 @@ def run_mvgs(args):
     bufs = [buf, GradBuffer(P, S, dev, chunks=CHUNKS)]
     comp = torch.cuda.current_stream()
     s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
-    # each direction's bytes split over two streams (two copy engines in flight per direction)
-    NSPLIT = int(os.environ.get("MVGS_E2E_SPLIT", "2"))
-    s_in2, s_out2 = torch.cuda.Stream(), torch.cuda.Stream()
     mk = lambda: [torch.cuda.Event() for _ in range(2)]  # noqa: E731
     in_ready, in_free, out_ready, out_free = mk(), mk(), mk(), mk()
-    in_ready2, out_free2 = mk(), mk()
 
     def e2e_step(i):
         b = i % 2
         if i >= 2:
             s_in.wait_event(in_free[b])
-            s_in2.wait_event(in_free[b])
         with torch.cuda.stream(s_in):
             for k, t in host_in.items():
-                if NSPLIT > 1 and k == "sh":
-                    continue
                 g_slots[b][k].copy_(t, non_blocking=True)
             dL_slots[b].copy_(host_dL, non_blocking=True)
-        if NSPLIT > 1:
-            with torch.cuda.stream(s_in2):
-                g_slots[b]["sh"].copy_(host_in["sh"], non_blocking=True)
-            in_ready2[b].record(s_in2)
-            comp.wait_event(in_ready2[b])
         in_ready[b].record(s_in)
         comp.wait_event(in_ready[b])
         if i >= 2:
             comp.wait_event(out_free[b])
-            if NSPLIT > 1:
-                comp.wait_event(out_free2[b])
         ob = bufs[b]
         mvgs.preprocess(R.ctx, g_slots[b], R.cams)
         mvgs.render_fwd(R.ctx, *outs)
@@ -296,17 +282,8 @@ def run_mvgs(args):
         in_free[b].record(comp)
         out_ready[b].record(comp)
         s_out.wait_event(out_ready[b])
-        if NSPLIT > 1:
-            half = ob.flat.numel() // 2
-            with torch.cuda.stream(s_out):
-                host_out[b][:half].copy_(ob.flat[:half], non_blocking=True)
-            s_out2.wait_event(out_ready[b])
-            with torch.cuda.stream(s_out2):
-                host_out[b][half:].copy_(ob.flat[half:], non_blocking=True)
-            out_free2[b].record(s_out2)
-        else:
-            with torch.cuda.stream(s_out):
-                host_out[b].copy_(ob.flat, non_blocking=True)
+        with torch.cuda.stream(s_out):
+            host_out[b].copy_(ob.flat, non_blocking=True)
         out_free[b].record(s_out)
 
     if dist is not None:
@@ -315,12 +292,9 @@ def run_mvgs(args):
     e0, e1_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(comp)
     s_in.wait_event(e0)
-    s_in2.wait_event(e0)
     for i in range(args.e2e_steps):
         e2e_step(i)
     comp.wait_event(out_free[(args.e2e_steps - 1) % 2])
-    if NSPLIT > 1:
-        comp.wait_event(out_free2[(args.e2e_steps - 1) % 2])
     e1_.record(comp)
     torch.cuda.synchronize()
     e2e_ms = e0.elapsed_time(e1_) / args.e2e_steps
