@@ -382,6 +382,7 @@ __global__ __launch_bounds__(BLK, 2) void k_gauss_bwd(Launch L, mvgs_grads gr, m
     __shared__ int wc[BLK / 32][32];
     __shared__ float4 scam[32];  // per view of the chunk: camera centre (x, y, z), Jacobian clamp limit x
     __shared__ float scl[32];    // clamp limit y
+    __shared__ mvgs_camera scams[32];  // the chunk's cameras (LDS in the per-pair chain)
     __shared__ int sboff[32];  // first pair slot of this block in each view of the chunk
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const unsigned lt = (1u << lane) - 1u;
@@ -447,6 +448,8 @@ __global__ __launch_bounds__(BLK, 2) void k_gauss_bwd(Launch L, mvgs_grads gr, m
             const unsigned bal = __ballot_sync(FULLG, (pm >> k) & 1u);
             if (lane == 0) wc[warp][k] = __popc(bal);
         }
+        for (int i = threadIdx.x; i < nv * (int)(sizeof(mvgs_camera) / 4); i += BLK)
+            reinterpret_cast<uint32_t*>(scams)[i] = reinterpret_cast<const uint32_t*>(L.cams + v0)[i];
         if (threadIdx.x < nv) {
             sboff[threadIdx.x] = L.blk_off[(int64_t)(v0 + threadIdx.x) * L.NB + blk];
             const mvgs_camera& c = L.cams[v0 + threadIdx.x];
@@ -497,7 +500,7 @@ __global__ __launch_bounds__(BLK, 2) void k_gauss_bwd(Launch L, mvgs_grads gr, m
 #pragma unroll
             for (int u = 0; u < VB; u++) {
             if (!(fl[u] & PF_VISIBLE)) continue;  // not participating, or tiles == 0: inert (R27)
-            const mvgs_camera& c = L.cams[v0 + k0 + u];
+            const mvgs_camera& c = scams[k0 + u];
             const uint32_t flags = fl[u];
             const float4 pg0 = pga[u], pg1 = pgb[u], pg2 = pgc[u];
             pair_chain<D>(c, scam[k0 + u], scl[k0 + u], flags, pg0, pg1, pg2, mx, my, mz, Sg, sh, dsh, sW, sH, A);

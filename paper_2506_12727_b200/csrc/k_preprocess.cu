@@ -155,6 +155,7 @@ cudaError_t scan_exclusive(int* a, int n, int* total_slot, int* tmp, cudaStream_
 // ------------------------------------------------------------------ S1
 __global__ __launch_bounds__(BLK) void k_count(Launch L) {
     __shared__ int wc[BLK / 32][32];
+    __shared__ mvgs_camera scams[32];  // the chunk's cameras (LDS instead of per-field global loads)
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t g = (int64_t)blockIdx.x * BLK + threadIdx.x;
     const bool valid = g < L.P;
@@ -167,9 +168,13 @@ __global__ __launch_bounds__(BLK) void k_count(Launch L) {
     }
     for (int v0 = 0; v0 < L.V; v0 += 32) {
         const int nv = min(32, L.V - v0);
+        if (v0 > 0) __syncthreads();  // the previous chunk's cameras are no longer read
+        for (int i = threadIdx.x; i < nv * (int)(sizeof(mvgs_camera) / 4); i += BLK)
+            reinterpret_cast<uint32_t*>(scams)[i] = reinterpret_cast<const uint32_t*>(L.cams + v0)[i];
+        __syncthreads();
         unsigned pm = 0;
         for (int k = 0; k < nv; k++) {
-            const mvgs_camera& c = L.cams[v0 + k];
+            const mvgs_camera& c = scams[k];
             const bool vis = valid && ca_participates(c, mx, my, mz, smax, L.TX, L.TY);
             pm |= vis ? 1u << k : 0u;
             const unsigned bal = __ballot_sync(FULL, vis);
@@ -245,6 +250,7 @@ __global__ __launch_bounds__(BLK) void k_project(Launch L) {
     float* sh_s = reinterpret_cast<float*>(sh_s4);
     __shared__ int wc[BLK / 32][32];
     __shared__ int sboff[32];  // first pair slot of this block in each view of the chunk
+    __shared__ mvgs_camera scams[32];  // the chunk's cameras
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t g0 = (int64_t)blockIdx.x * BLK;
     const int64_t g = g0 + threadIdx.x;
@@ -294,11 +300,12 @@ __global__ __launch_bounds__(BLK) void k_project(Launch L) {
             if (lane == 0) wc[warp][k] = __popc(bal);
         }
         if (threadIdx.x < nv) sboff[threadIdx.x] = L.blk_off[(int64_t)(v0 + threadIdx.x) * L.NB + blockIdx.x];
+        for (int i = threadIdx.x; i < nv * (int)(sizeof(mvgs_camera) / 4); i += BLK)
+            reinterpret_cast<uint32_t*>(scams)[i] = reinterpret_cast<const uint32_t*>(L.cams + v0)[i];
         cp_async_wait_all();
         __syncthreads();
         for (int k = 0; k < nv; k++) {
-            const int v = v0 + k;
-            const mvgs_camera& c = L.cams[v];
+            const mvgs_camera& c = scams[k];
             const bool vis = (pm >> k) & 1u;
             const unsigned bal = __ballot_sync(FULL, vis);
             if (!vis) continue;
