@@ -448,3 +448,10 @@ def test_participation_bound_at_the_image_border():
     p, zv, zg = _gpu_pairs_in_oracle(o, gpu)
     inert_z = int(p["zvis"].sum() - p["vis"].sum())
     assert inert_z > 100 and gpu["stats"]["Q"] < int(p["zvis"].sum())  # the bound dropped some pairs
+
+
+def test_more_than_32_views():
+    """V = 40: two 32-view chunks in the per-Gaussian kernels and no stored participation
+    bits (V > 32 re-derives them) — lists, counts, images and gradients as the oracle's."""
+    g, cams = synth.make_scene(synth.scaled(synth.CONFIGS["tiny"], P=400, V=40, W=40, H=24))
+    _check_all(g, cams, bg=(0.1, 0.0, 0.2), seed=8)
