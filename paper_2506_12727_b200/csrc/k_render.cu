@@ -832,199 +832,6 @@ __global__ __launch_bounds__(128, MVGS_BWD_MINB) void k_render_bwd_p(Launch L, c
     if (CNT) count_evals(&L.counters64[1], &L.counters64[3], nev, nexp, sev);
 }
 
-// Two packed pixel pairs per thread (4 pixels): 64 threads per tile, warp w covers rows
-// 8w … 8w+7 (lane: column lane & 15, rows r, r+2 (pair 0) and r+4, r+6 (pair 1), r = 8w +
-// (lane >> 4)).  Same arithmetic per pixel as k_render_bwd_p; every warp reduction now sums
-// four pixels' terms, halving the reductions per pixel (MVGS_BWD_NP = 2).
-template <bool CNT>
-__global__ __launch_bounds__(64) void k_render_bwd_p2(Launch L, const float* __restrict__ dL_drgb,
-                                                      const float* __restrict__ in_T,
-                                                      const int32_t* __restrict__ in_n) {
-    constexpr int NT = 64, NW = 2, RB = 128, NPP = 2;
-    __shared__ BwdConsts sc[RB];
-    __shared__ uint32_t sq[RB];
-    __shared__ __align__(16) float sacc[NW][RB * NG];
-    __shared__ int smax;
-    __shared__ unsigned sev[2];
-    __shared__ uint8_t smask[RB];
-    __shared__ uint8_t slist[NW][RB];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int bucket = blockIdx.x;
-    const int v = bucket / L.T, tile = bucket - v * L.T;
-    const int ty = tile / L.TX, tx = tile - ty * L.TX;
-    const int x = tx * TILE + (lane & 15);
-    const int y0 = ty * TILE + 8 * warp + (lane >> 4);
-    const int start = L.bucket_off[bucket], end = L.bucket_off[bucket + 1];
-    if (end > L.cap_entries) return;
-    const int64_t HW = (int64_t)L.H * L.W;
-    float2 dLr[NPP], dLg[NPP], dLb[NPP], nTbg[NPP], T[NPP], accr[NPP], accg[NPP], accb[NPP], nfy[NPP];
-    int last[2 * NPP];
-    unsigned nev = 0;
-    int mylast = 0;
-#pragma unroll
-    for (int q = 0; q < NPP; q++) {
-        float dl[2][3], tf[2];
-#pragma unroll
-        for (int h = 0; h < 2; h++) {
-            const int y = y0 + 4 * q + 2 * h;
-            dl[h][0] = dl[h][1] = dl[h][2] = 0.f;
-            tf[h] = 1.f;
-            int ls = 0;
-            if (x < L.W && y < L.H) {
-                const int64_t pix = (int64_t)y * L.W + x;
-                dl[h][0] = dL_drgb[(3 * (int64_t)v + 0) * HW + pix];
-                dl[h][1] = dL_drgb[(3 * (int64_t)v + 1) * HW + pix];
-                dl[h][2] = dL_drgb[(3 * (int64_t)v + 2) * HW + pix];
-                tf[h] = in_T[v * HW + pix];
-                ls = in_n[v * HW + pix];
-            }
-            last[2 * q + h] = ls;
-            mylast = max(mylast, ls);
-        }
-        dLr[q] = f2(dl[0][0], dl[1][0]);
-        dLg[q] = f2(dl[0][1], dl[1][1]);
-        dLb[q] = f2(dl[0][2], dl[1][2]);
-        nTbg[q] = f2(-tf[0] * (L.bg[0] * dl[0][0] + L.bg[1] * dl[0][1] + L.bg[2] * dl[0][2]),
-                     -tf[1] * (L.bg[0] * dl[1][0] + L.bg[1] * dl[1][1] + L.bg[2] * dl[1][2]));
-        T[q] = f2(tf[0], tf[1]);
-        accr[q] = accg[q] = accb[q] = f2(0.f, 0.f);
-        nfy[q] = f2(-(float)(y0 + 4 * q), -(float)(y0 + 4 * q + 2));
-    }
-    if (threadIdx.x == 0) {
-        smax = 0;
-        sev[0] = sev[1] = 0;
-    }
-    __syncthreads();
-    unsigned nexp = 0;
-    if (mylast > 0) atomicMax(&smax, mylast);
-    __syncthreads();
-    const int maxlast = smax;
-    const int wmax = __reduce_max_sync(FULLR, mylast);
-    const int my_id = reduce_id(lane);
-    const bool owner = (__ffs(__match_any_sync(FULLR, my_id)) - 1) == lane;
-    const float hw = 0.5f * (float)L.W, hh = 0.5f * (float)L.H;
-    const float oscale = my_id == 0 ? -hw : my_id == 1 ? -hh : (my_id == 3 || my_id == 5) ? -0.5f : my_id == 4 ? -1.f : 1.f;
-    float* wacc = sacc[warp];
-    const float2 nfx = f2(-(float)x, -(float)x);
-    const float2 one = f2(1.f, 1.f), mone = f2(-1.f, -1.f), mhalf = f2(-0.5f, -0.5f);
-    const float2 hw2 = f2(hw * hw, hw * hw), hh2 = f2(hh * hh, hh * hh);
-    for (int b_end = maxlast; b_end > 0; b_end -= RB) {
-        const int b0 = max(0, b_end - RB);
-        const int cnt = b_end - b0;
-        __syncthreads();
-        for (int t = threadIdx.x; t < cnt; t += NT) {
-            const uint32_t qq = L.sorted[start + b0 + t];
-            sq[t] = qq;
-            const float4* r = L.rec + 3 * (int64_t)qq;
-            const float4 r0 = r[0], r1 = r[1], r2 = r[2];
-            BwdConsts k;
-            k.xy = make_float4(r0.x, r0.x, r0.y, r0.y);
-            k.ab = make_float4(r0.z, r0.z, r0.w, r0.w);
-            k.cnb = make_float4(r1.x, r1.x, -r0.w, -r0.w);
-            const float sb = skip_power(r1.y);
-            k.os = make_float4(r1.y, r1.y, sb, sb);
-            k.rg = make_float4(r1.z, r1.z, r1.w, r1.w);
-            k.bb = f2(r2.x, r2.x);
-            sc[t] = k;
-            const unsigned m4 = warp_block_mask(r0.x, r0.y, r0.z, r0.w, r1.x, sb, (float)(tx * TILE), (float)(ty * TILE));
-            smask[t] = (uint8_t)(((m4 & 3u) ? 1u : 0u) | ((m4 & 12u) ? 2u : 0u));  // 16×8 warp blocks
-        }
-        {
-            float4* w4 = reinterpret_cast<float4*>(wacc);
-            for (int i = lane; i < RB * NG / 4; i += 32) w4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-        }
-        __syncthreads();
-        const int nl = warp_batch_list(smask, min(cnt, wmax - b0), warp, lane, slist[warp]);
-        for (int u = nl - 1; u >= 0; u--) {
-            const int jj = slist[warp][u];
-            const int j = b0 + jj;
-            const float4 xy = sc[jj].xy, ab = sc[jj].ab, cnb = sc[jj].cnb, os = sc[jj].os;
-            const float2 dx = __fadd2_rn(f2(xy.x, xy.y), nfx);
-            float2 dy[NPP], power[NPP];
-            bool in[2 * NPP];
-            bool anyin = false;
-#pragma unroll
-            for (int q = 0; q < NPP; q++) {
-                dy[q] = __fadd2_rn(f2(xy.z, xy.w), nfy[q]);
-                const float2 Adx = __fmul2_rn(f2(ab.x, ab.y), dx);
-                const float2 CdyDy = __fmul2_rn(__fmul2_rn(f2(cnb.x, cnb.y), dy[q]), dy[q]);
-                const float2 inner = __ffma2_rn(Adx, dx, CdyDy);
-                const float2 nBdxdy = __fmul2_rn(__fmul2_rn(f2(cnb.z, cnb.w), dx), dy[q]);
-                power[q] = __ffma2_rn(mhalf, inner, nBdxdy);
-                in[2 * q] = j < last[2 * q] && !(power[q].x > 0.f) && !(power[q].x < os.z);
-                in[2 * q + 1] = j < last[2 * q + 1] && !(power[q].y > 0.f) && !(power[q].y < os.z);
-                anyin |= in[2 * q] || in[2 * q + 1];
-                if (CNT) nev += (unsigned)(j < last[2 * q]) + (unsigned)(j < last[2 * q + 1]);
-            }
-            if (!__any_sync(FULLR, anyin)) continue;
-            float val[NG];
-#pragma unroll
-            for (int k = 0; k < NG; k++) val[k] = 0.f;
-            bool anyv = false;
-#pragma unroll
-            for (int q = 0; q < NPP; q++) {
-                if (!(in[2 * q] || in[2 * q + 1])) continue;
-                if (CNT) nexp += (unsigned)in[2 * q] + (unsigned)in[2 * q + 1];
-                float G0, G1, oG0, oG1;
-                bwd_exp(power[q].x, os.x, G0, oG0);
-                bwd_exp(power[q].y, os.y, G1, oG1);
-                const float al0 = fminf(ALPHA_MAX, oG0), al1 = fminf(ALPHA_MAX, oG1);
-                const bool v0 = in[2 * q] && !(al0 < ALPHA_MIN), v1 = in[2 * q + 1] && !(al1 < ALPHA_MIN);
-                if (!(v0 || v1)) continue;
-                anyv = true;
-                const float2 alpha = f2(v0 ? al0 : 0.f, v1 ? al1 : 0.f);
-                const float2 Gc = f2(v0 && !(oG0 > ALPHA_MAX) ? G0 : 0.f, v1 && !(oG1 > ALPHA_MAX) ? G1 : 0.f);
-                const float2 om = __ffma2_rn(alpha, mone, one);
-                const float2 inv = f2(rcp_approx(om.x), rcp_approx(om.y));
-                T[q] = __fmul2_rn(T[q], inv);
-                const float2 w = __fmul2_rn(alpha, T[q]);
-                const float4 rg = sc[jj].rg;
-                const float2 bb = sc[jj].bb;
-                const float2 cr = f2(rg.x, rg.y), cg = f2(rg.z, rg.w);
-                float2 dLda = __fmul2_rn(__ffma2_rn(accr[q], mone, cr), dLr[q]);
-                dLda = __ffma2_rn(__ffma2_rn(accg[q], mone, cg), dLg[q], dLda);
-                dLda = __ffma2_rn(__ffma2_rn(accb[q], mone, bb), dLb[q], dLda);
-                dLda = __ffma2_rn(dLda, T[q], __fmul2_rn(nTbg[q], inv));
-                accr[q] = __ffma2_rn(alpha, cr, __fmul2_rn(om, accr[q]));
-                accg[q] = __ffma2_rn(alpha, cg, __fmul2_rn(om, accg[q]));
-                accb[q] = __ffma2_rn(alpha, bb, __fmul2_rn(om, accb[q]));
-                const float2 dLdo = __fmul2_rn(Gc, dLda);
-                const float2 dLdpw = __fmul2_rn(__fmul2_rn(Gc, f2(os.x, os.y)), dLda);
-                const float2 d = __fmul2_rn(dLdpw, dx), e = __fmul2_rn(dLdpw, dy[q]);
-                const float2 gxr = __ffma2_rn(f2(ab.x, ab.y), d, __fmul2_rn(f2(ab.z, ab.w), e));
-                const float2 gyr = __ffma2_rn(f2(cnb.x, cnb.y), e, __fmul2_rn(f2(ab.z, ab.w), d));
-                const float2 n2 = __ffma2_rn(__fmul2_rn(gxr, gxr), hw2, __fmul2_rn(__fmul2_rn(gyr, gyr), hh2));
-                val[0] += gxr.x + gxr.y;
-                val[1] += gyr.x + gyr.y;
-                val[2] += sqrt_approx(n2.x) + sqrt_approx(n2.y);
-                const float2 dd = __fmul2_rn(d, dx), de = __fmul2_rn(d, dy[q]), ee = __fmul2_rn(e, dy[q]);
-                val[3] += dd.x + dd.y;
-                val[4] += de.x + de.y;
-                val[5] += ee.x + ee.y;
-                val[6] += dLdo.x + dLdo.y;
-                const float2 wr = __fmul2_rn(w, dLr[q]), wg = __fmul2_rn(w, dLg[q]), wb = __fmul2_rn(w, dLb[q]);
-                val[7] += wr.x + wr.y;
-                val[8] += wg.x + wg.y;
-                val[9] += wb.x + wb.y;
-            }
-            if (!__any_sync(FULLR, anyv)) continue;
-            const float sum = warp_transpose_reduce10(val, lane);
-            if (owner) wacc[jj * NG + my_id] = sum * oscale;
-        }
-        __syncthreads();
-        for (int i = threadIdx.x; i < cnt * NG; i += NT) {
-            float s2 = 0.f;
-#pragma unroll
-            for (int w = 0; w < NW; w++) s2 += sacc[w][i];
-            if (s2 != 0.f) {
-                const int jj = i / NG, k = i - jj * NG;
-                atomicAdd(&L.pgrad[(int64_t)sq[jj] * PG_STRIDE + k], s2);
-            }
-        }
-    }
-    if (CNT) count_evals(&L.counters64[1], &L.counters64[3], nev, nexp, sev);
-}
-
 #ifndef MVGS_BWD_PACKED
 #define MVGS_BWD_PACKED 1
 #endif
@@ -1033,18 +840,7 @@ __global__ __launch_bounds__(64) void k_render_bwd_p2(Launch L, const float* __r
 #define MVGS_BWD_NPX 2
 #endif
 
-#ifndef MVGS_BWD_NP
-#define MVGS_BWD_NP 1  // packed pixel pairs per thread in the backward (2: k_render_bwd_p2)
-#endif
-
 cudaError_t launch_render_bwd(const Launch& L, const float* dL, const float* Tf, const int32_t* nc, cudaStream_t s) {
-    if (MVGS_BWD_PACKED && MVGS_BWD_NP == 2) {
-        if (L.count_evals)
-            k_render_bwd_p2<true><<<L.V * L.T, 64, 0, s>>>(L, dL, Tf, nc);
-        else
-            k_render_bwd_p2<false><<<L.V * L.T, 64, 0, s>>>(L, dL, Tf, nc);
-        return cudaGetLastError();
-    }
     if (MVGS_BWD_PACKED)
         if (L.count_evals)
             k_render_bwd_p<true><<<L.V * L.T, 128, 0, s>>>(L, dL, Tf, nc);
