@@ -127,9 +127,6 @@ struct ShRows {
     static constexpr int STRIDE = 4 * (NS4 | 1);
 };
 
-#ifndef GB_COMPACT
-#define GB_COMPACT 1  // per-lane compacted view loop (each lane walks its participating views)
-#endif
 #ifndef GB_VB
 #define GB_VB 1  // views whose pair loads are issued together (measured: 1 → 0.60 ms, 2 → 0.61, 4 → 0.67)
 #endif
@@ -376,9 +373,7 @@ template <int D>
 __global__ __launch_bounds__(BLK, 2) void k_gauss_bwd(Launch L, mvgs_grads gr, mvgs_adc adc, int64_t gbeg,
                                                                  int64_t gend) {
     constexpr int NS = ShRows<D>::NS, SS = ShRows<D>::STRIDE;
-#if !GB_COMPACT
     constexpr int VB = GB_VB;
-#endif
     constexpr int NS4 = NS / 4 > 0 ? NS / 4 : 1;  // float4 per row when NS % 4 == 0
     extern __shared__ float4 smem_sh4[];  // 16-byte aligned base
     float* smem_sh = reinterpret_cast<float*>(smem_sh4);
@@ -388,7 +383,6 @@ __global__ __launch_bounds__(BLK, 2) void k_gauss_bwd(Launch L, mvgs_grads gr, m
     __shared__ float4 scam[32];  // per view of the chunk: camera centre (x, y, z), Jacobian clamp limit x
     __shared__ float scl[32];    // clamp limit y
     __shared__ mvgs_camera scams[32];  // the chunk's cameras (LDS in the per-pair chain)
-    __shared__ unsigned sbal[BLK / 32][32];  // per (warp, view) participation ballots
     __shared__ int sboff[32];  // first pair slot of this block in each view of the chunk
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const unsigned lt = (1u << lane) - 1u;
@@ -452,10 +446,7 @@ __global__ __launch_bounds__(BLK, 2) void k_gauss_bwd(Launch L, mvgs_grads gr, m
         }
         for (int k = 0; k < nv; k++) {
             const unsigned bal = __ballot_sync(FULLG, (pm >> k) & 1u);
-            if (lane == 0) {
-                wc[warp][k] = __popc(bal);
-                sbal[warp][k] = bal;
-            }
+            if (lane == 0) wc[warp][k] = __popc(bal);
         }
         for (int i = threadIdx.x; i < nv * (int)(sizeof(mvgs_camera) / 4); i += BLK)
             reinterpret_cast<uint32_t*>(scams)[i] = reinterpret_cast<const uint32_t*>(L.cams + v0)[i];
@@ -479,29 +470,6 @@ __global__ __launch_bounds__(BLK, 2) void k_gauss_bwd(Launch L, mvgs_grads gr, m
             }
         }
         __syncthreads();
-#if GB_COMPACT
-        if (!sh_ready) {  // block-uniform
-            cp_async_wait_all();
-            __syncthreads();
-            sh_ready = true;
-        }
-        // Each lane walks only its own participating views (lowest set bit first): a warp runs
-        // max over lanes of popc(pm) rounds instead of one round per view of the chunk, and the
-        // lanes of a round all run the same chain code (cameras from shared memory per lane).
-        for (unsigned mm = pm; __any_sync(FULLG, mm != 0u);) {
-            if (mm) {
-                const int k = __ffs(mm) - 1;
-                mm &= mm - 1u;
-                const int64_t pair = (int64_t)sboff[k] + wc[warp][k] + __popc(sbal[warp][k] & lt);
-                const uint32_t flags = pair < L.cap_pairs ? L.pflag[pair] : 0u;
-                if (flags & PF_VISIBLE) {  // tiles == 0: inert (R27)
-                    const float4* pgp = reinterpret_cast<const float4*>(L.pgrad + pair * PG_STRIDE);
-                    pair_chain<D>(scams[k], scam[k], scl[k], flags, pgp[0], pgp[1], pgp[2], mx, my, mz, Sg, sh, dsh,
-                                  sW, sH, A);
-                }
-            }
-        }
-#else
         for (int k0 = 0; k0 < nv; k0 += VB) {
             // issue the loads of up to GB_VB views first (memory-level parallelism), then the math
             uint32_t fl[VB];
@@ -538,7 +506,6 @@ __global__ __launch_bounds__(BLK, 2) void k_gauss_bwd(Launch L, mvgs_grads gr, m
             pair_chain<D>(c, scam[k0 + u], scl[k0 + u], flags, pg0, pg1, pg2, mx, my, mz, Sg, sh, dsh, sW, sH, A);
             }
         }
-#endif
         __syncthreads();
     }
     if (!sh_ready) {  // no view chunk ran (V == 0 cannot happen, but keep the copy complete)
