@@ -127,6 +127,9 @@ struct ShRows {
     static constexpr int STRIDE = 4 * (NS4 | 1);
 };
 
+#ifndef GB_PREFETCH
+#define GB_PREFETCH 1  // L2 prefetch of the next view's pair flags and gradient slot
+#endif
 #ifndef GB_VB
 #define GB_VB 1  // views whose pair loads are issued together (measured: 1 → 0.60 ms, 2 → 0.61, 4 → 0.67)
 #endif
@@ -492,6 +495,22 @@ __global__ __launch_bounds__(BLK, 2) void k_gauss_bwd(Launch L, mvgs_grads gr, m
                 pgb[u] = pgp[1];
                 pgc[u] = pgp[2];
             }
+#if GB_PREFETCH
+            {  // next view's flags and gradient slot toward L2 while this view computes
+                const int kn = k0 + VB;
+                if (kn < nv) {
+                    const bool zn = (pm >> kn) & 1u;
+                    const unsigned baln = __ballot_sync(FULLG, zn);
+                    if (zn) {
+                        const int64_t pn = (int64_t)sboff[kn] + wc[warp][kn] + __popc(baln & lt);
+                        if (pn < L.cap_pairs) {
+                            asm volatile("prefetch.global.L2 [%0];" ::"l"(L.pflag + pn));
+                            asm volatile("prefetch.global.L2 [%0];" ::"l"(L.pgrad + pn * PG_STRIDE));
+                        }
+                    }
+                }
+            }
+#endif
             if (!sh_ready) {  // block-uniform: overlap the SH copy with the first pair loads
                 cp_async_wait_all();
                 __syncthreads();
