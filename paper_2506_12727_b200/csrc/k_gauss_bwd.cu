@@ -496,8 +496,10 @@ __global__ __launch_bounds__(BLK, 2) void k_gauss_bwd(Launch L, mvgs_grads gr, m
                 pgc[u] = pgp[2];
             }
 #if GB_PREFETCH
-            {  // next view's flags and gradient slot toward L2 while this view computes
-                const int kn = k0 + VB;
+            // the next GB_PREFETCH views' flags and gradient slots toward L2 while this view computes
+#pragma unroll
+            for (int pd = 1; pd <= GB_PREFETCH; pd++) {
+                const int kn = k0 + pd * VB;
                 if (kn < nv) {
                     const bool zn = (pm >> kn) & 1u;
                     const unsigned baln = __ballot_sync(FULLG, zn);
