@@ -33,6 +33,9 @@ namespace mvgs {
 #ifndef MVGS_BWD_RED4
 #define MVGS_BWD_RED4 0  // 1: backward flush with 16-byte vector reductions (measured: no gain)
 #endif
+#ifndef MVGS_FWD_PREFETCH
+#define MVGS_FWD_PREFETCH 1  // forward: next batch's indices a batch ahead, records prefetched to L2
+#endif
 #ifndef MVGS_FWD_BATCH
 #define MVGS_FWD_BATCH 1  // forward staged batch = 128 × this entries
 #endif
@@ -290,12 +293,15 @@ __global__ __launch_bounds__(RT) void k_render_fwd_p(Launch L, float* __restrict
     unsigned nev = 0, nexp = 0;
     if (threadIdx.x == 0) sev[0] = sev[1] = 0;
     __syncthreads();
+    // next batch's record index of this thread, loaded one batch ahead (FB == RT)
+    constexpr bool PF = MVGS_FWD_PREFETCH && FB == RT;
+    uint32_t qn = (PF && start + (int)threadIdx.x < end) ? L.sorted[start + threadIdx.x] : 0u;
     if (end <= L.cap_entries) {
         for (int b0 = start; b0 < end; b0 += FB) {
             if (__syncthreads_count(done0 && done1) == RT) break;
             for (int t = threadIdx.x; t < FB && b0 + t < end; t += RT) {
                 const int idx = b0 + t;
-                const float4* r = L.rec + 3 * (int64_t)L.sorted[idx];
+                const float4* r = L.rec + 3 * (int64_t)(PF ? qn : L.sorted[idx]);
                 const float4 r0 = r[0], r1 = r[1], r2 = r[2];
                 FwdConsts k;
                 k.xy = make_float4(r0.x, r0.x, r0.y, r0.y);
@@ -314,6 +320,10 @@ __global__ __launch_bounds__(RT) void k_render_fwd_p(Launch L, float* __restrict
             const int wl = threadIdx.x >> 5;
             const int jbase = b0 - start + 1;  // list index + 1 of batch entry 0
             const int nl = warp_batch_list(smask, cnt, wl, threadIdx.x & 31, slist[wl]);
+            if (PF) {  // the next batch: index now (consumed after this batch's walk)
+                const int nidx = b0 + FB + (int)threadIdx.x;
+                qn = nidx < end ? L.sorted[nidx] : 0u;
+            }
 #pragma unroll(kFwdUnroll)
             for (int u = 0; u < nl && !(done0 && done1); u++) {
                 const int j = slist[wl][u];
@@ -351,6 +361,11 @@ __global__ __launch_bounds__(RT) void k_render_fwd_p(Launch L, float* __restrict
                 const int jn = jbase + j;
                 last0 = bl0 ? jn : last0;
                 last1 = bl1 ? jn : last1;
+            }
+            if (PF && b0 + FB + (int)threadIdx.x < end) {  // warm the next batch's record in L2
+                const float4* rn = L.rec + 3 * (int64_t)qn;
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(rn));
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(rn + 2));
             }
         }
     }
