@@ -33,6 +33,9 @@ namespace mvgs {
 #ifndef MVGS_BWD_RED4
 #define MVGS_BWD_RED4 0  // 1: backward flush with 16-byte vector reductions (measured: no gain)
 #endif
+#ifndef MVGS_BWD_PREFETCH
+#define MVGS_BWD_PREFETCH 1  // backward: the same batch-ahead index load and L2 prefetch
+#endif
 #ifndef MVGS_FWD_PREFETCH
 #define MVGS_FWD_PREFETCH 1  // forward: next batch's indices a batch ahead, records prefetched to L2
 #endif
@@ -721,12 +724,19 @@ __global__ __launch_bounds__(128, MVGS_BWD_MINB) void k_render_bwd_p(Launch L, c
     const float2 nfx = f2(-(float)x, -(float)x), nfy = f2(-(float)y0, -(float)(y0 + 2));
     const float2 one = f2(1.f, 1.f), mone = f2(-1.f, -1.f), mhalf = f2(-0.5f, -0.5f);
     const float2 hw2 = f2(hw * hw, hw * hw), hh2 = f2(hh * hh, hh * hh);
+    // this thread's record index of the next (nearer) batch, loaded a batch ahead (RB == NT)
+    constexpr bool PF = MVGS_BWD_PREFETCH && RB == NT;
+    uint32_t qn = 0u;
+    if (PF && maxlast > 0) {
+        const int b0f = max(0, maxlast - RB);
+        if ((int)threadIdx.x < maxlast - b0f) qn = L.sorted[start + b0f + threadIdx.x];
+    }
     for (int b_end = maxlast; b_end > 0; b_end -= RB) {
         const int b0 = max(0, b_end - RB);
         const int cnt = b_end - b0;
         __syncthreads();
         for (int t = threadIdx.x; t < cnt; t += NT) {
-            const uint32_t q = L.sorted[start + b0 + t];
+            const uint32_t q = PF ? qn : L.sorted[start + b0 + t];
             sq[t] = q;
             const float4* r = L.rec + 3 * (int64_t)q;
             const float4 r0 = r[0], r1 = r[1], r2 = r[2];
@@ -748,6 +758,8 @@ __global__ __launch_bounds__(128, MVGS_BWD_MINB) void k_render_bwd_p(Launch L, c
         __syncthreads();
         // this warp's entries of the batch (culled by its pixel block), walked back to front
         const int nl = warp_batch_list(smask, min(cnt, wmax - b0), warp, lane, slist[warp]);
+        const int nb0 = max(0, b0 - RB), ncnt = b0 - nb0;  // the next batch (walked after this one)
+        if (PF && (int)threadIdx.x < ncnt) qn = L.sorted[start + nb0 + threadIdx.x];
 #pragma unroll(kBwdUnroll)
         for (int u = nl - 1; u >= 0; u--) {
             const int jj = slist[warp][u];
@@ -812,6 +824,11 @@ __global__ __launch_bounds__(128, MVGS_BWD_MINB) void k_render_bwd_p(Launch L, c
             val[9] = wb.x + wb.y;
             const float sum = warp_transpose_reduce10(val, lane);
             if (owner) wacc[jj * NG + my_id] = sum * oscale;
+        }
+        if (PF && (int)threadIdx.x < ncnt) {  // warm the next batch's record in L2
+            const float4* rn = L.rec + 3 * (int64_t)qn;
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(rn));
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(rn + 2));
         }
         __syncthreads();
 #if MVGS_BWD_RED4
