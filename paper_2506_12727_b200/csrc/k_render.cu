@@ -34,7 +34,7 @@ namespace mvgs {
 #define MVGS_BWD_RED4 0  // 1: backward flush with 16-byte vector reductions (measured: no gain)
 #endif
 #ifndef MVGS_BWD_PREFETCH
-#define MVGS_BWD_PREFETCH 1  // backward: the same batch-ahead index load and L2 prefetch
+#define MVGS_BWD_PREFETCH 0  // 1: backward batch-ahead index load + L2 prefetch (measured: no gain)
 #endif
 #ifndef MVGS_FWD_PREFETCH
 #define MVGS_FWD_PREFETCH 1  // forward: next batch's indices a batch ahead, records prefetched to L2
