@@ -549,17 +549,20 @@ __global__ __launch_bounds__(256) void k_dup(Launch L, const uint32_t* __restric
             lo += (31 - __clz(bal)) * step;  // lane 0 probes lo itself: bal ≠ 0
             hi = min(hi, lo + step);
         }
+        // the 32 pairs' (rect, slot, entry range) are loaded one group ahead of their use
+        uint2 rn = make_uint2(0u, 0u);
+        uint32_t qn = 0;
+        int ebn = Kw, enn = Kw;
+        if (lo + lane < Q) {
+            rn = rect[lo + lane];
+            qn = order[lo + lane];
+            ebn = ebase[lo + lane];
+            enn = ebase[lo + lane + 1];
+        }
         for (int i0 = lo; i0 < Q;) {
-            const int i = i0 + lane;
-            uint2 r = make_uint2(0u, 0u);
-            uint32_t q = 0;
-            int eb = Kw, en = Kw;
-            if (i < Q) {
-                r = rect[i];
-                q = order[i];
-                eb = ebase[i];
-                en = ebase[i + 1];
-            }
+            const uint2 r = rn;
+            const uint32_t q = qn;
+            const int eb = ebn, en = enn;
             const int s0 = max(eb, e0), s1 = min(en, e1);
             const int cnt = max(0, s1 - s0);
             int inc = cnt;
@@ -584,6 +587,18 @@ __global__ __launch_bounds__(256) void k_dup(Launch L, const uint32_t* __restric
             d.off0 = s0 - eb;
             desc[wid][lane] = d;
             __syncwarp();
+            if (enext < e1) {  // the next group, in flight while this one's entries are written
+                const int inx = i0 + 32 + lane;
+                rn = make_uint2(0u, 0u);
+                qn = 0;
+                ebn = enn = Kw;
+                if (inx < Q) {
+                    rn = rect[inx];
+                    qn = order[inx];
+                    ebn = ebase[inx];
+                    enn = ebase[inx + 1];
+                }
+            }
             // Entries in windows of 32: the owner of entry k is the last lane whose run starts at
             // or before k.  Lanes with entries have distinct, lane-ordered run starts, so a lane
             // starting inside the window marks its bit (and records itself at that position);
