@@ -116,6 +116,8 @@ __global__ __launch_bounds__(RS_T) void k_rs_scatter(const uint32_t* __restrict_
     if (t0 >= n) return;
     const int nt = min(TILE, n - t0);
     const uint32_t mask = (1u << nbits) - 1u;
+    // this tile's scanned offset of digit threadIdx.x: independent of the keys, loaded up front
+    const uint32_t goff = threadIdx.x <= mask ? (uint32_t)offs[(int64_t)threadIdx.x * ntiles + blockIdx.x] : 0u;
 #pragma unroll
     for (int i = 0; i < RS_BINS / 32; i++) hist[warp][lane + 32 * i] = 0;
     __syncwarp();
@@ -149,7 +151,7 @@ __global__ __launch_bounds__(RS_T) void k_rs_scatter(const uint32_t* __restrict_
         uint32_t ws;
         const uint32_t start = block_excl_scan_256_u(tot, &ws);
         dstart[threadIdx.x] = start;
-        gdelta[threadIdx.x] = threadIdx.x <= mask ? (uint32_t)offs[(int64_t)threadIdx.x * ntiles + blockIdx.x] - start : 0u;
+        gdelta[threadIdx.x] = goff - start;
         uint32_t run = start;
 #pragma unroll
         for (int w = 0; w < RS_NW; w++) {
@@ -349,6 +351,7 @@ __global__ __launch_bounds__(RS_T) void k_rs_onesweep(const uint32_t* __restrict
     if (t0 >= n) return;  // every later tile is past n as well
     const int nt = min(TILE, n - t0);
     const uint32_t mask = (1u << nbits) - 1u;
+    const uint32_t gb = gbase[threadIdx.x];  // this digit's global base (independent of the keys)
 #pragma unroll
     for (int i = 0; i < RS_BINS / 32; i++) hist[warp][lane + 32 * i] = 0;
     __syncwarp();
@@ -400,7 +403,7 @@ __global__ __launch_bounds__(RS_T) void k_rs_onesweep(const uint32_t* __restrict
         uint32_t all;
         const uint32_t start = block_excl_scan_256_u(tot, &all);
         if (d == 0) s_total = all;
-        gdelta[d] = gbase[d] + excl - start;
+        gdelta[d] = gb + excl - start;
         uint32_t run = start;
 #pragma unroll
         for (int w = 0; w < RS_NW; w++) {
