@@ -119,9 +119,12 @@ const char *mvgs_last_error(const mvgs_ctx *ctx);
 /* Grow capacities to at least (max_pairs, max_entries).  Synchronises the device. */
 mvgs_status mvgs_reserve(mvgs_ctx *ctx, int64_t max_pairs, int64_t max_entries);
 
-/* S1–S5: participation (z-test) and pair allocation, per-pair EWA
+/* S1–S5: participation and pair allocation, per-pair EWA
  * projection, conic, radius, tile rect and SH colour, duplication into
  * (view, tile) buckets, on-chip depth sort of every bucket, ranges.
+ * Participation = the z-test t.z > znear (R27) minus pairs whose tile rect is
+ * provably empty (a conservative screen-bound test); the
+ * remaining pairs with an empty rect stay allocated and inert.
  *   g     device parameter pointers (kept by the context for render_bwd /
  *         adc_stats; they must stay valid and unchanged until adc_stats).
  *   cams  host, V records; copied before return.
