@@ -134,8 +134,26 @@ __device__ __forceinline__ float pt_sqrt(float x) {
     return y;
 }
 
-__device__ __forceinline__ bool ca_participates(const mvgs_camera& c, float mx, float my, float mz, float smax,
-                                                int TX, int TY) {
+// Per-camera constants of the bound (computed by one code path for every caller).
+struct PartCam {
+    float limx, limy;  // Jacobian clamp limits 0.65·W/fx, 0.65·H/fy (R4)
+    float fx2, fy2;
+    float xmax, ymax;  // 16·TX, 16·TY
+};
+
+__device__ __forceinline__ PartCam make_partcam(const mvgs_camera& c, int TX, int TY) {
+    PartCam p;
+    p.limx = FMUL(FMUL(0.65f, __int2float_rn(c.width)), pt_rcp(c.fx));
+    p.limy = FMUL(FMUL(0.65f, __int2float_rn(c.height)), pt_rcp(c.fy));
+    p.fx2 = FMUL(c.fx, c.fx);
+    p.fy2 = FMUL(c.fy, c.fy);
+    p.xmax = 16.0f * (float)TX;
+    p.ymax = 16.0f * (float)TY;
+    return p;
+}
+
+__device__ __forceinline__ bool ca_participates(const mvgs_camera& c, const PartCam& pc, float mx, float my, float mz,
+                                                float smax) {
     const float tz = FMA(c.R[8], mz, FMA(c.R[7], my, FMA(c.R[6], mx, c.t[2])));  // the CA z-test (R27)
     if (!(tz > c.znear)) return false;
     // the bound: approximate but deterministic operations; their errors (≲ 1e-6 relative)
@@ -145,17 +163,21 @@ __device__ __forceinline__ bool ca_participates(const mvgs_camera& c, float mx, 
     const float itz = pt_rcp(tz);
     const float ux = FMUL(tx, itz), uy = FMUL(ty, itz);
     const float px = FMA(c.fx, ux, c.cx), py = FMA(c.fy, uy, c.cy);
-    const float limx = FMUL(FMUL(0.65f, __int2float_rn(c.width)), pt_rcp(c.fx));
-    const float limy = FMUL(FMUL(0.65f, __int2float_rn(c.height)), pt_rcp(c.fy));
-    const float cux = fminf(fabsf(ux), limx), cuy = fminf(fabsf(uy), limy);
-    const float jf = FMUL(FADD(FMUL(FMUL(c.fx, c.fx), FMA(cux, cux, 1.0f)), FMUL(FMUL(c.fy, c.fy), FMA(cuy, cuy, 1.0f))),
+    const float cux = fminf(fabsf(ux), pc.limx), cuy = fminf(fabsf(uy), pc.limy);
+    const float jf = FMUL(FADD(FMUL(pc.fx2, FMA(cux, cux, 1.0f)), FMUL(pc.fy2, FMA(cuy, cuy, 1.0f))),
                           FMUL(itz, itz));  // ‖J‖²_F
     const float tr = FMA(FMUL(jf, FMUL(smax, smax)), 1.001f, 0.92f);
     const float rub = FMA(3.0f, pt_sqrt(tr), 2.0f);  // > r, incl. the ceil
     if (!(rub < 1e30f)) return true;                 // overflow / NaN: keep the pair
-    if (FADD(px, rub) < 1.0f || FSUB(px, rub) > 16.0f * (float)TX) return false;
-    if (FADD(py, rub) < 1.0f || FSUB(py, rub) > 16.0f * (float)TY) return false;
+    if (FADD(px, rub) < 1.0f || FSUB(px, rub) > pc.xmax) return false;
+    if (FADD(py, rub) < 1.0f || FSUB(py, rub) > pc.ymax) return false;
     return true;
+}
+
+__device__ __forceinline__ bool ca_participates(const mvgs_camera& c, float mx, float my, float mz, float smax,
+                                                int TX, int TY) {
+    const PartCam pc = make_partcam(c, TX, TY);
+    return ca_participates(c, pc, mx, my, mz, smax);
 }
 
 // Per (Gaussian, view) projection state (§4.2).

@@ -156,6 +156,7 @@ cudaError_t scan_exclusive(int* a, int n, int* total_slot, int* tmp, cudaStream_
 __global__ __launch_bounds__(BLK) void k_count(Launch L) {
     __shared__ int wc[BLK / 32][32];
     __shared__ mvgs_camera scams[32];  // the chunk's cameras (LDS instead of per-field global loads)
+    __shared__ PartCam spc[32];        // and the bound's per-camera constants
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t g = (int64_t)blockIdx.x * BLK + threadIdx.x;
     const bool valid = g < L.P;
@@ -171,11 +172,12 @@ __global__ __launch_bounds__(BLK) void k_count(Launch L) {
         if (v0 > 0) __syncthreads();  // the previous chunk's cameras are no longer read
         for (int i = threadIdx.x; i < nv * (int)(sizeof(mvgs_camera) / 4); i += BLK)
             reinterpret_cast<uint32_t*>(scams)[i] = reinterpret_cast<const uint32_t*>(L.cams + v0)[i];
+        if (threadIdx.x < nv) spc[threadIdx.x] = make_partcam(L.cams[v0 + threadIdx.x], L.TX, L.TY);
         __syncthreads();
         unsigned pm = 0;
         for (int k = 0; k < nv; k++) {
             const mvgs_camera& c = scams[k];
-            const bool vis = valid && ca_participates(c, mx, my, mz, smax, L.TX, L.TY);
+            const bool vis = valid && ca_participates(c, spc[k], mx, my, mz, smax);
             pm |= vis ? 1u << k : 0u;
             const unsigned bal = __ballot_sync(FULL, vis);
             if (lane == 0) wc[warp][k] = __popc(bal);
