@@ -373,7 +373,10 @@ __device__ __forceinline__ void finish_gaussian(const Launch& L, const mvgs_grad
 template <int D>
 // Gaussians [gbeg, gend) only (gbeg a multiple of BLK): outputs are addressed relative to gbeg,
 // so a caller can reduce each finished chunk while the next one computes.
-__global__ __launch_bounds__(BLK, 2) void k_gauss_bwd(Launch L, mvgs_grads gr, mvgs_adc adc, int64_t gbeg,
+#ifndef MVGS_GB_MINB
+#define MVGS_GB_MINB 2  // resident 256-thread CTAs asked of k_gauss_bwd
+#endif
+__global__ __launch_bounds__(BLK, MVGS_GB_MINB) void k_gauss_bwd(Launch L, mvgs_grads gr, mvgs_adc adc, int64_t gbeg,
                                                                  int64_t gend) {
     constexpr int NS = ShRows<D>::NS, SS = ShRows<D>::STRIDE;
     constexpr int VB = GB_VB;
