@@ -19,16 +19,23 @@ constexpr unsigned FULL = 0xffffffffu;
 
 // ------------------------------------------------------------------ scan
 // Single-pass exclusive scan with decoupled look-back: one kernel per scan.  A CTA takes a
-// dynamic tile id (4096 ints), scans it, publishes its aggregate, and warp 0 looks back over
+// dynamic tile id (SCAN_T·SCAN_IPT ints), scans it, publishes its aggregate, and warp 0 looks back over
 // up to 32 predecessors at a time for the nearest inclusive prefix.  The status words and
 // the tile counter are cleared by a memset before every scan (no epochs: graph replays are
 // safe).  tmp layout (ints): [0] tile counter, [1] pad, [2 …] u64 status per tile.
-constexpr int SCAN_T = 1024, SCAN_IPT = 4, SCAN_TILE = SCAN_T * SCAN_IPT;
+#ifndef MVGS_SCAN_IPT
+#define MVGS_SCAN_IPT 16  // ints per thread (multiple of 4)
+#endif
+#ifndef MVGS_SCAN_T
+#define MVGS_SCAN_T 1024  // threads per scan CTA (≤ 1024)
+#endif
+constexpr int SCAN_T = MVGS_SCAN_T, SCAN_IPT = MVGS_SCAN_IPT, SCAN_TILE = SCAN_T * SCAN_IPT;
+static_assert(SCAN_IPT % 4 == 0, "SCAN_IPT: whole int4s");
 constexpr unsigned long long SC_AGG = 1ull << 32, SC_PRE = 2ull << 32;
 
 int scan_tmp_size(int n) { return 2 * ((n + SCAN_TILE - 1) / SCAN_TILE + 1) + 4; }
 
-__device__ __forceinline__ int block_exclusive_scan_1024(int x, int* sm /*[33]*/, int* total) {
+__device__ __forceinline__ int block_exclusive_scan(int x, int* sm /*[33]*/, int* total) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     int inc = x;
 #pragma unroll
@@ -39,7 +46,7 @@ __device__ __forceinline__ int block_exclusive_scan_1024(int x, int* sm /*[33]*/
     if (lane == 31) sm[warp] = inc;
     __syncthreads();
     if (warp == 0) {
-        int w = sm[lane];
+        int w = lane < SCAN_T / 32 ? sm[lane] : 0;
         int wi = w;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -81,15 +88,20 @@ __global__ __launch_bounds__(SCAN_T) void k_scan_1p(int* __restrict__ a, int n, 
     const int base = tile * SCAN_TILE + threadIdx.x * SCAN_IPT;
     int v[SCAN_IPT];
     if (base + SCAN_IPT <= n) {
-        const int4 q = *reinterpret_cast<const int4*>(a + base);
-        v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
+#pragma unroll
+        for (int j = 0; j < SCAN_IPT / 4; j++) {
+            const int4 q = *reinterpret_cast<const int4*>(a + base + 4 * j);
+            v[4 * j] = q.x; v[4 * j + 1] = q.y; v[4 * j + 2] = q.z; v[4 * j + 3] = q.w;
+        }
     } else {
 #pragma unroll
         for (int i = 0; i < SCAN_IPT; i++) v[i] = base + i < n ? a[base + i] : 0;
     }
-    const int sum = v[0] + v[1] + v[2] + v[3];
+    int sum = 0;
+#pragma unroll
+    for (int i = 0; i < SCAN_IPT; i++) sum += v[i];
     int tot;
-    const int ex = block_exclusive_scan_1024(sum, sm, &tot);
+    const int ex = block_exclusive_scan(sum, sm, &tot);
     if (threadIdx.x < 32) {
         const int lane = threadIdx.x;
         int excl = 0;
@@ -121,12 +133,15 @@ __global__ __launch_bounds__(SCAN_T) void k_scan_1p(int* __restrict__ a, int n, 
     __syncthreads();
     int run = s_pre + ex;
     if (base + SCAN_IPT <= n) {
-        int4 q;
-        q.x = run; run += v[0];
-        q.y = run; run += v[1];
-        q.z = run; run += v[2];
-        q.w = run;
-        *reinterpret_cast<int4*>(a + base) = q;
+#pragma unroll
+        for (int j = 0; j < SCAN_IPT / 4; j++) {
+            int4 q;
+            q.x = run; run += v[4 * j];
+            q.y = run; run += v[4 * j + 1];
+            q.z = run; run += v[4 * j + 2];
+            q.w = run; run += v[4 * j + 3];
+            *reinterpret_cast<int4*>(a + base + 4 * j) = q;
+        }
     } else {
 #pragma unroll
         for (int i = 0; i < SCAN_IPT; i++) {
