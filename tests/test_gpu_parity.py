@@ -29,6 +29,11 @@ def cases():
                             dict(bg=(0.1, 0.2, 0.3))),
         "indoor_small": (synth.make_scene(synth.scaled(synth.CONFIGS["playroom"], P=15_000, V=2, W=160, H=120)),
                          dict(bg=(0.0, 0.0, 0.0))),
+        # the SH degrees between 0 and 3 (the k_project / k_gauss_bwd instantiations D = 1, 2)
+        "sh1_small": (synth.make_scene(synth.scaled(synth.CONFIGS["garden"], P=4_000, V=2, W=100, H=70, sh_degree=1)),
+                      dict(bg=(0.3, 0.3, 0.3))),
+        "sh2_small": (synth.make_scene(synth.scaled(synth.CONFIGS["playroom"], P=4_000, V=3, W=90, H=81, sh_degree=2)),
+                      dict(bg=(0.0, 0.5, 1.0))),
     }
 
 
