@@ -145,12 +145,12 @@ def stage_models(P, NK, V, NB, Q, K, T, evf, evb, exf, exb, Qv):
 
 def launches_per_step(nbuckets, Q, K):
     """Kernels libmvgs launches per step: count + scan, project,
-    pair sort (upsweep + bases + 4 onesweep passes), pair-tiles + scan + dup,
+    pair sort (upsweep + bases + 4 onesweep passes; the last also writes the tile counts), scan + dup,
     entry sort (⌈log2(V·T)/8⌉ passes × (histogram + scan + scatter)),
     (the first pass's histogram is counted by dup), ranges close-up (segment minima + close;
     the bucket starts come out of the last entry pass), fwd, bwd, gauss_bwd."""
     ent_passes = (max(1, (nbuckets - 1).bit_length()) + 7) // 8
-    return (1 + 1) + 1 + (2 + 4) + (1 + 1 + 1) + (3 * ent_passes - 1) + 2 + 3  # scans: one kernel each
+    return (1 + 1) + 1 + (2 + 4) + (1 + 1) + (3 * ent_passes - 1) + 2 + 3  # scans: one kernel each
 
 
 # ---------------------------------------------------------------------- mvgs

@@ -326,6 +326,7 @@ template <bool PAYLOAD, int IPT>
 __global__ __launch_bounds__(RS_T) void k_rs_onesweep(const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin,
                                                       uint32_t* __restrict__ kout, uint32_t* __restrict__ vout,
                                                       const uint2* __restrict__ pin, uint2* __restrict__ pout,
+                                                      int* __restrict__ cnt_out,
                                                       const int* __restrict__ n_ptr, int64_t cap, int shift, int nbits,
                                                       int drop_inert, const uint32_t* __restrict__ gbase,
                                                       unsigned long long* __restrict__ status,
@@ -427,20 +428,27 @@ __global__ __launch_bounds__(RS_T) void k_rs_onesweep(const uint32_t* __restrict
     for (int l = threadIdx.x; l < nout; l += RS_T) {
         const uint32_t k = sk[l];
         const uint32_t dst = gdelta[(k >> shift) & mask] + l;
-        kout[dst] = k;
+        if (!PAYLOAD || !cnt_out) kout[dst] = k;
         vout[dst] = sv[l];
-        if (PAYLOAD) pout[dst] = sp[PAYLOAD ? l : 0];
+        if (PAYLOAD) {
+            const uint2 r = sp[PAYLOAD ? l : 0];
+            pout[dst] = r;
+            // last pass of the pair sort: the tiles each pair covers, in depth order, instead of
+            // the keys (nothing reads the sorted depths; S3 scans these into entry offsets)
+            if (cnt_out) cnt_out[dst] = (int)(((r.y & 0xffff) - (r.x & 0xffff)) * ((r.y >> 16) - (r.x >> 16)));
+        }
     }
 }
 
 // Stable LSD sort of (k, v[, payload])[0..*n_ptr) on bits [0, bits) with ≤ 8-bit
 // digits; with drop_inert the first pass removes keys equal to 0xffffffff and the
 // later passes run on *n_after elements; with identity_vals the first pass takes the
-// values to be the input positions (v is not read).  Returns the number of passes; the result
-// is in the first buffers when even, in the second ones when odd.
+// values to be the input positions (v is not read); with last_counts (payload sorts) the last
+// pass writes each element's rect tile count there instead of its sorted key.  Returns the
+// number of passes; the result is in the first buffers when even, in the second ones when odd.
 int radix_sort(uint32_t* k, uint32_t* v, uint32_t* k2, uint32_t* v2, uint2* pl, uint2* pl2, const int* n_ptr,
                const int* n_after, int64_t cap, int bits, bool drop_inert, bool identity_vals, const RadixScratch& rs,
-               cudaStream_t s, cudaError_t* err) {
+               cudaStream_t s, cudaError_t* err, int* last_counts) {
     const int ntiles = radix_tiles(cap);
     const int npass = (bits + 7) / 8;
     const int db = npass ? (bits + npass - 1) / npass : 0;
@@ -466,11 +474,13 @@ int radix_sort(uint32_t* k, uint32_t* v, uint32_t* k2, uint32_t* v2, uint2* pl, 
         if (pl) cudaFuncSetAttribute(k_rs_onesweep<true, OS_IPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)osm);
         else cudaFuncSetAttribute(k_rs_onesweep<false, OS_IPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)osm);
         if (pl)
-            k_rs_onesweep<true, OS_IPT><<<otiles, RS_T, osm, s>>>(ks, vin, kd, vd, ps, pd, np, cap, shift, nb,
+            k_rs_onesweep<true, OS_IPT><<<otiles, RS_T, osm, s>>>(ks, vin, kd, vd, ps, pd,
+                                                        pass == npass - 1 ? last_counts : nullptr, np, cap, shift, nb,
                                                         (drop_inert && pass == 0) ? 1 : 0, gbase + pass * RS_BINS,
                                                         rs.status, epoch, pass, tctr + pass);
         else
-            k_rs_onesweep<false, OS_IPT><<<otiles, RS_T, osm, s>>>(ks, vin, kd, vd, nullptr, nullptr, np, cap, shift, nb,
+            k_rs_onesweep<false, OS_IPT><<<otiles, RS_T, osm, s>>>(ks, vin, kd, vd, nullptr, nullptr, nullptr, np, cap,
+                                                         shift, nb,
                                                          (drop_inert && pass == 0) ? 1 : 0, gbase + pass * RS_BINS,
                                                          rs.status, epoch, pass, tctr + pass);
         if ((*err = cudaGetLastError()) != cudaSuccess) return pass;
@@ -490,16 +500,6 @@ __device__ __forceinline__ int view_of_pair(const Launch& L, uint32_t q) {
         else hi = mid - 1;
     }
     return lo;
-}
-
-// tiles covered by the i-th visible pair in depth order → scanned into entry offsets
-__global__ void k_pair_tiles(Launch L, const uint2* __restrict__ rect, int* __restrict__ ecount) {
-    const int Q = (int)min((int64_t)L.counters[C_NVIS], L.cap_pairs);  // visible pairs (compacted by the sort)
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < Q; i += stride) {
-        const uint2 r = rect[i];
-        ecount[i] = (int)(((r.y & 0xffff) - (r.x & 0xffff)) * ((r.y >> 16) - (r.x >> 16)));
-    }
 }
 
 // Duplication in depth order: pair i's entries are ebase[i] + (row-major tile index
@@ -731,7 +731,7 @@ __global__ void k_max_bucket(Launch L) {
 cudaError_t launch_sort_pairs(const Launch& L, const uint32_t** order_out, const uint2** rect_out, cudaStream_t s) {
     cudaError_t e;
     int np = radix_sort(L.pkey, L.pval, L.pkey2, L.pval2, L.prect, L.prect2, L.counters + C_Q, L.counters + C_NVIS,
-                        L.cap_pairs, 32, true, true, L.rs, s, &e);
+                        L.cap_pairs, 32, true, true, L.rs, s, &e, L.ecount);
     *order_out = (np & 1) ? L.pval2 : L.pval;
     *rect_out = (np & 1) ? L.prect2 : L.prect;
     return e;
@@ -739,7 +739,7 @@ cudaError_t launch_sort_pairs(const Launch& L, const uint32_t** order_out, const
 
 // S3: duplicate in depth order (entry offsets from a scan of the tile counts).
 cudaError_t launch_dup_sort(const Launch& L, const uint32_t* order, const uint2* rect, cudaStream_t s) {
-    k_pair_tiles<<<grid_for(L.cap_pairs, 256), 256, 0, s>>>(L, rect, L.ecount);
+    // L.ecount: the visible pairs' tile counts in depth order, written by the pair sort's last pass
     cudaError_t e = scan_exclusive(L.ecount, (int)L.cap_pairs, L.counters + C_K, L.scan_tmp, s,
                                    L.counters + C_NVIS);  // entry offsets of the visible pairs; K
     if (e != cudaSuccess) return e;
