@@ -130,7 +130,7 @@ def stage_models(P, NK, V, NB, Q, K, T, evf, evb, exf, exb, Qv):
     tiles > 0 (the rest are inert: only their depth, flags and sort key are written)."""
     pbytes = 4 * (11 + 3 * NK) * P
     return {
-        "count": ("hbm", 12 * P + 4 * V * NB),
+        "count": ("hbm", 24 * P + (4 * P if V <= 32 else 0) + 4 * V * NB),  # means + log_scales in, pmask out
         "scan_pairs": ("hbm", 3 * 4 * V * NB),
         "project": ("hbm", pbytes + 4 * V * NB + Qv * (48 + 4 + 4 + 8) + (Q - Qv) * (16 + 4 + 4)),
         "scan_buckets": ("hbm", 3 * 4 * V * T),
