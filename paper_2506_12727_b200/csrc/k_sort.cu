@@ -331,7 +331,7 @@ __global__ __launch_bounds__(RS_T) void k_rs_onesweep(const uint32_t* __restrict
                                                       int drop_inert, const uint32_t* __restrict__ gbase,
                                                       unsigned long long* __restrict__ status,
                                                       const uint32_t* __restrict__ epoch_base, int pass,
-                                                      int* __restrict__ tile_ctr) {
+                                                      int* __restrict__ tile_ctr, int gather) {
     __shared__ uint32_t hist[RS_NW][RS_BINS];
     __shared__ uint32_t gdelta[RS_BINS];  // global offset − local start, per digit
     constexpr int TILE = RS_T * IPT;
@@ -364,7 +364,7 @@ __global__ __launch_bounds__(RS_T) void k_rs_onesweep(const uint32_t* __restrict
         const bool ok = p < nt;
         key[it] = ok ? kin[t0 + p] : INERT;
         val[it] = vin ? (ok ? vin[t0 + p] : 0u) : (uint32_t)(t0 + p);  // no vin: the identity
-        if (PAYLOAD) pay[PAYLOAD ? it : 0] = ok ? pin[t0 + p] : make_uint2(0u, 0u);
+        if (PAYLOAD) pay[PAYLOAD ? it : 0] = ok ? pin[gather ? val[it] : (uint32_t)(t0 + p)] : make_uint2(0u, 0u);
     }
 #pragma unroll
     for (int it = 0; it < IPT; it++) {
@@ -446,9 +446,15 @@ __global__ __launch_bounds__(RS_T) void k_rs_onesweep(const uint32_t* __restrict
 // values to be the input positions (v is not read); with last_counts (payload sorts) the last
 // pass writes each element's rect tile count there instead of its sorted key.  Returns the
 // number of passes; the result is in the first buffers when even, in the second ones when odd.
+// Pair sort payload: carried through every pass (0), or gathered by the last pass from the
+// unsorted rects through the sorted values (1: the values are the input positions), so the
+// earlier passes move 8 B per pair instead of 16 and the rect array (8·Q, L2-resident) is read once.
+#ifndef MVGS_PAIR_GATHER
+#define MVGS_PAIR_GATHER 1
+#endif
 int radix_sort(uint32_t* k, uint32_t* v, uint32_t* k2, uint32_t* v2, uint2* pl, uint2* pl2, const int* n_ptr,
                const int* n_after, int64_t cap, int bits, bool drop_inert, bool identity_vals, const RadixScratch& rs,
-               cudaStream_t s, cudaError_t* err, int* last_counts) {
+               cudaStream_t s, cudaError_t* err, int* last_counts, bool gather_pl) {
     const int ntiles = radix_tiles(cap);
     const int npass = (bits + 7) / 8;
     const int db = npass ? (bits + npass - 1) / npass : 0;
@@ -470,19 +476,21 @@ int radix_sort(uint32_t* k, uint32_t* v, uint32_t* k2, uint32_t* v2, uint2* pl, 
         const uint32_t* vin = (pass == 0 && identity_vals) ? nullptr : vs;
         constexpr int OT = RS_T * OS_IPT;
         const int otiles = (int)((cap + OT - 1) / OT);
-        const size_t osm = (size_t)OT * ((pl ? 8 : 0) + 8);
-        if (pl) cudaFuncSetAttribute(k_rs_onesweep<true, OS_IPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)osm);
+        const bool with_pl = pl && (!gather_pl || pass == npass - 1);
+        const size_t osm = (size_t)OT * ((with_pl ? 8 : 0) + 8);
+        if (with_pl) cudaFuncSetAttribute(k_rs_onesweep<true, OS_IPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)osm);
         else cudaFuncSetAttribute(k_rs_onesweep<false, OS_IPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)osm);
-        if (pl)
-            k_rs_onesweep<true, OS_IPT><<<otiles, RS_T, osm, s>>>(ks, vin, kd, vd, ps, pd,
+        if (with_pl)
+            k_rs_onesweep<true, OS_IPT><<<otiles, RS_T, osm, s>>>(ks, vin, kd, vd, gather_pl ? pl : ps,
+                                                        gather_pl ? pl2 : pd,
                                                         pass == npass - 1 ? last_counts : nullptr, np, cap, shift, nb,
                                                         (drop_inert && pass == 0) ? 1 : 0, gbase + pass * RS_BINS,
-                                                        rs.status, epoch, pass, tctr + pass);
+                                                        rs.status, epoch, pass, tctr + pass, gather_pl ? 1 : 0);
         else
             k_rs_onesweep<false, OS_IPT><<<otiles, RS_T, osm, s>>>(ks, vin, kd, vd, nullptr, nullptr, nullptr, np, cap,
                                                          shift, nb,
                                                          (drop_inert && pass == 0) ? 1 : 0, gbase + pass * RS_BINS,
-                                                         rs.status, epoch, pass, tctr + pass);
+                                                         rs.status, epoch, pass, tctr + pass, 0);
         if ((*err = cudaGetLastError()) != cudaSuccess) return pass;
         uint32_t* t = ks; ks = kd; kd = t;
         t = vs; vs = vd; vd = t;
@@ -731,9 +739,9 @@ __global__ void k_max_bucket(Launch L) {
 cudaError_t launch_sort_pairs(const Launch& L, const uint32_t** order_out, const uint2** rect_out, cudaStream_t s) {
     cudaError_t e;
     int np = radix_sort(L.pkey, L.pval, L.pkey2, L.pval2, L.prect, L.prect2, L.counters + C_Q, L.counters + C_NVIS,
-                        L.cap_pairs, 32, true, true, L.rs, s, &e, L.ecount);
+                        L.cap_pairs, 32, true, true, L.rs, s, &e, L.ecount, MVGS_PAIR_GATHER != 0);
     *order_out = (np & 1) ? L.pval2 : L.pval;
-    *rect_out = (np & 1) ? L.prect2 : L.prect;
+    *rect_out = (MVGS_PAIR_GATHER || (np & 1)) ? L.prect2 : L.prect;
     return e;
 }
 
