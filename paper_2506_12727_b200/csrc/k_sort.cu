@@ -285,12 +285,25 @@ __global__ __launch_bounds__(256) void k_rs_upsweep(const uint32_t* __restrict__
     for (int i = threadIdx.x; i < 4 * RS_BINS; i += blockDim.x) (&h[0][0])[i] = 0;
     __syncthreads();
     const int n = (int)min((int64_t)*n_ptr, cap);
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        const uint32_t k = keys[i];
-        if (drop_inert && k == INERT) continue;
-        for (int p = 0; p < npass; p++) {
-            const int sh = p * db, nb = min(db, bits - sh);
-            atomicAdd(&h[p][(k >> sh) & ((1u << nb) - 1u)], 1u);
+    // UP_K loads in flight per thread before its atomics (one at a time left the kernel
+    // latency-bound: ≈ 8 KB in flight per SM)
+    constexpr int UP_K = 8;
+    const int stride = gridDim.x * blockDim.x;
+    for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < n; b += stride * UP_K) {
+        uint32_t kk[UP_K];
+#pragma unroll
+        for (int u = 0; u < UP_K; u++) {
+            const int i = b + u * stride;
+            kk[u] = i < n ? keys[i] : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < UP_K; u++) {
+            const uint32_t k = kk[u];
+            if (b + u * stride >= n || (drop_inert && k == INERT)) continue;
+            for (int p = 0; p < npass; p++) {
+                const int sh = p * db, nb = min(db, bits - sh);
+                atomicAdd(&h[p][(k >> sh) & ((1u << nb) - 1u)], 1u);
+            }
         }
     }
     __syncthreads();
