@@ -96,8 +96,11 @@ __global__ __launch_bounds__(RS_T) void k_rs_hist(const uint32_t* __restrict__ k
 // consecutive threads: every digit's run lands contiguously at
 // offsets[digit * ntiles + tile], so global writes are coalesced.
 // Optionally moves a 64-bit payload with each key.
+#ifndef MVGS_RS3_MINB
+#define MVGS_RS3_MINB 6  // resident CTAs asked of the three-kernel scatter (6: 40 registers, 72 B spill; 1: 60 registers)
+#endif
 template <bool PAYLOAD, int IPT>
-__global__ __launch_bounds__(RS_T) void k_rs_scatter(const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin,
+__global__ __launch_bounds__(RS_T, MVGS_RS3_MINB) void k_rs_scatter(const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin,
                                                      uint32_t* __restrict__ kout, uint32_t* __restrict__ vout,
                                                      const uint2* __restrict__ pin, uint2* __restrict__ pout,
                                                      const int* __restrict__ n_ptr, int64_t cap, int shift, int nbits,
