@@ -338,8 +338,11 @@ __device__ __forceinline__ unsigned long long ld_status(const unsigned long long
     return v;
 }
 
+#ifndef MVGS_OS_MINB
+#define MVGS_OS_MINB 1  // resident CTAs asked of the key/value onesweep passes (1: ptxas's choice)
+#endif
 template <bool PAYLOAD, int IPT>
-__global__ __launch_bounds__(RS_T) void k_rs_onesweep(const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin,
+__global__ __launch_bounds__(RS_T, PAYLOAD ? 1 : MVGS_OS_MINB) void k_rs_onesweep(const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin,
                                                       uint32_t* __restrict__ kout, uint32_t* __restrict__ vout,
                                                       const uint2* __restrict__ pin, uint2* __restrict__ pout,
                                                       int* __restrict__ cnt_out,
