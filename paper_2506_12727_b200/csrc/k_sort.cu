@@ -553,7 +553,12 @@ struct DupDesc {  // one pair of the warp's 32
 // Since a chunk is exactly one tile of the entry sort's first radix pass, the warp also counts
 // that pass's digits of the keys it writes (counts[digit·ntiles + chunk]): the pass needs no
 // histogram kernel re-reading the K keys.
-__global__ __launch_bounds__(256) void k_dup(Launch L, const uint32_t* __restrict__ order,
+#ifdef MVGS_DUP_MINB  // resident CTAs asked of k_dup (unset: ptxas's choice, 48 registers)
+#define DUP_BOUNDS __launch_bounds__(256, MVGS_DUP_MINB)
+#else
+#define DUP_BOUNDS __launch_bounds__(256)
+#endif
+__global__ DUP_BOUNDS void k_dup(Launch L, const uint32_t* __restrict__ order,
                                              const uint2* __restrict__ rect, const int* __restrict__ ebase,
                                              int* __restrict__ counts, int ntiles, uint32_t dmask) {
     __shared__ uint8_t spos[8][32];
