@@ -278,7 +278,8 @@ mvgs_status mvgs_export_lists(mvgs_ctx *ctx, int64_t *range_start, int32_t *entr
 
 /* Parity export (tests): per pair q < Q —
  *   pair_ids [Q,2] int32   (view, gid)
- *   pair_i   [Q,8] int32   (radius, rx0, ry0, rx1, ry1, tiles, clamp bits, 0)
+ *   pair_i   [Q,8] int32   (radius, rx0, ry0, rx1, ry1, tiles, clamp bits, 0); the radius
+ *                          is recomputed by the export (the path keeps only the rect)
  *   pair_f   [Q,12] fp32   (depth, px, py, A, B, C, opacity, r, g, b, 0, 0)
  *   pair_g   [Q,10] fp32   (Σ∇x, Σ∇y, e1, ∂A, ∂B, ∂C, ∂o, ∂r, ∂g, ∂b) after render_bwd
  * Any pointer may be NULL. */

@@ -51,7 +51,7 @@ _lib = None
 def lib():
     global _lib
     if _lib is None:
-        L = C.CDLL(build())
+        L = C.CDLL(build() if LIB == os.path.join(HERE, "liboracle.so") else LIB)
         vp, i64 = C.c_void_p, C.c_int64
         L.oracle_create.restype = vp
         L.oracle_create.argtypes = [C.POINTER(_Scene), vp, C.c_int, vp, C.c_int]
@@ -74,6 +74,32 @@ def lib():
         L.oracle_adc_example.argtypes = [C.c_int, vp, vp, vp, vp]
         _lib = L
     return _lib
+
+
+def use_library(path: str | None = None):
+    """Load the oracle from another build of oracle.c (mutation tests), or back from the
+    default build with path=None."""
+    global _lib
+    _lib = None
+    if path is not None:
+        global LIB
+        saved = LIB
+        LIB = path
+        try:
+            lib()
+        finally:
+            LIB = saved
+    return lib()
+
+
+def build_variant(src_text: str, out: str) -> str:
+    """Compile a modified copy of oracle.c (mutation tests) with the oracle's flags."""
+    import tempfile
+    with tempfile.NamedTemporaryFile("w", suffix=".c", delete=False) as f:
+        f.write(src_text)
+    subprocess.check_call(["gcc", *CFLAGS, f.name, "-o", out, "-lm"])
+    os.unlink(f.name)
+    return out
 
 
 def _p(a):
@@ -175,12 +201,12 @@ class Oracle:
 
     def pairs(self):
         n = self.V * self.P
-        ints = np.zeros((self.V, self.P, 8), np.int32)
+        ints = np.zeros((self.V, self.P, 9), np.int32)
         flts = np.zeros((self.V, self.P, 6), np.float32)
         rgb = np.zeros((self.V, self.P, 3))
         if n:
             lib().oracle_get_pairs(self._h, _p(ints), _p(flts), _p(rgb))
-        names = ["zvis", "vis", "radius", "rx0", "ry0", "rx1", "ry1", "tiles"]
+        names = ["zvis", "vis", "radius", "rx0", "ry0", "rx1", "ry1", "tiles", "clamp"]
         out = {k: ints[..., j] for j, k in enumerate(names)}
         out.update({k: flts[..., j] for j, k in enumerate(["depth", "px", "py", "A", "B", "C"])})
         out["rgb"] = rgb

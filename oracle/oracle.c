@@ -193,6 +193,46 @@ static void project32(const float mu[3], const float Sig[6], const og_cam *c, p3
     p->vis = p->tiles > 0;
 }
 
+/* O2 colour in fp32 (decision only: the SH clamp rgb < 0, R17, §4.4).
+ * dir = (μ − c_v)/‖μ − c_v‖ with c_v = −R_vᵀ t_v; real SH basis in [3DGS] order,
+ * each Y_k one fixed sequence of fp32 products/differences; acc = 0.5 then
+ * acc = fma(Y_k, sh_k, acc) for k ascending.  clamped[ch] = acc < 0.            */
+static void color32(const og_scene *g, int64_t i, const og_cam *c, int clamped[3])
+{
+    const float *R = c->R, *mu = g->means + 3 * i;
+    float cp[3];
+    for (int k = 0; k < 3; k++) cp[k] = -fmaf(R[6 + k], c->t[2], fmaf(R[3 + k], c->t[1], R[k] * c->t[0]));
+    float dx = mu[0] - cp[0], dy = mu[1] - cp[1], dz = mu[2] - cp[2];
+    float n2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+    float inv = 1.0f / sqrtf(n2);
+    float x = dx * inv, y = dy * inv, z = dz * inv;
+    float xx = x * x, yy = y * y, zz = z * z;
+    float Y[16];
+    Y[0] = 0.28209479177387814f;
+    Y[1] = -0.4886025119029199f * y;
+    Y[2] = 0.4886025119029199f * z;
+    Y[3] = -0.4886025119029199f * x;
+    Y[4] = (1.0925484305920792f * x) * y;
+    Y[5] = (-1.0925484305920792f * y) * z;
+    Y[6] = 0.31539156525252005f * ((2.0f * zz - xx) - yy);
+    Y[7] = (-1.0925484305920792f * x) * z;
+    Y[8] = 0.5462742152960396f * (xx - yy);
+    Y[9] = (-0.5900435899266435f * y) * (3.0f * xx - yy);
+    Y[10] = ((2.890611442640554f * x) * y) * z;
+    Y[11] = (-0.4570457994644658f * y) * ((4.0f * zz - xx) - yy);
+    Y[12] = (0.3731763325901154f * z) * ((2.0f * zz - 3.0f * xx) - 3.0f * yy);
+    Y[13] = (-0.4570457994644658f * x) * ((4.0f * zz - xx) - yy);
+    Y[14] = (1.445305721320277f * z) * (xx - yy);
+    Y[15] = (-0.5900435899266435f * x) * (xx - 3.0f * yy);
+    int nk = (g->sh_degree + 1) * (g->sh_degree + 1);
+    const float *sh = g->sh + (size_t)i * g->sh_stride * 3;
+    for (int ch = 0; ch < 3; ch++) {
+        float acc = 0.5f;
+        for (int k = 0; k < nk; k++) acc = fmaf(Y[k], sh[3 * k + ch], acc);
+        clamped[ch] = acc < 0.0f;
+    }
+}
+
 /* ============================================================= fp64 chain */
 static const double SH_C0 = 0.28209479177387814;
 static const double SH_C1 = 0.4886025119029199;
@@ -326,11 +366,11 @@ static void project64(const og_scene *g, int64_t i, const g64_t *a, const og_cam
     sh_basis(p->dir, Y, dY);
     int nk = (g->sh_degree + 1) * (g->sh_degree + 1);
     const float *sh = g->sh + (size_t)i * g->sh_stride * 3;
+    color32(g, i, cam, p->rgb_clamped); /* the clamp is a decision: fp32 CA (R17) */
     for (int ch = 0; ch < 3; ch++) {
         double v = 0.5;
         for (int k = 0; k < nk; k++) v += Y[k] * sh[3 * k + ch];
-        p->rgb_clamped[ch] = v < 0.0;
-        p->rgb[ch] = v < 0.0 ? 0.0 : v;
+        p->rgb[ch] = p->rgb_clamped[ch] ? 0.0 : v;
     }
 }
 
@@ -893,8 +933,9 @@ void oracle_get_lists(const oracle_t *h, int64_t *off, int32_t *gid)
     if (gid) memcpy(gid, h->gid, sizeof(int32_t) * h->K);
 }
 
-/* per (view, gid) decision-chain state: ints [V*P*8] = zvis vis radius rx0 ry0
- * rx1 ry1 tiles; floats [V*P*6] = depth px py A B C (fp32, bit-exact
+/* per (view, gid) decision-chain state: ints [V*P*9] = zvis vis radius rx0 ry0
+ * rx1 ry1 tiles clamp (bits 0-2 SH colour clamp per channel, 3-4 Jacobian clamp
+ * x/y; visible pairs only); floats [V*P*6] = depth px py A B C (fp32, bit-exact
  * targets); rgb [V*P*3] fp64. */
 void oracle_get_pairs(const oracle_t *h, int32_t *ints, float *flts, double *rgb)
 {
@@ -902,9 +943,13 @@ void oracle_get_pairs(const oracle_t *h, int32_t *ints, float *flts, double *rgb
     for (size_t k = 0; k < n; k++) {
         const p32_t *p = &h->p32[k];
         if (ints) {
-            int32_t *o = ints + 8 * k;
+            int32_t *o = ints + 9 * k;
             o[0] = p->zvis; o[1] = p->vis; o[2] = p->radius; o[3] = p->rx0;
-            o[4] = p->ry0; o[5] = p->rx1; o[6] = p->ry1; o[7] = p->tiles;
+            o[4] = p->ry0; o[5] = p->rx1; o[6] = p->ry1; o[7] = p->tiles; o[8] = 0;
+            if (p->vis && h->p64i[k] >= 0) {
+                const p64_t *q = &h->p64[h->p64i[k]];
+                o[8] = q->rgb_clamped[0] | q->rgb_clamped[1] << 1 | q->rgb_clamped[2] << 2 | q->clx << 3 | q->cly << 4;
+            }
         }
         if (flts) {
             float *f = flts + 6 * k;

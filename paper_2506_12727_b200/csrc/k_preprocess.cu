@@ -233,27 +233,29 @@ constexpr float c_SH3_6 = -0.5900435899266435f;
 // Real SH basis (R17), degree D, direction (x,y,z) unit.
 template <int D>
 __device__ __forceinline__ void sh_eval_basis(float x, float y, float z, float* Y) {
+    // canonical arithmetic: every product / difference one RN operation in
+    // a fixed order, so the clamp decision on Σ Y_k sh_k + 0.5 is the oracle's (color32)
     Y[0] = 0.28209479177387814f;
     if (D >= 1) {
-        Y[1] = -c_SH1 * y;
-        Y[2] = c_SH1 * z;
-        Y[3] = -c_SH1 * x;
+        Y[1] = FMUL(-c_SH1, y);
+        Y[2] = FMUL(c_SH1, z);
+        Y[3] = FMUL(-c_SH1, x);
     }
     if (D >= 2) {
-        const float xx = x * x, yy = y * y, zz = z * z;
-        Y[4] = c_SH2_0 * x * y;
-        Y[5] = c_SH2_1 * y * z;
-        Y[6] = c_SH2_2 * (2.f * zz - xx - yy);
-        Y[7] = c_SH2_3 * x * z;
-        Y[8] = c_SH2_4 * (xx - yy);
+        const float xx = FMUL(x, x), yy = FMUL(y, y), zz = FMUL(z, z);
+        Y[4] = FMUL(FMUL(c_SH2_0, x), y);
+        Y[5] = FMUL(FMUL(c_SH2_1, y), z);
+        Y[6] = FMUL(c_SH2_2, FSUB(FSUB(FMUL(2.f, zz), xx), yy));
+        Y[7] = FMUL(FMUL(c_SH2_3, x), z);
+        Y[8] = FMUL(c_SH2_4, FSUB(xx, yy));
         if (D >= 3) {
-            Y[9] = c_SH3_0 * y * (3.f * xx - yy);
-            Y[10] = c_SH3_1 * x * y * z;
-            Y[11] = c_SH3_2 * y * (4.f * zz - xx - yy);
-            Y[12] = c_SH3_3 * z * (2.f * zz - 3.f * xx - 3.f * yy);
-            Y[13] = c_SH3_4 * x * (4.f * zz - xx - yy);
-            Y[14] = c_SH3_5 * z * (xx - yy);
-            Y[15] = c_SH3_6 * x * (xx - 3.f * yy);
+            Y[9] = FMUL(FMUL(c_SH3_0, y), FSUB(FMUL(3.f, xx), yy));
+            Y[10] = FMUL(FMUL(FMUL(c_SH3_1, x), y), z);
+            Y[11] = FMUL(FMUL(c_SH3_2, y), FSUB(FSUB(FMUL(4.f, zz), xx), yy));
+            Y[12] = FMUL(FMUL(c_SH3_3, z), FSUB(FSUB(FMUL(2.f, zz), FMUL(3.f, xx)), FMUL(3.f, yy)));
+            Y[13] = FMUL(FMUL(c_SH3_4, x), FSUB(FSUB(FMUL(4.f, zz), xx), yy));
+            Y[14] = FMUL(FMUL(c_SH3_5, z), FSUB(xx, yy));
+            Y[15] = FMUL(FMUL(c_SH3_6, x), FSUB(xx, FMUL(3.f, yy)));
         }
     }
 }
@@ -345,13 +347,13 @@ __global__ __launch_bounds__(BLK) void k_project(Launch L) {
                 L.rec[3 * pair + 2] = make_float4(0.f, p.tz, 0.f, 0.f);
                 L.pflag[pair] = (p.clx ? 8u : 0u) | (p.cly ? 16u : 0u);
             } else {
-                // colour (R17), free arithmetic
-                const float cpx = -(c.R[0] * c.t[0] + c.R[3] * c.t[1] + c.R[6] * c.t[2]);
-                const float cpy = -(c.R[1] * c.t[0] + c.R[4] * c.t[1] + c.R[7] * c.t[2]);
-                const float cpz = -(c.R[2] * c.t[0] + c.R[5] * c.t[1] + c.R[8] * c.t[2]);
-                float dx = mx - cpx, dy = my - cpy, dz = mz - cpz;
-                const float inv = rsqrtf(dx * dx + dy * dy + dz * dz);
-                dx *= inv; dy *= inv; dz *= inv;
+                // colour (R17) in canonical arithmetic: its clamp (rgb < 0) is a decision (§4.4)
+                const float cpx = -ca_dot3(c.R[0], c.R[3], c.R[6], c.t[0], c.t[1], c.t[2]);
+                const float cpy = -ca_dot3(c.R[1], c.R[4], c.R[7], c.t[0], c.t[1], c.t[2]);
+                const float cpz = -ca_dot3(c.R[2], c.R[5], c.R[8], c.t[0], c.t[1], c.t[2]);
+                float dx = FSUB(mx, cpx), dy = FSUB(my, cpy), dz = FSUB(mz, cpz);
+                const float inv = FDIV(1.0f, FSQRT(FMA(dz, dz, FMA(dy, dy, FMUL(dx, dx)))));
+                dx = FMUL(dx, inv); dy = FMUL(dy, inv); dz = FMUL(dz, inv);
                 float Y[NK];
                 sh_eval_basis<D>(dx, dy, dz, Y);
                 float rgb[3];
@@ -366,7 +368,7 @@ __global__ __launch_bounds__(BLK) void k_project(Launch L) {
 #pragma unroll
                         for (int e = 0; e < 4; e++) {
                             const int f = 4 * i4 + e;
-                            if (f < NS) accs[f % 3] += Y[f / 3] * qe[e];
+                            if (f < NS) accs[f % 3] = FMA(Y[f / 3], qe[e], accs[f % 3]);
                         }
                     }
                 }
@@ -481,7 +483,7 @@ __global__ void k_export(Launch L, int64_t* range_start, int32_t* entry_gid, int
     for (int64_t q = t0; q < Q; q += stride) {
         int view = 0;
         int64_t gid = 0;
-        if (pair_ids) slot_ids(L, q, view, gid);
+        if (pair_ids || pair_i) slot_ids(L, q, view, gid);
         const float4 r0 = L.rec[3 * q], r1 = L.rec[3 * q + 1], r2 = L.rec[3 * q + 2];
         const uint32_t lo = __float_as_uint(r2.z), hi = __float_as_uint(r2.w);
         if (pair_ids) {
@@ -491,7 +493,16 @@ __global__ void k_export(Launch L, int64_t* range_start, int32_t* entry_gid, int
         if (pair_i) {
             const int rx0 = lo & 0xffff, ry0 = lo >> 16, rx1 = hi & 0xffff, ry1 = hi >> 16;
             int32_t* o = pair_i + 8 * q;
-            o[0] = 0;  // radius is not kept by the path; tests compare the rect
+            int radius = 0;  // not kept by the path: recomputed here through the same CA projection
+            if (gid >= 0) {
+                Activ a;
+                ca_activate(L.log_scales + 3 * gid, L.quats + 4 * gid, L.opac[gid], a);
+                Proj p;
+                ca_project(L.cams[view], L.means[3 * gid], L.means[3 * gid + 1], L.means[3 * gid + 2], a.Sig, L.TX,
+                           L.TY, p);
+                radius = p.radius;
+            }
+            o[0] = radius;
             o[1] = rx0; o[2] = ry0; o[3] = rx1; o[4] = ry1;
             o[5] = (rx1 - rx0) * (ry1 - ry0);
             o[6] = (int32_t)(L.pflag[q] & 0x1fu);

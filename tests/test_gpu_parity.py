@@ -71,13 +71,15 @@ def _gpu_pairs_in_oracle(o, gpu):
 
 def test_staged_pairs_bit_exact(case):
     """S1/S2: pair slots = participating (view, gid) in view-major, gid-ascending
-    order; rect, tiles, depth, μ', conic, opacity bit-exact (CA, §4)."""
+    order; radius, rect, tiles, depth, μ', conic, opacity and the SH clamp bits
+    bit-exact (CA, §4); rgb within 2e-6 (fp32 CA value vs the oracle's fp64 value)."""
     o, gpu = case["o"], case["gpu"]
     p, zv, zg = _gpu_pairs_in_oracle(o, gpu)
     assert gpu["stats"]["Q"] <= int(p["zvis"].sum())
     vis = p["vis"][zv, zg].astype(bool)
     pi, pf = gpu["pair_i"], gpu["pair_f"]
     np.testing.assert_array_equal(pi[:, 5], np.where(vis, p["tiles"][zv, zg], 0))
+    np.testing.assert_array_equal(pi[vis, 0], p["radius"][zv, zg][vis], err_msg="radius")
     for j, k in enumerate(["rx0", "ry0", "rx1", "ry1"], start=1):
         np.testing.assert_array_equal(pi[vis, j], p[k][zv, zg][vis], err_msg=k)
     np.testing.assert_array_equal(pf[:, 0].view(np.uint32), p["depth"][zv, zg].view(np.uint32))
@@ -85,6 +87,7 @@ def test_staged_pairs_bit_exact(case):
         np.testing.assert_array_equal(pf[vis, j].view(np.uint32), p[k][zv, zg][vis].view(np.uint32), err_msg=k)
     np.testing.assert_array_equal(pf[vis, 6].view(np.uint32), p["opacity"][zg[vis]].view(np.uint32))
     np.testing.assert_allclose(pf[vis, 7:10], p["rgb"][zv, zg][vis], rtol=2e-6, atol=2e-6)
+    np.testing.assert_array_equal(pi[vis, 6], p["clamp"][zv, zg][vis], err_msg="SH / Jacobian clamp bits")
 
 
 def test_lists_bit_exact(case):

@@ -464,3 +464,175 @@ def test_predicted_depth_single_gaussian():
     o2 = oracle.Oracle(g2, cam_identity(W=33, H=33, f=40.0))
     o2.forward()
     assert abs(o2.depth()[0, 16, 16] - (2.0 * 0.5 + 3.0 * 0.9 * 0.5)) < 1e-6
+
+
+# ---------------------------------------------- O1 general rotation, O2 off-axis EWA
+def _rodrigues(axis, theta):
+    """Rotation by θ about the unit axis n (Rodrigues): R = I + sinθ K + (1 − cosθ) K²,
+    K the cross-product matrix of n — built without any quaternion formula."""
+    n = np.asarray(axis, float) / np.linalg.norm(axis)
+    K = np.array([[0, -n[2], n[1]], [n[2], 0, -n[0]], [-n[1], n[0], 0]])
+    return np.eye(3) + math.sin(theta) * K + (1 - math.cos(theta)) * K @ K
+
+
+def _quat_axis_angle(axis, theta):
+    n = np.asarray(axis, float) / np.linalg.norm(axis)
+    return np.concatenate([[math.cos(theta / 2)], math.sin(theta / 2) * n])
+
+
+def _conic_to_cov(p, v=0, i=0):
+    A, B, C = (float(p[k][v, i]) for k in ("A", "B", "C"))
+    return np.linalg.inv(np.array([[A, B], [B, C]]))
+
+
+ROT_CASES = [((1, 0, 0), math.radians(37)), ((0, 1, 0), math.radians(-61)), ((1, 2, -0.5), math.radians(113)),
+             ((0.3, -1, 0.8), math.radians(-152))]
+
+
+@pytest.mark.parametrize("axis,theta", ROT_CASES)
+def test_P1b_rotation_matches_rodrigues_through_three_cameras(axis, theta):
+    """O1 R(q) for general axes and angles: Σ = R S² Rᵀ with R from Rodrigues'
+    axis–angle formula.  Three on-axis cameras looking along world z, x and y each see the
+    2×2 block (f/z)²·(R_c Σ R_cᵀ)[:2,:2] + 0.3·I as the inverse conic (P3's EWA with ũ = 0),
+    so together they fix all six entries of Σ.  A transposed R(q), or a sign error in an
+    off-diagonal entry, changes Σ for every generic rotation here."""
+    s = np.array([0.08, 0.03, 0.05])
+    z, f, W = 2.0, 400.0, 64
+    g = scene([0, 0, 0], log_scales=np.log(s), quats=_quat_axis_angle(axis, theta))
+    Rs = [np.eye(3), np.array([[0, 1, 0], [0, 0, 1], [1, 0, 0]]), np.array([[0, 0, 1], [1, 0, 0], [0, 1, 0]])]
+    cams = synth.cams_array([synth.make_camera(Rc, [0, 0, z], W, W, f) for Rc in Rs])
+    o = oracle.Oracle(g, cams)
+    p = o.pairs()
+    s32 = np.exp(np.log(s).astype(np.float32).astype(np.float64))
+    Rr = _rodrigues(axis, theta)
+    Sig = Rr @ np.diag(s32 ** 2) @ Rr.T
+    for v, Rc in enumerate(Rs):
+        got = (_conic_to_cov(p, v) - 0.3 * np.eye(2)) / (f / z) ** 2
+        ref = (Rc @ Sig @ Rc.T)[:2, :2]
+        np.testing.assert_allclose(got, ref, rtol=0, atol=2e-5 * np.abs(ref).max(), err_msg=f"camera {v}")
+    # the fp64 value chain (activate64/project64): the rendered α of the single Gaussian is
+    # o·exp(−½ dᵀ Σ'⁻¹ d) with Σ' from the same independent Σ (camera 0, bg = 0, rgb = 1)
+    g["sh"] = np.full((1, 1, 3), 0.5 / C0, np.float32)
+    o = oracle.Oracle(g, cams[:1])
+    im = o.forward()
+    Sp = (f / z) ** 2 * Sig[:2, :2] + 0.3 * np.eye(2)
+    Si = np.linalg.inv(Sp)
+    c = (W - 1) / 2
+    for (x, y) in [(31, 31), (28, 35), (36, 30), (33, 25)]:
+        d = np.array([c - x, c - y])
+        alpha = 0.5 * math.exp(-0.5 * d @ Si @ d)
+        assert im["n_contrib"][0, y, x] == 1
+        rgb1 = float(np.float32(0.5 / C0)) * C0 + 0.5
+        assert abs(im["rgb"][0, 0, y, x] - rgb1 * alpha) <= 1e-7 * alpha, (x, y)  # fp32 inputs
+
+
+def _pinhole(t, f, c):
+    return np.array([f * t[0] / t[2] + c, f * t[1] / t[2] + c])
+
+
+def _offaxis_case():
+    s = np.array([0.012, 0.006, 0.04])  # elongated in its local z
+    q = _quat_axis_angle((0.4, -0.7, 0.5), math.radians(71))
+    Rc = _rodrigues((0.2, 1.0, -0.3), math.radians(24))  # generic camera rotation (W ≠ I)
+    t_cam = np.array([0.7, -0.5, 2.0])  # off-axis: ux = 0.35, uy = −0.25 (inside the clamp)
+    tv = np.array([0.1, 0.2, -0.3])
+    mu = Rc.T @ (t_cam - tv)  # x_c = R μ + t  ⇒  μ = Rᵀ (x_c − t)
+    return s, q, Rc, tv, mu
+
+
+def test_P2b_offaxis_ewa_matches_pinhole_linearisation():
+    """O2 off-axis EWA: Σ' = J W Σ Wᵀ Jᵀ + 0.3·I where J is the
+    Jacobian of the pinhole map (x, y, z) ↦ (f x/z + c, f y/z + c) at the camera-space mean.
+    Here J is taken by central finite differences of that map in fp64 (no formula shared
+    with the oracle), W is the camera rotation and Σ comes from Rodrigues — off-axis
+    (ux = 0.35, uy = −0.25) and with a depth-elongated Σ, so the J02/J12 column matters:
+    flipping its sign moves Σ' by O(1)."""
+    s, q, Rc, tv, mu = _offaxis_case()
+    f, W = 50.0, 64
+    c = (W - 1) / 2
+    g = scene(mu, log_scales=np.log(s), quats=q)
+    cam = synth.cams_array([synth.make_camera(Rc, tv, W, W, f)])
+    p = oracle.Oracle(g, cam).pairs()
+    t = Rc.astype(np.float32).astype(np.float64) @ mu.astype(np.float32).astype(np.float64) \
+        + tv.astype(np.float32).astype(np.float64)
+    h = 1e-6
+    J = np.column_stack([(_pinhole(t + h * e, f, c) - _pinhole(t - h * e, f, c)) / (2 * h) for e in np.eye(3)])
+    s32 = np.exp(np.log(s).astype(np.float32).astype(np.float64))
+    Rr = _rodrigues((0.4, -0.7, 0.5), math.radians(71))
+    Sig = Rr @ np.diag(s32 ** 2) @ Rr.T
+    Wc = Rc.astype(np.float32).astype(np.float64)
+    Sp = J @ Wc @ Sig @ Wc.T @ J.T + 0.3 * np.eye(2)
+    got = _conic_to_cov(p)
+    np.testing.assert_allclose(got, Sp, rtol=0, atol=3e-5 * np.abs(Sp).max())
+    np.testing.assert_allclose([p["px"][0, 0], p["py"][0, 0]], _pinhole(t, f, c), rtol=0, atol=2e-4)
+    # the fp64 value chain (project64): α of the rendered Gaussian at pixels near μ' is
+    # o·exp(−½ dᵀ Σ'⁻¹ d), d = μ' − p, with the same independent Σ' and μ' = π(t)
+    g["sh"] = np.full((1, 1, 3), 0.5 / C0, np.float32)
+    im = oracle.Oracle(g, cam).forward()
+    mp = _pinhole(t, f, c)
+    Si = np.linalg.inv(Sp)
+    rgb1 = float(np.float32(0.5 / C0)) * C0 + 0.5
+    for (x, y) in [(int(mp[0]), int(mp[1])), (int(mp[0]) + 1, int(mp[1]) - 1), (int(mp[0]) - 1, int(mp[1]))]:
+        d = mp - [x, y]
+        alpha = 0.5 * math.exp(-0.5 * d @ Si @ d)
+        assert im["n_contrib"][0, y, x] == 1
+        assert abs(im["rgb"][0, 0, y, x] - rgb1 * alpha) <= 1e-6 * alpha, (x, y)
+    # J's third column really contributes here (the pin is not blind to its sign)
+    Jf = J.copy()
+    Jf[:, 2] *= -1
+    Spf = Jf @ Wc @ Sig @ Wc.T @ Jf.T + 0.3 * np.eye(2)
+    assert np.abs(Spf - Sp).max() > 0.2 * np.abs(Sp - 0.3 * np.eye(2)).max()
+
+
+def test_P2c_offaxis_ewa_monte_carlo():
+    """The same off-axis projection checked against samples: points drawn from a small
+    anisotropic Gaussian N(μ, Σ) (Σ from Rodrigues) are pushed through the exact pinhole
+    map; their empirical 2-D covariance approaches J W Σ Wᵀ Jᵀ = Σ' − 0.3·I (the EWA
+    first-order model) — within Monte-Carlo error plus the O(s/z) linearisation bias."""
+    s, q, Rc, tv, mu = _offaxis_case()
+    s = s / 4  # small footprint: linearisation bias ~ (s/z)²
+    f, W = 50.0, 64
+    c = (W - 1) / 2
+    g = scene(mu, log_scales=np.log(s), quats=q)
+    cam = synth.cams_array([synth.make_camera(Rc, tv, W, W, f)])
+    p = oracle.Oracle(g, cam).pairs()
+    got = _conic_to_cov(p) - 0.3 * np.eye(2)
+    rng = np.random.default_rng(2506)
+    n = 4_000_000
+    Rr = _rodrigues((0.4, -0.7, 0.5), math.radians(71))
+    s32 = np.exp(np.log(s).astype(np.float32).astype(np.float64))
+    X = mu + (rng.standard_normal((n, 3)) * s32) @ Rr.T
+    tc = X @ Rc.T + tv
+    uv = np.column_stack([f * tc[:, 0] / tc[:, 2] + c, f * tc[:, 1] / tc[:, 2] + c])
+    emp = np.cov(uv.T)
+    np.testing.assert_allclose(got, emp, rtol=0, atol=5e-3 * np.abs(emp).max())
+
+
+def test_P17b_sh_clamp_decision_is_the_sign_of_the_colour():
+    """The SH clamp (rgb < 0 → 0, masked gradient; R17) is a decision, taken in fp32 CA
+    (DESIGN.md §4.4): for random degree-3 coefficients and view directions its bits equal
+    the sign of Σ_k Y_k(dir)·sh_k + 0.5 computed with the textbook basis in fp64, wherever
+    that value is not within rounding of 0 (|v| > 1e-5)."""
+    rng = np.random.default_rng(17)
+    n = 600
+    means = rng.uniform(-1, 1, (n, 3))
+    sh = rng.normal(0, 0.5, (n, 16, 3)).astype(np.float32)
+    sh[:, 0, :] = rng.normal(-0.9, 0.6, (n, 3))  # many colours near and below 0
+    g = scene(means, log_scales=np.full((n, 3), -4.0), sh=sh, sh_degree=3)
+    cams = [synth.look_at(np.array(e), [0, 0, 0], 64, 64, 50.0) for e in ([4, 1, 2], [-3, 3, 1], [0.5, -4, 3])]
+    o = oracle.Oracle(g, synth.cams_array(cams))
+    p = o.pairs()
+    seen = 0
+    for v, cam in enumerate(cams):
+        Rv = np.array(cam["R"], np.float64).reshape(3, 3)
+        cpos = -Rv.T @ np.array(cam["t"], np.float64)
+        for i in np.nonzero(p["vis"][v])[0]:
+            d = means[i].astype(np.float32).astype(np.float64) - cpos
+            d /= np.linalg.norm(d)
+            Y = np.array([_Y_textbook(k, d) for k in range(16)])
+            val = Y @ sh[i].astype(np.float64) + 0.5
+            ok = np.abs(val) > 1e-5
+            bits = (p["clamp"][v, i] >> np.arange(3)) & 1
+            np.testing.assert_array_equal(bits[ok], (val < 0)[ok].astype(int), err_msg=f"view {v} gid {i}")
+            seen += int(np.sum(val < 0))
+    assert seen > 100  # the clamp is exercised
