@@ -286,6 +286,13 @@ mvgs_status mvgs_export_lists(mvgs_ctx *ctx, int64_t *range_start, int32_t *entr
 mvgs_status mvgs_export_pairs(mvgs_ctx *ctx, int32_t *pair_ids, int32_t *pair_i, float *pair_f, float *pair_g,
                               void *stream);
 
+/* Parity export (tests): while nblend is non-NULL, every following mvgs_render_bwd also
+ * writes nblend[V,H,W] (int32, caller-owned device buffer sized for that call) = the number of
+ * list entries the backward treated as blended at each pixel (its re-taken α ≥ 1/255 decisions
+ * up to n_contrib); it must equal the forward's count of blended entries.  NULL switches it
+ * off (the default).  MVGS_ERR_INVALID for a NULL ctx. */
+mvgs_status mvgs_set_debug_blend_counts(mvgs_ctx *ctx, int32_t *nblend);
+
 /* NEXT-1: partial rendering (Alg. 3).  Each (view, tile)
  * renders only the S pixels listed in `pix` — the index array A of Alg. 3 —
  * so a V-view batch can render one image's worth of pixels.

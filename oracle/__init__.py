@@ -64,6 +64,7 @@ def lib():
         L.oracle_num_entries.argtypes = [vp]
         L.oracle_phase_times.argtypes = [vp, vp]
         L.oracle_get_depth.argtypes = [vp, vp]
+        L.oracle_get_nblend.argtypes = [vp, vp]
         L.oracle_decision_hash.restype = C.c_uint64
         L.oracle_decision_hash.argtypes = [vp]
         for name, n in [("oracle_get_image", 3), ("oracle_get_lists", 2), ("oracle_get_pairs", 3),
@@ -186,6 +187,12 @@ class Oracle:
         nc = np.zeros((self.V, self.H, self.W), np.int32)
         lib().oracle_get_image(self._h, _p(rgb), _p(Tf), _p(nc))
         return dict(rgb=rgb, T_final=Tf, n_contrib=nc)
+
+    def nblend(self):
+        """Blended entries per pixel [V,H,W] of the last forward."""
+        n = np.zeros((self.V, self.H, self.W), np.int32)
+        lib().oracle_get_nblend(self._h, _p(n))
+        return n
 
     def depth(self):
         """Predicted depth Σ dᵢαᵢTᵢ [V,H,W] of the last forward (fp64)."""

@@ -62,14 +62,15 @@ enum { OG_NO_EARLY_TERMINATION = 1 };
  * DESIGN.md §4.  Every line below is one correctly rounded IEEE fp32 op or an
  * explicit fmaf; nothing is contracted (-ffp-contract=off).                  */
 
-/* CA exp: range reduction by n = rint(x·log2 e), two-step
- * Cody–Waite with ln2 = hi + lo, degree-6 Taylor/Horner, scale by 2^n built
- * from exponent bits. */
+/* CA exp: range reduction by n = the integer nearest (ties to
+ * even) to the EXACT product x·log2e — one fused rounding onto the integer grid,
+ * fma(x, log2e, 1.5·2^23) − 1.5·2^23 — then two-step Cody–Waite with
+ * ln2 = hi + lo, degree-6 Taylor/Horner, scale by 2^n built from exponent bits. */
 float oracle_ca_exp(float x)
 {
     if (x < -87.0f) return 0.0f;
     if (x > 88.0f) return INFINITY;
-    float n = rintf(x * 1.44269504f);
+    float n = fmaf(x, 1.44269504f, 12582912.0f) - 12582912.0f;
     float r = fmaf(n, -0.693145751953125f, x);
     r = fmaf(n, -1.428606765330187e-6f, r);
     float p = (float)(1.0 / 720.0);
@@ -442,6 +443,7 @@ typedef struct {
     double *img, *Tfin;    /* [V,3,H,W], [V,H,W]                             */
     double *dep;           /* [V,H,W] alpha-weighted expected depth (NEXT-2)  */
     int32_t *ncon;         /* [V,H,W]                                        */
+    int32_t *nbl;          /* [V,H,W] number of blended entries per pixel    */
     /* backward */
     double *pg;            /* [V*P*NG]                                       */
     int have_bwd;
@@ -473,7 +475,7 @@ void oracle_destroy(oracle_t *h)
     if (!h) return;
     free(h->p32); free(h->o32); free(h->g64); free(h->p64); free(h->p64i); free(h->off); free(h->gid);
     free(h->mask);
-    free(h->img); free(h->Tfin); free(h->ncon); free(h->pg); free(h->dep);
+    free(h->img); free(h->Tfin); free(h->ncon); free(h->nbl); free(h->pg); free(h->dep);
     free(h->d_means); free(h->d_ls); free(h->d_q); free(h->d_op); free(h->d_sh);
     free(h->e1); free(h->e2); free(h->eold); free(h->vis);
     free(h);
@@ -672,6 +674,7 @@ static void composite(oracle_t *h, const float *dLdC)
                 h->Tfin[(size_t)v * H * W + pix] = T64;
                 h->dep[(size_t)v * H * W + pix] = Dd;
                 h->ncon[(size_t)v * H * W + pix] = last;
+                h->nbl[(size_t)v * H * W + pix] = m;
                 if (!dLdC) continue;
                 /* ---- O6: adjoint of Eq. (1) for this pixel, from its definition:
                  * C = Σ_k c_k α_k T_k + T_fin·bg, T_k = Π_{j<k}(1−α_j).
@@ -863,10 +866,11 @@ static void gauss_backward(oracle_t *h)
 int oracle_forward(oracle_t *h)
 {
     size_t npx = (size_t)h->V * h->W * h->H;
-    free(h->img); free(h->Tfin); free(h->ncon);
+    free(h->img); free(h->Tfin); free(h->ncon); free(h->nbl);
     h->img = (double *)calloc(3 * npx, sizeof(double));
     h->Tfin = (double *)calloc(npx, sizeof(double));
     h->ncon = (int32_t *)calloc(npx, sizeof(int32_t));
+    h->nbl = (int32_t *)calloc(npx, sizeof(int32_t));
     free(h->dep);
     h->dep = (double *)calloc(npx, sizeof(double));
     composite(h, NULL);
@@ -878,10 +882,11 @@ int oracle_backward(oracle_t *h, const float *dLdC)
 {
     const int64_t P = h->g.P;
     size_t npx = (size_t)h->V * h->W * h->H;
-    free(h->img); free(h->Tfin); free(h->ncon); free(h->pg);
+    free(h->img); free(h->Tfin); free(h->ncon); free(h->nbl); free(h->pg);
     h->img = (double *)calloc(3 * npx, sizeof(double));
     h->Tfin = (double *)calloc(npx, sizeof(double));
     h->ncon = (int32_t *)calloc(npx, sizeof(int32_t));
+    h->nbl = (int32_t *)calloc(npx, sizeof(int32_t));
     h->pg = (double *)calloc((size_t)h->npg * NG + 1, sizeof(double));
     free(h->dep);
     h->dep = (double *)calloc(npx, sizeof(double));
@@ -920,6 +925,12 @@ void oracle_get_image(const oracle_t *h, double *rgb, double *Tfin, int32_t *nco
     if (rgb) memcpy(rgb, h->img, 3 * npx * sizeof(double));
     if (Tfin) memcpy(Tfin, h->Tfin, npx * sizeof(double));
     if (ncon) memcpy(ncon, h->ncon, npx * sizeof(int32_t));
+}
+
+/* blended entries per pixel [V,H,W] of the last forward (α ≥ 1/255, before termination) */
+void oracle_get_nblend(const oracle_t *h, int32_t *nbl)
+{
+    memcpy(nbl, h->nbl, sizeof(int32_t) * (size_t)h->V * h->W * h->H);
 }
 
 void oracle_get_depth(const oracle_t *h, double *dep)

@@ -25,8 +25,10 @@ constexpr float T_EPS = 1e-4f;              // R13
 // §4.3 canonical exp, core for x ∈ [−87, 88] (no range checks).  The compositing
 // kernels only evaluate it for power ∈ [−ln(255)−1e-3, 0] (skip bound, §4.5), where it
 // is bit-identical to ca_exp.
+// n = the integer nearest (ties to even) to the exact x·log2e: fma onto the 1.5·2²³ grid.
+constexpr float CA_MAGIC = 12582912.0f;  // 1.5·2²³
 __device__ __forceinline__ float ca_exp_core(float x) {
-    float n = rintf(FMUL(x, 1.44269504f));
+    float n = FSUB(FMA(x, 1.44269504f, CA_MAGIC), CA_MAGIC);
     float r = FMA(n, -0.693145751953125f, x);
     r = FMA(n, -1.428606765330187e-6f, r);
     float p = (float)(1.0 / 720.0);
@@ -43,7 +45,7 @@ __device__ __forceinline__ float ca_exp_core(float x) {
 __device__ __forceinline__ float ca_exp(float x) {
     if (x < -87.0f) return 0.0f;
     if (x > 88.0f) return __int_as_float(0x7f800000);
-    float n = rintf(FMUL(x, 1.44269504f));
+    float n = FSUB(FMA(x, 1.44269504f, CA_MAGIC), CA_MAGIC);
     float r = FMA(n, -0.693145751953125f, x);
     r = FMA(n, -1.428606765330187e-6f, r);
     float p = (float)(1.0 / 720.0);

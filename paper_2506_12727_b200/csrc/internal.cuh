@@ -50,6 +50,7 @@ struct Launch {  // everything a kernel needs about the current batch
     const uint32_t* sorted;  // [K] pair index of every entry in (view, tile, depth, gid) order
     int* counters;    // [C_NCOUNTERS]
     unsigned long long* counters64;  // [8]: fwd/bwd evaluations, fwd/bwd exps, entries needed
+    int32_t* dbg_nblend;  // parity export: per-pixel blended-entry count taken by the backward (or null)
 };
 
 #ifdef __CUDACC__
@@ -99,9 +100,6 @@ struct mvgs_ctx {
     int64_t cap_dssim_coef = 0;
     double* d_dssim_part = nullptr;  // per-block SSIM sums
     int64_t cap_dssim_part = 0;
-    unsigned long long* d_ent64 = nullptr;  // [cap_entries] bucket-sort keys (depth << 32 | pair)
-    int* d_bcur = nullptr;                  // [V*T] bucket cursors
-    int64_t cap_bcur = 0;
     uint32_t* d_pmask = nullptr;            // [P] participation bits (V ≤ 32)
     int64_t cap_pmask = 0;
     double* d_lab_part = nullptr;           // NEXT-4 per-CTA fp64 partials
@@ -113,8 +111,6 @@ struct mvgs_ctx {
     int64_t cap_adc_tmp = 0;
     unsigned long long* d_adc_rep = nullptr;  // [4] split, clone, pruned, total
     long long* h_adc_rep = nullptr;           // pinned mirror
-    mvgs_camera* h_cams = nullptr;  // pinned staging
-    cudaEvent_t cams_ev = nullptr;
     cudaStream_t last_stream = nullptr;
     bool timing = false;
     bool count_evals = true;
@@ -149,16 +145,6 @@ cudaError_t launch_adc_remap(const float* src, float* dst, int64_t width, const 
 cudaError_t launch_dssim3d(const mvgs_camera* h_cams, int V, int H, int W, const float* img, const float* tgt,
                            const float* depth, const float* Tf, float sigma_px, float* loss, float* grad, float* coef,
                            double* partial, cudaStream_t s);
-#ifndef MVGS_SORT_BUCKET
-// 1: S3–S5 as count / scatter / per-bucket bitonic sort (k_bucket.cu) — exact, but measured
-// 2.9 ms vs 1.26 ms for the pair sort + dup + entry sort path at garden scale (scattered 8-B
-// writes, log² shared-memory traffic); kept as an experiment, off by default.
-#define MVGS_SORT_BUCKET 0
-#endif
-cudaError_t launch_bucket_count(const Launch& L, int* gcnt, cudaStream_t s);
-cudaError_t launch_bucket_scatter(const Launch& L, int* gcur, unsigned long long* ent, cudaStream_t s);
-cudaError_t launch_bucket_sort(const Launch& L, unsigned long long* ent, uint32_t* sorted, cudaStream_t s);
-cudaError_t launch_max_bucket(const Launch& L, cudaStream_t s);
 int lab_partials();
 cudaError_t launch_loss_grad(const float* rgb, const float* tgt, int64_t n, int mode, float scale, float* dL,
                              double* loss, double* part, cudaStream_t s);
@@ -175,4 +161,5 @@ cudaError_t launch_gauss_bwd(const Launch& L, const mvgs_grads& gr, const mvgs_a
 cudaError_t launch_export(const Launch& L, int64_t* range_start, int32_t* entry_gid, int32_t* pair_ids,
                           int32_t* pair_i, float* pair_f, float* pair_g, cudaStream_t s);
 int scan_tmp_size(int n);
+cudaError_t launch_set_cams(const mvgs_camera* h_cams, int V, mvgs_camera* d_cams, cudaStream_t s);
 }  // namespace mvgs

@@ -10,6 +10,7 @@
 //                     per-Gaussian work (activations, Σ, SH load) is done once for
 //                     the whole batch; writes the pair-sort keys (depth, rect)
 //   (duplication, sorting and the per-(view, tile) ranges: k_sort.cu)
+#include <cstring>
 #include "ca.cuh"
 #include "internal.cuh"
 
@@ -381,12 +382,13 @@ __global__ __launch_bounds__(BLK) void k_project(Launch L) {
                     }
                     rgb[ch] = acc;
                 }
-                const uint32_t lo = (uint32_t)p.rx0 | ((uint32_t)p.ry0 << 16);
-                const uint32_t hi = (uint32_t)p.rx1 | ((uint32_t)p.ry1 << 16);
+                // per-pair constants of the compositing kernels: the exact skip bound of §4.5
+                // (−ln(255·o) − 10⁻³, any accurate logf) and 1/o (o·∂L/∂o → ∂L/∂o)
+                const float sb = -logf(255.0f * a.o) - 1e-3f;
                 float4* r = L.rec + 3 * pair;
                 r[0] = make_float4(p.px, p.py, p.A, p.B);
                 r[1] = make_float4(p.C, a.o, rgb[0], rgb[1]);
-                r[2] = make_float4(rgb[2], p.tz, __uint_as_float(lo), __uint_as_float(hi));
+                r[2] = make_float4(rgb[2], p.tz, sb, 1.0f / a.o);
                 L.pflag[pair] = flags | PF_VISIBLE;  // (its gradient slot is cleared by the forward)
             }
             my_vis += (tiles > 0 && pair < L.cap_pairs) ? 1u : 0u;
@@ -439,6 +441,32 @@ cudaError_t launch_project(const Launch& L, cudaStream_t s) {
     }
 }
 
+// ------------------------------------------------------------------ cameras
+// Up to 32 cameras travel as a kernel parameter (2.4 KB) and are stored to the context's
+// device array: graph-capturable with the values baked into the node, no host staging.
+struct CamBlock {
+    mvgs_camera c[32];
+};
+__global__ void k_set_cams(CamBlock b, int n, mvgs_camera* __restrict__ dst) {
+    const int words = n * (int)(sizeof(mvgs_camera) / 4);
+    const uint32_t* src = reinterpret_cast<const uint32_t*>(b.c);
+    uint32_t* d = reinterpret_cast<uint32_t*>(dst);
+    for (int i = threadIdx.x; i < words; i += blockDim.x) d[i] = src[i];
+}
+
+cudaError_t launch_set_cams(const mvgs_camera* h_cams, int V, mvgs_camera* d_cams, cudaStream_t s) {
+    static_assert(sizeof(mvgs_camera) % 4 == 0, "camera is word-sized");
+    for (int v0 = 0; v0 < V; v0 += 32) {
+        CamBlock b;
+        const int n = V - v0 < 32 ? V - v0 : 32;
+        memcpy(b.c, h_cams + v0, sizeof(mvgs_camera) * n);
+        k_set_cams<<<1, 256, 0, s>>>(b, n, d_cams + v0);
+        const cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+}
+
 // ------------------------------------------------------------------ export (tests)
 // (view, gid) of pair slot q, recomputed from the slot allocation (no per-pair ids are
 // stored by the path): the view and 256-Gaussian block by binary search over the scanned
@@ -485,7 +513,11 @@ __global__ void k_export(Launch L, int64_t* range_start, int32_t* entry_gid, int
         int64_t gid = 0;
         if (pair_ids || pair_i) slot_ids(L, q, view, gid);
         const float4 r0 = L.rec[3 * q], r1 = L.rec[3 * q + 1], r2 = L.rec[3 * q + 2];
-        const uint32_t lo = __float_as_uint(r2.z), hi = __float_as_uint(r2.w);
+        // the rect of a visible pair: its slot in the unsorted rect array (the pair sort gathers
+        // from it, MVGS_PAIR_GATHER, and leaves it intact); inert pairs have an empty rect
+        const bool inert = !(L.pflag[q] & PF_VISIBLE);  // tiles == 0: only depth and ids were written (R27)
+        const uint2 rr = inert ? make_uint2(0u, 0u) : L.prect[q];
+        const uint32_t lo = rr.x, hi = rr.y;
         if (pair_ids) {
             pair_ids[2 * q] = (int32_t)view;
             pair_ids[2 * q + 1] = (int32_t)gid;
@@ -508,7 +540,6 @@ __global__ void k_export(Launch L, int64_t* range_start, int32_t* entry_gid, int
             o[6] = (int32_t)(L.pflag[q] & 0x1fu);
             o[7] = 0;
         }
-        const bool inert = lo == hi;  // tiles == 0: only depth and ids were written (R27)
         if (pair_f) {
             float* f = pair_f + 12 * q;
             f[0] = r2.y;

@@ -27,15 +27,6 @@ namespace mvgs {
 #ifndef MVGS_FWD_UNROLL
 #define MVGS_FWD_UNROLL 1  // inner entry loops (experiment knobs)
 #endif
-#ifndef MVGS_BWD_UNROLL
-#define MVGS_BWD_UNROLL 1
-#endif
-#ifndef MVGS_BWD_RED4
-#define MVGS_BWD_RED4 0  // 1: backward flush with 16-byte vector reductions (measured: no gain)
-#endif
-#ifndef MVGS_BWD_PREFETCH
-#define MVGS_BWD_PREFETCH 0  // 1: backward batch-ahead index load + L2 prefetch (measured: no gain)
-#endif
 #ifndef MVGS_FWD_PREFETCH
 #define MVGS_FWD_PREFETCH 1  // forward: next batch's indices a batch ahead, records prefetched to L2
 #endif
@@ -45,7 +36,7 @@ namespace mvgs {
 #ifndef MVGS_BWD_MINB
 #define MVGS_BWD_MINB 6  // resident CTAs per SM asked of the packed backward (register cap 65536/(128·MINB))
 #endif
-constexpr int kFwdUnroll = MVGS_FWD_UNROLL, kBwdUnroll = MVGS_BWD_UNROLL;
+constexpr int kFwdUnroll = MVGS_FWD_UNROLL;
 constexpr int RT = 128;            // threads per CTA = entries per staged batch
 constexpr unsigned FULLR = 0xffffffffu;
 
@@ -145,97 +136,6 @@ __device__ __forceinline__ int warp_batch_list(const uint8_t* smask, int cnt, in
     return n;
 }
 
-// stage one record: (x, y, A, B) (C, o, skip bound, -) (r, g, b, depth)
-__device__ __forceinline__ void stage(const Launch& L, uint32_t q, float4* s0, float4* s1, float4* s2, int i) {
-    const float4* r = L.rec + 3 * (int64_t)q;
-    const float4 r0 = r[0], r1 = r[1], r2 = r[2];
-    s0[i] = r0;
-    s1[i] = make_float4(r1.x, r1.y, skip_power(r1.y), 0.f);
-    s2[i] = make_float4(r1.z, r1.w, r2.x, r2.y);
-}
-
-// DEPTH: also accumulate the alpha-weighted expected depth Σ dᵢ αᵢ Tᵢ (NEXT-2)
-template <bool DEPTH>
-__global__ __launch_bounds__(RT) void k_render_fwd(Launch L, float* __restrict__ out_rgb, float* __restrict__ out_T,
-                                                   int32_t* __restrict__ out_n, float* __restrict__ out_D) {
-    __shared__ float4 s0[RT], s1[RT], s2[RT];
-    __shared__ unsigned sev[2];
-    zero_pgrad_slice(L);
-    const int bucket = blockIdx.x;
-    const int v = bucket / L.T, tile = bucket - v * L.T;
-    const int ty = tile / L.TX, tx = tile - ty * L.TX;
-    int x, y[2];
-    pixel_pair(tx, ty, x, y[0], y[1]);
-    const int start = L.bucket_off[bucket], end = L.bucket_off[bucket + 1];
-    const float fx = (float)x;
-    float fy[2], T[2], C0[2], C1[2], C2[2], D[2];
-    int last[2];
-    bool done[2];
-#pragma unroll
-    for (int p = 0; p < 2; p++) {
-        fy[p] = (float)y[p];
-        T[p] = 1.0f;
-        C0[p] = C1[p] = C2[p] = D[p] = 0.f;
-        last[p] = 0;
-        done[p] = !(x < L.W && y[p] < L.H);
-    }
-    unsigned nev = 0, nexp = 0;
-    if (threadIdx.x == 0) sev[0] = sev[1] = 0;
-    __syncthreads();
-    if (end <= L.cap_entries) {
-        for (int b0 = start; b0 < end; b0 += RT) {
-            if (__syncthreads_count(done[0] && done[1]) == RT) break;
-            const int idx = b0 + threadIdx.x;
-            if (idx < end) stage(L, L.sorted[idx], s0, s1, s2, threadIdx.x);
-            __syncthreads();
-            const int cnt = min(RT, end - b0);
-            for (int j = 0; j < cnt && !(done[0] && done[1]); j++) {
-                const float4 a = s0[j];
-                const float4 c = s1[j];
-                const float dx = FSUB(a.x, fx);
-#pragma unroll
-                for (int p = 0; p < 2; p++) {
-                    if (done[p]) continue;
-                    nev++;
-                    const float dy = FSUB(a.y, fy[p]);
-                    const float power = ca_power(a.z, a.w, c.x, dx, dy);
-                    if (power > 0.0f || power < c.z) continue;
-                    nexp++;
-                    const float G = ca_exp_core(power);
-                    const float alpha = fminf(ALPHA_MAX, FMUL(c.y, G));
-                    if (alpha < ALPHA_MIN) continue;
-                    const float Tn = FMUL(T[p], FSUB(1.0f, alpha));
-                    if (Tn < T_EPS) {
-                        done[p] = true;
-                        continue;
-                    }
-                    const float w = alpha * T[p];
-                    const float4 col = s2[j];
-                    C0[p] += col.x * w;
-                    C1[p] += col.y * w;
-                    C2[p] += col.z * w;
-                    if (DEPTH) D[p] += col.w * w;
-                    T[p] = Tn;
-                    last[p] = b0 - start + j + 1;
-                }
-            }
-        }
-    }
-    count_evals(&L.counters64[0], &L.counters64[2], nev, nexp, sev);
-    const int64_t HW = (int64_t)L.H * L.W;
-#pragma unroll
-    for (int p = 0; p < 2; p++) {
-        if (!(x < L.W && y[p] < L.H)) continue;
-        const int64_t pix = (int64_t)y[p] * L.W + x;
-        out_rgb[(3 * (int64_t)v + 0) * HW + pix] = C0[p] + T[p] * L.bg[0];
-        out_rgb[(3 * (int64_t)v + 1) * HW + pix] = C1[p] + T[p] * L.bg[1];
-        out_rgb[(3 * (int64_t)v + 2) * HW + pix] = C2[p] + T[p] * L.bg[2];
-        out_T[v * HW + pix] = T[p];
-        out_n[v * HW + pix] = last[p];
-        if (DEPTH) out_D[v * HW + pix] = D[p];
-    }
-}
-
 // ---------------------------------------------------------------------------------------
 // Packed forward (default): the thread's two pixels are the lanes of FP32x2 registers; every
 // CA operation (power, canonical exp, α, T·(1 − α)) is the per-lane RN operation of the
@@ -252,10 +152,14 @@ struct FwdConsts {
 
 __device__ __forceinline__ float2 ff2(float a, float b) { return make_float2(a, b); }
 
-// ca_exp_core per lane, packed (same RN / FMA sequence)
+// ca_exp_core per lane, packed, for x ∈ [−87, 0] as the compositing kernels
+// use it (x ≥ the skip bound > −5.6).  Bit-identical to ca_exp_core: m = fma(x, log2e, 1.5·2²³)
+// puts the integer nearest to the exact x·log2e in m's low mantissa bits (two's complement,
+// |n| < 2²²), n = m − 1.5·2²³ exactly, and p·2ⁿ — exact, p ∈ [2^-½, 2^½], n ≥ −126 — is formed by
+// adding n to p's exponent field: (bits(m) << 23) + bits(p), one LEA per lane.
 __device__ __forceinline__ float2 ca_exp_core2(float2 x) {
-    const float2 t = __fmul2_rn(x, ff2(1.44269504f, 1.44269504f));
-    const float2 n = ff2(rintf(t.x), rintf(t.y));
+    const float2 m = __ffma2_rn(x, ff2(1.44269504f, 1.44269504f), ff2(CA_MAGIC, CA_MAGIC));
+    const float2 n = __fadd2_rn(m, ff2(-CA_MAGIC, -CA_MAGIC));
     float2 r = __ffma2_rn(n, ff2(-0.693145751953125f, -0.693145751953125f), x);
     r = __ffma2_rn(n, ff2(-1.428606765330187e-6f, -1.428606765330187e-6f), r);
     const float c6 = (float)(1.0 / 720.0), c5 = (float)(1.0 / 120.0), c4 = (float)(1.0 / 24.0),
@@ -266,9 +170,8 @@ __device__ __forceinline__ float2 ca_exp_core2(float2 x) {
     p = __ffma2_rn(p, r, ff2(0.5f, 0.5f));
     p = __ffma2_rn(p, r, ff2(1.f, 1.f));
     p = __ffma2_rn(p, r, ff2(1.f, 1.f));
-    const float2 sc = ff2(__int_as_float((__float2int_rn(n.x) + 127) << 23),
-                          __int_as_float((__float2int_rn(n.y) + 127) << 23));
-    return __fmul2_rn(p, sc);
+    return ff2(__int_as_float((__float_as_int(m.x) << 23) + __float_as_int(p.x)),
+               __int_as_float((__float_as_int(m.y) << 23) + __float_as_int(p.y)));
 }
 
 template <bool DEPTH, bool CNT>
@@ -390,23 +293,13 @@ __global__ __launch_bounds__(RT) void k_render_fwd_p(Launch L, float* __restrict
     }
 }
 
-#ifndef MVGS_FWD_PACKED
-#define MVGS_FWD_PACKED 1
-#endif
-
 cudaError_t launch_render_fwd(const Launch& L, float* rgb, float* Tf, int32_t* nc, float* depth, cudaStream_t s) {
-    if (MVGS_FWD_PACKED) {
-        if (depth)
-            k_render_fwd_p<true, true><<<L.V * L.T, RT, 0, s>>>(L, rgb, Tf, nc, depth);
-        else if (L.count_evals)
-            k_render_fwd_p<false, true><<<L.V * L.T, RT, 0, s>>>(L, rgb, Tf, nc, nullptr);
-        else
-            k_render_fwd_p<false, false><<<L.V * L.T, RT, 0, s>>>(L, rgb, Tf, nc, nullptr);
-    } else if (depth) {
-        k_render_fwd<true><<<L.V * L.T, RT, 0, s>>>(L, rgb, Tf, nc, depth);
-    } else {
-        k_render_fwd<false><<<L.V * L.T, RT, 0, s>>>(L, rgb, Tf, nc, nullptr);
-    }
+    if (depth)
+        k_render_fwd_p<true, true><<<L.V * L.T, RT, 0, s>>>(L, rgb, Tf, nc, depth);
+    else if (L.count_evals)
+        k_render_fwd_p<false, true><<<L.V * L.T, RT, 0, s>>>(L, rgb, Tf, nc, nullptr);
+    else
+        k_render_fwd_p<false, false><<<L.V * L.T, RT, 0, s>>>(L, rgb, Tf, nc, nullptr);
     return cudaGetLastError();
 }
 
@@ -441,204 +334,36 @@ __device__ __forceinline__ int reduce_id(int lane) {
     return b2 ? x1 : x0;
 }
 
-// per-pixel backward state
-struct BwdPix {
-    float dL0, dL1, dL2, T_fin, T, dL_bg;
-    float acc0, acc1, acc2, a_prev, c0p, c1p, c2p;
-    int last;
-};
-
-// NPX pixels per thread: a CTA of 256/NPX threads covers the 16×16 tile; warp w
-// covers rows (32·NPX/16)·w …, lane l column l & 15, rows r, r+2, r+4, …
-template <int NPX>
-__global__ __launch_bounds__(256 / NPX) void k_render_bwd(Launch L, const float* __restrict__ dL_drgb,
-                                                          const float* __restrict__ in_T,
-                                                          const int32_t* __restrict__ in_n) {
-    constexpr int NT = 256 / NPX;         // threads
-    constexpr int NW = NT / 32;           // warps
-    constexpr int RB = 128;               // entries per staged batch
-    constexpr int ROWS = 2 * NPX;         // rows per warp
-    __shared__ float4 s0[RB], s1[RB], s2[RB];
-    __shared__ uint32_t sq[RB];
-    __shared__ __align__(16) float sacc[NW][RB * NG];  // per-warp partial sums, no atomics
-    __shared__ int smax;
-    __shared__ unsigned sev[2];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int bucket = blockIdx.x;
-    const int v = bucket / L.T, tile = bucket - v * L.T;
-    const int ty = tile / L.TX, tx = tile - ty * L.TX;
-    const int x = tx * TILE + (lane & 15);
-    const int y0 = ty * TILE + ROWS * warp + (lane >> 4);
-    const int start = L.bucket_off[bucket], end = L.bucket_off[bucket + 1];
-    if (end > L.cap_entries) return;
-    const int64_t HW = (int64_t)L.H * L.W;
-    BwdPix px[NPX];
-    int mylast = 0;
-    unsigned nev = 0;
-#pragma unroll
-    for (int p = 0; p < NPX; p++) {
-        BwdPix& s = px[p];
-        const int y = y0 + 2 * p;
-        s.dL0 = s.dL1 = s.dL2 = 0.f;
-        s.T_fin = 1.f;
-        s.last = 0;
-        if (x < L.W && y < L.H) {
-            const int64_t pix = (int64_t)y * L.W + x;
-            s.dL0 = dL_drgb[(3 * (int64_t)v + 0) * HW + pix];
-            s.dL1 = dL_drgb[(3 * (int64_t)v + 1) * HW + pix];
-            s.dL2 = dL_drgb[(3 * (int64_t)v + 2) * HW + pix];
-            s.T_fin = in_T[v * HW + pix];
-            s.last = in_n[v * HW + pix];
-        }
-        s.T = s.T_fin;
-        s.dL_bg = L.bg[0] * s.dL0 + L.bg[1] * s.dL1 + L.bg[2] * s.dL2;
-        s.acc0 = s.acc1 = s.acc2 = 0.f;  // colour behind the current entry
-        s.a_prev = s.c0p = s.c1p = s.c2p = 0.f;
-        mylast = max(mylast, s.last);
-        nev += (unsigned)s.last;  // entries this pixel walks back over
-    }
-    if (threadIdx.x == 0) {
-        smax = 0;
-        sev[0] = sev[1] = 0;
-    }
-    __syncthreads();
-    unsigned nexp = 0;
-    if (mylast > 0) atomicMax(&smax, mylast);
-    __syncthreads();
-    const int maxlast = smax;
-    const int wmax = __reduce_max_sync(FULLR, mylast);  // entries beyond it are skipped warp-uniformly
-    const int my_id = reduce_id(lane);
-    const bool owner = (__ffs(__match_any_sync(FULLR, my_id)) - 1) == lane;
-    float* wacc = sacc[warp];
-    const float fx = (float)x;
-    const float fy0 = (float)y0;
-    const float hw = 0.5f * (float)L.W, hh = 0.5f * (float)L.H;
-    for (int b_end = maxlast; b_end > 0; b_end -= RB) {
-        const int b0 = max(0, b_end - RB);
-        const int cnt = b_end - b0;
-        __syncthreads();
-        for (int t = threadIdx.x; t < cnt; t += NT) {
-            const uint32_t q = L.sorted[start + b0 + t];
-            sq[t] = q;
-            stage(L, q, s0, s1, s2, t);
-        }
-        {  // each warp clears its own slots
-            float4* w4 = reinterpret_cast<float4*>(wacc);
-            for (int i = lane; i < RB * NG / 4; i += 32) w4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-        }
-        __syncthreads();
-        for (int jj = min(cnt, wmax - b0) - 1; jj >= 0; jj--) {
-            const int j = b0 + jj;
-            const float4 a = s0[jj];
-            const float4 c = s1[jj];
-            const float dx = FSUB(a.x, fx);
-            float val[NG];
-#pragma unroll
-            for (int k = 0; k < NG; k++) val[k] = 0.f;
-            bool contrib = false;
-#pragma unroll
-            for (int p = 0; p < NPX; p++) {
-                BwdPix& s = px[p];
-                if (j >= s.last) continue;
-                const float dy = FSUB(a.y, fy0 + (float)(2 * p));
-                const float power = ca_power(a.z, a.w, c.x, dx, dy);
-                if (power > 0.0f || power < c.z) continue;
-                nexp++;
-                // Decisions (α ≥ 1/255, α clamp) must be the forward's: take them from the
-                // hardware exp unless o·G is within 1e-5 (relative) of a threshold, where the
-                // canonical exp decides.  Values use the hardware exp.
-                float G = exp2f(power * 1.4426950408889634f);
-                float oG = c.y * G;
-                if (fabsf(oG - ALPHA_MIN) < 1e-5f * ALPHA_MIN || fabsf(oG - ALPHA_MAX) < 1e-5f * ALPHA_MAX) {
-                    G = ca_exp_core(power);
-                    oG = FMUL(c.y, G);
-                }
-                const float alpha = fminf(ALPHA_MAX, oG);
-                if (alpha < ALPHA_MIN) continue;
-                contrib = true;
-                const float inv_one_m = __fdividef(1.0f, 1.0f - alpha);
-                s.T = s.T * inv_one_m;
-                const float w = alpha * s.T;
-                const float4 col = s2[jj];
-                s.acc0 = s.a_prev * s.c0p + (1.f - s.a_prev) * s.acc0;
-                s.acc1 = s.a_prev * s.c1p + (1.f - s.a_prev) * s.acc1;
-                s.acc2 = s.a_prev * s.c2p + (1.f - s.a_prev) * s.acc2;
-                float dLda = (col.x - s.acc0) * s.dL0 + (col.y - s.acc1) * s.dL1 + (col.z - s.acc2) * s.dL2;
-                dLda = dLda * s.T - s.T_fin * inv_one_m * s.dL_bg;
-                s.a_prev = alpha;
-                s.c0p = col.x; s.c1p = col.y; s.c2p = col.z;
-                const bool clamped = oG > ALPHA_MAX;
-                const float dLdG = clamped ? 0.f : c.y * dLda;
-                const float dLdo = clamped ? 0.f : G * dLda;
-                const float dLdpw = G * dLdG;
-                const float gx = dLdpw * -(a.z * dx + a.w * dy) * hw;
-                const float gy = dLdpw * -(c.x * dy + a.w * dx) * hh;
-                val[0] += gx;
-                val[1] += gy;
-                const float n2 = gx * gx + gy * gy;
-                val[2] += n2 > 0.f ? n2 * rsqrtf(n2) : 0.f;
-                val[3] += -0.5f * dLdpw * dx * dx;
-                val[4] += -dLdpw * dx * dy;
-                val[5] += -0.5f * dLdpw * dy * dy;
-                val[6] += dLdo;
-                val[7] += w * s.dL0;
-                val[8] += w * s.dL1;
-                val[9] += w * s.dL2;
-            }
-            if (__any_sync(FULLR, contrib)) {
-                const float sum = warp_transpose_reduce10(val, lane);
-                if (owner) wacc[jj * NG + my_id] = sum;
-            }
-        }
-        __syncthreads();
-        for (int i = threadIdx.x; i < cnt * NG; i += NT) {
-            float s = 0.f;
-#pragma unroll
-            for (int w = 0; w < NW; w++) s += sacc[w][i];
-            if (s != 0.f) {
-                const int jj = i / NG, k = i - jj * NG;
-                atomicAdd(&L.pgrad[(int64_t)sq[jj] * PG_STRIDE + k], s);
-            }
-        }
-    }
-    count_evals(&L.counters64[1], &L.counters64[3], nev, nexp, sev);
-}
-
 // ---------------------------------------------------------------------------------------
-// Packed backward (default).  Same mapping as k_render_bwd<2> (128 threads, pixels at rows r
-// and r+2 of the thread's column), but the two pixels of a thread are the two lanes of FP32x2
-// registers: every per-pixel operation is one FFMA2/FMUL2/FADD2 for both pixels.  The body is
-// branch-free per pixel — a pixel that does not blend the entry (beyond its n_contrib, skip
-// bound, α < 1/255) gets α = 0 and a zero gradient weight, which leaves T and the colour
-// behind it unchanged exactly (÷(1 − 0), 0·c + 1·acc) — and only warp-uniform tests branch.
-// Decisions are the same as the scalar kernel's: the CA power with per-lane RN operations
-// (bit-identical to ca_power), the hardware exp with the CA fallback band.
-// The colour behind the current entry is updated eagerly after the entry (the same
-// expression the lazy form evaluates one entry later), so no previous-entry state is kept.
+// Backward (S7).  128 threads per (view, tile), two pixels per thread held as the lanes of
+// FP32x2 registers (rows r and r+2 of the thread's column; warp w owns rows 4w … 4w+3), the
+// tile's list walked back to front from each pixel's n_contrib in staged batches, each warp
+// over its compacted list of entries that can touch its 16×4 block (§4.8).
+//
+// Decisions are the forward's, re-taken in the same canonical arithmetic: the CA power, the
+// CA exp (ca_exp_core2, bit-identical to the forward's), α = min(0.99, o·G), skip α < 1/255,
+// clamp o·G > 0.99 — so the set of blended (pixel, entry) pairs is exactly the forward's, and
+// the gradient values use that same G (values are free, §4.4).  A pixel that does not blend
+// the entry gets α = 0 and zero gradient weights, which leaves its state unchanged exactly.
+//
+// State per pixel: T (transmittance in front of the current entry, rebuilt by T/(1 − α)) and
+// B̃ = −(T_final·(bg·∂L/∂C) + Σ_{k behind} (c_k·∂L/∂C)·α_k·T_k), so that
+//     ∂L/∂α_j = T_j·(c_j·∂L/∂C) + B̃/(1 − α_j)
+// (the adjoint of Eq. (1): every later term and the background carry (1 − α_j)), and
+// after the entry B̃ −= (c_j·∂L/∂C)·α_j·T_j.  Per (pixel, entry) the ten per-pair terms are
+// Σ∇x, Σ∇y (∇_{p_i}L in NDC, R2), ‖∇_{p_i}L‖ (E1, "norm and add"), ∂A, ∂B, ∂C, o·∂L/∂o,
+// ∂r, ∂g, ∂b; the thread adds its two pixels', the warp transpose-reduces them (12 shuffles),
+// the owner lane scales and stores its value in the warp's slot, and after the batch the four
+// warp slots are summed in fixed order and flushed with one red.add per nonzero value.
 struct BwdConsts {
     float4 xy;   // (x, x, y, y)
-    float4 ab;   // (A, A, B, B)
-    float4 cnb;  // (C, C, −B, −B)
-    float4 os;   // (o, o, skip bound, skip bound)
+    float4 ac;   // (A, A, C, C)
+    float4 bo;   // (B, B, o, o)
     float4 rg;   // (r, r, g, g)
-    float2 bb;   // (b, b)
+    float4 bs;   // (b, b, skip bound, −)
 };
 
 __device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
-// 16-byte vector reduction into global memory (sm_90+): the four floats are added atomically
-// element-wise; the address must be 16-byte aligned (pair gradient slots are 48 B).
-__device__ __forceinline__ void red_add_v4(float* p, float a, float b, float c, float d) {
-    asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(d)
-                 : "memory");
-}
-__device__ __forceinline__ void st_shared_f32(uint32_t addr, float v) {
-    asm volatile("st.shared.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
-}
-__device__ __forceinline__ float ex2_approx(float x) {
-    float y;
-    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-    return y;
-}
 __device__ __forceinline__ float sqrt_approx(float x) {
     float y;
     asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -649,23 +374,15 @@ __device__ __forceinline__ float rcp_approx(float x) {
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
 }
-// G and o·G of one lane: hardware exp, CA exp when o·G is within 1e-5 (relative) of a threshold
-__device__ __forceinline__ void bwd_exp(float power, float o, float& G, float& oG) {
-    G = ex2_approx(power * 1.4426950408889634f);
-    oG = o * G;
-    if (fabsf(oG - ALPHA_MIN) < 1e-5f * ALPHA_MIN || fabsf(oG - ALPHA_MAX) < 1e-5f * ALPHA_MAX) {
-        G = ca_exp_core(power);
-        oG = FMUL(o, G);
-    }
-}
 
 template <bool CNT>
 __global__ __launch_bounds__(128, MVGS_BWD_MINB) void k_render_bwd_p(Launch L, const float* __restrict__ dL_drgb,
                                                       const float* __restrict__ in_T,
                                                       const int32_t* __restrict__ in_n) {
-    constexpr int NT = 128, NW = 4, RB = 128;
+    constexpr int NW = 4, RB = 128;
     __shared__ BwdConsts sc[RB];
     __shared__ uint32_t sq[RB];
+    __shared__ float sio[RB];  // 1/o: slot 6 is reduced as o·∂L/∂o
     __shared__ __align__(16) float sacc[NW][RB * NG];
     __shared__ int smax;
     __shared__ unsigned sev[2];
@@ -682,7 +399,6 @@ __global__ __launch_bounds__(128, MVGS_BWD_MINB) void k_render_bwd_p(Launch L, c
     const int64_t HW = (int64_t)L.H * L.W;
     float dL[2][3], Tfin[2];
     int last[2];
-    unsigned nev = 0;
 #pragma unroll
     for (int p = 0; p < 2; p++) {
         const int y = y0 + 2 * p;
@@ -699,18 +415,16 @@ __global__ __launch_bounds__(128, MVGS_BWD_MINB) void k_render_bwd_p(Launch L, c
         }
     }
     const float2 dLr = f2(dL[0][0], dL[1][0]), dLg = f2(dL[0][1], dL[1][1]), dLb = f2(dL[0][2], dL[1][2]);
-    // −T_final·(∂L/∂C · bg): the background term of ∂L/∂α, scaled by 1/(1 − α) per entry
-    const float2 nTbg = f2(-Tfin[0] * (L.bg[0] * dL[0][0] + L.bg[1] * dL[0][1] + L.bg[2] * dL[0][2]),
-                           -Tfin[1] * (L.bg[0] * dL[1][0] + L.bg[1] * dL[1][1] + L.bg[2] * dL[1][2]));
     float2 T = f2(Tfin[0], Tfin[1]);
-    float2 accr = f2(0.f, 0.f), accg = accr, accb = accr;  // colour behind the current entry
+    float2 nB = f2(-Tfin[0] * (L.bg[0] * dL[0][0] + L.bg[1] * dL[0][1] + L.bg[2] * dL[0][2]),
+                   -Tfin[1] * (L.bg[0] * dL[1][0] + L.bg[1] * dL[1][1] + L.bg[2] * dL[1][2]));
     const int mylast = max(last[0], last[1]);
     if (threadIdx.x == 0) {
         smax = 0;
         sev[0] = sev[1] = 0;
     }
     __syncthreads();
-    unsigned nexp = 0;
+    unsigned nev = 0, nexp = 0, nbl0 = 0, nbl1 = 0;
     if (mylast > 0) atomicMax(&smax, mylast);
     __syncthreads();
     const int maxlast = smax;
@@ -718,37 +432,34 @@ __global__ __launch_bounds__(128, MVGS_BWD_MINB) void k_render_bwd_p(Launch L, c
     const int my_id = reduce_id(lane);
     const bool owner = (__ffs(__match_any_sync(FULLR, my_id)) - 1) == lane;
     const float hw = 0.5f * (float)L.W, hh = 0.5f * (float)L.H;
-    // per-value scale applied by the owner after the reduction (see the V terms below)
-    const float oscale = my_id == 0 ? -hw : my_id == 1 ? -hh : (my_id == 3 || my_id == 5) ? -0.5f : my_id == 4 ? -1.f : 1.f;
+    // per-value scale applied by the owner after the reduction: Σ∇ = −(W/2, H/2)·(A d + B e,
+    // C e + B d) with d, e = ∂L/∂power·(dx, dy); ∂A = −½Σ d·dx, ∂B = −Σ d·dy, ∂C = −½Σ e·dy;
+    // the colour terms were accumulated with −w; slot 6 (o·∂L/∂o) is scaled by 1/o at the flush
+    const float oscale = my_id == 0 ? -hw : my_id == 1 ? -hh : (my_id == 3 || my_id == 5) ? -0.5f
+                       : (my_id == 4 || my_id >= 7) ? -1.f : 1.f;
     float* wacc = sacc[warp];
     const float2 nfx = f2(-(float)x, -(float)x), nfy = f2(-(float)y0, -(float)(y0 + 2));
-    const float2 one = f2(1.f, 1.f), mone = f2(-1.f, -1.f), mhalf = f2(-0.5f, -0.5f);
+    const float2 mhalf = f2(-0.5f, -0.5f);
     const float2 hw2 = f2(hw * hw, hw * hw), hh2 = f2(hh * hh, hh * hh);
-    // this thread's record index of the next (nearer) batch, loaded a batch ahead (RB == NT)
-    constexpr bool PF = MVGS_BWD_PREFETCH && RB == NT;
-    uint32_t qn = 0u;
-    if (PF && maxlast > 0) {
-        const int b0f = max(0, maxlast - RB);
-        if ((int)threadIdx.x < maxlast - b0f) qn = L.sorted[start + b0f + threadIdx.x];
-    }
     for (int b_end = maxlast; b_end > 0; b_end -= RB) {
         const int b0 = max(0, b_end - RB);
         const int cnt = b_end - b0;
         __syncthreads();
-        for (int t = threadIdx.x; t < cnt; t += NT) {
-            const uint32_t q = PF ? qn : L.sorted[start + b0 + t];
+        if ((int)threadIdx.x < cnt) {
+            const int t = threadIdx.x;
+            const uint32_t q = L.sorted[start + b0 + t];
             sq[t] = q;
             const float4* r = L.rec + 3 * (int64_t)q;
             const float4 r0 = r[0], r1 = r[1], r2 = r[2];
             BwdConsts k;
             k.xy = make_float4(r0.x, r0.x, r0.y, r0.y);
-            k.ab = make_float4(r0.z, r0.z, r0.w, r0.w);
-            k.cnb = make_float4(r1.x, r1.x, -r0.w, -r0.w);
-            const float sb = skip_power(r1.y);
-            k.os = make_float4(r1.y, r1.y, sb, sb);
+            k.ac = make_float4(r0.z, r0.z, r1.x, r1.x);
+            k.bo = make_float4(r0.w, r0.w, r1.y, r1.y);
             k.rg = make_float4(r1.z, r1.z, r1.w, r1.w);
-            k.bb = f2(r2.x, r2.x);
+            const float sb = skip_power(r1.y);
+            k.bs = make_float4(r2.x, r2.x, sb, 0.f);
             sc[t] = k;
+            sio[t] = 1.0f / r1.y;
             smask[t] = (uint8_t)warp_block_mask(r0.x, r0.y, r0.z, r0.w, r1.x, sb, (float)(tx * TILE), (float)(ty * TILE));
         }
         {
@@ -758,128 +469,94 @@ __global__ __launch_bounds__(128, MVGS_BWD_MINB) void k_render_bwd_p(Launch L, c
         __syncthreads();
         // this warp's entries of the batch (culled by its pixel block), walked back to front
         const int nl = warp_batch_list(smask, min(cnt, wmax - b0), warp, lane, slist[warp]);
-        const int nb0 = max(0, b0 - RB), ncnt = b0 - nb0;  // the next batch (walked after this one)
-        if (PF && (int)threadIdx.x < ncnt) qn = L.sorted[start + nb0 + threadIdx.x];
-#pragma unroll(kBwdUnroll)
         for (int u = nl - 1; u >= 0; u--) {
             const int jj = slist[warp][u];
             const int j = b0 + jj;
             if (CNT) nev += (unsigned)(j < last[0]) + (unsigned)(j < last[1]);
-            const float4 xy = sc[jj].xy, ab = sc[jj].ab, cnb = sc[jj].cnb, os = sc[jj].os;
+            const float4 xy = sc[jj].xy, ac = sc[jj].ac, bo = sc[jj].bo;
+            const float sb = sc[jj].bs.z;
             const float2 dx = __fadd2_rn(f2(xy.x, xy.y), nfx);
             const float2 dy = __fadd2_rn(f2(xy.z, xy.w), nfy);
             // ca_power per lane: FMA(−0.5, FMA(A·dx, dx, (C·dy)·dy), −(B·dx)·dy)
-            const float2 Adx = __fmul2_rn(f2(ab.x, ab.y), dx);
-            const float2 CdyDy = __fmul2_rn(__fmul2_rn(f2(cnb.x, cnb.y), dy), dy);
-            const float2 inner = __ffma2_rn(Adx, dx, CdyDy);
-            const float2 nBdxdy = __fmul2_rn(__fmul2_rn(f2(cnb.z, cnb.w), dx), dy);
-            const float2 power = __ffma2_rn(mhalf, inner, nBdxdy);
-            const bool in0 = j < last[0] && !(power.x > 0.f) && !(power.x < os.z);
-            const bool in1 = j < last[1] && !(power.y > 0.f) && !(power.y < os.z);
+            const float2 A2 = f2(ac.x, ac.y), C2 = f2(ac.z, ac.w), B2 = f2(bo.x, bo.y);
+            const float2 inner = __ffma2_rn(__fmul2_rn(A2, dx), dx, __fmul2_rn(__fmul2_rn(C2, dy), dy));
+            const float2 Bdd = __fmul2_rn(__fmul2_rn(B2, dx), dy);
+            const float2 power = __ffma2_rn(mhalf, inner, f2(-Bdd.x, -Bdd.y));
+            const bool in0 = j < last[0] && !(power.x > 0.f) && !(power.x < sb);
+            const bool in1 = j < last[1] && !(power.y > 0.f) && !(power.y < sb);
             if (!__any_sync(FULLR, in0 || in1)) continue;
             if (CNT) nexp += (unsigned)in0 + (unsigned)in1;
-            float G0, G1, oG0, oG1;
-            bwd_exp(power.x, os.x, G0, oG0);
-            bwd_exp(power.y, os.y, G1, oG1);
-            const float al0 = fminf(ALPHA_MAX, oG0), al1 = fminf(ALPHA_MAX, oG1);
-            const bool v0 = in0 && !(al0 < ALPHA_MIN), v1 = in1 && !(al1 < ALPHA_MIN);
-            if (!__any_sync(FULLR, v0 || v1)) continue;
-            const float2 alpha = f2(v0 ? al0 : 0.f, v1 ? al1 : 0.f);
-            // o·G for ∂/∂G and ∂/∂o; zero where clamped (α = 0.99 has zero gradient, R11)
-            const float2 Gc = f2(v0 && !(oG0 > ALPHA_MAX) ? G0 : 0.f, v1 && !(oG1 > ALPHA_MAX) ? G1 : 0.f);
-            const float2 om = __ffma2_rn(alpha, mone, one);
+            const float2 G = ca_exp_core2(power);
+            const float2 oG = __fmul2_rn(f2(bo.z, bo.w), G);
+            const bool bl0 = in0 && !(fminf(ALPHA_MAX, oG.x) < ALPHA_MIN);
+            const bool bl1 = in1 && !(fminf(ALPHA_MAX, oG.y) < ALPHA_MIN);
+            if (!__any_sync(FULLR, bl0 || bl1)) continue;
+            if (CNT) {
+                nbl0 += bl0;
+                nbl1 += bl1;
+            }
+            const float2 alpha = f2(bl0 ? fminf(ALPHA_MAX, oG.x) : 0.f, bl1 ? fminf(ALPHA_MAX, oG.y) : 0.f);
+            // o·G where it has a gradient: zero where clamped (α = 0.99 has zero gradient, R11)
+            const float2 oGc = f2(bl0 && !(oG.x > ALPHA_MAX) ? oG.x : 0.f, bl1 && !(oG.y > ALPHA_MAX) ? oG.y : 0.f);
+            const float2 om = __ffma2_rn(alpha, f2(-1.f, -1.f), f2(1.f, 1.f));
             const float2 inv = f2(rcp_approx(om.x), rcp_approx(om.y));
             T = __fmul2_rn(T, inv);
-            const float2 w = __fmul2_rn(alpha, T);
+            const float2 nw = __fmul2_rn(alpha, f2(-T.x, -T.y));  // −α·T
             const float4 rg = sc[jj].rg;
-            const float2 bb = sc[jj].bb;
-            const float2 cr = f2(rg.x, rg.y), cg = f2(rg.z, rg.w);
-            float2 dLda = __fmul2_rn(__ffma2_rn(accr, mone, cr), dLr);
-            dLda = __ffma2_rn(__ffma2_rn(accg, mone, cg), dLg, dLda);
-            dLda = __ffma2_rn(__ffma2_rn(accb, mone, bb), dLb, dLda);
-            dLda = __ffma2_rn(dLda, T, __fmul2_rn(nTbg, inv));
-            // colour behind the next (nearer) entry: α·c + (1 − α)·acc
-            accr = __ffma2_rn(alpha, cr, __fmul2_rn(om, accr));
-            accg = __ffma2_rn(alpha, cg, __fmul2_rn(om, accg));
-            accb = __ffma2_rn(alpha, bb, __fmul2_rn(om, accb));
-            const float2 dLdo = __fmul2_rn(Gc, dLda);
-            const float2 dLdpw = __fmul2_rn(__fmul2_rn(Gc, f2(os.x, os.y)), dLda);
+            const float2 bb = f2(sc[jj].bs.x, sc[jj].bs.y);
+            const float2 cdL = __ffma2_rn(bb, dLb, __ffma2_rn(f2(rg.z, rg.w), dLg, __fmul2_rn(f2(rg.x, rg.y), dLr)));
+            const float2 dLda = __ffma2_rn(nB, inv, __fmul2_rn(T, cdL));
+            nB = __ffma2_rn(cdL, nw, nB);
+            const float2 dLdpw = __fmul2_rn(oGc, dLda);  // ∂L/∂power = o·G·∂L/∂α
             const float2 d = __fmul2_rn(dLdpw, dx), e = __fmul2_rn(dLdpw, dy);
-            // ∂L/∂p' (pixels → NDC): gx = −hw·(A d + B e), gy = −hh·(C e + B d)
-            const float2 gxr = __ffma2_rn(f2(ab.x, ab.y), d, __fmul2_rn(f2(ab.z, ab.w), e));
-            const float2 gyr = __ffma2_rn(f2(cnb.x, cnb.y), e, __fmul2_rn(f2(ab.z, ab.w), d));
+            const float2 gxr = __ffma2_rn(A2, d, __fmul2_rn(B2, e));
+            const float2 gyr = __ffma2_rn(C2, e, __fmul2_rn(B2, d));
             const float2 n2 = __ffma2_rn(__fmul2_rn(gxr, gxr), hw2, __fmul2_rn(__fmul2_rn(gyr, gyr), hh2));
+            const float2 dd = __fmul2_rn(d, dx), de = __fmul2_rn(d, dy), ee = __fmul2_rn(e, dy);
+            const float2 wr = __fmul2_rn(nw, dLr), wg = __fmul2_rn(nw, dLg), wb = __fmul2_rn(nw, dLb);
             float val[NG];
             val[0] = gxr.x + gxr.y;
             val[1] = gyr.x + gyr.y;
             val[2] = sqrt_approx(n2.x) + sqrt_approx(n2.y);  // ‖∇_{p_i}L‖ per pixel, then add
-            const float2 dd = __fmul2_rn(d, dx), de = __fmul2_rn(d, dy), ee = __fmul2_rn(e, dy);
             val[3] = dd.x + dd.y;
             val[4] = de.x + de.y;
             val[5] = ee.x + ee.y;
-            val[6] = dLdo.x + dLdo.y;
-            const float2 wr = __fmul2_rn(w, dLr), wg = __fmul2_rn(w, dLg), wb = __fmul2_rn(w, dLb);
+            val[6] = dLdpw.x + dLdpw.y;
             val[7] = wr.x + wr.y;
             val[8] = wg.x + wg.y;
             val[9] = wb.x + wb.y;
             const float sum = warp_transpose_reduce10(val, lane);
             if (owner) wacc[jj * NG + my_id] = sum * oscale;
         }
-        if (PF && (int)threadIdx.x < ncnt) {  // warm the next batch's record in L2
-            const float4* rn = L.rec + 3 * (int64_t)qn;
-            asm volatile("prefetch.global.L2 [%0];" ::"l"(rn));
-            asm volatile("prefetch.global.L2 [%0];" ::"l"(rn + 2));
-        }
         __syncthreads();
-#if MVGS_BWD_RED4
-        // one 16-byte vector reduction per (entry, quarter of its slot): 3 instead of ≤ 10
-        for (int i = threadIdx.x; i < cnt * 3; i += NT) {
-            const int jj = i / 3, qd = i - jj * 3;
-            float a[4];
-#pragma unroll
-            for (int e = 0; e < 4; e++) {
-                const int k = 4 * qd + e;
-                float sum = 0.f;
-                if (k < NG) {
-#pragma unroll
-                    for (int w = 0; w < NW; w++) sum += sacc[w][jj * NG + k];
-                }
-                a[e] = sum;
-            }
-            if (a[0] != 0.f || a[1] != 0.f || a[2] != 0.f || a[3] != 0.f)
-                red_add_v4(L.pgrad + (int64_t)sq[jj] * PG_STRIDE + 4 * qd, a[0], a[1], a[2], a[3]);
-        }
-#else
-        for (int i = threadIdx.x; i < cnt * NG; i += NT) {
+        for (int i = threadIdx.x; i < cnt * NG; i += 128) {
             float s = 0.f;
 #pragma unroll
             for (int w = 0; w < NW; w++) s += sacc[w][i];
             if (s != 0.f) {
                 const int jj = i / NG, k = i - jj * NG;
+                if (k == 6) s *= sio[jj];
                 atomicAdd(&L.pgrad[(int64_t)sq[jj] * PG_STRIDE + k], s);
             }
         }
-#endif
     }
-    if (CNT) count_evals(&L.counters64[1], &L.counters64[3], nev, nexp, sev);
+    if (CNT) {
+        count_evals(&L.counters64[1], &L.counters64[3], nev, nexp, sev);
+        if (L.dbg_nblend) {  // parity export: entries blended per pixel, as this kernel decided
+            const int yy[2] = {y0, y0 + 2};
+            const unsigned nb[2] = {nbl0, nbl1};
+#pragma unroll
+            for (int p = 0; p < 2; p++)
+                if (x < L.W && yy[p] < L.H) L.dbg_nblend[v * HW + (int64_t)yy[p] * L.W + x] = (int32_t)nb[p];
+        }
+    }
 }
 
-#ifndef MVGS_BWD_PACKED
-#define MVGS_BWD_PACKED 1
-#endif
-
-#ifndef MVGS_BWD_NPX
-#define MVGS_BWD_NPX 2
-#endif
-
 cudaError_t launch_render_bwd(const Launch& L, const float* dL, const float* Tf, const int32_t* nc, cudaStream_t s) {
-    if (MVGS_BWD_PACKED)
-        if (L.count_evals)
-            k_render_bwd_p<true><<<L.V * L.T, 128, 0, s>>>(L, dL, Tf, nc);
-        else
-            k_render_bwd_p<false><<<L.V * L.T, 128, 0, s>>>(L, dL, Tf, nc);
+    if (L.count_evals || L.dbg_nblend)
+        k_render_bwd_p<true><<<L.V * L.T, 128, 0, s>>>(L, dL, Tf, nc);
     else
-        k_render_bwd<MVGS_BWD_NPX><<<L.V * L.T, 256 / MVGS_BWD_NPX, 0, s>>>(L, dL, Tf, nc);
+        k_render_bwd_p<false><<<L.V * L.T, 128, 0, s>>>(L, dL, Tf, nc);
     return cudaGetLastError();
 }
 

@@ -747,17 +747,6 @@ __global__ __launch_bounds__(RC_T) void k_ranges_close(Launch L, const int* __re
     }
 }
 
-// longest bucket (statistics)
-__global__ void k_max_bucket(Launch L) {
-    const int64_t nb = (int64_t)L.V * L.T;
-    int m = 0;
-    for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nb; b += (int64_t)gridDim.x * blockDim.x)
-        m = max(m, L.bucket_off[b + 1] - L.bucket_off[b]);
-    for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(FULLS, m, o));
-    if ((threadIdx.x & 31) == 0 && m > 0) atomicMax(&L.counters[C_MAXB], m);
-}
-
-
 // S4a: pairs by depth, carrying each pair's packed tile rect.  pkey/prect were written
 // by k_project (the values start as the pair slots themselves); the depth order and the rects in that order → *order_out, *rect_out.
 cudaError_t launch_sort_pairs(const Launch& L, const uint32_t** order_out, const uint2** rect_out, cudaStream_t s) {
@@ -806,11 +795,4 @@ cudaError_t launch_sort_entries(const Launch& L, uint32_t** sorted_vals, cudaStr
     return cudaGetLastError();
 }
 
-}  // namespace mvgs
-
-namespace mvgs {
-cudaError_t launch_max_bucket(const Launch& L, cudaStream_t s) {
-    k_max_bucket<<<64, 256, 0, s>>>(L);
-    return cudaGetLastError();
-}
 }  // namespace mvgs

@@ -109,12 +109,10 @@ cudaError_t alloc_sort_scratch(mvgs_ctx* c) {
 }
 
 cudaError_t alloc_entries(mvgs_ctx* c, int64_t n) {
-    cudaFree(c->d_key); cudaFree(c->d_val); cudaFree(c->d_key2); cudaFree(c->d_val2); cudaFree(c->d_ent64);
+    cudaFree(c->d_key); cudaFree(c->d_val); cudaFree(c->d_key2); cudaFree(c->d_val2);
     c->d_key = c->d_val = c->d_key2 = c->d_val2 = nullptr;
-    c->d_ent64 = nullptr;
     c->cap_entries = 0;
     cudaError_t e;
-    if (MVGS_SORT_BUCKET && (e = cudaMalloc(&c->d_ent64, 8 * n)) != cudaSuccess) return e;
     if ((e = cudaMalloc(&c->d_key, 4 * n)) != cudaSuccess) return e;
     if ((e = cudaMalloc(&c->d_val, 4 * n)) != cudaSuccess) return e;
     if ((e = cudaMalloc(&c->d_key2, 4 * n)) != cudaSuccess) return e;
@@ -213,8 +211,7 @@ mvgs_status mvgs_create(mvgs_ctx** out, int device, int64_t max_pairs, int64_t m
         (e = cudaMemset(ctx->d_counters, 0, sizeof(int) * C_NCOUNTERS)) != cudaSuccess ||
         (e = cudaMalloc(&ctx->d_counters64, sizeof(unsigned long long) * 8)) != cudaSuccess ||
         (e = cudaMemset(ctx->d_counters64, 0, sizeof(unsigned long long) * 8)) != cudaSuccess ||
-        (e = cudaMalloc(&ctx->d_lab_part, sizeof(double) * lab_partials())) != cudaSuccess ||
-        (e = cudaEventCreateWithFlags(&ctx->cams_ev, cudaEventDisableTiming)) != cudaSuccess) {
+        (e = cudaMalloc(&ctx->d_lab_part, sizeof(double) * lab_partials())) != cudaSuccess) {
         mvgs_destroy(ctx);
         return MVGS_ERR_CUDA;
     }
@@ -234,11 +231,9 @@ void mvgs_destroy(mvgs_ctx* ctx) {
     cudaFree(ctx->d_pflag);
     cudaFree(ctx->d_counters); cudaFree(ctx->d_counters64); cudaFree(ctx->d_scan);
     cudaFree(ctx->d_dssim_coef); cudaFree(ctx->d_dssim_part);
-    cudaFree(ctx->d_bcur); cudaFree(ctx->d_ent64); cudaFree(ctx->d_lab_part); cudaFree(ctx->d_pmask);
+    cudaFree(ctx->d_lab_part); cudaFree(ctx->d_pmask);
     cudaFree(ctx->d_adc_cnt); cudaFree(ctx->d_adc_flags); cudaFree(ctx->d_adc_tmp); cudaFree(ctx->d_adc_rep);
     if (ctx->h_adc_rep) cudaFreeHost(ctx->h_adc_rep);
-    if (ctx->h_cams) cudaFreeHost(ctx->h_cams);
-    if (ctx->cams_ev) cudaEventDestroy(ctx->cams_ev);
     for (int i = 0; i < MVGS_NUM_STAGES; i++)
         for (auto& p : ctx->ev_rec[i]) {
             cudaEventDestroy(p.first);
@@ -294,7 +289,6 @@ mvgs_status mvgs_preprocess(mvgs_ctx* ctx, const mvgs_gaussians* g, const mvgs_c
         CK(grow(ctx->d_pmask, ctx->cap_pmask, need_pmask));
         CK(grow(ctx->d_blk, ctx->cap_blk, nblk + 1));
         CK(grow(ctx->d_bucket, ctx->cap_buckets, nbuck + 1));
-        CK(grow(ctx->d_bcur, ctx->cap_bcur, nbuck + 1));
         if (need_scan > ctx->cap_scan) {
             cudaFree(ctx->d_scan);
             ctx->d_scan = nullptr;
@@ -303,24 +297,17 @@ mvgs_status mvgs_preprocess(mvgs_ctx* ctx, const mvgs_gaussians* g, const mvgs_c
         }
         if (V > ctx->cap_cams) {
             cudaFree(ctx->d_cams);
-            if (ctx->h_cams) cudaFreeHost(ctx->h_cams);
             ctx->d_cams = nullptr;
-            ctx->h_cams = nullptr;
             int64_t n = V + 8;
             CK(cudaMalloc(&ctx->d_cams, sizeof(mvgs_camera) * n));
-            CK(cudaMallocHost(&ctx->h_cams, sizeof(mvgs_camera) * n));
             ctx->cap_cams = n;
         }
     }
-    // cameras: host → pinned staging (after the previous copy drained) → device.  Under CUDA
-    // graph capture there is no previous copy to wait for: the captured copy reads the staging
-    // buffer at every replay, i.e. the cameras given here.
-    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
-    CK(cudaStreamIsCapturing(s, &cap));
-    if (cap == cudaStreamCaptureStatusNone) CK(cudaEventSynchronize(ctx->cams_ev));
-    memcpy(ctx->h_cams, cams, sizeof(mvgs_camera) * V);
-    CK(cudaMemcpyAsync(ctx->d_cams, ctx->h_cams, sizeof(mvgs_camera) * V, cudaMemcpyHostToDevice, s));
-    if (cap == cudaStreamCaptureStatusNone) CK(cudaEventRecord(ctx->cams_ev, s));
+    // cameras: written to the device by a tiny kernel that receives them BY VALUE (kernel
+    // parameters, ≤ 32 per launch).  No host buffer is shared between calls, the host never
+    // waits, and a CUDA graph captured here replays exactly the cameras given here (the values
+    // live in its kernel node), however the context is used afterwards.
+    CK(launch_set_cams(cams, V, ctx->d_cams, s));
 
     ctx->g = *g;
     Launch& L = ctx->L;
@@ -347,21 +334,7 @@ mvgs_status mvgs_preprocess(mvgs_ctx* ctx, const mvgs_gaussians* g, const mvgs_c
     const uint32_t* order = L.pval;
     const uint2* rect = L.prect;
     uint32_t* sorted = L.val;
-    if (NB > 0 && MVGS_SORT_BUCKET) {
-        // S3 counts + S5 ranges, S3 duplication into buckets, S4 per-bucket depth sort (k_bucket.cu)
-        {
-            STAGE(ST_SORT_PAIRS);
-            CK(launch_bucket_count(L, ctx->d_bucket, s));
-            CK(scan_exclusive(ctx->d_bucket, (int)nbuck, ctx->d_counters + C_K, ctx->d_scan, s));
-        }
-        { STAGE(ST_DUP); CK(launch_bucket_scatter(L, ctx->d_bcur, ctx->d_ent64, s)); }
-        {
-            STAGE(ST_SORT_ENTRIES);
-            CK(launch_bucket_sort(L, ctx->d_ent64, L.val, s));
-            CK(launch_max_bucket(L, s));
-        }
-        sorted = L.val;
-    } else if (NB > 0) {
+    if (NB > 0) {
         { STAGE(ST_SORT_PAIRS); CK(launch_sort_pairs(L, &order, &rect, s)); }                        // S4a
         { STAGE(ST_DUP); CK(launch_dup_sort(L, order, rect, s)); }                                   // S3
         { STAGE(ST_SORT_ENTRIES); CK(launch_sort_entries(L, &sorted, s)); }                          // S4b + S5
@@ -498,6 +471,12 @@ mvgs_status mvgs_export_pairs(mvgs_ctx* ctx, int32_t* pair_ids, int32_t* pair_i,
     if (!ctx) return MVGS_ERR_INVALID;
     if (ctx->state < 1) return fail(ctx, MVGS_ERR_STATE, "export before preprocess");
     CK(launch_export(ctx->L, nullptr, nullptr, pair_ids, pair_i, pair_f, pair_g, (cudaStream_t)stream));
+    return MVGS_OK;
+}
+
+mvgs_status mvgs_set_debug_blend_counts(mvgs_ctx* ctx, int32_t* nblend) {
+    if (!ctx) return MVGS_ERR_INVALID;
+    ctx->L.dbg_nblend = nblend;
     return MVGS_OK;
 }
 

@@ -22,7 +22,7 @@ SYMBOLS = ["mvgs_create", "mvgs_destroy", "mvgs_last_error", "mvgs_reserve", "mv
            "mvgs_render_bwd", "mvgs_adc_stats", "mvgs_adc_stats_range", "mvgs_query", "mvgs_export_lists", "mvgs_export_pairs",
            "mvgs_set_timing", "mvgs_stage_times", "mvgs_set_eval_counting", "mvgs_render_fwd_partial", "mvgs_render_bwd_partial",
            "mvgs_render_fwd_depth", "mvgs_dssim3d", "mvgs_adc_step", "mvgs_adc_remap",
-           "mvgs_loss_grad", "mvgs_grad_moments", "mvgs_grad_variance"]
+           "mvgs_loss_grad", "mvgs_grad_moments", "mvgs_grad_variance", "mvgs_set_debug_blend_counts"]
 PARTIAL_THREAD_EFFICIENT, PARTIAL_MASKED = 0, 1
 STAGE_NAMES = ["count", "scan_pairs", "project", "scan_buckets", "sort_pairs", "dup", "sort_entries", "render_fwd",
                "render_bwd", "gauss_bwd", "dssim"]
@@ -100,6 +100,7 @@ def _load():
     L.mvgs_export_pairs.argtypes = [vp, vp, vp, vp, vp, vp]
     L.mvgs_set_timing.argtypes = [vp, C.c_int]
     L.mvgs_set_eval_counting.argtypes = [vp, C.c_int]
+    L.mvgs_set_debug_blend_counts.argtypes = [vp, vp]
     L.mvgs_render_fwd_partial.argtypes = [vp, vp, C.c_int32, C.c_int32, vp, vp, vp, vp]
     L.mvgs_render_bwd_partial.argtypes = [vp, vp, C.c_int32, C.c_int32, vp, vp, vp, vp]
     L.mvgs_dssim3d.argtypes = [vp, vp, C.c_int32, C.c_int32, C.c_int32, vp, vp, vp, vp, C.c_float, vp, vp, vp]
@@ -301,6 +302,11 @@ def export_lists(ctx, range_start, entry_gid, stream=None):
 def export_pairs(ctx, pair_ids=None, pair_i=None, pair_f=None, pair_g=None, stream=None):
     _check(ctx, _lib.mvgs_export_pairs(ctx, _ptr(pair_ids), _ptr(pair_i), _ptr(pair_f), _ptr(pair_g),
                                        _stream(stream)))
+
+
+def set_debug_blend_counts(ctx, nblend=None):
+    """Parity export: per-pixel count of entries the backward blended ([V,H,W] int32), or off."""
+    _check(ctx, _lib.mvgs_set_debug_blend_counts(ctx, _ptr(nblend) if nblend is not None else None))
 
 
 def set_timing(ctx, enable: bool):

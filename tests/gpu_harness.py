@@ -18,7 +18,14 @@ def run_gpu(g, cams, dLdC=None, bg=(0.0, 0.0, 0.0), max_pairs=0, max_entries=0, 
     rgb, Tf, nc = R.forward()
     out = dict(stats=R.stats)
     if dLdC is not None:
+        nbl = None
+        if export:  # the backward's own blended-entry count per pixel (its re-taken decisions)
+            nbl = torch.full((len(cams), R.H, R.W), -1, dtype=torch.int32, device="cuda")
+            mvgs.set_debug_blend_counts(R.ctx, nbl)
         grads, adc = R.backward(torch.from_numpy(np.ascontiguousarray(dLdC, np.float32)).cuda())
+        if nbl is not None:
+            mvgs.set_debug_blend_counts(R.ctx, None)
+            out["bwd_nblend"] = nbl.cpu().numpy()
         out.update({k: v.cpu().numpy() for k, v in grads.items()})
         out.update({k: v.cpu().numpy() for k, v in adc.items()})
     torch.cuda.synchronize()

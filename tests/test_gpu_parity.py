@@ -99,9 +99,11 @@ def test_lists_bit_exact(case):
 
 
 def test_forward(case):
-    """S6: n_contrib bit-exact; image and T_final ≤ 1e-5 abs (fp32 vs fp64 oracle)."""
+    """S6: n_contrib bit-exact; image and T_final ≤ 1e-5 abs (fp32 vs fp64 oracle).  S7's
+    re-taken decisions: the backward blends exactly the forward's entries at every pixel."""
     gpu, ref = case["gpu"], case["ref_im"]
     np.testing.assert_array_equal(gpu["n_contrib"], ref["n_contrib"])
+    np.testing.assert_array_equal(gpu["bwd_nblend"], case["o"].nblend())
     assert np.max(np.abs(gpu["rgb"] - ref["rgb"])) <= 1e-5
     assert np.max(np.abs(gpu["T_final"] - ref["T_final"])) <= 1e-5
 
@@ -141,6 +143,7 @@ def _check_all(g, cams, bg=(0.0, 0.0, 0.0), seed=3, **kw):
     off, gid = o.lists()
     np.testing.assert_array_equal(gpu["range_start"], off)
     np.testing.assert_array_equal(gpu["entry_gid"], gid)
+    np.testing.assert_array_equal(gpu["bwd_nblend"], o.nblend())
     for k in ["d_means", "d_log_scales", "d_quats", "d_opacity_logits", "d_sh", "e1", "e2", "e_old"]:
         assert_close_rel(gpu[k], ref[k], k, scale=scale[k])
     np.testing.assert_array_equal(gpu["vis"], ref["vis"])
@@ -362,6 +365,53 @@ def test_warp_culling_on_thin_correlated_ellipses():
     rho2 = np.where(AC > 0, p["B"].astype(np.float64) ** 2 / np.where(AC > 0, AC, 1), 0.0)
     assert rho2[p["vis"] > 0].max() > 0.99  # the adversarial (strongly correlated) case is exercised
     np.testing.assert_array_equal(gpu["vis"], ref["vis"])
+
+
+def test_backward_decisions_at_the_alpha_thresholds():
+    """S7 re-takes the forward's α ≥ 1/255 and α-clamp (o·G > 0.99) decisions (R11, R12).
+    Well-conditioned, mildly anisotropic Gaussians whose opacities put o·G within a few
+    ulp-scale steps of both thresholds somewhere on their footprints — opacities just above
+    1/255 (so the α = 1/255 contour crosses many pixels) and just above 0.99 (so the clamp
+    contour does) — and every pixel's blended-entry count taken by the backward equals the
+    oracle's; n_contrib, lists and images bit-exact / ≤ 1e-5; per-pair records and every
+    gradient to the §5 rule."""
+    rng = np.random.default_rng(77)
+    n = 600
+    W, H, f = 96, 80, 70.0
+    z = rng.uniform(2.0, 5.0, n)
+    px, py = rng.uniform(-8, W + 8, n), rng.uniform(-8, H + 8, n)
+    means = np.column_stack([(px - (W - 1) / 2) / f * z, (py - (H - 1) / 2) / f * z, z])
+    s = rng.uniform(0.02, 0.06, n)[:, None] * z[:, None] / 3 * rng.uniform(0.7, 1.3, (n, 3))
+    kind = rng.integers(0, 3, n)
+    # kind 0: o ∈ 1/255·(1, 1.2]; kind 1: o ∈ 0.99·(1, 1.004]; kind 2: ordinary
+    o = np.where(kind == 0, (1 + rng.uniform(1e-6, 0.2, n)) / 255,
+                 np.where(kind == 1, 0.99 * (1 + rng.uniform(1e-6, 4e-3, n)), rng.uniform(0.05, 0.95, n)))
+    s[kind == 1] *= 2.5  # wide footprints: the clamp contour o·G = 0.99 spans more pixels
+    logit = np.log(o / (1 - o))
+    g = _scene(means, np.log(s), logit, rgb=rng.uniform(0, 1, (n, 3)))
+    q = rng.normal(size=(n, 4))
+    g["quats"] = (q / np.linalg.norm(q, axis=1, keepdims=True)).astype(np.float32)
+    cam = synth.cams_array([synth.make_camera(np.eye(3), [0, 0, 0], W, H, f),
+                            synth.make_camera(np.eye(3), [0.05, 0.02, 0.2], W, H, 80.0)])
+    gpu, o_ = _check_all(g, cam, bg=(0.2, 0.1, 0.3), seed=21)
+    # the thresholds are really straddled: pixels where some o·G is within 1e-4 (relative) of them
+    p = o_.pairs()
+    near_lo = near_hi = 0
+    op = p["opacity"].astype(np.float64)
+    for v in range(len(cam)):
+        for i in np.nonzero(p["vis"][v])[0]:
+            A, B, C = (float(p[k][v, i]) for k in ("A", "B", "C"))
+            yy, xx = np.mgrid[0:H, 0:W]
+            dx, dy = p["px"][v, i] - xx, p["py"][v, i] - yy
+            oG = op[i] * np.exp(-0.5 * (A * dx * dx + C * dy * dy) - B * dx * dy)
+            near_lo += int(np.sum(np.abs(oG * 255 - 1) < 1e-3))
+            near_hi += int(np.sum(np.abs(oG / 0.99 - 1) < 1e-3))
+    assert near_lo > 20 and near_hi > 20, (near_lo, near_hi)
+    ref = o_.pair_grads()
+    p2, zv, zg = _gpu_pairs_in_oracle(o_, gpu)
+    names = ["sum_grad_x", "sum_grad_y", "e1", "dA", "dB", "dC", "dopacity", "dr", "dg", "db"]
+    for k, nm in enumerate(names):
+        assert_close_rel(gpu["pair_g"][:, k], ref[zv, zg][:, k], nm)
 
 
 def test_eval_counting_off_changes_nothing():
