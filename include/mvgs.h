@@ -94,6 +94,13 @@ typedef struct {
     float *e2_acc;    /* [P] nullable, += e2  */
     float *denom_acc; /* [P] nullable, += vis */
     float *e_old_acc; /* [P] nullable, += e_old (single-view ADC metric, NEXT-3 mode 0) */
+    float *max_radius;/* [P] nullable, max= the largest screen radius ⌈3√λ_max⌉ (px, R7) over the
+                         batch's views where the Gaussian covers ≥1 tile — the running
+                         max_screen_radius of SPEC S:248 that the ADC prune reads             */
+    float *gsum;      /* [P,2] nullable, overwritten: Σ_views Σ_pixels ∇_{p_i}L (NDC, R2) — the
+                         vector whose norm is E_old.  Additive over views, so a multi-GPU
+                         caller sums it with the gradients and takes E_old = ‖gsum‖ after the
+                         all-reduce                                            */
 } mvgs_adc;
 
 typedef struct {

@@ -15,6 +15,7 @@ constexpr int NG = 10;            // per-pair gradient record: Σ∇x Σ∇y e1 
 constexpr int PG_STRIDE = 12;     // floats per pair-gradient slot (48 B, 16-B aligned)
 constexpr int REC_F4 = 3;         // float4 per pair render record (48 B)
 constexpr uint32_t PF_VISIBLE = 32u;
+constexpr int PF_RADIUS_SHIFT = 8;  // pflag bits 8..31: the pair's CA radius (R7), saturated at 2^24 − 1
 
 // device counters (int32 slots in ctx->d_counters)
 enum { C_Q = 0, C_K = 1, C_OVERFLOW = 2, C_MAXB = 3, C_NVIS = 4, C_NCOUNTERS = 8 };
@@ -38,7 +39,7 @@ struct Launch {  // everything a kernel needs about the current batch
     int* blk_off;     // [V*NB + 1]  exclusive scan of per-(view, block) participation counts
     int* bucket_off;  // [V*T + 1]   exclusive scan of per-(view, tile) entry counts
     float4* rec;      // [cap_pairs * 3]
-    uint32_t* pflag;  // [cap_pairs] bit0-2 rgb clamped, bit3-4 Jacobian clamps, bit5 tiles > 0
+    uint32_t* pflag;  // [cap_pairs] bit0-2 rgb clamped, bit3-4 Jacobian clamps, bit5 tiles > 0, bits 8..31 radius
     float* pgrad;     // [cap_pairs * PG_STRIDE]
     uint32_t *key, *val, *key2, *val2;  // [cap_entries] entry (bucket key, pair) ping-pong
     uint32_t *pkey, *pval, *pkey2, *pval2;  // [cap_pairs] pair (depth key, pair) ping-pong
@@ -74,7 +75,8 @@ struct mvgs_ctx {
     int device = 0;
     int64_t cap_pairs = 0, cap_entries = 0;
     int64_t cap_blk = 0, cap_buckets = 0, cap_cams = 0, cap_scan = 0;
-    int state = 0;  // 0 none, 1 preprocessed, 2 forward done, 3 backward done
+    int state = 0;  // 0 none, 1 preprocessed, 2 forward done, 3 backward done, 4 partial forward done
+    int partial_S = 0, partial_mode = -1;  // the partial forward's sample size and launch shape
     mvgs::Launch L{};
     mvgs_gaussians g{};
     // device buffers

@@ -140,6 +140,7 @@ struct GAcc {
     float dmx = 0.f, dmy = 0.f, dmz = 0.f;
     float G00 = 0.f, G01 = 0.f, G02 = 0.f, G11 = 0.f, G12 = 0.f, G22 = 0.f;  // ∂L/∂Σ (symmetric)
     float dop = 0.f, e1 = 0.f, e2 = 0.f, gsx = 0.f, gsy = 0.f, nvis = 0.f;
+    float rmax = 0.f;  // largest screen radius over the visible views (k_project's CA radius, flags >> 8)
 };
 
 template <int D>
@@ -154,6 +155,7 @@ __device__ __forceinline__ void pair_chain(const mvgs_camera& c, float4 cam4, fl
     float& gsx = A.gsx; float& gsy = A.gsy; float& nvis = A.nvis;
     // pg: (Σ∇x, Σ∇y, e1, ∂A) (∂B, ∂C, ∂o, ∂r) (∂g, ∂b, -, -)
     nvis += 1.f;
+    A.rmax = fmaxf(A.rmax, (float)(flags >> PF_RADIUS_SHIFT));
     e1 += pg0.z;
     e2 += g_sqrt(pg0.x * pg0.x + pg0.y * pg0.y);
     gsx += pg0.x;
@@ -365,6 +367,11 @@ __device__ __forceinline__ void finish_gaussian(const Launch& L, const mvgs_grad
         if (adc.e_old_acc) adc.e_old_acc[o] += eo;
     }
     adc.vis[o] = nvis;
+    if (adc.gsum) {
+        adc.gsum[2 * o] = gsx;
+        adc.gsum[2 * o + 1] = gsy;
+    }
+    if (adc.max_radius && A.rmax > 0.f) adc.max_radius[o] = fmaxf(adc.max_radius[o], A.rmax);
     if (adc.e1_acc) adc.e1_acc[o] += e1;
     if (adc.e2_acc) adc.e2_acc[o] += e2;
     if (adc.denom_acc) adc.denom_acc[o] += nvis;

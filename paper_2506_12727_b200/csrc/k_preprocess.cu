@@ -389,7 +389,7 @@ __global__ __launch_bounds__(BLK) void k_project(Launch L) {
                 r[0] = make_float4(p.px, p.py, p.A, p.B);
                 r[1] = make_float4(p.C, a.o, rgb[0], rgb[1]);
                 r[2] = make_float4(rgb[2], p.tz, sb, 1.0f / a.o);
-                L.pflag[pair] = flags | PF_VISIBLE;  // (its gradient slot is cleared by the forward)
+                L.pflag[pair] = flags | PF_VISIBLE | ((uint32_t)min(p.radius, 0xffffff) << PF_RADIUS_SHIFT);  // (its gradient slot is cleared by the forward)
             }
             my_vis += (tiles > 0 && pair < L.cap_pairs) ? 1u : 0u;
             my_tiles += (unsigned long long)tiles;

@@ -269,6 +269,9 @@ mvgs_status mvgs_preprocess(mvgs_ctx* ctx, const mvgs_gaussians* g, const mvgs_c
         return fail(ctx, MVGS_ERR_INVALID, "null parameter pointer");
     const int W = cams[0].width, H = cams[0].height;
     if (W <= 0 || H <= 0) return fail(ctx, MVGS_ERR_INVALID, "non-positive image size");
+    for (int v = 0; v < V; v++)  // depth keys are the float bits of t.z > znear > 0 (R9): ordered only if positive
+        if (!(cams[v].znear > 0.f) || !(cams[v].fx > 0.f) || !(cams[v].fy > 0.f))
+            return fail(ctx, MVGS_ERR_INVALID, "camera needs znear > 0, fx > 0, fy > 0 (R3, R9)");
     for (int v = 1; v < V; v++)
         if (cams[v].width != W || cams[v].height != H) return fail(ctx, MVGS_ERR_INVALID, "views differ in size (R25)");
     const int TX = (W + TILE - 1) / TILE, TY = (H + TILE - 1) / TILE;
@@ -391,14 +394,17 @@ mvgs_status mvgs_render_fwd_partial(mvgs_ctx* ctx, const int32_t* pix, int32_t S
     cudaStream_t s = (cudaStream_t)stream;
     ctx->last_stream = s;
     { STAGE(ST_FWD); CK(launch_render_fwd_partial(ctx->L, pix, S, mode, rgb, T_final, n_contrib, s)); }
-    ctx->state = 2;
+    ctx->state = 4;  // partial forward: its [V,T,S] outputs are only valid for the matching partial backward
+    ctx->partial_S = S;
+    ctx->partial_mode = mode;
     return MVGS_OK;
 }
 
 mvgs_status mvgs_render_bwd_partial(mvgs_ctx* ctx, const int32_t* pix, int32_t S, int32_t mode, const float* dL_drgb,
                                     const float* T_final, const int32_t* n_contrib, void* stream) {
     if (!ctx) return MVGS_ERR_INVALID;
-    if (ctx->state != 2) return fail(ctx, MVGS_ERR_STATE, "render_bwd_partial needs a render_fwd of a fresh preprocess");
+    if (ctx->state != 4 || ctx->partial_S != S || ctx->partial_mode != mode)
+        return fail(ctx, MVGS_ERR_STATE, "render_bwd_partial needs a render_fwd_partial (same S and mode) of a fresh preprocess");
     if (!pix || !dL_drgb || !T_final || !n_contrib || S < 1 || S > 256 ||
         (mode != MVGS_PARTIAL_THREAD_EFFICIENT && mode != MVGS_PARTIAL_MASKED))
         return fail(ctx, MVGS_ERR_INVALID, "partial: null pointer, S outside [1, 256] or unknown mode");
@@ -435,11 +441,12 @@ mvgs_status mvgs_adc_stats(mvgs_ctx* ctx, const mvgs_grads* grads, const mvgs_ad
 mvgs_status mvgs_query(mvgs_ctx* ctx, mvgs_stats* out) {
     if (!ctx || !out) return MVGS_ERR_INVALID;
     CK(cudaSetDevice(ctx->device));
-    CK(cudaDeviceSynchronize());
     int h[C_NCOUNTERS];
     unsigned long long h64[5];
-    CK(cudaMemcpy(h, ctx->d_counters, sizeof(h), cudaMemcpyDeviceToHost));
-    CK(cudaMemcpy(h64, ctx->d_counters64, sizeof(h64), cudaMemcpyDeviceToHost));
+    // ordered on the stream of the last enqueuing call; waits for that stream only, not the device
+    CK(cudaMemcpyAsync(h, ctx->d_counters, sizeof(h), cudaMemcpyDeviceToHost, ctx->last_stream));
+    CK(cudaMemcpyAsync(h64, ctx->d_counters64, sizeof(h64), cudaMemcpyDeviceToHost, ctx->last_stream));
+    CK(cudaStreamSynchronize(ctx->last_stream));
     memset(out, 0, sizeof(*out));
     out->Q = h[C_Q];
     out->K = std::max((int64_t)h[C_K], (int64_t)h64[4]);  // entries needed, even past a pair overflow

@@ -97,11 +97,19 @@ def adc_stats_allreduce(ctx, buf: GradBuffer, group=None, stream=None, compute=N
 
         def compute(c, lo, hi, gr, ad):
             mvgs.adc_stats_range(ctx, lo, hi, gr, ad, stream=stream)
+    import contextlib
+
+    # ProcessGroupNCCL orders each collective after torch's CURRENT stream: make the stream the
+    # kernels are enqueued on the current one, so a chunk is never reduced before it is written
+    if stream is not None and not isinstance(stream, torch.cuda.Stream):
+        stream = torch.cuda.ExternalStream(int(stream))  # a raw cudaStream_t handle
+    on_stream = torch.cuda.stream(stream) if stream is not None else contextlib.nullcontext()
     works = []
-    for c in range(len(buf.bounds)):
-        lo, hi, gr, ad = buf.chunk_outputs(c)
-        if hi > lo:
-            compute(c, lo, hi, gr, ad)
-        works.append(dist.all_reduce(buf.chunk_flat[c], op=dist.ReduceOp.SUM, group=group, async_op=True))
-    for w in works:
-        w.wait()
+    with on_stream:
+        for c in range(len(buf.bounds)):
+            lo, hi, gr, ad = buf.chunk_outputs(c)
+            if hi > lo:
+                compute(c, lo, hi, gr, ad)
+            works.append(dist.all_reduce(buf.chunk_flat[c], op=dist.ReduceOp.SUM, group=group, async_op=True))
+        for w in works:
+            w.wait()

@@ -44,8 +44,11 @@ class Grads(C.Structure):
     _fields_ = [(k, C.c_void_p) for k in ("d_means", "d_log_scales", "d_quats", "d_opacity_logits", "d_sh")]
 
 
+ADC_FIELDS = ("e1", "e2", "e_old", "vis", "e1_acc", "e2_acc", "denom_acc", "e_old_acc", "max_radius", "gsum")
+
+
 class Adc(C.Structure):
-    _fields_ = [(k, C.c_void_p) for k in ("e1", "e2", "e_old", "vis", "e1_acc", "e2_acc", "denom_acc", "e_old_acc")]
+    _fields_ = [(k, C.c_void_p) for k in ADC_FIELDS]
 
 
 class AdcConfig(C.Structure):
@@ -214,14 +217,14 @@ def render_bwd_partial(ctx, pix, S: int, mode: int, dL_drgb, T_final, n_contrib,
 
 def adc_stats(ctx, grads: dict, adc: dict, stream=None):
     gr = Grads(*[_ptr(grads[k]) for k in ("d_means", "d_log_scales", "d_quats", "d_opacity_logits", "d_sh")])
-    ad = Adc(*[_ptr(adc.get(k)) for k in ("e1", "e2", "e_old", "vis", "e1_acc", "e2_acc", "denom_acc", "e_old_acc")])
+    ad = Adc(*[_ptr(adc.get(k)) for k in ADC_FIELDS])
     _check(ctx, _lib.mvgs_adc_stats(ctx, C.byref(gr), C.byref(ad), _stream(stream)))
 
 
 def adc_stats_range(ctx, g_begin: int, g_end: int, grads: dict, adc: dict, stream=None):
     """S8–S9 for Gaussians [g_begin, g_end) (g_begin % 256 == 0); the tensors hold rows g_begin.. ."""
     gr = Grads(*[_ptr(grads[k]) for k in ("d_means", "d_log_scales", "d_quats", "d_opacity_logits", "d_sh")])
-    ad = Adc(*[_ptr(adc.get(k)) for k in ("e1", "e2", "e_old", "vis", "e1_acc", "e2_acc", "denom_acc", "e_old_acc")])
+    ad = Adc(*[_ptr(adc.get(k)) for k in ADC_FIELDS])
     _check(ctx, _lib.mvgs_adc_stats_range(ctx, int(g_begin), int(g_end), C.byref(gr), C.byref(ad), _stream(stream)))
 
 
@@ -379,7 +382,8 @@ class Rasterizer:
         z = lambda *s: torch.empty(s, dtype=torch.float32, device=dev)  # noqa: E731
         grads = dict(d_means=z(P, 3), d_log_scales=z(P, 3), d_quats=z(P, 4), d_opacity_logits=z(P),
                      d_sh=z(P, g["sh"].shape[1], 3))
-        adc = dict(e1=z(P), e2=z(P), e_old=z(P), vis=z(P))
+        adc = dict(e1=z(P), e2=z(P), e_old=z(P), vis=z(P), gsum=z(P, 2),
+                   max_radius=torch.zeros(P, dtype=torch.float32, device=dev))  # max= accumulator
         return grads, adc
 
     def backward(self, dL_drgb, out=None, stream=None):

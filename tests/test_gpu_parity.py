@@ -122,9 +122,10 @@ def test_backward_param_grads_and_adc(case):
     """S8/S9: every parameter gradient summed over views and E1, E2,
     E_old, vis; GPU-side E ordering invariants."""
     gpu, ref = case["gpu"], case["ref_g"]
-    for k in ["d_means", "d_log_scales", "d_quats", "d_opacity_logits", "d_sh", "e1", "e2", "e_old"]:
+    for k in ["d_means", "d_log_scales", "d_quats", "d_opacity_logits", "d_sh", "e1", "e2", "e_old", "gsum"]:
         assert_close_rel(gpu[k], ref[k], k, scale=case["scale"][k])
     np.testing.assert_array_equal(gpu["vis"], ref["vis"])
+    np.testing.assert_array_equal(gpu["max_radius"], ref["max_radius"])  # SPEC S:248, R7 radius: integer
     assert np.all(gpu["e1"] >= gpu["e2"] * (1 - 1e-5))
     assert np.all(gpu["e2"] >= gpu["e_old"] * (1 - 1e-5))
 
@@ -144,9 +145,10 @@ def _check_all(g, cams, bg=(0.0, 0.0, 0.0), seed=3, **kw):
     np.testing.assert_array_equal(gpu["range_start"], off)
     np.testing.assert_array_equal(gpu["entry_gid"], gid)
     np.testing.assert_array_equal(gpu["bwd_nblend"], o.nblend())
-    for k in ["d_means", "d_log_scales", "d_quats", "d_opacity_logits", "d_sh", "e1", "e2", "e_old"]:
+    for k in ["d_means", "d_log_scales", "d_quats", "d_opacity_logits", "d_sh", "e1", "e2", "e_old", "gsum"]:
         assert_close_rel(gpu[k], ref[k], k, scale=scale[k])
     np.testing.assert_array_equal(gpu["vis"], ref["vis"])
+    np.testing.assert_array_equal(gpu["max_radius"], ref["max_radius"])
     return gpu, o
 
 
