@@ -234,13 +234,16 @@ class Oracle:
                  e_old=np.zeros(P), vis=np.zeros(P))
         lib().oracle_get_grads(self._h, *[_p(o[k]) for k in ("d_means", "d_log_scales", "d_quats",
                                                              "d_opacity_logits", "d_sh", "e1", "e2", "e_old", "vis")])
-        # SPEC S:248 max_screen_radius: the largest radius (R7) over the views where the pair covers a tile
+        return o
+
+    def adc_extra(self):
+        """max_radius [P]: SPEC S:248's max_screen_radius, the largest radius (R7) over the views
+        where the pair covers a tile; gsum [P,2]: Σ over views and pixels of ∇_{p_i}L, the vector
+        whose norm is E_old.  From the last backward; small scenes only (per-pair arrays)."""
         pr = self.pairs()
         rad = np.where(pr["tiles"] > 0, pr["radius"], 0)
-        o["max_radius"] = rad.max(axis=0).astype(np.float64) if self.V else np.zeros(P)
-        # Σ over views and pixels of ∇_{p_i}L (the vector whose norm is E_old)
-        o["gsum"] = self.pair_grads()[:, :, 0:2].sum(axis=0)
-        return o
+        mr = rad.max(axis=0).astype(np.float64) if self.V else np.zeros(self.P)
+        return dict(max_radius=mr, gsum=self.pair_grads()[:, :, 0:2].sum(axis=0))
 
 
 def run(g, cams, bg=(0.0, 0.0, 0.0), dLdC=None, flags=0):

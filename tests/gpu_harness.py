@@ -88,13 +88,16 @@ def assert_close_rel(got, ref, name, rtol=1e-3, floor=1e-6, scale=None, ctol=1e-
     assert np.all(d <= lim), msg
 
 
-def per_view_scale(g, cams, dLdC, bg=(0.0, 0.0, 0.0), tile_mask=None):
+def per_view_scale(g, cams, dLdC, bg=(0.0, 0.0, 0.0), tile_mask=None, extra=True):
     """Σ_v |gradient of view v alone| for every output (the oracle, one view at a time)."""
     import oracle
     out = None
     for v in range(len(cams)):
         m = None if tile_mask is None else tile_mask[v:v + 1]
-        r = oracle.Oracle(g, cams[v:v + 1], bg=bg, tile_mask=m).backward(dLdC[v:v + 1])
+        ov = oracle.Oracle(g, cams[v:v + 1], bg=bg, tile_mask=m)
+        r = ov.backward(dLdC[v:v + 1])
+        if extra:  # per-pair arrays: oracle-sized scenes only
+            r["gsum"] = ov.adc_extra()["gsum"]
         if out is None:
             out = {k: np.abs(x) for k, x in r.items()}
         else:

@@ -37,7 +37,7 @@ def garden(require_gpu):
     gpu = run_gpu(g, cams, dL)
     o = oracle.Oracle(g, cams, tile_mask=mask)
     ref = o.backward(dL)
-    scale = per_view_scale(g, cams, dL, tile_mask=mask)
+    scale = per_view_scale(g, cams, dL, tile_mask=mask, extra=False)
     return dict(g=g, cams=cams, mask=mask, pix=pix, dL=dL, gpu=gpu, o=o, ref=ref, im=o.image(), T=T, scale=scale)
 
 

@@ -47,6 +47,7 @@ def case(request):
     dL = synth.make_dLdC_scaled(V, H, W, 11)
     o = oracle.Oracle(g, cams, bg=kw["bg"])
     ref_g = o.backward(dL)
+    ref_g.update(o.adc_extra())
     ref_im = o.image()
     gpu = run_gpu(g, cams, dL, bg=kw["bg"])
     scale = per_view_scale(g, cams, dL, kw["bg"])
@@ -136,6 +137,7 @@ def _check_all(g, cams, bg=(0.0, 0.0, 0.0), seed=3, **kw):
     dL = synth.make_dLdC_scaled(V, H, W, seed)
     o = oracle.Oracle(g, cams, bg=bg)
     ref = o.backward(dL)
+    ref.update(o.adc_extra())
     im = o.image()
     gpu = run_gpu(g, cams, dL, bg=bg, **kw)
     scale = per_view_scale(g, cams, dL, bg)
