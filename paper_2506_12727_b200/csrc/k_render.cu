@@ -63,7 +63,6 @@ __device__ __forceinline__ void count_evals(unsigned long long* ctr0, unsigned l
 // Below −ln(255·o) − SKIP_MARGIN the CA value o·G is < (1/255)·e^(−1e-3)·(1 + 1e-6),
 // so the CA decision is "skip" as well; the CA exp is only evaluated above this bound.
 constexpr float SKIP_MARGIN = 1e-3f;
-__device__ __forceinline__ float skip_power(float o) { return -logf(255.0f * o) - SKIP_MARGIN; }
 
 // pixel coordinates of this thread's two pixels: warp w covers rows 4w..4w+3
 __device__ __forceinline__ void pixel_pair(int tx, int ty, int& x, int& y0, int& y1) {
@@ -137,19 +136,12 @@ __device__ __forceinline__ int warp_batch_list(const uint8_t* smask, int cnt, in
 }
 
 // ---------------------------------------------------------------------------------------
-// Packed forward (default): the thread's two pixels are the lanes of FP32x2 registers; every
-// CA operation (power, canonical exp, α, T·(1 − α)) is the per-lane RN operation of the
-// scalar kernel, so decisions, T_final and n_contrib are bit-identical to k_render_fwd.
-// A lane that does not blend the entry gets weight 0 and keeps its T.
-struct FwdConsts {
-    float4 xy;   // (x, x, y, y)
-    float4 ab;   // (A, A, −B, −B)
-    float4 cs;   // (C, C, skip bound, skip bound)
-    float4 orr;  // (o, o, r, r)
-    float4 gb;   // (g, g, b, b)
-    float2 dd;   // (depth, depth)
-};
-
+// Packed forward: the thread's two pixels are the lanes of FP32x2 registers; every CA operation
+// (power, canonical exp, α, T·(1 − α)) is the per-lane RN operation of the scalar forms, so
+// decisions, T_final and n_contrib are bit-identical to the canonical arithmetic of §4.  A
+// lane that does not blend the entry gets weight 0 and keeps its T.  A terminated pixel keeps
+// its T with the sign flipped (T > 0 while the pixel is live), so "done" needs no flag
+// register: every test on a live pixel is a test on T's sign.
 __device__ __forceinline__ float2 ff2(float a, float b) { return make_float2(a, b); }
 
 // ca_exp_core per lane, packed, for x ∈ [−87, 0] as the compositing kernels
@@ -180,7 +172,9 @@ __global__ __launch_bounds__(RT) void k_render_fwd_p(Launch L, float* __restrict
                                                      float* __restrict__ out_D) {
     constexpr int FB = RT * MVGS_FWD_BATCH;  // entries per staged batch (≤ 256: uint8 list indices)
     static_assert(FB <= 256, "list indices are bytes");
-    __shared__ FwdConsts sf[FB];
+    // staged entry constants, one array (an entry's three loads share one address):
+    //   (μ'x, μ'y, A, C), (B, o, skip bound, depth), (r, g, b, −)
+    __shared__ float4 se[3][FB];
     __shared__ uint8_t smask[FB];
     __shared__ uint8_t slist[RT / 32][FB];
     __shared__ unsigned sev[2];
@@ -193,9 +187,10 @@ __global__ __launch_bounds__(RT) void k_render_fwd_p(Launch L, float* __restrict
     const int start = L.bucket_off[bucket], end = L.bucket_off[bucket + 1];
     const float2 nfx = ff2(-(float)x, -(float)x), nfy = ff2(-(float)y[0], -(float)y[1]);
     const float2 one = ff2(1.f, 1.f), mone = ff2(-1.f, -1.f), mhalf = ff2(-0.5f, -0.5f);
-    float2 T = one, C0 = ff2(0.f, 0.f), C1 = C0, C2 = C0, D = C0;
+    // T < 0: the pixel is done (terminated, or outside the image)
+    float2 T = ff2((x < L.W && y[0] < L.H) ? 1.f : -1.f, (x < L.W && y[1] < L.H) ? 1.f : -1.f);
+    float2 C0 = ff2(0.f, 0.f), C1 = C0, C2 = C0, D = C0;
     int last0 = 0, last1 = 0;
-    bool done0 = !(x < L.W && y[0] < L.H), done1 = !(x < L.W && y[1] < L.H);
     unsigned nev = 0, nexp = 0;
     if (threadIdx.x == 0) sev[0] = sev[1] = 0;
     __syncthreads();
@@ -204,21 +199,15 @@ __global__ __launch_bounds__(RT) void k_render_fwd_p(Launch L, float* __restrict
     uint32_t qn = (PF && start + (int)threadIdx.x < end) ? L.sorted[start + threadIdx.x] : 0u;
     if (end <= L.cap_entries) {
         for (int b0 = start; b0 < end; b0 += FB) {
-            if (__syncthreads_count(done0 && done1) == RT) break;
+            if (__syncthreads_count(T.x < 0.f && T.y < 0.f) == RT) break;
             for (int t = threadIdx.x; t < FB && b0 + t < end; t += RT) {
                 const int idx = b0 + t;
                 const float4* r = L.rec + 3 * (int64_t)(PF ? qn : L.sorted[idx]);
-                const float4 r0 = r[0], r1 = r[1], r2 = r[2];
-                FwdConsts k;
-                k.xy = make_float4(r0.x, r0.x, r0.y, r0.y);
-                k.ab = make_float4(r0.z, r0.z, -r0.w, -r0.w);
-                const float sb = skip_power(r1.y);
-                k.cs = make_float4(r1.x, r1.x, sb, sb);
-                k.orr = make_float4(r1.y, r1.y, r1.z, r1.z);
-                k.gb = make_float4(r1.w, r1.w, r2.x, r2.x);
-                k.dd = ff2(r2.y, r2.y);
-                sf[t] = k;
-                smask[t] = (uint8_t)warp_block_mask(r0.x, r0.y, r0.z, r0.w, r1.x, sb, (float)(tx * TILE),
+                const float4 r0 = r[0], r1 = r[1], r2 = r[2];  // (x, y, A, B) (C, o, r, g) (b, depth, sb, 1/o)
+                se[0][t] = make_float4(r0.x, r0.y, r0.z, r1.x);
+                se[1][t] = make_float4(r0.w, r1.y, r2.z, r2.y);
+                se[2][t] = make_float4(r1.z, r1.w, r2.x, 0.f);
+                smask[t] = (uint8_t)warp_block_mask(r0.x, r0.y, r0.z, r0.w, r1.x, r2.z, (float)(tx * TILE),
                                                     (float)(ty * TILE));
             }
             __syncthreads();
@@ -231,39 +220,36 @@ __global__ __launch_bounds__(RT) void k_render_fwd_p(Launch L, float* __restrict
                 qn = nidx < end ? L.sorted[nidx] : 0u;
             }
 #pragma unroll(kFwdUnroll)
-            for (int u = 0; u < nl && !(done0 && done1); u++) {
+            for (int u = 0; u < nl && !(T.x < 0.f && T.y < 0.f); u++) {
                 const int j = slist[wl][u];
-                if (CNT) nev += (unsigned)!done0 + (unsigned)!done1;
-                const float4 xy = sf[j].xy, ab = sf[j].ab, cs = sf[j].cs;
-                const float2 dx = __fadd2_rn(ff2(xy.x, xy.y), nfx);
-                const float2 dy = __fadd2_rn(ff2(xy.z, xy.w), nfy);
-                const float2 Adx = __fmul2_rn(ff2(ab.x, ab.y), dx);
-                const float2 CdyDy = __fmul2_rn(__fmul2_rn(ff2(cs.x, cs.y), dy), dy);
+                if (CNT) nev += (unsigned)(T.x > 0.f) + (unsigned)(T.y > 0.f);
+                const float4 e0 = se[0][j], e1 = se[1][j];
+                const float2 dx = __fadd2_rn(ff2(e0.x, e0.x), nfx);
+                const float2 dy = __fadd2_rn(ff2(e0.y, e0.y), nfy);
+                const float2 Adx = __fmul2_rn(ff2(e0.z, e0.z), dx);
+                const float2 CdyDy = __fmul2_rn(__fmul2_rn(ff2(e0.w, e0.w), dy), dy);
                 const float2 inner = __ffma2_rn(Adx, dx, CdyDy);
-                const float2 nBdxdy = __fmul2_rn(__fmul2_rn(ff2(ab.z, ab.w), dx), dy);
+                const float2 nBdxdy = __fmul2_rn(__fmul2_rn(ff2(-e1.x, -e1.x), dx), dy);
                 const float2 power = __ffma2_rn(mhalf, inner, nBdxdy);
-                const bool in0 = !done0 && !(power.x > 0.f) && !(power.x < cs.z);
-                const bool in1 = !done1 && !(power.y > 0.f) && !(power.y < cs.z);
+                const bool in0 = T.x > 0.f && !(power.x > 0.f) && !(power.x < e1.z);
+                const bool in1 = T.y > 0.f && !(power.y > 0.f) && !(power.y < e1.z);
                 if (!(in0 || in1)) continue;
                 if (CNT) nexp += (unsigned)in0 + (unsigned)in1;
-                const float4 orr = sf[j].orr;
                 const float2 G = ca_exp_core2(power);
-                const float2 oG = __fmul2_rn(ff2(orr.x, orr.y), G);
+                const float2 oG = __fmul2_rn(ff2(e1.y, e1.y), G);
                 const float2 alpha = ff2(fminf(ALPHA_MAX, oG.x), fminf(ALPHA_MAX, oG.y));
                 const bool ok0 = in0 && !(alpha.x < ALPHA_MIN), ok1 = in1 && !(alpha.y < ALPHA_MIN);
                 if (!(ok0 || ok1)) continue;
                 const float2 Tn = __fmul2_rn(T, __ffma2_rn(alpha, mone, one));  // T·(1 − α), CA
                 const bool term0 = ok0 && Tn.x < T_EPS, term1 = ok1 && Tn.y < T_EPS;
                 const bool bl0 = ok0 && !term0, bl1 = ok1 && !term1;
-                done0 |= term0;
-                done1 |= term1;
                 const float2 w = __fmul2_rn(ff2(bl0 ? alpha.x : 0.f, bl1 ? alpha.y : 0.f), T);
-                const float4 gb = sf[j].gb;
-                C0 = __ffma2_rn(ff2(orr.z, orr.w), w, C0);
-                C1 = __ffma2_rn(ff2(gb.x, gb.y), w, C1);
-                C2 = __ffma2_rn(ff2(gb.z, gb.w), w, C2);
-                if (DEPTH) D = __ffma2_rn(sf[j].dd, w, D);
-                T = ff2(bl0 ? Tn.x : T.x, bl1 ? Tn.y : T.y);
+                const float4 e2 = se[2][j];
+                C0 = __ffma2_rn(ff2(e2.x, e2.x), w, C0);
+                C1 = __ffma2_rn(ff2(e2.y, e2.y), w, C1);
+                C2 = __ffma2_rn(ff2(e2.z, e2.z), w, C2);
+                if (DEPTH) D = __ffma2_rn(ff2(e1.w, e1.w), w, D);
+                T = ff2(bl0 ? Tn.x : (term0 ? -T.x : T.x), bl1 ? Tn.y : (term1 ? -T.y : T.y));
                 const int jn = jbase + j;
                 last0 = bl0 ? jn : last0;
                 last1 = bl1 ? jn : last1;
@@ -278,7 +264,7 @@ __global__ __launch_bounds__(RT) void k_render_fwd_p(Launch L, float* __restrict
     if (CNT) count_evals(&L.counters64[0], &L.counters64[2], nev, nexp, sev);
     const int64_t HW = (int64_t)L.H * L.W;
     const float Cs[2][3] = {{C0.x, C1.x, C2.x}, {C0.y, C1.y, C2.y}};
-    const float Ts[2] = {T.x, T.y}, Ds[2] = {D.x, D.y};
+    const float Ts[2] = {fabsf(T.x), fabsf(T.y)}, Ds[2] = {D.x, D.y};
     const int ls[2] = {last0, last1};
 #pragma unroll
     for (int p = 0; p < 2; p++) {
@@ -306,22 +292,40 @@ cudaError_t launch_render_fwd(const Launch& L, float* rgb, float* Tf, int32_t* n
 // Transpose-reduce of 10 per-lane values over a warp.  Level l (xor 16, 8, 4,
 // 2, 1) halves the number of values each lane carries; the lane keeps the
 // half selected by its bit and receives the partner's copy of that half.
-// Returns the warp sum of value `id` (id computed once by reduce_id).
-__device__ __forceinline__ float warp_transpose_reduce10(const float (&v)[NG], int lane) {
-    const bool b16 = lane & 16, b8 = lane & 8, b4 = lane & 4, b2 = lane & 2;
+// Returns the warp sum of value `id` (id computed once by reduce_id).  The
+// keep/send choices are byte permutes driven by per-lane selector registers
+// (sel: 0x3210 keeps the first operand, 0x7654 the second), computed once, so
+// no predicate register has to stay live across the entry loop.
+__device__ __forceinline__ float psel(float a, float b, uint32_t sel) {  // sel ? … : byte-permute select
+    uint32_t d;
+    asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(__float_as_uint(a)), "r"(__float_as_uint(b)), "r"(sel));
+    return __uint_as_float(d);
+}
+struct RedSel {
+    uint32_t s16, s8, s4, s2;  // 0x7654 where the lane's bit is set (takes the second operand), else 0x3210
+};
+__device__ __forceinline__ RedSel red_sel(int lane) {
+    RedSel r;
+    r.s16 = (lane & 16) ? 0x7654u : 0x3210u;
+    r.s8 = (lane & 8) ? 0x7654u : 0x3210u;
+    r.s4 = (lane & 4) ? 0x7654u : 0x3210u;
+    r.s2 = (lane & 2) ? 0x7654u : 0x3210u;
+    return r;
+}
+__device__ __forceinline__ float warp_transpose_reduce10(const float (&v)[NG], const RedSel& rs) {
     float u[5];
 #pragma unroll
     for (int k = 0; k < 5; k++) {
-        const float keep = b16 ? v[k + 5] : v[k];
-        const float send = b16 ? v[k] : v[k + 5];
+        const float keep = psel(v[k], v[k + 5], rs.s16);
+        const float send = psel(v[k + 5], v[k], rs.s16);
         u[k] = keep + __shfl_xor_sync(FULLR, send, 16);
     }
-    float w0 = (b8 ? u[2] : u[0]) + __shfl_xor_sync(FULLR, b8 ? u[0] : u[2], 8);
-    float w1 = (b8 ? u[3] : u[1]) + __shfl_xor_sync(FULLR, b8 ? u[1] : u[3], 8);
+    float w0 = psel(u[0], u[2], rs.s8) + __shfl_xor_sync(FULLR, psel(u[2], u[0], rs.s8), 8);
+    float w1 = psel(u[1], u[3], rs.s8) + __shfl_xor_sync(FULLR, psel(u[3], u[1], rs.s8), 8);
     float w2 = u[4] + __shfl_xor_sync(FULLR, u[4], 8);
-    float x0 = (b4 ? w1 : w0) + __shfl_xor_sync(FULLR, b4 ? w0 : w1, 4);
+    float x0 = psel(w0, w1, rs.s4) + __shfl_xor_sync(FULLR, psel(w1, w0, rs.s4), 4);
     float x1 = w2 + __shfl_xor_sync(FULLR, w2, 4);
-    float y = (b2 ? x1 : x0) + __shfl_xor_sync(FULLR, b2 ? x0 : x1, 2);
+    float y = psel(x0, x1, rs.s2) + __shfl_xor_sync(FULLR, psel(x1, x0, rs.s2), 2);
     y += __shfl_xor_sync(FULLR, y, 1);
     return y;
 }
@@ -355,14 +359,6 @@ __device__ __forceinline__ int reduce_id(int lane) {
 // ∂r, ∂g, ∂b; the thread adds its two pixels', the warp transpose-reduces them (12 shuffles),
 // the owner lane scales and stores its value in the warp's slot, and after the batch the four
 // warp slots are summed in fixed order and flushed with one red.add per nonzero value.
-struct BwdConsts {
-    float4 xy;   // (x, x, y, y)
-    float4 ac;   // (A, A, C, C)
-    float4 bo;   // (B, B, o, o)
-    float4 rg;   // (r, r, g, g)
-    float4 bs;   // (b, b, skip bound, −)
-};
-
 __device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
 __device__ __forceinline__ float sqrt_approx(float x) {
     float y;
@@ -375,15 +371,18 @@ __device__ __forceinline__ float rcp_approx(float x) {
     return y;
 }
 
+// Staged per-entry constants of the backward: three float4 loads per (warp, entry); every
+// packed operation takes the entry's scalars as broadcast operands.
+//   e0 = (μ'x, μ'y, A, C), e1 = (B, o, skip bound, 1/o), e2 = (r, g, b, −)
 template <bool CNT>
 __global__ __launch_bounds__(128, MVGS_BWD_MINB) void k_render_bwd_p(Launch L, const float* __restrict__ dL_drgb,
                                                       const float* __restrict__ in_T,
                                                       const int32_t* __restrict__ in_n) {
     constexpr int NW = 4, RB = 128;
-    __shared__ BwdConsts sc[RB];
+    __shared__ float4 se[3][RB];  // one array: the three loads of an entry share its address (immediate offsets)
     __shared__ uint32_t sq[RB];
-    __shared__ float sio[RB];  // 1/o: slot 6 is reduced as o·∂L/∂o
     __shared__ __align__(16) float sacc[NW][RB * NG];
+    __shared__ float skscale[NG];
     __shared__ int smax;
     __shared__ unsigned sev[2];
     __shared__ uint8_t smask[RB];
@@ -419,9 +418,17 @@ __global__ __launch_bounds__(128, MVGS_BWD_MINB) void k_render_bwd_p(Launch L, c
     float2 nB = f2(-Tfin[0] * (L.bg[0] * dL[0][0] + L.bg[1] * dL[0][1] + L.bg[2] * dL[0][2]),
                    -Tfin[1] * (L.bg[0] * dL[1][0] + L.bg[1] * dL[1][1] + L.bg[2] * dL[1][2]));
     const int mylast = max(last[0], last[1]);
+    const float hw = 0.5f * (float)L.W, hh = 0.5f * (float)L.H;
     if (threadIdx.x == 0) {
         smax = 0;
         sev[0] = sev[1] = 0;
+    }
+    // per-value scale applied at the flush: Σ∇ = −(W/2, H/2)·(A d + B e, C e + B d) with
+    // d, e = ∂L/∂power·(dx, dy); ∂A = −½Σ d·dx, ∂B = −Σ d·dy, ∂C = −½Σ e·dy; the colour terms
+    // were accumulated with −w; slot 6 (o·∂L/∂o) is scaled by the entry's 1/o
+    if (threadIdx.x < NG) {
+        const int k = threadIdx.x;
+        skscale[k] = k == 0 ? -hw : k == 1 ? -hh : (k == 3 || k == 5) ? -0.5f : (k == 4 || k >= 7) ? -1.f : 1.f;
     }
     __syncthreads();
     unsigned nev = 0, nexp = 0, nbl0 = 0, nbl1 = 0;
@@ -431,13 +438,12 @@ __global__ __launch_bounds__(128, MVGS_BWD_MINB) void k_render_bwd_p(Launch L, c
     const int wmax = __reduce_max_sync(FULLR, mylast);
     const int my_id = reduce_id(lane);
     const bool owner = (__ffs(__match_any_sync(FULLR, my_id)) - 1) == lane;
-    const float hw = 0.5f * (float)L.W, hh = 0.5f * (float)L.H;
-    // per-value scale applied by the owner after the reduction: Σ∇ = −(W/2, H/2)·(A d + B e,
-    // C e + B d) with d, e = ∂L/∂power·(dx, dy); ∂A = −½Σ d·dx, ∂B = −Σ d·dy, ∂C = −½Σ e·dy;
-    // the colour terms were accumulated with −w; slot 6 (o·∂L/∂o) is scaled by 1/o at the flush
-    const float oscale = my_id == 0 ? -hw : my_id == 1 ? -hh : (my_id == 3 || my_id == 5) ? -0.5f
-                       : (my_id == 4 || my_id >= 7) ? -1.f : 1.f;
-    float* wacc = sacc[warp];
+    const RedSel rsel = red_sel(lane);
+    // this lane's value of entry jj goes to sacc[warp][jj·NG + my_id]; non-owners (the same sum
+    // held by several lanes) write to a dummy word, so the store needs no predicate
+    __shared__ float sdummy[NW * 32];
+    float* wslot = owner ? &sacc[warp][my_id] : &sdummy[threadIdx.x];
+    const int wstride = owner ? NG : 0;
     const float2 nfx = f2(-(float)x, -(float)x), nfy = f2(-(float)y0, -(float)(y0 + 2));
     const float2 mhalf = f2(-0.5f, -0.5f);
     const float2 hw2 = f2(hw * hw, hw * hw), hh2 = f2(hh * hh, hh * hh);
@@ -450,20 +456,14 @@ __global__ __launch_bounds__(128, MVGS_BWD_MINB) void k_render_bwd_p(Launch L, c
             const uint32_t q = L.sorted[start + b0 + t];
             sq[t] = q;
             const float4* r = L.rec + 3 * (int64_t)q;
-            const float4 r0 = r[0], r1 = r[1], r2 = r[2];
-            BwdConsts k;
-            k.xy = make_float4(r0.x, r0.x, r0.y, r0.y);
-            k.ac = make_float4(r0.z, r0.z, r1.x, r1.x);
-            k.bo = make_float4(r0.w, r0.w, r1.y, r1.y);
-            k.rg = make_float4(r1.z, r1.z, r1.w, r1.w);
-            const float sb = skip_power(r1.y);
-            k.bs = make_float4(r2.x, r2.x, sb, 0.f);
-            sc[t] = k;
-            sio[t] = 1.0f / r1.y;
-            smask[t] = (uint8_t)warp_block_mask(r0.x, r0.y, r0.z, r0.w, r1.x, sb, (float)(tx * TILE), (float)(ty * TILE));
+            const float4 r0 = r[0], r1 = r[1], r2 = r[2];  // (x, y, A, B) (C, o, r, g) (b, depth, sb, 1/o)
+            se[0][t] = make_float4(r0.x, r0.y, r0.z, r1.x);
+            se[1][t] = make_float4(r0.w, r1.y, r2.z, r2.w);
+            se[2][t] = make_float4(r1.z, r1.w, r2.x, 0.f);
+            smask[t] = (uint8_t)warp_block_mask(r0.x, r0.y, r0.z, r0.w, r1.x, r2.z, (float)(tx * TILE), (float)(ty * TILE));
         }
         {
-            float4* w4 = reinterpret_cast<float4*>(wacc);
+            float4* w4 = reinterpret_cast<float4*>(sacc[warp]);
             for (int i = lane; i < RB * NG / 4; i += 32) w4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
         }
         __syncthreads();
@@ -473,23 +473,24 @@ __global__ __launch_bounds__(128, MVGS_BWD_MINB) void k_render_bwd_p(Launch L, c
             const int jj = slist[warp][u];
             const int j = b0 + jj;
             if (CNT) nev += (unsigned)(j < last[0]) + (unsigned)(j < last[1]);
-            const float4 xy = sc[jj].xy, ac = sc[jj].ac, bo = sc[jj].bo;
-            const float sb = sc[jj].bs.z;
-            const float2 dx = __fadd2_rn(f2(xy.x, xy.y), nfx);
-            const float2 dy = __fadd2_rn(f2(xy.z, xy.w), nfy);
+            const float4 e0 = se[0][jj], e1 = se[1][jj];
+            const float2 dx = __fadd2_rn(f2(e0.x, e0.x), nfx);
+            const float2 dy = __fadd2_rn(f2(e0.y, e0.y), nfy);
             // ca_power per lane: FMA(−0.5, FMA(A·dx, dx, (C·dy)·dy), −(B·dx)·dy)
-            const float2 A2 = f2(ac.x, ac.y), C2 = f2(ac.z, ac.w), B2 = f2(bo.x, bo.y);
+            const float2 A2 = f2(e0.z, e0.z), C2 = f2(e0.w, e0.w), B2 = f2(e1.x, e1.x);
             const float2 inner = __ffma2_rn(__fmul2_rn(A2, dx), dx, __fmul2_rn(__fmul2_rn(C2, dy), dy));
             const float2 Bdd = __fmul2_rn(__fmul2_rn(B2, dx), dy);
             const float2 power = __ffma2_rn(mhalf, inner, f2(-Bdd.x, -Bdd.y));
+            const float sb = e1.z;
             const bool in0 = j < last[0] && !(power.x > 0.f) && !(power.x < sb);
             const bool in1 = j < last[1] && !(power.y > 0.f) && !(power.y < sb);
             if (!__any_sync(FULLR, in0 || in1)) continue;
             if (CNT) nexp += (unsigned)in0 + (unsigned)in1;
             const float2 G = ca_exp_core2(power);
-            const float2 oG = __fmul2_rn(f2(bo.z, bo.w), G);
-            const bool bl0 = in0 && !(fminf(ALPHA_MAX, oG.x) < ALPHA_MIN);
-            const bool bl1 = in1 && !(fminf(ALPHA_MAX, oG.y) < ALPHA_MIN);
+            const float2 oG = __fmul2_rn(f2(e1.y, e1.y), G);
+            // α = min(0.99, o·G) < 1/255 ⇔ o·G < 1/255
+            const bool bl0 = in0 && !(oG.x < ALPHA_MIN);
+            const bool bl1 = in1 && !(oG.y < ALPHA_MIN);
             if (!__any_sync(FULLR, bl0 || bl1)) continue;
             if (CNT) {
                 nbl0 += bl0;
@@ -497,14 +498,14 @@ __global__ __launch_bounds__(128, MVGS_BWD_MINB) void k_render_bwd_p(Launch L, c
             }
             const float2 alpha = f2(bl0 ? fminf(ALPHA_MAX, oG.x) : 0.f, bl1 ? fminf(ALPHA_MAX, oG.y) : 0.f);
             // o·G where it has a gradient: zero where clamped (α = 0.99 has zero gradient, R11)
-            const float2 oGc = f2(bl0 && !(oG.x > ALPHA_MAX) ? oG.x : 0.f, bl1 && !(oG.y > ALPHA_MAX) ? oG.y : 0.f);
+            const float2 oGc = f2(oG.x > ALPHA_MAX ? 0.f : alpha.x, oG.y > ALPHA_MAX ? 0.f : alpha.y);
             const float2 om = __ffma2_rn(alpha, f2(-1.f, -1.f), f2(1.f, 1.f));
             const float2 inv = f2(rcp_approx(om.x), rcp_approx(om.y));
             T = __fmul2_rn(T, inv);
             const float2 nw = __fmul2_rn(alpha, f2(-T.x, -T.y));  // −α·T
-            const float4 rg = sc[jj].rg;
-            const float2 bb = f2(sc[jj].bs.x, sc[jj].bs.y);
-            const float2 cdL = __ffma2_rn(bb, dLb, __ffma2_rn(f2(rg.z, rg.w), dLg, __fmul2_rn(f2(rg.x, rg.y), dLr)));
+            const float4 e2 = se[2][jj];
+            const float2 cdL = __ffma2_rn(f2(e2.z, e2.z), dLb,
+                                          __ffma2_rn(f2(e2.y, e2.y), dLg, __fmul2_rn(f2(e2.x, e2.x), dLr)));
             const float2 dLda = __ffma2_rn(nB, inv, __fmul2_rn(T, cdL));
             nB = __ffma2_rn(cdL, nw, nB);
             const float2 dLdpw = __fmul2_rn(oGc, dLda);  // ∂L/∂power = o·G·∂L/∂α
@@ -525,8 +526,7 @@ __global__ __launch_bounds__(128, MVGS_BWD_MINB) void k_render_bwd_p(Launch L, c
             val[7] = wr.x + wr.y;
             val[8] = wg.x + wg.y;
             val[9] = wb.x + wb.y;
-            const float sum = warp_transpose_reduce10(val, lane);
-            if (owner) wacc[jj * NG + my_id] = sum * oscale;
+            wslot[jj * wstride] = warp_transpose_reduce10(val, rsel);
         }
         __syncthreads();
         for (int i = threadIdx.x; i < cnt * NG; i += 128) {
@@ -535,7 +535,7 @@ __global__ __launch_bounds__(128, MVGS_BWD_MINB) void k_render_bwd_p(Launch L, c
             for (int w = 0; w < NW; w++) s += sacc[w][i];
             if (s != 0.f) {
                 const int jj = i / NG, k = i - jj * NG;
-                if (k == 6) s *= sio[jj];
+                s *= k == 6 ? se[1][jj].w : skscale[k];
                 atomicAdd(&L.pgrad[(int64_t)sq[jj] * PG_STRIDE + k], s);
             }
         }
