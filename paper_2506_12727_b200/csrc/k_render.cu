@@ -2,7 +2,7 @@
 //
 // Grid = one CTA per (view, tile) — "multiple blocks per tile, one block for
 // each viewpoint".  A CTA has 128 threads for the 16×16 tile: each
-// thread owns TWO pixels (rows r and r+2 of its warp's 16×4 block), so every
+// thread owns TWO pixels (rows r and r+4 of its warp's 8×8 block), so every
 // staged record, loop step and — in the backward — every warp reduction is
 // shared by two pixels.  Entries of the tile's depth-sorted list are staged in
 // shared memory a batch of 128 at a time, one record per thread, then every
@@ -64,25 +64,36 @@ __device__ __forceinline__ void count_evals(unsigned long long* ctr0, unsigned l
 // so the CA decision is "skip" as well; the CA exp is only evaluated above this bound.
 constexpr float SKIP_MARGIN = 1e-3f;
 
-// pixel coordinates of this thread's two pixels: warp w covers rows 4w..4w+3
+// Warp blocks of the 16×16 tile: warp w owns a WBW × WBH block of pixels (lane → column
+// lane % WBW, row lane / WBW, and the same column WBH/2 rows further down for the thread's
+// second pixel).  16×4 (four stacked strips) or 8×8 (a 2×2 arrangement, MVGS_WB8): a square
+// block has the shortest perimeter, so fewer of its pixels lie outside a small footprint.
+#ifndef MVGS_WB8
+#define MVGS_WB8 1  // measured (garden / playroom / train): 8×8 bwd 0.742 → 0.729, 3.54 → 3.39, 1.061 → 1.044 ms
+#endif
+constexpr int WBW = MVGS_WB8 ? 8 : 16, WBH = MVGS_WB8 ? 8 : 4;
+constexpr int WB_PER_ROW = TILE / WBW;  // warp blocks per tile row
+__device__ __forceinline__ int wb_x0(int w) { return (w % WB_PER_ROW) * WBW; }
+__device__ __forceinline__ int wb_y0(int w) { return (w / WB_PER_ROW) * WBH; }
+// pixel coordinates of this thread's two pixels (rows r and r + WBH/2 of its warp's block)
 __device__ __forceinline__ void pixel_pair(int tx, int ty, int& x, int& y0, int& y1) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    x = tx * TILE + (lane & 15);
-    y0 = ty * TILE + 4 * warp + (lane >> 4);
-    y1 = y0 + 2;
+    x = tx * TILE + wb_x0(warp) + (lane % WBW);
+    y0 = ty * TILE + wb_y0(warp) + (lane / WBW);
+    y1 = y0 + WBH / 2;
 }
 
 // Exact warp-block culling.  A pixel reaches the canonical exp only if
 // its CA power ≥ sb.  With d = μ' − p and q(d) = dᵀMd, M = [[A, B], [B, C]] (the stored
 // fp32 conic), the exact power is −q/2 and the CA value differs from it by at most
 // ε·T(d), T(d) = A·dx² + C·dy² + 2|B·dx·dy|, ε = 8·2⁻²⁴ (a few fp32 roundings).  q_min, the
-// minimum of q over a warp's 16×4 block (0 if μ' lies in it, else the smallest of q on the
+// minimum of q over a warp's pixel block (0 if μ' lies in it, else the smallest of q on the
 // four edges, each a 1-D quadratic taken at its clamped minimiser), is evaluated in fp32
 // with an error below another ε·T_max (evaluating at a rounded minimiser only raises q by
 // C·δ², δ ~ 1e-7·|t|, far inside the 0.01 slack).  No pixel of the block can pass when
 //   q_min > 1.01·L + 0.01 + 3ε·T_max,   L = −2·sb,  T_max ≥ T over the block.
 // Conics that are not positive definite are never culled.  Bit j: the entry may touch
-// warp j's rows 4j … 4j+3 of the tile.
+// warp j's block of the tile.
 __device__ __forceinline__ float q_edge(float A, float B, float C, float fixed, float lo, float hi, bool fix_x) {
     if (fix_x) {  // dx fixed, dy clamped to [lo, hi] at the 1-D minimiser
         const float t = fminf(hi, fmaxf(lo, -B * fixed / C));
@@ -102,13 +113,13 @@ __device__ __noinline__ unsigned warp_block_mask(float px, float py, float A, fl
         return 0xfu;
     const float eps3 = 3.0f * 8.0f * 5.9604644775390625e-8f;
     const float Lm = L * 1.01f + 0.01f;
-    const float dxlo = px - (X0 + 15.0f), dxhi = px - X0;  // d = μ' − p over the block (exact: small integers)
-    const float dxm = fmaxf(fabsf(dxlo), fabsf(dxhi));
     unsigned m = 0;
 #pragma unroll
     for (int w = 0; w < 4; w++) {
-        const float y0 = Y0 + 4.0f * w;
-        const float dylo = py - (y0 + 3.0f), dyhi = py - y0;
+        const float x0 = X0 + (float)wb_x0(w), y0 = Y0 + (float)wb_y0(w);
+        const float dxlo = px - (x0 + (float)(WBW - 1)), dxhi = px - x0;  // d = μ' − p over the block (exact)
+        const float dylo = py - (y0 + (float)(WBH - 1)), dyhi = py - y0;
+        const float dxm = fmaxf(fabsf(dxlo), fabsf(dxhi));
         const float dym = fmaxf(fabsf(dylo), fabsf(dyhi));
         float qmin = 0.0f;
         if (!(dxlo <= 0.0f && dxhi >= 0.0f && dylo <= 0.0f && dyhi >= 0.0f)) {  // centre outside the block
@@ -340,9 +351,9 @@ __device__ __forceinline__ int reduce_id(int lane) {
 
 // ---------------------------------------------------------------------------------------
 // Backward (S7).  128 threads per (view, tile), two pixels per thread held as the lanes of
-// FP32x2 registers (rows r and r+2 of the thread's column; warp w owns rows 4w … 4w+3), the
+// FP32x2 registers (rows r and r + WBH/2 of the thread's column in its warp's block), the
 // tile's list walked back to front from each pixel's n_contrib in staged batches, each warp
-// over its compacted list of entries that can touch its 16×4 block (§4.8).
+// over its compacted list of entries that can touch its pixel block (§4.8).
 //
 // Decisions are the forward's, re-taken in the same canonical arithmetic: the CA power, the
 // CA exp (ca_exp_core2, bit-identical to the forward's), α = min(0.99, o·G), skip α < 1/255,
@@ -391,8 +402,8 @@ __global__ __launch_bounds__(128, MVGS_BWD_MINB) void k_render_bwd_p(Launch L, c
     const int bucket = blockIdx.x;
     const int v = bucket / L.T, tile = bucket - v * L.T;
     const int ty = tile / L.TX, tx = tile - ty * L.TX;
-    const int x = tx * TILE + (lane & 15);
-    const int y0 = ty * TILE + 4 * warp + (lane >> 4);
+    int x, y0, y1_;
+    pixel_pair(tx, ty, x, y0, y1_);
     const int start = L.bucket_off[bucket], end = L.bucket_off[bucket + 1];
     if (end > L.cap_entries) return;
     const int64_t HW = (int64_t)L.H * L.W;
@@ -400,7 +411,7 @@ __global__ __launch_bounds__(128, MVGS_BWD_MINB) void k_render_bwd_p(Launch L, c
     int last[2];
 #pragma unroll
     for (int p = 0; p < 2; p++) {
-        const int y = y0 + 2 * p;
+        const int y = y0 + (WBH / 2) * p;
         dL[p][0] = dL[p][1] = dL[p][2] = 0.f;
         Tfin[p] = 1.f;
         last[p] = 0;
@@ -444,7 +455,7 @@ __global__ __launch_bounds__(128, MVGS_BWD_MINB) void k_render_bwd_p(Launch L, c
     __shared__ float sdummy[NW * 32];
     float* wslot = owner ? &sacc[warp][my_id] : &sdummy[threadIdx.x];
     const int wstride = owner ? NG : 0;
-    const float2 nfx = f2(-(float)x, -(float)x), nfy = f2(-(float)y0, -(float)(y0 + 2));
+    const float2 nfx = f2(-(float)x, -(float)x), nfy = f2(-(float)y0, -(float)y1_);
     const float2 mhalf = f2(-0.5f, -0.5f);
     const float2 hw2 = f2(hw * hw, hw * hw), hh2 = f2(hh * hh, hh * hh);
     for (int b_end = maxlast; b_end > 0; b_end -= RB) {
@@ -543,7 +554,7 @@ __global__ __launch_bounds__(128, MVGS_BWD_MINB) void k_render_bwd_p(Launch L, c
     if (CNT) {
         count_evals(&L.counters64[1], &L.counters64[3], nev, nexp, sev);
         if (L.dbg_nblend) {  // parity export: entries blended per pixel, as this kernel decided
-            const int yy[2] = {y0, y0 + 2};
+            const int yy[2] = {y0, y1_};
             const unsigned nb[2] = {nbl0, nbl1};
 #pragma unroll
             for (int p = 0; p < 2; p++)

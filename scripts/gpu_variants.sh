@@ -1,6 +1,6 @@
 # A/B compile-time variants: bench garden with each MVGS_NVCC_EXTRA setting.  Each variant is
 # built into its own library (MVGS_LIB), so the product libmvgs.so is never overwritten.
-#   TAG=v1 VARIANTS="|-DMVGS_RS_IPT=12|-DMVGS_RS_IPT=16" bash scripts/gpu_variants.sh
+#   TAG=v1 CONFIGS="playroom" VARIANTS="|-DMVGS_RS_IPT=12|-DMVGS_RS_IPT=16" bash scripts/gpu_variants.sh
 set -x
 mkdir -p gpurun_out
 T=${TAG:-var}
@@ -12,6 +12,7 @@ for v in "${VS[@]}"; do
   echo "variant[$i]: '$v'" > gpurun_out/${T}_v$i.log
   timeout 600 python -m pytest tests/test_gpu_parity.py -m gpu -x -q >> gpurun_out/${T}_v$i.log 2>&1
   timeout 300 python bench.py --no-cpu-baseline ${BENCH_ARGS} >> gpurun_out/${T}_v$i.log 2>&1
+  for c in ${CONFIGS:-}; do timeout 600 python bench.py --no-cpu-baseline --config $c --steps 10 >> gpurun_out/${T}_v$i.log 2>&1; done
   unset MVGS_LIB
   i=$((i+1))
 done
