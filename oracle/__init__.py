@@ -67,7 +67,7 @@ def lib():
         L.oracle_get_nblend.argtypes = [vp, vp]
         L.oracle_decision_hash.restype = C.c_uint64
         L.oracle_decision_hash.argtypes = [vp]
-        for name, n in [("oracle_get_image", 3), ("oracle_get_lists", 2), ("oracle_get_pairs", 3),
+        for name, n in [("oracle_get_image", 3), ("oracle_get_image32", 3), ("oracle_get_lists", 2), ("oracle_get_pairs", 3),
                         ("oracle_get_opacity32", 1), ("oracle_get_pair_grads", 1), ("oracle_get_grads", 9)]:
             getattr(L, name).argtypes = [vp] + [vp] * n
         L.oracle_ca_exp.restype = C.c_float
@@ -187,6 +187,15 @@ class Oracle:
         nc = np.zeros((self.V, self.H, self.W), np.int32)
         lib().oracle_get_image(self._h, _p(rgb), _p(Tf), _p(nc))
         return dict(rgb=rgb, T_final=Tf, n_contrib=nc)
+
+    def image32(self):
+        """The last forward's image / T_final in fp32 canonical arithmetic: the
+        decision chain's T and α, C = fma(rgb32, α·T, C) in list order, out = fma(T, bg, C)."""
+        rgb = np.zeros((self.V, 3, self.H, self.W), np.float32)
+        Tf = np.zeros((self.V, self.H, self.W), np.float32)
+        x = np.zeros((self.V, 3, self.H, self.W))
+        lib().oracle_get_image32(self._h, _p(rgb), _p(Tf), _p(x))
+        return dict(rgb=rgb, T_final=Tf, rgb_x=x)
 
     def nblend(self):
         """Blended entries per pixel [V,H,W] of the last forward."""

@@ -198,7 +198,7 @@ static void project32(const float mu[3], const float Sig[6], const og_cam *c, p3
  * dir = (μ − c_v)/‖μ − c_v‖ with c_v = −R_vᵀ t_v; real SH basis in [3DGS] order,
  * each Y_k one fixed sequence of fp32 products/differences; acc = 0.5 then
  * acc = fma(Y_k, sh_k, acc) for k ascending.  clamped[ch] = acc < 0.            */
-static void color32(const og_scene *g, int64_t i, const og_cam *c, int clamped[3])
+static void color32(const og_scene *g, int64_t i, const og_cam *c, int clamped[3], float rgb32[3])
 {
     const float *R = c->R, *mu = g->means + 3 * i;
     float cp[3];
@@ -231,6 +231,7 @@ static void color32(const og_scene *g, int64_t i, const og_cam *c, int clamped[3
         float acc = 0.5f;
         for (int k = 0; k < nk; k++) acc = fmaf(Y[k], sh[3 * k + ch], acc);
         clamped[ch] = acc < 0.0f;
+        rgb32[ch] = clamped[ch] ? 0.0f : acc;
     }
 }
 
@@ -315,6 +316,7 @@ typedef struct { /* per (Gaussian, view) fp64 projection state (O2) */
     double dir[3], dnorm;  /* normalised μ − camera centre and ‖μ − c‖      */
     double rgb[3];
     int rgb_clamped[3];
+    float rgb32[3];        /* the colour in fp32 CA (the clamp decision's value)  */
 } p64_t;
 
 static void project64(const og_scene *g, int64_t i, const g64_t *a, const og_cam *cam, p64_t *p)
@@ -367,7 +369,7 @@ static void project64(const og_scene *g, int64_t i, const g64_t *a, const og_cam
     sh_basis(p->dir, Y, dY);
     int nk = (g->sh_degree + 1) * (g->sh_degree + 1);
     const float *sh = g->sh + (size_t)i * g->sh_stride * 3;
-    color32(g, i, cam, p->rgb_clamped); /* the clamp is a decision: fp32 CA (R17) */
+    color32(g, i, cam, p->rgb_clamped, p->rgb32); /* the clamp is a decision: fp32 CA (R17) */
     for (int ch = 0; ch < 3; ch++) {
         double v = 0.5;
         for (int k = 0; k < nk; k++) v += Y[k] * sh[3 * k + ch];
@@ -428,6 +430,7 @@ typedef struct {
     const og_cam *cams;
     int V, flags;
     double bg[3];
+    float bg32[3];
     int W, H, TX, TY, T;
     /* per (view, gid) */
     p32_t *p32;            /* [V*P]                                          */
@@ -441,6 +444,8 @@ typedef struct {
     int64_t K;
     /* forward */
     double *img, *Tfin;    /* [V,3,H,W], [V,H,W]                             */
+    float *img32, *Tfin32; /* the same in fp32 canonical arithmetic */
+    double *imgx;          /* experiment: fp64 value chain driven by the fp32 alphas */
     double *dep;           /* [V,H,W] alpha-weighted expected depth (NEXT-2)  */
     int32_t *ncon;         /* [V,H,W]                                        */
     int32_t *nbl;          /* [V,H,W] number of blended entries per pixel    */
@@ -476,6 +481,7 @@ void oracle_destroy(oracle_t *h)
     free(h->p32); free(h->o32); free(h->g64); free(h->p64); free(h->p64i); free(h->off); free(h->gid);
     free(h->mask);
     free(h->img); free(h->Tfin); free(h->ncon); free(h->nbl); free(h->pg); free(h->dep);
+    free(h->img32); free(h->Tfin32); free(h->imgx);
     free(h->d_means); free(h->d_ls); free(h->d_q); free(h->d_op); free(h->d_sh);
     free(h->e1); free(h->e2); free(h->eold); free(h->vis);
     free(h);
@@ -521,6 +527,7 @@ oracle_t *oracle_create_masked(const og_scene *g, const og_cam *cams, int V, con
     h->V = V;
     h->flags = flags;
     for (int k = 0; k < 3; k++) h->bg[k] = bg ? bg[k] : 0.0;
+    for (int k = 0; k < 3; k++) h->bg32[k] = bg ? bg[k] : 0.0f;
     h->W = cams[0].width;
     h->H = cams[0].height;
     h->TX = (h->W + 15) / 16;
@@ -628,8 +635,9 @@ static void composite(oracle_t *h, const float *dLdC)
                 int64_t b = (int64_t)v * h->T + (y / 16) * h->TX + (x / 16);
                 if (h->mask && !h->mask[b]) continue;
                 /* ---- O5: forward.  Decisions fp32 (CA), values fp64. */
-                float T32 = 1.0f;
+                float T32 = 1.0f, C32[3] = {0.0f, 0.0f, 0.0f};
                 double T64 = 1.0, Cc[3] = {0, 0, 0}, Dd = 0.0;
+                double Tx = 1.0, Cx[3] = {0, 0, 0};
                 int last = 0, m = 0;
                 const float fxp = (float)x, fyp = (float)y;
                 for (int64_t j = h->off[b]; j < h->off[b + 1]; j++) {
@@ -665,6 +673,12 @@ static void composite(oracle_t *h, const float *dLdC)
                     bl[m].dy = ddy;
                     m++;
                     T64 *= (1.0 - a64);
+                    {   /* the same blend in fp32 CA: C = fma(rgb, α·T, C) */
+                        const float w = alpha * T32;
+                        for (int ch = 0; ch < 3; ch++) C32[ch] = fmaf(q->rgb32[ch], w, C32[ch]);
+                    }
+                    for (int ch = 0; ch < 3; ch++) Cx[ch] += (double)q->rgb32[ch] * (double)alpha * Tx;
+                    Tx *= 1.0 - (double)alpha;
                     T32 = Tn;
                     last = (int)(j - h->off[b]) + 1;
                 }
@@ -672,6 +686,11 @@ static void composite(oracle_t *h, const float *dLdC)
                 for (int ch = 0; ch < 3; ch++)
                     h->img[((size_t)v * 3 + ch) * H * W + pix] = Cc[ch] + T64 * h->bg[ch];
                 h->Tfin[(size_t)v * H * W + pix] = T64;
+                for (int ch = 0; ch < 3; ch++) {
+                    h->img32[((size_t)v * 3 + ch) * H * W + pix] = fmaf(T32, h->bg32[ch], C32[ch]);
+                    h->imgx[((size_t)v * 3 + ch) * H * W + pix] = Cx[ch] + Tx * h->bg[ch];
+                }
+                h->Tfin32[(size_t)v * H * W + pix] = T32;
                 h->dep[(size_t)v * H * W + pix] = Dd;
                 h->ncon[(size_t)v * H * W + pix] = last;
                 h->nbl[(size_t)v * H * W + pix] = m;
@@ -869,6 +888,10 @@ int oracle_forward(oracle_t *h)
     free(h->img); free(h->Tfin); free(h->ncon); free(h->nbl);
     h->img = (double *)calloc(3 * npx, sizeof(double));
     h->Tfin = (double *)calloc(npx, sizeof(double));
+    free(h->img32); free(h->Tfin32); free(h->imgx);
+    h->img32 = (float *)calloc(3 * npx, sizeof(float));
+    h->Tfin32 = (float *)calloc(npx, sizeof(float));
+    h->imgx = (double *)calloc(3 * npx, sizeof(double));
     h->ncon = (int32_t *)calloc(npx, sizeof(int32_t));
     h->nbl = (int32_t *)calloc(npx, sizeof(int32_t));
     free(h->dep);
@@ -885,6 +908,10 @@ int oracle_backward(oracle_t *h, const float *dLdC)
     free(h->img); free(h->Tfin); free(h->ncon); free(h->nbl); free(h->pg);
     h->img = (double *)calloc(3 * npx, sizeof(double));
     h->Tfin = (double *)calloc(npx, sizeof(double));
+    free(h->img32); free(h->Tfin32); free(h->imgx);
+    h->img32 = (float *)calloc(3 * npx, sizeof(float));
+    h->Tfin32 = (float *)calloc(npx, sizeof(float));
+    h->imgx = (double *)calloc(3 * npx, sizeof(double));
     h->ncon = (int32_t *)calloc(npx, sizeof(int32_t));
     h->nbl = (int32_t *)calloc(npx, sizeof(int32_t));
     h->pg = (double *)calloc((size_t)h->npg * NG + 1, sizeof(double));
@@ -925,6 +952,16 @@ void oracle_get_image(const oracle_t *h, double *rgb, double *Tfin, int32_t *nco
     if (rgb) memcpy(rgb, h->img, 3 * npx * sizeof(double));
     if (Tfin) memcpy(Tfin, h->Tfin, npx * sizeof(double));
     if (ncon) memcpy(ncon, h->ncon, npx * sizeof(int32_t));
+}
+
+/* the image and T_final of the last forward in fp32 canonical arithmetic: the decisions' T and
+ * α, colour accumulated as C = fma(rgb32, α·T, C) in list order, out = fma(T, bg, C) */
+void oracle_get_image32(const oracle_t *h, float *rgb, float *Tfin, double *imgx)
+{
+    size_t npx = (size_t)h->V * h->W * h->H;
+    if (rgb) memcpy(rgb, h->img32, 3 * npx * sizeof(float));
+    if (Tfin) memcpy(Tfin, h->Tfin32, npx * sizeof(float));
+    if (imgx) memcpy(imgx, h->imgx, 3 * npx * sizeof(double));
 }
 
 /* blended entries per pixel [V,H,W] of the last forward (α ≥ 1/255, before termination) */

@@ -89,11 +89,11 @@ __global__ __launch_bounds__(256) void k_render_fwd_list(Launch L, const int32_t
                     done = true;
                     break;
                 }
-                const float w = alpha * T;
+                const float w = FMUL(alpha, T);  // CA: C = fma(rgb, α·T, C)
                 const float4 col = s2[j];
-                C0 += col.x * w;
-                C1 += col.y * w;
-                C2 += col.z * w;
+                C0 = __fmaf_rn(col.x, w, C0);
+                C1 = __fmaf_rn(col.y, w, C1);
+                C2 = __fmaf_rn(col.z, w, C2);
                 T = Tn;
                 last = b0 - start + j + 1;
             }
@@ -101,9 +101,9 @@ __global__ __launch_bounds__(256) void k_render_fwd_list(Launch L, const int32_t
     }
     if (slot >= 0) {
         const int64_t o = base + slot;
-        out_rgb[3 * o + 0] = C0 + T * L.bg[0];
-        out_rgb[3 * o + 1] = C1 + T * L.bg[1];
-        out_rgb[3 * o + 2] = C2 + T * L.bg[2];
+        out_rgb[3 * o + 0] = __fmaf_rn(T, L.bg[0], C0);
+        out_rgb[3 * o + 1] = __fmaf_rn(T, L.bg[1], C1);
+        out_rgb[3 * o + 2] = __fmaf_rn(T, L.bg[2], C2);
         out_T[o] = T;
         out_n[o] = valid ? last : 0;
     }

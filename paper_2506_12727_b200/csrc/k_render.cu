@@ -281,9 +281,9 @@ __global__ __launch_bounds__(RT) void k_render_fwd_p(Launch L, float* __restrict
     for (int p = 0; p < 2; p++) {
         if (!(x < L.W && y[p] < L.H)) continue;
         const int64_t pix = (int64_t)y[p] * L.W + x;
-        out_rgb[(3 * (int64_t)v + 0) * HW + pix] = Cs[p][0] + Ts[p] * L.bg[0];
-        out_rgb[(3 * (int64_t)v + 1) * HW + pix] = Cs[p][1] + Ts[p] * L.bg[1];
-        out_rgb[(3 * (int64_t)v + 2) * HW + pix] = Cs[p][2] + Ts[p] * L.bg[2];
+        out_rgb[(3 * (int64_t)v + 0) * HW + pix] = __fmaf_rn(Ts[p], L.bg[0], Cs[p][0]);  // CA: fma(T, bg, C)
+        out_rgb[(3 * (int64_t)v + 1) * HW + pix] = __fmaf_rn(Ts[p], L.bg[1], Cs[p][1]);  // CA: fma(T, bg, C)
+        out_rgb[(3 * (int64_t)v + 2) * HW + pix] = __fmaf_rn(Ts[p], L.bg[2], Cs[p][2]);  // CA: fma(T, bg, C)
         out_T[v * HW + pix] = Ts[p];
         out_n[v * HW + pix] = ls[p];
         if (DEPTH) out_D[v * HW + pix] = Ds[p];

@@ -1,22 +1,40 @@
-"""Parity at BASELINE.json's full size in the launch configuration bench.py times
-(garden: 3 M Gaussians, SH 3, 4 views of 1237×822): the GPU runs the whole batch;
-the oracle (tile-mask mode) recomputes a seeded sample of (view, tile) buckets —
-including the ragged last row/column — one by one.  ∂L/∂C is zero outside the
-sampled tiles, so every gradient and E statistic of all 3 M Gaussians is
-comparable exactly under the DESIGN.md §5 rules."""
+"""Parity at BASELINE.json's shapes in the launch configuration bench.py times: the GPU runs
+the whole batch; the oracle (tile-mask mode) recomputes a seeded sample of (view, tile)
+buckets — including the ragged last row/column — one by one.  ∂L/∂C is zero outside the
+sampled tiles, so every gradient and E statistic of all Gaussians is comparable exactly
+under the DESIGN.md §5 rules.
+
+Cases (each is a different bucket-key width of the entry sort):
+  garden    3 M Gaussians, 4 views of 1237×822  — 16,224 buckets (2 passes of 7-bit digits)
+  train     1.1 M, 8 views of 980×545           — 17,360 buckets (15 bits: 8 + 7)
+  playroom  2.5 M, 8 views of 1264×832          — 32,864 buckets (15 bits, indoor layout)
+  large     the large-batch geometry (32 views of 1600×1064, 214,400 buckets ≥ 2^16:
+            3 passes of 6-bit digits) with 400 k Gaussians so the oracle stays in seconds
+"""
+import dataclasses
+
 import numpy as np
 import pytest
 
 import oracle
 import synth
-from gpu_harness import assert_close_rel, per_view_scale, run_gpu
+from gpu_harness import assert_close_rel, input_sensitivity, per_view_scale, run_gpu
 
 pytestmark = [pytest.mark.gpu, pytest.mark.slow]
 
+GRAD_KEYS = ["d_means", "d_log_scales", "d_quats", "d_opacity_logits", "d_sh", "e1", "e2", "e_old"]
 
-@pytest.fixture(scope="module")
-def garden(require_gpu):
-    cfg = synth.CONFIGS["garden"]
+CASES = {
+    "garden": (synth.CONFIGS["garden"], 40),
+    "train": (synth.CONFIGS["train"], 24),
+    "playroom": (synth.CONFIGS["playroom"], 24),
+    "large": (dataclasses.replace(synth.CONFIGS["large"], P=400_000), 6),
+}
+
+
+@pytest.fixture(scope="module", params=list(CASES))
+def big(request, require_gpu):
+    cfg, per_view = CASES[request.param]
     g, cams = synth.make_scene(cfg)
     V, H, W = cfg.V, cfg.H, cfg.W
     TX, TY = (W + 15) // 16, (H + 15) // 16
@@ -24,7 +42,7 @@ def garden(require_gpu):
     rng = np.random.default_rng(123)
     mask = np.zeros((V, T), np.uint8)
     for v in range(V):
-        mask[v, rng.choice(T, 40, replace=False)] = 1
+        mask[v, rng.choice(T, per_view, replace=False)] = 1
         mask[v, (TY - 1) * TX + rng.integers(0, TX)] = 1      # ragged last row
         mask[v, rng.integers(0, TY) * TX + TX - 1] = 1        # ragged last column
         mask[v, T - 1] = 1                                    # ragged corner
@@ -38,29 +56,46 @@ def garden(require_gpu):
     o = oracle.Oracle(g, cams, tile_mask=mask)
     ref = o.backward(dL)
     scale = per_view_scale(g, cams, dL, tile_mask=mask, extra=False)
-    return dict(g=g, cams=cams, mask=mask, pix=pix, dL=dL, gpu=gpu, o=o, ref=ref, im=o.image(), T=T, scale=scale)
+    sens = input_sensitivity(g, cams, dL, GRAD_KEYS, tile_mask=mask)
+    return dict(sens=sens, name=request.param, g=g, cams=cams, mask=mask, pix=pix, dL=dL, gpu=gpu, o=o, ref=ref, im=o.image(),
+                T=T, V=V, scale=scale)
 
 
-def test_fullsize_lists_of_sampled_buckets(garden):
-    o, gpu, mask = garden["o"], garden["gpu"], garden["mask"]
+def test_fullsize_lists_of_sampled_buckets(big):
+    o, gpu, mask = big["o"], big["gpu"], big["mask"]
     off, gid = o.lists()
     rs, eg = gpu["range_start"], gpu["entry_gid"]
-    assert gpu["stats"]["K"] > 20_000_000
+    if big["name"] == "garden":
+        assert gpu["stats"]["K"] > 20_000_000
+    if big["name"] == "large":
+        assert big["V"] * big["T"] >= 1 << 16
+    assert gpu["stats"]["max_bucket"] > 0
     for b in np.nonzero(mask.reshape(-1))[0]:
         np.testing.assert_array_equal(eg[rs[b]:rs[b + 1]], gid[off[b]:off[b + 1]], err_msg=f"bucket {b}")
 
 
-def test_fullsize_forward_on_sampled_tiles(garden):
-    gpu, im, pix = garden["gpu"], garden["im"], garden["pix"]
+def test_fullsize_forward_on_sampled_tiles(big):
+    """n_contrib bit-exact; the image and T_final bit-exact against the oracle's fp32
+    canonical-arithmetic evaluation, and against its fp64 values within 1e-5 + 2^-24 per
+    list entry walked (R47: the fp32 rounding of each entry's α — not the
+    compositing arithmetic — is what a long list accumulates)."""
+    gpu, im, pix, o = big["gpu"], big["im"], big["pix"], big["o"]
     np.testing.assert_array_equal(gpu["n_contrib"][pix], im["n_contrib"][pix])
+    i32 = o.image32()
+    np.testing.assert_array_equal(gpu["rgb"].transpose(0, 2, 3, 1)[pix], i32["rgb"].transpose(0, 2, 3, 1)[pix])
+    np.testing.assert_array_equal(gpu["T_final"][pix], i32["T_final"][pix])
     d = np.abs(gpu["rgb"].transpose(0, 2, 3, 1)[pix] - im["rgb"].transpose(0, 2, 3, 1)[pix])
-    assert d.max() <= 1e-5
-    assert np.max(np.abs(gpu["T_final"][pix] - im["T_final"][pix])) <= 1e-5
+    lim = 1e-5 + 2.0 ** -24 * im["n_contrib"][pix].astype(np.float64)
+    assert np.all(d <= lim[:, None])
+    assert np.all(np.abs(gpu["T_final"][pix] - im["T_final"][pix]) <= lim)
 
 
-def test_fullsize_gradients_and_adc(garden):
-    gpu, ref, sc = garden["gpu"], garden["ref"], garden["scale"]
-    for k in ["d_means", "d_log_scales", "d_quats", "d_opacity_logits", "d_sh", "e1", "e2", "e_old"]:
-        assert_close_rel(gpu[k], ref[k], k, scale=sc[k])
+def test_fullsize_gradients_and_adc(big):
+    """DESIGN.md §5 rules; elements the oracle itself cannot pin to 1e-3 under 1-ulp changes of
+    its fp32 inputs (ill-conditioned: measured ~3e-4 of playroom's d_log_scales) may deviate
+    by twice that sensitivity, at most 0.1 % of any tensor."""
+    gpu, ref, sc, sens = big["gpu"], big["ref"], big["scale"], big["sens"]
+    for k in GRAD_KEYS:
+        assert_close_rel(gpu[k], ref[k], k, scale=sc[k], sens=sens[k])
     np.testing.assert_array_equal(gpu["vis"], ref["vis"])
     assert np.all(gpu["e1"] >= gpu["e2"] * (1 - 1e-5)) and np.all(gpu["e2"] >= gpu["e_old"] * (1 - 1e-5))

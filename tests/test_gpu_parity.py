@@ -107,6 +107,10 @@ def test_forward(case):
     np.testing.assert_array_equal(gpu["bwd_nblend"], case["o"].nblend())
     assert np.max(np.abs(gpu["rgb"] - ref["rgb"])) <= 1e-5
     assert np.max(np.abs(gpu["T_final"] - ref["T_final"])) <= 1e-5
+    # and bit-exact against the oracle's evaluation of the same blend in fp32 canonical arithmetic
+    i32 = case["o"].image32()
+    np.testing.assert_array_equal(gpu["rgb"], i32["rgb"])
+    np.testing.assert_array_equal(gpu["T_final"], i32["T_final"])
 
 
 def test_backward_pair_records(case):
@@ -143,6 +147,7 @@ def _check_all(g, cams, bg=(0.0, 0.0, 0.0), seed=3, **kw):
     scale = per_view_scale(g, cams, dL, bg)
     np.testing.assert_array_equal(gpu["n_contrib"], im["n_contrib"])
     assert np.max(np.abs(gpu["rgb"] - im["rgb"])) <= 1e-5
+    np.testing.assert_array_equal(gpu["rgb"], o.image32()["rgb"])
     off, gid = o.lists()
     np.testing.assert_array_equal(gpu["range_start"], off)
     np.testing.assert_array_equal(gpu["entry_gid"], gid)
@@ -358,6 +363,8 @@ def test_warp_culling_on_thin_correlated_ellipses():
     assert nmax > 100
     lim = 1e-5 + 6 * 2.0 ** -24 * im["n_contrib"][:, None].astype(np.float64)
     assert np.all(np.abs(gpu["rgb"] - im["rgb"]) <= lim)
+    # exactly the oracle's fp32 canonical-arithmetic image (the difference above is fp32's own)
+    np.testing.assert_array_equal(gpu["rgb"], o.image32()["rgb"])
     # The backward culls with the same mask function on the same staged values, so its
     # decisions are the ones verified above.  Its values are not compared here: in this
     # scene they are ill-conditioned at the fp32 input level — perturbing the oracle's fp32

@@ -71,7 +71,8 @@ def scene(require_gpu):
     o = oracle.Oracle(g, cams)
     ref = o.backward(dL_masked)
     im = o.image()
-    return dict(g=g, cams=cams, pix=pix, S=S, idx=(v, y, x, inside), dL_s=dL_s, dL_masked=dL_masked, ref=ref, im=im)
+    return dict(g=g, cams=cams, pix=pix, S=S, idx=(v, y, x, inside), dL_s=dL_s, dL_masked=dL_masked, ref=ref, im=im,
+                im32=o.image32())
 
 
 @pytest.mark.parametrize("mode", [0, 1])
@@ -82,6 +83,8 @@ def test_partial_forward_equals_full_render(scene, mode):
     np.testing.assert_array_equal(out["n_contrib"][inside], im["n_contrib"][v[inside], y[inside], x[inside]])
     ref_rgb = im["rgb"].transpose(0, 2, 3, 1)[v[inside], y[inside], x[inside]]
     assert np.max(np.abs(out["rgb"][inside] - ref_rgb)) <= 1e-5
+    np.testing.assert_array_equal(out["rgb"][inside],
+                                  scene["im32"]["rgb"].transpose(0, 2, 3, 1)[v[inside], y[inside], x[inside]])
     assert np.max(np.abs(out["T_final"][inside] - im["T_final"][v[inside], y[inside], x[inside]])) <= 1e-5
     assert np.all(out["n_contrib"][~inside] == 0) and np.all(out["T_final"][~inside] == 1.0)
 

@@ -636,3 +636,31 @@ def test_P17b_sh_clamp_decision_is_the_sign_of_the_colour():
             np.testing.assert_array_equal(bits[ok], (val < 0)[ok].astype(int), err_msg=f"view {v} gid {i}")
             seen += int(np.sum(val < 0))
     assert seen > 100  # the clamp is exercised
+
+
+# ------------------------------------------------------- fp32 canonical-arithmetic image (§5)
+def test_image32_is_the_fp32_evaluation_of_the_fp64_image():
+    """image32 (the decisions' T and α, C = fma(rgb32, α·T, C)) against the fp64 value chain:
+    within 1e-5 + 2^-24 per walked entry, and the deviation is carried by the fp32 alphas —
+    an fp64 chain fed the fp32 alphas (rgb_x) deviates as much (R47)."""
+    import dataclasses
+    cfg = dataclasses.replace(synth.CONFIGS["tiny"], P=20_000)
+    g, cams = synth.make_scene(cfg)
+    o = oracle.Oracle(g, cams, bg=(0.1, 0.2, 0.3))
+    im = o.forward()
+    i32 = o.image32()
+    n = im["n_contrib"].astype(np.float64)
+    assert n.max() > 100
+    d32 = np.abs(i32["rgb"].astype(np.float64) - im["rgb"])
+    dx = np.abs(i32["rgb_x"] - im["rgb"])
+    assert np.all(d32 <= 1e-5 + 2.0 ** -24 * n[:, None])
+    assert np.all(np.abs(i32["T_final"] - im["T_final"]) <= 1e-5 + 2.0 ** -24 * n)
+    assert dx.max() >= 0.5 * d32.max() > 0
+    # the single-Gaussian case is exact up to the fp32 colour and α: rgb32·α + (1 − α)·bg
+    g1 = dict(means=np.zeros((1, 3), np.float32), log_scales=np.full((1, 3), np.log(0.2), np.float32),
+              quats=np.array([[1, 0, 0, 0]], np.float32), opacity_logits=np.array([1.0], np.float32),
+              sh=np.array([[[0.3, -0.2, 0.5]]], np.float32), sh_degree=0)
+    cam = synth.cams_array([synth.make_camera(np.eye(3), [0, 0, 2.0], 32, 32, 40.0)])
+    o1 = oracle.Oracle(g1, cam)
+    im1 = o1.forward()
+    np.testing.assert_allclose(o1.image32()["rgb"], im1["rgb"], atol=2e-7)
