@@ -125,6 +125,17 @@ def measured_peaks():
     return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
 
 
+def measured_alu_peak():
+    """FFMA2 TFLOP/s measured on a B200 of this pool (scripts/microbench_alu.cu), or None."""
+    try:
+        return float(json.load(open(os.path.join(ROOT, "profiles", "r2_alu_peaks.json")))["ffma2_tflops"])
+    except (OSError, ValueError, KeyError):
+        try:  # the file holds one JSON object per line (two runs)
+            return float(json.loads(open(os.path.join(ROOT, "profiles", "r2_alu_peaks.json")).readline())["ffma2_tflops"])
+        except (OSError, ValueError, KeyError):
+            return None
+
+
 def stage_models(P, NK, V, NB, Q, K, T, evf, evb, exf, exb, Qv):
     """(bound, algorithmic units per launch) per stage — DESIGN.md §7.  Qv = pairs with
     tiles > 0 (the rest are inert: only their depth, flags and sort key are written)."""
@@ -327,6 +338,7 @@ def run_mvgs(args):
     roof = {"bound": bound, "achieved": round(achieved, 3), "peak": round(peak, 3), "unit": unit,
             "frac": round(achieved / peak, 4), "traffic": traffic, "kernel": dom,
             "peak_source": peak_src if bound == "hbm" else "derived: 148 SM x 128 FP32 lanes x 2 x sm_max_mhz",
+            **({} if bound == "hbm" else {"peak_measured": measured_alu_peak()}),
             "stage_ms": {k: round(v, 4) for k, v in stages.items()},
             "stage_frac": {k: round(models[k][1] / (stages[k] / 1e3) / (1e9 * float(peaks["hbm_gbs"]) if models[k][0] == "hbm" else peak * 1e12), 4)
                            for k in stages if stages[k] > 0}}
@@ -335,8 +347,7 @@ def run_mvgs(args):
         "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": N, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic (mvgs-synth v1, seeded; DESIGN.md §6)",
-        "config": {"workload": f"{cfg.name}: {P} Gaussians SH{cfg.sh_degree}, {Vr} views/GPU at {cfg.W}x{cfg.H}",
-                   "views_per_step": views_total, "global_batch_views": views_total, "parallelism": f"views dp{N}",
+        "config": {**workload_config(cfg, P, Vr, N),
                    "allreduce_chunks": CHUNKS,
                    "l2": "inputs larger than L2 (params %.0f MB)" % (sum(v.nbytes for v in g_np.values()
                                                                        if isinstance(v, np.ndarray)) / 1e6),
@@ -363,11 +374,31 @@ def run_mvgs(args):
 
 
 # ---------------------------------------------------------------- oracle arm
-def oracle_sample(g_np, cams, dL, frac, seed=0):
-    """Time the oracle (single-threaded C, as it stands) on a bounded sample of the
-    workload: view 0 with a seeded fraction `frac` of its 16×16 tiles (∂L/∂C zero
-    elsewhere), all stages S1–S9.  Returns (views/s = frac / seconds, seconds, sample)."""
+def host_cpu():
+    """(logical cores, model name) of this host (the GPU box's, when run there)."""
+    model = "unknown"
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return os.cpu_count() or 1, model
+
+
+def oracle_threads():
+    """All host cores (SURVEY §8(d) M6 oracle-mt), capped at 64 (per-thread pair accumulators)."""
+    return max(1, min(64, int(os.environ.get("MVGS_ORACLE_THREADS", os.cpu_count() or 1))))
+
+
+def oracle_sample(g_np, cams, dL, frac, seed=0, threads=1):
+    """Time the oracle (the C oracle as it stands, on `threads` host threads: OpenMP over
+    Gaussians and (view, tile) buckets) on a bounded sample of the workload: view 0 with a
+    seeded fraction `frac` of its 16×16 tiles (∂L/∂C zero elsewhere), all stages S1–S9.
+    Returns (views/s = frac / seconds, seconds, sample)."""
     import oracle
+    oracle.set_threads(threads)
     W, H = int(cams[0]["width"]), int(cams[0]["height"])
     TX, TY = (W + 15) // 16, (H + 15) // 16
     T = TX * TY
@@ -386,41 +417,53 @@ def oracle_sample(g_np, cams, dL, frac, seed=0):
     o = oracle.Oracle(g_np, cams[:1], tile_mask=mask)
     o.backward(d)
     dt = time.perf_counter() - t0
+    oracle.set_threads(1)
     f = nt / T
-    sample = (f"view 0 of the {len(cams)}-view batch, {nt}/{T} of its 16x16 tiles (seeded), all "
-              f"{g_np['means'].shape[0]} Gaussians projected, S1-S9, single-threaded C oracle; "
-              f"value = sampled fraction of a view / {dt:.2f} s")
+    cores, model = host_cpu()
+    sample = (f"view 0 of the {len(cams)}-view batch, {nt}/{T} of its 16x16 tiles, all "
+              f"{g_np['means'].shape[0]} Gaussians projected, S1-S9, the C oracle on {threads} OpenMP threads "
+              f"({cores} logical cores, {model}); value = sampled views / {dt:.2f} s")
     return f / dt, dt, sample
 
 
 def cpu_baseline(cfg, g_np, cams, dL):
-    vps, dt, sample = oracle_sample(g_np, cams, dL, 1.0)
-    return {"value": round(vps, 5), "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample}
+    th = oracle_threads()
+    vps, dt, sample = oracle_sample(g_np, cams, dL, 1.0, threads=th)
+    return {"value": round(vps, 5), "unit": UNIT, "cores": th, "kind": "oracle", "sample": sample}
+
+
+def workload_config(cfg, P, Vr, N):
+    return {"workload": f"{cfg.name}: {P} Gaussians SH{cfg.sh_degree}, {Vr} views/GPU at {cfg.W}x{cfg.H}",
+            "views_per_step": Vr * N, "global_batch_views": Vr * N, "parallelism": f"views dp{N}"}
 
 
 def run_reference(args):
+    """The base contract's reference arm for this tier: the oracle, timed as it stands on the
+    host's cores, each step one full view of the same workload as the cpu_baseline leg."""
     ws, rank, _ = dist_setup()
     if rank != 0:
         return
     cfg = synth.CONFIGS[args.config]
     g_np, cams = synth.make_scene(cfg)
     dL = synth.make_dLdC(cfg.V, cfg.H, cfg.W, cfg.seed)
-    frac = 0.5  # ≈ 9 s per step at garden size: K = 20 steps finish in ≈ 3 minutes
+    th = oracle_threads()
     for w in range(min(args.warmup, 1)):
-        oracle_sample(g_np, cams, dL, frac, seed=1000 + w)
+        oracle_sample(g_np, cams, dL, 1.0, threads=th)
     vals, times = [], []
     for k in range(args.steps):
-        vps, dt, sample = oracle_sample(g_np, cams, dL, frac, seed=k)
+        vps, dt, sample = oracle_sample(g_np, cams, dL, 1.0, threads=th)
         vals.append(vps)
         times.append(dt)
     value = len(vals) / sum(1.0 / v for v in vals)  # total sampled views / total time
+    N = args.gpus if ws == 1 else ws
+    conf = workload_config(cfg, cfg.P, cfg.V, 1)
+    conf["sample"] = sample
     line = {"impl": "reference", "metric": METRIC, "value": round(value, 5), "unit": UNIT,
-            "n_gpus": args.gpus if ws == 1 else ws, "steps": args.steps, "warmup": args.warmup,
+            "n_gpus": N, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(1e3 * statistics.mean(times), 2), "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (mvgs-synth v1, seeded)",
-            "config": {"workload": f"{cfg.name}: {cfg.P} Gaussians SH{cfg.sh_degree}, {cfg.V} views at {cfg.W}x{cfg.H}",
-                       "sample": sample},
-            "cpu_baseline": {"value": round(value, 5), "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+            "config": conf,
+            "cpu_baseline": {"value": round(value, 5), "unit": UNIT, "cores": th, "kind": "oracle", "sample": sample},
             "e2e": {"value": round(value, 5), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 

@@ -18,7 +18,7 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 SRC = os.path.join(HERE, "oracle.c")
 LIB = os.path.join(HERE, "liboracle.so")
-CFLAGS = ["-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared", "-Wall"]
+CFLAGS = ["-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared", "-Wall", "-fopenmp"]
 
 NO_EARLY_TERMINATION = 1
 NG = 10  # per-pair gradient record: gx gy e1 dA dB dC dO dr dg db
@@ -70,11 +70,23 @@ def lib():
         for name, n in [("oracle_get_image", 3), ("oracle_get_image32", 3), ("oracle_get_lists", 2), ("oracle_get_pairs", 3),
                         ("oracle_get_opacity32", 1), ("oracle_get_pair_grads", 1), ("oracle_get_grads", 9)]:
             getattr(L, name).argtypes = [vp] + [vp] * n
+        L.oracle_set_threads.argtypes = [C.c_int]
+        L.oracle_get_threads.restype = C.c_int
         L.oracle_ca_exp.restype = C.c_float
         L.oracle_ca_exp.argtypes = [C.c_float]
         L.oracle_adc_example.argtypes = [C.c_int, vp, vp, vp, vp]
         _lib = L
     return _lib
+
+
+def set_threads(n: int) -> None:
+    """Host threads of the oracle (1, the default, runs every loop in its written order; more
+    is only for the CPU timing baseline — bench.py's cpu_baseline / --impl reference)."""
+    lib().oracle_set_threads(int(n))
+
+
+def get_threads() -> int:
+    return int(lib().oracle_get_threads())
 
 
 def use_library(path: str | None = None):

@@ -35,6 +35,9 @@
  */
 #define _POSIX_C_SOURCE 199309L
 #include <math.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
 #include <stdint.h>
 #include <time.h>
 #include <stdlib.h>
@@ -468,6 +471,16 @@ static int entry_cmp(const void *x, const void *y)
     return (a->gid > b->gid) - (a->gid < b->gid);
 }
 
+/* Host threads for the timing baseline (oracle-mt): 1 (the default, every
+ * test) runs every loop in its written order.  With n > 1 the independent loops — per
+ * Gaussian (O1, O2, O7, O8), per (view, tile) list (O4) and per (view, tile) bucket of pixels
+ * (O5, O6) — are split over OpenMP threads; the per-pair gradient sums of O6 go to one
+ * accumulator per thread, added in thread order afterwards (the only change of arithmetic:
+ * the order of those fp64 sums). */
+static int g_threads = 1;
+void oracle_set_threads(int n) { g_threads = n < 1 ? 1 : n; }
+int oracle_get_threads(void) { return g_threads; }
+
 static uint32_t fbits(float f)
 {
     union { float f; uint32_t u; } u;
@@ -544,7 +557,7 @@ oracle_t *oracle_create_masked(const og_scene *g, const og_cam *cams, int V, con
     h->o32 = (float *)calloc(P + 1, sizeof(float));
     h->g64 = (g64_t *)calloc(P + 1, sizeof(g64_t));
     /* O1 + O2 (fp32 decisions) */
-    int64_t nvis = 0;
+#pragma omp parallel for schedule(dynamic, 4096) num_threads(g_threads)
     for (int64_t i = 0; i < P; i++) {
         float Sig[6];
         activate32(g, i, &h->o32[i], Sig);
@@ -553,14 +566,20 @@ oracle_t *oracle_create_masked(const og_scene *g, const og_cam *cams, int V, con
         for (int v = 0; v < V; v++) {
             p32_t *p = &h->p32[(size_t)v * P + i];
             project32(mu, Sig, &cams[v], p);
-            h->p64i[(size_t)v * P + i] = (p->vis && rect_hits_mask(h, v, p)) ? (int32_t)nvis++ : -1;
+            h->p64i[(size_t)v * P + i] = (p->vis && rect_hits_mask(h, v, p)) ? 0 : -1;
         }
     }
+    /* fp64 slots of the visible pairs, numbered in (Gaussian, view) order */
+    int64_t nvis = 0;
+    for (int64_t i = 0; i < P; i++)
+        for (int v = 0; v < V; v++)
+            if (h->p64i[(size_t)v * P + i] >= 0) h->p64i[(size_t)v * P + i] = (int32_t)nvis++;
     /* O2 fp64 values for the visible pairs */
     h->p64 = (p64_t *)calloc((size_t)nvis + 1, sizeof(p64_t));
     h->npg = nvis;
-    for (int v = 0; v < V; v++)
-        for (int64_t i = 0; i < P; i++) {
+#pragma omp parallel for schedule(dynamic, 4096) num_threads(g_threads)
+    for (int64_t i = 0; i < P; i++)
+        for (int v = 0; v < V; v++) {
             int32_t k = h->p64i[(size_t)v * P + i];
             if (k >= 0) project64(g, i, &h->g64[i], &cams[v], &h->p64[k]);
         }
@@ -597,6 +616,7 @@ oracle_t *oracle_create_masked(const og_scene *g, const og_cam *cams, int V, con
                     fill[b]++;
                 }
         }
+#pragma omp parallel for schedule(dynamic, 64) num_threads(g_threads)
     for (int64_t b = 0; b < nb; b++)
         qsort(ent + h->off[b], (size_t)(h->off[b + 1] - h->off[b]), sizeof(entry_t), entry_cmp);
     h->gid = (int32_t *)malloc(sizeof(int32_t) * (h->K + 1));
@@ -625,15 +645,32 @@ static void composite(oracle_t *h, const float *dLdC)
     h->dhash = 0;
     const int64_t P = h->g.P;
     const int W = h->W, H = h->H, V = h->V;
+    const int64_t nb = (int64_t)V * h->T;
     int64_t maxlen = 0;
-    for (int64_t b = 0; b < (int64_t)V * h->T; b++)
+    for (int64_t b = 0; b < nb; b++)
         if (h->off[b + 1] - h->off[b] > maxlen) maxlen = h->off[b + 1] - h->off[b];
+    uint64_t *bh = (uint64_t *)calloc((size_t)nb + 1, sizeof(uint64_t)); /* per-bucket decision hash */
+    const int nt = g_threads;
+    double **pgt = (double **)calloc((size_t)nt, sizeof(double *)); /* per-thread pair sums (thread 0: h->pg) */
+    if (dLdC)
+        for (int t = 0; t < nt; t++)
+            pgt[t] = t == 0 ? h->pg : (double *)calloc((size_t)h->npg * NG + 1, sizeof(double));
+#pragma omp parallel num_threads(nt)
+    {
+    int tid = 0;
+#ifdef _OPENMP
+    tid = omp_get_thread_num();
+#endif
+    double *pgbase = dLdC ? pgt[tid] : NULL;
     blend_t *bl = (blend_t *)malloc(sizeof(blend_t) * (maxlen + 1));
-    for (int v = 0; v < V; v++)
-        for (int y = 0; y < H; y++)
-            for (int x = 0; x < W; x++) {
-                int64_t b = (int64_t)v * h->T + (y / 16) * h->TX + (x / 16);
-                if (h->mask && !h->mask[b]) continue;
+#pragma omp for schedule(dynamic, 1)
+    for (int64_t b = 0; b < nb; b++) {
+        if (h->mask && !h->mask[b]) continue;
+        const int v = (int)(b / h->T), tile = (int)(b % h->T);
+        const int ty0 = (tile / h->TX) * 16, tx0 = (tile % h->TX) * 16;
+        uint64_t hsh = 0;
+        for (int y = ty0; y < ty0 + 16 && y < H; y++)
+            for (int x = tx0; x < tx0 + 16 && x < W; x++) {
                 /* ---- O5: forward.  Decisions fp32 (CA), values fp64. */
                 float T32 = 1.0f, C32[3] = {0.0f, 0.0f, 0.0f};
                 double T64 = 1.0, Cc[3] = {0, 0, 0}, Dd = 0.0;
@@ -661,9 +698,9 @@ static void composite(oracle_t *h, const float *dLdC)
                     double a64 = clamped ? 0.99 : h->g64[i].o * G;
                     for (int ch = 0; ch < 3; ch++) Cc[ch] += q->rgb[ch] * a64 * T64;
                     Dd += q->t[2] * a64 * T64; /* predicted depth Σ dᵢαᵢTᵢ */
-                    h->dhash = mix(h->dhash, ((uint64_t)j << 20) ^ ((uint64_t)(y * W + x) << 1) ^ (uint64_t)clamped);
-                    h->dhash = mix(h->dhash, (uint64_t)(q->clx | q->cly << 1 | q->rgb_clamped[0] << 2
-                                                        | q->rgb_clamped[1] << 3 | q->rgb_clamped[2] << 4));
+                    hsh = mix(hsh, ((uint64_t)j << 20) ^ ((uint64_t)(y * W + x) << 1) ^ (uint64_t)clamped);
+                    hsh = mix(hsh, (uint64_t)(q->clx | q->cly << 1 | q->rgb_clamped[0] << 2
+                                              | q->rgb_clamped[1] << 3 | q->rgb_clamped[2] << 4));
                     bl[m].gid = i;
                     bl[m].clamped = clamped;
                     bl[m].alpha = a64;
@@ -705,7 +742,7 @@ static void composite(oracle_t *h, const float *dLdC)
                 for (int k = m - 1; k >= 0; k--) {
                     int32_t i = bl[k].gid;
                     const p64_t *q = &h->p64[h->p64i[(size_t)v * P + i]];
-                    double *pg = &h->pg[(size_t)h->p64i[(size_t)v * P + i] * NG];
+                    double *pg = &pgbase[(size_t)h->p64i[(size_t)v * P + i] * NG];
                     double aT = bl[k].alpha * bl[k].T;
                     double dLda = 0;
                     for (int ch = 0; ch < 3; ch++) {
@@ -734,7 +771,18 @@ static void composite(oracle_t *h, const float *dLdC)
                     pg[6] += dLdo;
                 }
             }
+        bh[b] = hsh;
+    }
     free(bl);
+    }
+    for (int64_t b = 0; b < nb; b++) h->dhash = mix(h->dhash, bh[b]);
+    if (dLdC)
+        for (int t = 1; t < nt; t++) { /* thread order */
+            for (size_t k = 0; k < (size_t)h->npg * NG; k++) h->pg[k] += pgt[t][k];
+            free(pgt[t]);
+        }
+    free(pgt);
+    free(bh);
 }
 
 /* O7 + O8: per-Gaussian chain rule summed over views, and the E statistics. */
@@ -744,8 +792,11 @@ static void gauss_backward(oracle_t *h)
     const int V = h->V;
     const int S = h->g.sh_stride;
     const int nk = (h->g.sh_degree + 1) * (h->g.sh_degree + 1);
+#pragma omp parallel num_threads(g_threads)
+    {
     adc_pair *ap = (adc_pair *)malloc(sizeof(adc_pair) * V);
     int *present = (int *)malloc(sizeof(int) * V);
+#pragma omp for schedule(dynamic, 4096)
     for (int64_t i = 0; i < P; i++) {
         const g64_t *a = &h->g64[i];
         const float *sh = h->g.sh + (size_t)i * S * 3;
@@ -880,6 +931,7 @@ static void gauss_backward(oracle_t *h)
     }
     free(ap);
     free(present);
+    }
 }
 
 int oracle_forward(oracle_t *h)

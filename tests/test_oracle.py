@@ -664,3 +664,29 @@ def test_image32_is_the_fp32_evaluation_of_the_fp64_image():
     o1 = oracle.Oracle(g1, cam)
     im1 = o1.forward()
     np.testing.assert_allclose(o1.image32()["rgb"], im1["rgb"], atol=2e-7)
+
+
+def test_threads_change_no_result():
+    """oracle-mt (the timing baseline): lists, images, decisions identical, and the per-pair /
+    per-Gaussian sums equal to fp64 reordering."""
+    import dataclasses
+    cfg = dataclasses.replace(synth.CONFIGS["tiny"], P=3000, sh_degree=0)
+    g, cams = synth.make_scene(cfg)
+    dL = synth.make_dLdC_scaled(cfg.V, cfg.H, cfg.W, 1)
+    res = []
+    for n in (1, 4):
+        oracle.set_threads(n)
+        try:
+            o = oracle.Oracle(g, cams, bg=(0.1, 0.2, 0.3))
+            r = o.backward(dL)
+            res.append((o.lists(), o.image(), o.decision_hash(), r))
+        finally:
+            oracle.set_threads(1)
+    (l1, i1, h1, r1), (l4, i4, h4, r4) = res
+    for a, b in zip(l1, l4):
+        np.testing.assert_array_equal(a, b)
+    for k in i1:
+        np.testing.assert_array_equal(i1[k], i4[k])
+    assert h1 == h4
+    for k in r1:
+        np.testing.assert_allclose(r4[k], r1[k], rtol=1e-12, atol=1e-12 * max(1e-300, np.abs(r1[k]).max()))
