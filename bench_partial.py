@@ -93,6 +93,16 @@ def main():
         res[arm] = {"ms_per_step": round(ms, 4), "fwd_ms": round(stages["render_fwd"], 4),
                     "bwd_ms": round(stages["render_bwd"], 4), "pixels_per_step": px,
                     "views_per_s": round(V / (ms / 1e3), 2)}
+        # occupancy: threads holding a pixel / threads launched, and lane-steps
+        # of the entry walk spent on a live pixel / executed (the kernels count them)
+        if arm == "full":  # 256 pixel slots per (view, tile) CTA (128 threads × 2 pixels)
+            res[arm]["occupancy_threads"] = round(V * H * W / (V * T * 256), 4)
+        else:
+            st = mvgs.query(R.ctx)
+            res[arm]["threads_launched"] = st["threads_launched"]
+            res[arm]["threads_active"] = st["threads_active"]
+            res[arm]["occupancy_threads"] = round(st["threads_active"] / max(1, st["threads_launched"]), 4)
+            res[arm]["occupancy_lane_steps"] = round(st["lane_steps_active"] / max(1, st["lane_steps_launched"]), 4)
     line = {"metric": "Table-4 analog: multi-view step time, full vs masked-partial vs thread-efficient-partial",
             "unit": "ms/step", "config": {"workload": f"{cfg.name}: {cfg.P} Gaussians SH{cfg.sh_degree}, {V} views "
                                                       f"{W}x{H}, S={S} sampled pixels per (view, tile)"},

@@ -10,7 +10,7 @@
  *     (tile, view) ............................................. P:571–579
  *   - E_old, E1, E2 ............................................ P:14–21
  * Every reading of a point the paper leaves open is listed in DESIGN.md §3
- * (R1–R28); the fp32 arithmetic of every discrete decision is DESIGN.md §4.
+ * (R1–R49); the fp32 arithmetic of every discrete decision is DESIGN.md §4.
  *
  * Conventions shared by every call
  *   - All array arguments are caller-owned, contiguous, device pointers
@@ -116,6 +116,10 @@ typedef struct {
     int64_t eval_bwd;      /* (pixel, entry) evaluations of the last render_bwd              */
     int64_t exp_fwd;       /* of eval_fwd, those above the exact skip bound (G evaluated)    */
     int64_t exp_bwd;       /* of eval_bwd, likewise                                          */
+    /* occupancy of the last mvgs_render_fwd_partial: threads launched /
+     * holding a listed in-image pixel, and lane-steps of the entry walk executed (32 × each
+     * warp's longest lane, per staged batch) / spent on a live pixel                     */
+    int64_t threads_launched, threads_active, lane_steps_launched, lane_steps_active;
 } mvgs_stats;
 
 /* Create a context on `device` with initial capacities (0 = a small default).

@@ -50,7 +50,7 @@ struct Launch {  // everything a kernel needs about the current batch
     int* scan_tmp;    // scan block sums
     const uint32_t* sorted;  // [K] pair index of every entry in (view, tile, depth, gid) order
     int* counters;    // [C_NCOUNTERS]
-    unsigned long long* counters64;  // [8]: fwd/bwd evaluations, fwd/bwd exps, entries needed
+    unsigned long long* counters64;  // [16]: fwd/bwd evaluations, fwd/bwd exps, entries needed, partial-render occupancy (5–8)
     int32_t* dbg_nblend;  // parity export: per-pixel blended-entry count taken by the backward (or null)
 };
 

@@ -69,13 +69,19 @@ __global__ __launch_bounds__(256) void k_render_fwd_list(Launch L, const int32_t
     float T = 1.0f, C0 = 0.f, C1 = 0.f, C2 = 0.f;
     int last = 0;
     bool done = !valid;
+    // occupancy statistics: threads launched / with a pixel, and lane-steps of
+    // the entry walk executed by each warp (32 × its longest lane per batch) / spent on a live pixel
+    const int nact = __syncthreads_count(valid);
+    unsigned long long wsteps = 0, my_steps = 0;
     if (end <= L.cap_entries) {
         for (int b0 = start; b0 < end; b0 += PRB) {
             if (__syncthreads_count(done) == (int)blockDim.x) break;
             for (int t = threadIdx.x; t < PRB && b0 + t < end; t += blockDim.x) stage_p(L, L.sorted[b0 + t], s0, s1, s2, t);
             __syncthreads();
             const int cnt = min(PRB, end - b0);
+            int bsteps = 0;
             for (int j = 0; j < cnt && !done; j++) {
+                bsteps++;
                 const float4 a = s0[j];
                 const float4 c = s1[j];
                 const float dx = FSUB(a.x, fx), dy = FSUB(a.y, fy);
@@ -97,6 +103,21 @@ __global__ __launch_bounds__(256) void k_render_fwd_list(Launch L, const int32_t
                 T = Tn;
                 last = b0 - start + j + 1;
             }
+            my_steps += (unsigned long long)bsteps;
+            wsteps += (unsigned long long)__reduce_max_sync(0xffffffffu, (unsigned)bsteps);
+        }
+    }
+    {
+        unsigned long long ms = my_steps;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) ms += __shfl_xor_sync(0xffffffffu, ms, o);
+        if ((threadIdx.x & 31) == 0) {
+            atomicAdd(&L.counters64[7], 32ull * wsteps);
+            atomicAdd(&L.counters64[8], ms);
+        }
+        if (threadIdx.x == 0) {
+            atomicAdd(&L.counters64[5], (unsigned long long)blockDim.x);
+            atomicAdd(&L.counters64[6], (unsigned long long)nact);
         }
     }
     if (slot >= 0) {

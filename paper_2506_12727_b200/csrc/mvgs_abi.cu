@@ -209,8 +209,8 @@ mvgs_status mvgs_create(mvgs_ctx** out, int device, int64_t max_pairs, int64_t m
         (e = alloc_sort_scratch(ctx)) != cudaSuccess ||
         (e = cudaMalloc(&ctx->d_counters, sizeof(int) * C_NCOUNTERS)) != cudaSuccess ||
         (e = cudaMemset(ctx->d_counters, 0, sizeof(int) * C_NCOUNTERS)) != cudaSuccess ||
-        (e = cudaMalloc(&ctx->d_counters64, sizeof(unsigned long long) * 8)) != cudaSuccess ||
-        (e = cudaMemset(ctx->d_counters64, 0, sizeof(unsigned long long) * 8)) != cudaSuccess ||
+        (e = cudaMalloc(&ctx->d_counters64, sizeof(unsigned long long) * 16)) != cudaSuccess ||
+        (e = cudaMemset(ctx->d_counters64, 0, sizeof(unsigned long long) * 16)) != cudaSuccess ||
         (e = cudaMalloc(&ctx->d_lab_part, sizeof(double) * lab_partials())) != cudaSuccess) {
         mvgs_destroy(ctx);
         return MVGS_ERR_CUDA;
@@ -393,6 +393,7 @@ mvgs_status mvgs_render_fwd_partial(mvgs_ctx* ctx, const int32_t* pix, int32_t S
     CK(cudaSetDevice(ctx->device));
     cudaStream_t s = (cudaStream_t)stream;
     ctx->last_stream = s;
+    CK(cudaMemsetAsync(ctx->d_counters64 + 5, 0, 4 * sizeof(unsigned long long), s));  // occupancy counters
     { STAGE(ST_FWD); CK(launch_render_fwd_partial(ctx->L, pix, S, mode, rgb, T_final, n_contrib, s)); }
     ctx->state = 4;  // partial forward: its [V,T,S] outputs are only valid for the matching partial backward
     ctx->partial_S = S;
@@ -442,7 +443,7 @@ mvgs_status mvgs_query(mvgs_ctx* ctx, mvgs_stats* out) {
     if (!ctx || !out) return MVGS_ERR_INVALID;
     CK(cudaSetDevice(ctx->device));
     int h[C_NCOUNTERS];
-    unsigned long long h64[5];
+    unsigned long long h64[9];
     // ordered on the stream of the last enqueuing call; waits for that stream only, not the device
     CK(cudaMemcpyAsync(h, ctx->d_counters, sizeof(h), cudaMemcpyDeviceToHost, ctx->last_stream));
     CK(cudaMemcpyAsync(h64, ctx->d_counters64, sizeof(h64), cudaMemcpyDeviceToHost, ctx->last_stream));
@@ -461,6 +462,10 @@ mvgs_status mvgs_query(mvgs_ctx* ctx, mvgs_stats* out) {
     out->eval_bwd = (int64_t)h64[1];
     out->exp_fwd = (int64_t)h64[2];
     out->exp_bwd = (int64_t)h64[3];
+    out->threads_launched = (int64_t)h64[5];
+    out->threads_active = (int64_t)h64[6];
+    out->lane_steps_launched = (int64_t)h64[7];
+    out->lane_steps_active = (int64_t)h64[8];
     out->overflow = h[C_OVERFLOW] || out->Q > ctx->cap_pairs || out->K > ctx->cap_entries;
     if (out->overflow) return fail(ctx, MVGS_ERR_CAPACITY, "capacity exceeded: reserve stats.Q / stats.K and re-run");
     return MVGS_OK;

@@ -75,7 +75,8 @@ class Stats(C.Structure):
     _fields_ = [("Q", C.c_int64), ("K", C.c_int64), ("cap_pairs", C.c_int64), ("cap_entries", C.c_int64),
                 ("max_bucket", C.c_int64), ("n_visible", C.c_int64), ("overflow", C.c_int32), ("V", C.c_int32),
                 ("tiles_x", C.c_int32), ("tiles_y", C.c_int32), ("eval_fwd", C.c_int64), ("eval_bwd", C.c_int64),
-                ("exp_fwd", C.c_int64), ("exp_bwd", C.c_int64)]
+                ("exp_fwd", C.c_int64), ("exp_bwd", C.c_int64), ("threads_launched", C.c_int64),
+                ("threads_active", C.c_int64), ("lane_steps_launched", C.c_int64), ("lane_steps_active", C.c_int64)]
 
 
 CAM_BYTES = 76

@@ -41,7 +41,7 @@ def run_partial(g, cams, pix, mode, dL_s=None):
     Tf = torch.empty((V, T, S), device=dev)
     nc = torch.empty((V, T, S), dtype=torch.int32, device=dev)
     mvgs.render_fwd_partial(R.ctx, p, S, mode, rgb, Tf, nc)
-    out = dict(stats=R.stats)
+    out = dict(stats=R.stats, occ=mvgs.query(R.ctx))
     if dL_s is not None:
         grads, adc = R.alloc_backward()
         mvgs.render_bwd_partial(R.ctx, p, S, mode, torch.from_numpy(dL_s).to(dev), Tf, nc)
@@ -116,3 +116,21 @@ def test_identity_list_equals_full_kernel(scene):
     v, y, x, inside = dense_index(ident, (203 + 15) // 16, 137, 203)
     np.testing.assert_array_equal(a["n_contrib"][inside], full["n_contrib"][v[inside], y[inside], x[inside]])
     assert np.max(np.abs(a["rgb"][inside] - full["rgb"].transpose(0, 2, 3, 1)[v[inside], y[inside], x[inside]])) <= 1e-6
+
+
+def test_occupancy_counts(scene):
+    """threads launched / holding a pixel, counted by the kernel.  Masked:
+    256 threads per (view, tile), the listed in-image pixels active; thread-efficient:
+    ⌈S/32⌉·32 threads, the same pixels active; lane-steps of the entry walk: efficient
+    wastes no more than masked."""
+    v, y, x, inside = scene["idx"]
+    pix = scene["pix"]
+    V, T, S = pix.shape
+    n_in = int(np.count_nonzero(inside))
+    occ = {m: run_partial(scene["g"], scene["cams"], pix, m)["occ"] for m in (0, 1)}
+    eff, msk = occ[0], occ[1]  # mode 0: thread-efficient, 1: masked
+    assert msk["threads_launched"] == V * T * 256
+    assert eff["threads_launched"] == V * T * (-(-S // 32) * 32)
+    assert msk["threads_active"] == n_in and eff["threads_active"] == n_in
+    assert eff["lane_steps_active"] == msk["lane_steps_active"]  # the same pixels walk the same entries
+    assert eff["lane_steps_active"] / eff["lane_steps_launched"] >= msk["lane_steps_active"] / msk["lane_steps_launched"]
