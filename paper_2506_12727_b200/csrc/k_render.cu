@@ -62,7 +62,6 @@ __device__ __forceinline__ void count_evals(unsigned long long* ctr0, unsigned l
 // Exact early skip: α = min(0.99, o·G) < 1/255 ⇔ power < −ln(255·o).
 // Below −ln(255·o) − SKIP_MARGIN the CA value o·G is < (1/255)·e^(−1e-3)·(1 + 1e-6),
 // so the CA decision is "skip" as well; the CA exp is only evaluated above this bound.
-constexpr float SKIP_MARGIN = 1e-3f;
 
 // Warp blocks of the 16×16 tile: warp w owns a WBW × WBH block of pixels (lane → column
 // lane % WBW, row lane / WBW, and the same column WBH/2 rows further down for the thread's
