@@ -345,6 +345,14 @@ int mvgs_stage_times(mvgs_ctx *ctx, float *ms, int n);
  * Returns MVGS_ERR_INVALID for a NULL ctx. */
 mvgs_status mvgs_set_eval_counting(mvgs_ctx *ctx, int enable);
 
+/* Forward staging by TMA (Alg. 2's batched fetch): when enabled,
+ * mvgs_render_fwd stages each batch of list records with cp.async.bulk.tensor gather4 into a
+ * double-buffered shared-memory ring signalled by mbarriers, instead of per-thread loads.
+ * Results are bit-identical either way; it is off by default because it measured slower
+ * (garden forward 0.379 → 0.436 ms).  MVGS_ERR_CUDA if the driver refused the tensor map,
+ * MVGS_ERR_INVALID for a NULL ctx. */
+mvgs_status mvgs_set_tma(mvgs_ctx *ctx, int enable);
+
 #ifdef __cplusplus
 }
 #endif

@@ -6,6 +6,7 @@
 #include <utility>
 #include <vector>
 #include <cuda_runtime.h>
+#include <cuda.h>
 #include "../../include/mvgs.h"
 
 namespace mvgs {
@@ -75,6 +76,9 @@ struct mvgs_ctx {
     int device = 0;
     int64_t cap_pairs = 0, cap_entries = 0;
     int64_t cap_blk = 0, cap_buckets = 0, cap_cams = 0, cap_scan = 0;
+    CUtensorMap rec_map{};  // TMA view of d_rec (tma.cuh), re-encoded when the pair capacity changes
+    bool rec_map_ok = false;
+    bool use_tma = false;   // forward staging by TMA gather4 (mvgs_set_tma / MVGS_TMA=1); measured slower, off
     int state = 0;  // 0 none, 1 preprocessed, 2 forward done, 3 backward done, 4 partial forward done
     int partial_S = 0, partial_mode = -1;  // the partial forward's sample size and launch shape
     mvgs::Launch L{};
@@ -131,7 +135,8 @@ cudaError_t launch_dup_sort(const Launch& L, const uint32_t* order, const uint2*
 cudaError_t launch_sort_entries(const Launch& L, uint32_t** sorted_vals, cudaStream_t s);
 int64_t radix_counts_size(int64_t cap);
 int radix_tiles(int64_t cap);
-cudaError_t launch_render_fwd(const Launch& L, float* rgb, float* Tf, int32_t* nc, float* depth, cudaStream_t s);
+cudaError_t launch_render_fwd(const Launch& L, float* rgb, float* Tf, int32_t* nc, float* depth, const CUtensorMap* tm,
+                              cudaStream_t s);
 int64_t dssim_partials(int V, int H, int W);
 struct AdcParamsHost {
     float tau_split, tau_clone, ln_size, ln_split, logit_prune, ln_prune_scale;

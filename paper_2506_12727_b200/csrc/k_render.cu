@@ -19,8 +19,10 @@
 // stores — shared-memory float atomics would be CAS loops), and after the
 // batch the 4 warp slots are summed in fixed order and flushed to the pair's
 // gradient slot with one global red.add per nonzero value.
+#include <cudaTypedefs.h>
 #include "ca.cuh"
 #include "internal.cuh"
+#include "tma.cuh"
 
 namespace mvgs {
 
@@ -289,7 +291,162 @@ __global__ __launch_bounds__(RT) void k_render_fwd_p(Launch L, float* __restrict
     }
 }
 
-cudaError_t launch_render_fwd(const Launch& L, float* rgb, float* Tf, int32_t* nc, float* depth, cudaStream_t s) {
+// Forward with TMA staging (tma.cuh): the batch's records arrive by gather4 into a double
+// buffer of raw 64-byte rows (x, y, A, B) (C, o, r, g) (b, depth, skip bound, 1/o) (0 …);
+// warp 0 issues batch b+1 right after batch b's masks are built, so it lands while batch b is
+// walked.  The walk and every decision are those of k_render_fwd_p.
+template <bool DEPTH, bool CNT>
+__global__ __launch_bounds__(RT) void k_render_fwd_tma(Launch L, const __grid_constant__ CUtensorMap tm,
+                                                       float* __restrict__ out_rgb, float* __restrict__ out_T,
+                                                       int32_t* __restrict__ out_n, float* __restrict__ out_D) {
+    __shared__ __align__(128) float4 srec[2][RT][TMA_ROW_FLOATS / 4];
+    __shared__ __align__(8) uint64_t mbar[2];
+    __shared__ uint8_t smask[RT];
+    __shared__ uint8_t slist[RT / 32][RT];
+    __shared__ unsigned sev[2];
+    zero_pgrad_slice(L);
+    const int bucket = blockIdx.x;
+    const int v = bucket / L.T, tile = bucket - v * L.T;
+    const int ty = tile / L.TX, tx = tile - ty * L.TX;
+    const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+    int x, y[2];
+    pixel_pair(tx, ty, x, y[0], y[1]);
+    const int start = L.bucket_off[bucket], end = L.bucket_off[bucket + 1];
+    const int nbat = end <= L.cap_entries ? (end - start + RT - 1) / RT : 0;
+    const float2 nfx = ff2(-(float)x, -(float)x), nfy = ff2(-(float)y[0], -(float)y[1]);
+    const float2 one = ff2(1.f, 1.f), mone = ff2(-1.f, -1.f), mhalf = ff2(-0.5f, -0.5f);
+    float2 T = ff2((x < L.W && y[0] < L.H) ? 1.f : -1.f, (x < L.W && y[1] < L.H) ? 1.f : -1.f);
+    float2 C0 = ff2(0.f, 0.f), C1 = C0, C2 = C0, D = C0;
+    int last0 = 0, last1 = 0;
+    unsigned nev = 0, nexp = 0;
+    if (threadIdx.x == 0) {
+        sev[0] = sev[1] = 0;
+        mbar_init(&mbar[0], 1);
+        mbar_init(&mbar[1], 1);
+        mbar_fence_init();
+    }
+    __syncthreads();
+    // warp 0 holds the pair slots of the next batch to issue (4 per lane), loaded a batch early
+    int qi[4] = {0, 0, 0, 0};
+    auto load_idx = [&](int b) {
+        const int e = start + b * RT + 4 * lane;
+#pragma unroll
+        for (int i = 0; i < 4; i++) qi[i] = (b < nbat && e + i < end) ? (int)L.sorted[e + i] : 0;
+    };
+    auto issue = [&](int b) {  // warp 0: batch b's records → srec[b & 1]
+        const int cnt = min(RT, end - (start + b * RT));
+        const int ng = (cnt + 3) >> 2;
+        if (lane == 0) mbar_arrive_expect_tx(&mbar[b & 1], (unsigned)(ng * 4 * TMA_ROW_BYTES));
+        __syncwarp();
+        if (lane < ng) tma_gather4(&srec[b & 1][4 * lane][0], &tm, &mbar[b & 1], qi[0], qi[1], qi[2], qi[3]);
+    };
+    if (wl == 0 && nbat > 0) {
+        load_idx(0);
+        issue(0);
+        load_idx(1);
+    }
+    for (int b = 0; b < nbat; b++) {
+        const int buf = b & 1;
+        const int b0 = start + b * RT;
+        const int cnt = min(RT, end - b0);
+        mbar_wait(&mbar[buf], (unsigned)((b >> 1) & 1));
+        if ((int)threadIdx.x < cnt) {
+            const float4 r0 = srec[buf][threadIdx.x][0], r1 = srec[buf][threadIdx.x][1];
+            const float sb = srec[buf][threadIdx.x][2].z;
+            smask[threadIdx.x] = (uint8_t)warp_block_mask(r0.x, r0.y, r0.z, r0.w, r1.x, sb, (float)(tx * TILE),
+                                                          (float)(ty * TILE));
+        }
+        // masks ready, batch b−1's walk (buffer buf ^ 1) finished everywhere
+        if (__syncthreads_count(T.x < 0.f && T.y < 0.f) == RT) break;  // nothing in flight here
+        if (wl == 0 && b + 1 < nbat) {
+            issue(b + 1);
+            load_idx(b + 2);
+        }
+        const int jbase = b0 - start + 1;  // list index + 1 of batch entry 0
+        const int nl = warp_batch_list(smask, cnt, wl, lane, slist[wl]);
+        const float4(*rb)[TMA_ROW_FLOATS / 4] = srec[buf];
+#pragma unroll(kFwdUnroll)
+        for (int u = 0; u < nl && !(T.x < 0.f && T.y < 0.f); u++) {
+            const int j = slist[wl][u];
+            if (CNT) nev += (unsigned)(T.x > 0.f) + (unsigned)(T.y > 0.f);
+            const float4 e0 = rb[j][0], e2 = rb[j][2];  // (x, y, A, B), (b, depth, sb, 1/o)
+            const float Cc = rb[j][1].x;
+            const float2 dx = __fadd2_rn(ff2(e0.x, e0.x), nfx);
+            const float2 dy = __fadd2_rn(ff2(e0.y, e0.y), nfy);
+            const float2 Adx = __fmul2_rn(ff2(e0.z, e0.z), dx);
+            const float2 CdyDy = __fmul2_rn(__fmul2_rn(ff2(Cc, Cc), dy), dy);
+            const float2 inner = __ffma2_rn(Adx, dx, CdyDy);
+            const float2 nBdxdy = __fmul2_rn(__fmul2_rn(ff2(-e0.w, -e0.w), dx), dy);
+            const float2 power = __ffma2_rn(mhalf, inner, nBdxdy);
+            const bool in0 = T.x > 0.f && !(power.x > 0.f) && !(power.x < e2.z);
+            const bool in1 = T.y > 0.f && !(power.y > 0.f) && !(power.y < e2.z);
+            if (!(in0 || in1)) continue;
+            if (CNT) nexp += (unsigned)in0 + (unsigned)in1;
+            const float4 e1 = rb[j][1];  // (C, o, r, g)
+            const float2 G = ca_exp_core2(power);
+            const float2 oG = __fmul2_rn(ff2(e1.y, e1.y), G);
+            const float2 alpha = ff2(fminf(ALPHA_MAX, oG.x), fminf(ALPHA_MAX, oG.y));
+            const bool ok0 = in0 && !(alpha.x < ALPHA_MIN), ok1 = in1 && !(alpha.y < ALPHA_MIN);
+            if (!(ok0 || ok1)) continue;
+            const float2 Tn = __fmul2_rn(T, __ffma2_rn(alpha, mone, one));  // T·(1 − α), CA
+            const bool term0 = ok0 && Tn.x < T_EPS, term1 = ok1 && Tn.y < T_EPS;
+            const bool bl0 = ok0 && !term0, bl1 = ok1 && !term1;
+            const float2 w = __fmul2_rn(ff2(bl0 ? alpha.x : 0.f, bl1 ? alpha.y : 0.f), T);
+            C0 = __ffma2_rn(ff2(e1.z, e1.z), w, C0);
+            C1 = __ffma2_rn(ff2(e1.w, e1.w), w, C1);
+            C2 = __ffma2_rn(ff2(e2.x, e2.x), w, C2);
+            if (DEPTH) D = __ffma2_rn(ff2(e2.y, e2.y), w, D);
+            T = ff2(bl0 ? Tn.x : (term0 ? -T.x : T.x), bl1 ? Tn.y : (term1 ? -T.y : T.y));
+            const int jn = jbase + j;
+            last0 = bl0 ? jn : last0;
+            last1 = bl1 ? jn : last1;
+        }
+    }
+    if (CNT) count_evals(&L.counters64[0], &L.counters64[2], nev, nexp, sev);
+    const int64_t HW = (int64_t)L.H * L.W;
+    const float Cs[2][3] = {{C0.x, C1.x, C2.x}, {C0.y, C1.y, C2.y}};
+    const float Ts[2] = {fabsf(T.x), fabsf(T.y)}, Ds[2] = {D.x, D.y};
+    const int ls[2] = {last0, last1};
+#pragma unroll
+    for (int p = 0; p < 2; p++) {
+        if (!(x < L.W && y[p] < L.H)) continue;
+        const int64_t pix = (int64_t)y[p] * L.W + x;
+        out_rgb[(3 * (int64_t)v + 0) * HW + pix] = __fmaf_rn(Ts[p], L.bg[0], Cs[p][0]);  // CA: fma(T, bg, C)
+        out_rgb[(3 * (int64_t)v + 1) * HW + pix] = __fmaf_rn(Ts[p], L.bg[1], Cs[p][1]);
+        out_rgb[(3 * (int64_t)v + 2) * HW + pix] = __fmaf_rn(Ts[p], L.bg[2], Cs[p][2]);
+        out_T[v * HW + pix] = Ts[p];
+        out_n[v * HW + pix] = ls[p];
+        if (DEPTH) out_D[v * HW + pix] = Ds[p];
+    }
+}
+
+bool encode_record_map(CUtensorMap* tm, const void* rec, int64_t cap_pairs) {
+    static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
+    if (!enc) {
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&enc, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            return false;
+    }
+    const cuuint64_t dims[2] = {12, (cuuint64_t)(cap_pairs > 0 ? cap_pairs : 1)};
+    const cuuint64_t strides[1] = {48};
+    const cuuint32_t box[2] = {TMA_ROW_FLOATS, 1}, es[2] = {1, 1};
+    return enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(rec), dims, strides, box, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+cudaError_t launch_render_fwd(const Launch& L, float* rgb, float* Tf, int32_t* nc, float* depth, const CUtensorMap* tm,
+                              cudaStream_t s) {
+    if (tm) {
+        if (depth)
+            k_render_fwd_tma<true, true><<<L.V * L.T, RT, 0, s>>>(L, *tm, rgb, Tf, nc, depth);
+        else if (L.count_evals)
+            k_render_fwd_tma<false, true><<<L.V * L.T, RT, 0, s>>>(L, *tm, rgb, Tf, nc, nullptr);
+        else
+            k_render_fwd_tma<false, false><<<L.V * L.T, RT, 0, s>>>(L, *tm, rgb, Tf, nc, nullptr);
+        return cudaGetLastError();
+    }
     if (depth)
         k_render_fwd_p<true, true><<<L.V * L.T, RT, 0, s>>>(L, rgb, Tf, nc, depth);
     else if (L.count_evals)

@@ -8,6 +8,7 @@
 #include <new>
 #include "ca.cuh"
 #include "internal.cuh"
+#include "tma.cuh"
 
 using namespace mvgs;
 
@@ -71,6 +72,7 @@ cudaError_t alloc_pairs(mvgs_ctx* c, int64_t n) {
     if ((e = cudaMalloc(&c->d_pflag, sizeof(uint32_t) * n)) != cudaSuccess) return e;
     if ((e = cudaMalloc(&c->d_prect2, sizeof(uint2) * n)) != cudaSuccess) return e;
     c->cap_pairs = n;
+    c->rec_map_ok = mvgs::encode_record_map(&c->rec_map, c->d_rec, n);
     return cudaSuccess;
 }
 
@@ -194,6 +196,7 @@ mvgs_status mvgs_create(mvgs_ctx** out, int device, int64_t max_pairs, int64_t m
     mvgs_ctx* ctx = new (std::nothrow) mvgs_ctx();
     if (!ctx) return MVGS_ERR_INVALID;
     ctx->device = device;
+    if (const char* m = getenv("MVGS_TMA")) ctx->use_tma = strcmp(m, "1") == 0;
     cudaError_t e = cudaSetDevice(device);
     if (e != cudaSuccess) {
         delete ctx;
@@ -363,7 +366,8 @@ mvgs_status mvgs_render_fwd_depth(mvgs_ctx* ctx, float* rgb, float* T_final, int
     cudaStream_t s = (cudaStream_t)stream;
     CK(cudaMemsetAsync(ctx->d_counters64, 0, sizeof(unsigned long long), s));
     CK(cudaMemsetAsync(ctx->d_counters64 + 2, 0, sizeof(unsigned long long), s));
-    { STAGE(ST_FWD); CK(launch_render_fwd(ctx->L, rgb, T_final, n_contrib, depth, s)); }  // S6
+    const CUtensorMap* tm = (ctx->use_tma && ctx->rec_map_ok) ? &ctx->rec_map : nullptr;
+    { STAGE(ST_FWD); CK(launch_render_fwd(ctx->L, rgb, T_final, n_contrib, depth, tm, s)); }  // S6
     ctx->state = 2;
     return MVGS_OK;
 }
@@ -489,6 +493,13 @@ mvgs_status mvgs_export_pairs(mvgs_ctx* ctx, int32_t* pair_ids, int32_t* pair_i,
 mvgs_status mvgs_set_debug_blend_counts(mvgs_ctx* ctx, int32_t* nblend) {
     if (!ctx) return MVGS_ERR_INVALID;
     ctx->L.dbg_nblend = nblend;
+    return MVGS_OK;
+}
+
+mvgs_status mvgs_set_tma(mvgs_ctx* ctx, int enable) {
+    if (!ctx) return MVGS_ERR_INVALID;
+    if (enable && !ctx->rec_map_ok) return fail(ctx, MVGS_ERR_CUDA, "the driver refused the record tensor map");
+    ctx->use_tma = enable != 0;
     return MVGS_OK;
 }
 

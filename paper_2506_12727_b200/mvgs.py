@@ -22,7 +22,7 @@ SYMBOLS = ["mvgs_create", "mvgs_destroy", "mvgs_last_error", "mvgs_reserve", "mv
            "mvgs_render_bwd", "mvgs_adc_stats", "mvgs_adc_stats_range", "mvgs_query", "mvgs_export_lists", "mvgs_export_pairs",
            "mvgs_set_timing", "mvgs_stage_times", "mvgs_set_eval_counting", "mvgs_render_fwd_partial", "mvgs_render_bwd_partial",
            "mvgs_render_fwd_depth", "mvgs_dssim3d", "mvgs_adc_step", "mvgs_adc_remap",
-           "mvgs_loss_grad", "mvgs_grad_moments", "mvgs_grad_variance", "mvgs_set_debug_blend_counts"]
+           "mvgs_loss_grad", "mvgs_grad_moments", "mvgs_grad_variance", "mvgs_set_debug_blend_counts", "mvgs_set_tma"]
 PARTIAL_THREAD_EFFICIENT, PARTIAL_MASKED = 0, 1
 STAGE_NAMES = ["count", "scan_pairs", "project", "scan_buckets", "sort_pairs", "dup", "sort_entries", "render_fwd",
                "render_bwd", "gauss_bwd", "dssim"]
@@ -104,6 +104,7 @@ def _load():
     L.mvgs_export_pairs.argtypes = [vp, vp, vp, vp, vp, vp]
     L.mvgs_set_timing.argtypes = [vp, C.c_int]
     L.mvgs_set_eval_counting.argtypes = [vp, C.c_int]
+    L.mvgs_set_tma.argtypes = [vp, C.c_int]
     L.mvgs_set_debug_blend_counts.argtypes = [vp, vp]
     L.mvgs_render_fwd_partial.argtypes = [vp, vp, C.c_int32, C.c_int32, vp, vp, vp, vp]
     L.mvgs_render_bwd_partial.argtypes = [vp, vp, C.c_int32, C.c_int32, vp, vp, vp, vp]
@@ -315,6 +316,11 @@ def set_debug_blend_counts(ctx, nblend=None):
 
 def set_timing(ctx, enable: bool):
     _check(ctx, _lib.mvgs_set_timing(ctx, int(bool(enable))))
+
+
+def set_tma(ctx, enable: bool):
+    """Forward staging by TMA gather4 (bit-identical results; off by default, measured slower)."""
+    _check(ctx, _lib.mvgs_set_tma(ctx, int(bool(enable))))
 
 
 def set_eval_counting(ctx, enable: bool):

@@ -524,3 +524,29 @@ def test_more_than_32_views():
     bits (V > 32 re-derives them) — lists, counts, images and gradients as the oracle's."""
     g, cams = synth.make_scene(synth.scaled(synth.CONFIGS["tiny"], P=400, V=40, W=40, H=24))
     _check_all(g, cams, bg=(0.1, 0.0, 0.2), seed=8)
+
+
+@pytest.mark.gpu
+def test_tma_staged_forward_is_bit_identical(require_gpu):
+    """The forward with TMA gather4 staging (mvgs_set_tma) against the default per-thread staging:
+    images, T_final and n_contrib bit-identical, on a scene with lists of many batches."""
+    import dataclasses
+
+    import torch
+
+    from gpu_harness import to_dev
+    from paper_2506_12727_b200 import mvgs
+    cfg = dataclasses.replace(synth.CONFIGS["tiny"], P=20_000)
+    g, cams = synth.make_scene(cfg)
+    out = []
+    for tma in (False, True):
+        R = mvgs.Rasterizer(0)
+        mvgs.set_tma(R.ctx, tma)
+        R.preprocess(to_dev(g), cams)
+        rgb, Tf, nc = R.forward()
+        torch.cuda.synchronize()
+        out.append((rgb.cpu().numpy(), Tf.cpu().numpy(), nc.cpu().numpy(), R.stats["max_bucket"]))
+        del R
+    assert out[0][3] > 512  # several staged batches per list
+    for a, b in zip(out[0][:3], out[1][:3]):
+        np.testing.assert_array_equal(a, b)
