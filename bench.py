@@ -56,6 +56,11 @@ def parse():
     ap.add_argument("--views", type=int, default=0,
                     help="views per GPU per step (default: the config's batch); the views-per-batch sweep")
     ap.add_argument("--impl", default="mvgs", choices=["mvgs", "reference"])
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="weak: the config's batch per GPU; strong: the config's batch split over the GPUs "
+                         "(SURVEY §8(d): large, 32 views)")
+    ap.add_argument("--exchange", default="allreduce", choices=["allreduce", "owner"],
+                    help="N>1 exchange: chunked all-reduce of the flat buffer, or owner-sharded slots (DESIGN §11)")
     ap.add_argument("--e2e-steps", type=int, default=16)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile", action="store_true",
@@ -176,12 +181,16 @@ def run_mvgs(args):
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2506_12727_b200 import mvgs
-    from paper_2506_12727_b200.dist import GradBuffer, adc_stats_allreduce, view_shard
+    from paper_2506_12727_b200.dist import GradBuffer, adc_stats_allreduce, adc_stats_owner, owner_bounds, view_shard
 
     cfg = synth.CONFIGS[args.config]
-    Vr = args.views or cfg.V  # views per rank (weak scaling: the per-GPU batch is fixed)
-    g_np, cams_all = synth.make_scene(synth.scaled(cfg, V=Vr * N))
-    lo, hi = view_shard(Vr * N, N, rank)
+    if args.scaling == "weak":  # the per-GPU batch is fixed
+        V_all = (args.views or cfg.V) * N
+    else:  # strong: the batch is fixed and split over the GPUs
+        V_all = args.views or cfg.V
+    g_np, cams_all = synth.make_scene(synth.scaled(cfg, V=V_all))
+    lo, hi = view_shard(V_all, N, rank)
+    Vr = hi - lo
     cams = synth.subset_views(cams_all, lo, hi)
     P = g_np["means"].shape[0]
     NK = (g_np["sh_degree"] + 1) ** 2
@@ -197,14 +206,24 @@ def run_mvgs(args):
     mvgs.reserve(R.ctx, int(st0["Q"] * 1.15) + 4096, int(st0["K"] * 1.15) + 65536)
     # one flat buffer for every output that is a sum over views (single all-reduce)
     # with N > 1, chunk-major so each chunk's all-reduce overlaps the next chunk's kernel
-    CHUNKS = int(os.environ.get("MVGS_AR_CHUNKS", "4")) if dist is not None else 1
-    buf = GradBuffer(P, S, dev, chunks=CHUNKS)
+    CHUNKS = int(os.environ.get("MVGS_AR_CHUNKS", "4")) if (dist is not None and args.exchange == "allreduce") else 1
+    owner = args.exchange == "owner"
+    if owner:  # this rank's outputs: the full sums of the Gaussians it owns (reduce-scatter semantics)
+        ob = owner_bounds(P, N)
+        buf = GradBuffer(int(ob[rank + 1] - ob[rank]), S, dev)
+    else:
+        buf = GradBuffer(P, S, dev, chunks=CHUNKS)
     flat = buf.flat
     outs = R.alloc_forward()
 
+    checked = [False]  # the first (warm-up) exchange verifies every slice size across ranks
+
     def grads_out(b):
         mvgs.render_bwd(R.ctx, dL_cur[0], outs[1], outs[2])
-        if dist is None:
+        if owner:
+            adc_stats_owner(R.ctx, P, cams_all, rank, N, b.grads, b.adc, check=not checked[0])
+            checked[0] = True
+        elif dist is None:
             mvgs.adc_stats(R.ctx, b.grads, b.adc)
         else:
             adc_stats_allreduce(R.ctx, b)
@@ -251,7 +270,7 @@ def run_mvgs(args):
         t = torch.tensor([ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    views_total = Vr * N
+    views_total = V_all
     value = views_total / (ms / 1e3)
 
     # ---- e2e: the same step through the public API with HOST buffers: every step copies
@@ -267,7 +286,7 @@ def run_mvgs(args):
     d2h = host_out[0].numel() * 4
     g_slots = [g, {k: (torch.empty_like(v) if torch.is_tensor(v) else v) for k, v in g.items()}]
     dL_slots = [dL, torch.empty_like(dL)]
-    bufs = [buf, GradBuffer(P, S, dev, chunks=CHUNKS)]
+    bufs = [buf, GradBuffer(buf.P, S, dev, chunks=CHUNKS)]
     comp = torch.cuda.current_stream()
     s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
     mk = lambda: [torch.cuda.Event() for _ in range(2)]  # noqa: E731
@@ -345,9 +364,10 @@ def run_mvgs(args):
 
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": N, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": args.scaling,
         "vs_baseline": None, "dtype": "f32", "data": "synthetic (mvgs-synth v1, seeded; DESIGN.md §6)",
-        "config": {**workload_config(cfg, P, Vr, N),
+        "config": {**workload_config(cfg, P, Vr, N, V_all),
+                   "exchange": args.exchange if N > 1 or owner else "none (1 GPU)",
                    "allreduce_chunks": CHUNKS,
                    "l2": "inputs larger than L2 (params %.0f MB)" % (sum(v.nbytes for v in g_np.values()
                                                                        if isinstance(v, np.ndarray)) / 1e6),
@@ -432,9 +452,11 @@ def cpu_baseline(cfg, g_np, cams, dL):
     return {"value": round(vps, 5), "unit": UNIT, "cores": th, "kind": "oracle", "sample": sample}
 
 
-def workload_config(cfg, P, Vr, N):
-    return {"workload": f"{cfg.name}: {P} Gaussians SH{cfg.sh_degree}, {Vr} views/GPU at {cfg.W}x{cfg.H}",
-            "views_per_step": Vr * N, "global_batch_views": Vr * N, "parallelism": f"views dp{N}"}
+def workload_config(cfg, P, Vr, N, V_all=None):
+    V_all = Vr * N if V_all is None else V_all
+    per = f"{Vr} views/GPU" if V_all == Vr * N else f"{V_all} views over {N} GPUs"
+    return {"workload": f"{cfg.name}: {P} Gaussians SH{cfg.sh_degree}, {per} at {cfg.W}x{cfg.H}",
+            "views_per_step": V_all, "global_batch_views": V_all, "parallelism": f"views dp{N}"}
 
 
 def run_reference(args):

@@ -179,6 +179,39 @@ mvgs_status mvgs_adc_stats(mvgs_ctx *ctx, const mvgs_grads *grads, const mvgs_ad
 mvgs_status mvgs_adc_stats_range(mvgs_ctx *ctx, int64_t g_begin, int64_t g_end, const mvgs_grads *grads,
                                  const mvgs_adc *adc, void *stream);
 
+/* ---- Owner-sharded exchange (SURVEY §8(e) lever 3) ------------------------
+ * Every output is a sum over views, so instead of all-reducing
+ * 4·(11+S+5)·P bytes of per-Gaussian outputs, ranks can send each per-pair gradient slot
+ * (48 B: Σ∇, e1, ∂conic, ∂o, ∂rgb and the pair's flags) to the rank that OWNS its Gaussian; the
+ * owner lays out all views' slots of its Gaussians exactly as a single GPU would (the same
+ * participation decisions and ballot ranking) and runs S8–S9 over all views.  E1, E2 and
+ * E_old are then exact; the owner holds the full sums for its range (reduce-scatter semantics).
+ *
+ * mvgs_owner_slices (after mvgs_render_bwd): for this context's views and owners
+ *   [g_bounds[o], g_bounds[o+1]) (g_bounds host [N+1], 0 = first, P = last, multiples of 256 or P),
+ *   writes slot_off (host [V][N+1]): owner o's slots of local view v are
+ *   [slot_off[v][o], slot_off[v][o+1]) of the slot array returned in *slots (device,
+ *   PG_STRIDE = 12 floats per slot).  Synchronises the stream.
+ * mvgs_owner_prepare: this context owns [g_begin, g_end) (g_begin % 256 == 0, or an empty range) of the Gaussians
+ *   of its last preprocess; cams_all (host [V_all]) are every rank's views in global order.
+ *   Builds the owner's slot layout and writes view_off (host [V_all+1]): view v's slots go to
+ *   [view_off[v], view_off[v+1]) of *recv (device, context-owned, 12 floats per slot) —
+ *   exactly as many as the renderer of view v reports for this owner.  Synchronises.
+ * mvgs_owner_adc_stats: S8–S9 of the owned range over all views from *recv; outputs are
+ *   addressed relative to g_begin (as mvgs_adc_stats_range).  MVGS_ERR_STATE without a
+ *   preceding mvgs_owner_prepare. */
+mvgs_status mvgs_owner_slices(mvgs_ctx *ctx, const int64_t *g_bounds, int32_t N, int64_t *slot_off, float **slots,
+                              void *stream);
+mvgs_status mvgs_owner_prepare(mvgs_ctx *ctx, const mvgs_camera *cams_all, int32_t V_all, int64_t g_begin,
+                               int64_t g_end, int64_t *view_off, float **recv, void *stream);
+mvgs_status mvgs_owner_adc_stats(mvgs_ctx *ctx, const mvgs_grads *grads, const mvgs_adc *adc, void *stream);
+
+/* E_old = ‖gsum‖ for n Gaussians (R49): gsum device [n,2] (8-B aligned), e_old [n] overwritten
+ * and/or e_old_acc [n] += (either may be NULL, not both).  Used after a multi-GPU sum of gsum,
+ * where E_old is not additive but gsum is. */
+mvgs_status mvgs_e_old_from_gsum(mvgs_ctx *ctx, const float *gsum, int64_t n, float *e_old, float *e_old_acc,
+                                 void *stream);
+
 /* NEXT-2: the 3D distance-aware D-SSIM loss and its gradient.
  *   SSIM = (2μ1μ2 + C1)(2τ12 + C2) / ((μ1² + μ2² + C1)(τ1² + τ2² + C2))
  * with the moments μ, τ taken under the 3D kernel

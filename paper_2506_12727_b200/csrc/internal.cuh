@@ -15,6 +15,7 @@ constexpr int BLK = 256;          // Gaussians per preprocessing block (pair-slo
 constexpr int NG = 10;            // per-pair gradient record: Σ∇x Σ∇y e1 ∂A ∂B ∂C ∂o ∂r ∂g ∂b
 constexpr int PG_STRIDE = 12;     // floats per pair-gradient slot (48 B, 16-B aligned)
 constexpr int REC_F4 = 3;         // float4 per pair render record (48 B)
+constexpr int PG_FLAGS = 10;      // float of a gradient slot that carries the pair's flags word
 constexpr uint32_t PF_VISIBLE = 32u;
 constexpr int PF_RADIUS_SHIFT = 8;  // pflag bits 8..31: the pair's CA radius (R7), saturated at 2^24 − 1
 
@@ -60,13 +61,19 @@ struct Launch {  // everything a kernel needs about the current batch
 // backward accumulates into (red.add).  The forward kernels are compute-bound with
 // little DRAM traffic, so these fire-and-forget stores ride along instead of costing
 // the HBM-bound projection 48 B per pair; each CTA clears one grid-strided slice.
+// The slot's 11th float (PG_FLAGS) carries the pair's flags word (pflag), so a gradient slot is
+// a self-contained 48-byte record: the per-Gaussian kernel needs no second load, and an owner
+// rank can receive slots from other ranks and run the chain on them.
 __device__ __forceinline__ void zero_pgrad_slice(const Launch& L) {
     const int64_t Q = min((int64_t)L.counters[C_Q], L.cap_pairs);
     float4* p4 = reinterpret_cast<float4*>(L.pgrad);
     const int64_t n4 = Q * (PG_STRIDE / 4);
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride)
-        p4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride) {
+        const int64_t q = i / (PG_STRIDE / 4);
+        const bool last = i - q * (PG_STRIDE / 4) == PG_STRIDE / 4 - 1;
+        p4[i] = make_float4(0.f, 0.f, last ? __uint_as_float(L.pflag[q]) : 0.f, 0.f);
+    }
 }
 #endif
 
@@ -117,6 +124,22 @@ struct mvgs_ctx {
     int64_t cap_adc_tmp = 0;
     unsigned long long* d_adc_rep = nullptr;  // [4] split, clone, pruned, total
     long long* h_adc_rep = nullptr;           // pinned mirror
+    // owner-sharded exchange: the layout of ALL views' pair slots of the
+    // Gaussians [og_begin, og_end) this rank owns, and the slots received from the other ranks
+    mvgs::Launch Lo{};
+    mvgs_camera* d_ocams = nullptr;
+    int64_t cap_ocams = 0;
+    int* d_oblk = nullptr;          // [V_all * NB + 1] scanned participation counts (owner blocks only)
+    int64_t cap_oblk = 0;
+    int* d_oscan = nullptr;         // scan scratch
+    int64_t cap_oscan = 0;
+    uint32_t* d_opmask = nullptr;   // [P] participation bits of the owned Gaussians in all views (V_all ≤ 32)
+    int64_t cap_opmask = 0;
+    float* d_orecv = nullptr;       // [Q_own * PG_STRIDE] gradient slots of the owned Gaussians, all views
+    int64_t cap_orecv = 0;          // in slots
+    int64_t og_begin = 0, og_end = 0;
+    bool owner_ready = false;
+    std::vector<int> h_blk;         // host copy of blk_off (slice offsets)
     cudaStream_t last_stream = nullptr;
     bool timing = false;
     bool count_evals = true;
@@ -129,6 +152,8 @@ namespace mvgs {
 // launchers (return cudaGetLastError())
 cudaError_t scan_exclusive(int* a, int n, int* total_slot, int* tmp, cudaStream_t s, const int* n_live = nullptr);
 cudaError_t launch_count(const Launch& L, cudaStream_t s);
+cudaError_t launch_count_range(const Launch& L, int b0, int b1, cudaStream_t s);
+cudaError_t launch_e_old(const float* gsum, int64_t n, float* e_old, float* e_old_acc, cudaStream_t s);
 cudaError_t launch_project(const Launch& L, cudaStream_t s);
 cudaError_t launch_sort_pairs(const Launch& L, const uint32_t** order_out, const uint2** rect_out, cudaStream_t s);
 cudaError_t launch_dup_sort(const Launch& L, const uint32_t* order, const uint2* rect, cudaStream_t s);

@@ -497,16 +497,16 @@ __global__ __launch_bounds__(BLK, MVGS_GB_MINB) void k_gauss_bwd(Launch L, mvgs_
                 if (!zvis) continue;
                 const int64_t pair = (int64_t)sboff[k] + wc[warp][k] + __popc(bal & lt);
                 if (pair >= L.cap_pairs) continue;
-                // flags and gradient slot loaded together (the slot is ignored for inert pairs;
-                // loading it only after the flag was measured slower: one more dependent trip)
-                fl[u] = L.pflag[pair];
+                // the gradient slot carries the pair's flags word in float PG_FLAGS (the slot of an
+                // inert pair holds zeros and its flags, which say it is inert)
                 const float4* pgp = reinterpret_cast<const float4*>(L.pgrad + pair * PG_STRIDE);
                 pga[u] = pgp[0];
                 pgb[u] = pgp[1];
                 pgc[u] = pgp[2];
+                fl[u] = __float_as_uint(pgc[u].z);
             }
 #if GB_PREFETCH
-            // the next GB_PREFETCH views' flags and gradient slots toward L2 while this view computes
+            // the next GB_PREFETCH views' gradient slots toward L2 while this view computes
 #pragma unroll
             for (int pd = 1; pd <= GB_PREFETCH; pd++) {
                 const int kn = k0 + pd * VB;
@@ -515,10 +515,7 @@ __global__ __launch_bounds__(BLK, MVGS_GB_MINB) void k_gauss_bwd(Launch L, mvgs_
                     const unsigned baln = __ballot_sync(FULLG, zn);
                     if (zn) {
                         const int64_t pn = (int64_t)sboff[kn] + wc[warp][kn] + __popc(baln & lt);
-                        if (pn < L.cap_pairs) {
-                            asm volatile("prefetch.global.L2 [%0];" ::"l"(L.pflag + pn));
-                            asm volatile("prefetch.global.L2 [%0];" ::"l"(L.pgrad + pn * PG_STRIDE));
-                        }
+                        if (pn < L.cap_pairs) asm volatile("prefetch.global.L2 [%0];" ::"l"(L.pgrad + pn * PG_STRIDE));
                     }
                 }
             }
@@ -587,6 +584,23 @@ cudaError_t launch_gauss_bwd(const Launch& L, const mvgs_grads& gr, const mvgs_a
         case 2: return launch_gauss_bwd_t<2>(L, gr, adc, gb, ge, s);
         default: return launch_gauss_bwd_t<3>(L, gr, adc, gb, ge, s);
     }
+}
+
+// E_old = ‖Σ_views Σ_pixels ∇_{p_i}L‖ from the summed vector gsum [P,2] (R49): after a
+// multi-GPU sum of gsum, every rank's E_old is the single-GPU one.
+__global__ void k_e_old(const float* __restrict__ gsum, int64_t n, float* __restrict__ e_old,
+                        float* __restrict__ e_old_acc) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const float2 v = reinterpret_cast<const float2*>(gsum)[i];
+    const float e = sqrtf(v.x * v.x + v.y * v.y);
+    if (e_old) e_old[i] = e;
+    if (e_old_acc) e_old_acc[i] += e;
+}
+
+cudaError_t launch_e_old(const float* gsum, int64_t n, float* e_old, float* e_old_acc, cudaStream_t s) {
+    if (n > 0) k_e_old<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(gsum, n, e_old, e_old_acc);
+    return cudaGetLastError();
 }
 
 }  // namespace mvgs

@@ -169,12 +169,13 @@ cudaError_t scan_exclusive(int* a, int n, int* total_slot, int* tmp, cudaStream_
 }
 
 // ------------------------------------------------------------------ S1
-__global__ __launch_bounds__(BLK) void k_count(Launch L) {
+__global__ __launch_bounds__(BLK) void k_count(Launch L, int blk0) {  // blocks blk0 + blockIdx.x
     __shared__ int wc[BLK / 32][32];
     __shared__ mvgs_camera scams[32];  // the chunk's cameras (LDS instead of per-field global loads)
     __shared__ PartCam spc[32];        // and the bound's per-camera constants
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int64_t g = (int64_t)blockIdx.x * BLK + threadIdx.x;
+    const int blk = blk0 + blockIdx.x;
+    const int64_t g = (int64_t)blk * BLK + threadIdx.x;
     const bool valid = g < L.P;
     float mx = 0.f, my = 0.f, mz = 0.f, smax = 0.f;
     if (valid) {
@@ -204,14 +205,20 @@ __global__ __launch_bounds__(BLK) void k_count(Launch L) {
             int s = 0;
 #pragma unroll
             for (int w = 0; w < BLK / 32; w++) s += wc[w][threadIdx.x];
-            L.blk_off[(int64_t)(v0 + threadIdx.x) * L.NB + blockIdx.x] = s;
+            L.blk_off[(int64_t)(v0 + threadIdx.x) * L.NB + blk] = s;
         }
         __syncthreads();
     }
 }
 
 cudaError_t launch_count(const Launch& L, cudaStream_t s) {
-    k_count<<<L.NB, BLK, 0, s>>>(L);
+    k_count<<<L.NB, BLK, 0, s>>>(L, 0);
+    return cudaGetLastError();
+}
+
+// Participation counts of the 256-Gaussian blocks [b0, b1) only (an owner rank's range, §11).
+cudaError_t launch_count_range(const Launch& L, int b0, int b1, cudaStream_t s) {
+    if (b1 > b0) k_count<<<b1 - b0, BLK, 0, s>>>(L, b0);
     return cudaGetLastError();
 }
 

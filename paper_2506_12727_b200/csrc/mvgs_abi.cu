@@ -235,6 +235,7 @@ void mvgs_destroy(mvgs_ctx* ctx) {
     cudaFree(ctx->d_counters); cudaFree(ctx->d_counters64); cudaFree(ctx->d_scan);
     cudaFree(ctx->d_dssim_coef); cudaFree(ctx->d_dssim_part);
     cudaFree(ctx->d_lab_part); cudaFree(ctx->d_pmask);
+    cudaFree(ctx->d_ocams); cudaFree(ctx->d_oblk); cudaFree(ctx->d_oscan); cudaFree(ctx->d_opmask); cudaFree(ctx->d_orecv);
     cudaFree(ctx->d_adc_cnt); cudaFree(ctx->d_adc_flags); cudaFree(ctx->d_adc_tmp); cudaFree(ctx->d_adc_rep);
     if (ctx->h_adc_rep) cudaFreeHost(ctx->h_adc_rep);
     for (int i = 0; i < MVGS_NUM_STAGES; i++)
@@ -642,6 +643,118 @@ mvgs_status mvgs_grad_variance(mvgs_ctx* ctx, const double* sum, int64_t n, cons
         return fail(ctx, MVGS_ERR_INVALID, "grad_variance: bad arguments");
     CK(cudaSetDevice(ctx->device));
     CK(launch_variance(sum, n, sumsq, K, variance, ctx->d_lab_part, (cudaStream_t)stream));
+    return MVGS_OK;
+}
+
+// ---------------------------------------------------------------- owner-sharded exchange (§11)
+mvgs_status mvgs_owner_slices(mvgs_ctx* ctx, const int64_t* g_bounds, int32_t N, int64_t* slot_off, float** slots,
+                              void* stream) {
+    if (!ctx) return MVGS_ERR_INVALID;
+    if (ctx->state != 3) return fail(ctx, MVGS_ERR_STATE, "owner_slices needs a preceding render_bwd");
+    if (!g_bounds || !slot_off || !slots || N < 1) return fail(ctx, MVGS_ERR_INVALID, "owner_slices: bad arguments");
+    const Launch& L = ctx->L;
+    if (g_bounds[0] != 0 || g_bounds[N] != L.P) return fail(ctx, MVGS_ERR_INVALID, "owner_slices: bounds must span [0, P]");
+    for (int o = 0; o < N; o++)
+        if (g_bounds[o + 1] < g_bounds[o] || ((g_bounds[o] % BLK) != 0 && g_bounds[o] != L.P))
+            return fail(ctx, MVGS_ERR_INVALID, "owner_slices: bounds ascending, multiples of 256");
+    CK(cudaSetDevice(ctx->device));
+    cudaStream_t s = (cudaStream_t)stream;
+    const int64_t n = (int64_t)L.V * L.NB + 1;
+    ctx->h_blk.resize((size_t)n);
+    CK(cudaMemcpyAsync(ctx->h_blk.data(), ctx->d_blk, sizeof(int) * n, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    for (int v = 0; v < L.V; v++)
+        for (int o = 0; o <= N; o++) {
+            const int64_t b = (g_bounds[o] + BLK - 1) / BLK;  // first block of owner o (NB for the end)
+            slot_off[(int64_t)v * (N + 1) + o] =
+                b >= L.NB ? ctx->h_blk[(size_t)(v + 1) * L.NB] : ctx->h_blk[(size_t)v * L.NB + b];
+        }
+    *slots = ctx->d_pgrad;
+    return MVGS_OK;
+}
+
+mvgs_status mvgs_owner_prepare(mvgs_ctx* ctx, const mvgs_camera* cams_all, int32_t V_all, int64_t g_begin,
+                               int64_t g_end, int64_t* view_off, float** recv, void* stream) {
+    if (!ctx) return MVGS_ERR_INVALID;
+    if (ctx->state < 1) return fail(ctx, MVGS_ERR_STATE, "owner_prepare needs a preprocess (the Gaussians)");
+    if (!cams_all || !view_off || !recv || V_all < 1 || V_all > 65535)
+        return fail(ctx, MVGS_ERR_INVALID, "owner_prepare: bad arguments");
+    const Launch& L = ctx->L;
+    if (g_begin < 0 || g_end < g_begin || g_end > L.P || ((g_begin % BLK) != 0 && g_begin != g_end))
+        return fail(ctx, MVGS_ERR_INVALID, "owner_prepare: need 0 <= g_begin <= g_end <= P, g_begin % 256 == 0");
+    for (int v = 0; v < V_all; v++)
+        if (cams_all[v].width != L.W || cams_all[v].height != L.H || !(cams_all[v].znear > 0.f) ||
+            !(cams_all[v].fx > 0.f) || !(cams_all[v].fy > 0.f))
+            return fail(ctx, MVGS_ERR_INVALID, "owner_prepare: cameras must match the batch size, znear, fx, fy > 0");
+    CK(cudaSetDevice(ctx->device));
+    cudaStream_t s = (cudaStream_t)stream;
+    const int64_t nblk = (int64_t)V_all * L.NB;
+    if (nblk + 1 > INT32_MAX) return fail(ctx, MVGS_ERR_INVALID, "owner_prepare: batch too large");
+    const int64_t need_scan = scan_tmp_size((int)std::max<int64_t>(nblk, 1));
+    if (nblk + 1 > ctx->cap_oblk || need_scan > ctx->cap_oscan || V_all > ctx->cap_ocams ||
+        (V_all <= 32 && L.P > ctx->cap_opmask)) {
+        CK(cudaStreamSynchronize(s));
+        CK(grow(ctx->d_oblk, ctx->cap_oblk, nblk + 1));
+        CK(grow(ctx->d_oscan, ctx->cap_oscan, need_scan));
+        CK(grow(ctx->d_ocams, ctx->cap_ocams, (int64_t)V_all));
+        if (V_all <= 32) CK(grow(ctx->d_opmask, ctx->cap_opmask, std::max<int64_t>(L.P, 1)));
+    }
+    CK(launch_set_cams(cams_all, V_all, ctx->d_ocams, s));
+    Launch& Lo = ctx->Lo;
+    Lo = L;
+    Lo.V = V_all;
+    Lo.cams = ctx->d_ocams;
+    Lo.blk_off = ctx->d_oblk;
+    Lo.pmask = V_all <= 32 ? ctx->d_opmask : nullptr;
+    CK(cudaMemsetAsync(ctx->d_oblk, 0, sizeof(int) * (nblk + 1), s));
+    const int b0 = (int)(g_begin / BLK), b1 = (int)((g_end + BLK - 1) / BLK);
+    CK(launch_count_range(Lo, b0, b1, s));                                   // S1 for the owned blocks, all views
+    CK(scan_exclusive(ctx->d_oblk, (int)nblk, nullptr, ctx->d_oscan, s));  // view-major slot layout
+    ctx->h_blk.resize((size_t)nblk + 1);
+    CK(cudaMemcpyAsync(ctx->h_blk.data(), ctx->d_oblk, sizeof(int) * (nblk + 1), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    for (int v = 0; v < V_all; v++) view_off[v] = ctx->h_blk[(size_t)v * L.NB];
+    view_off[V_all] = ctx->h_blk[(size_t)nblk];
+    const int64_t q = view_off[V_all];
+    if (q > ctx->cap_orecv || !ctx->d_orecv) {
+        cudaFree(ctx->d_orecv);
+        ctx->d_orecv = nullptr;
+        ctx->cap_orecv = 0;
+        const int64_t nq = q + q / 4 + 1024;
+        CK(cudaMalloc(&ctx->d_orecv, sizeof(float) * PG_STRIDE * nq));
+        ctx->cap_orecv = nq;
+    }
+    Lo.pgrad = ctx->d_orecv;
+    Lo.cap_pairs = ctx->cap_orecv;
+    ctx->og_begin = g_begin;
+    ctx->og_end = g_end;
+    ctx->owner_ready = true;
+    *recv = ctx->d_orecv;
+    return MVGS_OK;
+}
+
+mvgs_status mvgs_owner_adc_stats(mvgs_ctx* ctx, const mvgs_grads* grads, const mvgs_adc* adc, void* stream) {
+    if (!ctx) return MVGS_ERR_INVALID;
+    if (!ctx->owner_ready) return fail(ctx, MVGS_ERR_STATE, "owner_adc_stats needs mvgs_owner_prepare");
+    if (!grads || !adc) return fail(ctx, MVGS_ERR_INVALID, "null grads/adc");
+    const int64_t gb = ctx->og_begin, ge = ctx->og_end;
+    if (ge > gb && (!grads->d_means || !grads->d_log_scales || !grads->d_quats || !grads->d_opacity_logits ||
+                    !grads->d_sh || !adc->e1 || !adc->e2 || !adc->vis))
+        return fail(ctx, MVGS_ERR_INVALID, "null output pointer");
+    CK(cudaSetDevice(ctx->device));
+    cudaStream_t s = (cudaStream_t)stream;
+    ctx->last_stream = s;
+    if (ge > gb) { STAGE(ST_GAUSS); CK(launch_gauss_bwd(ctx->Lo, *grads, *adc, gb, ge, s)); }  // S8 + S9, all views
+    return MVGS_OK;
+}
+
+mvgs_status mvgs_e_old_from_gsum(mvgs_ctx* ctx, const float* gsum, int64_t n, float* e_old, float* e_old_acc,
+                                 void* stream) {
+    if (!ctx) return MVGS_ERR_INVALID;
+    if (n < 0 || (n > 0 && (!gsum || (!e_old && !e_old_acc)))) return fail(ctx, MVGS_ERR_INVALID, "e_old_from_gsum: bad arguments");
+    if (((uintptr_t)gsum & 7) != 0) return fail(ctx, MVGS_ERR_INVALID, "e_old_from_gsum: gsum not 8-B aligned");
+    CK(cudaSetDevice(ctx->device));
+    CK(launch_e_old(gsum, n, e_old, e_old_acc, (cudaStream_t)stream));
     return MVGS_OK;
 }
 

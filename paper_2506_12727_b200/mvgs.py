@@ -16,13 +16,15 @@ LIB_PATH = os.environ.get("MVGS_LIB", os.path.join(HERE, "libmvgs.so"))  # overr
 
 MVGS_OK, MVGS_ERR_INVALID, MVGS_ERR_CAPACITY, MVGS_ERR_STATE, MVGS_ERR_CUDA = 0, -1, -2, -3, -4
 NG = 10
+PG_STRIDE = 12  # floats per per-pair gradient slot
 
 # the exported symbols include/mvgs.h declares (checked by tests/test_abi.py)
 SYMBOLS = ["mvgs_create", "mvgs_destroy", "mvgs_last_error", "mvgs_reserve", "mvgs_preprocess", "mvgs_render_fwd",
            "mvgs_render_bwd", "mvgs_adc_stats", "mvgs_adc_stats_range", "mvgs_query", "mvgs_export_lists", "mvgs_export_pairs",
            "mvgs_set_timing", "mvgs_stage_times", "mvgs_set_eval_counting", "mvgs_render_fwd_partial", "mvgs_render_bwd_partial",
            "mvgs_render_fwd_depth", "mvgs_dssim3d", "mvgs_adc_step", "mvgs_adc_remap",
-           "mvgs_loss_grad", "mvgs_grad_moments", "mvgs_grad_variance", "mvgs_set_debug_blend_counts", "mvgs_set_tma"]
+           "mvgs_loss_grad", "mvgs_grad_moments", "mvgs_grad_variance", "mvgs_set_debug_blend_counts", "mvgs_set_tma",
+           "mvgs_owner_slices", "mvgs_owner_prepare", "mvgs_owner_adc_stats", "mvgs_e_old_from_gsum"]
 PARTIAL_THREAD_EFFICIENT, PARTIAL_MASKED = 0, 1
 STAGE_NAMES = ["count", "scan_pairs", "project", "scan_buckets", "sort_pairs", "dup", "sort_entries", "render_fwd",
                "render_bwd", "gauss_bwd", "dssim"]
@@ -105,6 +107,10 @@ def _load():
     L.mvgs_set_timing.argtypes = [vp, C.c_int]
     L.mvgs_set_eval_counting.argtypes = [vp, C.c_int]
     L.mvgs_set_tma.argtypes = [vp, C.c_int]
+    L.mvgs_owner_slices.argtypes = [vp, vp, C.c_int32, vp, vp, vp]
+    L.mvgs_owner_prepare.argtypes = [vp, vp, C.c_int32, C.c_int64, C.c_int64, vp, vp, vp]
+    L.mvgs_owner_adc_stats.argtypes = [vp, vp, vp, vp]
+    L.mvgs_e_old_from_gsum.argtypes = [vp, vp, C.c_int64, vp, vp, vp]
     L.mvgs_set_debug_blend_counts.argtypes = [vp, vp]
     L.mvgs_render_fwd_partial.argtypes = [vp, vp, C.c_int32, C.c_int32, vp, vp, vp, vp]
     L.mvgs_render_bwd_partial.argtypes = [vp, vp, C.c_int32, C.c_int32, vp, vp, vp, vp]
@@ -316,6 +322,51 @@ def set_debug_blend_counts(ctx, nblend=None):
 
 def set_timing(ctx, enable: bool):
     _check(ctx, _lib.mvgs_set_timing(ctx, int(bool(enable))))
+
+
+class DeviceArray:
+    """Zero-copy view of context-owned device memory (float32) for torch (cuda array interface)."""
+
+    def __init__(self, ptr: int, n: int):
+        self.__cuda_array_interface__ = {"shape": (int(n),), "typestr": "<f4", "data": (int(ptr), False),
+                                         "version": 3, "strides": None}
+
+
+def _as_tensor(ptr: int, n: int):
+    return torch.as_tensor(DeviceArray(ptr, n), device="cuda") if n > 0 else torch.empty(0, device="cuda")
+
+
+def owner_slices(ctx, g_bounds, V: int, stream=None):
+    """(slot_off [V, N+1] int64, slot tensor [Q·12] float32 view of the context's gradient slots)."""
+    gb = np.ascontiguousarray(g_bounds, np.int64)
+    N = len(gb) - 1
+    off = np.zeros((V, N + 1), np.int64)
+    p = C.c_void_p()
+    _check(ctx, _lib.mvgs_owner_slices(ctx, gb.ctypes.data, N, off.ctypes.data, C.byref(p), _stream(stream)))
+    return off, _as_tensor(p.value, int(off[-1, -1]) * PG_STRIDE if V else 0)
+
+
+def owner_prepare(ctx, cams_all, g_begin: int, g_end: int, stream=None):
+    """(view_off [V_all+1] int64, receive tensor [view_off[-1]·12] float32, context-owned)."""
+    cams_all = np.ascontiguousarray(cams_all)
+    V = len(cams_all)
+    off = np.zeros(V + 1, np.int64)
+    p = C.c_void_p()
+    _check(ctx, _lib.mvgs_owner_prepare(ctx, cams_all.ctypes.data, V, int(g_begin), int(g_end), off.ctypes.data,
+                                        C.byref(p), _stream(stream)))
+    return off, _as_tensor(p.value, int(off[-1]) * PG_STRIDE)
+
+
+def owner_adc_stats(ctx, grads: dict, adc: dict, stream=None):
+    gr = Grads(*[_ptr(grads[k]) for k in ("d_means", "d_log_scales", "d_quats", "d_opacity_logits", "d_sh")])
+    ad = Adc(*[_ptr(adc.get(k)) for k in ADC_FIELDS])
+    _check(ctx, _lib.mvgs_owner_adc_stats(ctx, C.byref(gr), C.byref(ad), _stream(stream)))
+
+
+def e_old_from_gsum(ctx, gsum, e_old=None, e_old_acc=None, stream=None):
+    """E_old = ‖gsum‖ per Gaussian (gsum [n,2] device fp32), into e_old and/or += e_old_acc."""
+    n = int(gsum.shape[0])
+    _check(ctx, _lib.mvgs_e_old_from_gsum(ctx, _ptr(gsum), n, _ptr(e_old), _ptr(e_old_acc), _stream(stream)))
 
 
 def set_tma(ctx, enable: bool):
