@@ -255,11 +255,16 @@ def run_mvgs(args):
         dist.barrier()
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]  # per-step distribution
     ev0.record()
-    for _ in range(args.steps):
+    evs[0].record()
+    for i in range(args.steps):
         step()
+        evs[i + 1].record()
     ev1.record()
     torch.cuda.synchronize()
+    per_step = sorted(evs[i].elapsed_time(evs[i + 1]) for i in range(args.steps))
+    pct = lambda q: per_step[min(len(per_step) - 1, int(round(q * (len(per_step) - 1))))]  # noqa: E731
     if dist is not None:
         dist.barrier()
     clocks = clk.stop()
@@ -408,7 +413,9 @@ def run_mvgs(args):
 
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": N, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": args.scaling,
+        "warmup": args.warmup, "ms_per_step": round(ms, 4),
+        "step_ms_p10_p50_p90": [round(pct(0.1), 4), round(pct(0.5), 4), round(pct(0.9), 4)],
+        "higher_is_better": True, "scaling": args.scaling,
         "vs_baseline": None, "dtype": "f32", "data": "synthetic (mvgs-synth v1, seeded; DESIGN.md §6)",
         "config": {**workload_config(cfg, P, Vr, N, V_all),
                    "exchange": args.exchange if N > 1 or owner else "none (1 GPU)",

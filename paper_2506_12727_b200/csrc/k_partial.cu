@@ -298,11 +298,16 @@ cudaError_t launch_render_bwd_partial(const Launch& L, const int32_t* pix, int S
                                       const float* Tf, const int32_t* nc, cudaStream_t s) {
     const int nt = partial_threads(S, mode);
     const size_t smem = sizeof(float) * (nt / 32) * PRB * NG;
+    cudaError_t e;
     if (mode == MVGS_PARTIAL_MASKED) {
-        cudaFuncSetAttribute(k_render_bwd_list<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if ((e = cudaFuncSetAttribute(k_render_bwd_list<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) !=
+            cudaSuccess)
+            return e;
         k_render_bwd_list<true><<<L.V * L.T, nt, smem, s>>>(L, pix, S, dL, Tf, nc);
     } else {
-        cudaFuncSetAttribute(k_render_bwd_list<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if ((e = cudaFuncSetAttribute(k_render_bwd_list<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) !=
+            cudaSuccess)
+            return e;
         k_render_bwd_list<false><<<L.V * L.T, nt, smem, s>>>(L, pix, S, dL, Tf, nc);
     }
     return cudaGetLastError();

@@ -1,8 +1,10 @@
 """NEXT-2 parity: the 3D distance-aware D-SSIM through the C ABI
 against oracle/dssim.py, and the renderer's predicted depth against the
 oracle rasterizer's.  Tolerances: loss |Δ| ≤ 1e-5 (a mean of
-fp32 SSIM values summed in fp64); gradient per element |Δ| ≤ 2e-3·|ref| +
-1e-3·max|ref| (fp32 moments, variance by cancellation, hardware exp);
+fp32 SSIM values summed in fp64); gradient per tensor ‖Δ‖/‖ref‖ ≤ 1e-3 and per element
+|Δ| ≤ 1e-3·|ref| + 1e-5·max|ref| (the main rule's relative part; the floor absorbs fp32
+moments — variance by cancellation — and the hardware exp; measured need 1.8e-6, tensor
+error 4e-6, scripts/dssim_err_probe.py);
 depth |Δ| ≤ 2e-5·max depth (same decisions as the image, fp32 sum)."""
 import numpy as np
 import pytest
@@ -32,7 +34,9 @@ def gpu_dssim(img, tgt, depth, Tf, cams, sigma=1.5, grad=True):
 
 
 def check_grad(g, ref):
-    tol = 2e-3 * np.abs(ref) + 1e-3 * np.max(np.abs(ref))
+    rel = np.linalg.norm(g - ref) / np.linalg.norm(ref)
+    assert rel <= 1e-3, rel
+    tol = 1e-3 * np.abs(ref) + 1e-5 * np.max(np.abs(ref))
     bad = np.abs(g - ref) > tol
     assert not bad.any(), f"{bad.sum()} elements out of tolerance, max |Δ| {np.max(np.abs(g - ref)):.3e}"
 
