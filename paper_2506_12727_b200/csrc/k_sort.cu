@@ -105,7 +105,8 @@ __global__ __launch_bounds__(RS_T, MVGS_RS3_MINB) void k_rs_scatter(const uint32
                                                      const uint2* __restrict__ pin, uint2* __restrict__ pout,
                                                      const int* __restrict__ n_ptr, int64_t cap, int shift, int nbits,
                                                      const int* __restrict__ offs, int ntiles,
-                                                     int* __restrict__ range_min) {
+                                                     int* __restrict__ range_min, const uint2* __restrict__ gather_pl,
+                                                     int* __restrict__ cnt_out) {
     constexpr int TILE = RS_T * IPT;
     __shared__ uint32_t hist[RS_NW][RS_BINS];
     __shared__ uint32_t dstart[RS_BINS];   // first local position of each digit
@@ -131,7 +132,7 @@ __global__ __launch_bounds__(RS_T, MVGS_RS3_MINB) void k_rs_scatter(const uint32
         const int p = warp * 32 * IPT + it * 32 + lane;
         const bool ok = p < nt;
         key[it] = ok ? kin[t0 + p] : 0u;
-        val[it] = ok ? vin[t0 + p] : 0u;
+        val[it] = ok ? (vin ? vin[t0 + p] : (uint32_t)(t0 + p)) : 0u;  // no vin: values are the positions
         if (PAYLOAD) pay[PAYLOAD ? it : 0] = ok ? pin[t0 + p] : make_uint2(0u, 0u);
     }
 #pragma unroll
@@ -188,6 +189,20 @@ __global__ __launch_bounds__(RS_T, MVGS_RS3_MINB) void k_rs_scatter(const uint32
         }
         return;
     }
+    if (gather_pl) {
+        // last pass of the pair sort: each pair's tile rect gathered through its (sorted) slot and
+        // its tile count written instead of the key (S3 scans the counts into entry offsets)
+        for (int l = threadIdx.x; l < nt; l += RS_T) {
+            const uint32_t k = sk[l];
+            const uint32_t dst = gdelta[(k >> shift) & mask] + l;
+            const uint32_t q = sv[l];
+            vout[dst] = q;
+            const uint2 r = k == 0xffffffffu ? make_uint2(0u, 0u) : gather_pl[q];  // inert: no rect
+            pout[dst] = r;
+            cnt_out[dst] = (int)(((r.y & 0xffff) - (r.x & 0xffff)) * ((r.y >> 16) - (r.x >> 16)));
+        }
+        return;
+    }
     for (int l = threadIdx.x; l < nt; l += RS_T) {
         const uint32_t k = sk[l];
         const uint32_t dst = gdelta[(k >> shift) & mask] + l;
@@ -233,13 +248,13 @@ static int radix_sort_3k_t(uint32_t* k, uint32_t* v, uint32_t* k2, uint32_t* v2,
         if constexpr (IPT == 8) {  // payload tiles only at 8 keys per thread (static shared memory)
             if (pl) {
                 k_rs_scatter<true, IPT><<<ntiles, RS_T, 0, s>>>(ks, vs, kd, vd, ps, pd, n_ptr, cap, shift, nb, counts,
-                                                               ntiles, rm);
+                                                               ntiles, rm, nullptr, nullptr);
                 launched = true;
             }
         }
         if (!launched)
             k_rs_scatter<false, IPT><<<ntiles, RS_T, 0, s>>>(ks, vs, kd, vd, nullptr, nullptr, n_ptr, cap, shift, nb,
-                                                        counts, ntiles, rm);
+                                                        counts, ntiles, rm, nullptr, nullptr);
         if ((*err = cudaGetLastError()) != cudaSuccess) return pass;
         uint32_t* t = ks; ks = kd; kd = t;
         t = vs; vs = vd; vd = t;
@@ -747,10 +762,57 @@ __global__ __launch_bounds__(RC_T) void k_ranges_close(Launch L, const int* __re
     }
 }
 
+// The pair sort on the three-kernel passes (per-tile histogram, device-wide scan of the
+// digit × tile counts, stable scatter) instead of onesweep look-back: inert pairs (key
+// 0xffffffff) are not dropped but sort last (every visible depth key is a positive float's
+// bits, below 0xffffffff), so the first n_visible sorted pairs are the visible ones; the first
+// pass takes the values to be the slots themselves; the last pass gathers each pair's rect
+// through its slot and writes its tile count.  Look-back chains made onesweep pay per tile
+// (1.12 ms per pass over 79 M pairs at `large`); these passes are plain streaming.
+#ifndef MVGS_PS_IPT
+#define MVGS_PS_IPT 8  // keys per thread of the pair-sort tiles
+#endif
+static int radix_sort_pairs_3k(const Launch& L, cudaStream_t s, cudaError_t* err) {
+    constexpr int IPT = MVGS_PS_IPT;
+    const int64_t cap = L.cap_pairs;
+    const int ntiles = (int)((cap + RS_T * IPT - 1) / (RS_T * IPT));
+    const int bits = 32, npass = 4, db = 8;
+    *err = cudaSuccess;
+    if (ntiles == 0) return 0;
+    const int* n_ptr = L.counters + C_Q;
+    uint32_t *ks = L.pkey, *vs = nullptr, *kd = L.pkey2, *vd = L.pval;
+    uint32_t* vbuf[2] = {L.pval, L.pval2};
+    for (int pass = 0; pass < npass; pass++) {
+        const int shift = pass * db;
+        const int nb = min(db, bits - shift);
+        k_rs_hist<IPT><<<ntiles, RS_T, 0, s>>>(ks, n_ptr, cap, shift, nb, L.rs_counts, ntiles);
+        if ((*err = scan_exclusive(L.rs_counts, (1 << nb) * ntiles, nullptr, L.scan_tmp, s)) != cudaSuccess) return pass;
+        vd = vbuf[pass & 1];
+        const bool last = pass == npass - 1;
+        k_rs_scatter<false, IPT><<<ntiles, RS_T, 0, s>>>(ks, vs, kd, vd, nullptr, last ? L.prect2 : nullptr, n_ptr, cap,
+                                                        shift, nb, L.rs_counts, ntiles, nullptr,
+                                                        last ? L.prect : nullptr, last ? L.ecount : nullptr);
+        if ((*err = cudaGetLastError()) != cudaSuccess) return pass;
+        uint32_t* t = ks; ks = kd; kd = t;
+        vs = vd;
+    }
+    return npass;
+}
+
+#ifndef MVGS_PAIR_SORT_3K
+#define MVGS_PAIR_SORT_3K 1  // the pair sort on three-kernel passes (0: onesweep)
+#endif
+
 // S4a: pairs by depth, carrying each pair's packed tile rect.  pkey/prect were written
 // by k_project (the values start as the pair slots themselves); the depth order and the rects in that order → *order_out, *rect_out.
 cudaError_t launch_sort_pairs(const Launch& L, const uint32_t** order_out, const uint2** rect_out, cudaStream_t s) {
     cudaError_t e;
+    if (MVGS_PAIR_SORT_3K) {
+        const int np = radix_sort_pairs_3k(L, s, &e);
+        *order_out = (np & 1) ? L.pval : L.pval2;  // pass p writes pval[p & 1]: the last (p = 3) wrote pval2
+        *rect_out = L.prect2;
+        return e;
+    }
     int np = radix_sort(L.pkey, L.pval, L.pkey2, L.pval2, L.prect, L.prect2, L.counters + C_Q, L.counters + C_NVIS,
                         L.cap_pairs, 32, true, true, L.rs, s, &e, L.ecount, MVGS_PAIR_GATHER != 0);
     *order_out = (np & 1) ? L.pval2 : L.pval;
