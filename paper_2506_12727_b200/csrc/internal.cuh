@@ -22,10 +22,6 @@ constexpr int PF_RADIUS_SHIFT = 8;  // pflag bits 8..31: the pair's CA radius (R
 // device counters (int32 slots in ctx->d_counters)
 enum { C_Q = 0, C_K = 1, C_OVERFLOW = 2, C_MAXB = 3, C_NVIS = 4, C_NCOUNTERS = 8 };
 
-struct RadixScratch {
-    unsigned long long* status;  // [256 × tiles] look-back words (epoch-tagged)
-    uint32_t* small;             // digit totals, bases, tile counters, device pass epoch
-};
 
 struct Launch {  // everything a kernel needs about the current batch
     int64_t P;
@@ -48,7 +44,6 @@ struct Launch {  // everything a kernel needs about the current batch
     uint2 *prect, *prect2;                  // [cap_pairs] packed tile rect carried through the pair sort
     int* ecount;      // [cap_pairs + 1] tiles per depth-ordered pair → entry offsets
     int* rs_counts;   // (unused) radix digit × tile counts
-    RadixScratch rs;  // onesweep radix scratch
     int* scan_tmp;    // scan block sums
     const uint32_t* sorted;  // [K] pair index of every entry in (view, tile, depth, gid) order
     int* counters;    // [C_NCOUNTERS]
@@ -103,9 +98,6 @@ struct mvgs_ctx {
     int* d_ecount = nullptr;
     int* d_rs = nullptr;
     int64_t cap_rs = 0;
-    unsigned long long* d_rs_status = nullptr;
-    uint32_t* d_rs_small = nullptr;
-    uint32_t rs_epoch = 0;
     int* d_counters = nullptr;
     unsigned long long* d_counters64 = nullptr;
     int* d_scan = nullptr;  // scan block sums

@@ -4,9 +4,10 @@
 // and sorts the 64-bit keys.  Here the same total order (view, tile, depth,
 // gid) (R9, R10) is produced with two short stable LSD radix sorts and no
 // atomics:
-//   1. sort the pairs by depth bits (4 × 8-bit passes over Q pairs, Q ≪ K),
-//      carrying each pair's packed tile rect; pairs start in (view, gid) order
-//      and the sort is stable, so equal depths stay in gid order;
+//   1. sort the pairs by depth bits (4 × 8-bit passes over Q pairs, Q ≪ K;
+//      pairs with no tile carry key 0xffffffff and sort last); pairs start in
+//      (view, gid) order and the sort is stable, so equal depths stay in gid
+//      order; the last pass gathers each pair's packed tile rect;
 //   2. duplicate: walk the pairs in that order and write one entry per covered
 //      tile, key = view·T + tile (positions from an exclusive scan of the
 //      per-pair tile counts — coalesced, deterministic);
@@ -28,13 +29,6 @@ constexpr int RS_T = 256, RS_IPT = 8, RS_TILE = RS_T * RS_IPT, RS_NW = RS_T / 32
 int radix_tiles(int64_t cap) { return (int)((cap + RS_TILE - 1) / RS_TILE); }
 int64_t radix_counts_size(int64_t cap) { return (int64_t)RS_BINS * radix_tiles(cap) + 1; }
 
-static int grid_for(int64_t n, int threads) {
-    int dev = 0, nsm = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    int64_t b = (n + threads - 1) / threads;
-    return (int)max((int64_t)1, min(b, (int64_t)nsm * 16));
-}
 
 // exclusive scan over the 256 threads of a CTA (one value each)
 __device__ __forceinline__ uint32_t block_excl_scan_256_u(uint32_t x, uint32_t* total) {
@@ -279,258 +273,6 @@ static void entry_digits(const Launch& L, int* bits, int* db) {
     const int np = (b + 7) / 8;
     *bits = b;
     *db = (b + np - 1) / np;
-}
-
-// ---------------------------------------------------------------- onesweep
-// Stable LSD radix sort, one kernel per pass.  The digit totals of every pass are
-// counted once up front (the key multiset never changes between passes); within a
-// pass each tile takes a dynamic id, ranks its keys on chip, publishes its per-digit
-// counts and obtains its exclusive per-digit prefix by decoupled look-back over the
-// preceding tiles (status words tagged with a per-pass epoch, so nothing is cleared
-// between passes).  The first pass can drop "inert" keys (0xffffffff), compacting
-// the pairs with no tile before the remaining passes.
-#ifndef MVGS_OS_IPT
-#define MVGS_OS_IPT 8  // keys per thread of the onesweep tiles (dynamic shared memory)
-#endif
-constexpr int OS_IPT = MVGS_OS_IPT;
-constexpr uint32_t INERT = 0xffffffffu;
-constexpr unsigned long long ST_AGG = 1ull << 32, ST_PRE = 2ull << 32;
-
-__global__ __launch_bounds__(256) void k_rs_upsweep(const uint32_t* __restrict__ keys, const int* __restrict__ n_ptr,
-                                                    int64_t cap, int npass, int db, int bits, int drop_inert,
-                                                    uint32_t* __restrict__ totals) {
-    __shared__ uint32_t h[4][RS_BINS];
-    for (int i = threadIdx.x; i < 4 * RS_BINS; i += blockDim.x) (&h[0][0])[i] = 0;
-    __syncthreads();
-    const int n = (int)min((int64_t)*n_ptr, cap);
-    // UP_K loads in flight per thread before its atomics (one at a time left the kernel
-    // latency-bound: ≈ 8 KB in flight per SM)
-    constexpr int UP_K = 8;
-    const int stride = gridDim.x * blockDim.x;
-    for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < n; b += stride * UP_K) {
-        uint32_t kk[UP_K];
-#pragma unroll
-        for (int u = 0; u < UP_K; u++) {
-            const int i = b + u * stride;
-            kk[u] = i < n ? keys[i] : 0u;
-        }
-#pragma unroll
-        for (int u = 0; u < UP_K; u++) {
-            const uint32_t k = kk[u];
-            if (b + u * stride >= n || (drop_inert && k == INERT)) continue;
-            for (int p = 0; p < npass; p++) {
-                const int sh = p * db, nb = min(db, bits - sh);
-                atomicAdd(&h[p][(k >> sh) & ((1u << nb) - 1u)], 1u);
-            }
-        }
-    }
-    __syncthreads();
-    for (int p = 0; p < npass; p++)
-        if (h[p][threadIdx.x]) atomicAdd(&totals[p * RS_BINS + threadIdx.x], h[p][threadIdx.x]);
-}
-
-// also advances the device-side pass epoch (graph replays never see stale words)
-__global__ __launch_bounds__(256) void k_rs_bases(const uint32_t* __restrict__ totals, uint32_t* __restrict__ gbase,
-                                                  int npass, uint32_t* __restrict__ epoch) {
-    if (threadIdx.x == 0) {
-        epoch[1] = epoch[0] + 1;  // epoch of pass 0
-        epoch[0] += (uint32_t)npass;
-    }
-    for (int p = 0; p < npass; p++) {
-        uint32_t tot;
-        const uint32_t ex = block_excl_scan_256_u(totals[p * RS_BINS + threadIdx.x], &tot);
-        gbase[p * RS_BINS + threadIdx.x] = ex;
-        __syncthreads();
-    }
-}
-
-__device__ __forceinline__ void st_status(unsigned long long* p, unsigned long long v) {
-    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;\n" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ unsigned long long ld_status(const unsigned long long* p) {
-    unsigned long long v;
-    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];\n" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
-
-#ifndef MVGS_OS_MINB
-#define MVGS_OS_MINB 1  // resident CTAs asked of the key/value onesweep passes (1: ptxas's choice)
-#endif
-template <bool PAYLOAD, int IPT>
-__global__ __launch_bounds__(RS_T, PAYLOAD ? 1 : MVGS_OS_MINB) void k_rs_onesweep(const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin,
-                                                      uint32_t* __restrict__ kout, uint32_t* __restrict__ vout,
-                                                      const uint2* __restrict__ pin, uint2* __restrict__ pout,
-                                                      int* __restrict__ cnt_out,
-                                                      const int* __restrict__ n_ptr, int64_t cap, int shift, int nbits,
-                                                      int drop_inert, const uint32_t* __restrict__ gbase,
-                                                      unsigned long long* __restrict__ status,
-                                                      const uint32_t* __restrict__ epoch_base, int pass,
-                                                      int* __restrict__ tile_ctr, int gather) {
-    __shared__ uint32_t hist[RS_NW][RS_BINS];
-    __shared__ uint32_t gdelta[RS_BINS];  // global offset − local start, per digit
-    constexpr int TILE = RS_T * IPT;
-    extern __shared__ uint2 os_dyn[];  // sp[TILE] (payload), then sk[TILE], sv[TILE]
-    uint2* sp = os_dyn;
-    uint32_t* sk = reinterpret_cast<uint32_t*>(os_dyn + (PAYLOAD ? TILE : 0));
-    uint32_t* sv = sk + TILE;
-    __shared__ int s_tile;
-    __shared__ uint32_t s_total;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const unsigned lt = (1u << lane) - 1u;
-    if (threadIdx.x == 0) s_tile = atomicAdd(tile_ctr, 1);  // dynamic ids: predecessors are running
-    __syncthreads();
-    const int tile = s_tile;
-    const uint32_t epoch = (epoch_base[1] + (uint32_t)pass) & 0x3fffffffu;  // 30-bit tag
-    const int n = (int)min((int64_t)*n_ptr, cap);
-    const int t0 = tile * TILE;
-    if (t0 >= n) return;  // every later tile is past n as well
-    const int nt = min(TILE, n - t0);
-    const uint32_t mask = (1u << nbits) - 1u;
-    const uint32_t gb = gbase[threadIdx.x];  // this digit's global base (independent of the keys)
-#pragma unroll
-    for (int i = 0; i < RS_BINS / 32; i++) hist[warp][lane + 32 * i] = 0;
-    __syncwarp();
-    uint32_t key[IPT], val[IPT], loc[IPT];
-    uint2 pay[PAYLOAD ? IPT : 1];
-#pragma unroll
-    for (int it = 0; it < IPT; it++) {
-        const int p = warp * 32 * IPT + it * 32 + lane;
-        const bool ok = p < nt;
-        key[it] = ok ? kin[t0 + p] : INERT;
-        val[it] = vin ? (ok ? vin[t0 + p] : 0u) : (uint32_t)(t0 + p);  // no vin: the identity
-        if (PAYLOAD) pay[PAYLOAD ? it : 0] = ok ? pin[gather ? val[it] : (uint32_t)(t0 + p)] : make_uint2(0u, 0u);
-    }
-#pragma unroll
-    for (int it = 0; it < IPT; it++) {
-        const int p = warp * 32 * IPT + it * 32 + lane;
-        const bool ok = p < nt && !(drop_inert && key[it] == INERT);
-        const uint32_t d = (key[it] >> shift) & mask;
-        const unsigned peers = digit_peers(d, ok, nbits);
-        const uint32_t before = ok ? hist[warp][d] : 0u;
-        loc[it] = ok ? before + __popc(peers & lt) : 0xffffffffu;
-        __syncwarp();
-        if (ok && lane == __ffs(peers) - 1) hist[warp][d] = before + __popc(peers);
-        __syncwarp();
-    }
-    __syncthreads();
-    {  // thread = digit: publish, look back, tile-local starts and warp bases
-        const int d = threadIdx.x;
-        uint32_t tot = 0;
-#pragma unroll
-        for (int w = 0; w < RS_NW; w++) tot += hist[w][d];
-        unsigned long long* st = status + (size_t)tile * RS_BINS + d;
-        const unsigned long long ep = (unsigned long long)epoch << 34;
-        uint32_t excl = 0;
-        if (tile == 0) {
-            st_status(st, ep | ST_PRE | tot);
-        } else {
-            st_status(st, ep | ST_AGG | tot);
-            for (int p = tile - 1; p >= 0; p--) {
-                unsigned long long w;
-                do {
-                    w = ld_status(status + (size_t)p * RS_BINS + d);
-                } while ((w >> 34) != epoch || !(w & (ST_AGG | ST_PRE)));
-                excl += (uint32_t)w;
-                if (w & ST_PRE) break;
-            }
-            st_status(st, ep | ST_PRE | (excl + tot));
-        }
-        uint32_t all;
-        const uint32_t start = block_excl_scan_256_u(tot, &all);
-        if (d == 0) s_total = all;
-        gdelta[d] = gb + excl - start;
-        uint32_t run = start;
-#pragma unroll
-        for (int w = 0; w < RS_NW; w++) {
-            const uint32_t c = hist[w][d];
-            hist[w][d] = run;
-            run += c;
-        }
-    }
-    __syncthreads();
-#pragma unroll
-    for (int it = 0; it < IPT; it++) {
-        if (loc[it] != 0xffffffffu) {
-            const uint32_t l = hist[warp][(key[it] >> shift) & mask] + loc[it];
-            sk[l] = key[it];
-            sv[l] = val[it];
-            if (PAYLOAD) sp[PAYLOAD ? l : 0] = pay[PAYLOAD ? it : 0];
-        }
-    }
-    __syncthreads();
-    const int nout = (int)s_total;
-    for (int l = threadIdx.x; l < nout; l += RS_T) {
-        const uint32_t k = sk[l];
-        const uint32_t dst = gdelta[(k >> shift) & mask] + l;
-        if (!PAYLOAD || !cnt_out) kout[dst] = k;
-        vout[dst] = sv[l];
-        if (PAYLOAD) {
-            const uint2 r = sp[PAYLOAD ? l : 0];
-            pout[dst] = r;
-            // last pass of the pair sort: the tiles each pair covers, in depth order, instead of
-            // the keys (nothing reads the sorted depths; S3 scans these into entry offsets)
-            if (cnt_out) cnt_out[dst] = (int)(((r.y & 0xffff) - (r.x & 0xffff)) * ((r.y >> 16) - (r.x >> 16)));
-        }
-    }
-}
-
-// Stable LSD sort of (k, v[, payload])[0..*n_ptr) on bits [0, bits) with ≤ 8-bit
-// digits; with drop_inert the first pass removes keys equal to 0xffffffff and the
-// later passes run on *n_after elements; with identity_vals the first pass takes the
-// values to be the input positions (v is not read); with last_counts (payload sorts) the last
-// pass writes each element's rect tile count there instead of its sorted key.  Returns the
-// number of passes; the result is in the first buffers when even, in the second ones when odd.
-// Pair sort payload: carried through every pass (0), or gathered by the last pass from the
-// unsorted rects through the sorted values (1: the values are the input positions), so the
-// earlier passes move 8 B per pair instead of 16 and the rect array (8·Q, L2-resident) is read once.
-#ifndef MVGS_PAIR_GATHER
-#define MVGS_PAIR_GATHER 1
-#endif
-int radix_sort(uint32_t* k, uint32_t* v, uint32_t* k2, uint32_t* v2, uint2* pl, uint2* pl2, const int* n_ptr,
-               const int* n_after, int64_t cap, int bits, bool drop_inert, bool identity_vals, const RadixScratch& rs,
-               cudaStream_t s, cudaError_t* err, int* last_counts, bool gather_pl) {
-    const int ntiles = radix_tiles(cap);
-    const int npass = (bits + 7) / 8;
-    const int db = npass ? (bits + npass - 1) / npass : 0;
-    *err = cudaSuccess;
-    if (ntiles == 0 || npass == 0) return 0;
-    uint32_t* totals = rs.small;                      // [4][256]
-    uint32_t* gbase = rs.small + 4 * RS_BINS;         // [4][256]
-    int* tctr = (int*)(rs.small + 8 * RS_BINS);       // [4]
-    uint32_t* epoch = rs.small + 8 * RS_BINS + 8;     // [2] device pass epoch (never cleared)
-    if ((*err = cudaMemsetAsync(rs.small, 0, sizeof(uint32_t) * (8 * RS_BINS + 4), s)) != cudaSuccess) return 0;
-    k_rs_upsweep<<<grid_for(cap, 256), 256, 0, s>>>(k, n_ptr, cap, npass, db, bits, drop_inert ? 1 : 0, totals);
-    k_rs_bases<<<1, 256, 0, s>>>(totals, gbase, npass, epoch);
-    uint32_t *ks = k, *vs = v, *kd = k2, *vd = v2;
-    uint2 *ps = pl, *pd = pl2;
-    for (int pass = 0; pass < npass; pass++) {
-        const int shift = pass * db;
-        const int nb = min(db, bits - shift);
-        const int* np = (pass == 0) ? n_ptr : (drop_inert ? n_after : n_ptr);
-        const uint32_t* vin = (pass == 0 && identity_vals) ? nullptr : vs;
-        constexpr int OT = RS_T * OS_IPT;
-        const int otiles = (int)((cap + OT - 1) / OT);
-        const bool with_pl = pl && (!gather_pl || pass == npass - 1);
-        const size_t osm = (size_t)OT * ((with_pl ? 8 : 0) + 8);
-        if (with_pl) cudaFuncSetAttribute(k_rs_onesweep<true, OS_IPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)osm);
-        else cudaFuncSetAttribute(k_rs_onesweep<false, OS_IPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)osm);
-        if (with_pl)
-            k_rs_onesweep<true, OS_IPT><<<otiles, RS_T, osm, s>>>(ks, vin, kd, vd, gather_pl ? pl : ps,
-                                                        gather_pl ? pl2 : pd,
-                                                        pass == npass - 1 ? last_counts : nullptr, np, cap, shift, nb,
-                                                        (drop_inert && pass == 0) ? 1 : 0, gbase + pass * RS_BINS,
-                                                        rs.status, epoch, pass, tctr + pass, gather_pl ? 1 : 0);
-        else
-            k_rs_onesweep<false, OS_IPT><<<otiles, RS_T, osm, s>>>(ks, vin, kd, vd, nullptr, nullptr, nullptr, np, cap,
-                                                         shift, nb,
-                                                         (drop_inert && pass == 0) ? 1 : 0, gbase + pass * RS_BINS,
-                                                         rs.status, epoch, pass, tctr + pass, 0);
-        if ((*err = cudaGetLastError()) != cudaSuccess) return pass;
-        uint32_t* t = ks; ks = kd; kd = t;
-        t = vs; vs = vd; vd = t;
-        uint2* tp = ps; ps = pd; pd = tp;
-    }
-    return npass;
 }
 
 // view of a pair from the view-major pair offsets (blk_off[v·NB] = first pair of view v)
@@ -799,24 +541,11 @@ static int radix_sort_pairs_3k(const Launch& L, cudaStream_t s, cudaError_t* err
     return npass;
 }
 
-#ifndef MVGS_PAIR_SORT_3K
-#define MVGS_PAIR_SORT_3K 1  // the pair sort on three-kernel passes (0: onesweep)
-#endif
-
-// S4a: pairs by depth, carrying each pair's packed tile rect.  pkey/prect were written
-// by k_project (the values start as the pair slots themselves); the depth order and the rects in that order → *order_out, *rect_out.
 cudaError_t launch_sort_pairs(const Launch& L, const uint32_t** order_out, const uint2** rect_out, cudaStream_t s) {
     cudaError_t e;
-    if (MVGS_PAIR_SORT_3K) {
-        const int np = radix_sort_pairs_3k(L, s, &e);
-        *order_out = (np & 1) ? L.pval : L.pval2;  // pass p writes pval[p & 1]: the last (p = 3) wrote pval2
-        *rect_out = L.prect2;
-        return e;
-    }
-    int np = radix_sort(L.pkey, L.pval, L.pkey2, L.pval2, L.prect, L.prect2, L.counters + C_Q, L.counters + C_NVIS,
-                        L.cap_pairs, 32, true, true, L.rs, s, &e, L.ecount, MVGS_PAIR_GATHER != 0);
-    *order_out = (np & 1) ? L.pval2 : L.pval;
-    *rect_out = (MVGS_PAIR_GATHER || (np & 1)) ? L.prect2 : L.prect;
+    const int np = radix_sort_pairs_3k(L, s, &e);
+    *order_out = (np & 1) ? L.pval : L.pval2;  // pass p writes pval[p & 1]: the last (p = 3) wrote pval2
+    *rect_out = L.prect2;
     return e;
 }
 

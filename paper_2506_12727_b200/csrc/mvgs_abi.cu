@@ -82,21 +82,11 @@ cudaError_t alloc_sort_scratch(mvgs_ctx* c) {
     const int64_t need = radix_counts_size(cap);
     if (need > c->cap_rs || !c->d_rs) {
         cudaFree(c->d_rs);
-        cudaFree(c->d_rs_status);
         c->d_rs = nullptr;
-        c->d_rs_status = nullptr;
         c->cap_rs = 0;
         cudaError_t e = cudaMalloc(&c->d_rs, sizeof(int) * need);
         if (e != cudaSuccess) return e;
-        if ((e = cudaMalloc(&c->d_rs_status, sizeof(unsigned long long) * need)) != cudaSuccess) return e;
-        // epoch-tagged look-back words must never match a live epoch: start from zeros
-        if ((e = cudaMemset(c->d_rs_status, 0, sizeof(unsigned long long) * need)) != cudaSuccess) return e;
         c->cap_rs = need;
-    }
-    if (!c->d_rs_small) {
-        cudaError_t e = cudaMalloc(&c->d_rs_small, sizeof(uint32_t) * 4096);
-        if (e != cudaSuccess) return e;
-        if ((e = cudaMemset(c->d_rs_small, 0, sizeof(uint32_t) * 4096)) != cudaSuccess) return e;
     }
     const int64_t need_scan = scan_tmp_size((int)std::max(need, c->cap_pairs + 1));
     if (need_scan > c->cap_scan || !c->d_scan) {
@@ -180,7 +170,6 @@ void fill_launch(mvgs_ctx* c) {
     L.prect2 = c->d_prect2;
     L.ecount = c->d_ecount;
     L.rs_counts = c->d_rs;
-    L.rs = RadixScratch{c->d_rs_status, c->d_rs_small};
     L.scan_tmp = c->d_scan;
     L.counters = c->d_counters;
     L.counters64 = c->d_counters64;
@@ -230,7 +219,7 @@ void mvgs_destroy(mvgs_ctx* ctx) {
     cudaFree(ctx->d_rec); cudaFree(ctx->d_pgrad);
     cudaFree(ctx->d_key); cudaFree(ctx->d_val); cudaFree(ctx->d_key2); cudaFree(ctx->d_val2);
     cudaFree(ctx->d_pkey); cudaFree(ctx->d_pval); cudaFree(ctx->d_pkey2); cudaFree(ctx->d_pval2);
-    cudaFree(ctx->d_ecount); cudaFree(ctx->d_rs); cudaFree(ctx->d_rs_status); cudaFree(ctx->d_rs_small); cudaFree(ctx->d_prect); cudaFree(ctx->d_prect2);
+    cudaFree(ctx->d_ecount); cudaFree(ctx->d_rs); cudaFree(ctx->d_prect); cudaFree(ctx->d_prect2);
     cudaFree(ctx->d_pflag);
     cudaFree(ctx->d_counters); cudaFree(ctx->d_counters64); cudaFree(ctx->d_scan);
     cudaFree(ctx->d_dssim_coef); cudaFree(ctx->d_dssim_part);
