@@ -35,6 +35,9 @@ namespace mvgs {
 #ifndef MVGS_FWD_BATCH
 #define MVGS_FWD_BATCH 1  // forward staged batch = 128 × this entries
 #endif
+#ifndef MVGS_FWD_PAIR
+#define MVGS_FWD_PAIR 1  // forward walk: two entries per step (experiment knob)
+#endif
 #ifndef MVGS_BWD_PAIR
 #define MVGS_BWD_PAIR 1  // backward walk: two entries per step (measured: garden bwd 0.739 → 0.713, playroom 3.44 → 3.31 ms)
 #endif
@@ -234,10 +237,9 @@ __global__ __launch_bounds__(RT) void k_render_fwd_p(Launch L, float* __restrict
                 const int nidx = b0 + FB + (int)threadIdx.x;
                 qn = nidx < end ? L.sorted[nidx] : 0u;
             }
-#pragma unroll(kFwdUnroll)
-            for (int u = 0; u < nl && !(T.x < 0.f && T.y < 0.f); u++) {
-                const int j = slist[wl][u];
-                if (CNT) nev += (unsigned)(T.x > 0.f) + (unsigned)(T.y > 0.f);
+            // one entry: the CA power and skip test (geometry only: liveness is applied at the
+            // entry's turn), the CA exp and α, then the blend in list order
+            auto geo = [&](int j, float2& power, bool& g0, bool& g1) {
                 const float4 e0 = se[0][j], e1 = se[1][j];
                 const float2 dx = __fadd2_rn(ff2(e0.x, e0.x), nfx);
                 const float2 dy = __fadd2_rn(ff2(e0.y, e0.y), nfy);
@@ -245,16 +247,17 @@ __global__ __launch_bounds__(RT) void k_render_fwd_p(Launch L, float* __restrict
                 const float2 CdyDy = __fmul2_rn(__fmul2_rn(ff2(e0.w, e0.w), dy), dy);
                 const float2 inner = __ffma2_rn(Adx, dx, CdyDy);
                 const float2 nBdxdy = __fmul2_rn(__fmul2_rn(ff2(-e1.x, -e1.x), dx), dy);
-                const float2 power = __ffma2_rn(mhalf, inner, nBdxdy);
-                const bool in0 = T.x > 0.f && !(power.x > 0.f) && !(power.x < e1.z);
-                const bool in1 = T.y > 0.f && !(power.y > 0.f) && !(power.y < e1.z);
-                if (!(in0 || in1)) continue;
-                if (CNT) nexp += (unsigned)in0 + (unsigned)in1;
-                const float2 G = ca_exp_core2(power);
-                const float2 oG = __fmul2_rn(ff2(e1.y, e1.y), G);
-                const float2 alpha = ff2(fminf(ALPHA_MAX, oG.x), fminf(ALPHA_MAX, oG.y));
+                power = __ffma2_rn(mhalf, inner, nBdxdy);
+                g0 = !(power.x > 0.f) && !(power.x < e1.z);
+                g1 = !(power.y > 0.f) && !(power.y < e1.z);
+            };
+            auto alpha_of = [&](int j, float2 power) {
+                const float o = se[1][j].y;
+                const float2 oG = __fmul2_rn(ff2(o, o), ca_exp_core2(power));
+                return ff2(fminf(ALPHA_MAX, oG.x), fminf(ALPHA_MAX, oG.y));
+            };
+            auto blend = [&](int j, float2 alpha, bool in0, bool in1) {
                 const bool ok0 = in0 && !(alpha.x < ALPHA_MIN), ok1 = in1 && !(alpha.y < ALPHA_MIN);
-                if (!(ok0 || ok1)) continue;
                 const float2 Tn = __fmul2_rn(T, __ffma2_rn(alpha, mone, one));  // T·(1 − α), CA
                 const bool term0 = ok0 && Tn.x < T_EPS, term1 = ok1 && Tn.y < T_EPS;
                 const bool bl0 = ok0 && !term0, bl1 = ok1 && !term1;
@@ -263,11 +266,55 @@ __global__ __launch_bounds__(RT) void k_render_fwd_p(Launch L, float* __restrict
                 C0 = __ffma2_rn(ff2(e2.x, e2.x), w, C0);
                 C1 = __ffma2_rn(ff2(e2.y, e2.y), w, C1);
                 C2 = __ffma2_rn(ff2(e2.z, e2.z), w, C2);
-                if (DEPTH) D = __ffma2_rn(ff2(e1.w, e1.w), w, D);
+                if (DEPTH) D = __ffma2_rn(ff2(se[1][j].w, se[1][j].w), w, D);
                 T = ff2(bl0 ? Tn.x : (term0 ? -T.x : T.x), bl1 ? Tn.y : (term1 ? -T.y : T.y));
                 const int jn = jbase + j;
                 last0 = bl0 ? jn : last0;
                 last1 = bl1 ? jn : last1;
+            };
+            int u = 0;
+#if MVGS_FWD_PAIR
+            // two entries per step: both geometries and exps first (independent chains), then the
+            // two blends in list order — the second sees the first's T, so every decision is the
+            // one-entry walk's
+            for (; u + 1 < nl && !(T.x < 0.f && T.y < 0.f); u += 2) {
+                const int ja = slist[wl][u], jb = slist[wl][u + 1];
+                float2 pa, pb;
+                bool ga0, ga1, gb0, gb1;
+                geo(ja, pa, ga0, ga1);
+                geo(jb, pb, gb0, gb1);
+                if (!(ga0 || ga1 || gb0 || gb1)) {
+                    if (CNT) nev += 2u * ((unsigned)(T.x > 0.f) + (unsigned)(T.y > 0.f));
+                    continue;
+                }
+                const float2 aa = alpha_of(ja, pa), ab = alpha_of(jb, pb);
+                const bool ia0 = T.x > 0.f && ga0, ia1 = T.y > 0.f && ga1;
+                if (CNT) {
+                    nev += (unsigned)(T.x > 0.f) + (unsigned)(T.y > 0.f);
+                    nexp += (unsigned)ia0 + (unsigned)ia1;
+                }
+                blend(ja, aa, ia0, ia1);
+                const bool ib0 = T.x > 0.f && gb0, ib1 = T.y > 0.f && gb1;
+                if (CNT) {
+                    nev += (unsigned)(T.x > 0.f) + (unsigned)(T.y > 0.f);
+                    nexp += (unsigned)ib0 + (unsigned)ib1;
+                }
+                blend(jb, ab, ib0, ib1);
+            }
+#endif
+#pragma unroll(kFwdUnroll)
+            for (; u < nl && !(T.x < 0.f && T.y < 0.f); u++) {
+                const int j = slist[wl][u];
+                if (CNT) nev += (unsigned)(T.x > 0.f) + (unsigned)(T.y > 0.f);
+                float2 power;
+                bool g0, g1;
+                geo(j, power, g0, g1);
+                const bool in0 = T.x > 0.f && g0, in1 = T.y > 0.f && g1;
+                if (!(in0 || in1)) continue;
+                if (CNT) nexp += (unsigned)in0 + (unsigned)in1;
+                const float2 alpha = alpha_of(j, power);
+                if (!((in0 && !(alpha.x < ALPHA_MIN)) || (in1 && !(alpha.y < ALPHA_MIN)))) continue;
+                blend(j, alpha, in0, in1);
             }
             if (PF && b0 + FB + (int)threadIdx.x < end) {  // warm the next batch's record in L2
                 const float4* rn = L.rec + 3 * (int64_t)qn;
