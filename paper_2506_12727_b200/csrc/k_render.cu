@@ -36,7 +36,7 @@ namespace mvgs {
 #define MVGS_FWD_BATCH 1  // forward staged batch = 128 × this entries
 #endif
 #ifndef MVGS_FWD_PAIR
-#define MVGS_FWD_PAIR 1  // forward walk: two entries per step (experiment knob)
+#define MVGS_FWD_PAIR 1  // forward walk: two entries per step (measured: garden fwd 0.409 → 0.375 ms; four: no gain)
 #endif
 #ifndef MVGS_BWD_PAIR
 #define MVGS_BWD_PAIR 1  // backward walk: two entries per step (measured: garden bwd 0.739 → 0.713, playroom 3.44 → 3.31 ms)
