@@ -238,9 +238,12 @@ def run_mvgs(args):
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
-    if args.profile:
+    if args.profile:  # the profiled step is bracketed for `ncu --profile-from-start off`
+        torch.cuda.synchronize()
+        torch.cuda.profiler.start()
         step()
         torch.cuda.synchronize()
+        torch.cuda.profiler.stop()
         print(json.dumps({"profile": True, "stats": mvgs.query(R.ctx)}), flush=True)
         return
     st = mvgs.query(R.ctx)  # structural stats of this workload incl. evaluation counts (sync, untimed)

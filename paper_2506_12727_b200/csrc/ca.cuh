@@ -203,8 +203,14 @@ __device__ __forceinline__ int ca_clamp_tile(float v, int tmax) {
     return __float2int_rz(v);
 }
 
+// Jacobian clamp limits of a camera (R4): 0.65·W/fx, 0.65·H/fy in CA arithmetic (per camera)
+__device__ __forceinline__ float2 ca_clamp_limits(const mvgs_camera& c) {
+    return make_float2(FDIV(FMUL(0.65f, __int2float_rn(c.width)), c.fx),
+                       FDIV(FMUL(0.65f, __int2float_rn(c.height)), c.fy));
+}
+
 __device__ __forceinline__ void ca_project(const mvgs_camera& c, float mx, float my, float mz,
-                                           const float Sig[6], int TX, int TY, Proj& p) {
+                                           const float Sig[6], int TX, int TY, float2 lim, Proj& p) {
     const float* R = c.R;
     p.tx = FMA(R[2], mz, FMA(R[1], my, FMA(R[0], mx, c.t[0])));
     p.ty = FMA(R[5], mz, FMA(R[4], my, FMA(R[3], mx, c.t[1])));
@@ -212,8 +218,7 @@ __device__ __forceinline__ void ca_project(const mvgs_camera& c, float mx, float
     float ux = FDIV(p.tx, p.tz), uy = FDIV(p.ty, p.tz);
     p.px = FMA(c.fx, ux, c.cx);
     p.py = FMA(c.fy, uy, c.cy);
-    float limx = FDIV(FMUL(0.65f, __int2float_rn(c.width)), c.fx);
-    float limy = FDIV(FMUL(0.65f, __int2float_rn(c.height)), c.fy);
+    const float limx = lim.x, limy = lim.y;
     p.uxc = fminf(limx, fmaxf(-limx, ux));
     p.uyc = fminf(limy, fmaxf(-limy, uy));
     p.clx = (ux > limx) || (ux < -limx);

@@ -276,6 +276,7 @@ __global__ __launch_bounds__(BLK) void k_project(Launch L) {
     extern __shared__ float4 sh_s4[];  // [BLK][SS] SH rows
     float* sh_s = reinterpret_cast<float*>(sh_s4);
     __shared__ int wc[BLK / 32][32];
+    __shared__ float2 slim[32];  // the chunk's Jacobian clamp limits (R4)
     __shared__ int sboff[32];  // first pair slot of this block in each view of the chunk
     __shared__ mvgs_camera scams[32];  // the chunk's cameras
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -326,21 +327,31 @@ __global__ __launch_bounds__(BLK) void k_project(Launch L) {
             const unsigned bal = __ballot_sync(FULL, (pm >> k) & 1u);
             if (lane == 0) wc[warp][k] = __popc(bal);
         }
-        if (threadIdx.x < nv) sboff[threadIdx.x] = L.blk_off[(int64_t)(v0 + threadIdx.x) * L.NB + blockIdx.x];
+        if (threadIdx.x < nv) {
+            sboff[threadIdx.x] = L.blk_off[(int64_t)(v0 + threadIdx.x) * L.NB + blockIdx.x];
+            slim[threadIdx.x] = ca_clamp_limits(L.cams[v0 + threadIdx.x]);  // once per view, not per pair
+        }
         for (int i = threadIdx.x; i < nv * (int)(sizeof(mvgs_camera) / 4); i += BLK)
             reinterpret_cast<uint32_t*>(scams)[i] = reinterpret_cast<const uint32_t*>(L.cams + v0)[i];
         cp_async_wait_all();
+        __syncthreads();
+        if (threadIdx.x < nv) {  // exclusive prefix over warps, per view: wc[w][k] ← Σ_{w' < w}
+            int run = 0;
+            for (int w = 0; w < BLK / 32; w++) {
+                const int c = wc[w][threadIdx.x];
+                wc[w][threadIdx.x] = run;
+                run += c;
+            }
+        }
         __syncthreads();
         for (int k = 0; k < nv; k++) {
             const mvgs_camera& c = scams[k];
             const bool vis = (pm >> k) & 1u;
             const unsigned bal = __ballot_sync(FULL, vis);
             if (!vis) continue;
-            int pre = 0;
-            for (int w = 0; w < warp; w++) pre += wc[w][k];
-            const int64_t pair = (int64_t)sboff[k] + pre + __popc(bal & lt);
+            const int64_t pair = (int64_t)sboff[k] + wc[warp][k] + __popc(bal & lt);
             Proj p;
-            ca_project(c, mx, my, mz, a.Sig, L.TX, L.TY, p);
+            ca_project(c, mx, my, mz, a.Sig, L.TX, L.TY, slim[k], p);
             const int tiles = p.ok ? (p.rx1 - p.rx0) * (p.ry1 - p.ry0) : 0;
             if (pair < L.cap_pairs) {  // depth key + rect for the pair sort (the value is the slot itself)
                 L.pkey[pair] = tiles > 0 ? __float_as_uint(p.tz) : 0xffffffffu;
@@ -538,7 +549,7 @@ __global__ void k_export(Launch L, int64_t* range_start, int32_t* entry_gid, int
                 ca_activate(L.log_scales + 3 * gid, L.quats + 4 * gid, L.opac[gid], a);
                 Proj p;
                 ca_project(L.cams[view], L.means[3 * gid], L.means[3 * gid + 1], L.means[3 * gid + 2], a.Sig, L.TX,
-                           L.TY, p);
+                           L.TY, ca_clamp_limits(L.cams[view]), p);
                 radius = p.radius;
             }
             o[0] = radius;
