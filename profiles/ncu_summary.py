@@ -13,8 +13,7 @@ import subprocess
 import sys
 from collections import OrderedDict
 
-STAGE_OF = [("k_count", "count"), ("k_project", "project"), ("k_rs_onesweep<1>", "sort_pairs"),
-            ("k_dup", "dup"), ("k_rs_scatter<0>", "sort_entries"), ("k_render_fwd", "render_fwd"),
+STAGE_OF = [("k_count", "count"), ("k_project", "project"), ("k_dup", "dup"), ("k_render_fwd", "render_fwd"),
             ("k_render_bwd", "render_bwd"), ("k_gauss_bwd", "gauss_bwd")]
 
 METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
@@ -59,18 +58,48 @@ def report(path):
         print("  stalls: " + ", ".join(f"{c} {100 * v / tot:.0f}%" for v, c in st[:8]))
 
 
+def _stage_of_sequence(names):
+    """Stage of each launch of one step, from the launch order: count, scan, project; the pair
+    sort (hist / scan / scatter passes) up to k_dup; dup (its scan and k_dup); the entry sort and
+    ranges up to the forward; then the forward, backward and per-Gaussian kernels."""
+    out, phase = [], "count"
+    for nm in names:
+        if nm.startswith("k_count"):
+            phase = "count"
+        elif nm.startswith("k_project"):
+            phase = "project"
+        elif phase == "project" and nm.startswith("k_rs_hist"):
+            phase = "sort_pairs"
+        elif nm.startswith("k_dup"):
+            phase = "dup"
+        elif phase == "dup" and not nm.startswith("k_dup"):
+            phase = "sort_entries"
+        elif nm.startswith("k_render_fwd"):
+            phase = "render_fwd"
+        elif nm.startswith("k_render_bwd"):
+            phase = "render_bwd"
+        elif nm.startswith("k_gauss_bwd"):
+            phase = "gauss_bwd"
+        if phase == "sort_pairs" and nm.startswith("k_scan_1p") and out and out[-1] == "sort_pairs" and \
+                names[len(out) - 1].startswith("k_rs_scatter"):
+            phase = "dup"  # the scan of the tile counts that follows the last pair pass
+        out.append(phase)
+    return out
+
+
 def traffic(path, out):
+    """DRAM bytes (read + write) per stage of one step, from an ncu --set full capture of that step
+    (bench.py --profile under ncu --profile-from-start off)."""
     h, units, rows = _raw(path)
+    sc = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    names = [r[h.index("Kernel Name")].replace("mvgs::", "").replace("void ", "") for r in rows]
+    stages = _stage_of_sequence(names)
     res = {}
-    for r in rows:
-        name = r[h.index("Kernel Name")].replace("mvgs::", "").replace("void ", "")
-        for pat, stage in STAGE_OF:
-            if name.startswith(pat.split("<")[0]) and (("<" not in pat) or pat.split("<")[1].split(">")[0] in name):
-                sc = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
-                tot = 0.0
-                for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"):  # units differ per metric
-                    tot += _num(r[h.index(m)]) * sc.get(units[h.index(m)], 1)
-                res[stage] = tot
+    for r, st in zip(rows, stages):
+        tot = 0.0
+        for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"):  # units differ per metric
+            tot += _num(r[h.index(m)]) * sc.get(units[h.index(m)], 1)
+        res[st] = res.get(st, 0.0) + tot
     json.dump(res, open(out, "w"), indent=1)
     print(json.dumps(res, indent=1))
 
