@@ -36,6 +36,7 @@ struct Launch {  // everything a kernel needs about the current batch
     // workspace
     int* blk_off;     // [V*NB + 1]  exclusive scan of per-(view, block) participation counts
     int* bucket_off;  // [V*T + 1]   exclusive scan of per-(view, tile) entry counts
+    const int* order; // [V*T] compositing CTA i renders bucket order[i] (longest list first), or null
     float4* rec;      // [cap_pairs * 3]
     uint32_t* pflag;  // [cap_pairs] bit0-2 rgb clamped, bit3-4 Jacobian clamps, bit5 tiles > 0, bits 8..31 radius
     float* pgrad;     // [cap_pairs * PG_STRIDE]
@@ -89,6 +90,8 @@ struct mvgs_ctx {
     mvgs_camera* d_cams = nullptr;
     int* d_blk = nullptr;
     int* d_bucket = nullptr;
+    int* d_order = nullptr;  // [V*T] longest-list-first CTA order of the compositing kernels
+    bool use_lpt = false;    // MVGS_LPT=1: longest-list-first CTA order (measured: no gain at garden / large, −1 % playroom)
     float4* d_rec = nullptr;
     uint32_t* d_pflag = nullptr;
     float* d_pgrad = nullptr;
@@ -150,6 +153,7 @@ cudaError_t launch_project(const Launch& L, cudaStream_t s);
 cudaError_t launch_sort_pairs(const Launch& L, const uint32_t** order_out, const uint2** rect_out, cudaStream_t s);
 cudaError_t launch_dup_sort(const Launch& L, const uint32_t* order, const uint2* rect, cudaStream_t s);
 cudaError_t launch_sort_entries(const Launch& L, uint32_t** sorted_vals, cudaStream_t s);
+cudaError_t launch_lpt_order(const Launch& L, int* order, cudaStream_t s);
 int64_t radix_counts_size(int64_t cap);
 int radix_tiles(int64_t cap);
 cudaError_t launch_render_fwd(const Launch& L, float* rgb, float* Tf, int32_t* nc, float* depth, const CUtensorMap* tm,

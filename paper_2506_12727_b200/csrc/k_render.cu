@@ -197,7 +197,7 @@ __global__ __launch_bounds__(RT) void k_render_fwd_p(Launch L, float* __restrict
     __shared__ uint8_t slist[RT / 32][FB];
     __shared__ unsigned sev[2];
     zero_pgrad_slice(L);
-    const int bucket = blockIdx.x;
+    const int bucket = L.order ? L.order[blockIdx.x] : blockIdx.x;  // longest list first
     const int v = bucket / L.T, tile = bucket - v * L.T;
     const int ty = tile / L.TX, tx = tile - ty * L.TX;
     int x, y[2];
@@ -355,7 +355,7 @@ __global__ __launch_bounds__(RT) void k_render_fwd_tma(Launch L, const __grid_co
     __shared__ uint8_t slist[RT / 32][RT];
     __shared__ unsigned sev[2];
     zero_pgrad_slice(L);
-    const int bucket = blockIdx.x;
+    const int bucket = L.order ? L.order[blockIdx.x] : blockIdx.x;  // longest list first
     const int v = bucket / L.T, tile = bucket - v * L.T;
     const int ty = tile / L.TX, tx = tile - ty * L.TX;
     const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
@@ -605,7 +605,7 @@ __global__ __launch_bounds__(128, MVGS_BWD_MINB) void k_render_bwd_p(Launch L, c
     __shared__ uint8_t smask[RB];
     __shared__ uint8_t slist[NW][RB];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int bucket = blockIdx.x;
+    const int bucket = L.order ? L.order[blockIdx.x] : blockIdx.x;  // longest list first
     const int v = bucket / L.T, tile = bucket - v * L.T;
     const int ty = tile / L.TX, tx = tile - ty * L.TX;
     int x, y0, y1_;

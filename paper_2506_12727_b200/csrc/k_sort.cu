@@ -541,6 +541,48 @@ static int radix_sort_pairs_3k(const Launch& L, cudaStream_t s, cudaError_t* err
     return npass;
 }
 
+// Longest-list-first order of the (view, tile) CTAs of the compositing kernels (LPT):
+// a thread waits for its block and a block for its list, so the long lists (garden: max
+// 7,812 vs mean 1,737 entries) are dispatched first and the short ones fill the tail.  One CTA
+// bins the buckets by list length (32-entry bins, descending; 255 = ≥ 8,160) and scatters their
+// ids in bin order; the order inside a bin is arbitrary (no result depends on CTA order).
+constexpr int LPT_T = 1024, LPT_BINS = 256;
+__global__ __launch_bounds__(LPT_T) void k_lpt_order(const int* __restrict__ off, int nb, int* __restrict__ order) {
+    __shared__ int cnt[LPT_BINS];
+    if (threadIdx.x < LPT_BINS) cnt[threadIdx.x] = 0;
+    __syncthreads();
+    auto bin_of = [&](int b) { return LPT_BINS - 1 - min(LPT_BINS - 1, (off[b + 1] - off[b]) >> 5); };
+    for (int b = threadIdx.x; b < nb; b += LPT_T) atomicAdd(&cnt[bin_of(b)], 1);
+    __syncthreads();
+    if (threadIdx.x < 32) {  // exclusive scan of the 256 bins by warp 0 (8 per lane)
+        int v[LPT_BINS / 32], sum = 0;
+#pragma unroll
+        for (int i = 0; i < LPT_BINS / 32; i++) {
+            v[i] = cnt[threadIdx.x * (LPT_BINS / 32) + i];
+            sum += v[i];
+        }
+        int inc = sum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(FULLS, inc, o);
+            if ((int)threadIdx.x >= o) inc += y;
+        }
+        int run = inc - sum;
+#pragma unroll
+        for (int i = 0; i < LPT_BINS / 32; i++) {
+            cnt[threadIdx.x * (LPT_BINS / 32) + i] = run;
+            run += v[i];
+        }
+    }
+    __syncthreads();
+    for (int b = threadIdx.x; b < nb; b += LPT_T) order[atomicAdd(&cnt[bin_of(b)], 1)] = b;
+}
+
+cudaError_t launch_lpt_order(const Launch& L, int* order, cudaStream_t s) {
+    k_lpt_order<<<1, LPT_T, 0, s>>>(L.bucket_off, L.V * L.T, order);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_sort_pairs(const Launch& L, const uint32_t** order_out, const uint2** rect_out, cudaStream_t s) {
     cudaError_t e;
     const int np = radix_sort_pairs_3k(L, s, &e);

@@ -186,6 +186,7 @@ mvgs_status mvgs_create(mvgs_ctx** out, int device, int64_t max_pairs, int64_t m
     if (!ctx) return MVGS_ERR_INVALID;
     ctx->device = device;
     if (const char* m = getenv("MVGS_TMA")) ctx->use_tma = strcmp(m, "1") == 0;
+    if (const char* m = getenv("MVGS_LPT")) ctx->use_lpt = strcmp(m, "1") == 0;
     cudaError_t e = cudaSetDevice(device);
     if (e != cudaSuccess) {
         delete ctx;
@@ -215,7 +216,7 @@ void mvgs_destroy(mvgs_ctx* ctx) {
     if (!ctx) return;
     cudaSetDevice(ctx->device);
     cudaDeviceSynchronize();
-    cudaFree(ctx->d_cams); cudaFree(ctx->d_blk); cudaFree(ctx->d_bucket);
+    cudaFree(ctx->d_cams); cudaFree(ctx->d_blk); cudaFree(ctx->d_bucket); cudaFree(ctx->d_order);
     cudaFree(ctx->d_rec); cudaFree(ctx->d_pgrad);
     cudaFree(ctx->d_key); cudaFree(ctx->d_val); cudaFree(ctx->d_key2); cudaFree(ctx->d_val2);
     cudaFree(ctx->d_pkey); cudaFree(ctx->d_pval); cudaFree(ctx->d_pkey2); cudaFree(ctx->d_pval2);
@@ -284,7 +285,9 @@ mvgs_status mvgs_preprocess(mvgs_ctx* ctx, const mvgs_gaussians* g, const mvgs_c
         CK(cudaDeviceSynchronize());
         CK(grow(ctx->d_pmask, ctx->cap_pmask, need_pmask));
         CK(grow(ctx->d_blk, ctx->cap_blk, nblk + 1));
+        int64_t cb = ctx->cap_buckets;
         CK(grow(ctx->d_bucket, ctx->cap_buckets, nbuck + 1));
+        CK(grow(ctx->d_order, cb, nbuck + 1));
         if (need_scan > ctx->cap_scan) {
             cudaFree(ctx->d_scan);
             ctx->d_scan = nullptr;
@@ -333,11 +336,13 @@ mvgs_status mvgs_preprocess(mvgs_ctx* ctx, const mvgs_gaussians* g, const mvgs_c
     if (NB > 0) {
         { STAGE(ST_SORT_PAIRS); CK(launch_sort_pairs(L, &order, &rect, s)); }                        // S4a
         { STAGE(ST_DUP); CK(launch_dup_sort(L, order, rect, s)); }                                   // S3
-        { STAGE(ST_SORT_ENTRIES); CK(launch_sort_entries(L, &sorted, s)); }                          // S4b + S5
+        { STAGE(ST_SORT_ENTRIES); CK(launch_sort_entries(L, &sorted, s));                           // S4b + S5
+          if (ctx->use_lpt) CK(launch_lpt_order(L, ctx->d_order, s)); }                              // CTA order
     } else {
         CK(cudaMemsetAsync(ctx->d_bucket, 0, sizeof(int) * (nbuck + 1), s));
     }
     L.sorted = sorted;
+    L.order = (NB > 0 && ctx->use_lpt) ? ctx->d_order : nullptr;
     ctx->state = 1;
     return MVGS_OK;
 }

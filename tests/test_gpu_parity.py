@@ -550,3 +550,20 @@ def test_tma_staged_forward_is_bit_identical(require_gpu):
     assert out[0][3] > 512  # several staged batches per list
     for a, b in zip(out[0][:3], out[1][:3]):
         np.testing.assert_array_equal(a, b)
+
+
+@pytest.mark.gpu
+def test_longest_list_first_cta_order_changes_nothing(require_gpu, monkeypatch):
+    """MVGS_LPT=1 (compositing CTAs in longest-list-first order): the same lists,
+    n_contrib and images bit-exact, gradients to the parity rule (only atomic order differs)."""
+    import dataclasses
+    cfg = dataclasses.replace(synth.CONFIGS["tiny"], P=20_000)
+    g, cams = synth.make_scene(cfg)
+    dL = synth.make_dLdC_scaled(cfg.V, cfg.H, cfg.W, 4)
+    base = run_gpu(g, cams, dL)
+    monkeypatch.setenv("MVGS_LPT", "1")
+    lpt = run_gpu(g, cams, dL)
+    for k in ("n_contrib", "rgb", "T_final", "range_start", "entry_gid", "vis", "max_radius"):
+        np.testing.assert_array_equal(lpt[k], base[k], err_msg=k)
+    for k in ("d_means", "d_log_scales", "d_quats", "d_opacity_logits", "d_sh", "e1", "e2", "e_old"):
+        np.testing.assert_allclose(lpt[k], base[k], rtol=1e-4, atol=1e-6 * np.abs(base[k]).max(), err_msg=k)
