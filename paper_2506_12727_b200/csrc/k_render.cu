@@ -596,7 +596,7 @@ __global__ __launch_bounds__(128, MVGS_BWD_MINB) void k_render_bwd_p(Launch L, c
                                                       const float* __restrict__ in_T,
                                                       const int32_t* __restrict__ in_n) {
     constexpr int NW = 4, RB = 128;
-    __shared__ float4 se[3][RB];  // one array: the three loads of an entry share its address (immediate offsets)
+    __shared__ float4 se[4][RB];  // one array: an entry's loads share its address (immediate offsets)
     __shared__ uint32_t sq[RB];
     __shared__ __align__(16) float sacc[NW][RB * NG];
     __shared__ float skscale[NG];
@@ -640,12 +640,13 @@ __global__ __launch_bounds__(128, MVGS_BWD_MINB) void k_render_bwd_p(Launch L, c
         smax = 0;
         sev[0] = sev[1] = 0;
     }
-    // per-value scale applied at the flush: Σ∇ = −(W/2, H/2)·(A d + B e, C e + B d) with
-    // d, e = ∂L/∂power·(dx, dy); ∂A = −½Σ d·dx, ∂B = −Σ d·dy, ∂C = −½Σ e·dy; the colour terms
+    // per-value scale applied at the flush: Σ∇ = −Σ (W/2·(A d + B e), H/2·(C e + B d)) (the
+    // W/2, H/2 are folded into the staged conic) with d, e = ∂L/∂power·(dx, dy);
+    // ∂A = −½Σ d·dx, ∂B = −Σ d·dy, ∂C = −½Σ e·dy; the colour terms
     // were accumulated with −w; slot 6 (o·∂L/∂o) is scaled by the entry's 1/o
     if (threadIdx.x < NG) {
         const int k = threadIdx.x;
-        skscale[k] = k == 0 ? -hw : k == 1 ? -hh : (k == 3 || k == 5) ? -0.5f : (k == 4 || k >= 7) ? -1.f : 1.f;
+        skscale[k] = (k == 0 || k == 1) ? -1.f : (k == 3 || k == 5) ? -0.5f : (k == 4 || k >= 7) ? -1.f : 1.f;
     }
     __syncthreads();
     unsigned nev = 0, nexp = 0, nbl0 = 0, nbl1 = 0;
@@ -663,7 +664,6 @@ __global__ __launch_bounds__(128, MVGS_BWD_MINB) void k_render_bwd_p(Launch L, c
     const int wstride = owner ? NG : 0;
     const float2 nfx = f2(-(float)x, -(float)x), nfy = f2(-(float)y0, -(float)y1_);
     const float2 mhalf = f2(-0.5f, -0.5f);
-    const float2 hw2 = f2(hw * hw, hw * hw), hh2 = f2(hh * hh, hh * hh);
     for (int b_end = maxlast; b_end > 0; b_end -= RB) {
         const int b0 = max(0, b_end - RB);
         const int cnt = b_end - b0;
@@ -677,6 +677,9 @@ __global__ __launch_bounds__(128, MVGS_BWD_MINB) void k_render_bwd_p(Launch L, c
             se[0][t] = make_float4(r0.x, r0.y, r0.z, r1.x);
             se[1][t] = make_float4(r0.w, r1.y, r2.z, r2.w);
             se[2][t] = make_float4(r1.z, r1.w, r2.x, 0.f);
+            // the conic scaled by the NDC factors: (W/2)·(A, B) and (H/2)·(C, B) give ∇_{p_i}L's
+            // components directly, so the per-pixel norm for E1 needs no further scaling
+            se[3][t] = make_float4(hw * r0.z, hw * r0.w, hh * r1.x, hh * r0.w);
             smask[t] = (uint8_t)warp_block_mask(r0.x, r0.y, r0.z, r0.w, r1.x, r2.z, (float)(tx * TILE), (float)(ty * TILE));
         }
         {
@@ -734,13 +737,12 @@ __global__ __launch_bounds__(128, MVGS_BWD_MINB) void k_render_bwd_p(Launch L, c
             dLdpw = __fmul2_rn(oGc, dLda);
         };
         auto terms = [&](int jj, float2 dx, float2 dy, float2 nw, float2 dLdpw, float (&val)[NG]) {
-            const float4 e0 = se[0][jj];
-            const float Bs = se[1][jj].x;
-            const float2 A2 = f2(e0.z, e0.z), C2 = f2(e0.w, e0.w), B2 = f2(Bs, Bs);
+            const float4 s3 = se[3][jj];  // (W/2·A, W/2·B, H/2·C, H/2·B)
             const float2 d = __fmul2_rn(dLdpw, dx), e = __fmul2_rn(dLdpw, dy);
-            const float2 gxr = __ffma2_rn(A2, d, __fmul2_rn(B2, e));
-            const float2 gyr = __ffma2_rn(C2, e, __fmul2_rn(B2, d));
-            const float2 n2 = __ffma2_rn(__fmul2_rn(gxr, gxr), hw2, __fmul2_rn(__fmul2_rn(gyr, gyr), hh2));
+            // −∇_{p_i}L per pixel (NDC): x = W/2·(A d + B e), y = H/2·(C e + B d)
+            const float2 gxr = __ffma2_rn(f2(s3.x, s3.x), d, __fmul2_rn(f2(s3.y, s3.y), e));
+            const float2 gyr = __ffma2_rn(f2(s3.z, s3.z), e, __fmul2_rn(f2(s3.w, s3.w), d));
+            const float2 n2 = __ffma2_rn(gxr, gxr, __fmul2_rn(gyr, gyr));
             const float2 dd = __fmul2_rn(d, dx), de = __fmul2_rn(d, dy), ee = __fmul2_rn(e, dy);
             const float2 wr = __fmul2_rn(nw, dLr), wg = __fmul2_rn(nw, dLg), wb = __fmul2_rn(nw, dLb);
             val[0] = gxr.x + gxr.y;
