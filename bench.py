@@ -61,8 +61,9 @@ def parse():
                          "(SURVEY §8(d): large, 32 views)")
     ap.add_argument("--exchange", default="allreduce", choices=["allreduce", "owner"],
                     help="N>1 exchange: chunked all-reduce of the flat buffer, or owner-sharded slots (DESIGN §11)")
-    ap.add_argument("--e2e-steps", type=int, default=16)
+    ap.add_argument("--e2e-steps", type=int, default=24)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--eager", action="store_true", help="time eager launches instead of one CUDA-graph replay per step")
     ap.add_argument("--profile", action="store_true",
                     help="sizing pass + warmup + one step, nothing else (for ncu)")
     return ap.parse_args()
@@ -249,8 +250,25 @@ def run_mvgs(args):
     st = mvgs.query(R.ctx)  # structural stats of this workload incl. evaluation counts (sync, untimed)
     if os.environ.get("MVGS_BENCH_COUNT", "0") != "1":
         mvgs.set_eval_counting(R.ctx, False)  # statistics off in the timed steps (same workload, same counts)
-    mvgs.set_timing(R.ctx, True)
-    mvgs.stage_times(R.ctx)  # clear
+    # One GPU: the step (S1–S9, every kernel) is captured once into a CUDA graph and replayed —
+    # the launch-bound tail of a 27-launch step.  Several GPUs: eager steps (the
+    # all-reduce chunks / owner exchange stay outside capture).
+    graph = None
+    if dist is None and not owner and not args.eager:
+        cs = torch.cuda.Stream()
+        cs.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(cs):
+            step()
+        torch.cuda.current_stream().wait_stream(cs)
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            step()
+        torch.cuda.synchronize()
+        for _ in range(args.warmup):
+            graph.replay()
+        torch.cuda.synchronize()
+    run_step = graph.replay if graph is not None else step
     clk = Clocks(local)
     clk.start()
     time.sleep(0.3)
@@ -262,7 +280,7 @@ def run_mvgs(args):
     ev0.record()
     evs[0].record()
     for i in range(args.steps):
-        step()
+        run_step()
         evs[i + 1].record()
     ev1.record()
     torch.cuda.synchronize()
@@ -272,6 +290,21 @@ def run_mvgs(args):
         dist.barrier()
     clocks = clk.stop()
     ms = ev0.elapsed_time(ev1) / args.steps
+    # Per-stage kernel times: a second timed region of the same K steps, eager, with a pair of
+    # CUDA events around every stage on the launching stream (events between kernels add
+    # ≈ 2 % of idle gaps, so the headline region above carries none).
+    mvgs.set_timing(R.ctx, True)
+    mvgs.stage_times(R.ctx)  # clear
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    es0, es1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    es0.record()
+    for i in range(args.steps):
+        step()
+    es1.record()
+    torch.cuda.synchronize()
+    ms_staged = es0.elapsed_time(es1) / args.steps
     stages = mvgs.stage_times(R.ctx)
     mvgs.set_timing(R.ctx, False)
     if dist is not None:
@@ -344,8 +377,8 @@ def run_mvgs(args):
             t = float(tt.item())
         return t
 
-    e2e_step(0)
-    e2e_step(1)
+    for i in range(6):  # warm-up: the pinned buffers' first transfers run slower
+        e2e_step(i)
     e2e_ms = e2e_time(e2e_step, args.e2e_steps)
 
     # host-resident parameters: whole parameter set up, whole output buffer down, every step
@@ -423,6 +456,9 @@ def run_mvgs(args):
         "config": {**workload_config(cfg, P, Vr, N, V_all),
                    "exchange": args.exchange if N > 1 or owner else "none (1 GPU)",
                    "allreduce_chunks": CHUNKS,
+                   "launch": "CUDA graph replay (one capture of S1-S9)" if graph is not None else "eager",
+                   "stage_timing": "second region of %d eager steps with events around each stage: %.4f ms/step"
+                                   % (args.steps, ms_staged),
                    "l2": "inputs larger than L2 (params %.0f MB)" % (sum(v.nbytes for v in g_np.values()
                                                                        if isinstance(v, np.ndarray)) / 1e6),
                    "Q": st["Q"], "K": st["K"], "max_bucket": st["max_bucket"], "n_visible": st["n_visible"],

@@ -89,24 +89,21 @@ __global__ __launch_bounds__(RS_T) void k_rs_hist(const uint32_t* __restrict__ k
 // tile is first re-ordered by digit in shared memory, then written out by
 // consecutive threads: every digit's run lands contiguously at
 // offsets[digit * ntiles + tile], so global writes are coalesced.
-// Optionally moves a 64-bit payload with each key.
 #ifndef MVGS_RS3_MINB
 #define MVGS_RS3_MINB 6  // resident CTAs asked of the three-kernel scatter (6: 40 registers, 72 B spill; 1: 60 registers)
 #endif
-template <bool PAYLOAD, int IPT>
+template <int IPT>
 __global__ __launch_bounds__(RS_T, MVGS_RS3_MINB) void k_rs_scatter(const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin,
                                                      uint32_t* __restrict__ kout, uint32_t* __restrict__ vout,
-                                                     const uint2* __restrict__ pin, uint2* __restrict__ pout,
+                                                     uint2* __restrict__ pout,
                                                      const int* __restrict__ n_ptr, int64_t cap, int shift, int nbits,
                                                      const int* __restrict__ offs, int ntiles,
                                                      int* __restrict__ range_min, const uint2* __restrict__ gather_pl,
                                                      int* __restrict__ cnt_out) {
     constexpr int TILE = RS_T * IPT;
     __shared__ uint32_t hist[RS_NW][RS_BINS];
-    __shared__ uint32_t dstart[RS_BINS];   // first local position of each digit
     __shared__ uint32_t gdelta[RS_BINS];   // global offset − local start, per digit
     __shared__ uint32_t sk[TILE], sv[TILE];
-    __shared__ uint2 sp[PAYLOAD ? TILE : 1];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const unsigned lt = (1u << lane) - 1u;
     const int n = (int)min((int64_t)*n_ptr, cap);
@@ -120,14 +117,12 @@ __global__ __launch_bounds__(RS_T, MVGS_RS3_MINB) void k_rs_scatter(const uint32
     for (int i = 0; i < RS_BINS / 32; i++) hist[warp][lane + 32 * i] = 0;
     __syncwarp();
     uint32_t key[IPT], val[IPT], loc[IPT];
-    uint2 pay[PAYLOAD ? IPT : 1];
 #pragma unroll
     for (int it = 0; it < IPT; it++) {
         const int p = warp * 32 * IPT + it * 32 + lane;
         const bool ok = p < nt;
         key[it] = ok ? kin[t0 + p] : 0u;
         val[it] = ok ? (vin ? vin[t0 + p] : (uint32_t)(t0 + p)) : 0u;  // no vin: values are the positions
-        if (PAYLOAD) pay[PAYLOAD ? it : 0] = ok ? pin[t0 + p] : make_uint2(0u, 0u);
     }
 #pragma unroll
     for (int it = 0; it < IPT; it++) {
@@ -148,7 +143,6 @@ __global__ __launch_bounds__(RS_T, MVGS_RS3_MINB) void k_rs_scatter(const uint32
         for (int w = 0; w < RS_NW; w++) tot += hist[w][threadIdx.x];
         uint32_t ws;
         const uint32_t start = block_excl_scan_256_u(tot, &ws);
-        dstart[threadIdx.x] = start;
         gdelta[threadIdx.x] = goff - start;
         uint32_t run = start;
 #pragma unroll
@@ -166,7 +160,6 @@ __global__ __launch_bounds__(RS_T, MVGS_RS3_MINB) void k_rs_scatter(const uint32
             const uint32_t l = hist[warp][(key[it] >> shift) & mask] + loc[it];
             sk[l] = key[it];
             sv[l] = val[it];
-            if (PAYLOAD) sp[PAYLOAD ? l : 0] = pay[PAYLOAD ? it : 0];
         }
     }
     __syncthreads();
@@ -202,15 +195,13 @@ __global__ __launch_bounds__(RS_T, MVGS_RS3_MINB) void k_rs_scatter(const uint32
         const uint32_t dst = gdelta[(k >> shift) & mask] + l;
         kout[dst] = k;
         vout[dst] = sv[l];
-        if (PAYLOAD) pout[dst] = sp[PAYLOAD ? l : 0];
     }
 }
 
-// Three-kernel variant (per-tile histogram, device-wide scan, scatter) — used for the
-// entries, whose many small tiles make onesweep look-back chains long.
-// Stable LSD sort of (k, v[, payload])[0..*n_ptr) on bits [0, bits) with ≤ 8-bit
-// digits.  Returns the number of passes; the result is in the first buffers when
-// even, in the second ones when odd.
+// Three-kernel passes (per-tile histogram, device-wide scan, scatter) for the entries, whose
+// many small tiles make onesweep look-back chains long.
+// Stable LSD sort of (k, v)[0..*n_ptr) on bits [0, bits) with ≤ 8-bit digits.  Returns the
+// number of passes; the result is in the first buffers when even, in the second ones when odd.
 // With range_min (entries: keys < 2^bits are bucket ids) the last pass also writes each
 // bucket's first position (atomicMin; the caller fills range_min with INT_MAX first and
 // closes empty buckets afterwards) and skips writing the sorted keys.
@@ -219,17 +210,15 @@ __global__ __launch_bounds__(RS_T, MVGS_RS3_MINB) void k_rs_scatter(const uint32
 #endif
 constexpr int RS3_IPT = MVGS_RS3_IPT;
 
-template <int IPT>
-static int radix_sort_3k_t(uint32_t* k, uint32_t* v, uint32_t* k2, uint32_t* v2, uint2* pl, uint2* pl2, const int* n_ptr,
-               int64_t cap, int bits, int* counts, int* scan_tmp, cudaStream_t s, cudaError_t* err,
-               int* range_min, bool first_counted) {
+int radix_sort_3k(uint32_t* k, uint32_t* v, uint32_t* k2, uint32_t* v2, const int* n_ptr, int64_t cap, int bits,
+                  int* counts, int* scan_tmp, cudaStream_t s, cudaError_t* err, int* range_min, bool first_counted) {
+    constexpr int IPT = RS3_IPT;
     const int ntiles = (int)((cap + RS_T * IPT - 1) / (RS_T * IPT));  // ≤ radix_tiles(cap): counts fit
     const int npass = (bits + 7) / 8;
     const int db = npass ? (bits + npass - 1) / npass : 0;
     *err = cudaSuccess;
     if (ntiles == 0) return 0;
     uint32_t *ks = k, *vs = v, *kd = k2, *vd = v2;
-    uint2 *ps = pl, *pd = pl2;
     for (int pass = 0; pass < npass; pass++) {
         const int shift = pass * db;
         const int nb = min(db, bits - shift);
@@ -238,32 +227,13 @@ static int radix_sort_3k_t(uint32_t* k, uint32_t* v, uint32_t* k2, uint32_t* v2,
         // only the live digits' counts (digit-major layout): a 7-bit pass scans half the table
         if ((*err = scan_exclusive(counts, (1 << nb) * ntiles, nullptr, scan_tmp, s)) != cudaSuccess) return pass;
         int* rm = (pass == npass - 1) ? range_min : nullptr;
-        bool launched = false;
-        if constexpr (IPT == 8) {  // payload tiles only at 8 keys per thread (static shared memory)
-            if (pl) {
-                k_rs_scatter<true, IPT><<<ntiles, RS_T, 0, s>>>(ks, vs, kd, vd, ps, pd, n_ptr, cap, shift, nb, counts,
-                                                               ntiles, rm, nullptr, nullptr);
-                launched = true;
-            }
-        }
-        if (!launched)
-            k_rs_scatter<false, IPT><<<ntiles, RS_T, 0, s>>>(ks, vs, kd, vd, nullptr, nullptr, n_ptr, cap, shift, nb,
-                                                        counts, ntiles, rm, nullptr, nullptr);
+        k_rs_scatter<IPT><<<ntiles, RS_T, 0, s>>>(ks, vs, kd, vd, nullptr, n_ptr, cap, shift, nb, counts, ntiles, rm,
+                                                 nullptr, nullptr);
         if ((*err = cudaGetLastError()) != cudaSuccess) return pass;
         uint32_t* t = ks; ks = kd; kd = t;
         t = vs; vs = vd; vd = t;
-        uint2* tp = ps; ps = pd; pd = tp;
     }
     return npass;
-}
-
-int radix_sort_3k(uint32_t* k, uint32_t* v, uint32_t* k2, uint32_t* v2, uint2* pl, uint2* pl2, const int* n_ptr,
-               int64_t cap, int bits, int* counts, int* scan_tmp, cudaStream_t s, cudaError_t* err,
-               int* range_min = nullptr, bool first_counted = false) {
-    // payload tiles stay at 8 keys per thread (static shared memory); key/value tiles take RS3_IPT
-    return pl ? radix_sort_3k_t<8>(k, v, k2, v2, pl, pl2, n_ptr, cap, bits, counts, scan_tmp, s, err, range_min, false)
-              : radix_sort_3k_t<RS3_IPT>(k, v, k2, v2, pl, pl2, n_ptr, cap, bits, counts, scan_tmp, s, err, range_min,
-                                         first_counted);
 }
 
 // digit width of the entry sort's passes (keys view·T + tile < V·T)
@@ -531,7 +501,7 @@ static int radix_sort_pairs_3k(const Launch& L, cudaStream_t s, cudaError_t* err
         if ((*err = scan_exclusive(L.rs_counts, (1 << nb) * ntiles, nullptr, L.scan_tmp, s)) != cudaSuccess) return pass;
         vd = vbuf[pass & 1];
         const bool last = pass == npass - 1;
-        k_rs_scatter<false, IPT><<<ntiles, RS_T, 0, s>>>(ks, vs, kd, vd, nullptr, last ? L.prect2 : nullptr, n_ptr, cap,
+        k_rs_scatter<IPT><<<ntiles, RS_T, 0, s>>>(ks, vs, kd, vd, last ? L.prect2 : nullptr, n_ptr, cap,
                                                         shift, nb, L.rs_counts, ntiles, nullptr,
                                                         last ? L.prect : nullptr, last ? L.ecount : nullptr);
         if ((*err = cudaGetLastError()) != cudaSuccess) return pass;
@@ -618,8 +588,8 @@ cudaError_t launch_sort_entries(const Launch& L, uint32_t** sorted_vals, cudaStr
     // bucket starts come out of the last pass (atomicMin): fill with INT_MAX first
     if ((e = cudaMemsetAsync(L.bucket_off, 0x7f, sizeof(int) * ((size_t)L.V * L.T + 1), s)) != cudaSuccess) return e;
     // the first pass's digit counts were written by k_dup
-    int np = radix_sort_3k(L.key, L.val, L.key2, L.val2, nullptr, nullptr, L.counters + C_K, L.cap_entries, bits,
-                           L.rs_counts, L.scan_tmp, s, &e, L.bucket_off, true);
+    int np = radix_sort_3k(L.key, L.val, L.key2, L.val2, L.counters + C_K, L.cap_entries, bits, L.rs_counts,
+                           L.scan_tmp, s, &e, L.bucket_off, true);
     *sorted_vals = (np & 1) ? L.val2 : L.val;
     if (e != cudaSuccess) return e;
     const int nseg = (L.V * L.T + RC_T - 1) / RC_T;

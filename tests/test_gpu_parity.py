@@ -199,6 +199,26 @@ def test_big_bucket_global_sort_path_and_depth_ties():
     assert gpu["stats"]["max_bucket"] > 2048
 
 
+def _depth_scene(z, rng):
+    n = len(z)
+    xy = rng.uniform(-0.5, 0.5, (n, 2)) * z[:, None]
+    ls = np.log(0.03 * z)[:, None].repeat(3, 1)
+    return _scene(np.column_stack([xy, z]), ls, rng.uniform(-2, 2, n), rgb=rng.uniform(0, 1, (n, 3)))
+
+
+def test_pair_sort_wide_depth_range():
+    """Visible depth keys spanning more than 2^27 float32 bit patterns (0.02 … 2000, five binary
+    exponents of depth): every pair-sort digit varies.  Lists, images and gradients against the
+    oracle."""
+    rng = np.random.default_rng(11)
+    z = rng.permutation(np.geomspace(0.02, 2000.0, 2500)).astype(np.float32)
+    assert int(z.max().view(np.uint32)) - int(z.min().view(np.uint32)) >= (1 << 27)
+    g = _depth_scene(z, rng)
+    cam = synth.cams_array([synth.make_camera(np.eye(3), [0, 0, 0], 40, 36, 30.0, znear=0.01)])
+    gpu, _ = _check_all(g, cam)
+    assert gpu["stats"]["n_visible"] > 1000
+
+
 def test_huge_gaussian_covers_every_tile_and_clamps():
     """One Gaussian covering the whole image (all tiles), opacity clamp at 0.99 (R11)
     in front of small ones; Jacobian clamp for an off-screen large one (R4)."""
