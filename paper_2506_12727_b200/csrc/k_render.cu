@@ -11,14 +11,13 @@
 // its pixels are done.
 //
 // Backward (adjoint of Eq. (1)): back to front from each pixel's
-// n_contrib, reconstructing T by division.  For each entry a thread adds its
-// two pixels' ten terms (Σ∇x, Σ∇y, ‖∇‖ for E1, ∂A, ∂B, ∂C, ∂o, ∂r, ∂g, ∂b;
-// ‖∇‖ is taken per pixel before adding — "norm and add"), the warp
-// transpose-reduces them (12 shuffles for 10 values; each lane ends up owning
-// one value's warp sum) into the warp's private slot for the entry (plain
-// stores — shared-memory float atomics would be CAS loops), and after the
-// batch the 4 warp slots are summed in fixed order and flushed to the pair's
-// gradient slot with one global red.add per nonzero value.
+// n_contrib, reconstructing T by division, one independent warp per (view,
+// tile, 8×8 block) staging its own batches (no CTA barrier).  For each entry a
+// lane adds its two pixels' ten terms (Σ∇x, Σ∇y, ‖∇‖ for E1, ∂A, ∂B, ∂C, ∂o,
+// ∂r, ∂g, ∂b; ‖∇‖ is taken per pixel before adding — "norm and add",
+// P:18–20), the warp transpose-reduces them (12 shuffles for 10 values; each
+// lane ends up owning one value's warp sum) and the ten owner lanes add them to
+// the pair's gradient slot with one global red.add warp instruction.
 #include <cudaTypedefs.h>
 #include "ca.cuh"
 #include "internal.cuh"
@@ -556,10 +555,10 @@ __device__ __forceinline__ int reduce_id(int lane) {
 }
 
 // ---------------------------------------------------------------------------------------
-// Backward (S7).  128 threads per (view, tile), two pixels per thread held as the lanes of
-// FP32x2 registers (rows r and r + WBH/2 of the thread's column in its warp's block), the
-// tile's list walked back to front from each pixel's n_contrib in staged batches, each warp
-// over its compacted list of entries that can touch its pixel block (§4.8).
+// Backward (S7).  One warp per (view, tile, 8×8 pixel block), two pixels per lane held as the
+// lanes of FP32x2 registers (rows r and r + WBH/2 of the lane's column in the block); the
+// tile's list walked back to front from the block's largest n_contrib over the entries that
+// can touch the block (§4.8).
 //
 // Decisions are the forward's, re-taken in the same canonical arithmetic: the CA power, the
 // CA exp (ca_exp_core2, bit-identical to the forward's), α = min(0.99, o·G), skip α < 1/255,
@@ -573,9 +572,10 @@ __device__ __forceinline__ int reduce_id(int lane) {
 // (the adjoint of Eq. (1): every later term and the background carry (1 − α_j)), and
 // after the entry B̃ −= (c_j·∂L/∂C)·α_j·T_j.  Per (pixel, entry) the ten per-pair terms are
 // Σ∇x, Σ∇y (∇_{p_i}L in NDC, R2), ‖∇_{p_i}L‖ (E1, "norm and add"), ∂A, ∂B, ∂C, o·∂L/∂o,
-// ∂r, ∂g, ∂b; the thread adds its two pixels', the warp transpose-reduces them (12 shuffles),
-// the owner lane scales and stores its value in the warp's slot, and after the batch the four
-// warp slots are summed in fixed order and flushed with one red.add per nonzero value.
+// ∂r, ∂g, ∂b; the lane adds its two pixels', the warp transpose-reduces them (12 shuffles, each
+// lane ends up owning one value's warp sum) and the ten owner lanes scale their sums and add
+// them to the pair's gradient slot (one red.add warp instruction per entry: ten lanes of one
+// 48-byte slot).
 __device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
 __device__ __forceinline__ float sqrt_approx(float x) {
     float y;
@@ -588,29 +588,70 @@ __device__ __forceinline__ float rcp_approx(float x) {
     return y;
 }
 
-// Staged per-entry constants of the backward: three float4 loads per (warp, entry); every
-// packed operation takes the entry's scalars as broadcast operands.
-//   e0 = (μ'x, μ'y, A, C), e1 = (B, o, skip bound, 1/o), e2 = (r, g, b, −)
+// ---------------------------------------------------------------------------------------
+// No warp of the backward ever waits for another.  Each warp stages its own batches of
+// WB_BATCH entries of the tile's list (two per lane: pair slot, record, and the culling test of
+// ITS pixel block only — cp.async brings batch b − 1's records while batch b is walked),
+// compacts the entries that may touch its block, walks them, and flushes each entry's sums at
+// once.  With one warp per CTA a finished warp frees its slot for the next.  Measured against
+// the round-2 CTA-per-tile kernel (four warps sharing each staged batch, three CTA barriers per
+// batch, per-warp slot arrays summed by a flush pass — barrier stalls 13 % of samples at garden,
+// 27 % at playroom): garden 0.691 vs 0.691 ms, playroom 2.91 vs 3.23 ms, train 0.93 vs 1.04 ms.
+// What it costs: each warp reads the records its list reaches (L2), and an entry walked by k
+// warps of a tile gets k red.adds instead of one.
+#ifndef MVGS_WB_BATCH
+#define MVGS_WB_BATCH 64
+#endif
+constexpr int WB_BATCH = MVGS_WB_BATCH;  // entries a warp stages at a time (two per lane)
+
+// warp_block_mask for one block: may a pixel of the WBW × WBH block at (x0, y0) pass the skip test?
+__device__ __noinline__ bool block_may_pass(float px, float py, float A, float B, float C, float sb, float x0,
+                                            float y0) {
+#ifdef MVGS_NO_CULL
+    return true;
+#endif
+    const float L = -2.0f * sb;
+    if (!(A > 0.0f) || !(C > 0.0f) || !((double)A * (double)C - (double)B * (double)B > 0.0) || !(L > 0.0f))
+        return true;
+    const float eps3 = 3.0f * 8.0f * 5.9604644775390625e-8f;
+    const float Lm = L * 1.01f + 0.01f;
+    const float dxlo = px - (x0 + (float)(WBW - 1)), dxhi = px - x0;
+    const float dylo = py - (y0 + (float)(WBH - 1)), dyhi = py - y0;
+    const float dxm = fmaxf(fabsf(dxlo), fabsf(dxhi));
+    const float dym = fmaxf(fabsf(dylo), fabsf(dyhi));
+    float qmin = 0.0f;
+    if (!(dxlo <= 0.0f && dxhi >= 0.0f && dylo <= 0.0f && dyhi >= 0.0f)) {
+        qmin = fminf(fminf(q_edge(A, B, C, dxlo, dylo, dyhi, true), q_edge(A, B, C, dxhi, dylo, dyhi, true)),
+                     fminf(q_edge(A, B, C, dylo, dxlo, dxhi, false), q_edge(A, B, C, dyhi, dxlo, dxhi, false)));
+    }
+    const float tmax = A * dxm * dxm + C * dym * dym + 2.0f * fabsf(B) * dxm * dym;
+    return !(qmin > Lm + eps3 * tmax);
+}
+
+#ifndef MVGS_BWD_WPC
+#define MVGS_BWD_WPC 1  // warps per CTA of the warp-independent backward (1: a finished warp frees its slot)
+#endif
+constexpr int BW_WPC = MVGS_BWD_WPC;
 template <bool CNT>
-__global__ __launch_bounds__(128, MVGS_BWD_MINB) void k_render_bwd_p(Launch L, const float* __restrict__ dL_drgb,
-                                                      const float* __restrict__ in_T,
-                                                      const int32_t* __restrict__ in_n) {
-    constexpr int NW = 4, RB = 128;
-    __shared__ float4 se[4][RB];  // one array: an entry's loads share its address (immediate offsets)
-    __shared__ uint32_t sq[RB];
-    __shared__ __align__(16) float sacc[NW][RB * NG];
-    __shared__ float skscale[NG];
-    __shared__ int smax;
+__global__ __launch_bounds__(32 * BW_WPC, MVGS_BWD_MINB * 4 / BW_WPC) void k_render_bwd_w(
+    Launch L, const float* __restrict__ dL_drgb, const float* __restrict__ in_T, const int32_t* __restrict__ in_n) {
+    constexpr int NW = BW_WPC, MB = WB_BATCH, SPL = MB / 32;
+    static_assert(MB % 32 == 0 && MB <= 256, "batch: lanes × SPL, byte list indices");
+    __shared__ float4 se[NW][4][MB];  // per warp: (μ'x, μ'y, A, C) (B, o, sb, 1/o) (r, g, b, −) (W/2·A, W/2·B, H/2·C, H/2·B)
+    __shared__ __align__(16) float4 sraw[NW][MB][3];  // per warp: the next batch's records, by cp.async
+    __shared__ uint32_t sq[2][NW][MB];  // pair slots of the staged batch (two batches in flight)
+    __shared__ uint8_t slist[NW][MB];
     __shared__ unsigned sev[2];
-    __shared__ uint8_t smask[RB];
-    __shared__ uint8_t slist[NW][RB];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int bucket = L.order ? L.order[blockIdx.x] : blockIdx.x;  // longest list first
+    const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;  // wl: warp within the CTA
+    const int gw = blockIdx.x * NW + wl;                       // the tile's four warps are consecutive
+    const int warp = gw & 3;                                   // pixel block of the tile
+    const int bucket = L.order ? L.order[gw >> 2] : (gw >> 2);
     const int v = bucket / L.T, tile = bucket - v * L.T;
     const int ty = tile / L.TX, tx = tile - ty * L.TX;
-    int x, y0, y1_;
-    pixel_pair(tx, ty, x, y0, y1_);
+    const int x = tx * TILE + wb_x0(warp) + (lane % WBW);
+    const int y0 = ty * TILE + wb_y0(warp) + (lane / WBW), y1_ = y0 + WBH / 2;
     const int start = L.bucket_off[bucket], end = L.bucket_off[bucket + 1];
+    if (CNT && threadIdx.x == 0) sev[0] = sev[1] = 0;
     if (end > L.cap_entries) return;
     const int64_t HW = (int64_t)L.H * L.W;
     float dL[2][3], Tfin[2];
@@ -634,72 +675,92 @@ __global__ __launch_bounds__(128, MVGS_BWD_MINB) void k_render_bwd_p(Launch L, c
     float2 T = f2(Tfin[0], Tfin[1]);
     float2 nB = f2(-Tfin[0] * (L.bg[0] * dL[0][0] + L.bg[1] * dL[0][1] + L.bg[2] * dL[0][2]),
                    -Tfin[1] * (L.bg[0] * dL[1][0] + L.bg[1] * dL[1][1] + L.bg[2] * dL[1][2]));
-    const int mylast = max(last[0], last[1]);
     const float hw = 0.5f * (float)L.W, hh = 0.5f * (float)L.H;
-    if (threadIdx.x == 0) {
-        smax = 0;
-        sev[0] = sev[1] = 0;
-    }
-    // per-value scale applied at the flush: Σ∇ = −Σ (W/2·(A d + B e), H/2·(C e + B d)) (the
-    // W/2, H/2 are folded into the staged conic) with d, e = ∂L/∂power·(dx, dy);
-    // ∂A = −½Σ d·dx, ∂B = −Σ d·dy, ∂C = −½Σ e·dy; the colour terms
-    // were accumulated with −w; slot 6 (o·∂L/∂o) is scaled by the entry's 1/o
-    if (threadIdx.x < NG) {
-        const int k = threadIdx.x;
-        skscale[k] = (k == 0 || k == 1) ? -1.f : (k == 3 || k == 5) ? -0.5f : (k == 4 || k >= 7) ? -1.f : 1.f;
-    }
-    __syncthreads();
     unsigned nev = 0, nexp = 0, nbl0 = 0, nbl1 = 0;
-    if (mylast > 0) atomicMax(&smax, mylast);
-    __syncthreads();
-    const int maxlast = smax;
-    const int wmax = __reduce_max_sync(FULLR, mylast);
+    const int wmax = __reduce_max_sync(FULLR, max(last[0], last[1]));
     const int my_id = reduce_id(lane);
     const bool owner = (__ffs(__match_any_sync(FULLR, my_id)) - 1) == lane;
     const RedSel rsel = red_sel(lane);
-    // this lane's value of entry jj goes to sacc[warp][jj·NG + my_id]; non-owners (the same sum
-    // held by several lanes) write to a dummy word, so the store needs no predicate
-    __shared__ float sdummy[NW * 32];
-    float* wslot = owner ? &sacc[warp][my_id] : &sdummy[threadIdx.x];
-    const int wstride = owner ? NG : 0;
+    // the owner lane's scale of its value: Σ∇ = −Σ (W/2·(A d + B e), H/2·(C e + B d)) (W/2, H/2 folded
+    // into the staged conic) with d, e = ∂L/∂power·(dx, dy); ∂A = −½Σ d·dx, ∂B = −Σ d·dy, ∂C = −½Σ e·dy;
+    // the colour terms were accumulated with −w; value 6 (o·∂L/∂o) takes the entry's 1/o
+    const float myscale = (my_id == 0 || my_id == 1) ? -1.f
+                          : (my_id == 3 || my_id == 5) ? -0.5f
+                          : (my_id == 4 || my_id >= 7) ? -1.f
+                                                       : 1.f;
+    float* const pg = L.pgrad + my_id;
     const float2 nfx = f2(-(float)x, -(float)x), nfy = f2(-(float)y0, -(float)y1_);
     const float2 mhalf = f2(-0.5f, -0.5f);
-    for (int b_end = maxlast; b_end > 0; b_end -= RB) {
-        const int b0 = max(0, b_end - RB);
-        const int cnt = b_end - b0;
-        __syncthreads();
-        if ((int)threadIdx.x < cnt) {
-            const int t = threadIdx.x;
-            const uint32_t q = L.sorted[start + b0 + t];
-            sq[t] = q;
-            const float4* r = L.rec + 3 * (int64_t)q;
-            const float4 r0 = r[0], r1 = r[1], r2 = r[2];  // (x, y, A, B) (C, o, r, g) (b, depth, sb, 1/o)
-            se[0][t] = make_float4(r0.x, r0.y, r0.z, r1.x);
-            se[1][t] = make_float4(r0.w, r1.y, r2.z, r2.w);
-            se[2][t] = make_float4(r1.z, r1.w, r2.x, 0.f);
-            // the conic scaled by the NDC factors: (W/2)·(A, B) and (H/2)·(C, B) give ∇_{p_i}L's
-            // components directly, so the per-pixel norm for E1 needs no further scaling
-            se[3][t] = make_float4(hw * r0.z, hw * r0.w, hh * r1.x, hh * r0.w);
-            smask[t] = (uint8_t)warp_block_mask(r0.x, r0.y, r0.z, r0.w, r1.x, r2.z, (float)(tx * TILE), (float)(ty * TILE));
+    const float bx0 = (float)(tx * TILE + wb_x0(warp)), by0 = (float)(ty * TILE + wb_y0(warp));
+    float4(*S)[MB] = se[wl];
+    // Batches are walked back to front.  The records of batch bi − 1 travel global → shared by
+    // cp.async (each lane copies the rows it will later transform, so only its own copies are
+    // waited for) while batch bi is walked; the pair slots of batch bi − 2 are loaded meanwhile.
+    const int nbat = (wmax + MB - 1) / MB;
+    uint32_t qn[SPL];
+    auto load_slots = [&](int bi) {
+#pragma unroll
+        for (int k = 0; k < SPL; k++) {
+            const int t = lane + 32 * k;
+            qn[k] = (bi >= 0 && bi * MB + t < wmax) ? L.sorted[start + bi * MB + t] : 0u;
         }
-        {
-            float4* w4 = reinterpret_cast<float4*>(sacc[warp]);
-            for (int i = lane; i < RB * NG / 4; i += 32) w4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    };
+    auto issue = [&](int bi) {  // batch bi's records → sraw, its slots → sq[bi & 1]
+#pragma unroll
+        for (int k = 0; k < SPL; k++) {
+            const int t = lane + 32 * k;
+            if (bi * MB + t < wmax) {
+                sq[bi & 1][wl][t] = qn[k];
+                const float* src = reinterpret_cast<const float*>(L.rec + 3 * (int64_t)qn[k]);
+                cp_async16(&sraw[wl][t][0].x, src);
+                cp_async16(&sraw[wl][t][1].x, src + 4);
+                cp_async16(&sraw[wl][t][2].x, src + 8);
+            }
         }
-        __syncthreads();
-        // this warp's entries of the batch (culled by its pixel block), walked back to front
-        const int nl = warp_batch_list(smask, min(cnt, wmax - b0), warp, lane, slist[warp]);
-        // Per entry: the front (offset, CA power, skip decision) and the back (CA exp, α, the state
-        // update T ← T/(1 − α), B̃ ← B̃ + (c·∂L/∂C)·(−α·T), the ten terms, the warp reduction).
-        // With MVGS_BWD_PAIR two entries are taken per step: both fronts and exps, then the two
-        // state updates in list order, then both term sets and reductions — independent chains
-        // the scheduler can interleave.  A lane that does not blend an entry gets α = 0: its
-        // state and terms are unchanged / zero, exactly as in the single-entry walk.
+        cp_async_commit();
+    };
+    if (nbat > 0) {
+        load_slots(nbat - 1);
+        issue(nbat - 1);
+        load_slots(nbat - 2);
+    }
+    for (int bi = nbat - 1; bi >= 0; bi--) {
+        const int b0 = bi * MB;
+        const int cnt = min(MB, wmax - b0);
+        const uint32_t* sqb = sq[bi & 1][wl];
+        cp_async_wait_all();
+        __syncwarp();  // the previous batch's staged entries are no longer read
+        unsigned inb[SPL];
+#pragma unroll
+        for (int k = 0; k < SPL; k++) {
+            const int t = lane + 32 * k;
+            bool in = false;
+            if (t < cnt) {
+                const float4 r0 = sraw[wl][t][0], r1 = sraw[wl][t][1], r2 = sraw[wl][t][2];
+                // (x, y, A, B) (C, o, r, g) (b, depth, sb, 1/o)
+                S[0][t] = make_float4(r0.x, r0.y, r0.z, r1.x);
+                S[1][t] = make_float4(r0.w, r1.y, r2.z, r2.w);
+                S[2][t] = make_float4(r1.z, r1.w, r2.x, 0.f);
+                S[3][t] = make_float4(hw * r0.z, hw * r0.w, hh * r1.x, hh * r0.w);
+                in = block_may_pass(r0.x, r0.y, r0.z, r0.w, r1.x, r2.z, bx0, by0);
+            }
+            inb[k] = __ballot_sync(FULLR, in);
+        }
+        if (bi > 0) {  // the next batch in flight during this batch's walk
+            issue(bi - 1);
+            load_slots(bi - 2);
+        }
+        int nl = 0;
+#pragma unroll
+        for (int k = 0; k < SPL; k++) {
+            if ((inb[k] >> lane) & 1u) slist[wl][nl + __popc(inb[k] & ((1u << lane) - 1u))] = (uint8_t)(lane + 32 * k);
+            nl += __popc(inb[k]);
+        }
+        __syncwarp();
         auto front = [&](int jj, int j, float2& dx, float2& dy, float2& power, bool& in0, bool& in1) {
-            const float4 e0 = se[0][jj], e1 = se[1][jj];
+            const float4 e0 = S[0][jj], e1 = S[1][jj];
             dx = __fadd2_rn(f2(e0.x, e0.x), nfx);
             dy = __fadd2_rn(f2(e0.y, e0.y), nfy);
-            // ca_power per lane: FMA(−0.5, FMA(A·dx, dx, (C·dy)·dy), −(B·dx)·dy)
             const float2 A2 = f2(e0.z, e0.z), C2 = f2(e0.w, e0.w), B2 = f2(e1.x, e1.x);
             const float2 inner = __ffma2_rn(__fmul2_rn(A2, dx), dx, __fmul2_rn(__fmul2_rn(C2, dy), dy));
             const float2 Bdd = __fmul2_rn(__fmul2_rn(B2, dx), dy);
@@ -708,12 +769,10 @@ __global__ __launch_bounds__(128, MVGS_BWD_MINB) void k_render_bwd_p(Launch L, c
             in0 = j < last[0] && !(power.x > 0.f) && !(power.x < sb);
             in1 = j < last[1] && !(power.y > 0.f) && !(power.y < sb);
         };
-        // α of a pixel pair (0 where it does not blend) and o·G where it has a gradient (R11)
         auto alphas = [&](int jj, float2 power, bool in0, bool in1, float2& alpha, float2& oGc) {
-            const float o = se[1][jj].y;
+            const float o = S[1][jj].y;
             const float2 G = ca_exp_core2(power);
             const float2 oG = __fmul2_rn(f2(o, o), G);
-            // α = min(0.99, o·G) < 1/255 ⇔ o·G < 1/255
             const bool bl0 = in0 && !(oG.x < ALPHA_MIN);
             const bool bl1 = in1 && !(oG.y < ALPHA_MIN);
             if (CNT) {
@@ -723,13 +782,12 @@ __global__ __launch_bounds__(128, MVGS_BWD_MINB) void k_render_bwd_p(Launch L, c
             alpha = f2(bl0 ? fminf(ALPHA_MAX, oG.x) : 0.f, bl1 ? fminf(ALPHA_MAX, oG.y) : 0.f);
             oGc = f2(oG.x > ALPHA_MAX ? 0.f : alpha.x, oG.y > ALPHA_MAX ? 0.f : alpha.y);
         };
-        // the state update of one entry; returns −α·T and ∂L/∂power (= o·G·∂L/∂α)
         auto state = [&](int jj, float2 alpha, float2 oGc, float2& nw, float2& dLdpw) {
             const float2 om = __ffma2_rn(alpha, f2(-1.f, -1.f), f2(1.f, 1.f));
             const float2 inv = f2(rcp_approx(om.x), rcp_approx(om.y));
             T = __fmul2_rn(T, inv);
-            nw = __fmul2_rn(alpha, f2(-T.x, -T.y));  // −α·T
-            const float4 e2 = se[2][jj];
+            nw = __fmul2_rn(alpha, f2(-T.x, -T.y));
+            const float4 e2 = S[2][jj];
             const float2 cdL = __ffma2_rn(f2(e2.z, e2.z), dLb,
                                           __ffma2_rn(f2(e2.y, e2.y), dLg, __fmul2_rn(f2(e2.x, e2.x), dLr)));
             const float2 dLda = __ffma2_rn(nB, inv, __fmul2_rn(T, cdL));
@@ -737,9 +795,8 @@ __global__ __launch_bounds__(128, MVGS_BWD_MINB) void k_render_bwd_p(Launch L, c
             dLdpw = __fmul2_rn(oGc, dLda);
         };
         auto terms = [&](int jj, float2 dx, float2 dy, float2 nw, float2 dLdpw, float (&val)[NG]) {
-            const float4 s3 = se[3][jj];  // (W/2·A, W/2·B, H/2·C, H/2·B)
+            const float4 s3 = S[3][jj];
             const float2 d = __fmul2_rn(dLdpw, dx), e = __fmul2_rn(dLdpw, dy);
-            // −∇_{p_i}L per pixel (NDC): x = W/2·(A d + B e), y = H/2·(C e + B d)
             const float2 gxr = __ffma2_rn(f2(s3.x, s3.x), d, __fmul2_rn(f2(s3.y, s3.y), e));
             const float2 gyr = __ffma2_rn(f2(s3.z, s3.z), e, __fmul2_rn(f2(s3.w, s3.w), d));
             const float2 n2 = __ffma2_rn(gxr, gxr, __fmul2_rn(gyr, gyr));
@@ -747,7 +804,7 @@ __global__ __launch_bounds__(128, MVGS_BWD_MINB) void k_render_bwd_p(Launch L, c
             const float2 wr = __fmul2_rn(nw, dLr), wg = __fmul2_rn(nw, dLg), wb = __fmul2_rn(nw, dLb);
             val[0] = gxr.x + gxr.y;
             val[1] = gyr.x + gyr.y;
-            val[2] = sqrt_approx(n2.x) + sqrt_approx(n2.y);  // ‖∇_{p_i}L‖ per pixel, then add
+            val[2] = sqrt_approx(n2.x) + sqrt_approx(n2.y);
             val[3] = dd.x + dd.y;
             val[4] = de.x + de.y;
             val[5] = ee.x + ee.y;
@@ -756,10 +813,14 @@ __global__ __launch_bounds__(128, MVGS_BWD_MINB) void k_render_bwd_p(Launch L, c
             val[8] = wg.x + wg.y;
             val[9] = wb.x + wb.y;
         };
+        // the owner lanes add the entry's warp sums to its gradient slot
+        auto flush = [&](int jj, float s) {
+            if (owner) atomicAdd(pg + (int64_t)sqb[jj] * PG_STRIDE, s * (my_id == 6 ? S[1][jj].w : myscale));
+        };
         int u = nl - 1;
 #if MVGS_BWD_PAIR
         for (; u >= 1; u -= 2) {
-            const int ja = slist[warp][u], jb = slist[warp][u - 1];  // a is behind b: a first
+            const int ja = slist[wl][u], jb = slist[wl][u - 1];  // a is behind b: a first
             if (CNT) nev += (unsigned)(b0 + ja < last[0]) + (unsigned)(b0 + ja < last[1]) +
                             (unsigned)(b0 + jb < last[0]) + (unsigned)(b0 + jb < last[1]);
             float2 dxa, dya, pwa, dxb, dyb, pwb;
@@ -782,12 +843,12 @@ __global__ __launch_bounds__(128, MVGS_BWD_MINB) void k_render_bwd_p(Launch L, c
             terms(jb, dxb, dyb, nwb, dpb, vb);
             const float sa = warp_transpose_reduce10(va, rsel);
             const float sbv = warp_transpose_reduce10(vb, rsel);
-            wslot[ja * wstride] = sa;
-            wslot[jb * wstride] = sbv;
+            flush(ja, sa);
+            flush(jb, sbv);
         }
 #endif
         for (; u >= 0; u--) {
-            const int jj = slist[warp][u];
+            const int jj = slist[wl][u];
             const int j = b0 + jj;
             if (CNT) nev += (unsigned)(j < last[0]) + (unsigned)(j < last[1]);
             float2 dx, dy, power;
@@ -802,21 +863,11 @@ __global__ __launch_bounds__(128, MVGS_BWD_MINB) void k_render_bwd_p(Launch L, c
             state(jj, alpha, oGc, nw, dLdpw);
             float val[NG];
             terms(jj, dx, dy, nw, dLdpw, val);
-            wslot[jj * wstride] = warp_transpose_reduce10(val, rsel);
-        }
-        __syncthreads();
-        for (int i = threadIdx.x; i < cnt * NG; i += 128) {
-            float s = 0.f;
-#pragma unroll
-            for (int w = 0; w < NW; w++) s += sacc[w][i];
-            if (s != 0.f) {
-                const int jj = i / NG, k = i - jj * NG;
-                s *= k == 6 ? se[1][jj].w : skscale[k];
-                atomicAdd(&L.pgrad[(int64_t)sq[jj] * PG_STRIDE + k], s);
-            }
+            flush(jj, warp_transpose_reduce10(val, rsel));
         }
     }
     if (CNT) {
+        __syncthreads();
         count_evals(&L.counters64[1], &L.counters64[3], nev, nexp, sev);
         if (L.dbg_nblend) {  // parity export: entries blended per pixel, as this kernel decided
             const int yy[2] = {y0, y1_};
@@ -829,10 +880,11 @@ __global__ __launch_bounds__(128, MVGS_BWD_MINB) void k_render_bwd_p(Launch L, c
 }
 
 cudaError_t launch_render_bwd(const Launch& L, const float* dL, const float* Tf, const int32_t* nc, cudaStream_t s) {
+    const int nb = L.V * L.T * (4 / BW_WPC);
     if (L.count_evals || L.dbg_nblend)
-        k_render_bwd_p<true><<<L.V * L.T, 128, 0, s>>>(L, dL, Tf, nc);
+        k_render_bwd_w<true><<<nb, 32 * BW_WPC, 0, s>>>(L, dL, Tf, nc);
     else
-        k_render_bwd_p<false><<<L.V * L.T, 128, 0, s>>>(L, dL, Tf, nc);
+        k_render_bwd_w<false><<<nb, 32 * BW_WPC, 0, s>>>(L, dL, Tf, nc);
     return cudaGetLastError();
 }
 
