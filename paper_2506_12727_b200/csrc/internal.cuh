@@ -61,14 +61,15 @@ struct Launch {  // everything a kernel needs about the current batch
 // a self-contained 48-byte record: the per-Gaussian kernel needs no second load, and an owner
 // rank can receive slots from other ranks and run the chain on them.
 __device__ __forceinline__ void zero_pgrad_slice(const Launch& L) {
-    const int64_t Q = min((int64_t)L.counters[C_Q], L.cap_pairs);
+    static_assert(PG_STRIDE == 12 && PG_FLAGS == 10, "slot = 3 float4, flags in the third one's z");
+    const int Q = (int)min((int64_t)L.counters[C_Q], L.cap_pairs);
     float4* p4 = reinterpret_cast<float4*>(L.pgrad);
-    const int64_t n4 = Q * (PG_STRIDE / 4);
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride) {
-        const int64_t q = i / (PG_STRIDE / 4);
-        const bool last = i - q * (PG_STRIDE / 4) == PG_STRIDE / 4 - 1;
-        p4[i] = make_float4(0.f, 0.f, last ? __uint_as_float(L.pflag[q]) : 0.f, 0.f);
+    const int stride = gridDim.x * blockDim.x;
+    for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < Q; q += stride) {  // one pair slot per step
+        const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+        p4[3 * (int64_t)q] = z;
+        p4[3 * (int64_t)q + 1] = z;
+        p4[3 * (int64_t)q + 2] = make_float4(0.f, 0.f, __uint_as_float(L.pflag[q]), 0.f);
     }
 }
 #endif
