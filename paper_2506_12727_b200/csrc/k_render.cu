@@ -100,12 +100,15 @@ __device__ __forceinline__ void pixel_pair(int tx, int ty, int& x, int& y0, int&
 //   q_min > 1.01·L + 0.01 + 3ε·T_max,   L = −2·sb,  T_max ≥ T over the block.
 // Conics that are not positive definite are never culled.  Bit j: the entry may touch
 // warp j's block of the tile.
-__device__ __forceinline__ float q_edge(float A, float B, float C, float fixed, float lo, float hi, bool fix_x) {
+// nBoC = −B/C, nBoA = −B/A (once per entry: the 1-D minimisers are −B·fixed/C and −B·fixed/A; a
+// rounded minimiser only raises q by C·δ², far inside the slack)
+__device__ __forceinline__ float q_edge(float A, float B, float C, float nBoA, float nBoC, float fixed, float lo,
+                                        float hi, bool fix_x) {
     if (fix_x) {  // dx fixed, dy clamped to [lo, hi] at the 1-D minimiser
-        const float t = fminf(hi, fmaxf(lo, -B * fixed / C));
+        const float t = fminf(hi, fmaxf(lo, nBoC * fixed));
         return A * fixed * fixed + 2.0f * B * fixed * t + C * t * t;
     }
-    const float t = fminf(hi, fmaxf(lo, -B * fixed / A));
+    const float t = fminf(hi, fmaxf(lo, nBoA * fixed));
     return A * t * t + 2.0f * B * t * fixed + C * fixed * fixed;
 }
 
@@ -119,6 +122,7 @@ __device__ __noinline__ unsigned warp_block_mask(float px, float py, float A, fl
         return 0xfu;
     const float eps3 = 3.0f * 8.0f * 5.9604644775390625e-8f;
     const float Lm = L * 1.01f + 0.01f;
+    const float nBoA = -B / A, nBoC = -B / C;
     unsigned m = 0;
 #pragma unroll
     for (int w = 0; w < 4; w++) {
@@ -129,8 +133,10 @@ __device__ __noinline__ unsigned warp_block_mask(float px, float py, float A, fl
         const float dym = fmaxf(fabsf(dylo), fabsf(dyhi));
         float qmin = 0.0f;
         if (!(dxlo <= 0.0f && dxhi >= 0.0f && dylo <= 0.0f && dyhi >= 0.0f)) {  // centre outside the block
-            qmin = fminf(fminf(q_edge(A, B, C, dxlo, dylo, dyhi, true), q_edge(A, B, C, dxhi, dylo, dyhi, true)),
-                         fminf(q_edge(A, B, C, dylo, dxlo, dxhi, false), q_edge(A, B, C, dyhi, dxlo, dxhi, false)));
+            qmin = fminf(fminf(q_edge(A, B, C, nBoA, nBoC, dxlo, dylo, dyhi, true),
+                               q_edge(A, B, C, nBoA, nBoC, dxhi, dylo, dyhi, true)),
+                         fminf(q_edge(A, B, C, nBoA, nBoC, dylo, dxlo, dxhi, false),
+                               q_edge(A, B, C, nBoA, nBoC, dyhi, dxlo, dxhi, false)));
         }
         const float tmax = A * dxm * dxm + C * dym * dym + 2.0f * fabsf(B) * dxm * dym;
         if (!(qmin > Lm + eps3 * tmax)) m |= 1u << w;
@@ -621,8 +627,11 @@ __device__ __noinline__ bool block_may_pass(float px, float py, float A, float B
     const float dym = fmaxf(fabsf(dylo), fabsf(dyhi));
     float qmin = 0.0f;
     if (!(dxlo <= 0.0f && dxhi >= 0.0f && dylo <= 0.0f && dyhi >= 0.0f)) {
-        qmin = fminf(fminf(q_edge(A, B, C, dxlo, dylo, dyhi, true), q_edge(A, B, C, dxhi, dylo, dyhi, true)),
-                     fminf(q_edge(A, B, C, dylo, dxlo, dxhi, false), q_edge(A, B, C, dyhi, dxlo, dxhi, false)));
+        const float nBoA = -B / A, nBoC = -B / C;
+        qmin = fminf(fminf(q_edge(A, B, C, nBoA, nBoC, dxlo, dylo, dyhi, true),
+                           q_edge(A, B, C, nBoA, nBoC, dxhi, dylo, dyhi, true)),
+                     fminf(q_edge(A, B, C, nBoA, nBoC, dylo, dxlo, dxhi, false),
+                           q_edge(A, B, C, nBoA, nBoC, dyhi, dxlo, dxhi, false)));
     }
     const float tmax = A * dxm * dxm + C * dym * dym + 2.0f * fabsf(B) * dxm * dym;
     return !(qmin > Lm + eps3 * tmax);
