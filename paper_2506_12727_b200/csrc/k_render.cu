@@ -778,7 +778,7 @@ __global__ __launch_bounds__(32 * BW_WPC, MVGS_BWD_MINB * 4 / BW_WPC) void k_ren
             in0 = j < last[0] && !(power.x > 0.f) && !(power.x < sb);
             in1 = j < last[1] && !(power.y > 0.f) && !(power.y < sb);
         };
-        auto alphas = [&](int jj, float2 power, bool in0, bool in1, float2& alpha, float2& oGc) {
+        auto alphas = [&](int jj, float2 power, bool in0, bool in1, float2& alpha, float2& oGc) -> bool {
             const float o = S[1][jj].y;
             const float2 G = ca_exp_core2(power);
             const float2 oG = __fmul2_rn(f2(o, o), G);
@@ -790,6 +790,7 @@ __global__ __launch_bounds__(32 * BW_WPC, MVGS_BWD_MINB * 4 / BW_WPC) void k_ren
             }
             alpha = f2(bl0 ? fminf(ALPHA_MAX, oG.x) : 0.f, bl1 ? fminf(ALPHA_MAX, oG.y) : 0.f);
             oGc = f2(oG.x > ALPHA_MAX ? 0.f : alpha.x, oG.y > ALPHA_MAX ? 0.f : alpha.y);
+            return bl0 || bl1;  // the lane blends the entry at one of its pixels
         };
         auto state = [&](int jj, float2 alpha, float2 oGc, float2& nw, float2& dLdpw) {
             const float2 om = __ffma2_rn(alpha, f2(-1.f, -1.f), f2(1.f, 1.f));
@@ -839,11 +840,9 @@ __global__ __launch_bounds__(32 * BW_WPC, MVGS_BWD_MINB * 4 / BW_WPC) void k_ren
             if (!__any_sync(FULLR, ia0 || ia1 || ib0 || ib1)) continue;
             if (CNT) nexp += (unsigned)ia0 + (unsigned)ia1 + (unsigned)ib0 + (unsigned)ib1;
             float2 ala, oga, alb, ogb;
-            alphas(ja, pwa, ia0, ia1, ala, oga);
-            alphas(jb, pwb, ib0, ib1, alb, ogb);
-            const bool anya = __any_sync(FULLR, ala.x > 0.f || ala.y > 0.f);
-            const bool anyb = __any_sync(FULLR, alb.x > 0.f || alb.y > 0.f);
-            if (!(anya || anyb)) continue;
+            const bool bla = alphas(ja, pwa, ia0, ia1, ala, oga);
+            const bool blb = alphas(jb, pwb, ib0, ib1, alb, ogb);
+            if (!__any_sync(FULLR, bla || blb)) continue;
             float2 nwa, dpa, nwb, dpb;
             state(ja, ala, oga, nwa, dpa);
             state(jb, alb, ogb, nwb, dpb);
@@ -866,8 +865,7 @@ __global__ __launch_bounds__(32 * BW_WPC, MVGS_BWD_MINB * 4 / BW_WPC) void k_ren
             if (!__any_sync(FULLR, in0 || in1)) continue;
             if (CNT) nexp += (unsigned)in0 + (unsigned)in1;
             float2 alpha, oGc;
-            alphas(jj, power, in0, in1, alpha, oGc);
-            if (!__any_sync(FULLR, alpha.x > 0.f || alpha.y > 0.f)) continue;
+            if (!__any_sync(FULLR, alphas(jj, power, in0, in1, alpha, oGc))) continue;
             float2 nw, dLdpw;
             state(jj, alpha, oGc, nw, dLdpw);
             float val[NG];
