@@ -327,7 +327,8 @@ def run_mvgs(args):
     #   (e2e.host_resident_params: the same with the whole parameter set uploaded and the whole
     #   gradient + ADC buffer downloaded every step — a model kept in host memory.)
     rng_t = np.random.default_rng(cfg.seed + 7)
-    host_tgt = torch.from_numpy(rng_t.random((Vr, 3, cfg.H, cfg.W), dtype=np.float32)).pin_memory()
+    # 8-bit target images, as photographs are stored (mvgs_loss_grad_u8 reads t/255): 1 B per value
+    host_tgt = torch.from_numpy(rng_t.integers(0, 256, (Vr, 3, cfg.H, cfg.W), dtype=np.uint8)).pin_memory()
     tgt_slots = [torch.empty_like(host_tgt, device=dev) for _ in range(2)]
     dL_e2e = torch.empty_like(dL)
     loss_dev = [torch.zeros(1, dtype=torch.float64, device=dev) for _ in range(2)]
@@ -336,8 +337,28 @@ def run_mvgs(args):
     s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
     mk = lambda: [torch.cuda.Event() for _ in range(2)]  # noqa: E731
     in_ready, in_free, out_ready, out_free = mk(), mk(), mk(), mk()
-    h2d = host_tgt.numel() * 4
+    h2d = host_tgt.numel() * host_tgt.element_size()
     d2h = 8
+
+    def e2e_compute(b):  # the device part of one training iteration (slot b's target and loss)
+        mvgs.preprocess(R.ctx, g, R.cams)
+        mvgs.render_fwd(R.ctx, *outs)
+        mvgs.loss_grad(R.ctx, outs[0], tgt_slots[b], dL_e2e, mode=mvgs.LOSS_L1, loss=loss_dev[b])
+        dL_cur[0] = dL_e2e
+        grads_out(buf)
+
+    # One GPU: each slot's compute is one CUDA graph (as the device-only step), replayed on the
+    # compute stream between the event waits of the copy streams.
+    e2e_graphs = [None, None]
+    if graph is not None:
+        for b in range(2):
+            e2e_compute(b)  # warm (outside capture)
+            torch.cuda.synchronize()
+            e2e_graphs[b] = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(e2e_graphs[b]):
+                e2e_compute(b)
+            torch.cuda.synchronize()
+        dL_cur[0] = dL
 
     def e2e_step(i):
         b = i % 2
@@ -349,11 +370,10 @@ def run_mvgs(args):
         comp.wait_event(in_ready[b])
         if i >= 2:
             comp.wait_event(out_free[b])
-        mvgs.preprocess(R.ctx, g, R.cams)
-        mvgs.render_fwd(R.ctx, *outs)
-        mvgs.loss_grad(R.ctx, outs[0], tgt_slots[b], dL_e2e, mode=mvgs.LOSS_L1, loss=loss_dev[b])
-        dL_cur[0] = dL_e2e
-        grads_out(buf)
+        if e2e_graphs[b] is not None:
+            e2e_graphs[b].replay()
+        else:
+            e2e_compute(b)
         in_free[b].record(comp)
         out_ready[b].record(comp)
         s_out.wait_event(out_ready[b])
@@ -475,8 +495,10 @@ def run_mvgs(args):
         "clocks": clocks,
         "e2e": {"value": round(views_total / (e2e_ms / 1e3), 3), "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": round(e2e_ms, 3),
-                "step": "target images up (pinned, double-buffered), render, l1 loss + dL/dC on the device, "
+                "step": "8-bit target images up (pinned, double-buffered), render, l1 loss + dL/dC on the device, "
                         "backward + S8-S9, loss down; Gaussians resident",
+                "launch": ("compute of each step one CUDA graph replay (per target slot); copies and "
+                           "event waits eager" if e2e_graphs[0] is not None else "eager"),
                 "host_resident_params": {"value": round(views_total / (e2e_full_ms / 1e3), 3), "unit": UNIT,
                                          "h2d_bytes_per_step": h2d_full, "d2h_bytes_per_step": d2h_full,
                                          "ms_per_step": round(e2e_full_ms, 3)}},

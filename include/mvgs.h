@@ -302,6 +302,12 @@ mvgs_status mvgs_adc_remap(mvgs_ctx *ctx, const float *src, float *dst, int64_t 
 mvgs_status mvgs_loss_grad(mvgs_ctx *ctx, const float *rgb, const float *target, int64_t n, int32_t mode, float scale,
                            float *dL_drgb, double *loss, void *stream);
 
+/* The same with an 8-bit target image (the photographs a training step uploads):
+ * C* = t · fl(1/255) in fp32 for each element t of `target` (device [n] uint8), otherwise
+ * identical to mvgs_loss_grad (a quarter of its host→device bytes per step). */
+mvgs_status mvgs_loss_grad_u8(mvgs_ctx *ctx, const float *rgb, const uint8_t *target, int64_t n, int32_t mode,
+                              float scale, float *dL_drgb, double *loss, void *stream);
+
 /* Monte-Carlo accumulators of the variance estimator of §4.2 for one mini-batch
  * gradient g (device [n] fp32, e.g. the ∂L/∂means of mvgs_adc_stats):
  *   sum[i] += g[i]  (device [n] fp64),   *sumsq += ‖g‖²  (device [1] fp64). */

@@ -177,6 +177,8 @@ cudaError_t launch_dssim3d(const mvgs_camera* h_cams, int V, int H, int W, const
 int lab_partials();
 cudaError_t launch_loss_grad(const float* rgb, const float* tgt, int64_t n, int mode, float scale, float* dL,
                              double* loss, double* part, cudaStream_t s);
+cudaError_t launch_loss_grad_u8(const float* rgb, const uint8_t* tgt, int64_t n, int mode, float scale, float* dL,
+                                double* loss, double* part, cudaStream_t s);
 cudaError_t launch_moments(const float* g, int64_t n, double* sum, double* sumsq, double* part, cudaStream_t s);
 cudaError_t launch_variance(const double* sum, int64_t n, const double* sumsq, int64_t K, double* out, double* part,
                             cudaStream_t s);

@@ -26,13 +26,20 @@ __device__ __forceinline__ double block_sum_d(double v, double* red) {
     return t;  // valid in thread 0
 }
 
-__global__ __launch_bounds__(LT) void k_loss_grad(const float* __restrict__ rgb, const float* __restrict__ tgt,
+// target element as a float: fp32 as given, or an 8-bit image value t/255 (t · fl(1/255))
+__device__ __forceinline__ float tgt_value(const float* t, int64_t i) { return t[i]; }
+__device__ __forceinline__ float tgt_value(const uint8_t* t, int64_t i) {
+    return __fmul_rn((float)t[i], 1.0f / 255.0f);  // rounded product (never contracted into the difference)
+}
+
+template <typename TT>
+__global__ __launch_bounds__(LT) void k_loss_grad(const float* __restrict__ rgb, const TT* __restrict__ tgt,
                                                   int64_t n, int mode, float scale, float* __restrict__ dL,
                                                   double* __restrict__ part) {
     __shared__ double red[LT / 32];
     double acc = 0.0;
     for (int64_t i = (int64_t)blockIdx.x * LT + threadIdx.x; i < n; i += (int64_t)gridDim.x * LT) {
-        const float d = rgb[i] - tgt[i];
+        const float d = rgb[i] - tgt_value(tgt, i);
         if (mode == 0) {
             dL[i] = d > 0.f ? scale : (d < 0.f ? -scale : 0.f);
             acc += (double)fabsf(d);
@@ -87,7 +94,14 @@ int lab_partials() { return LAB_GRID; }
 
 cudaError_t launch_loss_grad(const float* rgb, const float* tgt, int64_t n, int mode, float scale, float* dL,
                              double* loss, double* part, cudaStream_t s) {
-    k_loss_grad<<<LAB_GRID, LT, 0, s>>>(rgb, tgt, n, mode, scale, dL, part);
+    k_loss_grad<float><<<LAB_GRID, LT, 0, s>>>(rgb, tgt, n, mode, scale, dL, part);
+    if (loss) k_fsum<<<1, LT, 0, s>>>(part, LAB_GRID, 0, 1.0, nullptr, loss);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_loss_grad_u8(const float* rgb, const uint8_t* tgt, int64_t n, int mode, float scale, float* dL,
+                                double* loss, double* part, cudaStream_t s) {
+    k_loss_grad<uint8_t><<<LAB_GRID, LT, 0, s>>>(rgb, tgt, n, mode, scale, dL, part);
     if (loss) k_fsum<<<1, LT, 0, s>>>(part, LAB_GRID, 0, 1.0, nullptr, loss);
     return cudaGetLastError();
 }

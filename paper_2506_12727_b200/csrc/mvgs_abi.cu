@@ -622,6 +622,16 @@ mvgs_status mvgs_loss_grad(mvgs_ctx* ctx, const float* rgb, const float* target,
     return MVGS_OK;
 }
 
+mvgs_status mvgs_loss_grad_u8(mvgs_ctx* ctx, const float* rgb, const uint8_t* target, int64_t n, int32_t mode,
+                              float scale, float* dL_drgb, double* loss, void* stream) {
+    if (!ctx) return MVGS_ERR_INVALID;
+    if (n < 0 || (n > 0 && (!rgb || !target || !dL_drgb)) || (mode != 0 && mode != 1))
+        return fail(ctx, MVGS_ERR_INVALID, "loss_grad_u8: bad arguments");
+    CK(cudaSetDevice(ctx->device));
+    CK(launch_loss_grad_u8(rgb, target, n, mode, scale, dL_drgb, loss, ctx->d_lab_part, (cudaStream_t)stream));
+    return MVGS_OK;
+}
+
 mvgs_status mvgs_grad_moments(mvgs_ctx* ctx, const float* g, int64_t n, double* sum, double* sumsq, void* stream) {
     if (!ctx) return MVGS_ERR_INVALID;
     if (n < 0 || !sumsq || (n > 0 && (!g || !sum))) return fail(ctx, MVGS_ERR_INVALID, "grad_moments: bad arguments");

@@ -23,7 +23,7 @@ SYMBOLS = ["mvgs_create", "mvgs_destroy", "mvgs_last_error", "mvgs_reserve", "mv
            "mvgs_render_bwd", "mvgs_adc_stats", "mvgs_adc_stats_range", "mvgs_query", "mvgs_export_lists", "mvgs_export_pairs",
            "mvgs_set_timing", "mvgs_stage_times", "mvgs_set_eval_counting", "mvgs_render_fwd_partial", "mvgs_render_bwd_partial",
            "mvgs_render_fwd_depth", "mvgs_dssim3d", "mvgs_adc_step", "mvgs_adc_remap",
-           "mvgs_loss_grad", "mvgs_grad_moments", "mvgs_grad_variance", "mvgs_set_debug_blend_counts", "mvgs_set_tma",
+           "mvgs_loss_grad", "mvgs_loss_grad_u8", "mvgs_grad_moments", "mvgs_grad_variance", "mvgs_set_debug_blend_counts", "mvgs_set_tma",
            "mvgs_owner_slices", "mvgs_owner_prepare", "mvgs_owner_adc_stats", "mvgs_e_old_from_gsum"]
 PARTIAL_THREAD_EFFICIENT, PARTIAL_MASKED = 0, 1
 STAGE_NAMES = ["count", "scan_pairs", "project", "scan_buckets", "sort_pairs", "dup", "sort_entries", "render_fwd",
@@ -118,6 +118,7 @@ def _load():
     L.mvgs_adc_step.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]
     L.mvgs_adc_remap.argtypes = [vp, vp, vp, i64, vp, vp, i64, vp]
     L.mvgs_loss_grad.argtypes = [vp, vp, vp, i64, C.c_int32, C.c_float, vp, vp, vp]
+    L.mvgs_loss_grad_u8.argtypes = [vp, vp, vp, i64, C.c_int32, C.c_float, vp, vp, vp]
     L.mvgs_grad_moments.argtypes = [vp, vp, i64, vp, vp, vp]
     L.mvgs_grad_variance.argtypes = [vp, vp, i64, vp, i64, vp, vp]
     L.mvgs_stage_times.argtypes = [vp, C.POINTER(C.c_float), C.c_int]
@@ -283,8 +284,8 @@ def loss_grad(ctx, rgb, target, dL, mode: int = LOSS_L1, scale: float | None = N
     """NEXT-4: ∂loss/∂C of a rendered batch (ℓ1 or ℓ2, mean over all elements by default)."""
     n = int(rgb.numel())
     sc = 1.0 / n if scale is None else scale
-    _check(ctx, _lib.mvgs_loss_grad(ctx, _ptr(rgb), _ptr(target), n, int(mode), float(sc), _ptr(dL), _ptr(loss),
-                                    _stream(stream)))
+    fn = _lib.mvgs_loss_grad_u8 if target.dtype == torch.uint8 else _lib.mvgs_loss_grad  # 8-bit images: t/255
+    _check(ctx, fn(ctx, _ptr(rgb), _ptr(target), n, int(mode), float(sc), _ptr(dL), _ptr(loss), _stream(stream)))
 
 
 def grad_moments(ctx, g, acc_sum, acc_sumsq, stream=None):

@@ -62,6 +62,36 @@ def test_loss_grad_kernel(require_gpu, mode):
         mvgs.destroy(ctx)
 
 
+@pytest.mark.parametrize("mode", [0, 1])
+def test_loss_grad_u8_target(require_gpu, mode):
+    """mvgs_loss_grad_u8: an 8-bit target t is the fp32 value t·fl(1/255); the result equals the
+    fp32 entry point's on that target exactly (gradient and loss)."""
+    from paper_2506_12727_b200 import mvgs
+    rng = np.random.default_rng(2)
+    n = 500_003
+    t8 = rng.integers(0, 256, n).astype(np.uint8)
+    tf = t8.astype(np.float32) * np.float32(1.0 / 255.0)
+    a = rng.uniform(0, 1, n).astype(np.float32)
+    a[:64] = tf[:64]  # exact ties
+    ctx = mvgs.create(0)
+    try:
+        sc = float(np.float32(1.0 / n))
+        out = []
+        for tgt in (torch.from_numpy(t8).cuda(), torch.from_numpy(tf).cuda()):
+            dL = torch.empty(n, device="cuda")
+            loss = torch.zeros(1, dtype=torch.float64, device="cuda")
+            mvgs.loss_grad(ctx, torch.from_numpy(a).cuda(), tgt, dL, mode, sc, loss)
+            torch.cuda.synchronize()
+            out.append((dL.cpu().numpy(), float(loss)))
+        np.testing.assert_array_equal(out[0][0], out[1][0])
+        assert out[0][1] == out[1][1]
+        d = a - tf
+        ref = np.sign(d) * np.float32(sc) if mode == 0 else np.float32(2.0) * np.float32(sc) * d
+        np.testing.assert_array_equal(out[0][0], ref.astype(np.float32))
+    finally:
+        mvgs.destroy(ctx)
+
+
 @pytest.fixture(scope="module")
 def lab_scene(require_gpu):
     M, W, H = 5, 64, 48
