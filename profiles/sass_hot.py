@@ -18,7 +18,12 @@ def main():
                           "--launch-count", "1", "--print-source", "sass"], capture_output=True, text=True).stdout
     lines = out.splitlines()
     i = next(k for k, l in enumerate(lines) if l.startswith('"Address"'))
-    rows = list(csv.DictReader(io.StringIO("\n".join(lines[i:]))))
+    rows, seen = [], set()
+    for r in csv.DictReader(io.StringIO("\n".join(lines[i:]))):
+        if r["Address"] in seen:  # the source page can list a function's SASS twice
+            continue
+        seen.add(r["Address"])
+        rows.append(r)
     def num(x):
         try:
             return float(x)
