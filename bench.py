@@ -221,6 +221,9 @@ def run_mvgs(args):
 
     def grads_out(b):
         mvgs.render_bwd(R.ctx, dL_cur[0], outs[1], outs[2])
+        adc_out(b)
+
+    def adc_out(b):  # S8–S9 (+ the exchange when N > 1)
         if owner:
             adc_stats_owner(R.ctx, P, cams_all, rank, N, b.grads, b.adc, check=not checked[0])
             checked[0] = True
@@ -330,7 +333,6 @@ def run_mvgs(args):
     # 8-bit target images, as photographs are stored (mvgs_loss_grad_u8 reads t/255): 1 B per value
     host_tgt = torch.from_numpy(rng_t.integers(0, 256, (Vr, 3, cfg.H, cfg.W), dtype=np.uint8)).pin_memory()
     tgt_slots = [torch.empty_like(host_tgt, device=dev) for _ in range(2)]
-    dL_e2e = torch.empty_like(dL)
     loss_dev = [torch.zeros(1, dtype=torch.float64, device=dev) for _ in range(2)]
     loss_host = [torch.zeros(1, dtype=torch.float64).pin_memory() for _ in range(2)]
     comp = torch.cuda.current_stream()
@@ -343,9 +345,9 @@ def run_mvgs(args):
     def e2e_compute(b):  # the device part of one training iteration (slot b's target and loss)
         mvgs.preprocess(R.ctx, g, R.cams)
         mvgs.render_fwd(R.ctx, *outs)
-        mvgs.loss_grad(R.ctx, outs[0], tgt_slots[b], dL_e2e, mode=mvgs.LOSS_L1, loss=loss_dev[b])
-        dL_cur[0] = dL_e2e
-        grads_out(buf)
+        # the ℓ1 loss of the 8-bit targets fused into S7 (∂L/∂C formed per pixel in the backward)
+        mvgs.render_bwd_l1(R.ctx, outs[0], tgt_slots[b], outs[1], outs[2], loss=loss_dev[b])
+        adc_out(buf)
 
     # One GPU: each slot's compute is one CUDA graph (as the device-only step), replayed on the
     # compute stream between the event waits of the copy streams.
@@ -358,7 +360,6 @@ def run_mvgs(args):
             with torch.cuda.graph(e2e_graphs[b]):
                 e2e_compute(b)
             torch.cuda.synchronize()
-        dL_cur[0] = dL
 
     def e2e_step(i):
         b = i % 2
@@ -495,8 +496,8 @@ def run_mvgs(args):
         "clocks": clocks,
         "e2e": {"value": round(views_total / (e2e_ms / 1e3), 3), "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": round(e2e_ms, 3),
-                "step": "8-bit target images up (pinned, double-buffered), render, l1 loss + dL/dC on the device, "
-                        "backward + S8-S9, loss down; Gaussians resident",
+                "step": "8-bit target images up (pinned, double-buffered), render, backward with the l1 loss and "
+                        "dL/dC fused in (mvgs_render_bwd_l1) + S8-S9, loss down; Gaussians resident",
                 "launch": ("compute of each step one CUDA graph replay (per target slot); copies and "
                            "event waits eager" if e2e_graphs[0] is not None else "eager"),
                 "host_resident_params": {"value": round(views_total / (e2e_full_ms / 1e3), 3), "unit": UNIT,

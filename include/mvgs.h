@@ -163,6 +163,15 @@ mvgs_status mvgs_render_fwd_depth(mvgs_ctx *ctx, float *rgb, float *T_final, int
 mvgs_status mvgs_render_bwd(mvgs_ctx *ctx, const float *dL_drgb, const float *T_final, const int32_t *n_contrib,
                             void *stream);
 
+/* S7 with the ℓ1 photometric loss fused in, for a training step whose targets are 8-bit
+ * images: ∂L/∂C = scale·sign(C − t·fl(1/255)) is formed per pixel inside the backward — the
+ * values mvgs_loss_grad_u8 (mode 0) would write — from rgb [V,3,H,W] fp32 (render_fwd's image)
+ * and target [V,3,H,W] uint8 (device); `loss` (device [1] fp64, nullable) is overwritten with
+ * Σ|C − t/255| (summed with one double atomic per warp: the last bits depend on their order).
+ * Same state rules and outputs as mvgs_render_bwd; no ∂L/∂C buffer is written. */
+mvgs_status mvgs_render_bwd_l1(mvgs_ctx *ctx, const float *rgb, const uint8_t *target, float scale,
+                               const float *T_final, const int32_t *n_contrib, double *loss, void *stream);
+
 /* S8–S9: per-Gaussian chain rule summed over the batch's views
  * and the ADC statistics E1, E2, E_old, vis.  `grads` and `adc`
  * are host structs of device pointers.  Requires a preceding render_bwd. */

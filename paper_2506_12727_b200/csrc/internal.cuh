@@ -183,6 +183,8 @@ cudaError_t launch_moments(const float* g, int64_t n, double* sum, double* sumsq
 cudaError_t launch_variance(const double* sum, int64_t n, const double* sumsq, int64_t K, double* out, double* part,
                             cudaStream_t s);
 cudaError_t launch_render_bwd(const Launch& L, const float* dL, const float* Tf, const int32_t* nc, cudaStream_t s);
+cudaError_t launch_render_bwd_l1(const Launch& L, const float* rgb, const uint8_t* tgt, float scale, const float* Tf,
+                                 const int32_t* nc, double* loss, cudaStream_t s);
 cudaError_t launch_render_fwd_partial(const Launch& L, const int32_t* pix, int S, int mode, float* rgb, float* Tf,
                                       int32_t* nc, cudaStream_t s);
 cudaError_t launch_render_bwd_partial(const Launch& L, const int32_t* pix, int S, int mode, const float* dL,

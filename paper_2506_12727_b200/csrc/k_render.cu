@@ -641,9 +641,13 @@ __device__ __noinline__ bool block_may_pass(float px, float py, float A, float B
 #define MVGS_BWD_WPC 1  // warps per CTA of the warp-independent backward (1: a finished warp frees its slot)
 #endif
 constexpr int BW_WPC = MVGS_BWD_WPC;
-template <bool CNT>
+// L1: the ℓ1 loss fused in (mvgs_render_bwd_l1): `dL_drgb` is then the forward's image C and
+// ∂L/∂C = scale·sign(C − t·fl(1/255)) is formed per pixel from the 8-bit target exactly as
+// mvgs_loss_grad_u8 forms it; Σ|C − t/255| is added to *loss (one double atomic per warp).
+template <bool CNT, bool L1>
 __global__ __launch_bounds__(32 * BW_WPC, MVGS_BWD_MINB * 4 / BW_WPC) void k_render_bwd_w(
-    Launch L, const float* __restrict__ dL_drgb, const float* __restrict__ in_T, const int32_t* __restrict__ in_n) {
+    Launch L, const float* __restrict__ dL_drgb, const float* __restrict__ in_T, const int32_t* __restrict__ in_n,
+    const uint8_t* __restrict__ tgt, float scale, double* __restrict__ loss) {
     constexpr int NW = BW_WPC, MB = WB_BATCH, SPL = MB / 32;
     static_assert(MB % 32 == 0 && MB <= 256, "batch: lanes × SPL, byte list indices");
     __shared__ float4 se[NW][4][MB];  // per warp: (μ'x, μ'y, A, C) (B, o, sb, 1/o) (r, g, b, −) (W/2·A, W/2·B, H/2·C, H/2·B)
@@ -665,6 +669,7 @@ __global__ __launch_bounds__(32 * BW_WPC, MVGS_BWD_MINB * 4 / BW_WPC) void k_ren
     const int64_t HW = (int64_t)L.H * L.W;
     float dL[2][3], Tfin[2];
     int last[2];
+    double lsum = 0.0;  // L1: Σ|C − t/255| over the lane's pixels
 #pragma unroll
     for (int p = 0; p < 2; p++) {
         const int y = y0 + (WBH / 2) * p;
@@ -673,12 +678,25 @@ __global__ __launch_bounds__(32 * BW_WPC, MVGS_BWD_MINB * 4 / BW_WPC) void k_ren
         last[p] = 0;
         if (x < L.W && y < L.H) {
             const int64_t pix = (int64_t)y * L.W + x;
-            dL[p][0] = dL_drgb[(3 * (int64_t)v + 0) * HW + pix];
-            dL[p][1] = dL_drgb[(3 * (int64_t)v + 1) * HW + pix];
-            dL[p][2] = dL_drgb[(3 * (int64_t)v + 2) * HW + pix];
+#pragma unroll
+            for (int c = 0; c < 3; c++) {
+                const int64_t i = (3 * (int64_t)v + c) * HW + pix;
+                if (L1) {
+                    const float d = dL_drgb[i] - __fmul_rn((float)tgt[i], 1.0f / 255.0f);
+                    dL[p][c] = d > 0.f ? scale : (d < 0.f ? -scale : 0.f);
+                    lsum += (double)fabsf(d);
+                } else {
+                    dL[p][c] = dL_drgb[i];
+                }
+            }
             Tfin[p] = in_T[v * HW + pix];
             last[p] = in_n[v * HW + pix];
         }
+    }
+    if (L1 && loss) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) lsum += __shfl_xor_sync(FULLR, lsum, o);
+        if (lane == 0) atomicAdd(loss, lsum);
     }
     const float2 dLr = f2(dL[0][0], dL[1][0]), dLg = f2(dL[0][1], dL[1][1]), dLb = f2(dL[0][2], dL[1][2]);
     float2 T = f2(Tfin[0], Tfin[1]);
@@ -889,9 +907,19 @@ __global__ __launch_bounds__(32 * BW_WPC, MVGS_BWD_MINB * 4 / BW_WPC) void k_ren
 cudaError_t launch_render_bwd(const Launch& L, const float* dL, const float* Tf, const int32_t* nc, cudaStream_t s) {
     const int nb = L.V * L.T * (4 / BW_WPC);
     if (L.count_evals || L.dbg_nblend)
-        k_render_bwd_w<true><<<nb, 32 * BW_WPC, 0, s>>>(L, dL, Tf, nc);
+        k_render_bwd_w<true, false><<<nb, 32 * BW_WPC, 0, s>>>(L, dL, Tf, nc, nullptr, 0.f, nullptr);
     else
-        k_render_bwd_w<false><<<nb, 32 * BW_WPC, 0, s>>>(L, dL, Tf, nc);
+        k_render_bwd_w<false, false><<<nb, 32 * BW_WPC, 0, s>>>(L, dL, Tf, nc, nullptr, 0.f, nullptr);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_render_bwd_l1(const Launch& L, const float* rgb, const uint8_t* tgt, float scale, const float* Tf,
+                                 const int32_t* nc, double* loss, cudaStream_t s) {
+    const int nb = L.V * L.T * (4 / BW_WPC);
+    if (L.count_evals || L.dbg_nblend)
+        k_render_bwd_w<true, true><<<nb, 32 * BW_WPC, 0, s>>>(L, rgb, Tf, nc, tgt, scale, loss);
+    else
+        k_render_bwd_w<false, true><<<nb, 32 * BW_WPC, 0, s>>>(L, rgb, Tf, nc, tgt, scale, loss);
     return cudaGetLastError();
 }
 

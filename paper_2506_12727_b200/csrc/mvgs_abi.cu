@@ -382,6 +382,22 @@ mvgs_status mvgs_render_bwd(mvgs_ctx* ctx, const float* dL_drgb, const float* T_
     return MVGS_OK;
 }
 
+mvgs_status mvgs_render_bwd_l1(mvgs_ctx* ctx, const float* rgb, const uint8_t* target, float scale,
+                               const float* T_final, const int32_t* n_contrib, double* loss, void* stream) {
+    if (!ctx) return MVGS_ERR_INVALID;
+    if (ctx->state != 2) return fail(ctx, MVGS_ERR_STATE, "render_bwd_l1 needs a render_fwd of a fresh preprocess");
+    if (!rgb || !target || !T_final || !n_contrib) return fail(ctx, MVGS_ERR_INVALID, "null input");
+    CK(cudaSetDevice(ctx->device));
+    ctx->last_stream = (cudaStream_t)stream;
+    cudaStream_t s = (cudaStream_t)stream;
+    CK(cudaMemsetAsync(ctx->d_counters64 + 1, 0, sizeof(unsigned long long), s));
+    CK(cudaMemsetAsync(ctx->d_counters64 + 3, 0, sizeof(unsigned long long), s));
+    if (loss) CK(cudaMemsetAsync(loss, 0, sizeof(double), s));
+    { STAGE(ST_BWD); CK(launch_render_bwd_l1(ctx->L, rgb, target, scale, T_final, n_contrib, loss, s)); }  // S7 + ℓ1
+    ctx->state = 3;
+    return MVGS_OK;
+}
+
 mvgs_status mvgs_render_fwd_partial(mvgs_ctx* ctx, const int32_t* pix, int32_t S, int32_t mode, float* rgb,
                                     float* T_final, int32_t* n_contrib, void* stream) {
     if (!ctx) return MVGS_ERR_INVALID;

@@ -23,7 +23,7 @@ SYMBOLS = ["mvgs_create", "mvgs_destroy", "mvgs_last_error", "mvgs_reserve", "mv
            "mvgs_render_bwd", "mvgs_adc_stats", "mvgs_adc_stats_range", "mvgs_query", "mvgs_export_lists", "mvgs_export_pairs",
            "mvgs_set_timing", "mvgs_stage_times", "mvgs_set_eval_counting", "mvgs_render_fwd_partial", "mvgs_render_bwd_partial",
            "mvgs_render_fwd_depth", "mvgs_dssim3d", "mvgs_adc_step", "mvgs_adc_remap",
-           "mvgs_loss_grad", "mvgs_loss_grad_u8", "mvgs_grad_moments", "mvgs_grad_variance", "mvgs_set_debug_blend_counts", "mvgs_set_tma",
+           "mvgs_loss_grad", "mvgs_loss_grad_u8", "mvgs_render_bwd_l1", "mvgs_grad_moments", "mvgs_grad_variance", "mvgs_set_debug_blend_counts", "mvgs_set_tma",
            "mvgs_owner_slices", "mvgs_owner_prepare", "mvgs_owner_adc_stats", "mvgs_e_old_from_gsum"]
 PARTIAL_THREAD_EFFICIENT, PARTIAL_MASKED = 0, 1
 STAGE_NAMES = ["count", "scan_pairs", "project", "scan_buckets", "sort_pairs", "dup", "sort_entries", "render_fwd",
@@ -119,6 +119,7 @@ def _load():
     L.mvgs_adc_remap.argtypes = [vp, vp, vp, i64, vp, vp, i64, vp]
     L.mvgs_loss_grad.argtypes = [vp, vp, vp, i64, C.c_int32, C.c_float, vp, vp, vp]
     L.mvgs_loss_grad_u8.argtypes = [vp, vp, vp, i64, C.c_int32, C.c_float, vp, vp, vp]
+    L.mvgs_render_bwd_l1.argtypes = [vp, vp, vp, C.c_float, vp, vp, vp, vp]
     L.mvgs_grad_moments.argtypes = [vp, vp, i64, vp, vp, vp]
     L.mvgs_grad_variance.argtypes = [vp, vp, i64, vp, i64, vp, vp]
     L.mvgs_stage_times.argtypes = [vp, C.POINTER(C.c_float), C.c_int]
@@ -211,6 +212,13 @@ def dssim3d(ctx, cams: np.ndarray, img, target, depth, T_final, loss, dL_dimg=No
 
 def render_bwd(ctx, dL_drgb, T_final, n_contrib, stream=None):
     _check(ctx, _lib.mvgs_render_bwd(ctx, _ptr(dL_drgb), _ptr(T_final), _ptr(n_contrib), _stream(stream)))
+
+
+def render_bwd_l1(ctx, rgb, target_u8, T_final, n_contrib, scale: float | None = None, loss=None, stream=None):
+    """S7 with the ℓ1 loss of 8-bit targets fused in (∂L/∂C formed in the kernel; mean by default)."""
+    sc = 1.0 / int(rgb.numel()) if scale is None else scale
+    _check(ctx, _lib.mvgs_render_bwd_l1(ctx, _ptr(rgb), _ptr(target_u8), float(sc), _ptr(T_final), _ptr(n_contrib),
+                                        _ptr(loss), _stream(stream)))
 
 
 def render_fwd_partial(ctx, pix, S: int, mode: int, rgb, T_final, n_contrib, stream=None):

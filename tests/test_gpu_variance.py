@@ -92,6 +92,40 @@ def test_loss_grad_u8_target(require_gpu, mode):
         mvgs.destroy(ctx)
 
 
+def test_render_bwd_l1_equals_loss_kernel_then_backward(require_gpu):
+    """mvgs_render_bwd_l1 (the ℓ1 loss of 8-bit targets fused into S7) against
+    mvgs_loss_grad_u8 + mvgs_render_bwd on the same render: the same ∂L/∂C per pixel, so the
+    parameter gradients and E statistics agree to the atomics' summation order, and the loss
+    to the order of its per-warp double sums."""
+    from paper_2506_12727_b200 import mvgs
+    cfg = synth.scaled(synth.CONFIGS["garden"], P=20_000, V=3, W=173, H=131)
+    g, cams = synth.make_scene(cfg)
+    gd = to_dev(g)
+    rng = np.random.default_rng(5)
+    tgt = torch.from_numpy(rng.integers(0, 256, (3, 3, 131, 173), dtype=np.uint8)).cuda()
+    R = mvgs.Rasterizer(0)
+    out = {}
+    for fused in (False, True):
+        R.preprocess(gd, cams)
+        rgb, Tf, nc = R.forward()
+        loss = torch.zeros(1, dtype=torch.float64, device="cuda")
+        grads, adc = R.alloc_backward()
+        if fused:
+            mvgs.render_bwd_l1(R.ctx, rgb, tgt, Tf, nc, loss=loss)
+        else:
+            dL = torch.empty_like(rgb)
+            mvgs.loss_grad(R.ctx, rgb, tgt, dL, mvgs.LOSS_L1, loss=loss)
+            mvgs.render_bwd(R.ctx, dL, Tf, nc)
+        mvgs.adc_stats(R.ctx, grads, adc)
+        torch.cuda.synchronize()
+        out[fused] = ({k: v.cpu().numpy().astype(np.float64) for k, v in {**grads, **adc}.items()}, float(loss))
+    a, b = out[False], out[True]
+    assert abs(a[1] - b[1]) <= 1e-12 * abs(a[1])
+    for k in a[0]:
+        x, y = a[0][k], b[0][k]
+        assert np.linalg.norm(x - y) <= 1e-5 * max(np.linalg.norm(x), 1e-30), k
+
+
 @pytest.fixture(scope="module")
 def lab_scene(require_gpu):
     M, W, H = 5, 64, 48
